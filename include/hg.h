@@ -1,0 +1,165 @@
+/*
+ * hg.h -- C ABI of libhgrsvd: the block randomized SVD hot path of
+ * arXiv:1908.08281 on NVIDIA B200 (sm_100a).
+ *
+ * The path (section 3, Alg. 1 and Eqs. 1, 3, 11, 15):
+ *   1. hg_build_theta          diagonal b x b blocks X_ii of X = I - Theta/(1+mu),
+ *                              Theta = Dv^-1/2 H W De^-1 H^T Dv^-1/2      (Eq. 1)
+ *   2. hg_block_rsvd           per block, Alg. 1 with l = k, pi = q
+ *   3. hg_block_apply_inverse  F_i = scale * V_i Sigma_i^-1 U_i^T Y_i      (Eq. 3,
+ *                                                                           PAPER.md:160-163 Eq. 15)
+ *   hg_solve = 1 -> 2 -> 3 from the CSR incidence to F.
+ *
+ * Conventions for every entry point:
+ *   - Pointers are DEVICE pointers owned by the caller unless a name says
+ *     "host"; nothing is retained after return.  Matrices are dense row-major
+ *     fp32 unless noted.  "[a][b][c]" gives the dimensions, last contiguous.
+ *   - Work is enqueued on `stream` and is asynchronous unless stated.  The
+ *     library never allocates device memory on these calls: scratch comes
+ *     from the caller's workspace `ws` (size from hg_workspace_size, 256-byte
+ *     aligned).  Distinct workspaces make concurrent calls thread-safe.
+ *   - Host-side validation failures return HG_ERR_INVALID synchronously and
+ *     enqueue nothing.  Data-dependent failures found on the device are OR-ed
+ *     as bit flags into the caller's device word *d_status (0 = ok; the
+ *     caller zeroes it); hg_solve with HG_SYNC and hg_solve_host read it back
+ *     and return HG_ERR_NUMERICAL.  CUDA launch/runtime errors return
+ *     HG_ERR_CUDA.  hg_last_error() describes the last failure on the calling
+ *     host thread.
+ *   - Singular vectors are returned TRANSPOSED: Ut[i] = U_i^T (k x b) and
+ *     Vt[i] = V_i^T (k x b), i.e. each singular vector is one contiguous row.
+ *     Singular values are non-increasing; the sign of each pair (u_j, v_j) is
+ *     fixed so that the largest-|.| entry of u_j is positive.
+ */
+#ifndef HG_H_
+#define HG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* hg_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  HG_OK = 0,
+  HG_ERR_INVALID = 2,   /* bad argument / workspace too small (host-side, synchronous) */
+  HG_ERR_NUMERICAL = 3, /* device status word non-zero (see hg_status_flags)            */
+  HG_ERR_CUDA = 4       /* CUDA runtime / launch error                                   */
+} hg_status;
+
+/* Device status word bits (OR-ed into *d_status). */
+enum hg_status_flags {
+  HG_ST_ISOLATED_VERTEX = 1 << 0, /* delta(v) = 0                 */
+  HG_ST_EMPTY_EDGE = 1 << 1,      /* delta(e) = 0                                            */
+  HG_ST_CHOL_BREAKDOWN = 1 << 2,  /* CholeskyQR pivot <= 0: Y_i rank-deficient to fp32        */
+  HG_ST_JACOBI_CAP = 1 << 3,      /* one-sided Jacobi did not converge in the sweep cap      */
+  HG_ST_SINGULAR_SIGMA = 1 << 4,  /* sigma_j <= 1e-6 sigma_1 at apply      */
+  HG_ST_NONFINITE = 1 << 5        /* NaN/Inf met                                             */
+};
+
+/* flags */
+#define HG_RAW_THETA (1u << 0)  /* hg_build_theta: write Theta_ii instead of X_ii          */
+#define HG_SYNC (1u << 1)       /* hg_solve: synchronise `stream`, map *d_status to status  */
+#define HG_GEMM_SIMT (1u << 8)  /* verification only: CUDA-core fp32 GEMMs, not tcgen05    */
+
+/* Hypergraph incidence H (H(v,e) = 1 iff v in e) in CSR over
+ * vertices; values are implicitly 1.  Device pointers. */
+typedef struct {
+  int32_t n_vertices;     /* N = |V| (m in the paper)                        */
+  int32_t n_edges;        /* E = |E| (n in the paper)                        */
+  int64_t nnz;            /* number of incidences                            */
+  const int64_t* row_ptr; /* [N+1], row_ptr[0] = 0, row_ptr[N] = nnz         */
+  const int32_t* col_idx; /* [nnz] hyperedge ids in [0,E), strictly increasing per row */
+} hg_incidence;
+
+/* Bytes of workspace needed by any call below for these sizes (T may be 0
+ * when no apply is made).  Returns HG_ERR_INVALID on bad sizes. */
+hg_status hg_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t b, int32_t k, int32_t T,
+                            size_t* bytes);
+
+/* Eq. 1 diagonal blocks.  For block i (vertices [ib,(i+1)b)):
+ *   X_ii[u][v] = delta_uv - r_u r_v sum_{e ni u,v} w_e/delta(e) / (1+mu),  r = delta(v)^-1/2,
+ * with delta(v) = sum_e w_e H(v,e), delta(e) = sum_v H(v,e).
+ *   w        [E] hyperedge weights (> 0 expected; not normalised, reading A9)
+ *   mu       the regulariser theta > 0 (configs' "mu")
+ *   b        block size, N % b == 0
+ *   flags    HG_RAW_THETA writes Theta_ii instead of X_ii
+ *   blocks   out [N/b][b][b]; bitwise symmetric
+ *   dv_rsqrt out [N] r_v, may be NULL
+ * Device errors: HG_ST_ISOLATED_VERTEX, HG_ST_EMPTY_EDGE. */
+hg_status hg_build_theta(const hg_incidence* H, const float* w, float mu, int32_t b, uint32_t flags,
+                         float* blocks, float* dv_rsqrt, int32_t* d_status, void* ws, size_t ws_bytes,
+                         hg_stream_t stream);
+
+/* Alg. 1 step 1 test matrix (reading A6):
+ *   out[r][c] (rows x cols) = normal number r*cols + c of the Philox4x64-10
+ *   stream keyed by (seed, 0): raw block j = Philox(ctr=(j+1,0,0,0)) gives
+ *   normals 4j..4j+3 by Box-Muller in fp64, rounded to fp32.
+ * Exported so the stream can be pinned; hg_block_rsvd draws the same numbers
+ * internally (block i uses rows [ib,(i+1)b) of the N x k matrix). */
+hg_status hg_fill_gaussian(uint64_t seed, int32_t rows, int32_t cols, float* out, hg_stream_t stream);
+
+/* Alg. 1 on each of nb blocks, rank l = k (no oversampling,
+ * reading A3), q subspace-iteration passes:
+ *   Y0 = X Omega, S0 = qr(Y0); for i = 1..q: S~ = qr(X^T S), S = qr(X S~);
+ *   B = S^T X; B = U~ Sigma V^T; U = S U~.
+ * X_ii^T = X_ii is assumed (hg_build_theta writes bitwise-symmetric blocks;
+ * reading A12).  QR is CholeskyQR2; the SVD is one-sided Jacobi.
+ *   blocks [nb][b][b]   input blocks (symmetric)
+ *   1 <= k <= b, k % 8 == 0 is NOT required; b % 4 == 0 required (TMA strides)
+ *   Ut, Vt [nb][k][b]   out, U_i^T and V_i^T;  sigma [nb][k] out, non-increasing
+ * Device errors: HG_ST_CHOL_BREAKDOWN, HG_ST_JACOBI_CAP, HG_ST_NONFINITE. */
+hg_status hg_block_rsvd(const float* blocks, int32_t nb, int32_t b, int32_t k, int32_t q, uint64_t seed,
+                        uint32_t flags, float* Ut, float* sigma, float* Vt, int32_t* d_status, void* ws,
+                        size_t ws_bytes, hg_stream_t stream);
+
+/* Eq. 3 with Eq. 15 per block:
+ *   F_i = scale * V_i diag(1/sigma_i) U_i^T Y_i,   Y_i = rows [ib,(i+1)b) of Y.
+ *   Y, F [nb*b][T];  scale = mu/(1+mu) for Eq. 3.
+ * Device errors: HG_ST_SINGULAR_SIGMA (sigma_j <= 1e-6 sigma_1; reading A14). */
+hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const float* Vt, int32_t nb, int32_t b,
+                                 int32_t k, const float* Y, int32_t T, float scale, float* F,
+                                 int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
+
+/* The whole hot path: hg_build_theta -> hg_block_rsvd -> hg_block_apply_inverse
+ * with scale = mu/(1+mu).  sigma_out [N/b][k] may be NULL.  Asynchronous
+ * unless flags has HG_SYNC (then the stream is synchronised and a non-zero
+ * *d_status returns HG_ERR_NUMERICAL).  d_status may be NULL only with HG_SYNC
+ * (a word inside ws is used). */
+hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
+                   uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags,
+                   int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
+
+/* hg_solve from HOST buffers (end-to-end entry): copies row_ptr, col_idx, w, Y
+ * host->device, solves, copies F (and sigma_out if non-NULL) device->host,
+ * synchronises.  ws (device) is caller-provided as above; host buffers should
+ * be pinned for full copy bandwidth.  Returns the device status. */
+hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_ptr_host,
+                        const int32_t* col_idx_host, const float* w_host, float mu, int32_t b, int32_t k,
+                        int32_t q, uint64_t seed, const float* Y_host, int32_t T, float* F_host,
+                        float* sigma_host, uint32_t flags, void* ws, size_t ws_bytes, hg_stream_t stream);
+
+/* Verification export of the batched GEMM the path runs on (3xTF32 on
+ * tcgen05, or fp32 CUDA cores with HG_GEMM_SIMT):
+ *   for g < batch: D_g(m,n) = alpha * rs_g[m] * cs_g[n] * sum_kk A_g(m,kk) B_g(kk,n)
+ *   A_g(m,kk) = A[g*sa + (a_mn ? kk*lda + m : m*lda + kk)]
+ *   B_g(kk,n) = B[g*sb + (b_mn ? kk*ldb + n : n*ldb + kk)]
+ *   d_trans ? D[g*sd + n*ldd + m] : D[g*sd + m*ldd + n]
+ *   rs/cs may be NULL (= 1), with batch strides srs/scs. */
+hg_status hg_gemm(int32_t M, int32_t N, int32_t K, int32_t batch, const float* A, int32_t a_mn, int64_t lda,
+                  int64_t sa, const float* B, int32_t b_mn, int64_t ldb, int64_t sb, float* D, int32_t d_trans,
+                  int64_t ldd, int64_t sd, float alpha, const float* rs, int64_t srs, const float* cs,
+                  int64_t scs, uint32_t flags, hg_stream_t stream);
+
+/* Number of kernels the last hg_* call on this host thread enqueued. */
+int32_t hg_last_launch_count(void);
+
+/* Message for the last failing call on this host thread ("" if none). */
+const char* hg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HG_H_ */

@@ -1,0 +1,445 @@
+// abi.cu -- the C ABI (include/hg.h): validation, workspace carving and the
+// stage sequencing of the block randomized SVD path.
+//
+//   hg_build_theta          degrees -> Eq. 1 blocks
+//   hg_block_rsvd           Alg. 1 per block
+//   hg_block_apply_inverse  Eq. 3 with Eq. 15
+//   hg_solve(_host)         the three in sequence
+//
+// Panels (b x k per block) are stored transposed, [nb][k][b], so that each of
+// the k columns is contiguous; every GEMM below reads/writes that layout
+// directly (see gemm.cu for the operand-major conventions).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/hg.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+hg_status fail(hg_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+hg_status fail(hg_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+hg_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(HG_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define HG_CU(expr, where)                      \
+  do {                                          \
+    cudaError_t e_ = (expr);                    \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+constexpr size_t ALIGN = 256;
+
+struct Layout {
+  size_t de = 0, eval = 0, dvr = 0, blocks = 0, P[4] = {0, 0, 0, 0}, Ut = 0, Vt = 0;
+  size_t G = 0, L = 0, Linv = 0, Wf = 0, Uk = 0, work = 0, sig = 0, sigma = 0, rs = 0, Z = 0, status = 0;
+  size_t h_rowptr = 0, h_col = 0, h_w = 0, h_Y = 0, h_F = 0;
+  size_t total = 0;
+};
+
+Layout layout(int64_t N, int64_t E, int64_t nnz, int64_t b, int64_t k, int64_t T) {
+  Layout L;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + ALIGN - 1) / ALIGN * ALIGN;
+    return o;
+  };
+  const int64_t nb = N / b;
+  L.de = take(4 * E);
+  L.eval = take(4 * E);
+  L.dvr = take(4 * N);
+  L.blocks = take(4 * nb * b * b);
+  for (int i = 0; i < 4; ++i) L.P[i] = take(4 * nb * k * b);
+  L.Ut = take(4 * nb * k * b);
+  L.Vt = take(4 * nb * k * b);
+  L.G = take(4 * nb * k * k);
+  L.L = take(4 * nb * k * k);
+  L.Linv = take(4 * nb * k * k);
+  L.Wf = take(4 * nb * k * k);
+  L.Uk = take(4 * nb * k * k);
+  L.work = take(4 * nb * k * k);
+  L.sig = take(8 * nb * k + 4 * nb * k);
+  L.sigma = take(4 * nb * k);
+  L.rs = take(4 * nb * k);
+  L.Z = take(4 * nb * k * (T > 0 ? T : 1));
+  L.status = take(4);
+  L.h_rowptr = take(8 * (N + 1));
+  L.h_col = take(4 * (nnz > 0 ? nnz : 1));
+  L.h_w = take(4 * E);
+  L.h_Y = take(4 * N * (T > 0 ? T : 1));
+  L.h_F = take(4 * N * (T > 0 ? T : 1));
+  L.total = off;
+  return L;
+}
+
+template <class T>
+T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+hg_status check_sizes(int64_t N, int64_t b, int64_t k, int64_t q, int64_t T) {
+  if (N <= 0 || b <= 0) return fail(HG_ERR_INVALID, "need N > 0 and b > 0 (N=%lld, b=%lld)", (long long)N, (long long)b);
+  if (N % b) return fail(HG_ERR_INVALID, "N %% b != 0 (N=%lld, b=%lld); ragged blocks are not supported", (long long)N, (long long)b);
+  if (b % 4) return fail(HG_ERR_INVALID, "b must be a multiple of 4 (b=%lld)", (long long)b);
+  if (k < 1 || k > b) return fail(HG_ERR_INVALID, "need 1 <= k <= b (k=%lld, b=%lld)", (long long)k, (long long)b);
+  if (k % 4) return fail(HG_ERR_INVALID, "k must be a multiple of 4 (k=%lld)", (long long)k);
+  if (k > 512) return fail(HG_ERR_INVALID, "k > 512 is not supported (k=%lld)", (long long)k);
+  if (q < 0) return fail(HG_ERR_INVALID, "q must be >= 0 (q=%lld)", (long long)q);
+  if (T < 0 || (T % 4)) return fail(HG_ERR_INVALID, "T must be >= 0 and a multiple of 4 (T=%lld)", (long long)T);
+  if (N / b > 65535) return fail(HG_ERR_INVALID, "more than 65535 blocks");
+  return HG_OK;
+}
+
+hg_status check_ws(const void* ws, size_t ws_bytes, size_t need) {
+  if (!ws) return fail(HG_ERR_INVALID, "workspace is NULL");
+  if (reinterpret_cast<uintptr_t>(ws) % ALIGN) return fail(HG_ERR_INVALID, "workspace must be 256-byte aligned");
+  if (ws_bytes < need)
+    return fail(HG_ERR_INVALID, "workspace too small: %zu bytes given, %zu needed", ws_bytes, need);
+  return HG_OK;
+}
+
+hg_status gemm(const GemmDesc& g, cudaStream_t s, bool simt, const char* what) {
+  if (const char* m = gemm_check(g)) return fail(HG_ERR_INVALID, "%s: %s", what, m);
+  cudaError_t e = launch_gemm(g, s, simt);
+  ++g_launches;
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  return HG_OK;
+}
+
+// ---------------------------------------------------------------- stages
+struct Rsvd {
+  int nb, b, k;
+  bool simt;
+  cudaStream_t s;
+  const float* X;
+
+  // out_t = (X P)^T  with P given as P_t [k][b] (X symmetric: X^T P = X P, reading A12)
+  hg_status power(const float* P_t, float* out_t) const {
+    GemmDesc g;
+    g.M = b; g.N = k; g.K = b; g.batch = nb;
+    g.A = X; g.a_mn = false; g.lda = b; g.sa = (int64_t)b * b;
+    g.B = P_t; g.b_mn = false; g.ldb = b; g.sb = (int64_t)k * b;
+    g.D = out_t; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
+    return gemm(g, s, simt, "power product X*S");
+  }
+  // G = P^T P (k x k)
+  hg_status gram(const float* P_t, float* G) const {
+    GemmDesc g;
+    g.M = k; g.N = k; g.K = b; g.batch = nb;
+    g.A = P_t; g.a_mn = false; g.lda = b; g.sa = (int64_t)k * b;
+    g.B = P_t; g.b_mn = false; g.ldb = b; g.sb = (int64_t)k * b;
+    g.D = G; g.d_trans = false; g.ldd = k; g.sd = (int64_t)k * k;
+    return gemm(g, s, simt, "Gram P^T P");
+  }
+  // Q = P L^-T  ->  Q_t
+  hg_status qform(const float* P_t, const float* Linv, float* Q_t) const {
+    GemmDesc g;
+    g.M = b; g.N = k; g.K = k; g.batch = nb;
+    g.A = P_t; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
+    g.B = Linv; g.b_mn = false; g.ldb = k; g.sb = (int64_t)k * k;
+    g.D = Q_t; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
+    return gemm(g, s, simt, "Q = Y R^-1");
+  }
+};
+
+#define HG_TRY(expr)                 \
+  do {                               \
+    hg_status st_ = (expr);          \
+    if (st_ != HG_OK) return st_;    \
+  } while (0)
+
+hg_status cholqr2(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* Linv, float* work, int32_t* st) {
+  HG_TRY(R.gram(a_t, G));
+  HG_CU(launch_cholinv(R.nb, R.k, G, nullptr, Linv, work, st, R.s, &g_launches), "cholinv");
+  HG_TRY(R.qform(a_t, Linv, scratch_t));
+  HG_TRY(R.gram(scratch_t, G));
+  HG_CU(launch_cholinv(R.nb, R.k, G, nullptr, Linv, work, st, R.s, &g_launches), "cholinv");
+  HG_TRY(R.qform(scratch_t, Linv, a_t));
+  return HG_OK;
+}
+
+hg_status run_rsvd(const float* X, int nb, int b, int k, int q, uint64_t seed, bool simt, float* Ut, float* sigma,
+                   float* Vt, int32_t* st, void* ws, const Layout& Lo, cudaStream_t s) {
+  Rsvd R{nb, b, k, simt, s, X};
+  float* P[4];
+  for (int i = 0; i < 4; ++i) P[i] = at<float>(ws, Lo.P[i]);
+  float* G = at<float>(ws, Lo.G);
+  float* Lm = at<float>(ws, Lo.L);
+  float* Linv = at<float>(ws, Lo.Linv);
+  float* Wf = at<float>(ws, Lo.Wf);
+  float* Uk = at<float>(ws, Lo.Uk);
+  float* work = at<float>(ws, Lo.work);
+  double* sig = at<double>(ws, Lo.sig);
+
+  // Alg. 1 step 1-2: Omega, Y0 = X Omega, S0 = qr(Y0)
+  HG_CU(launch_omega_panels(seed, nb, b, k, P[0], s, &g_launches), "omega");
+  HG_TRY(R.power(P[0], P[1]));
+  HG_TRY(cholqr2(R, P[1], P[0], G, Linv, work, st));
+  float *cur = P[1], *oth = P[0];
+  // loop i = 1..q: S~ = qr(X^T S), S = qr(X S~)
+  for (int it = 0; it < 2 * q; ++it) {
+    HG_TRY(R.power(cur, oth));
+    HG_TRY(cholqr2(R, oth, cur, G, Linv, work, st));
+    float* t = cur; cur = oth; oth = t;
+  }
+  // step 4: B = S^T X, stored as B [k][b] = (X S)^T
+  float* Bt = oth;
+  HG_TRY(R.power(cur, Bt));
+  // step 5: one-sided Jacobi on W = L^T, B B^T = L L^T
+  HG_TRY(R.gram(Bt, G));
+  HG_CU(launch_cholinv(nb, k, G, Lm, Linv, work, st, s, &g_launches), "cholinv(B B^T)");
+  HG_CU(launch_jacobi(nb, k, Lm, Wf, st, s, &g_launches), "jacobi");
+  {  // U~ = L^-T W_f  (stored transposed: Uk[j] = u~_j)
+    GemmDesc g;
+    g.M = k; g.N = k; g.K = k; g.batch = nb;
+    g.A = Linv; g.a_mn = true; g.lda = k; g.sa = (int64_t)k * k;
+    g.B = Wf; g.b_mn = true; g.ldb = k; g.sb = (int64_t)k * k;
+    g.D = Uk; g.d_trans = true; g.ldd = k; g.sd = (int64_t)k * k;
+    HG_TRY(gemm(g, s, simt, "U~ = L^-T W_f"));
+  }
+  // V_w = B^T U~ -> P[2];  U_w = S U~ -> P[3]  (step 6)
+  for (int w = 0; w < 2; ++w) {
+    GemmDesc g;
+    g.M = b; g.N = k; g.K = k; g.batch = nb;
+    g.A = (w == 0) ? Bt : cur; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
+    g.B = Uk; g.b_mn = false; g.ldb = k; g.sb = (int64_t)k * k;
+    g.D = P[2 + w]; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
+    HG_TRY(gemm(g, s, simt, w == 0 ? "V = B^T U~" : "U = S U~"));
+  }
+  HG_CU(launch_finalize(nb, b, k, P[2], P[3], Ut, sigma, Vt, sig, st, s, &g_launches), "finalize");
+  return HG_OK;
+}
+
+hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb, int b, int k, const float* Y, int T,
+                    float scale, float* F, int32_t* st, void* ws, const Layout& Lo, cudaStream_t s, bool simt) {
+  if (T == 0) return HG_OK;
+  float* rs = at<float>(ws, Lo.rs);
+  float* Z = at<float>(ws, Lo.Z);
+  HG_CU(launch_inv_sigma(nb, k, sigma, scale, rs, st, s, &g_launches), "inv_sigma");
+  {  // Z = diag(scale/sigma) U^T Y_i   (k x T)
+    GemmDesc g;
+    g.M = k; g.N = T; g.K = b; g.batch = nb;
+    g.A = Ut; g.a_mn = false; g.lda = b; g.sa = (int64_t)k * b;
+    g.B = Y; g.b_mn = true; g.ldb = T; g.sb = (int64_t)b * T;
+    g.D = Z; g.d_trans = false; g.ldd = T; g.sd = (int64_t)k * T;
+    g.rs = rs; g.srs = k;
+    HG_TRY(gemm(g, s, simt, "Z = Sigma^-1 U^T Y"));
+  }
+  {  // F_i = V Z   (b x T)
+    GemmDesc g;
+    g.M = b; g.N = T; g.K = k; g.batch = nb;
+    g.A = Vt; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
+    g.B = Z; g.b_mn = true; g.ldb = T; g.sb = (int64_t)k * T;
+    g.D = F; g.d_trans = false; g.ldd = T; g.sd = (int64_t)b * T;
+    HG_TRY(gemm(g, s, simt, "F = V Z"));
+  }
+  return HG_OK;
+}
+
+hg_status run_theta(const hg_incidence* H, const float* w, float mu, int b, bool raw, float* blocks, float* dvr_out,
+                    int32_t* st, void* ws, const Layout& Lo, cudaStream_t s) {
+  float* dvr = dvr_out ? dvr_out : at<float>(ws, Lo.dvr);
+  HG_CU(launch_degrees(H->n_vertices, H->n_edges, H->nnz, H->row_ptr, H->col_idx, w, at<int32_t>(ws, Lo.de),
+                       at<float>(ws, Lo.eval), dvr, st, s, &g_launches),
+        "degrees");
+  HG_CU(launch_assemble(H->n_vertices / b, b, H->row_ptr, H->col_idx, at<float>(ws, Lo.eval), dvr, mu, raw, blocks,
+                        s, &g_launches),
+        "assemble");
+  return HG_OK;
+}
+
+hg_status check_H(const hg_incidence* H) {
+  if (!H) return fail(HG_ERR_INVALID, "H is NULL");
+  if (H->n_vertices <= 0 || H->n_edges <= 0 || H->nnz < 0)
+    return fail(HG_ERR_INVALID, "bad incidence sizes (N=%d, E=%d, nnz=%lld)", H->n_vertices, H->n_edges,
+                (long long)H->nnz);
+  if (!H->row_ptr || (H->nnz > 0 && !H->col_idx)) return fail(HG_ERR_INVALID, "incidence pointers are NULL");
+  return HG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hg_last_error(void) { return g_err.c_str(); }
+int32_t hg_last_launch_count(void) { return g_launches; }
+
+hg_status hg_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t b, int32_t k, int32_t T, size_t* bytes) {
+  g_err.clear();
+  if (!bytes) return fail(HG_ERR_INVALID, "bytes is NULL");
+  HG_TRY(check_sizes(N, b, k, 0, T));
+  if (E <= 0 || nnz < 0) return fail(HG_ERR_INVALID, "need E > 0 and nnz >= 0");
+  *bytes = layout(N, E, nnz, b, k, T).total;
+  return HG_OK;
+}
+
+hg_status hg_build_theta(const hg_incidence* H, const float* w, float mu, int32_t b, uint32_t flags, float* blocks,
+                         float* dv_rsqrt, int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  HG_TRY(check_H(H));
+  if (b <= 0 || H->n_vertices % b || b % 4) return fail(HG_ERR_INVALID, "need b > 0, b %% 4 == 0, N %% b == 0");
+  if (!(mu > 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and > 0");
+  if (!w || !blocks || !d_status) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, 4, 0);
+  HG_TRY(check_ws(ws, ws_bytes, Lo.dvr + 4 * (size_t)H->n_vertices));
+  return run_theta(H, w, mu, b, (flags & HG_RAW_THETA) != 0, blocks, dv_rsqrt, d_status, ws, Lo,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+hg_status hg_fill_gaussian(uint64_t seed, int32_t rows, int32_t cols, float* out, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (rows <= 0 || cols <= 0 || !out) return fail(HG_ERR_INVALID, "need rows, cols > 0 and out != NULL");
+  HG_CU(launch_gaussian_rowmajor(seed, rows, cols, out, reinterpret_cast<cudaStream_t>(stream), &g_launches),
+        "gaussian");
+  return HG_OK;
+}
+
+hg_status hg_block_rsvd(const float* blocks, int32_t nb, int32_t b, int32_t k, int32_t q, uint64_t seed,
+                        uint32_t flags, float* Ut, float* sigma, float* Vt, int32_t* d_status, void* ws,
+                        size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (nb <= 0) return fail(HG_ERR_INVALID, "nb must be > 0");
+  HG_TRY(check_sizes((int64_t)nb * b, b, k, q, 0));
+  if (!blocks || !Ut || !sigma || !Vt || !d_status) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  const Layout Lo = layout((int64_t)nb * b, 1, 0, b, k, 0);
+  HG_TRY(check_ws(ws, ws_bytes, Lo.status));
+  return run_rsvd(blocks, nb, b, k, q, seed, (flags & HG_GEMM_SIMT) != 0, Ut, sigma, Vt, d_status, ws, Lo,
+                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const float* Vt, int32_t nb, int32_t b,
+                                 int32_t k, const float* Y, int32_t T, float scale, float* F, int32_t* d_status,
+                                 void* ws, size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (nb <= 0) return fail(HG_ERR_INVALID, "nb must be > 0");
+  HG_TRY(check_sizes((int64_t)nb * b, b, k, 0, T));
+  if (!Ut || !sigma || !Vt || !d_status || (T > 0 && (!Y || !F))) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (!std::isfinite(scale)) return fail(HG_ERR_INVALID, "scale must be finite");
+  const Layout Lo = layout((int64_t)nb * b, 1, 0, b, k, T);
+  HG_TRY(check_ws(ws, ws_bytes, Lo.status));
+  return run_apply(Ut, sigma, Vt, nb, b, k, Y, T, scale, F, d_status, ws, Lo, reinterpret_cast<cudaStream_t>(stream),
+                   false);
+}
+
+static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
+                            uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags,
+                            int32_t* d_status, void* ws, size_t ws_bytes, cudaStream_t s) {
+  HG_TRY(check_H(H));
+  HG_TRY(check_sizes(H->n_vertices, b, k, q, T));
+  if (!(mu > 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and > 0");
+  if (!w || (T > 0 && (!Y || !F))) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, k, T);
+  HG_TRY(check_ws(ws, ws_bytes, Lo.h_rowptr));
+  const bool simt = (flags & HG_GEMM_SIMT) != 0;
+  int32_t* st = d_status;
+  if (!st) {
+    if (!(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
+    st = at<int32_t>(ws, Lo.status);
+    HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), s), "memset status");
+  }
+  const int nb = H->n_vertices / b;
+  float* blocks = at<float>(ws, Lo.blocks);
+  float* Ut = at<float>(ws, Lo.Ut);
+  float* Vt = at<float>(ws, Lo.Vt);
+  float* sigma = sigma_out ? sigma_out : at<float>(ws, Lo.sigma);
+  HG_TRY(run_theta(H, w, mu, b, false, blocks, nullptr, st, ws, Lo, s));
+  HG_TRY(run_rsvd(blocks, nb, b, k, q, seed, simt, Ut, sigma, Vt, st, ws, Lo, s));
+  HG_TRY(run_apply(Ut, sigma, Vt, nb, b, k, Y, T, mu / (1.0f + mu), F, st, ws, Lo, s, simt));
+  if (flags & HG_SYNC) {
+    int32_t h = 0;
+    HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
+    HG_CU(cudaStreamSynchronize(s), "synchronize");
+    if (h) return fail(HG_ERR_NUMERICAL, "device status 0x%x (bits: 1 isolated vertex, 2 empty hyperedge, 4 "
+                       "Cholesky breakdown, 8 Jacobi cap, 16 singular sigma, 32 non-finite)", h);
+  }
+  return HG_OK;
+}
+
+hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q, uint64_t seed,
+                   const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags, int32_t* d_status, void* ws,
+                   size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  return solve_impl(H, w, mu, b, k, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes,
+                    reinterpret_cast<cudaStream_t>(stream));
+}
+
+hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_ptr_host, const int32_t* col_idx_host,
+                        const float* w_host, float mu, int32_t b, int32_t k, int32_t q, uint64_t seed,
+                        const float* Y_host, int32_t T, float* F_host, float* sigma_host, uint32_t flags, void* ws,
+                        size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!row_ptr_host || !w_host || (nnz > 0 && !col_idx_host) || (T > 0 && (!Y_host || !F_host)))
+    return fail(HG_ERR_INVALID, "NULL host pointer");
+  HG_TRY(check_sizes(N, b, k, q, T));
+  if (E <= 0 || nnz < 0) return fail(HG_ERR_INVALID, "need E > 0, nnz >= 0");
+  const Layout Lo = layout(N, E, nnz, b, k, T);
+  HG_TRY(check_ws(ws, ws_bytes, Lo.total));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int64_t* d_rp = at<int64_t>(ws, Lo.h_rowptr);
+  int32_t* d_col = at<int32_t>(ws, Lo.h_col);
+  float* d_w = at<float>(ws, Lo.h_w);
+  float* d_Y = at<float>(ws, Lo.h_Y);
+  float* d_F = at<float>(ws, Lo.h_F);
+  HG_CU(cudaMemcpyAsync(d_rp, row_ptr_host, 8 * (size_t)(N + 1), cudaMemcpyHostToDevice, s), "H2D row_ptr");
+  if (nnz > 0) HG_CU(cudaMemcpyAsync(d_col, col_idx_host, 4 * (size_t)nnz, cudaMemcpyHostToDevice, s), "H2D col_idx");
+  HG_CU(cudaMemcpyAsync(d_w, w_host, 4 * (size_t)E, cudaMemcpyHostToDevice, s), "H2D w");
+  if (T > 0) HG_CU(cudaMemcpyAsync(d_Y, Y_host, 4 * (size_t)N * T, cudaMemcpyHostToDevice, s), "H2D Y");
+  hg_incidence H{N, E, nnz, d_rp, d_col};
+  const int nb = N / b;
+  float* d_sig = at<float>(ws, Lo.sigma);
+  int32_t* st = at<int32_t>(ws, Lo.status);
+  HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), s), "memset status");
+  HG_TRY(solve_impl(&H, d_w, mu, b, k, q, seed, d_Y, T, d_F, d_sig, flags & ~HG_SYNC, st, ws, ws_bytes, s));
+  if (T > 0) HG_CU(cudaMemcpyAsync(F_host, d_F, 4 * (size_t)N * T, cudaMemcpyDeviceToHost, s), "D2H F");
+  if (sigma_host)
+    HG_CU(cudaMemcpyAsync(sigma_host, d_sig, 4 * (size_t)nb * k, cudaMemcpyDeviceToHost, s), "D2H sigma");
+  int32_t h = 0;
+  HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
+  HG_CU(cudaStreamSynchronize(s), "synchronize");
+  if (h) return fail(HG_ERR_NUMERICAL, "device status 0x%x", h);
+  return HG_OK;
+}
+
+hg_status hg_gemm(int32_t M, int32_t N, int32_t K, int32_t batch, const float* A, int32_t a_mn, int64_t lda,
+                  int64_t sa, const float* B, int32_t b_mn, int64_t ldb, int64_t sb, float* D, int32_t d_trans,
+                  int64_t ldd, int64_t sd, float alpha, const float* rs, int64_t srs, const float* cs, int64_t scs,
+                  uint32_t flags, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!A || !B || !D) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  GemmDesc g;
+  g.M = M; g.N = N; g.K = K; g.batch = batch;
+  g.A = A; g.a_mn = a_mn != 0; g.lda = lda; g.sa = sa;
+  g.B = B; g.b_mn = b_mn != 0; g.ldb = ldb; g.sb = sb;
+  g.D = D; g.d_trans = d_trans != 0; g.ldd = ldd; g.sd = sd;
+  g.alpha = alpha; g.rs = rs; g.srs = srs; g.cs = cs; g.scs = scs;
+  return gemm(g, reinterpret_cast<cudaStream_t>(stream), (flags & HG_GEMM_SIMT) != 0, "hg_gemm");
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// finalize.cu -- Alg. 1 steps 5-6 epilogue and the Eq. 15 scale.
+//
+// Inputs per block: Vw_t = (B^T U~)^T and Uw_t = (S U~)^T (k x b, one row per
+// singular triplet, unsorted).  sigma_j = ||B^T u~_j|| accumulated in fp64
+// (the singular value of B for the eigenvector u~_j of B B^T), then the
+// triplets are sorted non-increasing (ties by index), v_j = B^T u~_j / sigma_j,
+// u_j = S u~_j, and the pair's sign is fixed so that the
+// largest-|.| entry of u_j (first index on ties) is positive.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+constexpr int NT = 256;
+
+__global__ void __launch_bounds__(NT) k_colnorm(int b, const float* __restrict__ Vw_t, double* __restrict__ sig) {
+  __shared__ double red[NT / 32];
+  const int64_t row = blockIdx.x;               // blk*k + j
+  const float* x = Vw_t + row * b;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < b; i += NT) {
+    const double v = x[i];
+    acc = fma(v, v, acc);
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < NT / 32; ++w) s += red[w];
+    sig[row] = sqrt(s);
+  }
+}
+
+// one CTA per block: rank of each sigma (descending, ties by index) -> perm, sigma_out
+__global__ void k_rank(int k, const double* __restrict__ sig, int32_t* __restrict__ perm, float* __restrict__ sigma,
+                       int32_t* status) {
+  const int blk = blockIdx.x;
+  const double* s = sig + (int64_t)blk * k;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const double v = s[j];
+    if (!isfinite(v)) hg_flag(status, HGS_NONFINITE);
+    int r = 0;
+    for (int l = 0; l < k; ++l) {
+      const double w = s[l];
+      r += (w > v) || (w == v && l < j);
+    }
+    perm[(int64_t)blk * k + r] = j;
+    sigma[(int64_t)blk * k + r] = (float)v;
+  }
+}
+
+// one CTA per (block, sorted index jj)
+__global__ void __launch_bounds__(NT) k_rows(int b, int k, const float* __restrict__ Vw_t,
+                                             const float* __restrict__ Uw_t, const int32_t* __restrict__ perm,
+                                             const double* __restrict__ sig, float* __restrict__ Ut,
+                                             float* __restrict__ Vt) {
+  __shared__ float bv[NT / 32];
+  __shared__ int bi[NT / 32];
+  const int blk = blockIdx.x / k, jj = blockIdx.x % k;
+  const int j = perm[(int64_t)blk * k + jj];
+  const int64_t src = ((int64_t)blk * k + j) * b, dst = ((int64_t)blk * k + jj) * b;
+  const float* u = Uw_t + src;
+  float best = -1.f;
+  int arg = 0x7fffffff;
+  for (int i = threadIdx.x; i < b; i += NT) {
+    const float a = fabsf(u[i]);
+    if (a > best) { best = a; arg = i; }        // i increases: first index kept on ties
+  }
+  for (int o = 16; o; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (ob > best || (ob == best && oi < arg)) { best = ob; arg = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { bv[threadIdx.x >> 5] = best; bi[threadIdx.x >> 5] = arg; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < NT / 32; ++w)
+      if (bv[w] > bv[0] || (bv[w] == bv[0] && bi[w] < bi[0])) { bv[0] = bv[w]; bi[0] = bi[w]; }
+  }
+  __syncthreads();
+  const float sgn = (u[bi[0]] < 0.f) ? -1.f : 1.f;
+  const double sv = sig[(int64_t)blk * k + j];
+  const float vs = (float)((double)sgn / sv);
+  const float* v = Vw_t + src;
+  for (int i = threadIdx.x; i < b; i += NT) {
+    Ut[dst + i] = sgn * u[i];
+    Vt[dst + i] = v[i] * vs;
+  }
+}
+
+__global__ void k_inv_sigma(int nb, int k, const float* __restrict__ sigma, float scale, float* __restrict__ rs,
+                            int32_t* status) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nb * k) return;
+  const int64_t blk = i / k;
+  const float s = sigma[i], s1 = sigma[blk * k];
+  if (!isfinite(s) || !(s > 1e-6f * s1)) {
+    hg_flag(status, isfinite(s) ? HGS_SINGULAR_SIGMA : HGS_NONFINITE);
+    rs[i] = 0.f;
+    return;
+  }
+  rs[i] = scale / s;
+}
+
+}  // namespace
+
+cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float* Uw_t, float* Ut, float* sigma,
+                            float* Vt, double* sig_raw, int32_t* status, cudaStream_t s, int* launches) {
+  int32_t* perm = reinterpret_cast<int32_t*>(sig_raw + (size_t)nb * k);
+  k_colnorm<<<nb * k, NT, 0, s>>>(b, Vw_t, sig_raw);
+  k_rank<<<nb, 256, 0, s>>>(k, sig_raw, perm, sigma, status);
+  k_rows<<<nb * k, NT, 0, s>>>(b, k, Vw_t, Uw_t, perm, sig_raw, Ut, Vt);
+  *launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_inv_sigma(int nb, int k, const float* sigma, float scale, float* rs, int32_t* status,
+                             cudaStream_t s, int* launches) {
+  const int64_t n = (int64_t)nb * k;
+  k_inv_sigma<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nb, k, sigma, scale, rs, status);
+  ++*launches;
+  return cudaGetLastError();
+}

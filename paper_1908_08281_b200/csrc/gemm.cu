@@ -1,0 +1,390 @@
+// gemm.cu -- batched FP32 GEMM on the 5th-generation tensor cores via 3xTF32.
+//
+// Every dense contraction of the path runs here:
+//   power products  Y = X_ii S       (X_ii^T S = X_ii S, reading A12)
+//   Gram matrices   G = P^T P        (CholeskyQR2)
+//   Q-formation     Q = P L^-T       (CholeskyQR2)
+//   B = S^T X_ii, V = B^T U~, U = S U~, and the Eq. 15 apply
+//
+// Design (sm_100a):
+//   * one CTA per 128 x BN output tile, 10 warps: warps 0-7 split each TMA-landed
+//     fp32 tile into tf32 hi (in place) and lo (second buffer), drain finished
+//     TMEM chunks and run the epilogue; warp 8 issues TMA (cp.async.bulk.tensor);
+//     warp 9 allocates TMEM and one lane issues tcgen05.mma.kind::tf32 (M=128, N=BN, K=8).
+//   * 3xTF32: D += A_lo B_hi + A_hi B_lo + A_hi B_hi with hi = rna_tf32(x),
+//     lo = rna_tf32(x - hi) (reading A13), fp32 accumulation in TMEM.
+//   * operands may be K-major or MN-major in global memory (both legal for
+//     kind::tf32); the mbarrier ring is full(TMA) -> conv(split) -> empty(commit).
+//   * accumulation: TMEM chunks of K = 64, ping-pong, summed in fp32 registers
+//     (see gemm_tf32x3_kernel); epilogue: scaled, coalesced stores (a warp owns 32
+//     consecutive rows m, so a transposed store D[n][m] is one 128-byte line).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 elements per 128-byte swizzle row
+
+struct EpiArgs {
+  int M, N, K;
+  float* D;
+  int64_t ldd, sd;
+  int d_trans;
+  float alpha;
+  const float* rs;
+  int64_t srs;
+  const float* cs;
+  int64_t scs;
+  int a_mn, b_mn;
+};
+
+constexpr int NEPI = 256;            // converter / epilogue threads (8 warps)
+constexpr int NTHREADS = NEPI + 64;  // + TMA warp + MMA warp
+constexpr int CHUNK_KB = 2;          // k-blocks accumulated per TMEM chunk (K = 64)
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 4;   // 16 KB
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = (STAGE_BYTES * 4 <= 200 * 1024) ? 4 : (STAGE_BYTES * 3 <= 200 * 1024 ? 3 : 2);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  static constexpr uint32_t TX = (uint32_t)(BM + BN) * BK * 4;
+  static constexpr int HALF = BN / 2;           // columns per epilogue warp
+};
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, M = 128, N = BN.
+__device__ __forceinline__ uint32_t make_idesc(int bn, int a_mn, int b_mn) {
+  uint32_t d = 0;
+  d |= 1u << 4;                      // c_format = F32
+  d |= 2u << 7;                      // a_format = TF32
+  d |= 2u << 10;                     // b_format = TF32
+  d |= (uint32_t)(a_mn & 1) << 15;   // a_major
+  d |= (uint32_t)(b_mn & 1) << 16;   // b_major
+  d |= (uint32_t)(bn >> 3) << 17;    // n_dim
+  d |= (uint32_t)(BM >> 4) << 24;    // m_dim
+  return d;
+}
+
+__device__ __forceinline__ float4 split_hi(float4& x) {
+  float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+  float4 l = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z), tf32_rna(x.w - h.w));
+  x = h;
+  return l;
+}
+
+// Accumulation: the tensor pipe's fp32 adder truncates, so an accumulator that
+// absorbs all K/8 * 3 MMAs loses accuracy linearly in K (measured 7e-6 relative
+// at K = 1024).  The MMAs of each K-chunk of 64 go to a fresh TMEM buffer (two
+// buffers, ping-pong); the epilogue warps drain finished chunks and sum them in
+// fp32 round-to-nearest registers, bounding the truncation to 24 MMAs.
+template <int BN>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       EpiArgs ea) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[C::STAGES], conv_bar[C::STAGES], empty_bar[C::STAGES];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, g = blockIdx.z;
+  const int num_kb = (ea.K + BK - 1) / BK;
+  const int nchunks = (num_kb + CHUNK_KB - 1) / CHUNK_KB;
+
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  auto sA_hi = [&](int s) { return base + s * C::STAGE_BYTES; };
+  auto sA_lo = [&](int s) { return base + s * C::STAGE_BYTES + C::A_BYTES; };
+  auto sB_hi = [&](int s) { return base + s * C::STAGE_BYTES + 2 * C::A_BYTES; };
+  auto sB_lo = [&](int s) { return base + s * C::STAGE_BYTES + 2 * C::A_BYTES + C::B_BYTES; };
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&conv_bar[s], NEPI / 32);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], NEPI / 32);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<C::TMEM_COLS>(&tmem_base_sh);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 8) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % C::STAGES;
+        const uint32_t ph = (kb / C::STAGES) & 1;
+        if (kb >= C::STAGES) mbar_wait(&empty_bar[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full_bar[s], C::TX);
+        const int k0 = kb * BK;
+        if (!ea.a_mn) {
+          tma_load_3d(sA_hi(s), &tmA, &full_bar[s], k0, m0, g);
+        } else {
+#pragma unroll
+          for (int c = 0; c < BM / 32; ++c) tma_load_3d(sA_hi(s) + c * 4096, &tmA, &full_bar[s], m0 + 32 * c, k0, g);
+        }
+        if (!ea.b_mn) {
+          tma_load_3d(sB_hi(s), &tmB, &full_bar[s], k0, n0, g);
+        } else {
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c) tma_load_3d(sB_hi(s) + c * 4096, &tmB, &full_bar[s], n0 + 32 * c, k0, g);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ---------------- MMA issuer (single thread)
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc(BN, ea.a_mn, ea.b_mn);
+      // K-major (SWIZZLE_128B): 8-row groups 1024 B apart (SBO), K-step = +32 B in the row.
+      // MN-major (SWIZZLE_128B_BASE32B): 32-element chunks BK*128 B apart (LBO),
+      // 4-row groups 512 B apart (SBO), K-step = +1024 B (8 rows).
+      const uint32_t a_lbo = ea.a_mn ? BK * 128 : 16, b_lbo = ea.b_mn ? BK * 128 : 16;
+      const uint32_t a_sbo = ea.a_mn ? 512 : 1024, b_sbo = ea.b_mn ? 512 : 1024;
+      const uint32_t a_lay = ea.a_mn ? 1 : 2, b_lay = ea.b_mn ? 1 : 2;
+      const uint32_t a_kstep = ea.a_mn ? 1024 : 32, b_kstep = ea.b_mn ? 1024 : 32;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % C::STAGES;
+        const uint32_t ph = (kb / C::STAGES) & 1;
+        const int c = kb / CHUNK_KB, buf = c & 1;
+        const bool first = (kb % CHUNK_KB) == 0;
+        if (first && c >= 2) {
+          mbar_wait(&tempty_bar[buf], ((c >> 1) - 1) & 1);
+          tc_fence_after();
+        }
+        mbar_wait(&conv_bar[s], ph);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(buf * BN);
+        const uint32_t ahi = smem_u32(sA_hi(s)), alo = smem_u32(sA_lo(s));
+        const uint32_t bhi = smem_u32(sB_hi(s)), blo = smem_u32(sB_lo(s));
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t dah = umma_desc(ahi + kk * a_kstep, a_lbo, a_sbo, a_lay);
+          const uint64_t dal = umma_desc(alo + kk * a_kstep, a_lbo, a_sbo, a_lay);
+          const uint64_t dbh = umma_desc(bhi + kk * b_kstep, b_lbo, b_sbo, b_lay);
+          const uint64_t dbl = umma_desc(blo + kk * b_kstep, b_lbo, b_sbo, b_lay);
+          mma_tf32(d, dal, dbh, idesc, (first && kk == 0) ? 0u : 1u);
+          mma_tf32(d, dah, dbl, idesc, 1);
+          mma_tf32(d, dah, dbh, idesc, 1);
+        }
+        mma_commit(&empty_bar[s]);
+        if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == num_kb - 1) mma_commit(&tfull_bar[buf]);
+      }
+    }
+  } else {
+    // ---------------- warps 0-7: tf32 hi/lo split, chunk drains, epilogue
+    const int t = threadIdx.x;
+    const int q = warp & 3, h = warp >> 2;          // TMEM lane quarter, column half
+    float acc[C::HALF];
+#pragma unroll
+    for (int j = 0; j < C::HALF; ++j) acc[j] = 0.f;
+    auto drain = [&](int dch) {
+      const int buf = dch & 1;
+      mbar_wait(&tfull_bar[buf], (dch >> 1) & 1);
+      tc_fence_after();
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * C::HALF);
+#pragma unroll
+      for (int j0 = 0; j0 < C::HALF; j0 += 16) {
+        float v[16];
+        tmem_ld16(ta + j0, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[j0 + i] += v[i];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+    };
+    int drained = 0;
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % C::STAGES;
+      const uint32_t ph = (kb / C::STAGES) & 1;
+      mbar_wait(&full_bar[s], ph);
+      float4* ah = reinterpret_cast<float4*>(sA_hi(s));
+      float4* al = reinterpret_cast<float4*>(sA_lo(s));
+#pragma unroll
+      for (int i = t; i < BM * BK / 4; i += NEPI) {
+        float4 x = ah[i];
+        float4 l = split_hi(x);
+        ah[i] = x;
+        al[i] = l;
+      }
+      float4* bh = reinterpret_cast<float4*>(sB_hi(s));
+      float4* bl = reinterpret_cast<float4*>(sB_lo(s));
+#pragma unroll
+      for (int i = t; i < BN * BK / 4; i += NEPI) {
+        float4 x = bh[i];
+        float4 l = split_hi(x);
+        bh[i] = x;
+        bl[i] = l;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv_bar[s]);
+      // drain chunk d once the MMAs of chunk d+1 are under way
+      while (drained < nchunks - 1 && kb >= (drained + 1) * CHUNK_KB + 1) drain(drained++);
+    }
+    while (drained < nchunks) drain(drained++);
+    // epilogue: scale and store from registers
+    const int m = m0 + q * 32 + lane;
+    if (m < ea.M) {
+      const float rsv = ea.alpha * (ea.rs ? ea.rs[(int64_t)g * ea.srs + m] : 1.0f);
+      float* Dg = ea.D + (int64_t)g * ea.sd;
+      const int nb0 = n0 + h * C::HALF;
+#pragma unroll
+      for (int j = 0; j < C::HALF; ++j) {
+        const int n = nb0 + j;
+        if (n < ea.N) {
+          float val = acc[j] * rsv;
+          if (ea.cs) val *= ea.cs[(int64_t)g * ea.scs + n];
+          if (ea.d_trans)
+            Dg[(int64_t)n * ea.ldd + m] = val;
+          else
+            Dg[(int64_t)m * ea.ldd + n] = val;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+// ------------------------------------------------------------------ SIMT fp32 (verification)
+__global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict__ A, int a_mn, int64_t lda,
+                                                        int64_t sa, const float* __restrict__ B, int b_mn,
+                                                        int64_t ldb, int64_t sb, EpiArgs ea) {
+  __shared__ float As[16][64 + 1], Bs[16][64 + 1];
+  const int g = blockIdx.z, m0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const float* Ag = A + (int64_t)g * sa;
+  const float* Bg = B + (int64_t)g * sb;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < ea.K; k0 += 16) {
+    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+      const int kk = i / 64, mm = i % 64;
+      const int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < ea.M && k < ea.K) ? Ag[a_mn ? (int64_t)k * lda + m : (int64_t)m * lda + k] : 0.f;
+      const int n = n0 + mm;
+      Bs[kk][mm] = (n < ea.N && k < ea.K) ? Bg[b_mn ? (int64_t)k * ldb + n : (int64_t)n * ldb + k] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(As[kk][ty * 4 + i], Bs[kk][tx * 4 + j], acc[i][j]);
+    __syncthreads();
+  }
+  float* Dg = ea.D + (int64_t)g * ea.sd;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m < ea.M && n < ea.N) {
+        float v = acc[i][j] * ea.alpha;
+        if (ea.rs) v *= ea.rs[(int64_t)g * ea.srs + m];
+        if (ea.cs) v *= ea.cs[(int64_t)g * ea.scs + n];
+        if (ea.d_trans)
+          Dg[(int64_t)n * ea.ldd + m] = v;
+        else
+          Dg[(int64_t)m * ea.ldd + n] = v;
+      }
+    }
+}
+
+// ------------------------------------------------------------------ host
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 3D map: (inner, outer, batch), row pitch ld elements, batch pitch bs elements; box (32, box_outer, 1).
+bool make_map(CUtensorMap* m, const float* ptr, int64_t inner, int64_t outer, int64_t batch, int64_t ld,
+              int64_t bs, int box_outer, bool mn_major) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  if (batch <= 1) bs = ld * outer;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)(batch < 1 ? 1 : batch)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)bs * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_outer, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN>
+cudaError_t launch_tc(const GemmDesc& g, const EpiArgs& ea, cudaStream_t stream) {
+  using C = Cfg<BN>;
+  static bool attr_set = false;  // per-instantiation; set once per process
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tf32x3_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  bool ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.batch, g.lda, g.sa, 32, true)
+                   : make_map(&ta, g.A, g.K, g.M, g.batch, g.lda, g.sa, BM, false);
+  ok = ok && (g.b_mn ? make_map(&tb, g.B, g.N, g.K, g.batch, g.ldb, g.sb, 32, true)
+                     : make_map(&tb, g.B, g.K, g.N, g.batch, g.ldb, g.sb, BN, false));
+  if (!ok) return cudaErrorInvalidValue;
+  dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, g.batch);
+  gemm_tf32x3_kernel<BN><<<grid, NTHREADS, C::SMEM, stream>>>(ta, tb, ea);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+const char* gemm_check(const GemmDesc& g) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return "gemm: non-positive size";
+  if (g.batch > 65535) return "gemm: batch > 65535";
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al16(g.A) || !al16(g.B)) return "gemm: A/B must be 16-byte aligned";
+  if ((g.lda & 3) || (g.ldb & 3)) return "gemm: lda/ldb must be multiples of 4";
+  if (g.batch > 1 && ((g.sa & 3) || (g.sb & 3))) return "gemm: batch strides must be multiples of 4";
+  if (g.a_mn ? g.lda < g.M : g.lda < g.K) return "gemm: lda too small";
+  if (g.b_mn ? g.ldb < g.N : g.ldb < g.K) return "gemm: ldb too small";
+  return nullptr;
+}
+
+cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
+  EpiArgs ea{g.M, g.N, g.K, g.D, g.ldd, g.sd, g.d_trans ? 1 : 0, g.alpha, g.rs, g.srs, g.cs, g.scs,
+             g.a_mn ? 1 : 0, g.b_mn ? 1 : 0};
+  if (simt) {
+    dim3 grid((g.M + 63) / 64, (g.N + 63) / 64, g.batch);
+    gemm_simt_kernel<<<grid, 256, 0, stream>>>(g.A, ea.a_mn, g.lda, g.sa, g.B, ea.b_mn, g.ldb, g.sb, ea);
+    return cudaGetLastError();
+  }
+  if (g.N <= 32) return launch_tc<32>(g, ea, stream);
+  if (g.N <= 64) return launch_tc<64>(g, ea, stream);
+  if (g.N <= 128) return launch_tc<128>(g, ea, stream);
+  return launch_tc<256>(g, ea, stream);
+}

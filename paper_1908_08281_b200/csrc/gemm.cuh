@@ -1,0 +1,33 @@
+// gemm.cuh -- batched GEMM descriptor shared by the orchestration code.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+// D_g(m,n) = alpha * rs_g[m] * cs_g[n] * sum_kk A_g(m,kk) B_g(kk,n),  g < batch
+//   A_g(m,kk) = A[g*sa + (a_mn ? kk*lda + m : m*lda + kk)]   (a_mn: "M-major" storage)
+//   B_g(kk,n) = B[g*sb + (b_mn ? kk*ldb + n : n*ldb + kk)]
+//   d_trans ? D[g*sd + n*ldd + m] : D[g*sd + m*ldd + n]
+struct GemmDesc {
+  int M = 0, N = 0, K = 0, batch = 1;
+  const float* A = nullptr;
+  bool a_mn = false;
+  int64_t lda = 0, sa = 0;
+  const float* B = nullptr;
+  bool b_mn = false;
+  int64_t ldb = 0, sb = 0;
+  float* D = nullptr;
+  bool d_trans = false;
+  int64_t ldd = 0, sd = 0;
+  float alpha = 1.0f;
+  const float* rs = nullptr;
+  int64_t srs = 0;
+  const float* cs = nullptr;
+  int64_t scs = 0;
+};
+
+// Enqueue the GEMM; returns cudaSuccess or the launch error.  `simt` selects the
+// CUDA-core fp32 verification kernel instead of the tcgen05 3xTF32 kernel.
+cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt);
+// Validation used by the ABI (alignment/stride requirements of TMA); returns a
+// static message or nullptr.
+const char* gemm_check(const GemmDesc& g);

@@ -1,0 +1,181 @@
+// jacobi.cu -- Alg. 1 step 5: SVD of the k x b matrix B by
+// one-sided (Hestenes) Jacobi, QR-preconditioned.
+//
+// With B B^T = L L^T (Cholesky of the Gram of B^T, computed by the GEMM + chol
+// kernels), W = L^T satisfies W^T W = B B^T.  One-sided Jacobi rotates column
+// pairs of W until all columns are mutually orthogonal: W J = W_f.  Then J is
+// the left singular vector matrix U~ of B, the column norms of W_f are the
+// singular values, and J = W^-1 W_f = L^-T W_f is recovered afterwards by a
+// GEMM (no rotation accumulator is stored).  Each rotation is the one that
+// zeroes the 2x2 Gram [[a_pp, a_pq], [a_pq, a_qq]] of the pair (Golub & Van
+// Loan sym.schur2): zeta = (a_qq - a_pp)/(2 a_pq), t = sgn(zeta)/(|zeta| +
+// sqrt(1+zeta^2)), c = 1/sqrt(1+t^2), s = c t; w_p <- c w_p - s w_q,
+// w_q <- s w_p + c w_q.
+//
+// Parallel order: round-robin tournament, k/2 disjoint pairs per round, k-1
+// rounds per sweep.  W (fp32) is split by rows over a thread-block cluster of
+// C = ceil(k/64) CTAs (one for k <= 64); each CTA holds its row slab in shared
+// memory, forms fp64 partial Gram entries for all pairs, exchanges them through
+// distributed shared memory, and every CTA sums the C partials in the same order
+// so all CTAs take identical rotation decisions.  A pair rotates only while
+// |a_pq| > tol sqrt(a_pp a_qq); the sweep loop stops after a sweep with no
+// rotation or flags HG_ST_JACOBI_CAP after MAX_SWEEPS.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int NT = 512;
+constexpr int MAX_SWEEPS = 40;
+constexpr double TOL = 3e-7;
+
+__device__ __forceinline__ void pair_of(int r, int i, int K2, int& p, int& q) {
+  const int n1 = K2 - 1;
+  if (i == 0) { p = 0; q = 1 + r; return; }
+  p = 1 + (r + i) % n1;
+  q = 1 + (r - i + n1) % n1;
+}
+
+__global__ void __launch_bounds__(NT) k_jacobi(int k, int C, int nbuf, const float* __restrict__ L,
+                                               float* __restrict__ Wf, int32_t* status) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (C > 1) ? (int)cluster.block_rank() : 0;
+  const int blk = blockIdx.x / C;
+  const int K2 = (k + 1) & ~1;          // pad to even with a virtual zero column
+  const int P = K2 / 2;
+  const int R = (k + C - 1) / C;        // rows per CTA
+  const int r0 = rank * R;
+  const int nr = max(0, min(R, k - r0));
+  const int ldw = K2 + 1;
+  float* W = reinterpret_cast<float*>(smem_raw);                               // [R][ldw]
+  double* part = reinterpret_cast<double*>(smem_raw + (((size_t)R * ldw * 4 + 15) & ~size_t(15)));  // [nbuf][C][P][3]
+  const int t = threadIdx.x;
+  const float* Lb = L + (int64_t)blk * k * k;
+
+  for (int i = t; i < R * ldw; i += NT) {
+    const int rl = i / ldw, c = i % ldw;
+    const int r = r0 + rl;
+    W[i] = (rl < nr && c < k) ? Lb[(int64_t)c * k + r] : 0.f;   // W = L^T
+  }
+  __syncthreads();
+
+  // thread -> (pair group, sub-lane): Gp threads per pair (power of two <= 32)
+  int Gp = NT / P;
+  if (Gp > 32) Gp = 32;
+  if (Gp < 1) Gp = 1;
+  { int g = 1; while (g * 2 <= Gp) g *= 2; Gp = g; }
+  const int groups = NT / Gp;
+  const int sub = t % Gp, grp = t / Gp;
+  const unsigned gmask = (Gp == 32) ? 0xffffffffu : (((1u << Gp) - 1u) << ((t & 31) / Gp * Gp));
+
+  int sweep = 0;
+  bool converged = false;
+  for (; sweep < MAX_SWEEPS && !converged; ++sweep) {
+    int any = 0;
+    for (int r = 0; r < K2 - 1; ++r) {
+      const int buf = r % nbuf;
+      // single-buffered exchange: everyone must have read the previous round's partials
+      if (nbuf == 1 && C > 1 && r > 0) cluster.sync();
+      // A: partial Gram entries over this CTA's rows
+      for (int i = grp; i < P; i += groups) {
+        int p, q;
+        pair_of(r, i, K2, p, q);
+        double app = 0, aqq = 0, apq = 0;
+        for (int rl = sub; rl < nr; rl += Gp) {
+          const double wp = W[rl * ldw + p], wq = W[rl * ldw + q];
+          app = fma(wp, wp, app);
+          aqq = fma(wq, wq, aqq);
+          apq = fma(wp, wq, apq);
+        }
+        for (int o = Gp / 2; o; o >>= 1) {
+          app += __shfl_xor_sync(gmask, app, o);
+          aqq += __shfl_xor_sync(gmask, aqq, o);
+          apq += __shfl_xor_sync(gmask, apq, o);
+        }
+        if (sub == 0) {
+          double* dst = part + (((size_t)buf * C + rank) * P + i) * 3;
+          if (C > 1) {
+            for (int cr = 0; cr < C; ++cr) {
+              double* rd = cluster.map_shared_rank(dst, cr);
+              rd[0] = app; rd[1] = aqq; rd[2] = apq;
+            }
+          } else {
+            dst[0] = app; dst[1] = aqq; dst[2] = apq;
+          }
+        }
+      }
+      if (C > 1) cluster.sync(); else __syncthreads();
+      // C: total Gram entries (fixed summation order), rotation, apply to local rows
+      int rot = 0;
+      for (int i = grp; i < P; i += groups) {
+        int p, q;
+        pair_of(r, i, K2, p, q);
+        double app = 0, aqq = 0, apq = 0;
+        for (int cr = 0; cr < C; ++cr) {
+          const double* src = part + (((size_t)buf * C + cr) * P + i) * 3;
+          app += src[0]; aqq += src[1]; apq += src[2];
+        }
+        if (p >= k || q >= k) continue;
+        if (!(fabs(apq) > TOL * sqrt(app * aqq))) continue;
+        const double zeta = (aqq - app) / (2.0 * apq);
+        const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cd = 1.0 / sqrt(1.0 + tt * tt);
+        const float c = (float)cd, s = (float)(cd * tt);
+        rot = 1;
+        for (int rl = sub; rl < nr; rl += Gp) {
+          const float wp = W[rl * ldw + p], wq = W[rl * ldw + q];
+          W[rl * ldw + p] = c * wp - s * wq;
+          W[rl * ldw + q] = s * wp + c * wq;
+        }
+      }
+      any |= __syncthreads_or(rot);
+    }
+    converged = (any == 0);
+  }
+  if (!converged && t == 0 && rank == 0) hg_flag(status, HGS_JACOBI_CAP);
+  float* out = Wf + (int64_t)blk * k * k;
+  for (int i = t; i < nr * k; i += NT) {
+    const int rl = i / k, c = i % k;
+    out[(int64_t)(r0 + rl) * k + c] = W[rl * ldw + c];
+  }
+  if (C > 1) cluster.sync();   // no CTA exits while others may still write its shared memory
+}
+
+}  // namespace
+
+cudaError_t launch_jacobi(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s,
+                          int* launches) {
+  const int C = (k + 63) / 64;
+  if (C > 8) return cudaErrorInvalidValue;
+  const int K2 = (k + 1) & ~1, P = K2 / 2, R = (k + C - 1) / C;
+  const size_t wbytes = (((size_t)R * (K2 + 1) * 4) + 15) & ~size_t(15);
+  const size_t pbytes = (size_t)C * P * 3 * sizeof(double);
+  const int nbuf = (wbytes + 2 * pbytes <= 220 * 1024) ? 2 : 1;
+  const size_t smem = wbytes + nbuf * pbytes;
+  cudaError_t e = cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (C > 1) {
+    e = cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nb * C);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, k_jacobi, k, C, nbuf, L, Wf, status);
+  ++*launches;
+  return e;
+}

@@ -1,0 +1,34 @@
+// kernels.cuh -- launchers for the non-GEMM kernels of the path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+// theta.cu -- PAPER.md:30-40 (degrees, Eq. 1, X = I - Theta/(1+mu))
+cudaError_t launch_degrees(int N, int E, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
+                           int32_t* de_cnt, float* edge_val, float* dv_rsqrt, int32_t* status,
+                           cudaStream_t s, int* launches);
+cudaError_t launch_assemble(int nb, int b, const int64_t* row_ptr, const int32_t* col_idx,
+                            const float* edge_val, const float* dv_rsqrt, float mu, bool raw_theta,
+                            float* blocks, cudaStream_t s, int* launches);
+
+// philox.cu -- Alg. 1 step 1, reading A6
+// panel: out[i][c][m] = Omega[i*b + m][c] (Omega is N x k, normal index r*k + c)
+cudaError_t launch_omega_panels(uint64_t seed, int nb, int b, int k, float* out, cudaStream_t s, int* launches);
+// row-major rows x cols: out[r][c] = normal r*cols + c
+cudaError_t launch_gaussian_rowmajor(uint64_t seed, int rows, int cols, float* out, cudaStream_t s,
+                                     int* launches);
+
+// chol.cu -- CholeskyQR: G = L L^T (lower L), Linv = L^-1; near-identity first-order path
+cudaError_t launch_cholinv(int nb, int k, const float* G, float* L, float* Linv, float* work,
+                           int32_t* status, cudaStream_t s, int* launches);
+
+// jacobi.cu -- one-sided Jacobi on W = L^T (k x k): W_f = W J with orthogonal columns
+cudaError_t launch_jacobi(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s,
+                          int* launches);
+
+// finalize.cu -- sigma_j = ||V_w column j|| (fp64), sort, normalise, sign rule
+cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float* Uw_t, float* Ut, float* sigma,
+                            float* Vt, double* sig_raw, int32_t* status, cudaStream_t s, int* launches);
+// apply prep: rs[i][j] = scale / sigma[i][j]; flags singular sigma
+cudaError_t launch_inv_sigma(int nb, int k, const float* sigma, float scale, float* rs, int32_t* status,
+                             cudaStream_t s, int* launches);

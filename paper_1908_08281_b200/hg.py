@@ -1,0 +1,236 @@
+"""Thin ctypes binding of libhgrsvd (include/hg.h) -- argument marshalling only.
+
+Every step of the path runs in the library's CUDA kernels; PyTorch is used
+only to own device memory and to name the current stream.  There is no CPU
+path: importing this module raises if libhgrsvd.so is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhgrsvd.so")
+
+HG_OK, HG_ERR_INVALID, HG_ERR_NUMERICAL, HG_ERR_CUDA = 0, 2, 3, 4
+HG_RAW_THETA, HG_SYNC, HG_GEMM_SIMT = 1 << 0, 1 << 1, 1 << 8
+ST_FLAGS = {1: "isolated vertex", 2: "empty hyperedge", 4: "Cholesky breakdown", 8: "Jacobi sweep cap",
+            16: "singular sigma", 32: "non-finite value"}
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1908_08281_b200.build` "
+                      "(there is no fallback path)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_P, _i32, _i64, _u32, _u64, _f32, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
+                                          ctypes.c_uint64, ctypes.c_float, ctypes.c_size_t)
+
+
+class _Incidence(ctypes.Structure):
+    _fields_ = [("n_vertices", _i32), ("n_edges", _i32), ("nnz", _i64), ("row_ptr", _P), ("col_idx", _P)]
+
+
+def _sig(name, restype, *argtypes):
+    f = getattr(_lib, name)
+    f.restype = restype
+    f.argtypes = list(argtypes)
+    return f
+
+
+_workspace_size = _sig("hg_workspace_size", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, _i32,
+                       ctypes.POINTER(_sz))
+_build_theta = _sig("hg_build_theta", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _u32, _P, _P, _P,
+                    _P, _sz, _P)
+_fill_gaussian = _sig("hg_fill_gaussian", ctypes.c_int, _u64, _i32, _i32, _P, _P)
+_block_rsvd = _sig("hg_block_rsvd", ctypes.c_int, _P, _i32, _i32, _i32, _i32, _u64, _u32, _P, _P, _P, _P, _P, _sz,
+                   _P)
+_block_apply = _sig("hg_block_apply_inverse", ctypes.c_int, _P, _P, _P, _i32, _i32, _i32, _P, _i32, _f32, _P, _P, _P,
+                    _sz, _P)
+_solve = _sig("hg_solve", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _i32, _i32, _u64, _P, _i32, _P,
+              _P, _u32, _P, _P, _sz, _P)
+_solve_host = _sig("hg_solve_host", ctypes.c_int, _i32, _i32, _i64, _P, _P, _P, _f32, _i32, _i32, _i32, _u64, _P,
+                   _i32, _P, _P, _u32, _P, _sz, _P)
+_gemm = _sig("hg_gemm", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i32, _i64, _i64, _P, _i32, _i64, _i64, _P, _i32,
+             _i64, _i64, _f32, _P, _i64, _P, _i64, _u32, _P)
+_last_error = _sig("hg_last_error", ctypes.c_char_p)
+_last_launches = _sig("hg_last_launch_count", ctypes.c_int32)
+
+EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_rsvd", "hg_block_apply_inverse",
+           "hg_solve", "hg_solve_host", "hg_gemm", "hg_last_error", "hg_last_launch_count")
+
+
+class HGError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"hg status {status}: {msg}")
+        self.status = status
+
+
+def _check(st: int):
+    if st != HG_OK:
+        raise HGError(st, _last_error().decode())
+
+
+def last_launch_count() -> int:
+    return int(_last_launches())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev(t: torch.Tensor, dtype) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise ValueError(f"expected a contiguous {dtype} tensor, got {t.dtype}")
+    return t
+
+
+def workspace_size(N: int, E: int, nnz: int, b: int, k: int, T: int) -> int:
+    out = _sz(0)
+    _check(_workspace_size(N, E, nnz, b, k, T, ctypes.byref(out)))
+    return int(out.value)
+
+
+class Workspace:
+    """Device scratch for the library (256-byte aligned torch allocation)."""
+
+    def __init__(self, nbytes: int, device=None):
+        self.buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=device or "cuda")
+        off = (-self.buf.data_ptr()) % 256
+        self.ptr = ctypes.c_void_p(self.buf.data_ptr() + off)
+        self.nbytes = nbytes
+
+    @classmethod
+    def for_sizes(cls, N, E, nnz, b, k, T, device=None):
+        return cls(workspace_size(N, E, nnz, b, k, T), device)
+
+
+@dataclass
+class Incidence:
+    row_ptr: torch.Tensor   # int64 [N+1] cuda
+    col_idx: torch.Tensor   # int32 [nnz] cuda
+    n_edges: int
+
+    @property
+    def N(self):
+        return self.row_ptr.numel() - 1
+
+    @property
+    def nnz(self):
+        return self.col_idx.numel()
+
+    def c(self) -> _Incidence:
+        _dev(self.row_ptr, torch.int64)
+        _dev(self.col_idx, torch.int32)
+        return _Incidence(self.N, self.n_edges, self.nnz, self.row_ptr.data_ptr(), self.col_idx.data_ptr())
+
+
+def build_theta(H: Incidence, w: torch.Tensor, mu: float, b: int, *, raw: bool = False,
+                ws: Optional[Workspace] = None, status: Optional[torch.Tensor] = None, stream=None):
+    """Diagonal blocks X_ii (or Theta_ii with raw=True) [N/b][b][b] and r = delta(v)^-1/2 [N]."""
+    _dev(w, torch.float32)
+    N = H.N
+    ws = ws or Workspace.for_sizes(N, H.n_edges, H.nnz, b, 4, 0)
+    blocks = torch.empty((N // b, b, b), dtype=torch.float32, device=w.device)
+    dvr = torch.empty(N, dtype=torch.float32, device=w.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=w.device)
+    inc = H.c()
+    _check(_build_theta(ctypes.byref(inc), _ptr(w), mu, b, HG_RAW_THETA if raw else 0, _ptr(blocks), _ptr(dvr),
+                        _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
+    return blocks, dvr, st
+
+
+def fill_gaussian(seed: int, rows: int, cols: int, device="cuda", stream=None) -> torch.Tensor:
+    out = torch.empty((rows, cols), dtype=torch.float32, device=device)
+    _check(_fill_gaussian(seed, rows, cols, _ptr(out), _stream(stream)))
+    return out
+
+
+def block_rsvd(blocks: torch.Tensor, k: int, q: int, seed: int, *, simt: bool = False,
+               ws: Optional[Workspace] = None, status: Optional[torch.Tensor] = None, stream=None):
+    """Alg. 1 on each block: returns Ut [nb][k][b], sigma [nb][k], Vt [nb][k][b], status."""
+    _dev(blocks, torch.float32)
+    nb, b, _ = blocks.shape
+    ws = ws or Workspace.for_sizes(nb * b, 1, 0, b, k, 0)
+    Ut = torch.empty((nb, k, b), dtype=torch.float32, device=blocks.device)
+    Vt = torch.empty_like(Ut)
+    sigma = torch.empty((nb, k), dtype=torch.float32, device=blocks.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=blocks.device)
+    _check(_block_rsvd(_ptr(blocks), nb, b, k, q, seed, HG_GEMM_SIMT if simt else 0, _ptr(Ut), _ptr(sigma), _ptr(Vt),
+                       _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
+    return Ut, sigma, Vt, st
+
+
+def block_apply_inverse(Ut: torch.Tensor, sigma: torch.Tensor, Vt: torch.Tensor, Y: torch.Tensor, scale: float, *,
+                        ws: Optional[Workspace] = None, status: Optional[torch.Tensor] = None, stream=None):
+    """F_i = scale * V_i Sigma_i^-1 U_i^T Y_i; returns F [N][T], status."""
+    for t in (Ut, sigma, Vt, Y):
+        _dev(t, torch.float32)
+    nb, k, b = Ut.shape
+    T = Y.shape[1]
+    ws = ws or Workspace.for_sizes(nb * b, 1, 0, b, k, T)
+    F = torch.empty((nb * b, T), dtype=torch.float32, device=Y.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=Y.device)
+    _check(_block_apply(_ptr(Ut), _ptr(sigma), _ptr(Vt), nb, b, k, _ptr(Y), T, scale, _ptr(F), _ptr(st), ws.ptr,
+                        ws.nbytes, _stream(stream)))
+    return F, st
+
+
+def solve(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, b: int, k: int, q: int, seed: int,
+          sync: bool = True, simt: bool = False, ws: Optional[Workspace] = None,
+          F: Optional[torch.Tensor] = None, sigma: Optional[torch.Tensor] = None,
+          status: Optional[torch.Tensor] = None, stream=None) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """The whole path from CSR H to F [N][T] (and sigma [N/b][k])."""
+    _dev(w, torch.float32)
+    _dev(Y, torch.float32)
+    N, T = H.N, Y.shape[1]
+    ws = ws or Workspace.for_sizes(N, H.n_edges, H.nnz, b, k, T)
+    F = F if F is not None else torch.empty((N, T), dtype=torch.float32, device=Y.device)
+    sigma = sigma if sigma is not None else torch.empty((N // b, k), dtype=torch.float32, device=Y.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=Y.device)
+    flags = (HG_SYNC if sync else 0) | (HG_GEMM_SIMT if simt else 0)
+    inc = H.c()
+    _check(_solve(ctypes.byref(inc), _ptr(w), mu, b, k, q, seed, _ptr(Y), T, _ptr(F), _ptr(sigma), flags, _ptr(st),
+                  ws.ptr, ws.nbytes, _stream(stream)))
+    return F, sigma, st
+
+
+def solve_host(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, seed: int, F=None, sigma=None,
+               ws: Optional[Workspace] = None, stream=None):
+    """End-to-end entry from HOST tensors (pinned for full copy bandwidth): returns F, sigma on the host."""
+    N, T, E, nnz = row_ptr.numel() - 1, Y.shape[1], w.numel(), col_idx.numel()
+    ws = ws or Workspace.for_sizes(N, E, nnz, b, k, T)
+    F = F if F is not None else torch.empty((N, T), dtype=torch.float32, pin_memory=True)
+    sigma = sigma if sigma is not None else torch.empty((N // b, k), dtype=torch.float32, pin_memory=True)
+    for t, dt in ((row_ptr, torch.int64), (col_idx, torch.int32), (w, torch.float32), (Y, torch.float32),
+                  (F, torch.float32), (sigma, torch.float32)):
+        if t.is_cuda or t.dtype != dt or not t.is_contiguous():
+            raise ValueError("solve_host expects contiguous host tensors")
+    _check(_solve_host(N, E, nnz, _ptr(row_ptr), _ptr(col_idx), _ptr(w), mu, b, k, q, seed, _ptr(Y), T, _ptr(F),
+                       _ptr(sigma), 0, ws.ptr, ws.nbytes, _stream(stream)))
+    return F, sigma
+
+
+def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, batch: int = 1, a_mn: bool = False, lda: int,
+         sa: int = 0, b_mn: bool = False, ldb: int, sb: int = 0, D: torch.Tensor, d_trans: bool = False, ldd: int,
+         sd: int = 0, alpha: float = 1.0, rs: Optional[torch.Tensor] = None, srs: int = 0,
+         cs: Optional[torch.Tensor] = None, scs: int = 0, simt: bool = False, stream=None):
+    """Verification export of the batched 3xTF32 GEMM (see hg.h)."""
+    _check(_gemm(M, N, K, batch, _ptr(A), int(a_mn), lda, sa, _ptr(B), int(b_mn), ldb, sb, _ptr(D), int(d_trans), ldd,
+                 sd, alpha, _ptr(rs), srs, _ptr(cs), scs, HG_GEMM_SIMT if simt else 0, _stream(stream)))
+    return D
+
+
+def incidence_to_device(row_ptr, col_idx, n_edges: int, device="cuda") -> Incidence:
+    return Incidence(torch.as_tensor(row_ptr, dtype=torch.int64).to(device).contiguous(),
+                     torch.as_tensor(col_idx, dtype=torch.int32).to(device).contiguous(), int(n_edges))

@@ -1,0 +1,51 @@
+"""Host-side checks of the C-ABI library (no GPU needed): it loads and exports
+every entry point include/hg.h declares, and host-side validation rejects bad
+sizes synchronously with HG_ERR_INVALID before touching the device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "hg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hg_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1908_08281_b200 import build
+    lib_path = build.build()
+    lib = ctypes.CDLL(lib_path)
+    names = declared_symbols()
+    assert len(names) >= 10
+    for n in names:
+        assert hasattr(lib, n), f"{n} declared in include/hg.h but not exported"
+    from paper_1908_08281_b200 import hg
+    assert set(hg.EXPORTS) == set(names)
+
+
+def test_host_validation_is_synchronous_and_invalid():
+    from paper_1908_08281_b200 import hg
+    with pytest.raises(hg.HGError) as e:
+        hg.workspace_size(100, 10, 10, 30, 8, 0)        # N % b != 0
+    assert e.value.status == hg.HG_ERR_INVALID and "N % b" in str(e.value)
+    for args in [(128, 10, 10, 64, 72, 0),                 # k > b
+                 (128, 10, 10, 64, 6, 0),                  # k % 4
+                 (128, 10, 10, 64, 8, 6),                  # T % 4
+                 (1024, 10, 10, 1024, 1024, 0)]:           # k > 512
+        with pytest.raises(hg.HGError) as e:
+            hg.workspace_size(*args)
+        assert e.value.status == hg.HG_ERR_INVALID
+    assert hg.workspace_size(512, 548, 4937, 128, 32, 20) > 0
+
+
+def test_workspace_grows_with_sizes():
+    from paper_1908_08281_b200 import hg
+    a = hg.workspace_size(4096, 4396, 62223, 256, 64, 100)
+    b = hg.workspace_size(4096, 4396, 62223, 256, 128, 100)
+    c = hg.workspace_size(8192, 4396, 62223, 256, 64, 100)
+    assert b > a and c > a

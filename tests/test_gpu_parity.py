@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C ABI) against the FP64 oracle.
+
+Tolerances (BASELINE.json north_star): relative Frobenius error of the applied
+inverse F <= 2e-5, singular values relative <= 1e-5.  Theta blocks: <= 1e-6 of
+max|Theta| (fp32 sums of a few dozen terms).  Reconstructions U Sigma V^T are
+compared (span-determined), never the sign-ambiguous vectors themselves.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth.hypergraph import CONFIGS, cfg5_points, make_input, make_tiny
+
+pytestmark = pytest.mark.gpu
+
+F_TOL, SIG_TOL, THETA_TOL, ORTH_TOL = 2e-5, 1e-5, 1e-6, 1e-5
+
+_cache = {}
+
+
+def hgm():
+    from paper_1908_08281_b200 import hg
+    return hg
+
+
+def dev_inputs(h):
+    hg = hgm()
+    key = id(h)
+    if key not in _cache:
+        _cache[key] = (hg.incidence_to_device(h.row_ptr, h.col_idx, h.E), torch.from_numpy(h.w).cuda(),
+                       torch.from_numpy(h.Y).cuda())
+    return _cache[key]
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def inputs():
+    cache = {}
+
+    def get(i):
+        if i not in cache:
+            cache[i] = make_input(CONFIGS[i])
+        return cache[i]
+    return get
+
+
+# ------------------------------------------------------------------ Omega
+@pytest.mark.parametrize("rows,cols,seed", [(1000, 33, 0), (4096, 64, 0), (7, 5, 123)])
+def test_gaussian_matches_oracle(rows, cols, seed):
+    g = hgm().fill_gaussian(seed, rows, cols).cpu().numpy()
+    o = oracle.gaussian_f32(seed, rows * cols).reshape(rows, cols)
+    d = np.abs(g.view(np.int32).astype(np.int64) - o.view(np.int32).astype(np.int64))
+    assert d.max() <= 1 and np.mean(d == 0) >= 0.9999
+
+
+# ------------------------------------------------------------------ GEMM
+SHAPES = [(128, 64, 128, 2), (256, 256, 1024, 3), (100, 20, 72, 2), (32, 32, 256, 4), (300, 1000, 256, 2),
+          (1024, 256, 1024, 1), (40, 500, 36, 3)]
+
+
+@pytest.mark.parametrize("simt", [False, True])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gemm_all_layouts_vs_fp64(shape, simt):
+    hg = hgm()
+    M, N, K, batch = shape
+    gen = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    for a_mn in (False, True):
+        for b_mn in (False, True):
+            for d_trans in (False, True):
+                A = torch.randn(batch, *((K, M) if a_mn else (M, K)), device="cuda", generator=gen)
+                B = torch.randn(batch, *((K, N) if b_mn else (N, K)), device="cuda", generator=gen)
+                D = torch.full((batch, N, M) if d_trans else (batch, M, N), float("nan"), device="cuda")
+                rs = torch.rand(batch, M, device="cuda", generator=gen) + 0.5
+                cs = torch.rand(batch, N, device="cuda", generator=gen) + 0.5
+                hg.gemm(A, B, M=M, N=N, K=K, batch=batch, a_mn=a_mn, lda=A.shape[2], sa=A[0].numel(), b_mn=b_mn,
+                        ldb=B.shape[2], sb=B[0].numel(), D=D, d_trans=d_trans, ldd=D.shape[2], sd=D[0].numel(),
+                        alpha=0.75, rs=rs, srs=M, cs=cs, scs=N, simt=simt)
+                Am = A.double().transpose(1, 2) if a_mn else A.double()
+                Bm = B.double() if b_mn else B.double().transpose(1, 2)
+                ref = 0.75 * rs.double()[:, :, None] * (Am @ Bm) * cs.double()[:, None, :]
+                got = D.double().transpose(1, 2) if d_trans else D.double()
+                assert torch.isfinite(got).all()
+                err = float((got - ref).norm() / ref.norm())
+                # 3xTF32 keeps fp32-level accuracy (1xTF32 would give ~1e-3)
+                assert err < 2e-6, (a_mn, b_mn, d_trans, err)
+
+
+# ------------------------------------------------------------------ Theta (Eq. 1)
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_theta_blocks_parity(inputs, cfg):
+    hg = hgm()
+    h = inputs(cfg)
+    c = CONFIGS[cfg]
+    H, w, _ = dev_inputs(h)
+    th, dvr, st = hg.build_theta(H, w, c.mu, c.b, raw=True)
+    X, _, st2 = hg.build_theta(H, w, c.mu, c.b)
+    assert int(st.item()) == 0 and int(st2.item()) == 0
+    assert bool((th == th.transpose(1, 2)).all()), "blocks must be bitwise symmetric (reading A12)"
+    assert bool((X == X.transpose(1, 2)).all())
+    sel = range(c.nb) if c.nb <= 16 else [0, 1, c.nb // 2, c.nb - 1]
+    dv, _ = oracle.degrees(h.row_ptr, h.col_idx, h.w)
+    np.testing.assert_allclose(dvr.double().cpu().numpy(), dv ** -0.5, rtol=2e-7)
+    for blk in sel:
+        ref = oracle.theta_block(h.row_ptr, h.col_idx, h.w, c.b, blk)
+        got = th[blk].double().cpu().numpy()
+        assert np.abs(got - ref).max() <= THETA_TOL * np.abs(ref).max()
+        refx = oracle.theta_block(h.row_ptr, h.col_idx, h.w, c.b, blk, mu=c.mu)
+        assert np.abs(X[blk].double().cpu().numpy() - refx).max() <= THETA_TOL
+
+
+def test_theta_error_flags():
+    hg = hgm()
+    # vertex 3 isolated; hyperedge 2 empty
+    rp = np.array([0, 2, 3, 4, 4], np.int64)
+    ci = np.array([0, 1, 0, 1], np.int32)
+    H = hg.incidence_to_device(rp, ci, 3)
+    w = torch.ones(3, device="cuda")
+    _, _, st = hg.build_theta(H, w, 1.0, 4)
+    s = int(st.item())
+    assert s & 1 and s & 2
+    with pytest.raises(hg.HGError) as e:
+        hg.solve(H, w, torch.zeros(4, 4, device="cuda"), mu=1.0, b=4, k=4, q=1, seed=0)
+    assert e.value.status == hg.HG_ERR_NUMERICAL
+
+
+# ------------------------------------------------------------------ whole path
+def check_against_oracle(h, c, F, sigma, blocks, Ut=None, Vt=None, X=None, k=None, q=None):
+    k = k or c.k
+    q = c.q if q is None else q
+    r = oracle.solve(h.row_ptr, h.col_idx, h.w, h.Y, mu=c.mu, b=c.b, k=k, q=q, seed=c.seed, blocks=blocks,
+                     want_UV=Ut is not None)
+    Fg = F.double().cpu().numpy()
+    sg = sigma.double().cpu().numpy()
+    worst = {"F": 0.0, "sigma": 0.0, "recon": 0.0, "orth": 0.0}
+    for s_, blk in enumerate(blocks):
+        fo = r.F[s_ * c.b:(s_ + 1) * c.b]
+        worst["F"] = max(worst["F"], rel(Fg[blk * c.b:(blk + 1) * c.b], fo))
+        worst["sigma"] = max(worst["sigma"], float(np.max(np.abs(sg[blk] - r.sigma[s_]) / r.sigma[s_])))
+        assert np.all(np.diff(sg[blk]) <= 0)
+        if Ut is not None:
+            U = Ut[blk].double().cpu().numpy().T
+            V = Vt[blk].double().cpu().numpy().T
+            rec = U @ np.diag(sg[blk]) @ V.T
+            rec_o = r.U[s_] @ np.diag(r.sigma[s_]) @ r.V[s_].T
+            worst["recon"] = max(worst["recon"], rel(rec, rec_o))
+            worst["orth"] = max(worst["orth"], np.abs(U.T @ U - np.eye(k)).max(), np.abs(V.T @ V - np.eye(k)).max())
+            idx = np.abs(U).argmax(0)
+            assert np.all(U[idx, np.arange(k)] > 0), "sign rule (SPEC.md:86)"
+    assert worst["F"] <= F_TOL, worst
+    assert worst["sigma"] <= SIG_TOL, worst
+    assert worst["recon"] <= F_TOL, worst
+    assert worst["orth"] <= ORTH_TOL, worst
+    return worst
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_solve_parity_configs_1_to_3(inputs, cfg):
+    hg = hgm()
+    h = inputs(cfg)
+    c = CONFIGS[cfg]
+    H, w, Y = dev_inputs(h)
+    X, _, _ = hg.build_theta(H, w, c.mu, c.b)
+    Ut, sigma, Vt, st = hg.block_rsvd(X, c.k, c.q, c.seed)
+    F, st2 = hg.block_apply_inverse(Ut, sigma, Vt, Y, c.mu / (1 + c.mu))
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0 and int(st2.item()) == 0
+    check_against_oracle(h, c, F, sigma, list(range(c.nb)), Ut, Vt)
+    # the composite entry point gives the same bits
+    F2, sigma2, st3 = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    assert int(st3.item()) == 0
+    assert torch.equal(F, F2) and torch.equal(sigma, sigma2)
+
+
+def test_solve_parity_config4_sampled_blocks(inputs):
+    """configs[3] (the bench workload) at full size; oracle on blocks {0, nb/2, nb-1}."""
+    hg = hgm()
+    h = inputs(4)
+    c = CONFIGS[4]
+    H, w, Y = dev_inputs(h)
+    X, _, _ = hg.build_theta(H, w, c.mu, c.b)
+    Ut, sigma, Vt, st = hg.block_rsvd(X, c.k, c.q, c.seed)
+    F, st2 = hg.block_apply_inverse(Ut, sigma, Vt, Y, c.mu / (1 + c.mu))
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0 and int(st2.item()) == 0
+    check_against_oracle(h, c, F, sigma, [0, c.nb // 2, c.nb - 1], Ut, Vt)
+
+
+CFG5_SUBSET = [(512, 64, 1), (512, 256, 4), (1024, 128, 2), (1024, 512, 1), (2048, 256, 1)]
+
+
+@pytest.mark.parametrize("b,k,q", CFG5_SUBSET)
+def test_solve_parity_config5_points(inputs, b, k, q):
+    hg = hgm()
+    h = inputs(5)
+    c = CONFIGS[5].with_(b=b, k=k, q=q)
+    assert (b, k, q) in cfg5_points()
+    H, w, Y = dev_inputs(h)
+    F, sigma, st = hg.solve(H, w, Y, mu=c.mu, b=b, k=k, q=q, seed=c.seed)
+    check_against_oracle(h, c, F, sigma, [0, c.nb - 1])
+
+
+def test_tiny_inputs_and_k_equals_b():
+    """Small ragged-tile shapes; with k = b the path is the exact block inverse (LU)."""
+    hg = hgm()
+    for (N, b, k, q) in [(32, 8, 4, 0), (32, 8, 8, 2), (48, 16, 12, 1), (40, 20, 20, 1)]:
+        h = make_tiny(N, b, k, q)
+        c = h.cfg
+        H, w, Y = dev_inputs(h)
+        F, sigma, st = hg.solve(H, w, Y, mu=1.0, b=b, k=k, q=q, seed=0)
+        check_against_oracle(h, c, F, sigma, list(range(N // b)))
+        if k == b:
+            for blk in range(N // b):
+                Xo = oracle.theta_block(h.row_ptr, h.col_idx, h.w, b, blk, mu=1.0)
+                lu = 0.5 * np.linalg.solve(Xo, h.Y[blk * b:(blk + 1) * b].astype(float))
+                assert rel(F[blk * b:(blk + 1) * b].double().cpu().numpy(), lu) <= F_TOL
+
+
+def test_deterministic_and_host_entry(inputs):
+    hg = hgm()
+    h = inputs(2)
+    c = CONFIGS[2]
+    H, w, Y = dev_inputs(h)
+    F1, s1, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)
+    F2, s2, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)
+    assert torch.equal(F1, F2) and torch.equal(s1, s2)
+    Fh, sh = hg.solve_host(torch.from_numpy(h.row_ptr), torch.from_numpy(h.col_idx), torch.from_numpy(h.w),
+                           torch.from_numpy(h.Y).pin_memory(), mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)
+    assert torch.equal(Fh, F1.cpu()) and torch.equal(sh, s1.cpu())
+    F3, _, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=1)
+    assert not torch.equal(F1, F3)
+
+
+def test_simt_verification_path_agrees(inputs):
+    hg = hgm()
+    h = inputs(1)
+    c = CONFIGS[1]
+    H, w, Y = dev_inputs(h)
+    Ft, st_, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)
+    Fs, ss, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0, simt=True)
+    assert rel(Ft.double().cpu().numpy(), Fs.double().cpu().numpy()) < 1e-5
+    check_against_oracle(h, c, Fs, ss, list(range(c.nb)))
+
+
+def test_device_call_validation():
+    hg = hgm()
+    h = make_tiny(32, 8, 4, 1)
+    H, w, Y = dev_inputs(h)
+    ws = hg.Workspace(1024)
+    with pytest.raises(hg.HGError) as e:
+        hg.solve(H, w, Y, mu=1.0, b=8, k=4, q=1, seed=0, ws=ws)
+    assert e.value.status == hg.HG_ERR_INVALID and "workspace too small" in str(e.value)
+    with pytest.raises(hg.HGError) as e:
+        hg.solve(H, w, Y, mu=-1.0, b=8, k=4, q=1, seed=0)
+    assert e.value.status == hg.HG_ERR_INVALID
+    with pytest.raises(hg.HGError) as e:
+        hg.solve(H, w, Y, mu=1.0, b=8, k=12, q=1, seed=0)
+    assert e.value.status == hg.HG_ERR_INVALID
