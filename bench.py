@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark of the block randomized SVD hot path (arXiv:1908.08281) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+A step is one pass of the whole hot path -- hg_solve: degrees, diagonal-block
+assembly, Alg. 1 on every block (Omega, 2q+2 block GEMMs, 2q+1 CholeskyQR2,
+B = S^T X, one-sided Jacobi SVD, U/V), and the Eq. 15 apply to the N x T
+tag-label RHS -- on configs[3] of BASELINE.json (N=65536, b=1024, k=256, q=3,
+T=1000) with inputs resident in HBM.  value = diagonal blocks per second over
+all ranks; the per-block inputs (256 MiB of X blocks, 250 MiB of Y) exceed the
+126 MB L2 every step, so no L2 flush is needed.
+
+One JSON line on rank 0.  Ranks (torchrun) run
+independent problems (Omega seed = rank): weak scaling, no collective on the
+data path; the step time is the max over ranks.
+
+--impl reference times the FP64 CPU oracle (oracle/, the stand-in reference:
+there is no reference implementation, only the paper) on a bounded sample of
+the same workload on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+TF32_OVER_BF16 = 1.1 / 2.25   # nominal dense tf32 / bf16 ratio (B200_PROFILING.md)
+
+
+# ---------------------------------------------------------------- distributed plumbing
+def dist_setup(backend: str):
+    """(rank, world, local_rank); initialises torch.distributed when WORLD_SIZE > 1."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return rank, world, local
+
+
+def barrier():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while the timed region runs."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - no NVML
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- helpers
+def load_peaks():
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def workload_config(args):
+    from synth.hypergraph import CONFIGS
+    c = CONFIGS[args.config]
+    kw = {}
+    if args.b:
+        kw["b"] = args.b
+    if args.k:
+        kw["k"] = args.k
+    if args.q is not None:
+        kw["q"] = args.q
+    return c.with_(**kw) if kw else c
+
+
+def config_json(c, note=None):
+    d = {"workload": f"configs[{ {'cfg1': 0, 'cfg2': 1, 'cfg3': 2, 'cfg4': 3, 'cfg5': 4}[c.name] }] {c.name}: "
+                     f"N={c.N}, b={c.b}, nb={c.nb}, k={c.k}, q={c.q}, T={c.T}, mu={c.mu}",
+         "N": c.N, "b": c.b, "nb": c.nb, "k": c.k, "q": c.q, "T": c.T, "mu": c.mu,
+         "l2": "inputs larger than L2 (X blocks 4*N*b bytes, Y 4*N*T bytes per step); no flush",
+         "data": "synthetic seeded image-tagging hypergraph (synth/hypergraph.py), stands in for the paper's "
+                 "private Flickr dataset"}
+    if note:
+        d["note"] = note
+    return d
+
+
+def oracle_sample(h, c, n_blocks, seed=0):
+    import oracle
+    nb = c.nb
+    blocks = [int(round(i * (nb - 1) / max(1, n_blocks - 1))) for i in range(n_blocks)] if n_blocks > 1 else [0]
+    r = oracle.solve(h.row_ptr, h.col_idx, h.w, h.Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, blocks=blocks)
+    return r
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    rank, world, local = dist_setup("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1908_08281_b200 import hg
+    from synth.hypergraph import make_input
+
+    c = workload_config(args)
+    h = make_input(c)
+    seed = rank                                     # independent problem per rank
+    H = hg.incidence_to_device(h.row_ptr, h.col_idx, h.E, device=dev)
+    w = torch.from_numpy(h.w).to(dev)
+    Y = torch.from_numpy(h.Y).to(dev)
+    ws = hg.Workspace.for_sizes(c.N, h.E, h.nnz, c.b, c.k, c.T, device=dev)
+    F = torch.empty((c.N, c.T), dtype=torch.float32, device=dev)
+    sigma = torch.empty((c.nb, c.k), dtype=torch.float32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, sync=False, ws=ws, F=F, sigma=sigma,
+                 status=status, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    launches_per_step = hg.last_launch_count()
+    torch.cuda.synchronize(dev)
+    if int(status.item()) != 0:
+        raise RuntimeError(f"device status {int(status.item())} during warm-up")
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms_local, dev)
+    value = world * c.nb / (ms / 1e3)
+
+    # per-stage attribution: the same steps with per-stage CUDA events on the stream
+    hg.profile_enable(True)
+    torch.cuda.synchronize(dev)
+    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pe0.record(stream)
+    for _ in range(args.steps):
+        step()
+    pe1.record(stream)
+    prof = hg.profile_collect()
+    hg.profile_enable(False)
+    torch.cuda.synchronize(dev)
+    prof_ms_per_step = pe0.elapsed_time(pe1) / args.steps
+    stages = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                  "share": v[0] / args.steps / prof_ms_per_step} for k, v in prof.items()}
+
+    peaks, peak_src = load_peaks()
+    tf32_sust = peaks["bf16_tflops_sustained"] * TF32_OVER_BF16
+    tf32_burst = peaks["bf16_tflops"] * TF32_OVER_BF16
+    # algorithmic work per launch
+    nb, b, k, q, T = c.nb, c.b, c.k, c.q, c.T
+    work = {
+        "gemm_power": ("tensor", 2.0 * b * b * k * nb, 2 * q + 2),
+        "gemm_gram": ("tensor", 2.0 * b * k * k * nb, 4 * q + 3),
+        "gemm_qform": ("tensor", 2.0 * b * k * k * nb, 4 * q + 2),
+        "gemm_apply": ("tensor", 2.0 * b * k * T * nb, 2),
+        "assemble": ("hbm", 4.0 * b * b * nb, 1),
+    }
+
+    def roof(stage):
+        if stage not in work or stage not in prof:
+            return None
+        bound, per_launch, _ = work[stage]
+        total_ms, n = prof[stage]
+        avg_s = total_ms / n / 1e3
+        if bound == "tensor":
+            useful = per_launch / avg_s / 1e12
+            achieved = 3.0 * useful          # 3xTF32: three tf32 products per fp32 product
+            return {"kernel": stage, "bound": "tensor", "achieved": achieved, "peak": tf32_sust, "unit": "TFLOP/s",
+                    "frac": achieved / tf32_sust, "useful_fp32_tflops": useful,
+                    "peak_note": f"tf32 dense = bf16_tflops_sustained ({peak_src}) x 1.1/2.25; "
+                                 f"burst-derived tf32 {tf32_burst:.0f}",
+                    "avg_launch_ms": avg_s * 1e3, "launches_per_step": n / args.steps, "traffic": None}
+        gbs = per_launch / avg_s / 1e9
+        return {"kernel": stage, "bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": gbs / peaks["hbm_gbs"], "avg_launch_ms": avg_s * 1e3, "traffic": None}
+
+    dominant = max(stages, key=lambda s: stages[s]["ms_per_step"]) if stages else None
+    traffic_file = os.path.join(HERE, "profiles", "traffic.json")
+    traffic = json.load(open(traffic_file)) if os.path.exists(traffic_file) else {}
+    gemm_roof = roof("gemm_power")
+    if gemm_roof and "gemm_power" in traffic:
+        gemm_roof["traffic"] = traffic["gemm_power"]
+    dom_roof = roof(dominant) if dominant in work else None
+    if dom_roof is None and dominant is not None:
+        dom_roof = {"kernel": dominant, "bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None,
+                    "note": "latency/ALU-bound SIMT stage; see DESIGN.md"}
+    if dom_roof and dominant in traffic:
+        dom_roof["traffic"] = traffic[dominant]
+    gemm_useful_tflops = None
+    if "gemm_power" in prof:
+        gemm_useful_tflops = (2 * q + 2) * 2.0 * b * b * k * nb / (prof["gemm_power"][0] / args.steps / 1e3) / 1e12
+
+    # end to end through the host entry point (pinned buffers, copies inside the timed region)
+    rp = torch.from_numpy(h.row_ptr).pin_memory()
+    ci = torch.from_numpy(h.col_idx).pin_memory()
+    wh = torch.from_numpy(h.w).pin_memory()
+    Yh = torch.from_numpy(h.Y).pin_memory()
+    Fh = torch.empty((c.N, c.T), dtype=torch.float32).pin_memory()
+    sh = torch.empty((c.nb, c.k), dtype=torch.float32).pin_memory()
+    for _ in range(max(1, min(args.warmup, 2))):
+        hg.solve_host(rp, ci, wh, Yh, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, F=Fh, sigma=sh, ws=ws, stream=stream)
+    barrier()
+    n_e2e = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ee0.record(stream)
+    for _ in range(n_e2e):
+        hg.solve_host(rp, ci, wh, Yh, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, F=Fh, sigma=sh, ws=ws, stream=stream)
+    ee1.record(stream)
+    torch.cuda.synchronize(dev)
+    wall_e2e = (time.perf_counter() - t0) / n_e2e
+    e2e_ms = max_over_ranks(max(ee0.elapsed_time(ee1) / n_e2e, wall_e2e * 1e3), dev)
+    h2d = (c.N + 1) * 8 + h.nnz * 4 + h.E * 4 + c.N * c.T * 4
+    d2h = c.N * c.T * 4 + c.nb * c.k * 4
+
+    # parity of the timed output on sampled blocks (rank 0; oracle = FP64 CPU)
+    parity = None
+    cpu_base = None
+    if rank == 0:
+        sel = [0, c.nb - 1]
+        t_or = time.perf_counter()
+        r = oracle_sample(h, c, 2, seed=seed) if c.nb > 1 else oracle_sample(h, c, 1, seed=seed)
+        Fg = Fh.double().numpy()
+        sg = sh.double().numpy()
+        ferr = max(float(np.linalg.norm(Fg[blk * c.b:(blk + 1) * c.b] - r.F[s_ * c.b:(s_ + 1) * c.b]) /
+                         np.linalg.norm(r.F[s_ * c.b:(s_ + 1) * c.b])) for s_, blk in enumerate(r.blocks))
+        serr = max(float(np.max(np.abs(sg[blk] - r.sigma[s_]) / r.sigma[s_])) for s_, blk in enumerate(r.blocks))
+        parity = {"blocks": r.blocks, "F_rel_fro": ferr, "sigma_rel_max": serr, "tol": {"F": 2e-5, "sigma": 1e-5},
+                  "ok": ferr <= 2e-5 and serr <= 1e-5}
+        del t_or, sel
+        if world == 1 and not args.no_cpu_baseline:
+            nthreads = cores()
+            n_s = max(1, min(c.nb, nthreads))
+            rr = oracle_sample(h, c, n_s, seed=seed)
+            cpu_base = {"value": n_s / rr.seconds, "unit": "blocks/s", "cores": rr.threads, "kind": "oracle",
+                        "sample": f"{n_s} of {c.nb} diagonal blocks of the same workload (Alg. 1 + apply, FP64, "
+                                  f"OpenMP over blocks), {rr.seconds:.1f} s"}
+
+    out = {
+        "metric": "diag_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config_json(c),
+        "solve_ms": ms, "blocks_per_s_per_gpu": c.nb / (ms / 1e3),
+        "gemm_useful_tflops": gemm_useful_tflops,
+        "gemm_tf32_pipe_frac": gemm_roof["frac"] if gemm_roof else None,
+        "roofline": dom_roof, "gemm_roofline": gemm_roof,
+        "stages": stages, "profiled_ms_per_step": prof_ms_per_step,
+        "e2e": {"value": world * c.nb / (e2e_ms / 1e3), "unit": "blocks/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "entry": "hg_solve_host"},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+        "parity": parity,
+        "cpu_baseline": cpu_base,
+        "peaks": {"source": peak_src, "tf32_tflops_sustained": tf32_sust, "tf32_tflops_burst": tf32_burst,
+                  "hbm_gbs": peaks["hbm_gbs"]},
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    import torch.distributed as dist
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- reference arm (the oracle)
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from synth.hypergraph import make_input
+    c = workload_config(args)
+    h = make_input(c)
+    nthreads = cores()
+    n_s = max(1, min(c.nb, nthreads))
+    for _ in range(args.warmup):
+        oracle_sample(h, c, n_s)
+    times = []
+    for _ in range(args.steps):
+        r = oracle_sample(h, c, n_s)
+        times.append(r.seconds)
+    t = sum(times) / len(times)
+    v = n_s / t
+    out = {"impl": "reference", "metric": "diag_blocks_per_s", "value": v, "unit": "blocks/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config_json(c, note="reference arm = FP64 CPU oracle (no reference implementation exists)"),
+           "cpu_baseline": {"value": v, "unit": "blocks/s", "cores": r.threads, "kind": "oracle",
+                            "sample": f"{n_s} of {c.nb} diagonal blocks per step (Alg. 1 + apply, FP64, OpenMP)"},
+           "e2e": {"value": v, "unit": "blocks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--b", type=int, default=None)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--q", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

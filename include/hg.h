@@ -108,7 +108,7 @@ hg_status hg_fill_gaussian(uint64_t seed, int32_t rows, int32_t cols, float* out
  * X_ii^T = X_ii is assumed (hg_build_theta writes bitwise-symmetric blocks;
  * reading A12).  QR is CholeskyQR2; the SVD is one-sided Jacobi.
  *   blocks [nb][b][b]   input blocks (symmetric)
- *   1 <= k <= b, k % 8 == 0 is NOT required; b % 4 == 0 required (TMA strides)
+ *   1 <= k <= min(b, 512); b % 4 == 0 and k % 4 == 0 (16-byte TMA row strides)
  *   Ut, Vt [nb][k][b]   out, U_i^T and V_i^T;  sigma [nb][k] out, non-increasing
  * Device errors: HG_ST_CHOL_BREAKDOWN, HG_ST_JACOBI_CAP, HG_ST_NONFINITE. */
 hg_status hg_block_rsvd(const float* blocks, int32_t nb, int32_t b, int32_t k, int32_t q, uint64_t seed,
@@ -152,6 +152,23 @@ hg_status hg_gemm(int32_t M, int32_t N, int32_t K, int32_t batch, const float* A
                   int64_t sa, const float* B, int32_t b_mn, int64_t ldb, int64_t sb, float* D, int32_t d_trans,
                   int64_t ldd, int64_t sd, float alpha, const float* rs, int64_t srs, const float* cs,
                   int64_t scs, uint32_t flags, hg_stream_t stream);
+
+/* Stage profiler (tracing).  hg_profile_enable(1) makes the calls on this host
+ * thread bracket each stage launch with CUDA events on its stream (off by
+ * default).  hg_profile_collect synchronises those events, writes per-stage
+ * totals -- names[i] (32-byte NUL-terminated slots), ms[i] summed elapsed time,
+ * counts[i] launches -- for up to max_stages stages, sets *n_out to the number
+ * of stages seen, and clears the record.  Stages: degrees, assemble, omega,
+ * gemm_power, gemm_gram, gemm_qform, gemm_svd, gemm_apply, cholinv, jacobi,
+ * finalize, inv_sigma.  Host pointers. */
+hg_status hg_profile_enable(int32_t on);
+hg_status hg_profile_collect(int32_t max_stages, char* names, double* ms, int32_t* counts, int32_t* n_out);
+
+/* Diagnostics (device-wide counters since the last reset; synchronous):
+ * out[0] near-identity CholeskyQR factorizations, out[1] full ones,
+ * out[2] max Jacobi sweeps of any block, out[3] total sweeps, out[4] blocks;
+ * with n >= 69, out[5..68] are clock64 phase stamps of the last full Cholesky. */
+hg_status hg_debug_counters(int64_t* out, int32_t n, int32_t reset);
 
 /* Number of kernels the last hg_* call on this host thread enqueued. */
 int32_t hg_last_launch_count(void);

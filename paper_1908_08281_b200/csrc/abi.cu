@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/hg.h"
 #include "gemm.cuh"
@@ -25,6 +26,52 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
+
+// ---------------------------------------------------------------- stage profiler
+// When enabled (hg_profile_enable), every launch group is bracketed by a pair of
+// CUDA events on the launching stream; hg_profile_collect sums the elapsed times
+// per stage.  Off by default: no events are recorded on the hot path.
+enum Stage { ST_DEGREES, ST_ASSEMBLE, ST_OMEGA, ST_GEMM_POWER, ST_GEMM_GRAM, ST_GEMM_QFORM, ST_GEMM_SVD,
+             ST_GEMM_APPLY, ST_CHOLINV, ST_JACOBI, ST_FINALIZE, ST_INV_SIGMA, ST_COUNT };
+const char* const kStageNames[ST_COUNT] = {"degrees", "assemble", "omega", "gemm_power", "gemm_gram",
+                                           "gemm_qform", "gemm_svd", "gemm_apply", "cholinv", "jacobi",
+                                           "finalize", "inv_sigma"};
+struct ProfRec {
+  int stage;
+  cudaEvent_t a, b;
+};
+thread_local bool g_prof_on = false;
+thread_local std::vector<ProfRec> g_prof;
+thread_local std::vector<cudaEvent_t> g_evpool;
+thread_local int g_cur_stage = -1;
+
+cudaEvent_t prof_event() {
+  if (!g_evpool.empty()) {
+    cudaEvent_t e = g_evpool.back();
+    g_evpool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct ProfScope {
+  bool on;
+  cudaStream_t s;
+  ProfRec r;
+  ProfScope(int stage, cudaStream_t st) : on(g_prof_on), s(st) {
+    if (!on) return;
+    r.stage = stage;
+    r.a = prof_event();
+    r.b = prof_event();
+    cudaEventRecord(r.a, s);
+  }
+  ~ProfScope() {
+    if (!on) return;
+    cudaEventRecord(r.b, s);
+    g_prof.push_back(r);
+  }
+};
 
 hg_status fail(hg_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 hg_status fail(hg_status s, const char* fmt, ...) {
@@ -118,8 +165,9 @@ hg_status check_ws(const void* ws, size_t ws_bytes, size_t need) {
   return HG_OK;
 }
 
-hg_status gemm(const GemmDesc& g, cudaStream_t s, bool simt, const char* what) {
+hg_status gemm(const GemmDesc& g, cudaStream_t s, bool simt, const char* what, int stage = ST_GEMM_SVD) {
   if (const char* m = gemm_check(g)) return fail(HG_ERR_INVALID, "%s: %s", what, m);
+  ProfScope ps(stage, s);
   cudaError_t e = launch_gemm(g, s, simt);
   ++g_launches;
   if (e != cudaSuccess) return cuda_fail(e, what);
@@ -140,7 +188,7 @@ struct Rsvd {
     g.A = X; g.a_mn = false; g.lda = b; g.sa = (int64_t)b * b;
     g.B = P_t; g.b_mn = false; g.ldb = b; g.sb = (int64_t)k * b;
     g.D = out_t; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
-    return gemm(g, s, simt, "power product X*S");
+    return gemm(g, s, simt, "power product X*S", ST_GEMM_POWER);
   }
   // G = P^T P (k x k)
   hg_status gram(const float* P_t, float* G) const {
@@ -149,7 +197,7 @@ struct Rsvd {
     g.A = P_t; g.a_mn = false; g.lda = b; g.sa = (int64_t)k * b;
     g.B = P_t; g.b_mn = false; g.ldb = b; g.sb = (int64_t)k * b;
     g.D = G; g.d_trans = false; g.ldd = k; g.sd = (int64_t)k * k;
-    return gemm(g, s, simt, "Gram P^T P");
+    return gemm(g, s, simt, "Gram P^T P", ST_GEMM_GRAM);
   }
   // Q = P L^-T  ->  Q_t
   hg_status qform(const float* P_t, const float* Linv, float* Q_t) const {
@@ -158,7 +206,7 @@ struct Rsvd {
     g.A = P_t; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
     g.B = Linv; g.b_mn = false; g.ldb = k; g.sb = (int64_t)k * k;
     g.D = Q_t; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
-    return gemm(g, s, simt, "Q = Y R^-1");
+    return gemm(g, s, simt, "Q = Y R^-1", ST_GEMM_QFORM);
   }
 };
 
@@ -170,10 +218,16 @@ struct Rsvd {
 
 hg_status cholqr2(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* Linv, float* work, int32_t* st) {
   HG_TRY(R.gram(a_t, G));
-  HG_CU(launch_cholinv(R.nb, R.k, G, nullptr, Linv, work, st, R.s, &g_launches), "cholinv");
+  {
+    ProfScope ps(ST_CHOLINV, R.s);
+    HG_CU(launch_cholinv(R.nb, R.k, G, nullptr, Linv, work, st, R.s, &g_launches), "cholinv");
+  }
   HG_TRY(R.qform(a_t, Linv, scratch_t));
   HG_TRY(R.gram(scratch_t, G));
-  HG_CU(launch_cholinv(R.nb, R.k, G, nullptr, Linv, work, st, R.s, &g_launches), "cholinv");
+  {
+    ProfScope ps(ST_CHOLINV, R.s);
+    HG_CU(launch_cholinv(R.nb, R.k, G, nullptr, Linv, work, st, R.s, &g_launches), "cholinv");
+  }
   HG_TRY(R.qform(scratch_t, Linv, a_t));
   return HG_OK;
 }
@@ -192,7 +246,10 @@ hg_status run_rsvd(const float* X, int nb, int b, int k, int q, uint64_t seed, b
   double* sig = at<double>(ws, Lo.sig);
 
   // Alg. 1 step 1-2: Omega, Y0 = X Omega, S0 = qr(Y0)
-  HG_CU(launch_omega_panels(seed, nb, b, k, P[0], s, &g_launches), "omega");
+  {
+    ProfScope ps(ST_OMEGA, s);
+    HG_CU(launch_omega_panels(seed, nb, b, k, P[0], s, &g_launches), "omega");
+  }
   HG_TRY(R.power(P[0], P[1]));
   HG_TRY(cholqr2(R, P[1], P[0], G, Linv, work, st));
   float *cur = P[1], *oth = P[0];
@@ -207,8 +264,14 @@ hg_status run_rsvd(const float* X, int nb, int b, int k, int q, uint64_t seed, b
   HG_TRY(R.power(cur, Bt));
   // step 5: one-sided Jacobi on W = L^T, B B^T = L L^T
   HG_TRY(R.gram(Bt, G));
-  HG_CU(launch_cholinv(nb, k, G, Lm, Linv, work, st, s, &g_launches), "cholinv(B B^T)");
-  HG_CU(launch_jacobi(nb, k, Lm, Wf, st, s, &g_launches), "jacobi");
+  {
+    ProfScope ps(ST_CHOLINV, s);
+    HG_CU(launch_cholinv(nb, k, G, Lm, Linv, work, st, s, &g_launches), "cholinv(B B^T)");
+  }
+  {
+    ProfScope ps(ST_JACOBI, s);
+    HG_CU(launch_jacobi(nb, k, Lm, Wf, st, s, &g_launches), "jacobi");
+  }
   {  // U~ = L^-T W_f  (stored transposed: Uk[j] = u~_j)
     GemmDesc g;
     g.M = k; g.N = k; g.K = k; g.batch = nb;
@@ -226,7 +289,10 @@ hg_status run_rsvd(const float* X, int nb, int b, int k, int q, uint64_t seed, b
     g.D = P[2 + w]; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
     HG_TRY(gemm(g, s, simt, w == 0 ? "V = B^T U~" : "U = S U~"));
   }
-  HG_CU(launch_finalize(nb, b, k, P[2], P[3], Ut, sigma, Vt, sig, st, s, &g_launches), "finalize");
+  {
+    ProfScope ps(ST_FINALIZE, s);
+    HG_CU(launch_finalize(nb, b, k, P[2], P[3], Ut, sigma, Vt, sig, st, s, &g_launches), "finalize");
+  }
   return HG_OK;
 }
 
@@ -235,7 +301,10 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
   if (T == 0) return HG_OK;
   float* rs = at<float>(ws, Lo.rs);
   float* Z = at<float>(ws, Lo.Z);
-  HG_CU(launch_inv_sigma(nb, k, sigma, scale, rs, st, s, &g_launches), "inv_sigma");
+  {
+    ProfScope ps(ST_INV_SIGMA, s);
+    HG_CU(launch_inv_sigma(nb, k, sigma, scale, rs, st, s, &g_launches), "inv_sigma");
+  }
   {  // Z = diag(scale/sigma) U^T Y_i   (k x T)
     GemmDesc g;
     g.M = k; g.N = T; g.K = b; g.batch = nb;
@@ -243,7 +312,7 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
     g.B = Y; g.b_mn = true; g.ldb = T; g.sb = (int64_t)b * T;
     g.D = Z; g.d_trans = false; g.ldd = T; g.sd = (int64_t)k * T;
     g.rs = rs; g.srs = k;
-    HG_TRY(gemm(g, s, simt, "Z = Sigma^-1 U^T Y"));
+    HG_TRY(gemm(g, s, simt, "Z = Sigma^-1 U^T Y", ST_GEMM_APPLY));
   }
   {  // F_i = V Z   (b x T)
     GemmDesc g;
@@ -251,7 +320,7 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
     g.A = Vt; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
     g.B = Z; g.b_mn = true; g.ldb = T; g.sb = (int64_t)k * T;
     g.D = F; g.d_trans = false; g.ldd = T; g.sd = (int64_t)b * T;
-    HG_TRY(gemm(g, s, simt, "F = V Z"));
+    HG_TRY(gemm(g, s, simt, "F = V Z", ST_GEMM_APPLY));
   }
   return HG_OK;
 }
@@ -259,12 +328,18 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
 hg_status run_theta(const hg_incidence* H, const float* w, float mu, int b, bool raw, float* blocks, float* dvr_out,
                     int32_t* st, void* ws, const Layout& Lo, cudaStream_t s) {
   float* dvr = dvr_out ? dvr_out : at<float>(ws, Lo.dvr);
-  HG_CU(launch_degrees(H->n_vertices, H->n_edges, H->nnz, H->row_ptr, H->col_idx, w, at<int32_t>(ws, Lo.de),
-                       at<float>(ws, Lo.eval), dvr, st, s, &g_launches),
-        "degrees");
-  HG_CU(launch_assemble(H->n_vertices / b, b, H->row_ptr, H->col_idx, at<float>(ws, Lo.eval), dvr, mu, raw, blocks,
-                        s, &g_launches),
-        "assemble");
+  {
+    ProfScope ps(ST_DEGREES, s);
+    HG_CU(launch_degrees(H->n_vertices, H->n_edges, H->nnz, H->row_ptr, H->col_idx, w, at<int32_t>(ws, Lo.de),
+                         at<float>(ws, Lo.eval), dvr, st, s, &g_launches),
+          "degrees");
+  }
+  {
+    ProfScope ps(ST_ASSEMBLE, s);
+    HG_CU(launch_assemble(H->n_vertices / b, b, H->row_ptr, H->col_idx, at<float>(ws, Lo.eval), dvr, mu, raw,
+                          blocks, s, &g_launches),
+          "assemble");
+  }
   return HG_OK;
 }
 
@@ -282,7 +357,70 @@ hg_status check_H(const hg_incidence* H) {
 extern "C" {
 
 const char* hg_last_error(void) { return g_err.c_str(); }
+
+hg_status hg_profile_enable(int32_t on) {
+  g_prof_on = on != 0;
+  return HG_OK;
+}
+
+hg_status hg_profile_collect(int32_t max_stages, char* names, double* ms, int32_t* counts, int32_t* n_out) {
+  g_err.clear();
+  if (!n_out) return fail(HG_ERR_INVALID, "n_out is NULL");
+  double tot[ST_COUNT] = {0};
+  int cnt[ST_COUNT] = {0};
+  for (auto& r : g_prof) {
+    float t = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return cuda_fail(e, "profile sync");
+    e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess) return cuda_fail(e, "profile elapsed");
+    tot[r.stage] += t;
+    cnt[r.stage] += 1;
+    g_evpool.push_back(r.a);
+    g_evpool.push_back(r.b);
+  }
+  g_prof.clear();
+  int n = 0;
+  for (int i = 0; i < ST_COUNT; ++i) {
+    if (!cnt[i]) continue;
+    if (n < max_stages) {
+      if (names) {
+        strncpy(names + 32 * n, kStageNames[i], 31);
+        names[32 * n + 31] = 0;
+      }
+      if (ms) ms[n] = tot[i];
+      if (counts) counts[n] = cnt[i];
+    }
+    ++n;
+  }
+  *n_out = n;
+  return HG_OK;
+}
 int32_t hg_last_launch_count(void) { return g_launches; }
+
+hg_status hg_debug_counters(int64_t* out, int32_t n, int32_t reset) {
+  g_err.clear();
+  if (!out || n < 5) return fail(HG_ERR_INVALID, "need out[5]");
+  if (n >= 5 + 64) {
+    long long clk[64];
+    HG_CU(chol_clocks(clk), "chol_clocks");
+    for (int i = 0; i < 64; ++i) out[5 + i] = clk[i];
+  }
+  if (n >= 69 + 16) {
+    long long clk[16];
+    HG_CU(jacobi_clocks(clk), "jacobi_clocks");
+    for (int i = 0; i < 16; ++i) out[69 + i] = clk[i];
+  }
+  unsigned long long c[2] = {0, 0}, j[3] = {0, 0, 0};
+  HG_CU(chol_debug(c, reset != 0), "chol_debug");
+  HG_CU(jacobi_debug(j, reset != 0), "jacobi_debug");
+  out[0] = (int64_t)c[0];
+  out[1] = (int64_t)c[1];
+  out[2] = (int64_t)j[0];
+  out[3] = (int64_t)j[1];
+  out[4] = (int64_t)j[2];
+  return HG_OK;
+}
 
 hg_status hg_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t b, int32_t k, int32_t T, size_t* bytes) {
   g_err.clear();

@@ -13,35 +13,172 @@
 // written by this first-order formula; otherwise the
 // full factorization runs.  A pivot <= 0 flags HG_ST_CHOL_BREAKDOWN.
 //
-// One CTA (1024 threads) per block; the working matrix lives in shared memory
-// for k <= 128 and in an L2-resident global scratch slab otherwise.
+// Full path: one CTA (32 warps) per block, the lower triangle held as 32x32
+// tiles (row pitch 36: 16-byte aligned rows read as float4 broadcasts) in
+// shared memory for k <= 256 (L2-resident global scratch beyond):
+//   right-looking tile Cholesky: per panel p, POTRF(p,p) | TRSM(i,p) | SYRK/GEMM
+//   trailing update -- three barriers per panel;
+//   in-place tile TRTRI (LAPACK trtri order): invert diagonal tiles, then for
+//   block columns j = nt-2..0: L_ij <- -(sum_{m=j+1..i} Linv_im L_mj) Linv_jj.
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace {
 
-constexpr int NT = 1024;
+constexpr int NT = 512, NWARP = NT / 32;   // 128 registers/thread: tile rows stay in registers
+constexpr int TS = 32, LDT = 36, TILE = TS * LDT;   // 16-byte rows: float4 row broadcasts
 constexpr float NEAR_ID_TOL = 1e-4f;
 
-__global__ void __launch_bounds__(NT) k_cholinv(int k, const float* __restrict__ G, float* __restrict__ Lout,
-                                                float* __restrict__ Linv, float* __restrict__ work, int smem_mat,
+__device__ unsigned long long g_chol_dbg[2];   // [0] near-identity factorizations, [1] full ones
+__device__ long long g_chol_clk[64];           // phase timestamps of block 0's last full factorization
+#define CHOL_CLK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_chol_clk[i] = clock64(); } while (0)
+
+__device__ __forceinline__ int tidx(int i, int j) { return i * (i + 1) / 2 + j; }   // i >= j
+
+// warp: Cholesky of a 32x32 SPD tile in place (lower triangle); lane = row, the
+// row lives in registers and column c is broadcast by shuffles (no smem round trips)
+__device__ void tile_potrf(float* T, int lane, int32_t* status, bool& bad) {
+  float a[TS];
+#pragma unroll
+  for (int t = 0; t < TS; ++t) a[t] = T[lane * LDT + t];
+#pragma unroll
+  for (int c = 0; c < TS; ++c) {
+    float d = __shfl_sync(0xffffffffu, a[c], c);
+    if (!(d > 0.f) || !isfinite(d)) {
+      bad = true;
+      d = 1.f;
+    }
+    const float s = __fsqrt_rn(d), inv = __frcp_rn(s);
+    if (lane == c) a[c] = s;
+    if (lane > c) a[c] *= inv;
+#pragma unroll 31
+    for (int l = c + 1; l < TS; ++l) {
+      const float v = __shfl_sync(0xffffffffu, a[c], l);   // L[l][c]
+      if (lane >= l) a[l] = fmaf(-a[c], v, a[l]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < TS; ++t) T[lane * LDT + t] = a[t];
+  __syncwarp();
+  if (bad && lane == 0) hg_flag(status, HGS_CHOL_BREAKDOWN);
+}
+
+// warp: A <- A L^-T (L lower 32x32), lane = row of A (row staged in registers)
+__device__ void tile_trsm(float* A, const float* L, int lane) {
+  float a[TS];
+#pragma unroll
+  for (int t = 0; t < TS; ++t) a[t] = A[lane * LDT + t];
+  const float rd = __frcp_rn(L[lane * LDT + lane]);     // lane c: 1 / L[c][c]
+#pragma unroll
+  for (int c = 0; c < TS; ++c) {
+    float x = a[c];
+#pragma unroll
+    for (int t = 0; t < c; ++t) x = fmaf(-a[t], L[c * LDT + t], x);
+    a[c] = x * __shfl_sync(0xffffffffu, rd, c);
+  }
+#pragma unroll
+  for (int t = 0; t < TS; ++t) A[lane * LDT + t] = a[t];
+  __syncwarp();
+}
+
+// dot of a 32-vector in registers with a shared-memory row (float4 broadcasts, 4 chains)
+__device__ __forceinline__ float dot32(const float (&b)[TS], const float* row) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+  for (int t = 0; t < TS; t += 4) {
+    const float4 a = *reinterpret_cast<const float4*>(row + t);
+    s0 = fmaf(a.x, b[t], s0);
+    s1 = fmaf(a.y, b[t + 1], s1);
+    s2 = fmaf(a.z, b[t + 2], s2);
+    s3 = fmaf(a.w, b[t + 3], s3);
+  }
+  return (s0 + s1) + (s2 + s3);
+}
+
+// warp: rows [r0, r0+8) of C -= A B^T (all 32x32); lane c owns output column c, holds row c of B
+__device__ void tile_sub_abt(float* C, const float* A, const float* B, int lane, int r0) {
+  float b[TS];
+#pragma unroll
+  for (int t = 0; t < TS; ++t) b[t] = B[lane * LDT + t];
+#pragma unroll
+  for (int r = r0; r < r0 + 8; ++r) C[r * LDT + lane] -= dot32(b, A + r * LDT);
+  __syncwarp();
+}
+
+// warp: rows [r0, r0+8) of C = sign*A B (overwrite) or += sign*A B; lane c owns column c
+__device__ void tile_add_ab(float* C, const float* A, const float* B, int lane, bool overwrite, float sign, int r0) {
+  float b[TS];
+#pragma unroll
+  for (int t = 0; t < TS; ++t) b[t] = B[t * LDT + lane];
+  __syncwarp();
+#pragma unroll
+  for (int r = r0; r < r0 + 8; ++r) {
+    const float v = sign * dot32(b, A + r * LDT);
+    C[r * LDT + lane] = overwrite ? v : C[r * LDT + lane] + v;
+  }
+  __syncwarp();
+}
+
+// warp: lower-triangular 32x32 tile inverse in place; lane c owns column c (registers)
+__device__ void tile_trtri(float* T, int lane) {
+  float x[TS];
+  const int c = lane;
+  const float rd = __frcp_rn(T[lane * LDT + lane]);     // lane r: 1 / T[r][r]
+#pragma unroll
+  for (int r = 0; r < TS; ++r) {
+    const float rr = __shfl_sync(0xffffffffu, rd, r);
+    if (r < c) {
+      x[r] = 0.f;
+    } else if (r == c) {
+      x[r] = rr;
+    } else {
+      float acc = 0.f;
+#pragma unroll
+      for (int t = 0; t < r; ++t)
+        if (t >= c) acc = fmaf(T[r * LDT + t], x[t], acc);
+      x[r] = -acc * rr;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < TS; ++r) T[r * LDT + c] = x[r];   // lower part only: x[r] = 0 above
+  __syncwarp();
+}
+
+// warps write the full k x k row-major matrix (zeros above the diagonal) from the
+// lower tiles: warp per (tile row, tile column, 8-row slab), lanes = columns
+__device__ void store_lower(float* out, const float* tiles, int k, int nt, int warp, int lane) {
+  for (int task = warp; task < nt * nt * 4; task += NWARP) {
+    const int tl = task >> 2, rq = (task & 3) * 8;
+    const int i = tl / nt, j = tl % nt;
+    const int c = j * TS + lane;
+    if (c >= k) continue;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = i * TS + rq + u;
+      if (r < k) out[(int64_t)r * k + c] = (c <= r) ? tiles[(int64_t)tidx(i, j) * TILE + (rq + u) * LDT + lane] : 0.f;
+    }
+  }
+}
+
+__global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, float* __restrict__ Lout,
+                                                float* __restrict__ Linv, float* __restrict__ work, int smem_tiles,
                                                 int32_t* status) {
   extern __shared__ __align__(16) float sm[];
-  __shared__ float red[NT / 32];
+  __shared__ float red[NWARP];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nt = (k + TS - 1) / TS;
+  const int ntiles = nt * (nt + 1) / 2;
   const int64_t kk = (int64_t)k * k;
   const int64_t off = (int64_t)blockIdx.x * kk;
-  float* A = smem_mat ? sm : work + off;
-  float* colbuf = smem_mat ? sm + kk : sm;   // [32 warps][k]
   const float* Gb = G + off;
   float* Lb = Lout ? Lout + off : nullptr;
   float* Ib = Linv + off;
 
-  // load + distance from identity
+  // distance from the identity (near-identity path for the second CholeskyQR pass)
   float emax = 0.f;
   for (int64_t i = t; i < kk; i += NT) {
     const float g = Gb[i];
-    A[i] = g;
     const int r = (int)(i / k), c = (int)(i % k);
     const float e = fabsf(g - (r == c ? 1.f : 0.f));
     emax = fmaxf(emax, isfinite(g) ? e : INFINITY);
@@ -56,75 +193,127 @@ __global__ void __launch_bounds__(NT) k_cholinv(int k, const float* __restrict__
   }
   __syncthreads();
   const float E = red[0];
-  if (!isfinite(E)) {
-    if (t == 0) hg_flag(status, HGS_NONFINITE);
-  }
+  if (!isfinite(E) && t == 0) hg_flag(status, HGS_NONFINITE);
+  if (t == 0) atomicAdd(&g_chol_dbg[E <= NEAR_ID_TOL ? 0 : 1], 1ull);
   if (E <= NEAR_ID_TOL) {
     for (int64_t i = t; i < kk; i += NT) {
       const int r = (int)(i / k), c = (int)(i % k);
+      const float g = Gb[i];
       float l, li;
       if (c > r) { l = 0.f; li = 0.f; }
-      else if (c == r) { const float e = 0.5f * (A[i] - 1.f); l = 1.f + e; li = 1.f - e; }
-      else { l = A[i]; li = -A[i]; }
+      else if (c == r) { const float e = 0.5f * (g - 1.f); l = 1.f + e; li = 1.f - e; }
+      else { l = g; li = -g; }
       if (Lb) Lb[i] = l;
       Ib[i] = li;
     }
     return;
   }
-  // ---- right-looking Cholesky, lower triangle of A
-  for (int j = 0; j < k; ++j) {
-    __syncthreads();
-    float d = A[(int64_t)j * k + j];
-    if (!(d > 0.f) || !isfinite(d)) {
-      if (t == 0) hg_flag(status, HGS_CHOL_BREAKDOWN);
-      d = 1.f;
+
+  CHOL_CLK(0);
+  float* tiles = smem_tiles ? sm : work + (int64_t)blockIdx.x * ((int64_t)ntiles * TILE);
+  float* temp = smem_tiles ? sm + (int64_t)ntiles * TILE : sm;   // [nt-1] tiles in shared memory
+  auto T = [&](int i, int j) { return tiles + (int64_t)tidx(i, j) * TILE; };
+
+  // load the lower tiles (padding beyond k = identity): warp per (tile, 8-row slab),
+  // lanes = columns, 8 independent coalesced loads in flight per lane
+  for (int task = warp; task < ntiles * 4; task += NWARP) {
+    const int tl = task >> 2, rq = (task & 3) * 8;
+    int i = 0;
+    while ((i + 1) * (i + 2) / 2 <= tl) ++i;
+    const int j = tl - i * (i + 1) / 2;
+    const int c = j * TS + lane;
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = i * TS + rq + u;
+      v[u] = (r < k && c < k) ? Gb[(int64_t)r * k + c] : (r == c ? 1.f : 0.f);
     }
-    const float s = sqrtf(d), inv = 1.0f / s;
-    for (int i = j + 1 + t; i < k; i += NT) A[(int64_t)i * k + j] *= inv;
-    __syncthreads();
-    if (t == 0) A[(int64_t)j * k + j] = s;
-    const int n = k - j - 1;
-    for (int idx = t; idx < n * n; idx += NT) {
-      const int i = j + 1 + idx / n, l = j + 1 + idx % n;
-      if (l <= i) A[(int64_t)i * k + l] -= A[(int64_t)i * k + j] * A[(int64_t)l * k + j];
-    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) tiles[(int64_t)tl * TILE + (rq + u) * LDT + lane] = v[u];
   }
   __syncthreads();
-  if (Lb)
-    for (int64_t i = t; i < kk; i += NT) {
-      const int r = (int)(i / k), c = (int)(i % k);
-      Lb[i] = (c <= r) ? A[i] : 0.f;
+
+  // ---- right-looking tile Cholesky
+  CHOL_CLK(1);
+  bool bad = false;
+  for (int p = 0; p < nt; ++p) {
+    if (warp == 0) tile_potrf(T(p, p), lane, status, bad);
+    __syncthreads();
+    CHOL_CLK(2 + 3 * p);
+    for (int i = p + 1 + warp; i < nt; i += NWARP) tile_trsm(T(i, p), T(p, p), lane);
+    __syncthreads();
+    CHOL_CLK(3 + 3 * p);
+    const int m = nt - p - 1;                       // trailing tiles (i,j), p < j <= i
+    for (int task = warp; task < m * (m + 1) / 2 * 4; task += NWARP) {
+      const int w = task >> 2;
+      int a = 0;
+      while ((a + 1) * (a + 2) / 2 <= w) ++a;
+      const int b = w - a * (a + 1) / 2;
+      const int i = p + 1 + a, j = p + 1 + b;
+      tile_sub_abt(T(i, j), T(i, p), T(j, p), lane, (task & 3) * 8);
     }
-  // ---- Linv = L^-1 column by column (forward substitution), one warp per column
-  float* x = colbuf + (int64_t)warp * k;
-  for (int c = warp; c < k; c += NT / 32) {
-    if (lane == 0) x[c] = 1.0f / A[(int64_t)c * k + c];
-    __syncwarp();
-    for (int i = c + 1; i < k; ++i) {
-      float acc = 0.f;
-      for (int j = c + lane; j < i; j += 32) acc = fmaf(A[(int64_t)i * k + j], x[j], acc);
-      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) x[i] = -acc / A[(int64_t)i * k + i];
-      __syncwarp();
-    }
-    for (int i = lane; i < k; i += 32) Ib[(int64_t)i * k + c] = (i >= c) ? x[i] : 0.f;
-    __syncwarp();
+    __syncthreads();
+    CHOL_CLK(4 + 3 * p);
   }
+  if (Lb) store_lower(Lb, tiles, k, nt, warp, lane);
+  // ---- in-place tile TRTRI
+  CHOL_CLK(40);
+  for (int d = warp; d < nt; d += NWARP) tile_trtri(T(d, d), lane);
+  __syncthreads();
+  CHOL_CLK(41);
+  for (int j = nt - 2; j >= 0; --j) {
+    const int dn = nt - 1 - j;
+    for (int task = warp; task < dn * 4; task += NWARP) {   // temp[w] = sum_{m=j+1..i} Linv_im L_mj
+      const int w = task >> 2, i = j + 1 + w, r0 = (task & 3) * 8;
+      float* tmp = temp + (int64_t)w * TILE;
+      for (int m = j + 1; m <= i; ++m) tile_add_ab(tmp, T(i, m), T(m, j), lane, m == j + 1, 1.f, r0);
+    }
+    __syncthreads();
+    for (int task = warp; task < dn * 4; task += NWARP) {   // L_ij <- -temp Linv_jj
+      const int w = task >> 2, i = j + 1 + w;
+      tile_add_ab(T(i, j), temp + (int64_t)w * TILE, T(j, j), lane, true, -1.f, (task & 3) * 8);
+    }
+    __syncthreads();
+    CHOL_CLK(42 + (nt - 2 - j));
+  }
+  CHOL_CLK(60);
+  store_lower(Ib, tiles, k, nt, warp, lane);
+  __syncthreads();
+  CHOL_CLK(61);
 }
 
 }  // namespace
 
+cudaError_t chol_clocks(long long* out) { return cudaMemcpyFromSymbol(out, g_chol_clk, sizeof(g_chol_clk)); }
+
+cudaError_t chol_debug(unsigned long long* out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_chol_dbg, sizeof(g_chol_dbg));
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[2] = {0, 0};
+    e = cudaMemcpyToSymbol(g_chol_dbg, z, sizeof z);
+  }
+  return e;
+}
+
+size_t cholinv_work_floats(int k) {
+  const int nt = (k + TS - 1) / TS;
+  return (size_t)nt * (nt + 1) / 2 * TILE;
+}
+
 cudaError_t launch_cholinv(int nb, int k, const float* G, float* L, float* Linv, float* work, int32_t* status,
                            cudaStream_t s, int* launches) {
-  const bool smem_mat = k <= 128;
-  const size_t smem = ((smem_mat ? (size_t)k * k : 0) + (size_t)(NT / 32) * k) * sizeof(float);
+  const int nt = (k + TS - 1) / TS;
+  const size_t tiles_bytes = cholinv_work_floats(k) * sizeof(float);
+  const size_t temp_bytes = (size_t)(nt > 1 ? nt - 1 : 1) * TILE * sizeof(float);
+  const bool smem_tiles = tiles_bytes + temp_bytes <= 200 * 1024;
+  const size_t smem = (smem_tiles ? tiles_bytes : 0) + temp_bytes;
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(k_cholinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  k_cholinv<<<nb, NT, smem, s>>>(k, G, L, Linv, work, smem_mat ? 1 : 0, status);
+  k_cholinv<<<nb, NT, smem, s>>>(k, G, L, Linv, work, smem_tiles ? 1 : 0, status);
   ++*launches;
   return cudaGetLastError();
 }

@@ -22,6 +22,9 @@
 // rotation or flags HG_ST_JACOBI_CAP after MAX_SWEEPS.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+#include <cmath>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -31,16 +34,26 @@ namespace {
 
 constexpr int NT = 512;
 constexpr int MAX_SWEEPS = 40;
-constexpr double TOL = 3e-7;
+
+__device__ unsigned long long g_jac_dbg[3];   // [0] max sweeps, [1] total sweeps, [2] blocks
+__device__ long long g_jac_clk[16];           // block 0 / rank 0 / thread 0: phase stamps of sweep 1, rounds 0-2
+#define JAC_CLK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0 && sweep == 1 && r < 3) g_jac_clk[(i) + 4 * r] = clock64(); } while (0)
+
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 __device__ __forceinline__ void pair_of(int r, int i, int K2, int& p, int& q) {
   const int n1 = K2 - 1;
   if (i == 0) { p = 0; q = 1 + r; return; }
-  p = 1 + (r + i) % n1;
-  q = 1 + (r - i + n1) % n1;
+  int x = r + i, y = r - i + n1;          // both in [0, 2 n1)
+  if (x >= n1) x -= n1;
+  if (y >= n1) y -= n1;
+  p = 1 + x;
+  q = 1 + y;
 }
 
-__global__ void __launch_bounds__(NT) k_jacobi(int k, int C, int nbuf, const float* __restrict__ L,
+__global__ void __launch_bounds__(NT) k_jacobi(int k, int C, int nbuf, double tol, const float* __restrict__ L,
                                                float* __restrict__ Wf, int32_t* status) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   cg::cluster_group cluster = cg::this_cluster();
@@ -53,9 +66,10 @@ __global__ void __launch_bounds__(NT) k_jacobi(int k, int C, int nbuf, const flo
   const int nr = max(0, min(R, k - r0));
   const int ldw = K2 + 1;
   float* W = reinterpret_cast<float*>(smem_raw);                               // [R][ldw]
-  double* part = reinterpret_cast<double*>(smem_raw + (((size_t)R * ldw * 4 + 15) & ~size_t(15)));  // [nbuf][C][P][3]
+  double* part = reinterpret_cast<double*>(smem_raw + (((size_t)R * ldw * 4 + 15) & ~size_t(15)));  // [nbuf][C][P][4]
   const int t = threadIdx.x;
   const float* Lb = L + (int64_t)blk * k * k;
+  const double tol2 = tol * tol;
 
   for (int i = t; i < R * ldw; i += NT) {
     const int rl = i / ldw, c = i % ldw;
@@ -79,53 +93,78 @@ __global__ void __launch_bounds__(NT) k_jacobi(int k, int C, int nbuf, const flo
     int any = 0;
     for (int r = 0; r < K2 - 1; ++r) {
       const int buf = r % nbuf;
+      JAC_CLK(0);
       // single-buffered exchange: everyone must have read the previous round's partials
-      if (nbuf == 1 && C > 1 && r > 0) cluster.sync();
+      if (nbuf == 1 && C > 1 && r > 0) cluster_barrier();
       // A: partial Gram entries over this CTA's rows
       for (int i = grp; i < P; i += groups) {
         int p, q;
         pair_of(r, i, K2, p, q);
-        double app = 0, aqq = 0, apq = 0;
+        // per-thread partials in fp32 over <= 64 rows (rounding <= ~u sum|w_p w_q|,
+        // far below the rotation threshold), cross-thread / cross-CTA sums in fp64
+        float fpp = 0.f, fqq = 0.f, fpq = 0.f;
         for (int rl = sub; rl < nr; rl += Gp) {
-          const double wp = W[rl * ldw + p], wq = W[rl * ldw + q];
-          app = fma(wp, wp, app);
-          aqq = fma(wq, wq, aqq);
-          apq = fma(wp, wq, apq);
+          const float wp = W[rl * ldw + p], wq = W[rl * ldw + q];
+          fpp = fmaf(wp, wp, fpp);
+          fqq = fmaf(wq, wq, fqq);
+          fpq = fmaf(wp, wq, fpq);
         }
+        double app = fpp, aqq = fqq, apq = fpq;
         for (int o = Gp / 2; o; o >>= 1) {
           app += __shfl_xor_sync(gmask, app, o);
           aqq += __shfl_xor_sync(gmask, aqq, o);
           apq += __shfl_xor_sync(gmask, apq, o);
         }
         if (sub == 0) {
-          double* dst = part + (((size_t)buf * C + rank) * P + i) * 3;
+          double* dst = part + (((size_t)buf * C + rank) * P + i) * 4;
           if (C > 1) {
+            const uint32_t la = smem_u32(dst);
             for (int cr = 0; cr < C; ++cr) {
-              double* rd = cluster.map_shared_rank(dst, cr);
-              rd[0] = app; rd[1] = aqq; rd[2] = apq;
+              uint32_t ra;
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(cr));
+              asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ra), "d"(app), "d"(aqq) : "memory");
+              asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra + 16), "d"(apq) : "memory");
             }
           } else {
             dst[0] = app; dst[1] = aqq; dst[2] = apq;
           }
         }
       }
-      if (C > 1) cluster.sync(); else __syncthreads();
-      // C: total Gram entries (fixed summation order), rotation, apply to local rows
+      JAC_CLK(1);
+      if (C > 1) cluster_barrier(); else __syncthreads();
+      JAC_CLK(2);
+      // C: total Gram entries (fixed summation order), rotation, apply to local rows.
+      // The group leader decides (a_pq^2 > tol^2 a_pp a_qq) and forms (c, s) in fp64;
+      // the group gets them by shuffle.
       int rot = 0;
       for (int i = grp; i < P; i += groups) {
         int p, q;
         pair_of(r, i, K2, p, q);
-        double app = 0, aqq = 0, apq = 0;
-        for (int cr = 0; cr < C; ++cr) {
-          const double* src = part + (((size_t)buf * C + cr) * P + i) * 3;
-          app += src[0]; aqq += src[1]; apq += src[2];
+        float c = 1.f, s = 0.f;
+        int act = 0;
+        if (sub == 0) {
+          double app = 0, aqq = 0, apq = 0;
+          for (int cr = 0; cr < C; ++cr) {
+            const double* src = part + (((size_t)buf * C + cr) * P + i) * 4;
+            app += src[0]; aqq += src[1]; apq += src[2];
+          }
+          if (p < k && q < k && apq * apq > tol2 * app * aqq) {
+            // the angle may be approximate (fp32); the pair (c, s) must be orthogonal
+            // to fp32 rounding and unbiased -- biased rotations drift the column norms
+            // over the ~k*sweeps rotations each column sees -- so c = rsqrt(1+t^2) in fp64
+            const float zeta = (float)(aqq - app) / (float)(2.0 * apq);
+            const float tf = copysignf(1.0f, zeta) / (fabsf(zeta) + sqrtf(fmaf(zeta, zeta, 1.0f)));
+            const double td = tf;
+            const double cd = rsqrt(fma(td, td, 1.0));
+            c = (float)cd;
+            s = (float)(cd * td);
+            act = 1;
+          }
         }
-        if (p >= k || q >= k) continue;
-        if (!(fabs(apq) > TOL * sqrt(app * aqq))) continue;
-        const double zeta = (aqq - app) / (2.0 * apq);
-        const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cd = 1.0 / sqrt(1.0 + tt * tt);
-        const float c = (float)cd, s = (float)(cd * tt);
+        act = __shfl_sync(gmask, act, (t & 31) / Gp * Gp);
+        if (!act) continue;
+        c = __shfl_sync(gmask, c, (t & 31) / Gp * Gp);
+        s = __shfl_sync(gmask, s, (t & 31) / Gp * Gp);
         rot = 1;
         for (int rl = sub; rl < nr; rl += Gp) {
           const float wp = W[rl * ldw + p], wq = W[rl * ldw + q];
@@ -133,20 +172,51 @@ __global__ void __launch_bounds__(NT) k_jacobi(int k, int C, int nbuf, const flo
           W[rl * ldw + q] = s * wp + c * wq;
         }
       }
-      any |= __syncthreads_or(rot);
+      any |= rot;
+      JAC_CLK(3);
+      __syncthreads();
     }
-    converged = (any == 0);
+    converged = (__syncthreads_or(any) == 0);
   }
   if (!converged && t == 0 && rank == 0) hg_flag(status, HGS_JACOBI_CAP);
+  if (t == 0 && rank == 0) {
+    atomicMax(&g_jac_dbg[0], (unsigned long long)sweep);
+    atomicAdd(&g_jac_dbg[1], (unsigned long long)sweep);
+    atomicAdd(&g_jac_dbg[2], 1ull);
+  }
   float* out = Wf + (int64_t)blk * k * k;
   for (int i = t; i < nr * k; i += NT) {
     const int rl = i / k, c = i % k;
     out[(int64_t)(r0 + rl) * k + c] = W[rl * ldw + c];
   }
-  if (C > 1) cluster.sync();   // no CTA exits while others may still write its shared memory
+  if (C > 1) cluster_barrier();   // no CTA exits while others may still write its shared memory
 }
 
 }  // namespace
+
+cudaError_t jacobi_clocks(long long* out) { return cudaMemcpyFromSymbol(out, g_jac_clk, sizeof(g_jac_clk)); }
+
+cudaError_t jacobi_debug(unsigned long long* out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_jac_dbg, sizeof(g_jac_dbg));
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[3] = {0, 0, 0};
+    e = cudaMemcpyToSymbol(g_jac_dbg, z, sizeof z);
+  }
+  return e;
+}
+
+// Rotation threshold: a pair is rotated while |a_pq| > tol sqrt(a_pp a_qq).  The
+// applied-inverse error tracks ~6 tol (measured at configs[3]: tol 3e-7 -> 2.3e-6,
+// 9.5e-7 -> 5.7e-6, 3e-6 -> 1.8e-5) at no measurable sweep cost, so tol = 3e-7,
+// above the fp32 rounding floor of the rotated columns; HG_JACOBI_TOL overrides it.
+double jacobi_tol(int k) {
+  static double env = [] {
+    const char* v = getenv("HG_JACOBI_TOL");
+    return v ? atof(v) : 0.0;
+  }();
+  if (env > 0) return env;
+  return 3e-7;
+}
 
 cudaError_t launch_jacobi(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s,
                           int* launches) {
@@ -154,7 +224,7 @@ cudaError_t launch_jacobi(int nb, int k, const float* L, float* Wf, int32_t* sta
   if (C > 8) return cudaErrorInvalidValue;
   const int K2 = (k + 1) & ~1, P = K2 / 2, R = (k + C - 1) / C;
   const size_t wbytes = (((size_t)R * (K2 + 1) * 4) + 15) & ~size_t(15);
-  const size_t pbytes = (size_t)C * P * 3 * sizeof(double);
+  const size_t pbytes = (size_t)C * P * 4 * sizeof(double);
   const int nbuf = (wbytes + 2 * pbytes <= 220 * 1024) ? 2 : 1;
   const size_t smem = wbytes + nbuf * pbytes;
   cudaError_t e = cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -175,7 +245,7 @@ cudaError_t launch_jacobi(int nb, int k, const float* L, float* Wf, int32_t* sta
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, k_jacobi, k, C, nbuf, L, Wf, status);
+  e = cudaLaunchKernelEx(&cfg, k_jacobi, k, C, nbuf, jacobi_tol(k), L, Wf, status);
   ++*launches;
   return e;
 }

@@ -32,3 +32,9 @@ cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float
 // apply prep: rs[i][j] = scale / sigma[i][j]; flags singular sigma
 cudaError_t launch_inv_sigma(int nb, int k, const float* sigma, float scale, float* rs, int32_t* status,
                              cudaStream_t s, int* launches);
+
+// debug counters (device globals): chol {near-identity, full}; jacobi {max sweeps, total sweeps, blocks}
+cudaError_t chol_debug(unsigned long long* out, bool reset);
+cudaError_t jacobi_debug(unsigned long long* out, bool reset);
+cudaError_t chol_clocks(long long* out);
+cudaError_t jacobi_clocks(long long* out);

@@ -57,10 +57,14 @@ _solve_host = _sig("hg_solve_host", ctypes.c_int, _i32, _i32, _i64, _P, _P, _P, 
 _gemm = _sig("hg_gemm", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i32, _i64, _i64, _P, _i32, _i64, _i64, _P, _i32,
              _i64, _i64, _f32, _P, _i64, _P, _i64, _u32, _P)
 _last_error = _sig("hg_last_error", ctypes.c_char_p)
+_prof_enable = _sig("hg_profile_enable", ctypes.c_int, _i32)
+_prof_collect = _sig("hg_profile_collect", ctypes.c_int, _i32, _P, _P, _P, ctypes.POINTER(_i32))
 _last_launches = _sig("hg_last_launch_count", ctypes.c_int32)
+_debug_counters = _sig("hg_debug_counters", ctypes.c_int, _P, _i32, _i32)
 
 EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_rsvd", "hg_block_apply_inverse",
-           "hg_solve", "hg_solve_host", "hg_gemm", "hg_last_error", "hg_last_launch_count")
+           "hg_solve", "hg_solve_host", "hg_gemm", "hg_last_error", "hg_last_launch_count", "hg_profile_enable",
+           "hg_profile_collect", "hg_debug_counters")
 
 
 class HGError(RuntimeError):
@@ -76,6 +80,34 @@ def _check(st: int):
 
 def last_launch_count() -> int:
     return int(_last_launches())
+
+
+def debug_counters(reset: bool = False) -> dict:
+    import numpy as np
+    out = np.zeros(85, dtype=np.int64)
+    _check(_debug_counters(out.ctypes.data_as(_P), 85, int(reset)))
+    return {"chol_near_identity": int(out[0]), "chol_full": int(out[1]), "jacobi_max_sweeps": int(out[2]),
+            "jacobi_total_sweeps": int(out[3]), "jacobi_blocks": int(out[4]), "chol_clk": out[5:69].tolist(),
+            "jac_clk": out[69:85].tolist()}
+
+
+def profile_enable(on: bool = True):
+    _check(_prof_enable(1 if on else 0))
+
+
+def profile_collect() -> dict:
+    """{stage: (total_ms, launches)} recorded since the last collect (synchronises)."""
+    import numpy as np
+    names = ctypes.create_string_buffer(32 * 32)
+    ms = np.zeros(32)
+    cnt = np.zeros(32, dtype=np.int32)
+    n = _i32(0)
+    _check(_prof_collect(32, names, ms.ctypes.data_as(_P), cnt.ctypes.data_as(_P), ctypes.byref(n)))
+    out = {}
+    for i in range(min(n.value, 32)):
+        nm = names.raw[32 * i:32 * (i + 1)].split(b"\0", 1)[0].decode()
+        out[nm] = (float(ms[i]), int(cnt[i]))
+    return out
 
 
 def _ptr(t: Optional[torch.Tensor]):

@@ -171,7 +171,7 @@ def make_input(cfg: SynthConfig) -> HypergraphInput:
     return HypergraphInput(cfg, row_ptr, cols, w, Y)
 
 
-def make_tiny(N: int, b: int, k: int, q: int, *, K: int = 3, n_tag: int = 6, G: int = 3,
+def make_tiny(N: int, b: int, k: int, q: int, *, K: int = 3, n_tag: int = 8, G: int = 3,
               d: int = 8, C: int = 2, unit_w: bool = False, seed: int = 0) -> HypergraphInput:
     """A small hypergraph with the same recipe (tests; group sizes capped at N)."""
     cfg = SynthConfig(f"tiny{N}", N=N, d=d, C=C, K=K, n_tag=n_tag, zipf_s=1.1, G=G,

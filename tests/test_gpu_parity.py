@@ -103,7 +103,8 @@ def test_theta_blocks_parity(inputs, cfg):
     assert bool((X == X.transpose(1, 2)).all())
     sel = range(c.nb) if c.nb <= 16 else [0, 1, c.nb // 2, c.nb - 1]
     dv, _ = oracle.degrees(h.row_ptr, h.col_idx, h.w)
-    np.testing.assert_allclose(dvr.double().cpu().numpy(), dv ** -0.5, rtol=2e-7)
+    # delta(v) is an fp32 sum of ~20-60 weights: a few ulps (1e-6 = 16 ulp)
+    np.testing.assert_allclose(dvr.double().cpu().numpy(), dv ** -0.5, rtol=1e-6)
     for blk in sel:
         ref = oracle.theta_block(h.row_ptr, h.col_idx, h.w, c.b, blk)
         got = th[blk].double().cpu().numpy()
