@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -408,7 +409,7 @@ hg_status hg_debug_counters(int64_t* out, int32_t n, int32_t reset) {
   }
   if (n >= 69 + 16) {
     long long clk[16];
-    HG_CU(jacobi_clocks(clk), "jacobi_clocks");
+    HG_CU(getenv("HG_JACOBI") ? jacobi_clocks(clk) : jacobi_blk_clocks(clk), "jacobi_clocks");
     for (int i = 0; i < 16; ++i) out[69 + i] = clk[i];
   }
   unsigned long long c[2] = {0, 0}, j[3] = {0, 0, 0};

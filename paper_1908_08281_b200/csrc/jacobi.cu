@@ -64,7 +64,14 @@ __global__ void __launch_bounds__(NT) k_jacobi(int k, int C, int nbuf, double to
   const int R = (k + C - 1) / C;        // rows per CTA
   const int r0 = rank * R;
   const int nr = max(0, min(R, k - r0));
-  const int ldw = K2 + 1;
+  // thread -> (pair group, sub-lane): Gp threads per pair (power of two <= 32)
+  int Gp = NT / P;
+  if (Gp > 32) Gp = 32;
+  if (Gp < 1) Gp = 1;
+  { int g = 1; while (g * 2 <= Gp) g *= 2; Gp = g; }
+  // row pitch = 32/Gp (mod 32): a warp holds 32/Gp consecutive pairs x Gp row-strided
+  // threads, so column p+g of row sub+Gp*j lands in bank p + g + (32/Gp)*sub: all distinct
+  const int ldw = K2 + 32 / Gp + ((32 / Gp) == 32 ? 0 : 0);
   float* W = reinterpret_cast<float*>(smem_raw);                               // [R][ldw]
   double* part = reinterpret_cast<double*>(smem_raw + (((size_t)R * ldw * 4 + 15) & ~size_t(15)));  // [nbuf][C][P][4]
   const int t = threadIdx.x;
@@ -78,11 +85,6 @@ __global__ void __launch_bounds__(NT) k_jacobi(int k, int C, int nbuf, double to
   }
   __syncthreads();
 
-  // thread -> (pair group, sub-lane): Gp threads per pair (power of two <= 32)
-  int Gp = NT / P;
-  if (Gp > 32) Gp = 32;
-  if (Gp < 1) Gp = 1;
-  { int g = 1; while (g * 2 <= Gp) g *= 2; Gp = g; }
   const int groups = NT / Gp;
   const int sub = t % Gp, grp = t / Gp;
   const unsigned gmask = (Gp == 32) ? 0xffffffffu : (((1u << Gp) - 1u) << ((t & 31) / Gp * Gp));
@@ -202,6 +204,11 @@ cudaError_t jacobi_debug(unsigned long long* out, bool reset) {
     unsigned long long z[3] = {0, 0, 0};
     e = cudaMemcpyToSymbol(g_jac_dbg, z, sizeof z);
   }
+  unsigned long long b[3] = {0, 0, 0};
+  if (e == cudaSuccess) e = jacobi_blk_debug(b, reset);
+  out[0] = out[0] > b[0] ? out[0] : b[0];
+  out[1] += b[1];
+  out[2] += b[2];
   return e;
 }
 
@@ -218,12 +225,26 @@ double jacobi_tol(int k) {
   return 3e-7;
 }
 
+cudaError_t launch_jacobi_scalar(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s,
+                                 int* launches);
+
+// HG_JACOBI=scalar selects the scalar cyclic kernel (comparison / verification)
 cudaError_t launch_jacobi(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s,
                           int* launches) {
+  static const bool scalar = [] {
+    const char* v = getenv("HG_JACOBI");
+    return v && v[0] == 's';
+  }();
+  if (scalar) return launch_jacobi_scalar(nb, k, L, Wf, status, s, launches);
+  return launch_jacobi_blk(nb, k, L, Wf, status, s, launches);
+}
+
+cudaError_t launch_jacobi_scalar(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s,
+                                 int* launches) {
   const int C = (k + 63) / 64;
   if (C > 8) return cudaErrorInvalidValue;
   const int K2 = (k + 1) & ~1, P = K2 / 2, R = (k + C - 1) / C;
-  const size_t wbytes = (((size_t)R * (K2 + 1) * 4) + 15) & ~size_t(15);
+  const size_t wbytes = (((size_t)R * (K2 + 32) * 4) + 15) & ~size_t(15);
   const size_t pbytes = (size_t)C * P * 4 * sizeof(double);
   const int nbuf = (wbytes + 2 * pbytes <= 220 * 1024) ? 2 : 1;
   const size_t smem = wbytes + nbuf * pbytes;

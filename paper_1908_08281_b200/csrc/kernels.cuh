@@ -38,3 +38,7 @@ cudaError_t chol_debug(unsigned long long* out, bool reset);
 cudaError_t jacobi_debug(unsigned long long* out, bool reset);
 cudaError_t chol_clocks(long long* out);
 cudaError_t jacobi_clocks(long long* out);
+cudaError_t launch_jacobi_blk(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s,
+                              int* launches);
+cudaError_t jacobi_blk_debug(unsigned long long* out, bool reset);
+cudaError_t jacobi_blk_clocks(long long* out);
