@@ -210,6 +210,7 @@ def run_ours(args):
     value = world * c.nb / (ms / 1e3)
 
     # per-stage attribution: the same steps with per-stage CUDA events on the stream
+    hg.debug_counters(reset=True)
     hg.profile_enable(True)
     torch.cuda.synchronize(dev)
     pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -221,6 +222,9 @@ def run_ours(args):
     hg.profile_enable(False)
     torch.cuda.synchronize(dev)
     prof_ms_per_step = pe0.elapsed_time(pe1) / args.steps
+    dbg = hg.debug_counters()
+    sweeps_avg = dbg["jacobi_total_sweeps"] / max(1, dbg["jacobi_blocks"])
+    chol_full_frac = dbg["chol_full"] / max(1, dbg["chol_full"] + dbg["chol_near_identity"])
     stages = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                   "share": v[0] / args.steps / prof_ms_per_step} for k, v in prof.items()}
 
@@ -237,10 +241,28 @@ def run_ours(args):
         "assemble": ("hbm", 4.0 * b * b * nb, 1),
     }
 
+    # CUDA-core fp32 peak for ALU-bound stages: 148 SMs x 128 FMA/clk x 2 flop x max SM clock
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+    # one-sided Jacobi: per sweep k(k-1)/2 pairs x k rows x (3 dot FMA + 4 rotation ops) ~ 6 k^3 flop
+    work["jacobi"] = ("alu", 6.0 * k ** 3 * sweeps_avg * nb, 1)
+    # Cholesky k^3/3 + triangular inverse k^3/3 FMA per full factorization (first-order ones ~k^2)
+    work["cholinv"] = ("alu", 2.0 * (2.0 / 3.0) * k ** 3 * chol_full_frac * nb, 4 * q + 3)
+
     def roof(stage):
         if stage not in work or stage not in prof:
             return None
         bound, per_launch, _ = work[stage]
+        if bound == "alu":
+            total_ms, n = prof[stage]
+            avg_s = total_ms / n / 1e3
+            tf = per_launch / avg_s / 1e12
+            return {"kernel": stage, "bound": "alu", "achieved": tf, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": tf / fp32_peak, "avg_launch_ms": avg_s * 1e3, "launches_per_step": n / args.steps,
+                    "peak_note": "fp32 CUDA-core peak: 148 SM x 128 FMA/clk x 2 x sm_max_mhz (B200_PROFILING.md units)",
+                    "work_note": ("6 k^3 flop per block per sweep, %.2f sweeps avg" % sweeps_avg) if stage == "jacobi"
+                    else ("(4/3) k^3 flop per full factorization, %.0f%% full" % (100 * chol_full_frac)),
+                    "traffic": None}
         total_ms, n = prof[stage]
         avg_s = total_ms / n / 1e3
         if bound == "tensor":
@@ -327,6 +349,7 @@ def run_ours(args):
         "gemm_tf32_pipe_frac": gemm_roof["frac"] if gemm_roof else None,
         "roofline": dom_roof, "gemm_roofline": gemm_roof,
         "stages": stages, "profiled_ms_per_step": prof_ms_per_step,
+        "jacobi_sweeps_avg": sweeps_avg, "jacobi_sweeps_max": dbg["jacobi_max_sweeps"],
         "e2e": {"value": world * c.nb / (e2e_ms / 1e3), "unit": "blocks/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "entry": "hg_solve_host"},
         "gpu_launches": launches_per_step * args.steps,

