@@ -61,6 +61,7 @@ struct Cfg {
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr uint32_t TX = (uint32_t)(BM + BN) * BK * 4;
   static constexpr int HALF = BN / 2;           // columns per epilogue warp
+  static_assert(8 * 32 * (HALF + 4) * 4 <= STAGES * STAGE_BYTES, "epilogue staging must fit the pipeline smem");
 };
 
 // kind::tf32 instruction descriptor: D f32, A/B tf32, M = 128, N = BN.
@@ -261,22 +262,63 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       while (drained < nchunks - 1 && kb >= (drained + 1) * CHUNK_KB + 1) drain(drained++);
     }
     while (drained < nchunks) drain(drained++);
-    // epilogue: scale and store from registers
-    const int m = m0 + q * 32 + lane;
-    if (m < ea.M) {
-      const float rsv = ea.alpha * (ea.rs ? ea.rs[(int64_t)g * ea.srs + m] : 1.0f);
-      float* Dg = ea.D + (int64_t)g * ea.sd;
-      const int nb0 = n0 + h * C::HALF;
+    // epilogue: scale and store.  Transposed output D[n][m]: a warp's 32 rows m are
+    // one 128-byte line per column n, stored straight from registers.  Row-major
+    // output D[m][n]: each warp stages its 32 x HALF sub-tile in the (now idle)
+    // pipeline shared memory and writes it back row by row (128 bytes per store
+    // instruction instead of 32 scattered rows).
+    const int mrow = q * 32 + lane;
+    const int m = m0 + mrow;
+    const float rsv = (m < ea.M) ? ea.alpha * (ea.rs ? ea.rs[(int64_t)g * ea.srs + m] : 1.0f) : 0.f;
+    float* Dg = ea.D + (int64_t)g * ea.sd;
+    const int nb0 = n0 + h * C::HALF;
+    if (ea.d_trans) {
+      if (m < ea.M) {
 #pragma unroll
-      for (int j = 0; j < C::HALF; ++j) {
-        const int n = nb0 + j;
-        if (n < ea.N) {
-          float val = acc[j] * rsv;
-          if (ea.cs) val *= ea.cs[(int64_t)g * ea.scs + n];
-          if (ea.d_trans)
+        for (int j = 0; j < C::HALF; ++j) {
+          const int n = nb0 + j;
+          if (n < ea.N) {
+            float val = acc[j] * rsv;
+            if (ea.cs) val *= ea.cs[(int64_t)g * ea.scs + n];
             Dg[(int64_t)n * ea.ldd + m] = val;
-          else
-            Dg[(int64_t)m * ea.ldd + n] = val;
+          }
+        }
+      }
+    } else {
+      // pitch HALF + 4: float4 writes of 8 lanes per phase hit disjoint banks
+      constexpr int LDS = C::HALF + 4;
+      float* st = reinterpret_cast<float*>(base) + warp * 32 * LDS;
+#pragma unroll
+      for (int j = 0; j < C::HALF; j += 4)
+        *reinterpret_cast<float4*>(st + lane * LDS + j) =
+            make_float4(acc[j] * rsv, acc[j + 1] * rsv, acc[j + 2] * rsv, acc[j + 3] * rsv);
+      __syncwarp();
+      const int mrows = min(32, ea.M - (m0 + q * 32));
+      const bool vec = ((ea.ldd & 3) == 0) && ((reinterpret_cast<uintptr_t>(Dg) & 15) == 0);
+      constexpr int CW = C::HALF < 128 ? C::HALF : 128;   // columns per warp instruction
+      for (int r = 0; r < mrows; ++r) {
+        float* drow = Dg + (int64_t)(m0 + q * 32 + r) * ea.ldd;
+#pragma unroll
+        for (int c = 0; c < C::HALF; c += CW) {
+          const int cl = c + 4 * lane;
+          if (cl >= C::HALF) continue;
+          const int n = nb0 + cl;
+          float4 v = *reinterpret_cast<const float4*>(st + r * LDS + cl);
+          if (ea.cs) {
+            const float* csg = ea.cs + (int64_t)g * ea.scs;
+            if (n < ea.N) v.x *= csg[n];
+            if (n + 1 < ea.N) v.y *= csg[n + 1];
+            if (n + 2 < ea.N) v.z *= csg[n + 2];
+            if (n + 3 < ea.N) v.w *= csg[n + 3];
+          }
+          if (vec && n + 3 < ea.N) {
+            *reinterpret_cast<float4*>(drow + n) = v;
+          } else {
+            if (n < ea.N) drow[n] = v.x;
+            if (n + 1 < ea.N) drow[n + 1] = v.y;
+            if (n + 2 < ea.N) drow[n + 2] = v.z;
+            if (n + 3 < ea.N) drow[n + 3] = v.w;
+          }
         }
       }
     }
