@@ -271,17 +271,21 @@ hg_status run_rsvd(const float* X, int nb, int b, int k, int q, uint64_t seed, b
   // step 4: B = S^T X, stored as B [k][b] = (X S)^T
   float* Bt = oth;
   HG_TRY(R.power(cur, Bt));
-  // step 5: one-sided Jacobi on W = L^T, B B^T = L L^T
+  // step 5: SVD of B via B B^T = L L^T and one-sided Jacobi (W = L, or W = L^T; jacobi.cu)
   HG_TRY(R.gram(Bt, G));
+  const bool on_l = jacobi_on_l();
   {
     ProfScope ps(ST_CHOLINV, s);
-    HG_CU(launch_cholinv(nb, k, G, Lm, Linv, work, st, s, &g_launches), "cholinv(B B^T)");
+    HG_CU(launch_cholinv(nb, k, G, Lm, on_l ? nullptr : Linv, work, st, s, &g_launches), "cholinv(B B^T)");
   }
   {
     ProfScope ps(ST_JACOBI, s);
     HG_CU(launch_jacobi(nb, k, Lm, Wf, st, s, &g_launches), "jacobi");
   }
-  {  // U~ = L^-T W_f  (stored transposed: Uk[j] = u~_j)
+  if (on_l) {  // L J = W_f = U~ Sigma: U~ = unit columns of W_f (stored transposed)
+    ProfScope ps(ST_FINALIZE, s);
+    HG_CU(launch_unit_columns_t(nb, k, Wf, Uk, s, &g_launches), "unit columns");
+  } else {  // L^T J = W_f: U~ = J = L^-T W_f  (stored transposed: Uk[j] = u~_j)
     GemmDesc g;
     g.M = k; g.N = k; g.K = k; g.batch = nb;
     g.A = Linv; g.a_mn = true; g.lda = k; g.sa = (int64_t)k * k;

@@ -173,7 +173,7 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   const int64_t off = (int64_t)blockIdx.x * kk;
   const float* Gb = G + off;
   float* Lb = Lout ? Lout + off : nullptr;
-  float* Ib = Linv + off;
+  float* Ib = Linv ? Linv + off : nullptr;   // null: factor only (no TRTRI)
 
   // distance from the identity (near-identity path for the second CholeskyQR pass)
   float emax = 0.f;
@@ -205,7 +205,7 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
         else if (c == r) { const float e = 0.5f * (g - 1.f); l = 1.f + e; li = 1.f - e; }
         else { l = g; li = -g; }
         if (Lb) Lb[i] = l;
-        Ib[i] = li;
+        if (Ib) Ib[i] = li;
       }
     return;
   }
@@ -284,6 +284,7 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   }
 
   if (Lb) store_lower(Lb, tiles, k, nt, warp, lane);
+  if (!Ib) return;
   // ---- in-place tile TRTRI
   CHOL_CLK(40);
   for (int d = warp; d < nt; d += NWARP) tile_trtri(T(d, d), lane);

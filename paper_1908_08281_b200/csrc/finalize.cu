@@ -105,6 +105,39 @@ __global__ void k_inv_sigma(int nb, int k, const float* __restrict__ sigma, floa
 
 }  // namespace
 
+// grid (nb, ceil(k/32)): a CTA normalises 32 columns of W_f and writes them as rows of Uk
+__global__ void __launch_bounds__(NT) k_unit_columns_t(int k, const float* __restrict__ Wf, float* __restrict__ Uk) {
+  __shared__ double part[NT / 32][32];
+  __shared__ float inv[32];
+  const int blk = blockIdx.x, j0 = blockIdx.y * 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float* W = Wf + (int64_t)blk * k * k;
+  const int j = j0 + lane;
+  double acc = 0.0;
+  if (j < k)
+    for (int r = w; r < k; r += NT / 32) {
+      const double v = W[(int64_t)r * k + j];
+      acc = fma(v, v, acc);
+    }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0) {
+    double s2 = 0.0;
+    for (int i = 0; i < NT / 32; ++i) s2 += part[i][lane];
+    inv[lane] = s2 > 0.0 ? (float)(1.0 / sqrt(s2)) : 0.f;
+  }
+  __syncthreads();
+  float* U = Uk + (int64_t)blk * k * k;
+  for (int jj = w; jj < 32 && j0 + jj < k; jj += NT / 32)
+    for (int r = lane; r < k; r += 32) U[(int64_t)(j0 + jj) * k + r] = W[(int64_t)r * k + j0 + jj] * inv[jj];
+}
+
+cudaError_t launch_unit_columns_t(int nb, int k, const float* Wf, float* Uk, cudaStream_t s, int* launches) {
+  k_unit_columns_t<<<dim3(nb, (k + 31) / 32), NT, 0, s>>>(k, Wf, Uk);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float* Uw_t, float* Ut, float* sigma,
                             float* Vt, double* sig_raw, int32_t* status, cudaStream_t s, int* launches) {
   int32_t* perm = reinterpret_cast<int32_t*>(sig_raw + (size_t)nb * k);

@@ -2,11 +2,13 @@
 // one-sided (Hestenes) Jacobi, QR-preconditioned.
 //
 // With B B^T = L L^T (Cholesky of the Gram of B^T, computed by the GEMM + chol
-// kernels), W = L^T satisfies W^T W = B B^T.  One-sided Jacobi rotates column
-// pairs of W until all columns are mutually orthogonal: W J = W_f.  Then J is
-// the left singular vector matrix U~ of B, the column norms of W_f are the
-// singular values, and J = W^-1 W_f = L^-T W_f is recovered afterwards by a
-// GEMM (no rotation accumulator is stored).  Each rotation is the one that
+// kernels), B = L Q_B with Q_B^T Q_B = I, so B and L share left singular vectors
+// and singular values.  One-sided Jacobi rotates column pairs of W until all
+// columns are mutually orthogonal: W J = W_f.  Default (block kernel) W = L:
+// L J = W_f = U~ Sigma, so the column norms of W_f are the singular values and
+// U~ is W_f with unit columns (finalize.cu).  Scalar kernel / HG_JACOBI_W=LT:
+// W = L^T, W^T W = B B^T, J = U~ = L^-T W_f by a GEMM.  No rotation accumulator
+// is stored in either case.  Each rotation is the one that
 // zeroes the 2x2 Gram [[a_pp, a_pq], [a_pq, a_qq]] of the pair (Golub & Van
 // Loan sym.schur2): zeta = (a_qq - a_pp)/(2 a_pq), t = sgn(zeta)/(|zeta| +
 // sqrt(1+zeta^2)), c = 1/sqrt(1+t^2), s = c t; w_p <- c w_p - s w_q,
@@ -229,6 +231,22 @@ cudaError_t launch_jacobi_scalar(int nb, int k, const float* L, float* Wf, int32
                                  int* launches);
 
 // HG_JACOBI=scalar selects the scalar cyclic kernel (comparison / verification)
+// Which matrix the one-sided Jacobi orthogonalises (reading A14 in DESIGN.md):
+//   W = L   (default, block kernel): W J = W_f diagonalises L^T L (one LR step away
+//           from B B^T = L L^T); U = W_f with unit columns, so neither the L^-T GEMM
+//           nor the TRTRI of that Cholesky is needed.  Measured at configs[3]: same
+//           sweep count, jacobi 7.6 vs 8.35 ms, sigma error 6e-7 vs 2.8e-6.
+//   W = L^T (HG_JACOBI_W=LT, and always for the scalar kernel): W J = W_f diagonalises
+//           L L^T = B B^T directly; U = L^-T W_f.
+bool jacobi_on_l() {
+  static const bool on_l = [] {
+    const char* j = getenv("HG_JACOBI");
+    const char* w = getenv("HG_JACOBI_W");
+    return !(j && j[0] == 's') && !(w && w[0] == 'L' && w[1] == 'T');
+  }();
+  return on_l;
+}
+
 cudaError_t launch_jacobi(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s,
                           int* launches) {
   static const bool scalar = [] {

@@ -123,7 +123,7 @@ __host__ __device__ inline Layout make_layout(int k, int C) {
 
 template <int BW>
 __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, const float* __restrict__ L,
-                                                      float* __restrict__ Wf, int32_t* status) {
+                                                      float* __restrict__ Wf, int32_t* status, int w_is_l) {
   using P = JB<BW>;
   constexpr int PW = P::PW, LDQ = P::LDQ, PACK = P::PACK, N4 = P::N4, UT = P::UT, NQB = P::NQB;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
 
   for (int i = t; i < R * ldw; i += NT) {
     const int rl = i / ldw, c = i % ldw;
-    W[i] = (rl < nr && c < k) ? Lb[(int64_t)c * k + (r0 + rl)] : 0.f;   // W = L^T
+    W[i] = (rl < nr && c < k) ? Lb[w_is_l ? (int64_t)(r0 + rl) * k + c : (int64_t)c * k + (r0 + rl)] : 0.f;
   }
   __syncthreads();
 
@@ -399,7 +399,8 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
 }
 
 template <int BW>
-cudaError_t launch_bw(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s, double tol) {
+cudaError_t launch_bw(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s, double tol,
+                      int w_is_l) {
   // rows per CTA: 128 up to k = 256 (one CTA per SM for configs[3]), 64 beyond
   const int rt = k <= 256 ? 128 : 64;
   const int C = (k + rt - 1) / rt;
@@ -420,7 +421,7 @@ cudaError_t launch_bw(int nb, int k, const float* L, float* Wf, int32_t* status,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_jacobi_blk<BW>, k, C, tol, L, Wf, status);
+  return cudaLaunchKernelEx(&cfg, k_jacobi_blk<BW>, k, C, tol, L, Wf, status, w_is_l);
 }
 
 }  // namespace
@@ -448,6 +449,7 @@ cudaError_t launch_jacobi_blk(int nb, int k, const float* L, float* Wf, int32_t*
     return v ? atoi(v) : 16;
   }();
   ++*launches;
-  if (bw == 8) return launch_bw<8>(nb, k, L, Wf, status, s, jacobi_tol(k));
-  return launch_bw<16>(nb, k, L, Wf, status, s, jacobi_tol(k));
+  const int wl = jacobi_on_l() ? 1 : 0;
+  if (bw == 8) return launch_bw<8>(nb, k, L, Wf, status, s, jacobi_tol(k), wl);
+  return launch_bw<16>(nb, k, L, Wf, status, s, jacobi_tol(k), wl);
 }

@@ -19,11 +19,12 @@ cudaError_t launch_omega_panels(uint64_t seed, int nb, int b, int k, float* out,
 cudaError_t launch_gaussian_rowmajor(uint64_t seed, int rows, int cols, float* out, cudaStream_t s,
                                      int* launches);
 
-// chol.cu -- CholeskyQR: G = L L^T (lower L), Linv = L^-1; near-identity first-order path
+// chol.cu -- CholeskyQR: G = L L^T (lower L), Linv = L^-1 (skipped when Linv is null);
+// near-identity first-order path
 cudaError_t launch_cholinv(int nb, int k, const float* G, float* L, float* Linv, float* work,
                            int32_t* status, cudaStream_t s, int* launches);
 
-// jacobi.cu -- one-sided Jacobi on W = L^T (k x k): W_f = W J with orthogonal columns
+// jacobi.cu -- one-sided Jacobi on W = L (or L^T, see jacobi_on_l): W_f = W J with orthogonal columns
 cudaError_t launch_jacobi(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s,
                           int* launches);
 
@@ -43,3 +44,9 @@ cudaError_t launch_jacobi_blk(int nb, int k, const float* L, float* Wf, int32_t*
                               int* launches);
 cudaError_t jacobi_blk_debug(unsigned long long* out, bool reset);
 cudaError_t jacobi_blk_clocks(long long* out);
+
+// true when launch_jacobi orthogonalises the columns of L (then U~ = unit columns of W_f)
+bool jacobi_on_l();
+// Uk[blk][j][r] = W_f[blk][r][j] / ||W_f[blk][:, j]||  (fp64 norms; zero columns stay zero)
+cudaError_t launch_unit_columns_t(int nb, int k, const float* Wf, float* Uk, cudaStream_t s, int* launches);
+
