@@ -26,19 +26,16 @@
 
 namespace {
 
-constexpr int NT = 512;
+constexpr int NT = 512;   // 4 owner warps per owned pair (nown <= 4)
 constexpr int MAX_SWEEPS = 40;
 constexpr size_t SMEM_CAP = 220 * 1024;
 
 __device__ unsigned long long g_jb_dbg[3];   // [0] max sweeps, [1] total sweeps, [2] blocks
-__device__ long long g_jb_clk[16];           // block 0 / rank 0 / thread 0: sweep 1, outer rounds 0-3
-#define JB_CLK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0 && sweep == 1 && ro < 4) g_jb_clk[(i) + 4 * ro] = clock64(); } while (0)
+__device__ long long g_jb_clk[16];           // block 0 / rank 0 / thread 0: sweep 1, outer rounds 0-1
+#define JB_CLK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0 && sweep == 1 && ro < 2) g_jb_clk[(i) + 8 * ro] = clock64(); } while (0)
 
 __device__ __forceinline__ void cluster_barrier_jb() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void group_bar(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // round-robin tournament on n players (n even): round r, pair i
@@ -84,8 +81,248 @@ struct JB {
   __host__ __device__ static int pk(int a, int b) { return a * PW - (a * (a - 1)) / 2 + (b - a); }   // a <= b
 };
 
+// Q layout in shared memory (pitch LDQ): element (a, j) at a * LDQ + (j ^ qsw(a)).  The
+// XOR stays inside aligned groups of 4 (float4 rows stay float4 rows, permuted) and
+// makes the lane-per-row column accesses of the inner rounds bank-conflict free.
+__device__ __forceinline__ int qsw(int a) { return (a >> 3) & 3; }
+
+// Rotation of the 2x2 Gram [[app, apq], [apq, aqq]] (Golub & Van Loan sym.schur2) with
+// an approximate angle from fast fp32 intrinsics (any angle near the optimum still
+// annihilates a_pq to first order); (c, s) orthogonal to fp32 rounding: c = (1+t^2)^-1/2
+// from rsqrtf refined by one fp64 Newton step.  Returns the new diagonal entries.
+__device__ __forceinline__ void jrot(double app, double aqq, double apq, float& c, float& s, double& dp, double& dq) {
+  const float zeta = __fdividef((float)(aqq - app), (float)(2.0 * apq));
+  const float az = fabsf(zeta);
+  const float tf = copysignf(__fdividef(1.0f, az + sqrtf(fmaf(az, az, 1.0f))), zeta);
+  const double td = tf;
+  const double xx = fma(td, td, 1.0);
+  double cd = (double)rsqrtf((float)xx);
+  cd = cd * fma(-0.5 * xx * cd, cd, 1.5);
+  c = (float)cd;
+  s = (float)(cd * td);
+  const double c2 = (double)c, s2 = (double)s;
+  const double x = 2.0 * c2 * s2 * apq;
+  dp = c2 * c2 * app - x + s2 * s2 * aqq;     // G'[p][p] = c^2 a_pp - 2cs a_pq + s^2 a_qq
+  dq = s2 * s2 * app + x + c2 * c2 * aqq;     // G'[q][q] = s^2 a_pp + 2cs a_pq + c^2 a_qq
+}
+
+// Diagonal-round inner sweep: the pairs inside one column block (columns base ..
+// base + BW - 1 of the PW x PW problem) never touch the other block, so each block is
+// an independent BW x BW problem, solved by one warp (lane = row, lanes >= BW idle).
+// Round-robin by the circle method: slot 0 holds column 0, slot s >= 1 holds column
+// 1 + (s - 1 + r) % (BW - 1), pairs are slots (i, BW - 1 - i); after each round slots
+// 1..BW-1 rotate by one, so register indices are compile-time constants inside the
+// runtime round loop.  G <- J^T G J (columns lane-locally with (c, s) broadcast through
+// shared memory, rows by shuffles), Q <- Q J on the block's columns.  Q rows of the
+// block are (re)initialised here to the identity over all PW columns.
+template <int BW>
+__device__ __forceinline__ int diag_col(int s, int r) { return s == 0 ? 0 : 1 + (s - 1 + r) % (BW - 1); }
+
+template <int BW>
+__device__ int inner_sweep_diag(const double* G, float* Q, int base, double tol2, double2* cs, int lane) {
+  constexpr int PW = 2 * BW, LDQ = JB<BW>::LDQ;
+  const bool act = lane < BW;
+  const int row = base + (act ? lane : 0);
+  const int sw = qsw(row);
+  float* qrow = Q + row * LDQ;
+  double g[BW];
+#pragma unroll
+  for (int j = 0; j < BW; ++j) g[j] = act ? G[row * LDQ + base + j] : 0.0;   // round 0: slot j = column j
+  if (act) {
+#pragma unroll
+    for (int j = 0; j < PW; ++j) qrow[j ^ sw] = (j == row) ? 1.f : 0.f;
+  }
+  double d = act ? G[row * LDQ + row] : 1.0;
+  {  // no pair of the block above the threshold: nothing can rotate, skip
+    int need = 0;
+#pragma unroll
+    for (int j = 0; j < BW; ++j) {
+      const double dj = __shfl_sync(0xffffffffu, d, j);
+      need |= act && j != lane && g[j] * g[j] > tol2 * d * dj;
+    }
+    if (__ballot_sync(0xffffffffu, need) == 0u) return 0;
+  }
+  int rot_any = 0;
+#pragma unroll 1
+  for (int r = 0; r < BW - 1; ++r) {
+    int pa = lane, pj = 0, pslot = 0;
+    bool first = false;
+    if (act) {
+      const int sl = lane == 0 ? 0 : 1 + ((lane - 1 - r) % (BW - 1) + (BW - 1)) % (BW - 1);
+      const int ps = BW - 1 - sl;
+      pa = diag_col<BW>(ps, r);
+      first = sl < ps;
+      pj = min(sl, ps);
+      pslot = ps;
+    }
+    double apq = 0.0;   // G[lane][pa] = g[pslot]
+#pragma unroll
+    for (int j = 0; j < BW; ++j) apq = (j == pslot) ? g[j] : apq;
+    const double aqq = __shfl_sync(0xffffffffu, d, pa);
+    float c = 1.f, s = 0.f;
+    double dp = d, dq = aqq;
+    if (first && apq * apq > tol2 * d * aqq) jrot(d, aqq, apq, c, s, dp, dq);
+    const float c_o = __shfl_sync(0xffffffffu, c, pa);
+    const float s_o = __shfl_sync(0xffffffffu, s, pa);
+    const double dq_o = __shfl_sync(0xffffffffu, dq, pa);
+    if (first) d = dp;
+    else if (act) { c = c_o; s = s_o; d = dq_o; }
+    if (__ballot_sync(0xffffffffu, first && s != 0.f) != 0u) {
+      rot_any = 1;
+      if (first) cs[pj] = make_double2((double)c, (double)s);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < BW / 2; ++i) {   // columns: slots (i, BW - 1 - i)
+        const double2 v = cs[i];
+        const double gp = g[i], gq = g[BW - 1 - i];
+        g[i] = fma(v.x, gp, -v.y * gq);
+        g[BW - 1 - i] = fma(v.y, gp, v.x * gq);
+        if (act) {
+          const int cp = base + diag_col<BW>(i, r), cq = base + diag_col<BW>(BW - 1 - i, r);
+          const float cf = (float)v.x, sf = (float)v.y;
+          const float qp = qrow[cp ^ sw], qq = qrow[cq ^ sw];
+          qrow[cp ^ sw] = fmaf(cf, qp, -sf * qq);
+          qrow[cq ^ sw] = fmaf(sf, qp, cf * qq);
+        }
+      }
+      const double cd = c, sd = first ? -(double)s : (double)s;   // rows
+#pragma unroll
+      for (int j = 0; j < BW; ++j) {
+        const double o = __shfl_sync(0xffffffffu, g[j], pa);
+        g[j] = fma(sd, o, cd * g[j]);
+      }
+      __syncwarp();   // cs is rewritten next round
+    }
+    const double t0 = g[1];   // advance the slot assignment to round r + 1
+#pragma unroll
+    for (int j = 1; j < BW - 1; ++j) g[j] = g[j + 1];
+    g[BW - 1] = t0;
+  }
+  return rot_any;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// named barrier that also ORs a predicate over the participating threads
+__device__ __forceinline__ int named_bar_or(int id, int n, int pred) {
+  int out;
+  asm volatile(
+      "{\n\t.reg .pred pi, po;\n\tsetp.ne.s32 pi, %1, 0;\n\tbar.red.or.pred po, %2, %3, pi;\n\tselp.s32 %0, 1, 0, po;\n\t}"
+      : "=r"(out)
+      : "r"(pred), "r"(id), "r"(n)
+      : "memory");
+  return out;
+}
+
+// Cross rounds of the inner sweep (BW rounds, pairs (j, BW + (j + r) % BW)) by the
+// four warps h = 0..3 of an owner group (128 threads, named barrier bar_id).  Warp h
+// holds register slots j and BW + j for j in [h QW, (h+1) QW) of every row (lane =
+// row).  Register slots, not columns, are paired, so that register indices are
+// compile-time constants inside the runtime round loop: slot j (< BW) holds column j,
+// slot BW + j holds column BW + (j + r) % BW, pairs are slots (j, BW + j) = columns
+// (j, BW + (j + r) % BW).  After each round the J-half slots rotate by one, passing one
+// value per thread to the neighbouring warp through xch.
+// Per round: the warp holding slot BW + a computes the angle of pair (a, .) from the
+// shared diagonal dsm and its own register a_pq, writes (c, s) to cs and the new
+// diagonal to dsm; barrier (OR-reduces "anything rotated"); every warp rotates its
+// column pairs (G and Q) and, by shuffles, its part of every row; barrier; slot
+// rotation.  Rotation arithmetic: jrot.
+template <int BW>
+__device__ int inner_sweep_cross4(const double* G, float* Q, double tol2, double2* cs, double* dsm, double* xch,
+                                  int lane, int h, int bar_id) {
+  constexpr int PW = 2 * BW, LDQ = JB<BW>::LDQ, QW = BW / 4;
+  const int j0 = h * QW;
+  const bool act = lane < PW;
+  const int sw = qsw(lane);
+  float* qrow = Q + (act ? lane : 0) * LDQ;
+  double gI[QW], gJ[QW];
+#pragma unroll
+  for (int i = 0; i < QW; ++i) {
+    gI[i] = act ? G[lane * LDQ + j0 + i] : 0.0;
+    gJ[i] = act ? G[lane * LDQ + BW + j0 + i] : 0.0;
+    if (act) {
+      qrow[(j0 + i) ^ sw] = (lane == j0 + i) ? 1.f : 0.f;
+      qrow[(BW + j0 + i) ^ sw] = (lane == BW + j0 + i) ? 1.f : 0.f;
+    }
+  }
+  if (h == 0 && act) dsm[lane] = G[lane * LDQ + lane];
+  named_bar(bar_id, 128);
+  // no cross entry above the threshold: no round can rotate (G never changes), skip
+  int need = 0;
+  if (lane < BW) {
+    const double da = dsm[lane];
+#pragma unroll
+    for (int i = 0; i < QW; ++i) need |= gJ[i] * gJ[i] > tol2 * da * dsm[BW + j0 + i];
+  }
+  if (!named_bar_or(bar_id, 128, need)) return 0;
+  int rot_any = 0;
+  const bool prow = lane < BW && (lane / QW) == h;   // this lane computes the angle of pair `lane`
+#pragma unroll 1
+  for (int r = 0; r < BW; ++r) {
+    int rot = 0;
+    if (prow) {
+      const int pa = BW + (lane + r) % BW;
+      double apq = gJ[0];   // slot BW + lane = gJ[lane - j0]
+#pragma unroll
+      for (int i = 1; i < QW; ++i) apq = (lane - j0 == i) ? gJ[i] : apq;
+      const double app = dsm[lane], aqq = dsm[pa];
+      float c = 1.f, s = 0.f;
+      if (apq * apq > tol2 * app * aqq) {
+        double dp, dq;
+        jrot(app, aqq, apq, c, s, dp, dq);
+        dsm[lane] = dp;
+        dsm[pa] = dq;
+        rot = s != 0.f;
+      }
+      cs[lane] = make_double2((double)c, (double)s);
+    }
+    if (named_bar_or(bar_id, 128, rot)) {
+      rot_any = 1;
+#pragma unroll
+      for (int i = 0; i < QW; ++i) {   // columns: slot pair (j, BW + j), columns (j, BW + (j + r) % BW)
+        const int j = j0 + i;
+        const double2 v = cs[j];
+        const double gp = gI[i], gq = gJ[i];
+        gI[i] = fma(v.x, gp, -v.y * gq);
+        gJ[i] = fma(v.y, gp, v.x * gq);
+        if (PW == 32 || act) {
+          const int cq = BW + (j + r) % BW;
+          const float cf = (float)v.x, sf = (float)v.y;
+          const float qp = qrow[j ^ sw], qq = qrow[cq ^ sw];
+          qrow[j ^ sw] = fmaf(cf, qp, -sf * qq);
+          qrow[cq ^ sw] = fmaf(sf, qp, cf * qq);
+        }
+      }
+      int pa = lane, pj = 0;   // rows: row_p' = c row_p - s row_q ; row_q' = s row_p + c row_q
+      bool first = false;
+      if (lane < BW) { pa = BW + (lane + r) % BW; pj = lane; first = true; }
+      else if (act) { pa = ((lane - BW - r) % BW + BW) % BW; pj = pa; }
+      const double2 v = cs[pj];
+      const double cd = act ? v.x : 1.0, sd = act ? (first ? -v.y : v.y) : 0.0;
+#pragma unroll
+      for (int i = 0; i < QW; ++i) {
+        const double oI = __shfl_sync(0xffffffffu, gI[i], pa);
+        const double oJ = __shfl_sync(0xffffffffu, gJ[i], pa);
+        gI[i] = fma(sd, oI, cd * gI[i]);
+        gJ[i] = fma(sd, oJ, cd * gJ[i]);
+      }
+    }
+    // slot rotation: new slot BW + j = old slot BW + j + 1 (wrapping inside the J half)
+    xch[h * 32 + lane] = gJ[0];
+    named_bar(bar_id, 128);
+    const double nxt = xch[((h + 1) & 3) * 32 + lane];
+#pragma unroll
+    for (int i = 0; i < QW - 1; ++i) gJ[i] = gJ[i + 1];
+    gJ[QW - 1] = nxt;
+  }
+  return rot_any;
+}
+
+// per-owned-pair scratch (doubles): cs (c, s) [BW x 2] | diagonal [PW] | xch [4 x 32]
+template <int BW>
+__host__ __device__ constexpr int jscr() { return 2 * BW + 2 * BW + 4 * 32; }
+
 struct Layout {
-  int K2, nblk, Pb, R, nch, rch, ldw, nown, gs;
+  int K2, nblk, Pb, R, nch, rch, ldw, nown;
   size_t offW, offGp, offG, offQ, offQb, offJ, offF, total;
 };
 
@@ -99,9 +336,6 @@ __host__ __device__ inline Layout make_layout(int k, int C) {
   L.R = ((k + C - 1) / C + 3) / 4 * 4;
   L.ldw = L.K2 + 4;
   L.nown = (L.Pb + C - 1) / C;
-  int np2 = 1;
-  while (np2 < L.nown) np2 <<= 1;
-  L.gs = NT / np2;                                   // threads per owned pair
   // partial Grams over row chunks of 32 (more Gram tasks); one chunk if shared memory is short
   for (int pass = 0; pass < 2; ++pass) {
     L.rch = pass == 0 ? 32 : L.R;
@@ -113,7 +347,7 @@ __host__ __device__ inline Layout make_layout(int k, int C) {
     L.offG = take((size_t)L.nown * P::PW * P::LDQ * 8);   // fp64 inner Gram
     L.offQ = take((size_t)L.nown * P::PW * P::LDQ * 4);
     L.offQb = take((size_t)P::NQB * P::PW * P::LDQ * 4);
-    L.offJ = take((size_t)P::MAXOWN * P::PW * 16);
+    L.offJ = take((size_t)L.nown * jscr<BW>() * 8);          // inner-round scratch per owned pair
     L.offF = take((size_t)128 * 4);
     L.total = off;
     if (L.total <= SMEM_CAP) break;
@@ -132,7 +366,6 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
   if (C > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int blk = blockIdx.x / C;
   const int nblk = Lo.nblk, Pb = Lo.Pb, R = Lo.R, ldw = Lo.ldw, nown = Lo.nown, nch = Lo.nch, rch = Lo.rch;
-  const int GS = Lo.gs;
   const int r0 = rank * R;
   const int nr = max(0, min(R, k - r0));
   float* W = reinterpret_cast<float*>(smem_raw + Lo.offW);
@@ -140,10 +373,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
   double* Gw = reinterpret_cast<double*>(smem_raw + Lo.offG);    // [nown][PW][LDQ]
   float* Qw = reinterpret_cast<float*>(smem_raw + Lo.offQ);      // [nown][PW][LDQ]
   float* Qb = reinterpret_cast<float*>(smem_raw + Lo.offQb);     // [NQB][PW][LDQ]
-  int* Jp = reinterpret_cast<int*>(smem_raw + Lo.offJ);          // [MAXOWN][PW] partner
-  float* Jd = reinterpret_cast<float*>(Jp + P::MAXOWN * PW);     // [MAXOWN][PW] J[a][a]
-  float* Jo = Jd + P::MAXOWN * PW;                               // [MAXOWN][PW] J[partner][a]
-  int* Jact = reinterpret_cast<int*>(Jo + P::MAXOWN * PW);       // [MAXOWN]
+  double* JS = reinterpret_cast<double*>(smem_raw + Lo.offJ);    // [nown][JSCR]: cs | dsm | xch
   int* flag = reinterpret_cast<int*>(smem_raw + Lo.offF);        // [Pb] rotated-this-round
   const int t = threadIdx.x;
   const double tol2 = tol * tol;
@@ -204,99 +434,41 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
       if (C > 1) cluster_barrier_jb(); else __syncthreads();
       JB_CLK(1);
 
-      // ---- 2. owners: sum partials, rotate on the PW x PW Gram, accumulate Q
-      const int gi = t / GS, tg = t % GS;
-      if (gi < nown) {
+      // ---- 2. owners: sum partials into the fp64 PW x PW Gram (all threads), then one
+      //         4 warps per owned pair run the inner sweep in registers (inner_sweep_cross4;
+      //         diagonal round: inner_sweep_diag on blocks I and J)
+      for (int e = t; e < nown * PW * PW; e += NT) {
+        const int gi = e / (PW * PW), ab = e % (PW * PW), a = ab / PW, b = ab % PW;
+        if (gi * C + rank >= Pb) continue;
+        const int lo = min(a, b), hi = max(a, b);
+        double sum = 0.0;
+        for (int c = 0; c < C; ++c)
+          for (int ch = 0; ch < nch; ++ch) sum += Gp[(((size_t)c * nch + ch) * nown + gi) * PACK + P::pk(lo, hi)];
+        Gw[(size_t)gi * PW * LDQ + a * LDQ + b] = sum;
+      }
+      __syncthreads();
+      JB_CLK(2);
+      {
+        const int warp = t >> 5, lane = t & 31;
+        const int gi = warp >> 2, h = warp & 3;   // owner group of 4 warps per owned pair
         const int g = gi * C + rank;
-        if (g < Pb) {
-          double* G = Gw + (size_t)gi * PW * LDQ;
-          float* Q = Qw + (size_t)gi * PW * LDQ;
-          int* jp = Jp + gi * PW;
-          float* jd = Jd + gi * PW;
-          float* jo = Jo + gi * PW;
-          const int bar_id = 1 + gi;
-          for (int e = tg; e < PW * PW; e += GS) {
-            const int a = e / PW, b = e % PW;
-            const int lo = min(a, b), hi = max(a, b);
-            double s = 0.0;
-            for (int c = 0; c < C; ++c)
-              for (int ch = 0; ch < nch; ++ch) s += Gp[(((size_t)c * nch + ch) * nown + gi) * PACK + P::pk(lo, hi)];
-            G[a * LDQ + b] = s;
-            Q[a * LDQ + b] = (a == b) ? 1.f : 0.f;
-          }
+        if (gi < nown && g < Pb) {
+          double* js = JS + (size_t)gi * jscr<BW>();
+          double2* cs = reinterpret_cast<double2*>(js);
           int rot_any = 0;
-          const int nin = diag ? BW - 1 : BW;
-          // thread tg owns column b = tg % PW, rows a = tg / PW + (GS / PW) u
-          const int bq = tg % PW, a0 = tg / PW, astep = GS / PW;
-          const int nu = PW / astep;                    // entries per thread
-          if (tg == 0) Jact[gi] = 0;
-          group_bar(bar_id, GS);
-          for (int ri = 0; ri < nin; ++ri) {
-            if (tg < BW) {
-              int p, q;
-              if (diag) {
-                const int h = BW / 2;
-                if (tg < h) { tourn(ri, tg, BW, p, q); }
-                else { tourn(ri, tg - h, BW, p, q); p += BW; q += BW; }
-              } else {
-                p = tg;
-                q = BW + ((tg + ri) % BW);
-              }
-              const double app = G[p * LDQ + p], aqq = G[q * LDQ + q], apq = G[p * LDQ + q];
-              float c = 1.f, s = 0.f;
-              if (apq * apq > tol2 * app * aqq) {
-                // approximate angle (fast fp32 intrinsics: any angle near the optimum still
-                // annihilates a_pq to first order); (c, s) orthogonal to fp32 rounding:
-                // c = (1+t^2)^-1/2 from rsqrtf refined by one fp64 Newton step
-                const float zeta = __fdividef((float)(aqq - app), (float)(2.0 * apq));
-                const float az = fabsf(zeta);   // zeta = 0 -> t = 1; huge zeta -> t = 0
-                const float tf = copysignf(__fdividef(1.0f, az + sqrtf(fmaf(az, az, 1.0f))), zeta);
-                const double td = tf;
-                const double xx = fma(td, td, 1.0);
-                double cd = (double)rsqrtf((float)xx);
-                cd = cd * fma(-0.5 * xx * cd, cd, 1.5);
-                c = (float)cd;
-                s = (float)(cd * td);
-                Jact[gi] = ri + 1;   // never reset: "== ri + 1" means this round rotates
-              }
-              // col_p' = c col_p - s col_q ; col_q' = s col_p + c col_q
-              jp[p] = q; jd[p] = c; jo[p] = -s;
-              jp[q] = p; jd[q] = c; jo[q] = s;
-            }
-            group_bar(bar_id, GS);
-            if (Jact[gi] != ri + 1) continue;   // no pair of this inner round rotates
-            rot_any = 1;
-            double gn[8];
-            float qn[8];
-            const int pb = jp[bq];
-            const double db = jd[bq], ob = jo[bq];
-            const bool bact = ob != 0.0;
-            unsigned touched = 0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              if (u >= nu) break;
-              const int a = a0 + astep * u;
-              const int pa = jp[a];
-              const double da = jd[a], oa = jo[a];
-              if (!bact && oa == 0.0) continue;   // neither row nor column rotates: unchanged
-              touched |= 1u << u;
-              // G' = J^T G J : G'[a][b] = sum_{x in {a,pa}, y in {b,pb}} J[x][a] G[x][y] J[y][b]
-              gn[u] = da * (db * G[a * LDQ + bq] + ob * G[a * LDQ + pb]) +
-                      oa * (db * G[pa * LDQ + bq] + ob * G[pa * LDQ + pb]);
-              // Q' = Q J : Q'[a][b] = Q[a][b] J[b][b] + Q[a][pb] J[pb][b]
-              qn[u] = bact ? (float)db * Q[a * LDQ + bq] + (float)ob * Q[a * LDQ + pb] : Q[a * LDQ + bq];
-            }
-            group_bar(bar_id, GS);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              if (u >= nu) break;
-              if (!(touched >> u & 1)) continue;
-              G[(a0 + astep * u) * LDQ + bq] = gn[u];
-              Q[(a0 + astep * u) * LDQ + bq] = qn[u];
-            }
-            group_bar(bar_id, GS);
+          if (!diag) {
+            rot_any = inner_sweep_cross4<BW>(Gw + (size_t)gi * PW * LDQ, Qw + (size_t)gi * PW * LDQ, tol2, cs,
+                                             js + 2 * BW, js + 2 * BW + PW, lane, h, 1 + gi);
+          } else if (h < 2) {   // diagonal round: block I by warp 0, block J by warp 1
+            int* rflag = reinterpret_cast<int*>(js + 2 * BW + PW);
+            const int rh = inner_sweep_diag<BW>(Gw + (size_t)gi * PW * LDQ, Qw + (size_t)gi * PW * LDQ, h * BW, tol2,
+                                                cs + h * (BW / 2), lane);
+            if (lane == 0) rflag[h] = rh;
+            named_bar(1 + gi, 64);
+            rot_any = rflag[0] | rflag[1];
           }
-          if (tg == 0) {
+          JB_CLK(3);
+          if (h == 0 && lane == 0) {
             for (int cr = 0; cr < C; ++cr) {
               if (cr == rank) flag[g] = rot_any;
               else st_cluster_s32(flag + g, cr, rot_any);
@@ -305,12 +477,13 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
         }
       }
       if (C > 1) cluster_barrier_jb(); else __syncthreads();
-      JB_CLK(2);
+      JB_CLK(4);
 
-      // ---- 3. apply [W_I W_J] <- [W_I W_J] Q, NQB pairs at a time
-      for (int g0 = 0; g0 < Pb; g0 += NQB) {
-        const int npair = min(NQB, Pb - g0);
-        constexpr int F4 = PW / 4;
+      // ---- 3. apply [W_I W_J] <- [W_I W_J] Q, qb <= NQB pairs at a time (<= 2 tasks per thread)
+      constexpr int F4 = PW / 4;
+      const int qb = min(NQB, (2 * NT) / (((nr + 3) / 4) * F4));
+      for (int g0 = 0; g0 < Pb; g0 += qb) {
+        const int npair = min(qb, Pb - g0);
         for (int e = t; e < npair * PW * F4; e += NT) {   // fetch Q (owner's smem) as float4 rows
           const int pp = e / (PW * F4), rem = e % (PW * F4), a = rem / F4, c4 = rem % F4;
           const int g = g0 + pp;
@@ -318,7 +491,11 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
           const int owner = g % C, slot = g / C;
           const float* src = Qw + (size_t)slot * PW * LDQ + a * LDQ + 4 * c4;
           const float4 v = (owner == rank) ? *reinterpret_cast<const float4*>(src) : ld_cluster_f4(src, owner);
-          *reinterpret_cast<float4*>(Qb + (size_t)pp * PW * LDQ + a * LDQ + 4 * c4) = v;
+          const int sw = qsw(a);   // un-swizzle (see qsw): out[i] = v[i ^ sw]
+          float4 o = v;
+          if (sw & 1) o = make_float4(o.y, o.x, o.w, o.z);
+          if (sw & 2) o = make_float4(o.z, o.w, o.x, o.y);
+          *reinterpret_cast<float4*>(Qb + (size_t)pp * PW * LDQ + a * LDQ + 4 * c4) = o;
         }
         __syncthreads();
         const int rq_n = (nr + 3) / 4;
@@ -380,7 +557,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
         __syncthreads();
       }
       for (int g = 0; g < Pb; ++g) any |= flag[g];
-      JB_CLK(3);
+      JB_CLK(5);
     }
     converged = (any == 0);
   }
@@ -406,7 +583,9 @@ cudaError_t launch_bw(int nb, int k, const float* L, float* Wf, int32_t* status,
   const int C = (k + rt - 1) / rt;
   if (C > 8) return cudaErrorInvalidValue;
   const Layout Lo = make_layout<BW>(k, C);
-  if (Lo.nown > JB<BW>::MAXOWN || Lo.Pb > 128 || Lo.total > 227 * 1024) return cudaErrorInvalidValue;
+  if (Lo.nown > JB<BW>::MAXOWN || Lo.nown > NT / 128 || Lo.Pb > 128 || Lo.total > 227 * 1024 ||
+      ((Lo.R + 3) / 4) * (JB<BW>::PW / 4) > 2 * NT)
+    return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k_jacobi_blk<BW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lo.total);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};

@@ -26,11 +26,11 @@ def hgm():
 
 def dev_inputs(h):
     hg = hgm()
-    key = id(h)
-    if key not in _cache:
-        _cache[key] = (hg.incidence_to_device(h.row_ptr, h.col_idx, h.E), torch.from_numpy(h.w).cuda(),
+    key = id(h)   # the entry keeps h alive, so its id cannot be reused by another input
+    if key not in _cache or _cache[key][0] is not h:
+        _cache[key] = (h, hg.incidence_to_device(h.row_ptr, h.col_idx, h.E), torch.from_numpy(h.w).cuda(),
                        torch.from_numpy(h.Y).cuda())
-    return _cache[key]
+    return _cache[key][1:]
 
 
 def rel(a, b):

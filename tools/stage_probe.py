@@ -56,7 +56,7 @@ def main():
         dbg["chol_phases_kcyc"] = {i: round((v - base) / 1e3, 1) for i, v in enumerate(clk) if v}
     jc = dbg.pop("jac_clk")
     if jc[0]:
-        dbg["jac_round_cyc"] = [jc[i] - jc[0] for i in range(12)]
+        dbg["jac_round_cyc"] = [jc[i] - jc[0] for i in range(16)]
     out = {"cfg": c.name, "b": c.b, "k": c.k, "q": c.q, "gen_s": tgen, "status": int(st.item()),
            "ms_per_step": e0.elapsed_time(e1) / a.reps,
            "stages": {k: round(v[0] / a.reps, 4) for k, v in sorted(prof.items(), key=lambda x: -x[1][0])},
