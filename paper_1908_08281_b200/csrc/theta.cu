@@ -4,14 +4,16 @@
 //   Theta_ii[u][v] = r_u r_v sum_{e ni u,v} w_e/delta(e),  r = delta(v)^-1/2   (Eq. 1)
 //   X_ii = I - Theta_ii/(1+mu)
 //
-// Assembly: one CTA per (block, 128-row tile U, 64-column tile V).  The CTA
-// hashes V's incidences (edge -> members of V, in shared memory); the thread
-// owning row u walks u's CSR row in ascending edge order and adds w_e/delta(e)
-// to acc[u][v] for every v of V sharing e.  Every (u,v) sum is therefore taken
-// over the common edges in ascending edge order -- the same sequence for (v,u)
-// -- so the written blocks are bitwise symmetric and run-to-run deterministic
-// with no atomics on values.  Traffic: the b x b block is written once
-// (4 b^2 bytes per block; HBM-write bound); CSR reads are ~2 nnz per tile row.
+// Assembly, default path: sorted per-block CSC keys + full-width row tiles
+// (k_seg_sort, k_assemble_rows; see "Sorted-CSC assembly" below).  Fallback
+// (blocks whose segments overflow shared memory, E*b >= 2^32, or HG_ASSEMBLE=tiles):
+// k_assemble, one CTA per (block, 128-row tile U, 64-column tile V) that hashes V's
+// incidences (edge -> members of V, in shared memory); the thread owning row u walks
+// u's CSR row in ascending edge order and adds w_e/delta(e) to acc[u][v] for every v
+// of V sharing e.  Both paths sum every (u,v) over the common edges in ascending edge
+// order -- the same sequence for (v,u) -- so the written blocks are bitwise symmetric,
+// identical between the paths and run-to-run deterministic with no atomics on values.
+// Traffic: the b x b block is written once (4 b^2 bytes per block; HBM-write bound).
 #include <cstdlib>
 
 #include "common.cuh"
