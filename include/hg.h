@@ -127,7 +127,12 @@ hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const floa
  * with scale = mu/(1+mu).  sigma_out [N/b][k] may be NULL.  Asynchronous
  * unless flags has HG_SYNC (then the stream is synchronised and a non-zero
  * *d_status returns HG_ERR_NUMERICAL).  d_status may be NULL only with HG_SYNC
- * (a word inside ws is used). */
+ * (a word inside ws is used).
+ * Concurrency: after the assembly, disjoint block ranges (HG_STREAMS parts,
+ * default 2, at most 4) run their rSVD + apply on library-owned non-blocking
+ * streams forked from and joined back into `stream` with events, so all work
+ * is still ordered after prior work on `stream` and before later work (also
+ * under stream capture).  The result is bitwise independent of the part count. */
 hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
                    uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags,
                    int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);

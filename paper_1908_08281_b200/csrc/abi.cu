@@ -15,6 +15,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -241,23 +242,50 @@ hg_status cholqr(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* L
   return HG_OK;
 }
 
-hg_status run_rsvd(const float* X, int nb, int b, int k, int q, uint64_t seed, bool simt, float* Ut, float* sigma,
-                   float* Vt, int32_t* st, void* ws, const Layout& Lo, cudaStream_t s) {
+// Block-indexed workspace buffers of the part [blk0, blk0 + nb) of an nb_total-block
+// problem (parts run concurrently on different streams; see solve_impl).
+struct Bufs {
+  float* P[4];
+  float *G, *L, *Linv, *Wf, *Uk, *work, *rs, *Z;
+  double* sig;
+  int32_t* perm;
+};
+Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k, int T) {
+  Bufs B;
+  const int64_t kb = (int64_t)blk0 * k * b, kk = (int64_t)blk0 * k * k, k1 = (int64_t)blk0 * k;
+  for (int i = 0; i < 4; ++i) B.P[i] = at<float>(ws, Lo.P[i]) + kb;
+  B.G = at<float>(ws, Lo.G) + kk;
+  B.L = at<float>(ws, Lo.L) + kk;
+  B.Linv = at<float>(ws, Lo.Linv) + kk;
+  B.Wf = at<float>(ws, Lo.Wf) + kk;
+  B.Uk = at<float>(ws, Lo.Uk) + kk;
+  B.work = at<float>(ws, Lo.work) + kk;
+  B.rs = at<float>(ws, Lo.rs) + k1;
+  B.Z = at<float>(ws, Lo.Z) + k1 * (T > 0 ? T : 1);
+  double* sig0 = at<double>(ws, Lo.sig);
+  B.sig = sig0 + k1;
+  B.perm = reinterpret_cast<int32_t*>(sig0 + (int64_t)nb_total * k) + k1;
+  return B;
+}
+
+// Alg. 1 on the nb blocks at X (global block index of the first: blk0, which keys Omega).
+hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64_t seed, bool simt, float* Ut,
+                   float* sigma, float* Vt, int32_t* st, const Bufs& Bf, cudaStream_t s) {
   Rsvd R{nb, b, k, simt, s, X};
   float* P[4];
-  for (int i = 0; i < 4; ++i) P[i] = at<float>(ws, Lo.P[i]);
-  float* G = at<float>(ws, Lo.G);
-  float* Lm = at<float>(ws, Lo.L);
-  float* Linv = at<float>(ws, Lo.Linv);
-  float* Wf = at<float>(ws, Lo.Wf);
-  float* Uk = at<float>(ws, Lo.Uk);
-  float* work = at<float>(ws, Lo.work);
-  double* sig = at<double>(ws, Lo.sig);
+  for (int i = 0; i < 4; ++i) P[i] = Bf.P[i];
+  float* G = Bf.G;
+  float* Lm = Bf.L;
+  float* Linv = Bf.Linv;
+  float* Wf = Bf.Wf;
+  float* Uk = Bf.Uk;
+  float* work = Bf.work;
+  double* sig = Bf.sig;
 
   // Alg. 1 step 1-2: Omega, Y0 = X Omega, S0 = qr(Y0)
   {
     ProfScope ps(ST_OMEGA, s);
-    HG_CU(launch_omega_panels(seed, nb, b, k, P[0], s, &g_launches), "omega");
+    HG_CU(launch_omega_panels(seed, blk0, nb, b, k, P[0], s, &g_launches), "omega");
   }
   HG_TRY(R.power(P[0], P[1]));
   HG_TRY(cholqr(R, P[1], P[0], G, Linv, work, st, 2 * k > b ? 3 : 2));
@@ -304,16 +332,16 @@ hg_status run_rsvd(const float* X, int nb, int b, int k, int q, uint64_t seed, b
   }
   {
     ProfScope ps(ST_FINALIZE, s);
-    HG_CU(launch_finalize(nb, b, k, P[2], P[3], Ut, sigma, Vt, sig, st, s, &g_launches), "finalize");
+    HG_CU(launch_finalize(nb, b, k, P[2], P[3], Ut, sigma, Vt, sig, Bf.perm, st, s, &g_launches), "finalize");
   }
   return HG_OK;
 }
 
 hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb, int b, int k, const float* Y, int T,
-                    float scale, float* F, int32_t* st, void* ws, const Layout& Lo, cudaStream_t s, bool simt) {
+                    float scale, float* F, int32_t* st, const Bufs& Bf, cudaStream_t s, bool simt) {
   if (T == 0) return HG_OK;
-  float* rs = at<float>(ws, Lo.rs);
-  float* Z = at<float>(ws, Lo.Z);
+  float* rs = Bf.rs;
+  float* Z = Bf.Z;
   {
     ProfScope ps(ST_INV_SIGMA, s);
     HG_CU(launch_inv_sigma(nb, k, sigma, scale, rs, st, s, &g_launches), "inv_sigma");
@@ -477,8 +505,8 @@ hg_status hg_block_rsvd(const float* blocks, int32_t nb, int32_t b, int32_t k, i
   if (!blocks || !Ut || !sigma || !Vt || !d_status) return fail(HG_ERR_INVALID, "NULL pointer argument");
   const Layout Lo = layout((int64_t)nb * b, 1, 0, b, k, 0);
   HG_TRY(check_ws(ws, ws_bytes, Lo.status));
-  return run_rsvd(blocks, nb, b, k, q, seed, (flags & HG_GEMM_SIMT) != 0, Ut, sigma, Vt, d_status, ws, Lo,
-                  reinterpret_cast<cudaStream_t>(stream));
+  return run_rsvd(blocks, nb, 0, b, k, q, seed, (flags & HG_GEMM_SIMT) != 0, Ut, sigma, Vt, d_status,
+                  part_bufs(ws, Lo, nb, 0, b, k, 0), reinterpret_cast<cudaStream_t>(stream));
 }
 
 hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const float* Vt, int32_t nb, int32_t b,
@@ -492,8 +520,47 @@ hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const floa
   if (!std::isfinite(scale)) return fail(HG_ERR_INVALID, "scale must be finite");
   const Layout Lo = layout((int64_t)nb * b, 1, 0, b, k, T);
   HG_TRY(check_ws(ws, ws_bytes, Lo.status));
-  return run_apply(Ut, sigma, Vt, nb, b, k, Y, T, scale, F, d_status, ws, Lo, reinterpret_cast<cudaStream_t>(stream),
-                   false);
+  return run_apply(Ut, sigma, Vt, nb, b, k, Y, T, scale, F, d_status, part_bufs(ws, Lo, nb, 0, b, k, T),
+                   reinterpret_cast<cudaStream_t>(stream), false);
+}
+
+// Part count for hg_solve (HG_STREAMS, default 2) and the auxiliary streams / events
+// of the fork-join (created once, non-blocking, reused).
+constexpr int kMaxParts = 4;
+static int solve_parts() {   // read per call (tests switch it)
+  const char* v = getenv("HG_STREAMS");
+  const int x = v ? atoi(v) : 2;
+  return x < 1 ? 1 : (x > kMaxParts ? kMaxParts : x);
+}
+static hg_status fork_streams(cudaStream_t s, int nparts, cudaStream_t* ps) {
+  static cudaStream_t aux[kMaxParts] = {};
+  static cudaEvent_t ev_fork = nullptr;
+  ps[0] = s;
+  if (nparts == 1) return HG_OK;
+  if (const char* v = getenv("HG_STREAMS_SERIAL")) {   // debugging: parts in sequence on `stream`
+    if (v[0] == '1') {
+      for (int p = 1; p < nparts; ++p) ps[p] = s;
+      return HG_OK;
+    }
+  }
+  if (!ev_fork) HG_CU(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event create");
+  HG_CU(cudaEventRecord(ev_fork, s), "fork record");
+  for (int p = 1; p < nparts; ++p) {
+    if (!aux[p]) HG_CU(cudaStreamCreateWithFlags(&aux[p], cudaStreamNonBlocking), "stream create");
+    HG_CU(cudaStreamWaitEvent(aux[p], ev_fork, 0), "fork wait");
+    ps[p] = aux[p];
+  }
+  return HG_OK;
+}
+static hg_status join_streams(cudaStream_t s, int nparts, const cudaStream_t* ps) {
+  static cudaEvent_t ev_join[kMaxParts] = {};
+  for (int p = 1; p < nparts; ++p) {
+    if (ps[p] == s) continue;
+    if (!ev_join[p]) HG_CU(cudaEventCreateWithFlags(&ev_join[p], cudaEventDisableTiming), "event create");
+    HG_CU(cudaEventRecord(ev_join[p], ps[p]), "join record");
+    HG_CU(cudaStreamWaitEvent(s, ev_join[p], 0), "join wait");
+  }
+  return HG_OK;
 }
 
 static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
@@ -518,8 +585,24 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   float* Vt = at<float>(ws, Lo.Vt);
   float* sigma = sigma_out ? sigma_out : at<float>(ws, Lo.sigma);
   HG_TRY(run_theta(H, w, mu, b, false, blocks, nullptr, st, ws, Lo, s));
-  HG_TRY(run_rsvd(blocks, nb, b, k, q, seed, simt, Ut, sigma, Vt, st, ws, Lo, s));
-  HG_TRY(run_apply(Ut, sigma, Vt, nb, b, k, Y, T, mu / (1.0f + mu), F, st, ws, Lo, s, simt));
+  // Blocks are independent (reading A5): the rSVD + apply of disjoint block ranges run
+  // on forked streams, so one part's tensor-core GEMMs fill the SMs that the other
+  // part's latency-bound Cholesky / Jacobi leave idle.  Bitwise the same result for
+  // any part count (Omega is keyed by the global block index).  One part while the
+  // stage profiler is on (per-stage attribution needs sequential stages).
+  const int nparts = g_prof_on ? 1 : std::max(1, std::min(solve_parts(), nb));
+  cudaStream_t ps[kMaxParts];
+  HG_TRY(fork_streams(s, nparts, ps));
+  for (int p = 0; p < nparts; ++p) {
+    const int blk0 = (int)((int64_t)nb * p / nparts), nbp = (int)((int64_t)nb * (p + 1) / nparts) - blk0;
+    const int64_t kb = (int64_t)blk0 * k * b;
+    const Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, k, T);
+    HG_TRY(run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, k, q, seed, simt, Ut + kb, sigma + (int64_t)blk0 * k,
+                    Vt + kb, st, Bf, ps[p]));
+    HG_TRY(run_apply(Ut + kb, sigma + (int64_t)blk0 * k, Vt + kb, nbp, b, k, T > 0 ? Y + (int64_t)blk0 * b * T : Y, T,
+                     mu / (1.0f + mu), T > 0 ? F + (int64_t)blk0 * b * T : F, st, Bf, ps[p], simt));
+  }
+  HG_TRY(join_streams(s, nparts, ps));
   if (flags & HG_SYNC) {
     int32_t h = 0;
     HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");

@@ -16,8 +16,9 @@
 // Full path: one CTA (32 warps) per block, the lower triangle held as 32x32
 // tiles (row pitch 36: 16-byte aligned rows read as float4 broadcasts) in
 // shared memory for k <= 256 (L2-resident global scratch beyond):
-//   right-looking tile Cholesky: per panel p, POTRF(p,p) | TRSM(i,p) | SYRK/GEMM
-//   trailing update -- three barriers per panel;
+//   right-looking tile Cholesky with one-panel lookahead: per panel p, TRSM(i,p) |
+//   trailing update, during which warp 0 updates tile (p+1,p+1) first and factors it
+//   (POTRF) -- two barriers per panel; tile products are register-blocked half tiles;
 //   in-place tile TRTRI (LAPACK trtri order): invert diagonal tiles, then for
 //   block columns j = nt-2..0: L_ij <- -(sum_{m=j+1..i} Linv_im L_mj) Linv_jj.
 #include "common.cuh"
@@ -81,42 +82,74 @@ __device__ void tile_trsm(float* A, const float* L, int lane) {
   __syncwarp();
 }
 
-// dot of a 32-vector in registers with a shared-memory row (float4 broadcasts, 4 chains)
-__device__ __forceinline__ float dot32(const float (&b)[TS], const float* row) {
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+// Register-blocked warp products on 16-row halves of 32x32 tiles (pitch LDT = 36).
+// Lane = (rg, cg) = (lane >> 2, lane & 3) owns rows r0 + rg + 8i (i < 2).  Rows are
+// interleaved so that the eight row groups fall in distinct 16-byte bank groups
+// ((row * 36 / 4) mod 8 = row mod 8): every float4 operand load is conflict-free.
+// C[r][c] -= sum_t A[r][t] B[c][t]; lane columns c = cg + 4j (j < 8), B rows float4 over t.
+__device__ void tile_sub_abt_h(float* C, const float* A, const float* B, int lane, int r0) {
+  const int rg = lane >> 2, cg = lane & 3;
+  float acc[2][8];
 #pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
   for (int t = 0; t < TS; t += 4) {
-    const float4 a = *reinterpret_cast<const float4*>(row + t);
-    s0 = fmaf(a.x, b[t], s0);
-    s1 = fmaf(a.y, b[t + 1], s1);
-    s2 = fmaf(a.z, b[t + 2], s2);
-    s3 = fmaf(a.w, b[t + 3], s3);
+    float4 a[2], b[8];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) a[i] = *reinterpret_cast<const float4*>(A + (r0 + rg + 8 * i) * LDT + t);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b[j] = *reinterpret_cast<const float4*>(B + (cg + 4 * j) * LDT + t);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        acc[i][j] = fmaf(a[i].x, b[j].x, acc[i][j]);
+        acc[i][j] = fmaf(a[i].y, b[j].y, acc[i][j]);
+        acc[i][j] = fmaf(a[i].z, b[j].z, acc[i][j]);
+        acc[i][j] = fmaf(a[i].w, b[j].w, acc[i][j]);
+      }
   }
-  return (s0 + s1) + (s2 + s3);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) C[(r0 + rg + 8 * i) * LDT + cg + 4 * j] -= acc[i][j];
+  __syncwarp();
 }
 
-// warp: rows [r0, r0+8) of C -= A B^T (all 32x32); lane c owns output column c, holds row c of B
-__device__ void tile_sub_abt(float* C, const float* A, const float* B, int lane, int r0) {
-  float b[TS];
+// acc[r][c] += sum_t A[r][t] B[t][c] for the lane's rows r0 + rg + 8i and columns
+// 8 cg .. 8 cg + 7 (B rows as two float4: the four column groups hit distinct bank groups)
+__device__ __forceinline__ void tile_ab_acc_h(float (&acc)[2][8], const float* A, const float* B, int lane, int r0) {
+  const int rg = lane >> 2, cg = lane & 3;
+#pragma unroll 2
+  for (int t = 0; t < TS; t += 4) {
+    float4 a[2];
 #pragma unroll
-  for (int t = 0; t < TS; ++t) b[t] = B[lane * LDT + t];
+    for (int i = 0; i < 2; ++i) a[i] = *reinterpret_cast<const float4*>(A + (r0 + rg + 8 * i) * LDT + t);
 #pragma unroll
-  for (int r = r0; r < r0 + 8; ++r) C[r * LDT + lane] -= dot32(b, A + r * LDT);
-  __syncwarp();
+    for (int u = 0; u < 4; ++u) {
+      const float4 b0 = *reinterpret_cast<const float4*>(B + (t + u) * LDT + 8 * cg);
+      const float4 b1 = *reinterpret_cast<const float4*>(B + (t + u) * LDT + 8 * cg + 4);
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float av = u == 0 ? a[i].x : u == 1 ? a[i].y : u == 2 ? a[i].z : a[i].w;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av, bb[j], acc[i][j]);
+      }
+    }
+  }
 }
 
-// warp: rows [r0, r0+8) of C = sign*A B (overwrite) or += sign*A B; lane c owns column c
-__device__ void tile_add_ab(float* C, const float* A, const float* B, int lane, bool overwrite, float sign, int r0) {
-  float b[TS];
+__device__ __forceinline__ void tile_store_h(float* C, const float (&v)[2][8], int lane, int r0) {
+  const int rg = lane >> 2, cg = lane & 3;
 #pragma unroll
-  for (int t = 0; t < TS; ++t) b[t] = B[t * LDT + lane];
-  __syncwarp();
-#pragma unroll
-  for (int r = r0; r < r0 + 8; ++r) {
-    const float v = sign * dot32(b, A + r * LDT);
-    C[r * LDT + lane] = overwrite ? v : C[r * LDT + lane] + v;
+  for (int i = 0; i < 2; ++i) {
+    float* row = C + (r0 + rg + 8 * i) * LDT + 8 * cg;
+    *reinterpret_cast<float4*>(row) = make_float4(v[i][0], v[i][1], v[i][2], v[i][3]);
+    *reinterpret_cast<float4*>(row + 4) = make_float4(v[i][4], v[i][5], v[i][6], v[i][7]);
   }
-  __syncwarp();
 }
 
 // warp: lower-triangular 32x32 tile inverse in place; lane c owns column c (registers)
@@ -187,7 +220,7 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   if (lane == 0) red[warp] = emax;
   __syncthreads();
   if (t < 32) {
-    float v = red[t];
+    float v = t < NWARP ? red[t] : 0.f;   // red holds NWARP partial maxima
     for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
     if (t == 0) red[0] = v;
   }
@@ -255,24 +288,36 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   // ---- right-looking tile Cholesky
   CHOL_CLK(1);
   bool bad = false;
+  // one-panel lookahead: warp 0 updates the next diagonal tile first and factors it
+  // while the other warps finish the trailing update
+  if (warp == 0) {
+    tile_potrf(T(0, 0), lane, status, bad);
+    if (bad && lane == 0) s_bad = 1;
+  }
+  __syncthreads();
   for (int p = 0; p < nt; ++p) {
-    if (warp == 0) {
-      tile_potrf(T(p, p), lane, status, bad);
-      if (bad && lane == 0) s_bad = 1;
-    }
-    __syncthreads();
     CHOL_CLK(2 + 3 * p);
     for (int i = p + 1 + warp; i < nt; i += NWARP) tile_trsm(T(i, p), T(p, p), lane);
     __syncthreads();
     CHOL_CLK(3 + 3 * p);
     const int m = nt - p - 1;                       // trailing tiles (i,j), p < j <= i
-    for (int task = warp; task < m * (m + 1) / 2 * 4; task += NWARP) {
-      const int w = task >> 2;
-      int a = 0;
-      while ((a + 1) * (a + 2) / 2 <= w) ++a;
-      const int b = w - a * (a + 1) / 2;
-      const int i = p + 1 + a, j = p + 1 + b;
-      tile_sub_abt(T(i, j), T(i, p), T(j, p), lane, (task & 3) * 8);
+    if (m > 0) {
+      if (warp == 0) {                              // lookahead: tile (p+1, p+1), then POTRF
+        tile_sub_abt_h(T(p + 1, p + 1), T(p + 1, p), T(p + 1, p), lane, 0);
+        tile_sub_abt_h(T(p + 1, p + 1), T(p + 1, p), T(p + 1, p), lane, 16);
+        tile_potrf(T(p + 1, p + 1), lane, status, bad);
+        if (bad && lane == 0) s_bad = 1;
+      } else {
+        const int ntask = (m * (m + 1) / 2 - 1) * 2;  // half tiles, diagonal (p+1, p+1) excluded
+        for (int task = warp - 1; task < ntask; task += NWARP - 1) {
+          const int w = (task >> 1) + 1;
+          int a = 0;
+          while ((a + 1) * (a + 2) / 2 <= w) ++a;
+          const int b = w - a * (a + 1) / 2;
+          const int i = p + 1 + a, j = p + 1 + b;
+          tile_sub_abt_h(T(i, j), T(i, p), T(j, p), lane, (task & 1) * 16);
+        }
+      }
     }
     __syncthreads();
     CHOL_CLK(4 + 3 * p);
@@ -292,15 +337,22 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   CHOL_CLK(41);
   for (int j = nt - 2; j >= 0; --j) {
     const int dn = nt - 1 - j;
-    for (int task = warp; task < dn * 4; task += NWARP) {   // temp[w] = sum_{m=j+1..i} Linv_im L_mj
-      const int w = task >> 2, i = j + 1 + w, r0 = (task & 3) * 8;
-      float* tmp = temp + (int64_t)w * TILE;
-      for (int m = j + 1; m <= i; ++m) tile_add_ab(tmp, T(i, m), T(m, j), lane, m == j + 1, 1.f, r0);
+    for (int task = warp; task < dn * 2; task += NWARP) {   // temp[w] = sum_{m=j+1..i} Linv_im L_mj
+      const int w = task >> 1, i = j + 1 + w, r0 = (task & 1) * 16;
+      float acc[2][8] = {};
+      for (int m = j + 1; m <= i; ++m) tile_ab_acc_h(acc, T(i, m), T(m, j), lane, r0);
+      tile_store_h(temp + (int64_t)w * TILE, acc, lane, r0);
     }
     __syncthreads();
-    for (int task = warp; task < dn * 4; task += NWARP) {   // L_ij <- -temp Linv_jj
-      const int w = task >> 2, i = j + 1 + w;
-      tile_add_ab(T(i, j), temp + (int64_t)w * TILE, T(j, j), lane, true, -1.f, (task & 3) * 8);
+    for (int task = warp; task < dn * 2; task += NWARP) {   // L_ij <- -temp Linv_jj
+      const int w = task >> 1, i = j + 1 + w, r0 = (task & 1) * 16;
+      float acc[2][8] = {};
+      tile_ab_acc_h(acc, temp + (int64_t)w * TILE, T(j, j), lane, r0);
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[a][c] = -acc[a][c];
+      tile_store_h(T(i, j), acc, lane, r0);
     }
     __syncthreads();
     CHOL_CLK(42 + (nt - 2 - j));

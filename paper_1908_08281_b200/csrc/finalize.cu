@@ -139,8 +139,8 @@ cudaError_t launch_unit_columns_t(int nb, int k, const float* Wf, float* Uk, cud
 }
 
 cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float* Uw_t, float* Ut, float* sigma,
-                            float* Vt, double* sig_raw, int32_t* status, cudaStream_t s, int* launches) {
-  int32_t* perm = reinterpret_cast<int32_t*>(sig_raw + (size_t)nb * k);
+                            float* Vt, double* sig_raw, int32_t* perm, int32_t* status, cudaStream_t s,
+                            int* launches) {
   k_colnorm<<<nb * k, NT, 0, s>>>(b, Vw_t, sig_raw);
   k_rank<<<nb, 256, 0, s>>>(k, sig_raw, perm, sigma, status);
   k_rows<<<nb * k, NT, 0, s>>>(b, k, Vw_t, Uw_t, perm, sig_raw, Ut, Vt);

@@ -18,6 +18,7 @@
 //   3. every CTA applies [W_I W_J] <- [W_I W_J] Q to its rows.
 // Cluster rounds per sweep: k/BW instead of k - 1; the Gram and the update are
 // register-blocked products instead of per-pair dot products.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -215,111 +216,151 @@ __device__ __forceinline__ int named_bar_or(int id, int n, int pred) {
 
 // Cross rounds of the inner sweep (BW rounds, pairs (j, BW + (j + r) % BW)) by the
 // four warps h = 0..3 of an owner group (128 threads, named barrier bar_id).  Warp h
-// holds register slots j and BW + j for j in [h QW, (h+1) QW) of every row (lane =
-// row).  Register slots, not columns, are paired, so that register indices are
-// compile-time constants inside the runtime round loop: slot j (< BW) holds column j,
-// slot BW + j holds column BW + (j + r) % BW, pairs are slots (j, BW + j) = columns
-// (j, BW + (j + r) % BW).  After each round the J-half slots rotate by one, passing one
-// value per thread to the neighbouring warp through xch.
-// Per round: the warp holding slot BW + a computes the angle of pair (a, .) from the
-// shared diagonal dsm and its own register a_pq, writes (c, s) to cs and the new
-// diagonal to dsm; barrier (OR-reduces "anything rotated"); every warp rotates its
-// column pairs (G and Q) and, by shuffles, its part of every row; barrier; slot
-// rotation.  Rotation arithmetic: jrot.
+// holds register slots j and BW + j for j in [h QW, (h+1) QW) of row `lane` of G
+// (fp64) and of Q (fp32).  Register slots, not columns, are paired, so register
+// indices are compile-time constants inside the runtime round loop: slot j (< BW)
+// holds column j, slot BW + j holds column BW + (j + r) % BW, pairs are slots
+// (j, BW + j) = columns (j, BW + (j + r) % BW).  After each round the J-half slots
+// (of G and of Q) rotate by one, one value per thread passing to the neighbouring
+// warp through shared memory; after BW rounds the slots are back in column order.
+// One warp of the group (aw, spread over the SMSPs by the caller) computes all BW
+// angles of a round from a_pq values the holders staged in shared memory together
+// with the slot exchange (2 barriers per round; the second ORs "anything rotated").
+// Rotation arithmetic: jrot.
+struct Cross4Scratch {
+  double* dsm;    // [PW] diagonal of G
+  double* apq;    // [BW] a_pq of the next round's pairs
+  double* xg;     // [4][32] G slot exchange
+  double2* csd;   // [BW] (c, s) fp64
+  float* xq;      // [4][32] Q slot exchange
+  float2* csf;    // [BW] (c, s) fp32
+};
+
 template <int BW>
-__device__ int inner_sweep_cross4(const double* G, float* Q, double tol2, double2* cs, double* dsm, double* xch,
-                                  int lane, int h, int bar_id) {
+__device__ int inner_sweep_cross4(const double* G, float* Q, double tol2, const Cross4Scratch& S, int lane, int h,
+                                  int aw, int bar_id) {
   constexpr int PW = 2 * BW, LDQ = JB<BW>::LDQ, QW = BW / 4;
   const int j0 = h * QW;
   const bool act = lane < PW;
-  const int sw = qsw(lane);
-  float* qrow = Q + (act ? lane : 0) * LDQ;
   double gI[QW], gJ[QW];
+  float qI[QW], qJ[QW];
 #pragma unroll
   for (int i = 0; i < QW; ++i) {
     gI[i] = act ? G[lane * LDQ + j0 + i] : 0.0;
     gJ[i] = act ? G[lane * LDQ + BW + j0 + i] : 0.0;
-    if (act) {
-      qrow[(j0 + i) ^ sw] = (lane == j0 + i) ? 1.f : 0.f;
-      qrow[(BW + j0 + i) ^ sw] = (lane == BW + j0 + i) ? 1.f : 0.f;
-    }
+    qI[i] = (lane == j0 + i) ? 1.f : 0.f;
+    qJ[i] = (lane == BW + j0 + i) ? 1.f : 0.f;
   }
-  if (h == 0 && act) dsm[lane] = G[lane * LDQ + lane];
+  if (h == 0 && act) S.dsm[lane] = G[lane * LDQ + lane];
+  if (lane < BW && lane / QW == h) S.apq[lane] = gJ[lane - j0];   // round 0: pair a = slot (a, BW + a)
   named_bar(bar_id, 128);
   // no cross entry above the threshold: no round can rotate (G never changes), skip
   int need = 0;
   if (lane < BW) {
-    const double da = dsm[lane];
+    const double da = S.dsm[lane];
 #pragma unroll
-    for (int i = 0; i < QW; ++i) need |= gJ[i] * gJ[i] > tol2 * da * dsm[BW + j0 + i];
+    for (int i = 0; i < QW; ++i) need |= gJ[i] * gJ[i] > tol2 * da * S.dsm[BW + j0 + i];
   }
-  if (!named_bar_or(bar_id, 128, need)) return 0;
   int rot_any = 0;
-  const bool prow = lane < BW && (lane / QW) == h;   // this lane computes the angle of pair `lane`
+  if (named_bar_or(bar_id, 128, need)) {
 #pragma unroll 1
-  for (int r = 0; r < BW; ++r) {
-    int rot = 0;
-    if (prow) {
-      const int pa = BW + (lane + r) % BW;
-      double apq = gJ[0];   // slot BW + lane = gJ[lane - j0]
-#pragma unroll
-      for (int i = 1; i < QW; ++i) apq = (lane - j0 == i) ? gJ[i] : apq;
-      const double app = dsm[lane], aqq = dsm[pa];
-      float c = 1.f, s = 0.f;
-      if (apq * apq > tol2 * app * aqq) {
-        double dp, dq;
-        jrot(app, aqq, apq, c, s, dp, dq);
-        dsm[lane] = dp;
-        dsm[pa] = dq;
-        rot = s != 0.f;
+    for (int r = 0; r < BW; ++r) {
+      // angles (warp aw, lane = pair a: rows a and pa = BW + (a + r) % BW)
+      int rot = 0;
+      if (h == aw && lane < BW) {
+        const int pa = BW + (lane + r) % BW;
+        const double apq = S.apq[lane], app = S.dsm[lane], aqq = S.dsm[pa];
+        float c = 1.f, sn = 0.f;
+        if (apq * apq > tol2 * app * aqq) {
+          double dp, dq;
+          jrot(app, aqq, apq, c, sn, dp, dq);
+          S.dsm[lane] = dp;
+          S.dsm[pa] = dq;
+          rot = sn != 0.f;
+        }
+        S.csd[lane] = make_double2((double)c, (double)sn);
+        S.csf[lane] = make_float2(c, sn);
       }
-      cs[lane] = make_double2((double)c, (double)s);
-    }
-    if (named_bar_or(bar_id, 128, rot)) {
-      rot_any = 1;
+      if (named_bar_or(bar_id, 128, rot)) {
+        rot_any = 1;
 #pragma unroll
-      for (int i = 0; i < QW; ++i) {   // columns: slot pair (j, BW + j), columns (j, BW + (j + r) % BW)
-        const int j = j0 + i;
-        const double2 v = cs[j];
-        const double gp = gI[i], gq = gJ[i];
-        gI[i] = fma(v.x, gp, -v.y * gq);
-        gJ[i] = fma(v.y, gp, v.x * gq);
-        if (PW == 32 || act) {
-          const int cq = BW + (j + r) % BW;
-          const float cf = (float)v.x, sf = (float)v.y;
-          const float qp = qrow[j ^ sw], qq = qrow[cq ^ sw];
-          qrow[j ^ sw] = fmaf(cf, qp, -sf * qq);
-          qrow[cq ^ sw] = fmaf(sf, qp, cf * qq);
+        for (int i = 0; i < QW; ++i) {   // columns of G and Q: slot pair (j, BW + j)
+          const double2 v = S.csd[j0 + i];
+          const float2 vf = S.csf[j0 + i];
+          const double gp = gI[i], gq = gJ[i];
+          gI[i] = fma(v.x, gp, -v.y * gq);
+          gJ[i] = fma(v.y, gp, v.x * gq);
+          const float qp = qI[i], qq = qJ[i];
+          qI[i] = fmaf(vf.x, qp, -vf.y * qq);
+          qJ[i] = fmaf(vf.y, qp, vf.x * qq);
+        }
+        int pa = lane, pj = 0;   // rows of G: row_p' = c row_p - s row_q ; row_q' = s row_p + c row_q
+        bool first = false;
+        if (lane < BW) { pa = BW + (lane + r) % BW; pj = lane; first = true; }
+        else if (act) { pa = ((lane - BW - r) % BW + BW) % BW; pj = pa; }
+        const double2 v = S.csd[pj];
+        const double cd = act ? v.x : 1.0, sd = act ? (first ? -v.y : v.y) : 0.0;
+#pragma unroll
+        for (int i = 0; i < QW; ++i) {
+          const double oI = __shfl_sync(0xffffffffu, gI[i], pa);
+          const double oJ = __shfl_sync(0xffffffffu, gJ[i], pa);
+          gI[i] = fma(sd, oI, cd * gI[i]);
+          gJ[i] = fma(sd, oJ, cd * gJ[i]);
         }
       }
-      int pa = lane, pj = 0;   // rows: row_p' = c row_p - s row_q ; row_q' = s row_p + c row_q
-      bool first = false;
-      if (lane < BW) { pa = BW + (lane + r) % BW; pj = lane; first = true; }
-      else if (act) { pa = ((lane - BW - r) % BW + BW) % BW; pj = pa; }
-      const double2 v = cs[pj];
-      const double cd = act ? v.x : 1.0, sd = act ? (first ? -v.y : v.y) : 0.0;
+      // slot rotation: new slot BW + j = old slot BW + j + 1 (wrapping inside the J half);
+      // the holder of old slot BW + a + 1 stages a_pq of round r + 1's pair a
+      S.xg[h * 32 + lane] = gJ[0];
+      S.xq[h * 32 + lane] = qJ[0];
+      if (lane < BW) {
+        const int sl = (lane + 1) % BW;   // old J slot index of round r + 1's partner of row a
+        if (sl / QW == h) {
+          double v = gJ[0];
 #pragma unroll
-      for (int i = 0; i < QW; ++i) {
-        const double oI = __shfl_sync(0xffffffffu, gI[i], pa);
-        const double oJ = __shfl_sync(0xffffffffu, gJ[i], pa);
-        gI[i] = fma(sd, oI, cd * gI[i]);
-        gJ[i] = fma(sd, oJ, cd * gJ[i]);
+          for (int i = 1; i < QW; ++i) v = (sl - j0 == i) ? gJ[i] : v;
+          S.apq[lane] = v;
+        }
       }
-    }
-    // slot rotation: new slot BW + j = old slot BW + j + 1 (wrapping inside the J half)
-    xch[h * 32 + lane] = gJ[0];
-    named_bar(bar_id, 128);
-    const double nxt = xch[((h + 1) & 3) * 32 + lane];
+      named_bar(bar_id, 128);
+      const double ng = S.xg[((h + 1) & 3) * 32 + lane];
+      const float nq = S.xq[((h + 1) & 3) * 32 + lane];
 #pragma unroll
-    for (int i = 0; i < QW - 1; ++i) gJ[i] = gJ[i + 1];
-    gJ[QW - 1] = nxt;
+      for (int i = 0; i < QW - 1; ++i) {
+        gJ[i] = gJ[i + 1];
+        qJ[i] = qJ[i + 1];
+      }
+      gJ[QW - 1] = ng;
+      qJ[QW - 1] = nq;
+    }
+  }
+  if (act) {   // slots are back in column order: write Q (swizzled, see qsw)
+    const int sw = qsw(lane);
+    float* qrow = Q + lane * LDQ;
+#pragma unroll
+    for (int i = 0; i < QW; ++i) {
+      qrow[(j0 + i) ^ sw] = qI[i];
+      qrow[(BW + j0 + i) ^ sw] = qJ[i];
+    }
   }
   return rot_any;
 }
 
-// per-owned-pair scratch (doubles): cs (c, s) [BW x 2] | diagonal [PW] | xch [4 x 32]
+// per-owned-pair scratch (doubles): dsm [PW] | apq [BW] | xg [4 x 32] | csd [BW x 2] |
+// xq [4 x 32 floats] | csf [BW x 2 floats]  (the diagonal round reuses csd as its cs and
+// the start of xg as its two "rotated" flags)
 template <int BW>
-__host__ __device__ constexpr int jscr() { return 2 * BW + 2 * BW + 4 * 32; }
+__host__ __device__ constexpr int jscr() { return 2 * BW + BW + 4 * 32 + 2 * BW + (4 * 32 + 2 * BW) / 2; }
+template <int BW>
+__device__ __forceinline__ Cross4Scratch cross4_scratch(double* js) {
+  Cross4Scratch S;
+  S.dsm = js;
+  S.apq = js + 2 * BW;
+  S.xg = js + 3 * BW;
+  S.csd = reinterpret_cast<double2*>(js + 3 * BW + 128);
+  S.xq = reinterpret_cast<float*>(js + 5 * BW + 128);
+  S.csf = reinterpret_cast<float2*>(S.xq + 128);
+  return S;
+}
 
 struct Layout {
   int K2, nblk, Pb, R, nch, rch, ldw, nown;
@@ -346,7 +387,7 @@ __host__ __device__ inline Layout make_layout(int k, int C) {
     L.offGp = take((size_t)C * L.nch * L.nown * P::PACK * 4);
     L.offG = take((size_t)L.nown * P::PW * P::LDQ * 8);   // fp64 inner Gram
     L.offQ = take((size_t)L.nown * P::PW * P::LDQ * 4);
-    L.offQb = take((size_t)P::NQB * P::PW * P::LDQ * 4);
+    L.offQb = L.offG;   // apply-phase staging aliases the fp64 Gram (disjoint lifetimes)
     L.offJ = take((size_t)L.nown * jscr<BW>() * 8);          // inner-round scratch per owned pair
     L.offF = take((size_t)128 * 4);
     L.total = off;
@@ -454,15 +495,15 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
         const int g = gi * C + rank;
         if (gi < nown && g < Pb) {
           double* js = JS + (size_t)gi * jscr<BW>();
-          double2* cs = reinterpret_cast<double2*>(js);
+          const Cross4Scratch S = cross4_scratch<BW>(js);
           int rot_any = 0;
           if (!diag) {
-            rot_any = inner_sweep_cross4<BW>(Gw + (size_t)gi * PW * LDQ, Qw + (size_t)gi * PW * LDQ, tol2, cs,
-                                             js + 2 * BW, js + 2 * BW + PW, lane, h, 1 + gi);
+            rot_any = inner_sweep_cross4<BW>(Gw + (size_t)gi * PW * LDQ, Qw + (size_t)gi * PW * LDQ, tol2, S, lane, h,
+                                             gi & 3, 1 + gi);
           } else if (h < 2) {   // diagonal round: block I by warp 0, block J by warp 1
-            int* rflag = reinterpret_cast<int*>(js + 2 * BW + PW);
+            int* rflag = reinterpret_cast<int*>(S.xg);
             const int rh = inner_sweep_diag<BW>(Gw + (size_t)gi * PW * LDQ, Qw + (size_t)gi * PW * LDQ, h * BW, tol2,
-                                                cs + h * (BW / 2), lane);
+                                                S.csd + h * (BW / 2), lane);
             if (lane == 0) rflag[h] = rh;
             named_bar(1 + gi, 64);
             rot_any = rflag[0] | rflag[1];
@@ -584,7 +625,8 @@ cudaError_t launch_bw(int nb, int k, const float* L, float* Wf, int32_t* status,
   if (C > 8) return cudaErrorInvalidValue;
   const Layout Lo = make_layout<BW>(k, C);
   if (Lo.nown > JB<BW>::MAXOWN || Lo.nown > NT / 128 || Lo.Pb > 128 || Lo.total > 227 * 1024 ||
-      ((Lo.R + 3) / 4) * (JB<BW>::PW / 4) > 2 * NT)
+      ((Lo.R + 3) / 4) * (JB<BW>::PW / 4) > 2 * NT ||
+      (size_t)std::min(JB<BW>::NQB, Lo.Pb) * 4 > (size_t)Lo.nown * 8)   // staged Q fits the aliased Gram
     return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k_jacobi_blk<BW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lo.total);
   if (e != cudaSuccess) return e;

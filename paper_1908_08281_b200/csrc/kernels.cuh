@@ -14,7 +14,8 @@ size_t assemble_keys_bytes(int64_t nnz, int nb);
 
 // philox.cu -- Alg. 1 step 1, reading A6
 // panel: out[i][c][m] = Omega[i*b + m][c] (Omega is N x k, normal index r*k + c)
-cudaError_t launch_omega_panels(uint64_t seed, int nb, int b, int k, float* out, cudaStream_t s, int* launches);
+cudaError_t launch_omega_panels(uint64_t seed, int blk0, int nb, int b, int k, float* out, cudaStream_t s,
+                                int* launches);
 // row-major rows x cols: out[r][c] = normal r*cols + c
 cudaError_t launch_gaussian_rowmajor(uint64_t seed, int rows, int cols, float* out, cudaStream_t s,
                                      int* launches);
@@ -30,7 +31,8 @@ cudaError_t launch_jacobi(int nb, int k, const float* L, float* Wf, int32_t* sta
 
 // finalize.cu -- sigma_j = ||V_w column j|| (fp64), sort, normalise, sign rule
 cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float* Uw_t, float* Ut, float* sigma,
-                            float* Vt, double* sig_raw, int32_t* status, cudaStream_t s, int* launches);
+                            float* Vt, double* sig_raw, int32_t* perm, int32_t* status, cudaStream_t s,
+                            int* launches);
 // apply prep: rs[i][j] = scale / sigma[i][j]; flags singular sigma
 cudaError_t launch_inv_sigma(int nb, int k, const float* sigma, float scale, float* rs, int32_t* status,
                              cudaStream_t s, int* launches);

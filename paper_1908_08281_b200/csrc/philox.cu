@@ -36,8 +36,8 @@ __device__ __forceinline__ void normals4(uint64_t seed, int64_t j, float z[4]) {
   }
 }
 
-// panel = 0: out[n] row-major.  panel = 1: out[(i*k + c)*b + m] with r = i*b + m.
-__global__ void k_gauss(uint64_t seed, int64_t total, int k, int b, int panel, float* __restrict__ out) {
+// Row-major: out[n] = normal n.
+__global__ void k_gauss(uint64_t seed, int64_t total, float* __restrict__ out) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (4 * j >= total) return;
   float z[4];
@@ -45,24 +45,32 @@ __global__ void k_gauss(uint64_t seed, int64_t total, int k, int b, int panel, f
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
     const int64_t n = 4 * j + t;
-    if (n >= total) break;
-    if (!panel) {
-      out[n] = z[t];
-    } else {
-      const int64_t r = n / k;
-      const int c = (int)(n % k);
-      const int64_t i = r / b, m = r % b;
-      out[(i * k + c) * b + m] = z[t];
-    }
+    if (n < total) out[n] = z[t];
   }
+}
+
+// Panels: block i (global blk0 + i) gets out[(i*k + c)*b + m] = Omega[(blk0+i)*b + m][c].
+// k % 4 == 0, so normals 4j..4j+3 share a row: a thread owns (m, c..c+3) and a warp
+// covers 32 consecutive m, i.e. every store instruction writes one 128-byte line.
+__global__ void k_gauss_panel(uint64_t seed, int64_t blk0, int b, int k, float* __restrict__ out) {
+  const int local = blockIdx.x * blockDim.x + threadIdx.x;   // (c/4) * b + m
+  if (local >= b * (k / 4)) return;
+  const int m = local % b, c = 4 * (local / b);
+  const int64_t i = blockIdx.y;
+  const int64_t r = (blk0 + i) * b + m;
+  float z[4];
+  normals4(seed, r * (k / 4) + c / 4, z);
+  float* o = out + (i * k + c) * b + m;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) o[(int64_t)t * b] = z[t];
 }
 
 }  // namespace
 
-cudaError_t launch_omega_panels(uint64_t seed, int nb, int b, int k, float* out, cudaStream_t s, int* launches) {
-  const int64_t total = (int64_t)nb * b * k;
-  const int64_t nblk = (total + 3) / 4;
-  k_gauss<<<(unsigned)((nblk + 255) / 256), 256, 0, s>>>(seed, total, k, b, 1, out);
+cudaError_t launch_omega_panels(uint64_t seed, int blk0, int nb, int b, int k, float* out, cudaStream_t s,
+                                int* launches) {
+  const int per = b * (k / 4);
+  k_gauss_panel<<<dim3((per + 255) / 256, nb), 256, 0, s>>>(seed, blk0, b, k, out);
   ++*launches;
   return cudaGetLastError();
 }
@@ -70,7 +78,7 @@ cudaError_t launch_omega_panels(uint64_t seed, int nb, int b, int k, float* out,
 cudaError_t launch_gaussian_rowmajor(uint64_t seed, int rows, int cols, float* out, cudaStream_t s, int* launches) {
   const int64_t total = (int64_t)rows * cols;
   const int64_t nblk = (total + 3) / 4;
-  k_gauss<<<(unsigned)((nblk + 255) / 256), 256, 0, s>>>(seed, total, cols, 1, 0, out);
+  k_gauss<<<(unsigned)((nblk + 255) / 256), 256, 0, s>>>(seed, total, out);
   ++*launches;
   return cudaGetLastError();
 }

@@ -238,6 +238,25 @@ def test_tiny_inputs_and_k_equals_b():
                 assert rel(F[blk * b:(blk + 1) * b].double().cpu().numpy(), lu) <= F_TOL
 
 
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_stream_parts_bitwise_identical(inputs, cfg, monkeypatch):
+    """hg_solve runs disjoint block ranges on forked streams (HG_STREAMS parts);
+    blocks are independent and Omega is keyed by the global block index, so any
+    part count gives the same bits (3 parts: uneven ranges)."""
+    hg = hgm()
+    h = inputs(cfg)
+    c = CONFIGS[cfg]
+    H, w, Y = dev_inputs(h)
+    out = {}
+    for parts in ("1", "2", "3"):
+        monkeypatch.setenv("HG_STREAMS", parts)
+        F, s, st = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)
+        assert int(st.item()) == 0
+        out[parts] = (F.clone(), s.clone())
+    for parts in ("2", "3"):
+        assert torch.equal(out[parts][0], out["1"][0]) and torch.equal(out[parts][1], out["1"][1]), parts
+
+
 def test_deterministic_and_host_entry(inputs):
     hg = hgm()
     h = inputs(2)
