@@ -172,7 +172,9 @@ hg_status hg_profile_collect(int32_t max_stages, char* names, double* ms, int32_
 /* Diagnostics (device-wide counters since the last reset; synchronous):
  * out[0] near-identity CholeskyQR factorizations, out[1] full ones,
  * out[2] max Jacobi sweeps of any block, out[3] total sweeps, out[4] blocks;
- * with n >= 69, out[5..68] are clock64 phase stamps of the last full Cholesky. */
+ * with n >= 69, out[5..68] are clock64 phase stamps of the last full Cholesky;
+ * with n >= 85, out[69..84] block-Jacobi outer-round stamps; with n >= 133,
+ * out[85..132] block-Jacobi inner-round stamps (a reset call enables them). */
 hg_status hg_debug_counters(int64_t* out, int32_t n, int32_t reset);
 
 /* Number of kernels the last hg_* call on this host thread enqueued. */

@@ -29,10 +29,11 @@ namespace {
 
 constexpr int NT = 512;   // 4 owner warps per owned pair (nown <= 4)
 constexpr int MAX_SWEEPS = 40;
-constexpr size_t SMEM_CAP = 220 * 1024;
 
 __device__ unsigned long long g_jb_dbg[3];   // [0] max sweeps, [1] total sweeps, [2] blocks
 __device__ long long g_jb_clk[16];           // block 0 / rank 0 / thread 0: sweep 1, outer rounds 0-1
+__device__ long long g_jb_iclk[48];          // inner rounds 0-3 of block 0, pair 0, sweep 1, outer round 0
+__device__ int g_jb_iclk_on;                 // set by the caller of the stamps (debug)
 #define JB_CLK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0 && sweep == 1 && ro < 2) g_jb_clk[(i) + 8 * ro] = clock64(); } while (0)
 
 __device__ __forceinline__ void cluster_barrier_jb() {
@@ -203,16 +204,6 @@ __device__ int inner_sweep_diag(const double* G, float* Q, int base, double tol2
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-// named barrier that also ORs a predicate over the participating threads
-__device__ __forceinline__ int named_bar_or(int id, int n, int pred) {
-  int out;
-  asm volatile(
-      "{\n\t.reg .pred pi, po;\n\tsetp.ne.s32 pi, %1, 0;\n\tbar.red.or.pred po, %2, %3, pi;\n\tselp.s32 %0, 1, 0, po;\n\t}"
-      : "=r"(out)
-      : "r"(pred), "r"(id), "r"(n)
-      : "memory");
-  return out;
-}
 
 // Cross rounds of the inner sweep (BW rounds, pairs (j, BW + (j + r) % BW)) by the
 // four warps h = 0..3 of an owner group (128 threads, named barrier bar_id).  Warp h
@@ -234,6 +225,7 @@ struct Cross4Scratch {
   double2* csd;   // [BW] (c, s) fp64
   float* xq;      // [4][32] Q slot exchange
   float2* csf;    // [BW] (c, s) fp32
+  int* flags;     // [2] "round rotates" (by round parity) | [4] per-warp "needs a sweep"
 };
 
 template <int BW>
@@ -261,10 +253,18 @@ __device__ int inner_sweep_cross4(const double* G, float* Q, double tol2, const 
 #pragma unroll
     for (int i = 0; i < QW; ++i) need |= gJ[i] * gJ[i] > tol2 * da * S.dsm[BW + j0 + i];
   }
+  need = __ballot_sync(0xffffffffu, need) != 0u;
+  if (lane == 0) S.flags[2 + h] = need;
+  named_bar(bar_id, 128);
   int rot_any = 0;
-  if (named_bar_or(bar_id, 128, need)) {
+  if (S.flags[2] | S.flags[3] | S.flags[4] | S.flags[5]) {
+    const bool stamp = g_jb_iclk_on && blockIdx.x == 0 && bar_id == 1 && lane == 0;
+    auto ICLK = [&](int r, int i) {
+      if (stamp && r < 4) g_jb_iclk[12 * r + 3 * i + (h == aw ? 0 : (h == ((aw + 1) & 3) ? 1 : 2))] = clock64();
+    };
 #pragma unroll 1
     for (int r = 0; r < BW; ++r) {
+      ICLK(r, 0);
       // angles (warp aw, lane = pair a: rows a and pa = BW + (a + r) % BW)
       int rot = 0;
       if (h == aw && lane < BW) {
@@ -281,7 +281,14 @@ __device__ int inner_sweep_cross4(const double* G, float* Q, double tol2, const 
         S.csd[lane] = make_double2((double)c, (double)sn);
         S.csf[lane] = make_float2(c, sn);
       }
-      if (named_bar_or(bar_id, 128, rot)) {
+      if (h == aw) {   // plain barrier + a flag word: bar.red.or measured ~400 cycles slower
+        const unsigned any = __ballot_sync(0xffffffffu, rot);
+        if (lane == 0) S.flags[r & 1] = any != 0u;
+      }
+      ICLK(r, 1);
+      named_bar(bar_id, 128);
+      if (S.flags[r & 1]) {
+        ICLK(r, 2);
         rot_any = 1;
 #pragma unroll
         for (int i = 0; i < QW; ++i) {   // columns of G and Q: slot pair (j, BW + j)
@@ -321,6 +328,7 @@ __device__ int inner_sweep_cross4(const double* G, float* Q, double tol2, const 
           S.apq[lane] = v;
         }
       }
+      ICLK(r, 3);
       named_bar(bar_id, 128);
       const double ng = S.xg[((h + 1) & 3) * 32 + lane];
       const float nq = S.xq[((h + 1) & 3) * 32 + lane];
@@ -346,10 +354,10 @@ __device__ int inner_sweep_cross4(const double* G, float* Q, double tol2, const 
 }
 
 // per-owned-pair scratch (doubles): dsm [PW] | apq [BW] | xg [4 x 32] | csd [BW x 2] |
-// xq [4 x 32 floats] | csf [BW x 2 floats]  (the diagonal round reuses csd as its cs and
-// the start of xg as its two "rotated" flags)
+// xq [4 x 32 floats] | csf [BW x 2 floats] | flags [6 ints]  (the diagonal round reuses
+// csd as its cs and the start of xg as its two "rotated" flags)
 template <int BW>
-__host__ __device__ constexpr int jscr() { return 2 * BW + BW + 4 * 32 + 2 * BW + (4 * 32 + 2 * BW) / 2; }
+__host__ __device__ constexpr int jscr() { return 2 * BW + BW + 4 * 32 + 2 * BW + (4 * 32 + 2 * BW) / 2 + 4; }
 template <int BW>
 __device__ __forceinline__ Cross4Scratch cross4_scratch(double* js) {
   Cross4Scratch S;
@@ -359,6 +367,7 @@ __device__ __forceinline__ Cross4Scratch cross4_scratch(double* js) {
   S.csd = reinterpret_cast<double2*>(js + 3 * BW + 128);
   S.xq = reinterpret_cast<float*>(js + 5 * BW + 128);
   S.csf = reinterpret_cast<float2*>(S.xq + 128);
+  S.flags = reinterpret_cast<int*>(S.csf + BW);
   return S;
 }
 
@@ -377,22 +386,19 @@ __host__ __device__ inline Layout make_layout(int k, int C) {
   L.R = ((k + C - 1) / C + 3) / 4 * 4;
   L.ldw = L.K2 + 4;
   L.nown = (L.Pb + C - 1) / C;
-  // partial Grams over row chunks of 32 (more Gram tasks); one chunk if shared memory is short
-  for (int pass = 0; pass < 2; ++pass) {
-    L.rch = pass == 0 ? 32 : L.R;
-    L.nch = (L.R + L.rch - 1) / L.rch;
-    size_t off = 0;
-    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) / 16 * 16; return o; };
-    L.offW = take((size_t)L.R * L.ldw * 4);
-    L.offGp = take((size_t)C * L.nch * L.nown * P::PACK * 4);
-    L.offG = take((size_t)L.nown * P::PW * P::LDQ * 8);   // fp64 inner Gram
-    L.offQ = take((size_t)L.nown * P::PW * P::LDQ * 4);
-    L.offQb = L.offG;   // apply-phase staging aliases the fp64 Gram (disjoint lifetimes)
-    L.offJ = take((size_t)L.nown * jscr<BW>() * 8);          // inner-round scratch per owned pair
-    L.offF = take((size_t)128 * 4);
-    L.total = off;
-    if (L.total <= SMEM_CAP) break;
-  }
+  // partial Grams: one per (CTA, owned pair) -- the row split is inside the CTA (phase 1)
+  L.rch = L.R;
+  L.nch = 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) / 16 * 16; return o; };
+  L.offW = take((size_t)L.R * L.ldw * 4);
+  L.offGp = take((size_t)C * L.nown * P::PACK * 4);
+  L.offG = take((size_t)L.nown * P::PW * P::LDQ * 8);   // fp64 inner Gram
+  L.offQ = take((size_t)L.nown * P::PW * P::LDQ * 4);
+  L.offQb = L.offG;   // apply-phase staging aliases the fp64 Gram (disjoint lifetimes)
+  L.offJ = take((size_t)L.nown * jscr<BW>() * 8);          // inner-round scratch per owned pair
+  L.offF = take((size_t)128 * 4);
+  L.total = off;
   return L;
 }
 
@@ -406,7 +412,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
   int rank = 0;
   if (C > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int blk = blockIdx.x / C;
-  const int nblk = Lo.nblk, Pb = Lo.Pb, R = Lo.R, ldw = Lo.ldw, nown = Lo.nown, nch = Lo.nch, rch = Lo.rch;
+  const int nblk = Lo.nblk, Pb = Lo.Pb, R = Lo.R, ldw = Lo.ldw, nown = Lo.nown;
   const int r0 = rank * R;
   const int nr = max(0, min(R, k - r0));
   float* W = reinterpret_cast<float*>(smem_raw + Lo.offW);
@@ -439,19 +445,19 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
     for (int ro = 0; ro < nblk; ++ro) {
       const bool diag = (ro == nblk - 1);
       JB_CLK(0);
-      // ---- 1. partial Grams: (pair, upper 4x4 tile, row chunk) -> owner's Gp[rank][chunk][slot]
-      for (int task = t; task < Pb * UT * nch; task += NT) {
-        const int ch = task % nch, pt = task / nch;
-        const int g = pt / UT;
-        int tt = pt % UT, ta = 0;
+      // ---- 1. partial Grams: (pair, upper 4x4 tile) over this CTA's rows -> owner's Gp[rank][slot]
+      //         (measured faster at configs[3] than 8x8 tiles with in-CTA row splits: 15k vs
+      //         18-21k cycles per outer round)
+      for (int task = t; task < Pb * UT; task += NT) {
+        const int g = task / UT;
+        int tt = task % UT, ta = 0;
         while (tt >= N4 - ta) { tt -= N4 - ta; ++ta; }
         const int tb = ta + tt;
         int I, J;
         blocks_of(ro, g, I, J);
         const int ca = colof(4 * ta, I, J), cb = colof(4 * tb, I, J);
         float acc[4][4] = {};
-        const int rend = min(nr, (ch + 1) * rch);
-        for (int rl = ch * rch; rl < rend; ++rl) {
+        for (int rl = 0; rl < nr; ++rl) {
           const float4 x = *reinterpret_cast<const float4*>(W + rl * ldw + ca);
           const float4 y = *reinterpret_cast<const float4*>(W + rl * ldw + cb);
           const float xa[4] = {x.x, x.y, x.z, x.w}, ya[4] = {y.x, y.y, y.z, y.w};
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
             for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(xa[i], ya[j], acc[i][j]);
         }
         const int owner = g % C, slot = g / C;
-        float* dst = Gp + (((size_t)rank * nch + ch) * nown + slot) * PACK;
+        float* dst = Gp + ((size_t)rank * nown + slot) * PACK;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
         const int lo = min(a, b), hi = max(a, b);
         double sum = 0.0;
         for (int c = 0; c < C; ++c)
-          for (int ch = 0; ch < nch; ++ch) sum += Gp[(((size_t)c * nch + ch) * nown + gi) * PACK + P::pk(lo, hi)];
+          sum += Gp[((size_t)c * nown + gi) * PACK + P::pk(lo, hi)];
         Gw[(size_t)gi * PW * LDQ + a * LDQ + b] = sum;
       }
       __syncthreads();
@@ -648,6 +654,11 @@ cudaError_t launch_bw(int nb, int k, const float* L, float* Wf, int32_t* status,
 }  // namespace
 
 cudaError_t jacobi_blk_clocks(long long* out) { return cudaMemcpyFromSymbol(out, g_jb_clk, sizeof(g_jb_clk)); }
+cudaError_t jacobi_blk_inner_clocks(long long* out, int enable) {
+  cudaError_t e = cudaMemcpyToSymbol(g_jb_iclk_on, &enable, sizeof(int));
+  if (e != cudaSuccess || !out) return e;
+  return cudaMemcpyFromSymbol(out, g_jb_iclk, sizeof(g_jb_iclk));
+}
 
 cudaError_t jacobi_blk_debug(unsigned long long* out, bool reset) {
   cudaError_t e = cudaMemcpyFromSymbol(out, g_jb_dbg, sizeof(g_jb_dbg));

@@ -51,4 +51,6 @@ cudaError_t jacobi_blk_clocks(long long* out);
 bool jacobi_on_l();
 // Uk[blk][j][r] = W_f[blk][r][j] / ||W_f[blk][:, j]||  (fp64 norms; zero columns stay zero)
 cudaError_t launch_unit_columns_t(int nb, int k, const float* Wf, float* Uk, cudaStream_t s, int* launches);
+// debug: inner-round clock stamps of the block Jacobi (enable != 0 switches them on; out may be NULL)
+cudaError_t jacobi_blk_inner_clocks(long long* out, int enable);
 

@@ -84,11 +84,11 @@ def last_launch_count() -> int:
 
 def debug_counters(reset: bool = False) -> dict:
     import numpy as np
-    out = np.zeros(85, dtype=np.int64)
-    _check(_debug_counters(out.ctypes.data_as(_P), 85, int(reset)))
+    out = np.zeros(133, dtype=np.int64)
+    _check(_debug_counters(out.ctypes.data_as(_P), 133, int(reset)))
     return {"chol_near_identity": int(out[0]), "chol_full": int(out[1]), "jacobi_max_sweeps": int(out[2]),
             "jacobi_total_sweeps": int(out[3]), "jacobi_blocks": int(out[4]), "chol_clk": out[5:69].tolist(),
-            "jac_clk": out[69:85].tolist()}
+            "jac_clk": out[69:85].tolist(), "jac_inner_clk": out[85:133].tolist()}
 
 
 def profile_enable(on: bool = True):

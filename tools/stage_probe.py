@@ -54,6 +54,11 @@ def main():
     if clk[0]:
         base = clk[0]
         dbg["chol_phases_kcyc"] = {i: round((v - base) / 1e3, 1) for i, v in enumerate(clk) if v}
+    ic = dbg.pop("jac_inner_clk")
+    if any(ic):
+        base = min(x for x in ic if x)
+        dbg["jac_inner_cyc"] = [[ic[12 * r + 3 * i + w] - base if ic[12 * r + 3 * i + w] else None for i in range(4)
+                                 for w in range(3)] for r in range(4)]
     jc = dbg.pop("jac_clk")
     if jc[0]:
         dbg["jac_round_cyc"] = [jc[i] - jc[0] for i in range(16)]
