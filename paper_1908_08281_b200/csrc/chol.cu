@@ -49,7 +49,11 @@ __device__ void tile_potrf(float* T, int lane, int32_t* status, bool& bad) {
       bad = true;
       d = 1.f;
     }
-    const float s = __fsqrt_rn(d), inv = __frcp_rn(s);
+    // 1/sqrt(d) from MUFU.RSQ + one Newton step (~1 ulp; the IEEE __fsqrt_rn /
+    // __frcp_rn sequences made the 32-step chain ~3x longer), sqrt(d) = d / sqrt(d)
+    float inv = rsqrtf(d);
+    inv = inv * fmaf(-0.5f * d * inv, inv, 1.5f);
+    const float s = d * inv;
     if (lane == c) a[c] = s;
     if (lane > c) a[c] *= inv;
 #pragma unroll 31
@@ -72,10 +76,10 @@ __device__ void tile_trsm(float* A, const float* L, int lane) {
   const float rd = __frcp_rn(L[lane * LDT + lane]);     // lane c: 1 / L[c][c]
 #pragma unroll
   for (int c = 0; c < TS; ++c) {
-    float x = a[c];
+    float x[4] = {a[c], 0.f, 0.f, 0.f};   // four independent chains (fixed order)
 #pragma unroll
-    for (int t = 0; t < c; ++t) x = fmaf(-a[t], L[c * LDT + t], x);
-    a[c] = x * __shfl_sync(0xffffffffu, rd, c);
+    for (int t = 0; t < c; ++t) x[t & 3] = fmaf(-a[t], L[c * LDT + t], x[t & 3]);
+    a[c] = ((x[0] + x[1]) + (x[2] + x[3])) * __shfl_sync(0xffffffffu, rd, c);
   }
 #pragma unroll
   for (int t = 0; t < TS; ++t) A[lane * LDT + t] = a[t];
@@ -165,11 +169,11 @@ __device__ void tile_trtri(float* T, int lane) {
     } else if (r == c) {
       x[r] = rr;
     } else {
-      float acc = 0.f;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};   // four independent chains (fixed order)
 #pragma unroll
       for (int t = 0; t < r; ++t)
-        if (t >= c) acc = fmaf(T[r * LDT + t], x[t], acc);
-      x[r] = -acc * rr;
+        if (t >= c) acc[t & 3] = fmaf(T[r * LDT + t], x[t], acc[t & 3]);
+      x[r] = -((acc[0] + acc[1]) + (acc[2] + acc[3])) * rr;
     }
   }
   __syncwarp();
