@@ -62,6 +62,7 @@ struct Cfg {
   static constexpr uint32_t TX = (uint32_t)(BM + BN) * BK * 4;
   static constexpr int HALF = BN / 2;           // columns per epilogue warp
   static_assert(8 * 32 * (HALF + 4) * 4 <= STAGES * STAGE_BYTES, "epilogue staging must fit the pipeline smem");
+  static_assert(8 * HALF * 36 * 4 <= STAGES * STAGE_BYTES, "transposed staging must fit the pipeline smem");
 };
 
 // kind::tf32 instruction descriptor: D f32, A/B tf32, M = 128, N = BN.
@@ -273,7 +274,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     float* Dg = ea.D + (int64_t)g * ea.sd;
     const int nb0 = n0 + h * C::HALF;
     if (ea.d_trans) {
-      if (m < ea.M) {
+      const int mw0 = m0 + q * 32;   // this warp's 32 rows m
+      const bool fast = !ea.cs && (ea.ldd & 3) == 0 && ((reinterpret_cast<uintptr_t>(Dg) & 15) == 0) &&
+                        mw0 + 32 <= ea.M;
+      if (fast) {
+        // stage the warp's HALF x 32 block transposed (st[j][lane], pitch 36), then store
+        // D[n][m] rows as float4: 8 lanes cover one row's 32 m, four rows per instruction
+        constexpr int TP = 36;
+        float* st = reinterpret_cast<float*>(base) + warp * C::HALF * TP;
+#pragma unroll
+        for (int j = 0; j < C::HALF; ++j) st[j * TP + lane] = acc[j] * rsv;
+        __syncwarp();
+        const int l4 = lane & 7;
+        float* dcol = Dg + mw0 + 4 * l4;
+        for (int j = lane >> 3; j < C::HALF; j += 4) {
+          const int n = nb0 + j;
+          if (n < ea.N)
+            *reinterpret_cast<float4*>(dcol + (int64_t)n * ea.ldd) = *reinterpret_cast<const float4*>(st + j * TP + 4 * l4);
+        }
+      } else if (m < ea.M) {
 #pragma unroll
         for (int j = 0; j < C::HALF; ++j) {
           const int n = nb0 + j;
