@@ -39,10 +39,14 @@ const char* const kStageNames[ST_COUNT] = {"degrees", "assemble", "omega", "gemm
                                            "gemm_qform", "gemm_svd", "gemm_apply", "cholinv", "jacobi",
                                            "finalize", "inv_sigma"};
 struct ProfRec {
-  int stage;
+  int stage, part;
   cudaEvent_t a, b;
 };
 thread_local bool g_prof_on = false;
+thread_local int g_prof_mode = 0;                 // 1: per-stage totals (parts in sequence), 2: timeline
+thread_local int g_cur_part = 0;
+thread_local cudaEvent_t g_t0 = nullptr;          // timeline origin (first solve since the last collect)
+thread_local bool g_t0_set = false;
 thread_local std::vector<ProfRec> g_prof;
 thread_local std::vector<cudaEvent_t> g_evpool;
 thread_local int g_cur_stage = -1;
@@ -64,6 +68,7 @@ struct ProfScope {
   ProfScope(int stage, cudaStream_t st) : on(g_prof_on), s(st) {
     if (!on) return;
     r.stage = stage;
+    r.part = g_cur_part;
     r.a = prof_event();
     r.b = prof_event();
     cudaEventRecord(r.a, s);
@@ -178,6 +183,15 @@ hg_status gemm(const GemmDesc& g, cudaStream_t s, bool simt, const char* what, i
 }
 
 // ---------------------------------------------------------------- stages
+// N-tile cap per GEMM role (HG_BN_POWER / HG_BN_GRAM / HG_BN_QFORM; 256 = widest).  The
+// per-part chains are latency-bound while the GPU has idle SMs, so narrower tiles (more
+// CTAs for the same MACs) can shorten a launch.
+static int bn_env(const char* name, int dflt) {
+  const char* v = getenv(name);
+  const int x = v ? atoi(v) : dflt;
+  return x >= 256 ? 256 : x >= 128 ? 128 : x >= 64 ? 64 : 32;
+}
+
 struct Rsvd {
   int nb, b, k;
   bool simt;
@@ -191,6 +205,7 @@ struct Rsvd {
     g.A = X; g.a_mn = false; g.lda = b; g.sa = (int64_t)b * b;
     g.B = P_t; g.b_mn = false; g.ldb = b; g.sb = (int64_t)k * b;
     g.D = out_t; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
+    g.bn_max = bn_env("HG_BN_POWER", 256);
     return gemm(g, s, simt, "power product X*S", ST_GEMM_POWER);
   }
   // G = P^T P (k x k)
@@ -200,6 +215,7 @@ struct Rsvd {
     g.A = P_t; g.a_mn = false; g.lda = b; g.sa = (int64_t)k * b;
     g.B = P_t; g.b_mn = false; g.ldb = b; g.sb = (int64_t)k * b;
     g.D = G; g.d_trans = false; g.ldd = k; g.sd = (int64_t)k * k;
+    g.bn_max = bn_env("HG_BN_GRAM", 256);
     return gemm(g, s, simt, "Gram P^T P", ST_GEMM_GRAM);
   }
   // Q = P L^-T  ->  Q_t
@@ -209,6 +225,7 @@ struct Rsvd {
     g.A = P_t; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
     g.B = Linv; g.b_mn = false; g.ldb = k; g.sb = (int64_t)k * k;
     g.D = Q_t; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
+    g.bn_max = bn_env("HG_BN_QFORM", 256);
     return gemm(g, s, simt, "Q = Y R^-1", ST_GEMM_QFORM);
   }
 };
@@ -366,22 +383,30 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
   return HG_OK;
 }
 
+hg_status run_degrees(const hg_incidence* H, const float* w, float* dvr, int32_t* st, void* ws, const Layout& Lo,
+                      cudaStream_t s) {
+  ProfScope ps(ST_DEGREES, s);
+  HG_CU(launch_degrees(H->n_vertices, H->n_edges, H->nnz, H->row_ptr, H->col_idx, w, at<int32_t>(ws, Lo.de),
+                       at<float>(ws, Lo.eval), dvr, st, s, &g_launches),
+        "degrees");
+  return HG_OK;
+}
+
+// Eq. 1 blocks [blk0, blk0 + nb) of the N/b diagonal blocks (degrees already computed)
+hg_status run_assemble(const hg_incidence* H, float mu, int b, bool raw, int blk0, int nb, float* blocks,
+                       const float* dvr, void* ws, const Layout& Lo, cudaStream_t s) {
+  ProfScope ps(ST_ASSEMBLE, s);
+  HG_CU(launch_assemble(blk0, nb, H->n_vertices / b, b, H->n_edges, H->nnz, H->row_ptr, H->col_idx,
+                        at<float>(ws, Lo.eval), dvr, mu, raw, blocks, at<void>(ws, Lo.keys), s, &g_launches),
+        "assemble");
+  return HG_OK;
+}
+
 hg_status run_theta(const hg_incidence* H, const float* w, float mu, int b, bool raw, float* blocks, float* dvr_out,
                     int32_t* st, void* ws, const Layout& Lo, cudaStream_t s) {
   float* dvr = dvr_out ? dvr_out : at<float>(ws, Lo.dvr);
-  {
-    ProfScope ps(ST_DEGREES, s);
-    HG_CU(launch_degrees(H->n_vertices, H->n_edges, H->nnz, H->row_ptr, H->col_idx, w, at<int32_t>(ws, Lo.de),
-                         at<float>(ws, Lo.eval), dvr, st, s, &g_launches),
-          "degrees");
-  }
-  {
-    ProfScope ps(ST_ASSEMBLE, s);
-    HG_CU(launch_assemble(H->n_vertices / b, b, H->n_edges, H->nnz, H->row_ptr, H->col_idx, at<float>(ws, Lo.eval),
-                          dvr, mu, raw, blocks, at<void>(ws, Lo.keys), s, &g_launches),
-          "assemble");
-  }
-  return HG_OK;
+  HG_TRY(run_degrees(H, w, dvr, st, ws, Lo, s));
+  return run_assemble(H, mu, b, raw, 0, H->n_vertices / b, blocks, dvr, ws, Lo, s);
 }
 
 hg_status check_H(const hg_incidence* H) {
@@ -400,7 +425,36 @@ extern "C" {
 const char* hg_last_error(void) { return g_err.c_str(); }
 
 hg_status hg_profile_enable(int32_t on) {
-  g_prof_on = on != 0;
+  g_prof_mode = on < 0 ? 0 : (on > 2 ? 2 : on);
+  g_prof_on = g_prof_mode != 0;
+  return HG_OK;
+}
+
+hg_status hg_profile_timeline(int32_t max_rec, int32_t* stage, int32_t* part, double* t_start_ms, double* t_end_ms,
+                              int32_t* n_out) {
+  g_err.clear();
+  if (!n_out) return fail(HG_ERR_INVALID, "n_out is NULL");
+  int n = 0;
+  for (auto& r : g_prof) {
+    float a = 0.f, b = 0.f;
+    HG_CU(cudaEventSynchronize(r.b), "timeline sync");
+    if (g_t0_set) {
+      HG_CU(cudaEventElapsedTime(&a, g_t0, r.a), "timeline elapsed");
+      HG_CU(cudaEventElapsedTime(&b, g_t0, r.b), "timeline elapsed");
+    }
+    if (n < max_rec) {
+      if (stage) stage[n] = r.stage;
+      if (part) part[n] = r.part;
+      if (t_start_ms) t_start_ms[n] = a;
+      if (t_end_ms) t_end_ms[n] = b;
+    }
+    ++n;
+    g_evpool.push_back(r.a);
+    g_evpool.push_back(r.b);
+  }
+  g_prof.clear();
+  g_t0_set = false;
+  *n_out = n;
   return HG_OK;
 }
 
@@ -603,24 +657,33 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   float* Ut = at<float>(ws, Lo.Ut);
   float* Vt = at<float>(ws, Lo.Vt);
   float* sigma = sigma_out ? sigma_out : at<float>(ws, Lo.sigma);
-  HG_TRY(run_theta(H, w, mu, b, false, blocks, nullptr, st, ws, Lo, s));
-  // Blocks are independent (reading A5): the rSVD + apply of disjoint block ranges run
+  float* dvr = at<float>(ws, Lo.dvr);
+  HG_TRY(run_degrees(H, w, dvr, st, ws, Lo, s));
+  // Blocks are independent (reading A5): the assembly, rSVD and apply of disjoint block ranges run
   // on forked streams, so one part's tensor-core GEMMs fill the SMs that the other
   // part's latency-bound Cholesky / Jacobi leave idle.  Bitwise the same result for
   // any part count (Omega is keyed by the global block index).  One part while the
   // stage profiler is on (per-stage attribution needs sequential stages).
-  const int nparts = g_prof_on ? 1 : std::max(1, std::min(solve_parts(), nb));
+  const int nparts = g_prof_mode == 1 ? 1 : std::max(1, std::min(solve_parts(), nb));
+  if (g_prof_mode == 2 && !g_t0_set) {
+    if (!g_t0) HG_CU(cudaEventCreate(&g_t0), "event create");
+    HG_CU(cudaEventRecord(g_t0, s), "t0 record");
+    g_t0_set = true;
+  }
   cudaStream_t ps[kMaxParts];
   HG_TRY(fork_streams(s, nparts, ps));
   for (int p = 0; p < nparts; ++p) {
     const int blk0 = (int)((int64_t)nb * p / nparts), nbp = (int)((int64_t)nb * (p + 1) / nparts) - blk0;
     const int64_t kb = (int64_t)blk0 * k * b;
     const Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, k, T);
+    g_cur_part = p;
+    HG_TRY(run_assemble(H, mu, b, false, blk0, nbp, blocks, dvr, ws, Lo, ps[p]));
     HG_TRY(run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, k, q, seed, simt, Ut + kb, sigma + (int64_t)blk0 * k,
                     Vt + kb, st, Bf, ps[p]));
     HG_TRY(run_apply(Ut + kb, sigma + (int64_t)blk0 * k, Vt + kb, nbp, b, k, T > 0 ? Y + (int64_t)blk0 * b * T : Y, T,
                      mu / (1.0f + mu), T > 0 ? F + (int64_t)blk0 * b * T : F, st, Bf, ps[p], simt));
   }
+  g_cur_part = 0;
   HG_TRY(join_streams(s, nparts, ps));
   if (flags & HG_SYNC) {
     int32_t h = 0;

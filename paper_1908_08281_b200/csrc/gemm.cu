@@ -472,8 +472,9 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
     gemm_simt_kernel<<<grid, 256, 0, stream>>>(g.A, ea.a_mn, g.lda, g.sa, g.B, ea.b_mn, g.ldb, g.sb, ea);
     return cudaGetLastError();
   }
-  if (g.N <= 32) return launch_tc<32>(g, ea, stream);
-  if (g.N <= 64) return launch_tc<64>(g, ea, stream);
-  if (g.N <= 128) return launch_tc<128>(g, ea, stream);
+  const int n = g.N < g.bn_max ? g.N : g.bn_max;
+  if (n <= 32) return launch_tc<32>(g, ea, stream);
+  if (n <= 64) return launch_tc<64>(g, ea, stream);
+  if (n <= 128) return launch_tc<128>(g, ea, stream);
   return launch_tc<256>(g, ea, stream);
 }

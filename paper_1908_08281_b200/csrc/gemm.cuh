@@ -23,6 +23,7 @@ struct GemmDesc {
   int64_t srs = 0;
   const float* cs = nullptr;
   int64_t scs = 0;
+  int bn_max = 256;   // widest N tile to use (smaller tiles = more CTAs for small outputs)
 };
 
 // Enqueue the GEMM; returns cudaSuccess or the launch error.  `simt` selects the

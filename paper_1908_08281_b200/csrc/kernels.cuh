@@ -7,9 +7,9 @@
 cudaError_t launch_degrees(int N, int E, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
                            int32_t* de_cnt, float* edge_val, float* dv_rsqrt, int32_t* status,
                            cudaStream_t s, int* launches);
-cudaError_t launch_assemble(int nb, int b, int E, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
-                            const float* edge_val, const float* dv_rsqrt, float mu, bool raw_theta, float* blocks,
-                            void* keys_ws, cudaStream_t s, int* launches);
+cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_t nnz, const int64_t* row_ptr,
+                            const int32_t* col_idx, const float* edge_val, const float* dv_rsqrt, float mu,
+                            bool raw_theta, float* blocks, void* keys_ws, cudaStream_t s, int* launches);
 size_t assemble_keys_bytes(int64_t nnz, int nb);
 
 // philox.cu -- Alg. 1 step 1, reading A6

@@ -19,7 +19,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
-cudaError_t launch_assemble_tiles(int nb, int b, const int64_t* row_ptr, const int32_t* col_idx,
+cudaError_t launch_assemble_tiles(int blk0, int nb, int b, const int64_t* row_ptr, const int32_t* col_idx,
                                   const float* edge_val, const float* dv_rsqrt, float mu, bool raw_theta,
                                   float* blocks, const int32_t* overflow, cudaStream_t s, int* launches);
 
@@ -73,12 +73,12 @@ struct AsmSmem {
 
 __device__ __forceinline__ int hslot(int e) { return (int)(((unsigned)e * 2654435761u) >> 20) & (HCAP - 1); }
 
-__global__ void __launch_bounds__(NT) k_assemble(int b, const int64_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(NT) k_assemble(int blk0, int b, const int64_t* __restrict__ row_ptr,
                                                  const int32_t* __restrict__ col,
                                                  const float* __restrict__ eval, const float* __restrict__ dvr,
                                                  float inv1pmu, int raw, float* __restrict__ blocks,
                                                  const int32_t* __restrict__ overflow) {
-  const int blk = blockIdx.z;
+  const int blk = blk0 + blockIdx.z;
   if (overflow && !overflow[blk]) return;     // block assembled by the sorted-CSC path
   extern __shared__ __align__(16) uint8_t smem_raw[];
   AsmSmem& S = *reinterpret_cast<AsmSmem*>(smem_raw);
@@ -192,13 +192,13 @@ constexpr int SEG_CAP = 16384;      // keys per segment in shared memory (64 KB)
 constexpr int ROWS_NT = 1024;
 constexpr int KEY_SMEM_CAP = 24576; // block keys cached in shared memory (96 KB)
 
-__global__ void __launch_bounds__(1024) k_seg_sort(int b, const int64_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(1024) k_seg_sort(int blk0, int b, const int64_t* __restrict__ row_ptr,
                                                    const int32_t* __restrict__ col, uint32_t* __restrict__ keys,
                                                    int32_t* __restrict__ overflow) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   int64_t* vp = reinterpret_cast<int64_t*>(smem_raw);                    // [SEG_V + 1]
   uint32_t* sk = reinterpret_cast<uint32_t*>(smem_raw + (SEG_V + 2) * 8);  // [SEG_CAP]
-  const int blk = blockIdx.x, seg = blockIdx.y, t = threadIdx.x;
+  const int blk = blk0 + blockIdx.x, seg = blockIdx.y, t = threadIdx.x;
   const int64_t vb = (int64_t)blk * b + (int64_t)seg * SEG_V;
   const int nv = min(SEG_V, b - seg * SEG_V);
   if (nv <= 0) return;
@@ -248,14 +248,14 @@ __device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_
   return lo;
 }
 
-__global__ void __launch_bounds__(ROWS_NT, 1) k_assemble_rows(int b, int TR, const int64_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(ROWS_NT, 1) k_assemble_rows(int blk0, int b, int TR, const int64_t* __restrict__ row_ptr,
                                                              const int32_t* __restrict__ col,
                                                              const uint32_t* __restrict__ keys,
                                                              const float* __restrict__ eval,
                                                              const float* __restrict__ dvr, float inv1pmu, int raw,
                                                              float* __restrict__ blocks,
                                                              const int32_t* __restrict__ overflow) {
-  const int blk = blockIdx.x;
+  const int blk = blk0 + blockIdx.x;
   if (overflow[blk]) return;                      // handled by the hashed-tile kernel
   extern __shared__ __align__(16) uint8_t smem_raw[];
   float* acc = reinterpret_cast<float*>(smem_raw);                       // [TR][b]
@@ -339,15 +339,16 @@ size_t assemble_keys_bytes(int64_t nnz, int nb) { return (size_t)nnz * 4 + (size
 
 // keys: nnz uint32 + nb int32 overflow flags (workspace).  E*b must be < 2^32 for the
 // sorted path (32-bit keys); otherwise every block takes the hashed-tile kernel.
-cudaError_t launch_assemble(int nb, int b, int E, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
-                            const float* edge_val, const float* dv_rsqrt, float mu, bool raw_theta, float* blocks,
-                            void* keys_ws, cudaStream_t s, int* launches) {
+cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_t nnz, const int64_t* row_ptr,
+                            const int32_t* col_idx, const float* edge_val, const float* dv_rsqrt, float mu,
+                            bool raw_theta, float* blocks, void* keys_ws, cudaStream_t s, int* launches) {
   uint32_t* keys = reinterpret_cast<uint32_t*>(keys_ws);
   int32_t* overflow = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(keys_ws) + ((size_t)nnz * 4 + 255) / 256 * 256);
   // HG_ASSEMBLE=tiles forces the hashed-tile kernel (verification: both paths are bit-identical)
   const char* force = getenv("HG_ASSEMBLE");
   const bool sorted_ok = (uint64_t)E * (uint64_t)b < (1ull << 32) && b <= 4 * SEG_V && !(force && force[0] == 't');
-  cudaError_t e = cudaMemsetAsync(overflow, sorted_ok ? 0 : 1, sizeof(int32_t) * nb, s);
+  (void)nb_total;
+  cudaError_t e = cudaMemsetAsync(overflow + blk0, sorted_ok ? 0 : 1, sizeof(int32_t) * nb, s);
   if (e != cudaSuccess) return e;
   if (sorted_ok) {
     const int nseg = (b + SEG_V - 1) / SEG_V;
@@ -358,7 +359,7 @@ cudaError_t launch_assemble(int nb, int b, int E, int64_t nnz, const int64_t* ro
       if (e != cudaSuccess) return e;
       attr1 = true;
     }
-    k_seg_sort<<<dim3(nb, nseg), 1024, ssmem, s>>>(b, row_ptr, col_idx, keys, overflow);
+    k_seg_sort<<<dim3(nb, nseg), 1024, ssmem, s>>>(blk0, b, row_ptr, col_idx, keys, overflow);
     int TR = 32768 / b;
     if (TR > 32) TR = 32;
     if (TR < 1) TR = 1;
@@ -369,16 +370,16 @@ cudaError_t launch_assemble(int nb, int b, int E, int64_t nnz, const int64_t* ro
       if (e != cudaSuccess) return e;
       attr2 = smem;
     }
-    k_assemble_rows<<<dim3(nb, (b + TR - 1) / TR), ROWS_NT, smem, s>>>(b, TR, row_ptr, col_idx, keys, edge_val,
+    k_assemble_rows<<<dim3(nb, (b + TR - 1) / TR), ROWS_NT, smem, s>>>(blk0, b, TR, row_ptr, col_idx, keys, edge_val,
                                                                       dv_rsqrt, 1.0f / (1.0f + mu),
                                                                       raw_theta ? 1 : 0, blocks, overflow);
     *launches += 2;
   }
-  return launch_assemble_tiles(nb, b, row_ptr, col_idx, edge_val, dv_rsqrt, mu, raw_theta, blocks, overflow, s,
+  return launch_assemble_tiles(blk0, nb, b, row_ptr, col_idx, edge_val, dv_rsqrt, mu, raw_theta, blocks, overflow, s,
                                launches);
 }
 
-cudaError_t launch_assemble_tiles(int nb, int b, const int64_t* row_ptr, const int32_t* col_idx,
+cudaError_t launch_assemble_tiles(int blk0, int nb, int b, const int64_t* row_ptr, const int32_t* col_idx,
                                   const float* edge_val, const float* dv_rsqrt, float mu, bool raw_theta,
                                   float* blocks, const int32_t* overflow, cudaStream_t s, int* launches) {
   static bool attr = false;
@@ -389,7 +390,7 @@ cudaError_t launch_assemble_tiles(int nb, int b, const int64_t* row_ptr, const i
     attr = true;
   }
   dim3 grid((b + TV - 1) / TV, (b + TU - 1) / TU, nb);
-  k_assemble<<<grid, NT, smem, s>>>(b, row_ptr, col_idx, edge_val, dv_rsqrt, 1.0f / (1.0f + mu), raw_theta ? 1 : 0,
+  k_assemble<<<grid, NT, smem, s>>>(blk0, b, row_ptr, col_idx, edge_val, dv_rsqrt, 1.0f / (1.0f + mu), raw_theta ? 1 : 0,
                                     blocks, overflow);
   ++*launches;
   return cudaGetLastError();

@@ -59,12 +59,13 @@ _gemm = _sig("hg_gemm", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i32, _i64, _i
 _last_error = _sig("hg_last_error", ctypes.c_char_p)
 _prof_enable = _sig("hg_profile_enable", ctypes.c_int, _i32)
 _prof_collect = _sig("hg_profile_collect", ctypes.c_int, _i32, _P, _P, _P, ctypes.POINTER(_i32))
+_prof_timeline = _sig("hg_profile_timeline", ctypes.c_int, _i32, _P, _P, _P, _P, ctypes.POINTER(_i32))
 _last_launches = _sig("hg_last_launch_count", ctypes.c_int32)
 _debug_counters = _sig("hg_debug_counters", ctypes.c_int, _P, _i32, _i32)
 
 EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_rsvd", "hg_block_apply_inverse",
            "hg_solve", "hg_solve_host", "hg_gemm", "hg_last_error", "hg_last_launch_count", "hg_profile_enable",
-           "hg_profile_collect", "hg_debug_counters")
+           "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters")
 
 
 class HGError(RuntimeError):
@@ -91,8 +92,27 @@ def debug_counters(reset: bool = False) -> dict:
             "jac_clk": out[69:85].tolist(), "jac_inner_clk": out[85:133].tolist()}
 
 
-def profile_enable(on: bool = True):
-    _check(_prof_enable(1 if on else 0))
+STAGES = ("degrees", "assemble", "omega", "gemm_power", "gemm_gram", "gemm_qform", "gemm_svd", "gemm_apply",
+          "cholinv", "jacobi", "finalize", "inv_sigma")
+
+
+def profile_enable(on=True):
+    """on: False/0 off, True/1 per-stage totals (stream parts in sequence), 2 timeline."""
+    _check(_prof_enable(int(on)))
+
+
+def profile_timeline(max_rec: int = 4096):
+    """[(stage, part, start_ms, end_ms)] since the first hg_solve after the last collect."""
+    import numpy as np
+    st = np.zeros(max_rec, np.int32)
+    pa = np.zeros(max_rec, np.int32)
+    t0 = np.zeros(max_rec, np.float64)
+    t1 = np.zeros(max_rec, np.float64)
+    n = _i32(0)
+    _check(_prof_timeline(max_rec, st.ctypes.data_as(_P), pa.ctypes.data_as(_P), t0.ctypes.data_as(_P),
+                          t1.ctypes.data_as(_P), ctypes.byref(n)))
+    m = min(n.value, max_rec)
+    return [(STAGES[st[i]], int(pa[i]), float(t0[i]), float(t1[i])) for i in range(m)]
 
 
 def profile_collect() -> dict:
