@@ -128,8 +128,8 @@ hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const floa
  * unless flags has HG_SYNC (then the stream is synchronised and a non-zero
  * *d_status returns HG_ERR_NUMERICAL).  d_status may be NULL only with HG_SYNC
  * (a word inside ws is used).
- * Concurrency: after the assembly, disjoint block ranges (HG_STREAMS parts,
- * default 2, at most 4) run their rSVD + apply on library-owned non-blocking
+ * Concurrency: after the degrees, disjoint block ranges (HG_STREAMS parts,
+ * default 4, at most 4) run their assembly, rSVD and apply on library-owned non-blocking
  * streams forked from and joined back into `stream` with events, so all work
  * is still ordered after prior work on `stream` and before later work (also
  * under stream capture).  The result is bitwise independent of the part count. */
@@ -141,6 +141,10 @@ hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, i
  * host->device, solves, copies F (and sigma_out if non-NULL) device->host,
  * synchronises.  ws (device) is caller-provided as above; host buffers should
  * be pinned for full copy bandwidth.  Returns the device status. */
+/* hg_solve from host buffers (pinned for full copy bandwidth): H and w are uploaded
+ * first; Y's rows are uploaded per part on a library copy stream and each part waits
+ * for its slice only before its apply (the upload overlaps the rSVD); each part
+ * downloads its F rows right after its apply.  Synchronous; returns the status. */
 hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_ptr_host,
                         const int32_t* col_idx_host, const float* w_host, float mu, int32_t b, int32_t k,
                         int32_t q, uint64_t seed, const float* Y_host, int32_t T, float* F_host,
@@ -168,6 +172,15 @@ hg_status hg_gemm(int32_t M, int32_t N, int32_t K, int32_t batch, const float* A
  * finalize, inv_sigma.  Host pointers. */
 hg_status hg_profile_enable(int32_t on);
 hg_status hg_profile_collect(int32_t max_stages, char* names, double* ms, int32_t* counts, int32_t* n_out);
+
+/* Timeline mode: hg_profile_enable(2) keeps hg_solve's stream parts concurrent
+ * (mode 1 runs them in sequence so per-stage totals do not overlap) and
+ * records, per stage launch group, its part and start / end in ms from the
+ * start of the first hg_solve since the last collect.  hg_profile_timeline
+ * writes up to max_rec records (stage ids in the order listed above), sets
+ * *n_out to the number recorded and clears the record.  Host pointers. */
+hg_status hg_profile_timeline(int32_t max_rec, int32_t* stage, int32_t* part, double* t_start_ms, double* t_end_ms,
+                              int32_t* n_out);
 
 /* Diagnostics (device-wide counters since the last reset; synchronous):
  * out[0] near-identity CholeskyQR factorizations, out[1] full ones,
