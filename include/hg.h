@@ -138,13 +138,12 @@ hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, i
                    int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
 
 /* hg_solve from HOST buffers (end-to-end entry): copies row_ptr, col_idx, w, Y
- * host->device, solves, copies F (and sigma_out if non-NULL) device->host,
+ * host->device, solves, copies F (and sigma_host if non-NULL) device->host,
  * synchronises.  ws (device) is caller-provided as above; host buffers should
- * be pinned for full copy bandwidth.  Returns the device status. */
-/* hg_solve from host buffers (pinned for full copy bandwidth): H and w are uploaded
- * first; Y's rows are uploaded per part on a library copy stream and each part waits
+ * be pinned for full copy bandwidth.  H and w are uploaded first on `stream`;
+ * Y's rows are uploaded per part on a library copy stream and each part waits
  * for its slice only before its apply (the upload overlaps the rSVD); each part
- * downloads its F rows right after its apply.  Synchronous; returns the status. */
+ * downloads its F rows right after its apply.  Returns the device status. */
 hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_ptr_host,
                         const int32_t* col_idx_host, const float* w_host, float mu, int32_t b, int32_t k,
                         int32_t q, uint64_t seed, const float* Y_host, int32_t T, float* F_host,
