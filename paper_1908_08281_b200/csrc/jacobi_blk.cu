@@ -83,6 +83,21 @@ struct JB {
   __host__ __device__ static int pk(int a, int b) { return a * PW - (a * (a - 1)) / 2 + (b - a); }   // a <= b
 };
 
+// An owned pair's fp64 Gram entry (a, b) read straight from the C packed fp32 partials
+// (one per cluster CTA, summed in rank order): the inner sweeps load their registers
+// from here, no separate fp64 Gram pass.
+template <int BW>
+struct GramSrc {
+  const float* Gp;   // partials of this pair: Gp[c * stride + pk(lo, hi)]
+  int C, stride;
+  __device__ __forceinline__ double operator()(int a, int b) const {
+    const int idx = JB<BW>::pk(min(a, b), max(a, b));
+    double s = 0.0;
+    for (int c = 0; c < C; ++c) s += Gp[(size_t)c * stride + idx];
+    return s;
+  }
+};
+
 // Q layout in shared memory (pitch LDQ): element (a, j) at a * LDQ + (j ^ qsw(a)).  The
 // XOR stays inside aligned groups of 4 (float4 rows stay float4 rows, permuted) and
 // makes the lane-per-row column accesses of the inner rounds bank-conflict free.
@@ -121,7 +136,7 @@ template <int BW>
 __device__ __forceinline__ int diag_col(int s, int r) { return s == 0 ? 0 : 1 + (s - 1 + r) % (BW - 1); }
 
 template <int BW>
-__device__ int inner_sweep_diag(const double* G, float* Q, int base, double tol2, double2* cs, int lane) {
+__device__ int inner_sweep_diag(const GramSrc<BW>& G, float* Q, int base, double tol2, double2* cs, int lane) {
   constexpr int PW = 2 * BW, LDQ = JB<BW>::LDQ;
   const bool act = lane < BW;
   const int row = base + (act ? lane : 0);
@@ -129,12 +144,12 @@ __device__ int inner_sweep_diag(const double* G, float* Q, int base, double tol2
   float* qrow = Q + row * LDQ;
   double g[BW];
 #pragma unroll
-  for (int j = 0; j < BW; ++j) g[j] = act ? G[row * LDQ + base + j] : 0.0;   // round 0: slot j = column j
+  for (int j = 0; j < BW; ++j) g[j] = act ? G(row, base + j) : 0.0;   // round 0: slot j = column j
   if (act) {
 #pragma unroll
     for (int j = 0; j < PW; ++j) qrow[j ^ sw] = (j == row) ? 1.f : 0.f;
   }
-  double d = act ? G[row * LDQ + row] : 1.0;
+  double d = act ? G(row, row) : 1.0;
   {  // no pair of the block above the threshold: nothing can rotate, skip
     int need = 0;
 #pragma unroll
@@ -229,7 +244,7 @@ struct Cross4Scratch {
 };
 
 template <int BW>
-__device__ int inner_sweep_cross4(const double* G, float* Q, double tol2, const Cross4Scratch& S, int lane, int h,
+__device__ int inner_sweep_cross4(const GramSrc<BW>& G, float* Q, double tol2, const Cross4Scratch& S, int lane, int h,
                                   int aw, int bar_id) {
   constexpr int PW = 2 * BW, LDQ = JB<BW>::LDQ, QW = BW / 4;
   const int j0 = h * QW;
@@ -238,12 +253,12 @@ __device__ int inner_sweep_cross4(const double* G, float* Q, double tol2, const 
   float qI[QW], qJ[QW];
 #pragma unroll
   for (int i = 0; i < QW; ++i) {
-    gI[i] = act ? G[lane * LDQ + j0 + i] : 0.0;
-    gJ[i] = act ? G[lane * LDQ + BW + j0 + i] : 0.0;
+    gI[i] = act ? G(lane, j0 + i) : 0.0;
+    gJ[i] = act ? G(lane, BW + j0 + i) : 0.0;
     qI[i] = (lane == j0 + i) ? 1.f : 0.f;
     qJ[i] = (lane == BW + j0 + i) ? 1.f : 0.f;
   }
-  if (h == 0 && act) S.dsm[lane] = G[lane * LDQ + lane];
+  if (h == 0 && act) S.dsm[lane] = G(lane, lane);
   if (lane < BW && lane / QW == h) S.apq[lane] = gJ[lane - j0];   // round 0: pair a = slot (a, BW + a)
   named_bar(bar_id, 128);
   // no cross entry above the threshold: no round can rotate (G never changes), skip
@@ -481,19 +496,9 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
       if (C > 1) cluster_barrier_jb(); else __syncthreads();
       JB_CLK(1);
 
-      // ---- 2. owners: sum partials into the fp64 PW x PW Gram (all threads), then one
-      //         4 warps per owned pair run the inner sweep in registers (inner_sweep_cross4;
-      //         diagonal round: inner_sweep_diag on blocks I and J)
-      for (int e = t; e < nown * PW * PW; e += NT) {
-        const int gi = e / (PW * PW), ab = e % (PW * PW), a = ab / PW, b = ab % PW;
-        if (gi * C + rank >= Pb) continue;
-        const int lo = min(a, b), hi = max(a, b);
-        double sum = 0.0;
-        for (int c = 0; c < C; ++c)
-          sum += Gp[((size_t)c * nown + gi) * PACK + P::pk(lo, hi)];
-        Gw[(size_t)gi * PW * LDQ + a * LDQ + b] = sum;
-      }
-      __syncthreads();
+      // ---- 2. owners: 4 warps per owned pair run the inner sweep in registers, loading the
+      //         fp64 Gram straight from the packed partials (inner_sweep_cross4; diagonal
+      //         round: inner_sweep_diag on blocks I and J)
       JB_CLK(2);
       {
         const int warp = t >> 5, lane = t & 31;
@@ -502,14 +507,14 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
         if (gi < nown && g < Pb) {
           double* js = JS + (size_t)gi * jscr<BW>();
           const Cross4Scratch S = cross4_scratch<BW>(js);
+          const GramSrc<BW> Gsrc{Gp + (size_t)gi * PACK, C, nown * PACK};
           int rot_any = 0;
           if (!diag) {
-            rot_any = inner_sweep_cross4<BW>(Gw + (size_t)gi * PW * LDQ, Qw + (size_t)gi * PW * LDQ, tol2, S, lane, h,
-                                             gi & 3, 1 + gi);
+            rot_any = inner_sweep_cross4<BW>(Gsrc, Qw + (size_t)gi * PW * LDQ, tol2, S, lane, h, gi & 3, 1 + gi);
           } else if (h < 2) {   // diagonal round: block I by warp 0, block J by warp 1
             int* rflag = reinterpret_cast<int*>(S.xg);
-            const int rh = inner_sweep_diag<BW>(Gw + (size_t)gi * PW * LDQ, Qw + (size_t)gi * PW * LDQ, h * BW, tol2,
-                                                S.csd + h * (BW / 2), lane);
+            const int rh = inner_sweep_diag<BW>(Gsrc, Qw + (size_t)gi * PW * LDQ, h * BW, tol2, S.csd + h * (BW / 2),
+                                                lane);
             if (lane == 0) rflag[h] = rh;
             named_bar(1 + gi, 64);
             rot_any = rflag[0] | rflag[1];
