@@ -198,9 +198,11 @@ __device__ void store_lower(float* out, const float* tiles, int k, int nt, int w
   }
 }
 
+// SMEM (template): tiles in shared memory (k <= 256) or in the L2 scratch, a compile-time
+// choice so that the shared-memory instantiation's tile pointers are provably shared.
+template <bool SMEM>
 __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, float* __restrict__ Lout,
-                                                float* __restrict__ Linv, float* __restrict__ work, int smem_tiles,
-                                                int32_t* status) {
+                                           float* __restrict__ Linv, float* __restrict__ work, int32_t* status) {
   extern __shared__ __align__(16) float sm[];
   __shared__ float red[NWARP];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -248,8 +250,8 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   }
 
   CHOL_CLK(0);
-  float* tiles = smem_tiles ? sm : work + (int64_t)blockIdx.x * ((int64_t)ntiles * TILE);
-  float* temp = smem_tiles ? sm + (int64_t)ntiles * TILE : sm;   // [nt-1] tiles in shared memory
+  float* tiles = SMEM ? sm : work + (int64_t)blockIdx.x * ((int64_t)ntiles * TILE);
+  float* temp = SMEM ? sm + (int64_t)ntiles * TILE : sm;   // [nt-1] tiles in shared memory
   auto T = [&](int i, int j) { return tiles + (int64_t)tidx(i, j) * TILE; };
 
   // Shifted retry (shifted CholeskyQR): if a pivot is <= 0 -- the fp32 Gram of an
@@ -392,13 +394,16 @@ cudaError_t launch_cholinv(int nb, int k, const float* G, float* L, float* Linv,
   const size_t temp_bytes = (size_t)(nt > 1 ? nt - 1 : 1) * TILE * sizeof(float);
   const bool smem_tiles = tiles_bytes + temp_bytes <= 200 * 1024;
   const size_t smem = (smem_tiles ? tiles_bytes : 0) + temp_bytes;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cholinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static size_t attr[2] = {0, 0};
+  if (smem > 48 * 1024 && smem > attr[smem_tiles]) {
+    cudaError_t e = smem_tiles
+                        ? cudaFuncSetAttribute(k_cholinv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                        : cudaFuncSetAttribute(k_cholinv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[smem_tiles] = smem;
   }
-  k_cholinv<<<nb, NT, smem, s>>>(k, G, L, Linv, work, smem_tiles ? 1 : 0, status);
+  if (smem_tiles) k_cholinv<true><<<nb, NT, smem, s>>>(k, G, L, Linv, work, status);
+  else k_cholinv<false><<<nb, NT, smem, s>>>(k, G, L, Linv, work, status);
   ++*launches;
   return cudaGetLastError();
 }
