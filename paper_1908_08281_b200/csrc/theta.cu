@@ -248,31 +248,14 @@ __device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_
   return lo;
 }
 
-__global__ void __launch_bounds__(ROWS_NT, 1) k_assemble_rows(int blk0, int b, int TR, const int64_t* __restrict__ row_ptr,
-                                                             const int32_t* __restrict__ col,
-                                                             const uint32_t* __restrict__ keys,
-                                                             const float* __restrict__ eval,
-                                                             const float* __restrict__ dvr, float inv1pmu, int raw,
-                                                             float* __restrict__ blocks,
-                                                             const int32_t* __restrict__ overflow) {
-  const int blk = blk0 + blockIdx.x;
-  if (overflow[blk]) return;                      // handled by the hashed-tile kernel
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  float* acc = reinterpret_cast<float*>(smem_raw);                       // [TR][b]
-  uint32_t* skeys = reinterpret_cast<uint32_t*>(smem_raw + (size_t)TR * b * 4);
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int64_t base = (int64_t)blk * b;
-  const int u0 = blockIdx.y * TR;
-  const int nu = min(TR, b - u0);
-  const int nseg = (b + SEG_V - 1) / SEG_V;
-  const int64_t kb0 = row_ptr[base];
-  const int nkeys = (int)(row_ptr[base + b] - kb0);
-  const bool cached = nkeys <= KEY_SMEM_CAP;
-  const uint32_t* K = cached ? skeys : keys + kb0;
-  if (cached)
-    for (int i = t; i < nkeys; i += ROWS_NT) skeys[i] = keys[kb0 + i];
-  for (int i = t; i < TR * b; i += ROWS_NT) acc[i] = 0.f;
-  __syncthreads();
+// The row walk, with the block's keys in shared memory (CACHED) or read from global memory:
+// a compile-time choice, so that the cached searches compile to shared loads (a runtime
+// select between the two pointers makes every key access a generic load).
+template <bool CACHED>
+__device__ __forceinline__ void assemble_rows_walk(int b, int nu, int nseg, int64_t base, int64_t kb0, int u0,
+                                                   const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                                   const uint32_t* __restrict__ K, const float* __restrict__ eval,
+                                                   float* acc, int lane, int warp) {
   for (int r = warp; r < nu; r += ROWS_NT / 32) {
     const int64_t u = base + u0 + r;
     const int64_t q0 = row_ptr[u], q1 = row_ptr[u + 1];
@@ -305,6 +288,34 @@ __global__ void __launch_bounds__(ROWS_NT, 1) k_assemble_rows(int blk0, int b, i
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(ROWS_NT, 1) k_assemble_rows(int blk0, int b, int TR, const int64_t* __restrict__ row_ptr,
+                                                             const int32_t* __restrict__ col,
+                                                             const uint32_t* __restrict__ keys,
+                                                             const float* __restrict__ eval,
+                                                             const float* __restrict__ dvr, float inv1pmu, int raw,
+                                                             float* __restrict__ blocks,
+                                                             const int32_t* __restrict__ overflow) {
+  const int blk = blk0 + blockIdx.x;
+  if (overflow[blk]) return;                      // handled by the hashed-tile kernel
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  float* acc = reinterpret_cast<float*>(smem_raw);                       // [TR][b]
+  uint32_t* skeys = reinterpret_cast<uint32_t*>(smem_raw + (size_t)TR * b * 4);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t base = (int64_t)blk * b;
+  const int u0 = blockIdx.y * TR;
+  const int nu = min(TR, b - u0);
+  const int nseg = (b + SEG_V - 1) / SEG_V;
+  const int64_t kb0 = row_ptr[base];
+  const int nkeys = (int)(row_ptr[base + b] - kb0);
+  const bool cached = nkeys <= KEY_SMEM_CAP;
+  if (cached)
+    for (int i = t; i < nkeys; i += ROWS_NT) skeys[i] = keys[kb0 + i];
+  for (int i = t; i < TR * b; i += ROWS_NT) acc[i] = 0.f;
+  __syncthreads();
+  if (cached) assemble_rows_walk<true>(b, nu, nseg, base, kb0, u0, row_ptr, col, skeys, eval, acc, lane, warp);
+  else assemble_rows_walk<false>(b, nu, nseg, base, kb0, u0, row_ptr, col, keys + kb0, eval, acc, lane, warp);
   __syncthreads();
   float* out = blocks + (int64_t)blk * b * b;
   for (int r = 0; r < nu; ++r) {
