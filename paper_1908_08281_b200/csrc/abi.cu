@@ -215,7 +215,9 @@ struct Rsvd {
     g.A = P_t; g.a_mn = false; g.lda = b; g.sa = (int64_t)k * b;
     g.B = P_t; g.b_mn = false; g.ldb = b; g.sb = (int64_t)k * b;
     g.D = G; g.d_trans = false; g.ldd = k; g.sd = (int64_t)k * k;
-    g.bn_max = bn_env("HG_BN_GRAM", 256);
+    // symmetric: 128-wide tiles on and below the diagonal only (k_cholinv reads the lower triangle)
+    g.bn_max = bn_env("HG_BN_GRAM", 128);
+    g.lower = !getenv("HG_GRAM_FULL");
     return gemm(g, s, simt, "Gram P^T P", ST_GEMM_GRAM);
   }
   // Q = P L^-T  ->  Q_t

@@ -217,7 +217,8 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   // distance from the identity (near-identity path for the second CholeskyQR pass)
   float emax = 0.f;
   for (int r = warp; r < k; r += NWARP)             // warp per row, lanes over columns (no divisions)
-    for (int c = lane; c < k; c += 32) {
+    for (int c = lane; c <= r; c += 32) {           // lower triangle (G symmetric; the Gram GEMM
+                                                    // may leave tiles above the diagonal unset)
       const float g = Gb[(int64_t)r * k + c];
       const float e = fabsf(g - (r == c ? 1.f : 0.f));
       emax = fmaxf(emax, isfinite(g) ? e : INFINITY);

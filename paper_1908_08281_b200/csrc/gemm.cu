@@ -45,6 +45,7 @@ struct EpiArgs {
   int64_t scs;
   int a_mn, b_mn;
   int trunc_hi;   // 1: hi = the raw fp32 tile (tensor core truncates to tf32), lo = x - trunc(x)
+  int lower;      // skip tiles entirely above the diagonal (GemmDesc::lower)
 };
 
 constexpr int NEPI = 256;            // converter / epilogue threads (8 warps)
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, g = blockIdx.z;
+  if (ea.lower && n0 >= m0 + BM) return;   // tile above the diagonal (uniform: before any setup)
   const int num_kb = (ea.K + BK - 1) / BK;
   const int nchunks = (num_kb + CHUNK_KB - 1) / CHUNK_KB;
 
@@ -466,7 +468,7 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
     return (v && v[0] == 'r') ? 0 : 1;
   }();
   EpiArgs ea{g.M, g.N, g.K, g.D, g.ldd, g.sd, g.d_trans ? 1 : 0, g.alpha, g.rs, g.srs, g.cs, g.scs,
-             g.a_mn ? 1 : 0, g.b_mn ? 1 : 0, trunc_hi};
+             g.a_mn ? 1 : 0, g.b_mn ? 1 : 0, trunc_hi, g.lower ? 1 : 0};
   if (simt) {
     dim3 grid((g.M + 63) / 64, (g.N + 63) / 64, g.batch);
     gemm_simt_kernel<<<grid, 256, 0, stream>>>(g.A, ea.a_mn, g.lda, g.sa, g.B, ea.b_mn, g.ldb, g.sb, ea);

@@ -24,6 +24,8 @@ struct GemmDesc {
   const float* cs = nullptr;
   int64_t scs = 0;
   int bn_max = 256;   // widest N tile to use (smaller tiles = more CTAs for small outputs)
+  bool lower = false; // symmetric result, consumer reads the lower triangle: skip output tiles
+                      // entirely above the diagonal (n0 >= m0 + 128); those entries are left unset
 };
 
 // Enqueue the GEMM; returns cudaSuccess or the launch error.  `simt` selects the
