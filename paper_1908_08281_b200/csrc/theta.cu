@@ -255,7 +255,8 @@ template <bool CACHED>
 __device__ __forceinline__ void assemble_rows_walk(int b, int nu, int nseg, int64_t base, int64_t kb0, int u0,
                                                    const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                                                    const uint32_t* __restrict__ K, const float* __restrict__ eval,
-                                                   float* acc, int lane, int warp) {
+                                                   const float* __restrict__ dvr, float inv1pmu, int raw,
+                                                   float* __restrict__ out, float* acc, int lane, int warp) {
   for (int r = warp; r < nu; r += ROWS_NT / 32) {
     const int64_t u = base + u0 + r;
     const int64_t q0 = row_ptr[u], q1 = row_ptr[u + 1];
@@ -287,6 +288,15 @@ __device__ __forceinline__ void assemble_rows_walk(int b, int nu, int nseg, int6
         __syncwarp();
       }
     }
+    // the row is complete: write it now (no block barrier -- rows are independent, so
+    // warps that finish early store while the heavy rows are still being walked)
+    const int uu = u0 + r;
+    const float du = dvr[base + uu];
+    float* orow = out + (int64_t)uu * b;
+    for (int v = lane; v < b; v += 32) {
+      const float th = (du * dvr[base + v]) * arow[v];
+      orow[v] = raw ? th : ((uu == v ? 1.0f : 0.0f) - th * inv1pmu);
+    }
   }
 }
 
@@ -314,18 +324,13 @@ __global__ void __launch_bounds__(ROWS_NT, 1) k_assemble_rows(int blk0, int b, i
     for (int i = t; i < nkeys; i += ROWS_NT) skeys[i] = keys[kb0 + i];
   for (int i = t; i < TR * b; i += ROWS_NT) acc[i] = 0.f;
   __syncthreads();
-  if (cached) assemble_rows_walk<true>(b, nu, nseg, base, kb0, u0, row_ptr, col, skeys, eval, acc, lane, warp);
-  else assemble_rows_walk<false>(b, nu, nseg, base, kb0, u0, row_ptr, col, keys + kb0, eval, acc, lane, warp);
-  __syncthreads();
   float* out = blocks + (int64_t)blk * b * b;
-  for (int r = 0; r < nu; ++r) {
-    const int uu = u0 + r;
-    const float du = dvr[base + uu];
-    for (int v = t; v < b; v += ROWS_NT) {
-      const float th = (du * dvr[base + v]) * acc[(size_t)r * b + v];
-      out[(int64_t)uu * b + v] = raw ? th : ((uu == v ? 1.0f : 0.0f) - th * inv1pmu);
-    }
-  }
+  if (cached)
+    assemble_rows_walk<true>(b, nu, nseg, base, kb0, u0, row_ptr, col, skeys, eval, dvr, inv1pmu, raw, out, acc, lane,
+                             warp);
+  else
+    assemble_rows_walk<false>(b, nu, nseg, base, kb0, u0, row_ptr, col, keys + kb0, eval, dvr, inv1pmu, raw, out, acc,
+                              lane, warp);
 }
 
 }  // namespace
