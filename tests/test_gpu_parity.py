@@ -257,6 +257,34 @@ def test_stream_parts_bitwise_identical(inputs, cfg, monkeypatch):
         assert torch.equal(out[parts][0], out["1"][0]) and torch.equal(out[parts][1], out["1"][1]), parts
 
 
+def test_timeline_profiler_parts_overlap(inputs, monkeypatch):
+    """hg_profile_enable(2): stream parts stay concurrent and every stage of every part is
+    recorded with its part index; the result equals the unprofiled one bit for bit."""
+    hg = hgm()
+    h = inputs(2)
+    c = CONFIGS[2]
+    H, w, Y = dev_inputs(h)
+    monkeypatch.setenv("HG_STREAMS", "2")
+    F0, s0, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)
+    hg.profile_enable(2)
+    try:
+        F1, s1, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)
+        recs = hg.profile_timeline()
+    finally:
+        hg.profile_enable(0)
+    assert torch.equal(F0, F1) and torch.equal(s0, s1)
+    parts = {r[1] for r in recs}
+    assert parts == {0, 1}
+    for p in parts:
+        stages = {r[0] for r in recs if r[1] == p}
+        assert {"assemble", "omega", "gemm_power", "gemm_gram", "gemm_qform", "cholinv", "jacobi", "finalize",
+                "gemm_apply"} <= stages, stages
+    assert all(r[3] >= r[2] >= -1.0 for r in recs)
+    # the two parts' Jacobi intervals overlap (concurrent streams)
+    j = sorted((r[2], r[3]) for r in recs if r[0] == "jacobi")
+    assert len(j) == 2 and j[1][0] < j[0][1]
+
+
 def test_deterministic_and_host_entry(inputs):
     hg = hgm()
     h = inputs(2)
