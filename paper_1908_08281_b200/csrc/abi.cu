@@ -49,7 +49,6 @@ thread_local cudaEvent_t g_t0 = nullptr;          // timeline origin (first solv
 thread_local bool g_t0_set = false;
 thread_local std::vector<ProfRec> g_prof;
 thread_local std::vector<cudaEvent_t> g_evpool;
-thread_local int g_cur_stage = -1;
 
 cudaEvent_t prof_event() {
   if (!g_evpool.empty()) {

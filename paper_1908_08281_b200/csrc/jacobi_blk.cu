@@ -388,7 +388,7 @@ __device__ __forceinline__ Cross4Scratch cross4_scratch(double* js) {
 
 struct Layout {
   int K2, nblk, Pb, R, nch, rch, ldw, nown;
-  size_t offW, offGp, offG, offQ, offQb, offJ, offF, total;
+  size_t offW, offGp, offQ, offQb, offJ, offF, total;
 };
 
 template <int BW>
@@ -408,9 +408,8 @@ __host__ __device__ inline Layout make_layout(int k, int C) {
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) / 16 * 16; return o; };
   L.offW = take((size_t)L.R * L.ldw * 4);
   L.offGp = take((size_t)C * L.nown * P::PACK * 4);
-  L.offG = take((size_t)L.nown * P::PW * P::LDQ * 8);   // fp64 inner Gram
   L.offQ = take((size_t)L.nown * P::PW * P::LDQ * 4);
-  L.offQb = L.offG;   // apply-phase staging aliases the fp64 Gram (disjoint lifetimes)
+  L.offQb = take((size_t)P::NQB * P::PW * P::LDQ * 4);   // apply-phase Q staging
   L.offJ = take((size_t)L.nown * jscr<BW>() * 8);          // inner-round scratch per owned pair
   L.offF = take((size_t)128 * 4);
   L.total = off;
@@ -432,7 +431,6 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
   const int nr = max(0, min(R, k - r0));
   float* W = reinterpret_cast<float*>(smem_raw + Lo.offW);
   float* Gp = reinterpret_cast<float*>(smem_raw + Lo.offGp);     // [C][nch][nown][PACK]
-  double* Gw = reinterpret_cast<double*>(smem_raw + Lo.offG);    // [nown][PW][LDQ]
   float* Qw = reinterpret_cast<float*>(smem_raw + Lo.offQ);      // [nown][PW][LDQ]
   float* Qb = reinterpret_cast<float*>(smem_raw + Lo.offQb);     // [NQB][PW][LDQ]
   double* JS = reinterpret_cast<double*>(smem_raw + Lo.offJ);    // [nown][JSCR]: cs | dsm | xch
@@ -636,8 +634,7 @@ cudaError_t launch_bw(int nb, int k, const float* L, float* Wf, int32_t* status,
   if (C > 8) return cudaErrorInvalidValue;
   const Layout Lo = make_layout<BW>(k, C);
   if (Lo.nown > JB<BW>::MAXOWN || Lo.nown > NT / 128 || Lo.Pb > 128 || Lo.total > 227 * 1024 ||
-      ((Lo.R + 3) / 4) * (JB<BW>::PW / 4) > 2 * NT ||
-      (size_t)std::min(JB<BW>::NQB, Lo.Pb) * 4 > (size_t)Lo.nown * 8)   // staged Q fits the aliased Gram
+      ((Lo.R + 3) / 4) * (JB<BW>::PW / 4) > 2 * NT)
     return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k_jacobi_blk<BW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lo.total);
   if (e != cudaSuccess) return e;

@@ -189,12 +189,13 @@ __global__ void __launch_bounds__(NT) k_assemble(int blk0, int b, const int64_t*
 //   symmetric.  Output rows are written once, coalesced.
 constexpr int SEG_V = 512;          // vertices per sorted segment
 constexpr int SEG_CAP = 16384;      // keys per segment in shared memory (64 KB)
-constexpr int ROWS_NT = 1024;
-constexpr int KEY_SMEM_CAP = 24576; // block keys cached in shared memory (96 KB)
+constexpr int NSEG_MAX = 4;         // b <= 4 SEG_V on the sorted path
+constexpr int ROWS_NT = 512;        // k_assemble_rows: one warp per row
+constexpr int TR_ROWS = ROWS_NT / 32;
 
 __global__ void __launch_bounds__(1024) k_seg_sort(int blk0, int b, const int64_t* __restrict__ row_ptr,
                                                    const int32_t* __restrict__ col, uint32_t* __restrict__ keys,
-                                                   int32_t* __restrict__ overflow) {
+                                                   int2* __restrict__ rng, int32_t* __restrict__ overflow) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   int64_t* vp = reinterpret_cast<int64_t*>(smem_raw);                    // [SEG_V + 1]
   uint32_t* sk = reinterpret_cast<uint32_t*>(smem_raw + (SEG_V + 2) * 8);  // [SEG_CAP]
@@ -237,26 +238,32 @@ __global__ void __launch_bounds__(1024) k_seg_sort(int blk0, int b, const int64_
     }
   }
   for (int i = t; i < n; i += 1024) keys[p0 + i] = sk[i];
-}
-
-__device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_t x) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  // member ranges of every incidence (u, e) of the block inside this segment: keys of
+  // edge e are [e b, (e+1) b); indices relative to the block's first incidence kb0
+  const int64_t kb0 = row_ptr[(int64_t)blk * b], kb1 = row_ptr[(int64_t)(blk + 1) * b];
+  const int s0 = (int)(p0 - kb0);
+  for (int64_t p = kb0 + t; p < kb1; p += 1024) {
+    const uint32_t e = (uint32_t)col[p];
+    int lo = 0, hi = n;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (sk[mid] < e * (uint32_t)b) lo = mid + 1; else hi = mid; }
+    int lo2 = lo, hi2 = n;
+    while (lo2 < hi2) { const int mid = (lo2 + hi2) >> 1; if (sk[mid] < (e + 1) * (uint32_t)b) lo2 = mid + 1; else hi2 = mid; }
+    rng[p * NSEG_MAX + seg] = make_int2(s0 + lo, s0 + lo2);
   }
-  return lo;
 }
 
-// The row walk, with the block's keys in shared memory (CACHED) or read from global memory:
-// a compile-time choice, so that the cached searches compile to shared loads (a runtime
-// select between the two pointers makes every key access a generic load).
-template <bool CACHED>
-__device__ __forceinline__ void assemble_rows_walk(int b, int nu, int nseg, int64_t base, int64_t kb0, int u0,
+
+// The row walk: one warp per row u, ascending edge order; for each edge e of the row the
+// members in the block are the key runs rng[p][segment] (p = global CSR position of (u, e);
+// run bounds relative to the block's first incidence, from k_seg_sort), read from
+// global memory (coalesced runs).  Each (u, v) sums its common edges in ascending edge
+// order.  The warp writes its row as soon as it is complete (rows are independent).
+__device__ __forceinline__ void assemble_rows_walk(int b, int nu, int nseg, int64_t base, int u0,
                                                    const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                                                   const uint32_t* __restrict__ K, const float* __restrict__ eval,
-                                                   const float* __restrict__ dvr, float inv1pmu, int raw,
-                                                   float* __restrict__ out, float* acc, int lane, int warp) {
+                                                   const uint32_t* __restrict__ K, const int2* __restrict__ rng,
+                                                   const float* __restrict__ eval, const float* __restrict__ dvr,
+                                                   float inv1pmu, int raw, float* __restrict__ out, float* acc,
+                                                   int lane, int warp) {
   for (int r = warp; r < nu; r += ROWS_NT / 32) {
     const int64_t u = base + u0 + r;
     const int64_t q0 = row_ptr[u], q1 = row_ptr[u + 1];
@@ -265,31 +272,26 @@ __device__ __forceinline__ void assemble_rows_walk(int b, int nu, int nseg, int6
       const int ne = (int)((q1 - c0) < 32 ? (q1 - c0) : 32);
       uint32_t e = 0;
       float val = 0.f;
-      int lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
+      int2 rg[NSEG_MAX];
+#pragma unroll
+      for (int sg = 0; sg < NSEG_MAX; ++sg) rg[sg] = make_int2(0, 0);
       if (lane < ne) {
         e = (uint32_t)col[c0 + lane];
         val = eval[e];
-        for (int sg = 0; sg < nseg && sg < 4; ++sg) {
-          const int s0 = (int)(row_ptr[base + sg * SEG_V] - kb0);
-          const int s1 = (int)(row_ptr[base + min(b, (sg + 1) * SEG_V)] - kb0);
-          lo[sg] = s0 + lower_bound_u32(K + s0, s1 - s0, e * (uint32_t)b);
-          hi[sg] = s0 + lower_bound_u32(K + s0, s1 - s0, (e + 1) * (uint32_t)b);
-        }
+        for (int sg = 0; sg < nseg; ++sg) rg[sg] = rng[(c0 + lane) * NSEG_MAX + sg];
       }
       for (int j = 0; j < ne; ++j) {             // ascending edge order
         const float vj = __shfl_sync(0xffffffffu, val, j);
         const uint32_t ebj = __shfl_sync(0xffffffffu, e, j) * (uint32_t)b;
 #pragma unroll
-        for (int sg = 0; sg < 4; ++sg) {
+        for (int sg = 0; sg < NSEG_MAX; ++sg) {
           if (sg >= nseg) break;
-          const int l = __shfl_sync(0xffffffffu, lo[sg], j), h = __shfl_sync(0xffffffffu, hi[sg], j);
+          const int l = __shfl_sync(0xffffffffu, rg[sg].x, j), h = __shfl_sync(0xffffffffu, rg[sg].y, j);
           for (int m = l + lane; m < h; m += 32) arow[K[m] - ebj] += vj;
         }
         __syncwarp();
       }
     }
-    // the row is complete: write it now (no block barrier -- rows are independent, so
-    // warps that finish early store while the heavy rows are still being walked)
     const int uu = u0 + r;
     const float du = dvr[base + uu];
     float* orow = out + (int64_t)uu * b;
@@ -300,37 +302,28 @@ __device__ __forceinline__ void assemble_rows_walk(int b, int nu, int nseg, int6
   }
 }
 
-__global__ void __launch_bounds__(ROWS_NT, 1) k_assemble_rows(int blk0, int b, int TR, const int64_t* __restrict__ row_ptr,
-                                                             const int32_t* __restrict__ col,
-                                                             const uint32_t* __restrict__ keys,
-                                                             const float* __restrict__ eval,
-                                                             const float* __restrict__ dvr, float inv1pmu, int raw,
-                                                             float* __restrict__ blocks,
-                                                             const int32_t* __restrict__ overflow) {
+__global__ void __launch_bounds__(ROWS_NT) k_assemble_rows(int blk0, int b, const int64_t* __restrict__ row_ptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const uint32_t* __restrict__ keys,
+                                                          const int2* __restrict__ rng,
+                                                          const float* __restrict__ eval,
+                                                          const float* __restrict__ dvr, float inv1pmu, int raw,
+                                                          float* __restrict__ blocks,
+                                                          const int32_t* __restrict__ overflow) {
   const int blk = blk0 + blockIdx.x;
   if (overflow[blk]) return;                      // handled by the hashed-tile kernel
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  float* acc = reinterpret_cast<float*>(smem_raw);                       // [TR][b]
-  uint32_t* skeys = reinterpret_cast<uint32_t*>(smem_raw + (size_t)TR * b * 4);
+  float* acc = reinterpret_cast<float*>(smem_raw);   // [TR_ROWS][b]
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t base = (int64_t)blk * b;
-  const int u0 = blockIdx.y * TR;
-  const int nu = min(TR, b - u0);
+  const int u0 = blockIdx.y * TR_ROWS;
+  const int nu = min(TR_ROWS, b - u0);
   const int nseg = (b + SEG_V - 1) / SEG_V;
   const int64_t kb0 = row_ptr[base];
-  const int nkeys = (int)(row_ptr[base + b] - kb0);
-  const bool cached = nkeys <= KEY_SMEM_CAP;
-  if (cached)
-    for (int i = t; i < nkeys; i += ROWS_NT) skeys[i] = keys[kb0 + i];
-  for (int i = t; i < TR * b; i += ROWS_NT) acc[i] = 0.f;
+  for (int i = t; i < TR_ROWS * b; i += ROWS_NT) acc[i] = 0.f;
   __syncthreads();
-  float* out = blocks + (int64_t)blk * b * b;
-  if (cached)
-    assemble_rows_walk<true>(b, nu, nseg, base, kb0, u0, row_ptr, col, skeys, eval, dvr, inv1pmu, raw, out, acc, lane,
-                             warp);
-  else
-    assemble_rows_walk<false>(b, nu, nseg, base, kb0, u0, row_ptr, col, keys + kb0, eval, dvr, inv1pmu, raw, out, acc,
-                              lane, warp);
+  assemble_rows_walk(b, nu, nseg, base, u0, row_ptr, col, keys + kb0, rng, eval, dvr, inv1pmu, raw,
+                     blocks + (int64_t)blk * b * b, acc, lane, warp);
 }
 
 }  // namespace
@@ -351,7 +344,11 @@ cudaError_t launch_degrees(int N, int E, int64_t nnz, const int64_t* row_ptr, co
   return cudaGetLastError();
 }
 
-size_t assemble_keys_bytes(int64_t nnz, int nb) { return (size_t)nnz * 4 + (size_t)nb * 4 + 256; }
+// keys [nnz] u32 | overflow [nb] i32 | member ranges [nnz][NSEG_MAX] int2 (256-byte aligned parts)
+static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+size_t assemble_keys_bytes(int64_t nnz, int nb) {
+  return al256((size_t)nnz * 4) + al256((size_t)nb * 4) + (size_t)nnz * NSEG_MAX * sizeof(int2) + 256;
+}
 
 // keys: nnz uint32 + nb int32 overflow flags (workspace).  E*b must be < 2^32 for the
 // sorted path (32-bit keys); otherwise every block takes the hashed-tile kernel.
@@ -359,11 +356,12 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
                             const int32_t* col_idx, const float* edge_val, const float* dv_rsqrt, float mu,
                             bool raw_theta, float* blocks, void* keys_ws, cudaStream_t s, int* launches) {
   uint32_t* keys = reinterpret_cast<uint32_t*>(keys_ws);
-  int32_t* overflow = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(keys_ws) + ((size_t)nnz * 4 + 255) / 256 * 256);
+  int32_t* overflow = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(keys_ws) + al256((size_t)nnz * 4));
+  int2* rng = reinterpret_cast<int2*>(reinterpret_cast<char*>(keys_ws) + al256((size_t)nnz * 4) +
+                                      al256((size_t)nb_total * 4));
   // HG_ASSEMBLE=tiles forces the hashed-tile kernel (verification: both paths are bit-identical)
   const char* force = getenv("HG_ASSEMBLE");
   const bool sorted_ok = (uint64_t)E * (uint64_t)b < (1ull << 32) && b <= 4 * SEG_V && !(force && force[0] == 't');
-  (void)nb_total;
   cudaError_t e = cudaMemsetAsync(overflow + blk0, sorted_ok ? 0 : 1, sizeof(int32_t) * nb, s);
   if (e != cudaSuccess) return e;
   if (sorted_ok) {
@@ -375,20 +373,17 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
       if (e != cudaSuccess) return e;
       attr1 = true;
     }
-    k_seg_sort<<<dim3(nb, nseg), 1024, ssmem, s>>>(blk0, b, row_ptr, col_idx, keys, overflow);
-    int TR = 32768 / b;
-    if (TR > 32) TR = 32;
-    if (TR < 1) TR = 1;
-    const size_t smem = (size_t)TR * b * 4 + (size_t)KEY_SMEM_CAP * 4;
+    k_seg_sort<<<dim3(nb, nseg), 1024, ssmem, s>>>(blk0, b, row_ptr, col_idx, keys, rng, overflow);
+    const size_t smem = (size_t)TR_ROWS * b * 4;
     static size_t attr2 = 0;
     if (smem > attr2) {
       e = cudaFuncSetAttribute(k_assemble_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       attr2 = smem;
     }
-    k_assemble_rows<<<dim3(nb, (b + TR - 1) / TR), ROWS_NT, smem, s>>>(blk0, b, TR, row_ptr, col_idx, keys, edge_val,
-                                                                      dv_rsqrt, 1.0f / (1.0f + mu),
-                                                                      raw_theta ? 1 : 0, blocks, overflow);
+    k_assemble_rows<<<dim3(nb, (b + TR_ROWS - 1) / TR_ROWS), ROWS_NT, smem, s>>>(
+        blk0, b, row_ptr, col_idx, keys, rng, edge_val, dv_rsqrt, 1.0f / (1.0f + mu), raw_theta ? 1 : 0, blocks,
+        overflow);
     *launches += 2;
   }
   return launch_assemble_tiles(blk0, nb, b, row_ptr, col_idx, edge_val, dv_rsqrt, mu, raw_theta, blocks, overflow, s,
