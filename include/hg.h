@@ -129,10 +129,14 @@ hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const floa
  * *d_status returns HG_ERR_NUMERICAL).  d_status may be NULL only with HG_SYNC
  * (a word inside ws is used).
  * Concurrency: after the degrees, disjoint block ranges (HG_STREAMS parts,
- * default 4, at most 4) run their assembly, rSVD and apply on library-owned non-blocking
+ * default 6, at most 8) run their assembly, rSVD and apply on library-owned non-blocking
  * streams forked from and joined back into `stream` with events, so all work
  * is still ordered after prior work on `stream` and before later work (also
- * under stream capture).  The result is bitwise independent of the part count. */
+ * under stream capture).  The result is bitwise independent of the part count.
+ * The whole sequence is captured once per distinct argument set into a CUDA graph
+ * (a per-thread cache of 8) and replayed with one cudaGraphLaunch on `stream`; when
+ * `stream` is itself capturing, or profiling is on, or HG_NO_GRAPH=1, the kernels
+ * are enqueued directly. */
 hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
                    uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags,
                    int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);

@@ -585,21 +585,38 @@ hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const floa
                    reinterpret_cast<cudaStream_t>(stream), false);
 }
 
-// Part count for hg_solve (HG_STREAMS, default 4: measured 12.76 ms vs 12.97 with 2 parts,
-// 13.8 with 1 at configs[3]) and the auxiliary streams / events
+// Part count for hg_solve (HG_STREAMS, default 6, at most 8: with graph replay measured
+// 11.99 ms at configs[3] vs 12.11 / 12.29 / 12.56 / 12.05 with 4 / 3 / 2 / 8 parts) and the
+// auxiliary streams / events
 // of the fork-join (created once, non-blocking, reused).
-constexpr int kMaxParts = 4;
+constexpr int kMaxParts = 8;
 static int solve_parts() {   // read per call (tests switch it)
   const char* v = getenv("HG_STREAMS");
-  const int x = v ? atoi(v) : 4;
+  const int x = v ? atoi(v) : 6;
   return x < 1 ? 1 : (x > kMaxParts ? kMaxParts : x);
 }
 // Parts run on library streams of default priority (HG_STREAM_PRIO=1: part p gets
 // greatest + p; measured 13.97 vs 13.80 ms at configs[3]: staggering the parts delays
 // the last part's latency-bound Jacobi, which sets the makespan).
+static cudaStream_t g_aux[kMaxParts] = {};
+static cudaEvent_t g_ev_fork = nullptr, g_ev_join[kMaxParts] = {};
+// library streams / events, created once and outside any stream capture
+static hg_status ensure_streams() {
+  if (g_ev_fork) return HG_OK;
+  int least = 0, greatest = 0;
+  HG_CU(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+  const char* pv = getenv("HG_STREAM_PRIO");
+  const bool prio = pv && pv[0] == '1';
+  for (int p = 0; p < kMaxParts; ++p) {
+    int pr = prio ? greatest + p : 0;
+    if (pr > least) pr = least;
+    HG_CU(cudaStreamCreateWithPriority(&g_aux[p], cudaStreamNonBlocking, pr), "stream create");
+    HG_CU(cudaEventCreateWithFlags(&g_ev_join[p], cudaEventDisableTiming), "event create");
+  }
+  HG_CU(cudaEventCreateWithFlags(&g_ev_fork, cudaEventDisableTiming), "event create");
+  return HG_OK;
+}
 static hg_status fork_streams(cudaStream_t s, int nparts, cudaStream_t* ps) {
-  static cudaStream_t aux[kMaxParts] = {};
-  static cudaEvent_t ev_fork = nullptr;
   ps[0] = s;
   if (nparts == 1) return HG_OK;
   if (const char* v = getenv("HG_STREAMS_SERIAL")) {   // debugging: parts in sequence on `stream`
@@ -608,18 +625,9 @@ static hg_status fork_streams(cudaStream_t s, int nparts, cudaStream_t* ps) {
       return HG_OK;
     }
   }
-  if (!ev_fork) {
-    HG_CU(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event create");
-    int least = 0, greatest = 0;
-    HG_CU(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
-    const char* pv = getenv("HG_STREAM_PRIO");
-    const bool prio = pv && pv[0] == '1';
-    for (int p = 0; p < kMaxParts; ++p) {
-      int pr = prio ? greatest + p : 0;
-      if (pr > least) pr = least;
-      HG_CU(cudaStreamCreateWithPriority(&aux[p], cudaStreamNonBlocking, pr), "stream create");
-    }
-  }
+  HG_TRY(ensure_streams());
+  cudaStream_t* aux = g_aux;
+  cudaEvent_t ev_fork = g_ev_fork;
   HG_CU(cudaEventRecord(ev_fork, s), "fork record");
   for (int p = 0; p < nparts; ++p) {
     HG_CU(cudaStreamWaitEvent(aux[p], ev_fork, 0), "fork wait");
@@ -628,12 +636,10 @@ static hg_status fork_streams(cudaStream_t s, int nparts, cudaStream_t* ps) {
   return HG_OK;
 }
 static hg_status join_streams(cudaStream_t s, int nparts, const cudaStream_t* ps) {
-  static cudaEvent_t ev_join[kMaxParts] = {};
   for (int p = 0; p < nparts; ++p) {
     if (ps[p] == s) continue;
-    if (!ev_join[p]) HG_CU(cudaEventCreateWithFlags(&ev_join[p], cudaEventDisableTiming), "event create");
-    HG_CU(cudaEventRecord(ev_join[p], ps[p]), "join record");
-    HG_CU(cudaStreamWaitEvent(s, ev_join[p], 0), "join wait");
+    HG_CU(cudaEventRecord(g_ev_join[p], ps[p]), "join record");
+    HG_CU(cudaStreamWaitEvent(s, g_ev_join[p], 0), "join wait");
   }
   return HG_OK;
 }
@@ -739,13 +745,109 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   return HG_OK;
 }
 
+// CUDA-graph cache of hg_solve: the whole multi-stream launch sequence (4 parts of ~67
+// kernels, their fork/join events) is captured once per distinct argument set and
+// replayed with one cudaGraphLaunch on the caller's stream.  Host enqueue of the parts
+// costs ~1.1 ms otherwise and staggers their start on the GPU by ~0.4 ms per part.
+namespace {
+struct SolveKey {
+  hg_incidence H;
+  const float *w, *Y;
+  float mu, *F, *sigma;
+  int32_t b, k, q, T, parts;
+  uint64_t seed;
+  uint32_t flags;
+  int32_t* st;
+  void* ws;
+  size_t ws_bytes;
+  std::string env;
+  bool operator==(const SolveKey& o) const {
+    return std::memcmp(&H, &o.H, sizeof H) == 0 && w == o.w && Y == o.Y && mu == o.mu && F == o.F &&
+           sigma == o.sigma && b == o.b && k == o.k && q == o.q && T == o.T && parts == o.parts && seed == o.seed &&
+           flags == o.flags && st == o.st && ws == o.ws && ws_bytes == o.ws_bytes && env == o.env;
+  }
+};
+struct GraphEntry {
+  SolveKey key;
+  cudaGraphExec_t exec;
+  int launches;
+};
+thread_local std::vector<GraphEntry> g_graphs;
+constexpr size_t kMaxGraphs = 8;
+std::string knob_env() {   // enqueue-time knobs that change the captured sequence
+  std::string e;
+  for (const char* n : {"HG_ASSEMBLE", "HG_STREAMS_SERIAL", "HG_BN_POWER", "HG_BN_GRAM", "HG_BN_QFORM", "HG_GRAM_FULL"}) {
+    const char* v = getenv(n);
+    e += v ? v : "-";
+    e += '|';
+  }
+  return e;
+}
+}  // namespace
+
 hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q, uint64_t seed,
                    const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags, int32_t* d_status, void* ws,
                    size_t ws_bytes, hg_stream_t stream) {
   g_err.clear();
   g_launches = 0;
-  return solve_impl(H, w, mu, b, k, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes,
-                    reinterpret_cast<cudaStream_t>(stream));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  HG_CU(cudaStreamIsCapturing(s, &cap), "capture status");
+  const char* ng = getenv("HG_NO_GRAPH");
+  if (g_prof_on || cap != cudaStreamCaptureStatusNone || (ng && ng[0] == '1'))
+    return solve_impl(H, w, mu, b, k, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes, s);
+  // host-side validation first (nothing is captured for an invalid call)
+  HG_TRY(check_H(H));
+  HG_TRY(check_sizes(H->n_vertices, b, k, q, T));
+  const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, k, T);
+  HG_TRY(check_ws(ws, ws_bytes, Lo.h_rowptr));
+  if (!d_status && !(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
+  int32_t* st = d_status ? d_status : at<int32_t>(ws, Lo.status);
+  SolveKey key{*H, w, Y, mu, F, sigma_out, b, k, q, T, solve_parts(), seed, flags & ~HG_SYNC, st, ws, ws_bytes,
+               knob_env()};
+  GraphEntry* ge = nullptr;
+  for (auto& e : g_graphs)
+    if (e.key == key) ge = &e;
+  if (!ge) {
+    HG_TRY(ensure_streams());
+    static thread_local cudaStream_t cs = nullptr;
+    if (!cs) HG_CU(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
+    HG_CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
+    hg_status r = HG_OK;
+    if (!d_status) {
+      cudaError_t e = cudaMemsetAsync(st, 0, sizeof(int32_t), cs);
+      if (e != cudaSuccess) r = cuda_fail(e, "memset status");
+    }
+    if (r == HG_OK)
+      r = solve_impl(H, w, mu, b, k, q, seed, Y, T, F, sigma_out, flags & ~HG_SYNC, st, ws, ws_bytes, cs);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+    if (r != HG_OK || ec != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      (void)cudaGetLastError();
+      return r != HG_OK ? r : cuda_fail(ec, "end capture");
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) return cuda_fail(ei, "graph instantiate");
+    if (g_graphs.size() >= kMaxGraphs) {
+      cudaGraphExecDestroy(g_graphs.front().exec);
+      g_graphs.erase(g_graphs.begin());
+    }
+    g_graphs.push_back(GraphEntry{key, exec, g_launches});
+    ge = &g_graphs.back();
+  }
+  HG_CU(cudaGraphLaunch(ge->exec, s), "graph launch");
+  g_launches = ge->launches;
+  if (flags & HG_SYNC) {
+    int32_t h = 0;
+    HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
+    HG_CU(cudaStreamSynchronize(s), "synchronize");
+    if (h) return fail(HG_ERR_NUMERICAL, "device status 0x%x (bits: 1 isolated vertex, 2 empty hyperedge, 4 "
+                       "Cholesky breakdown, 8 Jacobi cap, 16 singular sigma, 32 non-finite)", h);
+  }
+  return HG_OK;
 }
 
 hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_ptr_host, const int32_t* col_idx_host,
