@@ -708,6 +708,10 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     hg_status err = HG_OK;
     cps = copy_stream(&err);
     if (!cps) return err;
+    static cudaEvent_t ev_cps = nullptr;   // fork the copy stream from `s` (joins a capture)
+    if (!ev_cps) HG_CU(cudaEventCreateWithFlags(&ev_cps, cudaEventDisableTiming), "event create");
+    HG_CU(cudaEventRecord(ev_cps, s), "copy fork record");
+    HG_CU(cudaStreamWaitEvent(cps, ev_cps, 0), "copy fork wait");
     for (int p = 0; p < nparts; ++p) {
       const int64_t r0 = (int64_t)nb * p / nparts * b, r1 = (int64_t)nb * (p + 1) / nparts * b;
       if (!ev_y[p]) HG_CU(cudaEventCreateWithFlags(&ev_y[p], cudaEventDisableTiming), "event create");
@@ -745,30 +749,14 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   return HG_OK;
 }
 
-// CUDA-graph cache of hg_solve: the whole multi-stream launch sequence (4 parts of ~67
-// kernels, their fork/join events) is captured once per distinct argument set and
-// replayed with one cudaGraphLaunch on the caller's stream.  Host enqueue of the parts
-// costs ~1.1 ms otherwise and staggers their start on the GPU by ~0.4 ms per part.
+// CUDA-graph cache of hg_solve / hg_solve_host: the whole multi-stream launch sequence
+// (6 parts of ~67 kernels, their fork/join events, the host copies) is captured once per
+// distinct argument set and replayed with one cudaGraphLaunch on the caller's stream.
+// Enqueued directly, the parts cost ~1.1-1.5 ms of host time and start ~0.4 ms apart.
+extern "C++" {
 namespace {
-struct SolveKey {
-  hg_incidence H;
-  const float *w, *Y;
-  float mu, *F, *sigma;
-  int32_t b, k, q, T, parts;
-  uint64_t seed;
-  uint32_t flags;
-  int32_t* st;
-  void* ws;
-  size_t ws_bytes;
-  std::string env;
-  bool operator==(const SolveKey& o) const {
-    return std::memcmp(&H, &o.H, sizeof H) == 0 && w == o.w && Y == o.Y && mu == o.mu && F == o.F &&
-           sigma == o.sigma && b == o.b && k == o.k && q == o.q && T == o.T && parts == o.parts && seed == o.seed &&
-           flags == o.flags && st == o.st && ws == o.ws && ws_bytes == o.ws_bytes && env == o.env;
-  }
-};
 struct GraphEntry {
-  SolveKey key;
+  std::string key;
   cudaGraphExec_t exec;
   int launches;
 };
@@ -783,28 +771,20 @@ std::string knob_env() {   // enqueue-time knobs that change the captured sequen
   }
   return e;
 }
-}  // namespace
-
-hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q, uint64_t seed,
-                   const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags, int32_t* d_status, void* ws,
-                   size_t ws_bytes, hg_stream_t stream) {
-  g_err.clear();
-  g_launches = 0;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  HG_CU(cudaStreamIsCapturing(s, &cap), "capture status");
+template <class T>
+void key_add(std::string& k, const T& v) {
+  k.append(reinterpret_cast<const char*>(&v), sizeof v);
+}
+bool graphs_enabled(cudaStream_t s) {
   const char* ng = getenv("HG_NO_GRAPH");
-  if (g_prof_on || cap != cudaStreamCaptureStatusNone || (ng && ng[0] == '1'))
-    return solve_impl(H, w, mu, b, k, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes, s);
-  // host-side validation first (nothing is captured for an invalid call)
-  HG_TRY(check_H(H));
-  HG_TRY(check_sizes(H->n_vertices, b, k, q, T));
-  const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, k, T);
-  HG_TRY(check_ws(ws, ws_bytes, Lo.h_rowptr));
-  if (!d_status && !(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
-  int32_t* st = d_status ? d_status : at<int32_t>(ws, Lo.status);
-  SolveKey key{*H, w, Y, mu, F, sigma_out, b, k, q, T, solve_parts(), seed, flags & ~HG_SYNC, st, ws, ws_bytes,
-               knob_env()};
+  if (g_prof_on || (ng && ng[0] == '1')) return false;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) return false;
+  return cap == cudaStreamCaptureStatusNone;
+}
+// Replay the cached graph for `key`, capturing `enqueue(capture_stream)` first if needed.
+template <class Fn>
+hg_status graph_run(const std::string& key, cudaStream_t s, Fn enqueue) {
   GraphEntry* ge = nullptr;
   for (auto& e : g_graphs)
     if (e.key == key) ge = &e;
@@ -813,13 +793,8 @@ hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, i
     static thread_local cudaStream_t cs = nullptr;
     if (!cs) HG_CU(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
     HG_CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
-    hg_status r = HG_OK;
-    if (!d_status) {
-      cudaError_t e = cudaMemsetAsync(st, 0, sizeof(int32_t), cs);
-      if (e != cudaSuccess) r = cuda_fail(e, "memset status");
-    }
-    if (r == HG_OK)
-      r = solve_impl(H, w, mu, b, k, q, seed, Y, T, F, sigma_out, flags & ~HG_SYNC, st, ws, ws_bytes, cs);
+    g_launches = 0;
+    const hg_status r = enqueue(cs);
     cudaGraph_t graph = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
     if (r != HG_OK || ec != cudaSuccess) {
@@ -840,6 +815,35 @@ hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, i
   }
   HG_CU(cudaGraphLaunch(ge->exec, s), "graph launch");
   g_launches = ge->launches;
+  return HG_OK;
+}
+}  // namespace
+}  // extern "C++"
+
+hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q, uint64_t seed,
+                   const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags, int32_t* d_status, void* ws,
+                   size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!graphs_enabled(s))
+    return solve_impl(H, w, mu, b, k, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes, s);
+  // host-side validation first (nothing is captured for an invalid call)
+  HG_TRY(check_H(H));
+  HG_TRY(check_sizes(H->n_vertices, b, k, q, T));
+  const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, k, T);
+  HG_TRY(check_ws(ws, ws_bytes, Lo.h_rowptr));
+  if (!d_status && !(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
+  int32_t* st = d_status ? d_status : at<int32_t>(ws, Lo.status);
+  std::string key = "solve|" + knob_env();
+  key_add(key, *H);
+  key_add(key, w); key_add(key, mu); key_add(key, b); key_add(key, k); key_add(key, q); key_add(key, seed);
+  key_add(key, Y); key_add(key, T); key_add(key, F); key_add(key, sigma_out); key_add(key, flags & ~HG_SYNC);
+  key_add(key, st); key_add(key, ws); key_add(key, ws_bytes); key_add(key, solve_parts());
+  HG_TRY(graph_run(key, s, [&](cudaStream_t cs) -> hg_status {
+    if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), cs), "memset status");
+    return solve_impl(H, w, mu, b, k, q, seed, Y, T, F, sigma_out, flags & ~HG_SYNC, st, ws, ws_bytes, cs);
+  }));
   if (flags & HG_SYNC) {
     int32_t h = 0;
     HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
@@ -863,6 +867,8 @@ hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_pt
   const Layout Lo = layout(N, E, nnz, b, k, T);
   HG_TRY(check_ws(ws, ws_bytes, Lo.total));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int32_t* st = at<int32_t>(ws, Lo.status);
+  auto enqueue = [&](cudaStream_t s) -> hg_status {   // (shadows the caller's stream when captured)
   int64_t* d_rp = at<int64_t>(ws, Lo.h_rowptr);
   int32_t* d_col = at<int32_t>(ws, Lo.h_col);
   float* d_w = at<float>(ws, Lo.h_w);
@@ -874,7 +880,6 @@ hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_pt
   hg_incidence H{N, E, nnz, d_rp, d_col};
   const int nb = N / b;
   float* d_sig = at<float>(ws, Lo.sigma);
-  int32_t* st = at<int32_t>(ws, Lo.status);
   HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), s), "memset status");
   HostIO io;
   io.Y_host = Y_host;
@@ -882,6 +887,18 @@ hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_pt
   HG_TRY(solve_impl(&H, d_w, mu, b, k, q, seed, d_Y, T, d_F, d_sig, flags & ~HG_SYNC, st, ws, ws_bytes, s, io));
   if (sigma_host)
     HG_CU(cudaMemcpyAsync(sigma_host, d_sig, 4 * (size_t)nb * k, cudaMemcpyDeviceToHost, s), "D2H sigma");
+  return HG_OK;
+  };
+  if (graphs_enabled(s)) {
+    std::string key = "host|" + knob_env();
+    key_add(key, N); key_add(key, E); key_add(key, nnz); key_add(key, row_ptr_host); key_add(key, col_idx_host);
+    key_add(key, w_host); key_add(key, mu); key_add(key, b); key_add(key, k); key_add(key, q); key_add(key, seed);
+    key_add(key, Y_host); key_add(key, T); key_add(key, F_host); key_add(key, sigma_host);
+    key_add(key, flags & ~HG_SYNC); key_add(key, ws); key_add(key, ws_bytes); key_add(key, solve_parts());
+    HG_TRY(graph_run(key, s, enqueue));
+  } else {
+    HG_TRY(enqueue(s));
+  }
   int32_t h = 0;
   HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
   HG_CU(cudaStreamSynchronize(s), "synchronize");
