@@ -60,6 +60,16 @@ cudaEvent_t prof_event() {
   cudaEventCreate(&e);
   return e;
 }
+// record a profiling event; inside a stream capture it must be an external record node
+// (a plain record there only expresses a dependency inside the graph)
+inline void prof_record(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, s);
+}
+
 struct ProfScope {
   bool on;
   cudaStream_t s;
@@ -70,11 +80,11 @@ struct ProfScope {
     r.part = g_cur_part;
     r.a = prof_event();
     r.b = prof_event();
-    cudaEventRecord(r.a, s);
+    prof_record(r.a, s);
   }
   ~ProfScope() {
     if (!on) return;
-    cudaEventRecord(r.b, s);
+    prof_record(r.b, s);
     g_prof.push_back(r);
   }
 };
@@ -696,7 +706,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   const int nparts = g_prof_mode == 1 ? 1 : std::max(1, std::min(solve_parts(), nb));
   if (g_prof_mode == 2 && !g_t0_set) {
     if (!g_t0) HG_CU(cudaEventCreate(&g_t0), "event create");
-    HG_CU(cudaEventRecord(g_t0, s), "t0 record");
+    prof_record(g_t0, s);
     g_t0_set = true;
   }
   cudaStream_t ps[kMaxParts];
@@ -777,7 +787,7 @@ void key_add(std::string& k, const T& v) {
 }
 bool graphs_enabled(cudaStream_t s) {
   const char* ng = getenv("HG_NO_GRAPH");
-  if (g_prof_on || (ng && ng[0] == '1')) return false;
+  if (g_prof_mode == 1 || (ng && ng[0] == '1')) return false;   // timeline mode (2) captures too
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) return false;
   return cap == cudaStreamCaptureStatusNone;
@@ -786,8 +796,9 @@ bool graphs_enabled(cudaStream_t s) {
 template <class Fn>
 hg_status graph_run(const std::string& key, cudaStream_t s, Fn enqueue) {
   GraphEntry* ge = nullptr;
+  const bool cache = g_prof_mode != 2;   // timeline graphs carry this call's stage events: not reused
   for (auto& e : g_graphs)
-    if (e.key == key) ge = &e;
+    if (cache && e.key == key) ge = &e;
   if (!ge) {
     HG_TRY(ensure_streams());
     static thread_local cudaStream_t cs = nullptr;
@@ -806,6 +817,11 @@ hg_status graph_run(const std::string& key, cudaStream_t s, Fn enqueue) {
     const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     if (ei != cudaSuccess) return cuda_fail(ei, "graph instantiate");
+    if (!cache) {
+      HG_CU(cudaGraphLaunch(exec, s), "graph launch");
+      cudaGraphExecDestroy(exec);   // released once the launched work completes
+      return HG_OK;
+    }
     if (g_graphs.size() >= kMaxGraphs) {
       cudaGraphExecDestroy(g_graphs.front().exec);
       g_graphs.erase(g_graphs.begin());
