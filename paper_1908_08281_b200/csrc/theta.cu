@@ -192,6 +192,7 @@ constexpr int SEG_CAP = 16384;      // keys per segment in shared memory (64 KB)
 constexpr int NSEG_MAX = 4;         // b <= 4 SEG_V on the sorted path
 constexpr int ROWS_NT = 512;        // k_assemble_rows: one warp per row
 constexpr int TR_ROWS = ROWS_NT / 32;
+constexpr int STAGE_KEYS = 512;     // per-warp member-key staging (2 KB)
 
 __global__ void __launch_bounds__(1024) k_seg_sort(int blk0, int b, const int64_t* __restrict__ row_ptr,
                                                    const int32_t* __restrict__ col, uint32_t* __restrict__ keys,
@@ -263,7 +264,7 @@ __device__ __forceinline__ void assemble_rows_walk(int b, int nu, int nseg, int6
                                                    const uint32_t* __restrict__ K, const int2* __restrict__ rng,
                                                    const float* __restrict__ eval, const float* __restrict__ dvr,
                                                    float inv1pmu, int raw, float* __restrict__ out, float* acc,
-                                                   int lane, int warp) {
+                                                   uint32_t* stage, int lane, int warp) {
   for (int r = warp; r < nu; r += ROWS_NT / 32) {
     const int64_t u = base + u0 + r;
     const int64_t q0 = row_ptr[u], q1 = row_ptr[u + 1];
@@ -280,16 +281,50 @@ __device__ __forceinline__ void assemble_rows_walk(int b, int nu, int nseg, int6
         val = eval[e];
         for (int sg = 0; sg < nseg; ++sg) rg[sg] = rng[(c0 + lane) * NSEG_MAX + sg];
       }
-      for (int j = 0; j < ne; ++j) {             // ascending edge order
-        const float vj = __shfl_sync(0xffffffffu, val, j);
-        const uint32_t ebj = __shfl_sync(0xffffffffu, e, j) * (uint32_t)b;
+      // gather: lane j copies its edge's member runs into the warp's staging area (all
+      // loads in flight together), then the scatter runs in ascending edge order from
+      // shared memory -- one L2 round trip per row chunk instead of one per edge
+      int len = 0;
 #pragma unroll
-        for (int sg = 0; sg < NSEG_MAX; ++sg) {
-          if (sg >= nseg) break;
-          const int l = __shfl_sync(0xffffffffu, rg[sg].x, j), h = __shfl_sync(0xffffffffu, rg[sg].y, j);
-          for (int m = l + lane; m < h; m += 32) arow[K[m] - ebj] += vj;
+      for (int sg = 0; sg < NSEG_MAX; ++sg)
+        if (sg < nseg) len += rg[sg].y - rg[sg].x;
+      int off = len;                               // inclusive warp scan of the run lengths
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, off, o);
+        if (lane >= o) off += x;
+      }
+      const int total = __shfl_sync(0xffffffffu, off, 31);
+      off -= len;                                  // exclusive
+      if (total <= STAGE_KEYS) {
+        if (lane < ne) {
+          int d = off;
+#pragma unroll
+          for (int sg = 0; sg < NSEG_MAX; ++sg) {
+            if (sg >= nseg) break;
+            for (int m = rg[sg].x; m < rg[sg].y; ++m) stage[d++] = K[m];
+          }
         }
         __syncwarp();
+        for (int j = 0; j < ne; ++j) {             // ascending edge order
+          const float vj = __shfl_sync(0xffffffffu, val, j);
+          const uint32_t ebj = __shfl_sync(0xffffffffu, e, j) * (uint32_t)b;
+          const int o0 = __shfl_sync(0xffffffffu, off, j), n0 = __shfl_sync(0xffffffffu, len, j);
+          for (int i = lane; i < n0; i += 32) arow[stage[o0 + i] - ebj] += vj;
+          __syncwarp();
+        }
+      } else {
+        for (int j = 0; j < ne; ++j) {             // ascending edge order (long rows: direct)
+          const float vj = __shfl_sync(0xffffffffu, val, j);
+          const uint32_t ebj = __shfl_sync(0xffffffffu, e, j) * (uint32_t)b;
+#pragma unroll
+          for (int sg = 0; sg < NSEG_MAX; ++sg) {
+            if (sg >= nseg) break;
+            const int l = __shfl_sync(0xffffffffu, rg[sg].x, j), h = __shfl_sync(0xffffffffu, rg[sg].y, j);
+            for (int m = l + lane; m < h; m += 32) arow[K[m] - ebj] += vj;
+          }
+          __syncwarp();
+        }
       }
     }
     const int uu = u0 + r;
@@ -314,6 +349,7 @@ __global__ void __launch_bounds__(ROWS_NT) k_assemble_rows(int blk0, int b, cons
   if (overflow[blk]) return;                      // handled by the hashed-tile kernel
   extern __shared__ __align__(16) uint8_t smem_raw[];
   float* acc = reinterpret_cast<float*>(smem_raw);   // [TR_ROWS][b]
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smem_raw + (size_t)TR_ROWS * b * 4) + (threadIdx.x >> 5) * STAGE_KEYS;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t base = (int64_t)blk * b;
   const int u0 = blockIdx.y * TR_ROWS;
@@ -323,7 +359,7 @@ __global__ void __launch_bounds__(ROWS_NT) k_assemble_rows(int blk0, int b, cons
   for (int i = t; i < TR_ROWS * b; i += ROWS_NT) acc[i] = 0.f;
   __syncthreads();
   assemble_rows_walk(b, nu, nseg, base, u0, row_ptr, col, keys + kb0, rng, eval, dvr, inv1pmu, raw,
-                     blocks + (int64_t)blk * b * b, acc, lane, warp);
+                     blocks + (int64_t)blk * b * b, acc, stage, lane, warp);
 }
 
 }  // namespace
@@ -374,7 +410,7 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
       attr1 = true;
     }
     k_seg_sort<<<dim3(nb, nseg), 1024, ssmem, s>>>(blk0, b, row_ptr, col_idx, keys, rng, overflow);
-    const size_t smem = (size_t)TR_ROWS * b * 4;
+    const size_t smem = (size_t)TR_ROWS * b * 4 + (size_t)(ROWS_NT / 32) * STAGE_KEYS * 4;
     static size_t attr2 = 0;
     if (smem > attr2) {
       e = cudaFuncSetAttribute(k_assemble_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
