@@ -285,6 +285,28 @@ def test_timeline_profiler_parts_overlap(inputs, monkeypatch):
     assert len(j) == 2 and j[1][0] < j[0][1]
 
 
+def test_graph_replay_matches_direct_enqueue(inputs, monkeypatch):
+    """hg_solve replays a cached CUDA graph of its launch sequence; the direct path
+    (HG_NO_GRAPH=1), a second workspace (new capture) and a repeat call (replay) agree
+    bit for bit."""
+    hg = hgm()
+    h = inputs(2)
+    c = CONFIGS[2]
+    H, w, Y = dev_inputs(h)
+    monkeypatch.setenv("HG_NO_GRAPH", "1")
+    F0, s0, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)
+    monkeypatch.delenv("HG_NO_GRAPH")
+    F1, s1, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)
+    F2, s2, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)   # fresh outputs: new key
+    ws = hg.Workspace.for_sizes(c.N, h.E, h.nnz, c.b, c.k, c.T)
+    F3, s3, st3 = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0, ws=ws, sync=False)
+    hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0, ws=ws, F=F3, sigma=s3, status=st3, sync=False)
+    torch.cuda.synchronize()
+    assert int(st3.item()) == 0
+    for F, sg in ((F1, s1), (F2, s2), (F3, s3)):
+        assert torch.equal(F, F0) and torch.equal(sg, s0)
+
+
 def test_deterministic_and_host_entry(inputs):
     hg = hgm()
     h = inputs(2)
