@@ -156,6 +156,16 @@ def oracle_sample(h, c, n_blocks, seed=0):
     return r
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -337,7 +347,16 @@ def run_ours(args):
             rr = oracle_sample(h, c, n_s, seed=seed)
             cpu_base = {"value": n_s / rr.seconds, "unit": "blocks/s", "cores": rr.threads, "kind": "oracle",
                         "sample": f"{n_s} of {c.nb} diagonal blocks of the same workload (Alg. 1 + apply, FP64, "
-                                  f"OpenMP over blocks), {rr.seconds:.1f} s"}
+                                  f"OpenMP over blocks), {rr.seconds:.1f} s",
+                        "cpu_model": cpu_model()}
+            # single-thread figure on one block (report 1 thread and all cores)
+            import oracle
+            oracle.set_num_threads(1)
+            try:
+                r1 = oracle_sample(h, c, 1, seed=seed)
+                cpu_base["value_1thread"] = 1.0 / r1.seconds
+            finally:
+                oracle.set_num_threads(nthreads)
 
     out = {
         "metric": "diag_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
@@ -390,7 +409,8 @@ def run_reference(args):
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": config_json(c, note="reference arm = FP64 CPU oracle (no reference implementation exists)"),
            "cpu_baseline": {"value": v, "unit": "blocks/s", "cores": r.threads, "kind": "oracle",
-                            "sample": f"{n_s} of {c.nb} diagonal blocks per step (Alg. 1 + apply, FP64, OpenMP)"},
+                            "sample": f"{n_s} of {c.nb} diagonal blocks per step (Alg. 1 + apply, FP64, OpenMP)",
+                            "cpu_model": cpu_model()},
            "e2e": {"value": v, "unit": "blocks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

@@ -63,6 +63,8 @@ def lib() -> ctypes.CDLL:
                                P, P, P, P, P, P, cp, ci]
         L.or_solve.restype = ci
         L.or_num_threads.restype = ci
+        L.or_set_num_threads.argtypes = [ci]
+        L.or_set_num_threads.restype = None
         _lib = L
     return _lib
 
@@ -185,6 +187,15 @@ class SolveResult:
     def __init__(self, blocks, F, sigma, U, V, resid, X, seconds, threads):
         self.blocks, self.F, self.sigma, self.U, self.V = blocks, F, sigma, U, V
         self.resid, self.X, self.seconds, self.threads = resid, X, seconds, threads
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the oracle (results are bit-identical at any count)."""
+    lib().or_set_num_threads(int(n))
+
+
+def num_threads() -> int:
+    return int(lib().or_num_threads())
 
 
 def solve(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, seed: int,

@@ -578,6 +578,15 @@ int or_solve(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_id
   return OR_OK;
 }
 
+/* Threading only (test infrastructure): results are bit-identical at any thread count. */
+void or_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 int or_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

@@ -1,9 +1,11 @@
 """configs[4] sweep: N=32768, b in {512,1024,2048}, k in {64..512}, q in {1,2,4} (36 points).
 
 For every point: GPU solve time (CUDA events, median of reps), parity against the
-FP64 oracle on blocks {0, nb-1} (F rel-Frobenius, sigma rel), and accuracy of the
+FP64 oracle on blocks {0, nb-1} (F rel-Frobenius, sigma rel), accuracy of the
 rank-k block inverse against the exact block solve c X_ii^-1 Y_i (FP64 LU) on
-the same blocks.  One JSON line per point.
+the same blocks, and accuracy of the whole GPU F against the full solve
+F* = c X^-1 Y (FP64 block CG on the sparse operator; computed
+once: it does not depend on b, k, q).  One JSON line per point.
 
     python tools/sweep_cfg5.py [--points b,k,q ...] > profiles/r01_cfg5_sweep.jsonl
 """
@@ -23,6 +25,46 @@ from paper_1908_08281_b200 import hg  # noqa: E402
 from synth.hypergraph import CONFIGS, cfg5_points, make_input  # noqa: E402
 
 
+def full_solve_cg(h, mu, tol=1e-10, maxit=200):
+    """F* = c X^-1 Y, X = I - Theta/(1+mu), Theta = Dv^-1/2 H W De^-1 H^T Dv^-1/2,
+    by block CG in FP64 with all T right-hand sides at once (X is SPD, cond(X) <= (1+mu)/mu)."""
+    import scipy.sparse as sp
+    N = len(h.row_ptr) - 1
+    Hs = sp.csr_matrix((np.ones(len(h.col_idx)), h.col_idx, h.row_ptr), shape=(N, len(h.w)))
+    w = h.w.astype(np.float64)
+    de = np.asarray(Hs.sum(axis=0)).ravel()
+    dv = Hs @ w
+    dh = 1.0 / np.sqrt(dv)
+    we = w / de
+    c1 = 1.0 / (1.0 + mu)
+
+    def A(V):
+        Z = dh[:, None] * V
+        Z = Hs.T @ Z
+        Z = we[:, None] * Z
+        Z = Hs @ Z
+        return V - c1 * (dh[:, None] * Z)
+
+    B = (mu / (1.0 + mu)) * h.Y.astype(np.float64)
+    X = np.zeros_like(B)
+    R = B.copy()
+    P = R.copy()
+    rs = np.sum(R * R, axis=0)
+    bn = np.maximum(np.sum(B * B, axis=0), 1e-300)
+    it = 0
+    for it in range(1, maxit + 1):
+        AP = A(P)
+        alpha = rs / np.maximum(np.sum(P * AP, axis=0), 1e-300)
+        X += alpha * P
+        R -= alpha * AP
+        rs_new = np.sum(R * R, axis=0)
+        if np.max(np.sqrt(rs_new / bn)) < tol:
+            break
+        P = R + (rs_new / np.maximum(rs, 1e-300)) * P
+        rs = rs_new
+    return X, it
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--points", nargs="*")
@@ -34,6 +76,10 @@ def main():
     H = hg.incidence_to_device(h.row_ptr, h.col_idx, h.E)
     w = torch.from_numpy(h.w).cuda()
     Y = torch.from_numpy(h.Y).cuda()
+    t0 = time.time()
+    Fstar, cg_it = full_solve_cg(h, base.mu)
+    print(json.dumps({"full_solve_cg": {"iterations": cg_it, "seconds": time.time() - t0,
+                                        "norm": float(np.linalg.norm(Fstar))}}), flush=True)
     for (b, k, q) in pts:
         c = base.with_(b=b, k=k, q=q)
         out = {"b": b, "k": k, "q": q, "nb": c.nb}
@@ -53,6 +99,8 @@ def main():
             ms = float(np.median(ts))
             out.update({"solve_ms": ms, "blocks_per_s": c.nb / (ms / 1e3),
                         "gemm_useful_gflop": 4.0 * (q + 1) * c.N * b * k / 1e9})
+            Fall = F.double().cpu().numpy()
+            out["gpu_vs_full_solve"] = float(np.linalg.norm(Fall - Fstar) / np.linalg.norm(Fstar))
             blocks = [0, c.nb - 1]
             t0 = time.time()
             r = oracle.solve(h.row_ptr, h.col_idx, h.w, h.Y, mu=c.mu, b=b, k=k, q=q, seed=0, blocks=blocks,
