@@ -1,5 +1,5 @@
 import os, sys, time, torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_1908_08281_b200 import hg
 from synth.hypergraph import CONFIGS, make_input
 c = CONFIGS[4]
