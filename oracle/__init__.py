@@ -62,6 +62,10 @@ def lib() -> ctypes.CDLL:
         L.or_solve.argtypes = [i32, i32, P, P, P, dbl, i32, i32, i32, u64, P, i32, i32, P,
                                P, P, P, P, P, P, cp, ci]
         L.or_solve.restype = ci
+        L.or_apply_X.argtypes = [i32, i32, P, P, P, P, P, dbl, P, P, P]
+        L.or_apply_X.restype = None
+        L.or_cg_solve.argtypes = [i32, i32, P, P, P, dbl, P, i32, i32, dbl, P, P, P, cp, ci]
+        L.or_cg_solve.restype = ci
         L.or_num_threads.restype = ci
         L.or_set_num_threads.argtypes = [ci]
         L.or_set_num_threads.restype = None
@@ -228,3 +232,44 @@ def solve(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, seed: in
     if st != OK:
         raise OracleError(st, err.value.decode())
     return SolveResult(list(map(int, sel)), F, sigma, U, V, resid, X, dt, lib().or_num_threads())
+
+
+# ------------------------------------------------- second approach: CG
+def _csr(row_ptr, col_idx, w):
+    return (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col_idx, np.int32),
+            np.ascontiguousarray(w, np.float32))
+
+
+def apply_X(row_ptr, col_idx, w, p, *, mu: float) -> np.ndarray:
+    """X p for one length-N vector, matrix-free through H."""
+    row_ptr, col_idx, w = _csr(row_ptr, col_idx, w)
+    N, E = len(row_ptr) - 1, len(w)
+    dv, de = degrees(row_ptr, col_idx, w)
+    p = np.ascontiguousarray(p, np.float64)
+    out, t = np.zeros(N), np.zeros(E)
+    lib().or_apply_X(N, E, _p(row_ptr), _p(col_idx), _p(w), _p(dv), _p(de), mu, _p(p), _p(t), _p(out))
+    return out
+
+
+class CGResult:
+    def __init__(self, F, iters, rel_res, seconds, threads):
+        self.F, self.iters, self.rel_res, self.seconds, self.threads = F, iters, rel_res, seconds, threads
+
+
+def cg_solve(row_ptr, col_idx, w, Y, *, mu: float, max_iter: int, tol: float) -> CGResult:
+    """CG on X F = theta/(1+theta) Y (Eqs. 5, 16-20), one independent CG per column of Y."""
+    row_ptr, col_idx, w = _csr(row_ptr, col_idx, w)
+    Y = np.ascontiguousarray(Y, np.float32)
+    N, E = len(row_ptr) - 1, len(w)
+    T = Y.shape[1]
+    F = np.zeros((N, T))
+    iters = np.zeros(T, np.int32)
+    rel = np.zeros(T)
+    err = ctypes.create_string_buffer(256)
+    t0 = time.perf_counter()
+    st = lib().or_cg_solve(N, E, _p(row_ptr), _p(col_idx), _p(w), mu, _p(Y), T, max_iter, tol,
+                           _p(F), _p(iters), _p(rel), err, 256)
+    dt = time.perf_counter() - t0
+    if st != OK:
+        raise OracleError(st, err.value.decode())
+    return CGResult(F, iters, rel, dt, lib().or_num_threads())

@@ -20,6 +20,9 @@
  *   or_rsvd_block       PAPER.md:108-124 Alg. 1 (literal X^T in the loop), Eq. 7 residual
  *   or_apply_block      PAPER.md:43-45,160-163  Eq. 3 with Eq. 15: f = c V Sigma^-1 U^T y
  *   or_solve            the whole path over a chosen subset of diagonal blocks
+ *   or_apply_X          PAPER.md:30-40   X p = p - (1/(1+theta)) Dv^-1/2 H W De^-1 H^T Dv^-1/2 p (matrix-free)
+ *   or_cg_solve         PAPER.md:165-178 the paper's second approach: CG on Eq. 5, X f = theta/(1+theta) y
+ *                                        (Eqs. 16-20), one independent CG per right-hand-side column
  *
  * Pinned by tests/test_oracle_*.py against closed forms, library routines,
  * brute force and invariants.
@@ -575,6 +578,102 @@ int or_solve(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_id
   }
   free(dv); free(de);
   if (fail) { set_err(err, errlen, "numerical failure (SVD non-convergence or singular sigma)"); return fail; }
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Second approach: conjugate gradient on Eq. 5          */
+/* ------------------------------------------------------------------------ */
+/* out = X p for one vector p of length N, X = I - A/(1+mu), A = Eq. 1 applied
+ * right to left: s = Dv^-1/2 p;  t = H^T s;  t = W De^-1 t;  u = H t;
+ * A p = Dv^-1/2 u.  t is scratch of length E. */
+void or_apply_X(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
+                const double* dv, const double* de, double mu, const double* p, double* t, double* out) {
+  for (int32_t e = 0; e < E; ++e) t[e] = 0.0;
+  for (int32_t v = 0; v < N; ++v) {                    /* t = H^T Dv^-1/2 p */
+    double sv = p[v] / sqrt(dv[v]);
+    for (int64_t q = row_ptr[v]; q < row_ptr[v + 1]; ++q) t[col_idx[q]] += sv;
+  }
+  for (int32_t e = 0; e < E; ++e) t[e] *= (double)w[e] / de[e];   /* W De^-1 */
+  for (int32_t v = 0; v < N; ++v) {                    /* A p = Dv^-1/2 H t */
+    double u = 0.0;
+    for (int64_t q = row_ptr[v]; q < row_ptr[v + 1]; ++q) u += t[col_idx[q]];
+    out[v] = p[v] - (u / sqrt(dv[v])) / (1.0 + mu);
+  }
+}
+
+static double dot(int32_t n, const double* a, const double* b) {
+  double s = 0.0;
+  for (int32_t i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+
+/* CG (Eqs. 16-20) on X f = c y, c = theta/(1+theta) (Eq. 5),
+ * independently for every column t of Y (N x T, row-major fp32):
+ *   f_0 = 0 (reading C1), r_0 = c y - X f_0, p_0 = r_0;
+ *   for i >= 1:  alpha_i = r_{i-1}^T r_{i-1} / p_{i-1}^T X p_{i-1}      (Eq. 19)
+ *                f_i = f_{i-1} + alpha_i p_{i-1}                         (Eq. 16)
+ *                r_i = r_{i-1} - alpha_i X p_{i-1}                       (Eq. 17)
+ *                beta_i = r_i^T r_i / r_{i-1}^T r_{i-1}                  (Eq. 20)
+ *                p_i = r_i + beta_i p_{i-1}                              (Eq. 18)
+ * Stopping (reading C2): before iteration i, stop when ||r_{i-1}|| <= tol ||r_0||
+ * or i > max_iter.  A zero column (r_0 = 0) takes no iteration and f = 0.
+ * Outputs: F (N x T fp64), iters[T] (iterations taken), rel_res[T] = ||r||/||r_0||
+ * of the recurrence residual at exit (0 for a zero column). */
+int or_cg_solve(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
+                double mu, const float* Y, int32_t T, int32_t max_iter, double tol, double* F,
+                int32_t* iters, double* rel_res, char* err, int errlen) {
+  if (N <= 0 || E <= 0 || T < 0 || max_iter < 0 || !(mu > 0.0) || !(tol >= 0.0)) {
+    set_err(err, errlen, "invalid arguments (need N, E > 0, T >= 0, max_iter >= 0, mu > 0, tol >= 0)");
+    return OR_ERR_INVALID;
+  }
+  double* dv = (double*)malloc(sizeof(double) * (size_t)N);
+  double* de = (double*)malloc(sizeof(double) * (size_t)E);
+  int st = or_degrees(N, E, row_ptr, col_idx, w, dv, de, err, errlen);
+  if (st != OR_OK) { free(dv); free(de); return st; }
+  double c = mu / (1.0 + mu);
+  int fail = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int32_t col = 0; col < T; ++col) {
+    double* f = (double*)malloc(sizeof(double) * (size_t)N);
+    double* r = (double*)malloc(sizeof(double) * (size_t)N);
+    double* p = (double*)malloc(sizeof(double) * (size_t)N);
+    double* Xp = (double*)malloc(sizeof(double) * (size_t)N);
+    double* t = (double*)malloc(sizeof(double) * (size_t)E);
+    for (int32_t v = 0; v < N; ++v) f[v] = 0.0;
+    or_apply_X(N, E, row_ptr, col_idx, w, dv, de, mu, f, t, Xp);
+    for (int32_t v = 0; v < N; ++v) {
+      r[v] = c * (double)Y[(int64_t)v * T + col] - Xp[v];
+      p[v] = r[v];
+    }
+    double rr = dot(N, r, r), rr0 = rr;
+    int32_t i = 0;
+    if (rr0 > 0.0) {
+      while (i < max_iter && !(sqrt(rr) <= tol * sqrt(rr0))) {
+        or_apply_X(N, E, row_ptr, col_idx, w, dv, de, mu, p, t, Xp);
+        double pXp = dot(N, p, Xp);
+        if (!(pXp > 0.0)) {
+#pragma omp atomic write
+          fail = OR_ERR_NUMERICAL;
+          break;
+        }
+        double alpha = rr / pXp;
+        for (int32_t v = 0; v < N; ++v) f[v] += alpha * p[v];
+        for (int32_t v = 0; v < N; ++v) r[v] -= alpha * Xp[v];
+        double rr_new = dot(N, r, r);
+        double beta = rr_new / rr;
+        for (int32_t v = 0; v < N; ++v) p[v] = r[v] + beta * p[v];
+        rr = rr_new;
+        ++i;
+      }
+    }
+    for (int32_t v = 0; v < N; ++v) F[(int64_t)v * T + col] = f[v];
+    iters[col] = i;
+    rel_res[col] = rr0 > 0.0 ? sqrt(rr / rr0) : 0.0;
+    free(f); free(r); free(p); free(Xp); free(t);
+  }
+  free(dv); free(de);
+  if (fail) { set_err(err, errlen, "CG breakdown (p^T X p <= 0)"); return fail; }
   return OR_OK;
 }
 
