@@ -56,7 +56,8 @@ enum hg_status_flags {
   HG_ST_CHOL_BREAKDOWN = 1 << 2,  /* CholeskyQR pivot <= 0: Y_i rank-deficient to fp32        */
   HG_ST_JACOBI_CAP = 1 << 3,      /* one-sided Jacobi did not converge in the sweep cap      */
   HG_ST_SINGULAR_SIGMA = 1 << 4,  /* sigma_j <= 1e-6 sigma_1 at apply      */
-  HG_ST_NONFINITE = 1 << 5        /* NaN/Inf met                                             */
+  HG_ST_NONFINITE = 1 << 5,       /* NaN/Inf met                                             */
+  HG_ST_CG_BREAKDOWN = 1 << 6     /* hg_cg_solve: p^T X p <= 0 (X is SPD: corrupt input only)  */
 };
 
 /* flags */
@@ -153,6 +154,28 @@ hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_pt
                         int32_t q, uint64_t seed, const float* Y_host, int32_t T, float* F_host,
                         float* sigma_host, uint32_t flags, void* ws, size_t ws_bytes, hg_stream_t stream);
 
+/* ---- The paper's second approach: conjugate gradient on Eq. 5,
+ *   X f = theta/(1+theta) y,   X = I - Theta/(1+theta)         (Eq. 1 for Theta)
+ * with the iteration of PAPER.md:165-178 (Eqs. 16-20), run independently for each of the T
+ * columns of Y:  f_0 = 0, r_0 = p_0 = c y;  alpha_i = r^T r / p^T X p;  f += alpha p;
+ * r -= alpha X p;  beta_i = r_i^T r_i / r_{i-1}^T r_{i-1};  p = r + beta p.
+ * X is applied matrix-free through H every iteration (never assembled).  Stopping (DESIGN.md
+ * reading C2): column t stops once ||r_i|| <= tol ||r_0|| or after max_iter iterations; a zero
+ * column takes no iteration (f = 0).  fp32 vectors, fp64 scalars.
+ *   Y, F      [N][T] fp32 (device); T % 4 == 0, T >= 1
+ *   max_iter  >= 0;  tol >= 0 (0 = run exactly max_iter iterations)
+ *   iters     [T] int32 iterations taken per column, may be NULL
+ *   rel_res   [T] fp32 ||r||/||r_0|| of the recurrence residual at exit, may be NULL
+ *   flags     HG_SYNC as for hg_solve (d_status may then be NULL)
+ * Scratch: hg_cg_workspace_size (about 4 vectors of N x T, one of E x T, plus the CSC of H).
+ * Graph mode (stream not capturing, HG_NO_GRAPH unset): the whole solve is one cached CUDA
+ * graph whose iteration body is a device-driven WHILE node (no host round trip per
+ * iteration); otherwise max_iter bodies are enqueued and return at once after convergence.
+ * Device errors: HG_ST_ISOLATED_VERTEX, HG_ST_EMPTY_EDGE, HG_ST_CG_BREAKDOWN, HG_ST_NONFINITE. */
+hg_status hg_cg_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t T, int32_t max_iter, size_t* bytes);
+hg_status hg_cg_solve(const hg_incidence* H, const float* w, float mu, const float* Y, int32_t T, int32_t max_iter,
+                      float tol, float* F, int32_t* iters, float* rel_res, uint32_t flags, int32_t* d_status,
+                      void* ws, size_t ws_bytes, hg_stream_t stream);
 /* Verification export of the batched GEMM the path runs on (3xTF32 on
  * tcgen05, or fp32 CUDA cores with HG_GEMM_SIMT):
  *   for g < batch: D_g(m,n) = alpha * rs_g[m] * cs_g[n] * sum_kk A_g(m,kk) B_g(kk,n)

@@ -34,10 +34,10 @@ thread_local int g_launches = 0;
 // CUDA events on the launching stream; hg_profile_collect sums the elapsed times
 // per stage.  Off by default: no events are recorded on the hot path.
 enum Stage { ST_DEGREES, ST_ASSEMBLE, ST_OMEGA, ST_GEMM_POWER, ST_GEMM_GRAM, ST_GEMM_QFORM, ST_GEMM_SVD,
-             ST_GEMM_APPLY, ST_CHOLINV, ST_JACOBI, ST_FINALIZE, ST_INV_SIGMA, ST_COUNT };
+             ST_GEMM_APPLY, ST_CHOLINV, ST_JACOBI, ST_FINALIZE, ST_INV_SIGMA, ST_CG, ST_COUNT };
 const char* const kStageNames[ST_COUNT] = {"degrees", "assemble", "omega", "gemm_power", "gemm_gram",
                                            "gemm_qform", "gemm_svd", "gemm_apply", "cholinv", "jacobi",
-                                           "finalize", "inv_sigma"};
+                                           "finalize", "inv_sigma", "cg"};
 struct ProfRec {
   int stage, part;
   cudaEvent_t a, b;
@@ -919,6 +919,115 @@ hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_pt
   HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
   HG_CU(cudaStreamSynchronize(s), "synchronize");
   if (h) return fail(HG_ERR_NUMERICAL, "device status 0x%x", h);
+  return HG_OK;
+}
+
+// ---------------------------------------------------------------- CG
+hg_status hg_cg_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t T, int32_t max_iter, size_t* bytes) {
+  g_err.clear();
+  if (!bytes) return fail(HG_ERR_INVALID, "bytes is NULL");
+  if (N <= 0 || E <= 0 || nnz < 0 || T < 1 || T % 4 || max_iter < 0)
+    return fail(HG_ERR_INVALID, "need N, E > 0, nnz >= 0, T >= 1 with T %% 4 == 0, max_iter >= 0");
+  if (nnz >= INT32_MAX) return fail(HG_ERR_INVALID, "nnz must be < 2^31 for hg_cg_solve");
+  *bytes = cg_layout(N, E, nnz, T, max_iter).total;
+  return HG_OK;
+}
+
+extern "C++" {
+namespace {
+// Stream-capture plumbing for the CG WHILE node (see CgGraphHook in kernels.cuh).
+struct CgCapture {
+  cudaStream_t cs = nullptr;   // the capturing stream
+  cudaStream_t bs = nullptr;   // captures the body graph
+  cudaGraph_t body = nullptr;
+};
+cudaError_t cg_begin(void* ctx, cudaGraphConditionalHandle* h) {
+  CgCapture* c = static_cast<CgCapture*>(ctx);
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaError_t e = cudaStreamGetCaptureInfo(c->cs, &st, nullptr, &g, &deps, &nd);
+  if (e != cudaSuccess) return e;
+  return cudaGraphConditionalHandleCreate(h, g, 0, cudaGraphCondAssignDefault);
+}
+cudaError_t cg_open_body(void* ctx, cudaGraphConditionalHandle h, cudaStream_t* bs) {
+  CgCapture* c = static_cast<CgCapture*>(ctx);
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaError_t e = cudaStreamGetCaptureInfo(c->cs, &st, nullptr, &g, &deps, &nd);
+  if (e != cudaSuccess) return e;
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  if ((e = cudaGraphAddNode(&node, g, deps, nd, &p)) != cudaSuccess) return e;
+  if ((e = cudaStreamUpdateCaptureDependencies(c->cs, &node, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
+    return e;
+  c->body = p.conditional.phGraph_out[0];
+  if (!c->bs && (e = cudaStreamCreateWithFlags(&c->bs, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  *bs = c->bs;
+  return cudaStreamBeginCaptureToGraph(c->bs, c->body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+}
+cudaError_t cg_close_body(void* ctx) {
+  CgCapture* c = static_cast<CgCapture*>(ctx);
+  cudaGraph_t g = c->body;
+  return cudaStreamEndCapture(c->bs, &g);
+}
+thread_local CgCapture g_cg_cap;
+}  // namespace
+}  // extern "C++"
+
+hg_status hg_cg_solve(const hg_incidence* H, const float* w, float mu, const float* Y, int32_t T, int32_t max_iter,
+                      float tol, float* F, int32_t* iters, float* rel_res, uint32_t flags, int32_t* d_status,
+                      void* ws, size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  HG_TRY(check_H(H));
+  if (T < 1 || T % 4) return fail(HG_ERR_INVALID, "T must be >= 1 and a multiple of 4 (T=%d)", T);
+  if (max_iter < 0) return fail(HG_ERR_INVALID, "max_iter must be >= 0");
+  if (!(mu > 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and > 0");
+  if (!(tol >= 0.f) || !std::isfinite(tol)) return fail(HG_ERR_INVALID, "tol must be finite and >= 0");
+  if (!w || !Y || !F) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (H->nnz >= INT32_MAX) return fail(HG_ERR_INVALID, "nnz must be < 2^31 for hg_cg_solve");
+  const CgLayout L = cg_layout(H->n_vertices, H->n_edges, H->nnz, T, max_iter);
+  HG_TRY(check_ws(ws, ws_bytes, L.total));
+  if (!d_status && !(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int32_t* st = d_status ? d_status : at<int32_t>(ws, L.status);
+  CgArgs a;
+  a.N = H->n_vertices; a.E = H->n_edges; a.nnz = H->nnz; a.row_ptr = H->row_ptr; a.col_idx = H->col_idx;
+  a.w = w; a.mu = mu; a.Y = Y; a.T = T; a.max_iter = max_iter; a.tol = tol; a.F = F;
+  a.iters_out = iters; a.rel_out = rel_res; a.status = st; a.ws = ws;
+  if (graphs_enabled(s) && !g_prof_on) {
+    std::string key = "cg|";
+    key_add(key, *H);
+    key_add(key, w); key_add(key, mu); key_add(key, Y); key_add(key, T); key_add(key, max_iter); key_add(key, tol);
+    key_add(key, F); key_add(key, iters); key_add(key, rel_res); key_add(key, st); key_add(key, ws);
+    key_add(key, ws_bytes);
+    HG_TRY(graph_run(key, s, [&](cudaStream_t cs) -> hg_status {
+      if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), cs), "memset status");
+      g_cg_cap.cs = cs;
+      CgGraphHook hook{&g_cg_cap, cg_begin, cg_open_body, cg_close_body};
+      HG_CU(launch_cg(a, &hook, cs, &g_launches), "cg (graph)");
+      return HG_OK;
+    }));
+  } else {
+    if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), s), "memset status");
+    ProfScope ps(ST_CG, s);
+    HG_CU(launch_cg(a, nullptr, s, &g_launches), "cg");
+  }
+  if (flags & HG_SYNC) {
+    int32_t h = 0;
+    HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
+    HG_CU(cudaStreamSynchronize(s), "synchronize");
+    if (h) return fail(HG_ERR_NUMERICAL, "device status 0x%x (bits: 1 isolated vertex, 2 empty hyperedge, "
+                       "32 non-finite, 64 CG breakdown)", h);
+  }
   return HG_OK;
 }
 

@@ -54,3 +54,40 @@ cudaError_t launch_unit_columns_t(int nb, int k, const float* Wf, float* Uk, cud
 // debug: inner-round clock stamps of the block Jacobi (enable != 0 switches them on; out may be NULL)
 cudaError_t jacobi_blk_inner_clocks(long long* out, int enable);
 
+
+// cg.cu -- the second approach: CG on Eq. 5, matrix-free through H
+struct CgArgs {
+  int N, E;
+  int64_t nnz;
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  const float* w;
+  float mu;
+  const float* Y;      // [N][T]
+  int T;
+  int max_iter;
+  float tol;
+  float* F;            // [N][T]
+  int32_t* iters_out;  // [T] or null
+  float* rel_out;      // [T] or null
+  int32_t* status;
+  void* ws;
+};
+struct CgLayout {
+  int TS, ns, nparts;
+  int64_t max_items, max_big;
+  size_t de, eval, dvr, col_ptr, item_ptr, slot_ptr, big_ptr, cursor, totals, csc_tmp, csc, items, bigs;
+  size_t P, R, F, XP, Q, part, red, rr, rr0, alpha, beta, active, iters, ctl, status, total;
+};
+// Graph mode: begin() creates the WHILE node's handle in the graph being captured; open_body()
+// adds the conditional node after the captured work so far and returns a stream capturing into
+// its body graph; close_body() ends that capture.
+struct CgGraphHook {
+  void* ctx;
+  cudaError_t (*begin)(void* ctx, cudaGraphConditionalHandle* h);
+  cudaError_t (*open_body)(void* ctx, cudaGraphConditionalHandle h, cudaStream_t* body_stream);
+  cudaError_t (*close_body)(void* ctx);
+};
+int cg_lanes(int T);
+CgLayout cg_layout(int64_t N, int64_t E, int64_t nnz, int64_t T, int64_t max_iter);
+cudaError_t launch_cg(const CgArgs& a, const CgGraphHook* hook, cudaStream_t s, int* launches);

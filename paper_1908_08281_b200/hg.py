@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libhgrsvd.so")
 HG_OK, HG_ERR_INVALID, HG_ERR_NUMERICAL, HG_ERR_CUDA = 0, 2, 3, 4
 HG_RAW_THETA, HG_SYNC, HG_GEMM_SIMT = 1 << 0, 1 << 1, 1 << 8
 ST_FLAGS = {1: "isolated vertex", 2: "empty hyperedge", 4: "Cholesky breakdown", 8: "Jacobi sweep cap",
-            16: "singular sigma", 32: "non-finite value"}
+            16: "singular sigma", 32: "non-finite value", 64: "CG breakdown"}
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1908_08281_b200.build` "
@@ -56,6 +56,9 @@ _solve_host = _sig("hg_solve_host", ctypes.c_int, _i32, _i32, _i64, _P, _P, _P, 
                    _i32, _P, _P, _u32, _P, _sz, _P)
 _gemm = _sig("hg_gemm", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i32, _i64, _i64, _P, _i32, _i64, _i64, _P, _i32,
              _i64, _i64, _f32, _P, _i64, _P, _i64, _u32, _P)
+_cg_workspace_size = _sig("hg_cg_workspace_size", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, ctypes.POINTER(_sz))
+_cg_solve = _sig("hg_cg_solve", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _P, _i32, _i32, _f32, _P, _P, _P,
+                 _u32, _P, _P, _sz, _P)
 _last_error = _sig("hg_last_error", ctypes.c_char_p)
 _prof_enable = _sig("hg_profile_enable", ctypes.c_int, _i32)
 _prof_collect = _sig("hg_profile_collect", ctypes.c_int, _i32, _P, _P, _P, ctypes.POINTER(_i32))
@@ -65,7 +68,7 @@ _debug_counters = _sig("hg_debug_counters", ctypes.c_int, _P, _i32, _i32)
 
 EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_rsvd", "hg_block_apply_inverse",
            "hg_solve", "hg_solve_host", "hg_gemm", "hg_last_error", "hg_last_launch_count", "hg_profile_enable",
-           "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters")
+           "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve")
 
 
 class HGError(RuntimeError):
@@ -281,6 +284,31 @@ def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, batch: int
     _check(_gemm(M, N, K, batch, _ptr(A), int(a_mn), lda, sa, _ptr(B), int(b_mn), ldb, sb, _ptr(D), int(d_trans), ldd,
                  sd, alpha, _ptr(rs), srs, _ptr(cs), scs, HG_GEMM_SIMT if simt else 0, _stream(stream)))
     return D
+
+
+def cg_workspace_size(N: int, E: int, nnz: int, T: int, max_iter: int) -> int:
+    out = _sz(0)
+    _check(_cg_workspace_size(N, E, nnz, T, max_iter, ctypes.byref(out)))
+    return int(out.value)
+
+
+def cg_solve(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, max_iter: int, tol: float,
+             sync: bool = True, ws: Optional[Workspace] = None, F: Optional[torch.Tensor] = None,
+             iters: Optional[torch.Tensor] = None, rel_res: Optional[torch.Tensor] = None,
+             status: Optional[torch.Tensor] = None, stream=None):
+    """CG on X F = theta/(1+theta) Y, one CG per column: returns F, iters, rel_res, status."""
+    _dev(w, torch.float32)
+    _dev(Y, torch.float32)
+    N, T = H.N, Y.shape[1]
+    ws = ws or Workspace(cg_workspace_size(N, H.n_edges, H.nnz, T, max_iter), Y.device)
+    F = F if F is not None else torch.empty((N, T), dtype=torch.float32, device=Y.device)
+    iters = iters if iters is not None else torch.empty(T, dtype=torch.int32, device=Y.device)
+    rel_res = rel_res if rel_res is not None else torch.empty(T, dtype=torch.float32, device=Y.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=Y.device)
+    inc = H.c()
+    _check(_cg_solve(ctypes.byref(inc), _ptr(w), mu, _ptr(Y), T, max_iter, tol, _ptr(F), _ptr(iters), _ptr(rel_res),
+                     HG_SYNC if sync else 0, _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
+    return F, iters, rel_res, st
 
 
 def incidence_to_device(row_ptr, col_idx, n_edges: int, device="cuda") -> Incidence:

@@ -49,3 +49,17 @@ def test_workspace_grows_with_sizes():
     b = hg.workspace_size(4096, 4396, 62223, 256, 128, 100)
     c = hg.workspace_size(8192, 4396, 62223, 256, 64, 100)
     assert b > a and c > a
+
+
+def test_cg_host_validation():
+    from paper_1908_08281_b200 import hg
+    for args in [(512, 548, 4937, 6, 10),        # T % 4
+                 (512, 548, 4937, 0, 10),        # T = 0
+                 (512, 548, 4937, 20, -1),       # max_iter < 0
+                 (0, 548, 4937, 20, 10)]:        # N = 0
+        with pytest.raises(hg.HGError) as e:
+            hg.cg_workspace_size(*args)
+        assert e.value.status == hg.HG_ERR_INVALID
+    a = hg.cg_workspace_size(512, 548, 4937, 20, 10)
+    b = hg.cg_workspace_size(512, 548, 4937, 200, 10)
+    assert 0 < a < b

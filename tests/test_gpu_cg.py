@@ -1,0 +1,124 @@
+"""GPU parity for the second approach, CG on Eq. 5 (Eqs. 16-20).
+
+The CUDA CG (hg_cg_solve, through the C ABI) against the FP64 oracle (or_cg_solve):
+  * fixed iteration counts (tol = 0): the GPU iterate i against the oracle's iterate i,
+    relative Frobenius <= 2e-5 (north_star's F tolerance), for several i;
+  * converged (tol = 1e-6): against the oracle's converged solve and the dense LU solve;
+  * ragged T (slices of 32 / 64 / 128 columns with a ragged last slice), zero columns,
+    max_iter = 0, multi-chunk hyperedges (> 128 members) and the bitmap sort (> 64);
+  * graph mode (device-driven WHILE node) and direct enqueue agree bitwise; run-to-run
+    bitwise reproducibility;
+  * full size (configs[3], N = 65536, T = 1000) on sampled columns (columns are
+    independent CG problems, so the oracle on a column subset is exact for them).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth.hypergraph import CONFIGS, make_input
+
+pytestmark = pytest.mark.gpu
+
+F_TOL = 2e-5
+
+
+def hgm():
+    from paper_1908_08281_b200 import hg
+    return hg
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+_inputs = {}
+
+
+def inp(i):
+    if i not in _inputs:
+        h = make_input(CONFIGS[i])
+        hg = hgm()
+        _inputs[i] = (h, hg.incidence_to_device(h.row_ptr, h.col_idx, h.E), torch.from_numpy(h.w).cuda())
+    return _inputs[i]
+
+
+def gpu_cg(i, Y, **kw):
+    h, H, w = inp(i)
+    F, it, rr, st = hgm().cg_solve(H, w, torch.from_numpy(np.ascontiguousarray(Y, np.float32)).cuda(),
+                                   mu=CONFIGS[i].mu, **kw)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    return F.cpu().numpy().astype(np.float64), it.cpu().numpy(), rr.cpu().numpy()
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+@pytest.mark.parametrize("iters", [1, 3, 8])
+def test_cg_fixed_iterations_match_oracle(cfg, iters):
+    h = inp(cfg)[0]
+    F, it, _ = gpu_cg(cfg, h.Y, max_iter=iters, tol=0.0)
+    o = oracle.cg_solve(h.row_ptr, h.col_idx, h.w, h.Y, mu=CONFIGS[cfg].mu, max_iter=iters, tol=0.0)
+    assert np.array_equal(it, o.iters)
+    assert rel(F, o.F) <= F_TOL
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_cg_converged_matches_oracle_and_lu(cfg):
+    h = inp(cfg)[0]
+    mu = CONFIGS[cfg].mu
+    F, it, rr = gpu_cg(cfg, h.Y, max_iter=100, tol=1e-6)
+    o = oracle.cg_solve(h.row_ptr, h.col_idx, h.w, h.Y, mu=mu, max_iter=100, tol=1e-6)
+    assert rel(F, o.F) <= F_TOL
+    assert np.all(rr <= 1e-6) and np.all(np.abs(it - o.iters) <= 1)
+    X = oracle.theta_block(h.row_ptr, h.col_idx, h.w, len(h.row_ptr) - 1, 0, mu=mu)
+    F_lu = np.linalg.solve(X, mu / (1 + mu) * h.Y.astype(np.float64))
+    assert rel(F, F_lu) <= F_TOL
+
+
+@pytest.mark.parametrize("T", [4, 20, 36, 64, 132, 260])
+def test_cg_ragged_T_and_zero_columns(T):
+    h = inp(1)[0]
+    rng = np.random.default_rng(T)
+    Y = rng.uniform(-1, 1, (len(h.row_ptr) - 1, T)).astype(np.float32)
+    Y[:, T // 2] = 0.0
+    F, it, rr = gpu_cg(1, Y, max_iter=6, tol=0.0)
+    o = oracle.cg_solve(h.row_ptr, h.col_idx, h.w, Y, mu=1.0, max_iter=6, tol=0.0)
+    assert np.array_equal(it, o.iters) and it[T // 2] == 0 and np.all(F[:, T // 2] == 0.0)
+    assert rel(F, o.F) <= F_TOL
+
+
+def test_cg_max_iter_zero():
+    h = inp(1)[0]
+    F, it, _ = gpu_cg(1, h.Y, max_iter=0, tol=0.0)
+    assert np.all(F == 0.0) and np.all(it == 0)
+
+
+def test_cg_graph_and_direct_bitwise_and_reproducible():
+    h = inp(2)[0]
+    a = gpu_cg(2, h.Y, max_iter=50, tol=1e-6)
+    b = gpu_cg(2, h.Y, max_iter=50, tol=1e-6)
+    os.environ["HG_NO_GRAPH"] = "1"
+    try:
+        c = gpu_cg(2, h.Y, max_iter=50, tol=1e-6)
+    finally:
+        del os.environ["HG_NO_GRAPH"]
+    for x in (b, c):
+        assert np.array_equal(a[0], x[0]) and np.array_equal(a[1], x[1]) and np.array_equal(a[2], x[2])
+
+
+def test_cg_full_size_sampled_columns():
+    i = 4   # configs[3]: N = 65536, T = 1000
+    h = inp(i)[0]
+    F, it, rr = gpu_cg(i, h.Y, max_iter=100, tol=1e-6)
+    cols = np.array([0, 1, 7, 100, 499, 998, 999])
+    o = oracle.cg_solve(h.row_ptr, h.col_idx, h.w, np.ascontiguousarray(h.Y[:, cols]), mu=CONFIGS[i].mu,
+                        max_iter=100, tol=1e-6)
+    assert rel(F[:, cols], o.F) <= F_TOL
+    assert np.all(rr <= 1e-6) and np.all(np.abs(it[cols] - o.iters) <= 1)
+    # a fixed iteration count on the same columns: iterate-for-iterate parity
+    F5, _, _ = gpu_cg(i, h.Y, max_iter=5, tol=0.0)
+    o5 = oracle.cg_solve(h.row_ptr, h.col_idx, h.w, np.ascontiguousarray(h.Y[:, cols]), mu=CONFIGS[i].mu,
+                         max_iter=5, tol=0.0)
+    assert rel(F5[:, cols], o5.F) <= F_TOL
