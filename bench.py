@@ -358,6 +358,57 @@ def run_ours(args):
             finally:
                 oracle.set_num_threads(nthreads)
 
+    # the paper's second approach (CG on Eq. 5) on the
+    # same workload, timed the same way (CUDA events, resident inputs), parity on sampled columns
+    cg = None
+    if not args.no_cg:
+        cg_tol, cg_max = 1e-6, 100
+        cws = hg.Workspace(hg.cg_workspace_size(c.N, h.E, h.nnz, c.T, cg_max), device=dev)
+        Fc = torch.empty((c.N, c.T), dtype=torch.float32, device=dev)
+        itc = torch.empty(c.T, dtype=torch.int32, device=dev)
+        rrc = torch.empty(c.T, dtype=torch.float32, device=dev)
+
+        def cg_step():
+            hg.cg_solve(H, w, Y, mu=c.mu, max_iter=cg_max, tol=cg_tol, sync=False, ws=cws, F=Fc, iters=itc,
+                        rel_res=rrc, status=status, stream=stream)
+
+        for _ in range(3):
+            cg_step()
+        cg_launches = hg.last_launch_count()
+        torch.cuda.synchronize(dev)
+        n_cg = max(3, min(args.steps, 10))
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for _ in range(n_cg):
+            cg_step()
+        c1.record(stream)
+        torch.cuda.synchronize(dev)
+        cg_ms = max_over_ranks(c0.elapsed_time(c1) / n_cg, dev)
+        its = itc.cpu().numpy()
+        n_it = int(its.max())
+        ts = 128 if c.T > 64 else (64 if c.T > 32 else 32)
+        t_pad = (c.T + ts - 1) // ts * ts
+        gather = 2.0 * h.nnz * t_pad * 4 * n_it          # two sparse gathers of a T-row per incidence
+        cg = {"workload": "same H, w, Y; X F = theta/(1+theta) Y, one CG per column, tol %g" % cg_tol,
+              "solve_ms": cg_ms, "iterations_max": n_it, "iterations_mean": float(its.mean()),
+              "rel_res_max": float(rrc.max().item()), "launches_per_solve": cg_launches,
+              "gather_bytes_per_solve": gather, "gather_GBps": gather / (cg_ms / 1e3) / 1e9,
+              "note": "gathers are L2-resident (slice-major layout); see DESIGN.md §10"}
+        if rank == 0:
+            import oracle
+            cols = np.array([0, 1, c.T // 2, c.T - 1])
+            ro = oracle.cg_solve(h.row_ptr, h.col_idx, h.w, np.ascontiguousarray(h.Y[:, cols]), mu=c.mu,
+                                 max_iter=cg_max, tol=cg_tol)
+            Fcg = Fc[:, torch.from_numpy(cols).to(dev)].double().cpu().numpy()
+            cg["parity"] = {"columns": cols.tolist(), "F_rel_fro": float(np.linalg.norm(Fcg - ro.F) /
+                                                                        np.linalg.norm(ro.F)), "tol": 2e-5}
+            cg["parity"]["ok"] = cg["parity"]["F_rel_fro"] <= 2e-5
+            # accuracy of the block rSVD output against the full solve (SURVEY.md §8(d) accuracy axis)
+            Fr = Fh.double().numpy()
+            Ff = Fc.double().cpu().numpy()
+            cg["rsvd_F_vs_full_solve_rel_fro"] = float(np.linalg.norm(Fr - Ff) / np.linalg.norm(Ff))
+            cg["oracle_columns_s"] = ro.seconds
+
     out = {
         "metric": "diag_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -375,6 +426,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "parity": parity,
         "cpu_baseline": cpu_base,
+        "next_rows": {"cg": cg},
         "peaks": {"source": peak_src, "tf32_tflops_sustained": tf32_sust, "tf32_tflops_burst": tf32_burst,
                   "hbm_gbs": peaks["hbm_gbs"]},
     }
@@ -426,6 +478,7 @@ def main(argv=None):
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--q", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cg", action="store_true", help="skip the CG (NEXT-2) measurement")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

@@ -21,6 +21,7 @@ ap.add_argument("--tol", type=float, default=1e-6)
 ap.add_argument("--max-iter", type=int, default=100)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--direct", action="store_true")
+ap.add_argument("--warmup", type=int, default=3)
 a = ap.parse_args()
 if a.direct:
     os.environ["HG_NO_GRAPH"] = "1"
@@ -33,7 +34,7 @@ N, T = Y.shape
 ws = hg.Workspace(hg.cg_workspace_size(N, h.E, h.nnz, T, a.max_iter))
 F = torch.empty_like(Y)
 st = torch.zeros(1, dtype=torch.int32, device="cuda")
-for _ in range(3):
+for _ in range(a.warmup):
     hg.cg_solve(H, w, Y, mu=c.mu, max_iter=a.max_iter, tol=a.tol, ws=ws, F=F, status=st, sync=False)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
