@@ -247,11 +247,16 @@ struct Rsvd {
     if (st_ != HG_OK) return st_;    \
   } while (0)
 
+static int qr_passes_env() {   // read per call (tests switch it)
+  const char* v = getenv("HG_QR_PASSES");
+  return v ? atoi(v) : 1;
+}
+
 // CholeskyQR2 on a_t (result in a_t, scratch_t clobbered).  passes = 3 runs one more
 // pass (shifted CholeskyQR3): used for the first QR when 2k > b, where X Omega can be
 // ill-conditioned and k_cholinv's shifted retry leaves Q1 merely well-conditioned.
 hg_status cholqr(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* Linv, float* work, int32_t* st,
-                 int passes = 2) {
+                 int passes, float** q_out) {
   float* src = a_t;
   float* dst = scratch_t;
   for (int p = 0; p < passes; ++p) {
@@ -263,10 +268,7 @@ hg_status cholqr(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* L
     HG_TRY(R.qform(src, Linv, dst));
     float* tmp = src; src = dst; dst = tmp;
   }
-  if (src != a_t) {   // odd pass count: the result sits in scratch_t
-    HG_CU(cudaMemcpyAsync(a_t, src, sizeof(float) * (size_t)R.nb * R.k * R.b, cudaMemcpyDeviceToDevice, R.s),
-          "copy Q");
-  }
+  *q_out = src;   // a_t after an even pass count, scratch_t after an odd one
   return HG_OK;
 }
 
@@ -315,14 +317,24 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
     ProfScope ps(ST_OMEGA, s);
     HG_CU(launch_omega_panels(seed, blk0, nb, b, k, P[0], s, &g_launches), "omega");
   }
+  // Passes per QR: the final basis S (used by B = S^T X and U = S U~) gets
+  // CholeskyQR2; an intermediate basis is only multiplied by X next, so one CholeskyQR pass
+  // (span-exact, orthogonal to ~cond(Y)^2 u with cond(Y) <= 2 cond(X)) suffices.  The first
+  // QR of X Omega keeps three passes when 2k > b (X Omega ill-conditioned near k = b).
+  // HG_QR_PASSES=2 restores CholeskyQR2 for every QR.
+  const bool full_qr = qr_passes_env() >= 2;
+  auto passes = [&](bool first, bool last) { return (first && 2 * k > b) ? 3 : ((last || full_qr) ? 2 : 1); };
   HG_TRY(R.power(P[0], P[1]));
-  HG_TRY(cholqr(R, P[1], P[0], G, Linv, work, st, 2 * k > b ? 3 : 2));
-  float *cur = P[1], *oth = P[0];
+  float* cur = nullptr;
+  HG_TRY(cholqr(R, P[1], P[0], G, Linv, work, st, passes(true, q == 0), &cur));
+  float* oth = (cur == P[1]) ? P[0] : P[1];
   // loop i = 1..q: S~ = qr(X^T S), S = qr(X S~)
   for (int it = 0; it < 2 * q; ++it) {
     HG_TRY(R.power(cur, oth));
-    HG_TRY(cholqr(R, oth, cur, G, Linv, work, st));
-    float* t = cur; cur = oth; oth = t;
+    float* qn = nullptr;
+    HG_TRY(cholqr(R, oth, cur, G, Linv, work, st, passes(false, it == 2 * q - 1), &qn));
+    oth = (qn == oth) ? cur : oth;
+    cur = qn;
   }
   // step 4: B = S^T X, stored as B [k][b] = (X S)^T
   float* Bt = oth;
@@ -774,7 +786,8 @@ thread_local std::vector<GraphEntry> g_graphs;
 constexpr size_t kMaxGraphs = 8;
 std::string knob_env() {   // enqueue-time knobs that change the captured sequence
   std::string e;
-  for (const char* n : {"HG_ASSEMBLE", "HG_STREAMS_SERIAL", "HG_BN_POWER", "HG_BN_GRAM", "HG_BN_QFORM", "HG_GRAM_FULL"}) {
+  for (const char* n : {"HG_ASSEMBLE", "HG_STREAMS_SERIAL", "HG_BN_POWER", "HG_BN_GRAM", "HG_BN_QFORM", "HG_GRAM_FULL",
+                        "HG_QR_PASSES"}) {
     const char* v = getenv(n);
     e += v ? v : "-";
     e += '|';

@@ -347,3 +347,22 @@ def test_device_call_validation():
     with pytest.raises(hg.HGError) as e:
         hg.solve(H, w, Y, mu=1.0, b=8, k=12, q=1, seed=0)
     assert e.value.status == hg.HG_ERR_INVALID
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_qr_passes_knob_both_parity_green(inputs, cfg, monkeypatch):
+    """Intermediate bases take one CholeskyQR pass by default, the final S CholeskyQR2
+    (DESIGN.md "QR"); HG_QR_PASSES=2 runs CholeskyQR2 for every QR.  Both meet parity and
+    agree with each other to well inside the tolerance (same span, rounding differences)."""
+    hg = hgm()
+    h = inputs(cfg)
+    c = CONFIGS[cfg]
+    H, w, Y = dev_inputs(h)
+    F1, s1, st1 = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    monkeypatch.setenv("HG_QR_PASSES", "2")
+    F2, s2, st2 = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    monkeypatch.delenv("HG_QR_PASSES")
+    blocks = [0, c.nb - 1]
+    check_against_oracle(h, c, F1, s1, blocks)
+    check_against_oracle(h, c, F2, s2, blocks)
+    assert rel(F1.double().cpu().numpy(), F2.double().cpu().numpy()) <= 1e-5
