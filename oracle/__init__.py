@@ -62,6 +62,11 @@ def lib() -> ctypes.CDLL:
         L.or_solve.argtypes = [i32, i32, P, P, P, dbl, i32, i32, i32, u64, P, i32, i32, P,
                                P, P, P, P, P, P, cp, ci]
         L.or_solve.restype = ci
+        L.or_solve_mode.argtypes = [i32, i32, P, P, P, dbl, i32, i32, i32, u64, P, i32, i32, P,
+                                    P, P, P, P, P, P, i32, cp, ci]
+        L.or_solve_mode.restype = ci
+        L.or_apply_woodbury.argtypes = [i32, i32, i32, P, P, P, dbl, P]
+        L.or_apply_woodbury.restype = None
         L.or_apply_X.argtypes = [i32, i32, P, P, P, P, P, dbl, P, P, P]
         L.or_apply_X.restype = None
         L.or_cg_solve.argtypes = [i32, i32, P, P, P, dbl, P, i32, i32, dbl, P, P, P, cp, ci]
@@ -202,11 +207,24 @@ def num_threads() -> int:
     return int(lib().or_num_threads())
 
 
+def apply_woodbury(U, sigma, Y, mu: float) -> np.ndarray:
+    """Reading R2: F = c (Y + U diag(s/((1+mu) - s)) U^T Y), c = mu/(1+mu)."""
+    U = np.ascontiguousarray(U, np.float64)
+    s = np.ascontiguousarray(sigma, np.float64)
+    Y = np.ascontiguousarray(Y, np.float64)
+    m, k = U.shape
+    T = Y.shape[1]
+    F = np.zeros((m, T))
+    lib().or_apply_woodbury(m, k, T, _p(U), _p(s), _p(Y), mu, _p(F))
+    return F
+
+
 def solve(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, seed: int,
           blocks: Optional[Sequence[int]] = None, want_UV: bool = False,
-          want_X: bool = False) -> SolveResult:
+          want_X: bool = False, woodbury: bool = False) -> SolveResult:
     """The whole path (degrees -> X_ii -> Alg. 1 -> Eq. 3/15 apply) on `blocks`.
 
+    woodbury=True: reading R2 (Alg. 1 on Theta_ii, Woodbury apply).
     F rows for block i are F[s*b:(s+1)*b] where s is i's position in `blocks`.
     """
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
@@ -226,8 +244,9 @@ def solve(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, seed: in
     X = np.zeros((ns, b, b)) if want_X else None
     err = ctypes.create_string_buffer(256)
     t0 = time.perf_counter()
-    st = lib().or_solve(N, E, _p(row_ptr), _p(col_idx), _p(w), mu, b, k, q, seed, _p(Y), T, ns,
-                        _p(sel), _p(F), _p(sigma), _p(U), _p(V), _p(resid), _p(X), err, 256)
+    st = lib().or_solve_mode(N, E, _p(row_ptr), _p(col_idx), _p(w), mu, b, k, q, seed, _p(Y), T, ns,
+                             _p(sel), _p(F), _p(sigma), _p(U), _p(V), _p(resid), _p(X), 1 if woodbury else 0,
+                             err, 256)
     dt = time.perf_counter() - t0
     if st != OK:
         raise OracleError(st, err.value.decode())

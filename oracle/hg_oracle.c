@@ -19,7 +19,11 @@
  *   or_svd_gkr          PAPER.md:122     Alg. 1 step 5, SVD of B (Golub-Kahan-Reinsch)
  *   or_rsvd_block       PAPER.md:108-124 Alg. 1 (literal X^T in the loop), Eq. 7 residual
  *   or_apply_block      PAPER.md:43-45,160-163  Eq. 3 with Eq. 15: f = c V Sigma^-1 U^T y
- *   or_solve            the whole path over a chosen subset of diagonal blocks
+ *   or_apply_woodbury   SURVEY.md §8(f) NEXT-3 reading R2: X_ii^-1 ~ I + U diag(s/((1+theta)-s)) U^T from
+ *                       the rank-k rSVD U S V^T of Theta_ii (Woodbury identity on X = I - Theta/(1+theta),
+ *                       PAPER.md:40; Alg. 1 applied to the PSD low-rank part)
+ *   or_solve            the whole path over a chosen subset of diagonal blocks (mode 0: reading R1,
+ *                       Alg. 1 on X_ii + Eq. 15; mode 1: reading R2, Alg. 1 on Theta_ii + Woodbury)
  *   or_apply_X          PAPER.md:30-40   X p = p - (1/(1+theta)) Dv^-1/2 H W De^-1 H^T Dv^-1/2 p (matrix-free)
  *   or_cg_solve         PAPER.md:165-178 the paper's second approach: CG on Eq. 5, X f = theta/(1+theta) y
  *                                        (Eqs. 16-20), one independent CG per right-hand-side column
@@ -523,16 +527,49 @@ void or_apply_block(int32_t m, int32_t k, int32_t T, const double* U, const doub
   free(Z);
 }
 
+/* Reading R2 on one block: with Theta_ii ~ U diag(s) U^T (rank k),
+ *   X_ii = I - Theta_ii/(1+mu)  =>  X_ii^-1 ~ I + U diag(s_j / ((1+mu) - s_j)) U^T   (Woodbury)
+ * and F = c X_ii^-1 Y = c (Y + U diag(s_j/((1+mu) - s_j)) U^T Y), c = mu/(1+mu) (Eq. 3). */
+void or_apply_woodbury(int32_t m, int32_t k, int32_t T, const double* U, const double* sigma, const double* Y,
+                       double mu, double* F) {
+  double c = mu / (1.0 + mu);
+  double* Z = (double*)malloc(sizeof(double) * (size_t)k * (T > 0 ? T : 1));
+  mtm(k, m, T, U, Y, Z);                          /* U^T Y */
+  for (int j = 0; j < k; ++j) {
+    double d = sigma[j] / ((1.0 + mu) - sigma[j]);
+    for (int t = 0; t < T; ++t) Z[(int64_t)j * T + t] *= d;
+  }
+  mm(m, k, T, U, Z, F);                           /* U D U^T Y */
+  for (int64_t i = 0; i < (int64_t)m * T; ++i) F[i] = c * (Y[i] + F[i]);
+  free(Z);
+}
+
 /* ------------------------------------------------------------------------ */
 /* Whole path over a subset of diagonal blocks.                              */
 /* sel[n_sel] are block indices; outputs are packed in `sel` order:          */
 /*   F [n_sel*b][T], sigma [n_sel][k], U/V [n_sel][b][k] (optional),          */
 /*   resid [n_sel] (optional), X_out [n_sel][b][b] (optional, the X blocks).  */
 /* ------------------------------------------------------------------------ */
+int or_solve_mode(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
+                  double mu, int32_t b, int32_t k, int32_t q, uint64_t seed, const float* Y, int32_t T,
+                  int32_t n_sel, const int32_t* sel, double* F, double* sigma, double* U_out, double* V_out,
+                  double* resid, double* X_out, int32_t mode, char* err, int errlen);
+
 int or_solve(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
              double mu, int32_t b, int32_t k, int32_t q, uint64_t seed, const float* Y, int32_t T,
              int32_t n_sel, const int32_t* sel, double* F, double* sigma, double* U_out, double* V_out,
              double* resid, double* X_out, char* err, int errlen) {
+  return or_solve_mode(N, E, row_ptr, col_idx, w, mu, b, k, q, seed, Y, T, n_sel, sel, F, sigma, U_out, V_out,
+                       resid, X_out, 0, err, errlen);
+}
+
+/* mode 0: reading R1 (Alg. 1 on X_ii, Eq. 15 apply); mode 1: reading R2 (Alg. 1 on Theta_ii,
+ * Woodbury apply; X_out then holds the Theta_ii blocks the rSVD factored). */
+int or_solve_mode(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
+                  double mu, int32_t b, int32_t k, int32_t q, uint64_t seed, const float* Y, int32_t T,
+                  int32_t n_sel, const int32_t* sel, double* F, double* sigma, double* U_out, double* V_out,
+                  double* resid, double* X_out, int32_t mode, char* err, int errlen) {
+  if (mode != 0 && mode != 1) { set_err(err, errlen, "mode must be 0 (R1) or 1 (R2)"); return OR_ERR_INVALID; }
   if (N <= 0 || E <= 0 || b <= 0 || N % b != 0 || k < 1 || k > b || q < 0 || !(mu > 0.0) || T < 0) {
     set_err(err, errlen, "invalid arguments (need N % b == 0, 1 <= k <= b, q >= 0, mu > 0)");
     return OR_ERR_INVALID;
@@ -555,7 +592,7 @@ int or_solve(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_id
     double* U = (double*)malloc(sizeof(double) * bk);
     double* V = (double*)malloc(sizeof(double) * bk);
     double* Yi = (double*)malloc(sizeof(double) * (size_t)b * (T > 0 ? T : 1));
-    or_theta_block(b, blk, row_ptr, col_idx, w, dv, de, mu, X);
+    or_theta_block(b, blk, row_ptr, col_idx, w, dv, de, mode == 1 ? 0.0 : mu, X);
     or_gaussian_f32(seed, (int64_t)blk * b * k, (int64_t)bk, Omf);
     for (size_t i = 0; i < bk; ++i) Om[i] = (double)Omf[i];
     int r = or_rsvd_block(b, k, q, X, Om, U, sigma + (size_t)s * k, V, resid ? resid + s : NULL, NULL);
@@ -563,14 +600,15 @@ int or_solve(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_id
 #pragma omp atomic write
       fail = r;
     }
-    for (int j = 0; j < k; ++j)
+    for (int j = 0; j < k && mode == 0; ++j)
       if (!(sigma[(size_t)s * k + j] > 1e-12 * sigma[(size_t)s * k])) {
 #pragma omp atomic write
         fail = OR_ERR_NUMERICAL;
       }
     for (int i = 0; i < b; ++i)
       for (int t = 0; t < T; ++t) Yi[(int64_t)i * T + t] = (double)Y[((int64_t)blk * b + i) * T + t];
-    if (T > 0) or_apply_block(b, k, T, U, sigma + (size_t)s * k, V, Yi, c, F + (size_t)s * b * T);
+    if (T > 0 && mode == 0) or_apply_block(b, k, T, U, sigma + (size_t)s * k, V, Yi, c, F + (size_t)s * b * T);
+    if (T > 0 && mode == 1) or_apply_woodbury(b, k, T, U, sigma + (size_t)s * k, Yi, mu, F + (size_t)s * b * T);
     if (U_out) memcpy(U_out + (size_t)s * bk, U, sizeof(double) * bk);
     if (V_out) memcpy(V_out + (size_t)s * bk, V, sizeof(double) * bk);
     if (X_out) memcpy(X_out + (size_t)s * bb, X, sizeof(double) * bb);
