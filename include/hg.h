@@ -63,6 +63,8 @@ enum hg_status_flags {
 /* flags */
 #define HG_RAW_THETA (1u << 0)  /* hg_build_theta: write Theta_ii instead of X_ii          */
 #define HG_SYNC (1u << 1)       /* hg_solve: synchronise `stream`, map *d_status to status  */
+#define HG_WOODBURY (1u << 2)   /* hg_solve(_host): reading R2, see  */
+                                /* hg_block_apply_woodbury                                     */
 #define HG_GEMM_SIMT (1u << 8)  /* verification only: CUDA-core fp32 GEMMs, not tcgen05    */
 
 /* Hypergraph incidence H (H(v,e) = 1 iff v in e) in CSR over
@@ -124,8 +126,20 @@ hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const floa
                                  int32_t k, const float* Y, int32_t T, float scale, float* F,
                                  int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
 
+/* Reading R2 (the paper calls the X blocks "low-rank", PAPER.md:102,
+ * 138, yet X = I - Theta/(1+mu) is full-rank, its low-rank part being Theta): given the
+ * rank-k rSVD U Sigma V^T of Theta_ii (hg_build_theta with HG_RAW_THETA, then
+ * hg_block_rsvd), the Woodbury identity on X_ii = I - U Sigma U^T/(1+mu) gives
+ *   F_i = c (Y_i + U_i diag(sigma_j / ((1+mu) - sigma_j)) U_i^T Y_i),  c = mu/(1+mu)  (Eq. 3).
+ *   Ut [nb][k][b] (U_i^T), sigma [nb][k]; Y, F [nb*b][T];  mu > 0.
+ * Device errors: HG_ST_SINGULAR_SIGMA if some sigma_j >= 1+mu (impossible for Theta, pin P2). */
+hg_status hg_block_apply_woodbury(const float* Ut, const float* sigma, int32_t nb, int32_t b, int32_t k,
+                                  const float* Y, int32_t T, float mu, float* F, int32_t* d_status, void* ws,
+                                  size_t ws_bytes, hg_stream_t stream);
 /* The whole hot path: hg_build_theta -> hg_block_rsvd -> hg_block_apply_inverse
- * with scale = mu/(1+mu).  sigma_out [N/b][k] may be NULL.  Asynchronous
+ * with scale = mu/(1+mu); with flags HG_WOODBURY reading R2 instead: Theta_ii blocks ->
+ * hg_block_rsvd -> hg_block_apply_woodbury (sigma_out then holds Theta_ii's singular values).
+ * sigma_out [N/b][k] may be NULL.  Asynchronous
  * unless flags has HG_SYNC (then the stream is synchronised and a non-zero
  * *d_status returns HG_ERR_NUMERICAL).  d_status may be NULL only with HG_SYNC
  * (a word inside ws is used).

@@ -377,16 +377,24 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
   return HG_OK;
 }
 
+// Eq. 3 with Eq. 15 (reading R1): F_i = scale V_i Sigma_i^-1 U_i^T Y_i.
+// woodbury_opm = 1 + mu > 0 selects reading R2 (blocks are Theta_ii): F_i = scale (Y_i + U_i D U_i^T Y_i),
+// D = diag(sigma / ((1+mu) - sigma)) -- the Woodbury inverse of I - U Sigma U^T/(1+mu).
 hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb, int b, int k, const float* Y, int T,
-                    float scale, float* F, int32_t* st, const Bufs& Bf, cudaStream_t s, bool simt) {
+                    float scale, float* F, int32_t* st, const Bufs& Bf, cudaStream_t s, bool simt,
+                    float woodbury_opm = 0.f) {
   if (T == 0) return HG_OK;
+  const bool wb = woodbury_opm > 0.f;
   float* rs = Bf.rs;
   float* Z = Bf.Z;
   {
     ProfScope ps(ST_INV_SIGMA, s);
-    HG_CU(launch_inv_sigma(nb, k, sigma, scale, rs, st, s, &g_launches), "inv_sigma");
+    if (wb)
+      HG_CU(launch_woodbury_scale(nb, k, sigma, scale, woodbury_opm, rs, st, s, &g_launches), "woodbury scale");
+    else
+      HG_CU(launch_inv_sigma(nb, k, sigma, scale, rs, st, s, &g_launches), "inv_sigma");
   }
-  {  // Z = diag(scale/sigma) U^T Y_i   (k x T)
+  {  // Z = diag(rs) U^T Y_i   (k x T)
     GemmDesc g;
     g.M = k; g.N = T; g.K = b; g.batch = nb;
     g.A = Ut; g.a_mn = false; g.lda = b; g.sa = (int64_t)k * b;
@@ -395,13 +403,16 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
     g.rs = rs; g.srs = k;
     HG_TRY(gemm(g, s, simt, "Z = Sigma^-1 U^T Y", ST_GEMM_APPLY));
   }
-  {  // F_i = V Z   (b x T)
+  {  // R1: F_i = V Z;  R2: F_i = U Z + scale Y_i   (b x T)
     GemmDesc g;
     g.M = b; g.N = T; g.K = k; g.batch = nb;
-    g.A = Vt; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
+    g.A = wb ? Ut : Vt; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
     g.B = Z; g.b_mn = true; g.ldb = T; g.sb = (int64_t)k * T;
     g.D = F; g.d_trans = false; g.ldd = T; g.sd = (int64_t)b * T;
-    HG_TRY(gemm(g, s, simt, "F = V Z", ST_GEMM_APPLY));
+    if (wb) {
+      g.C = Y; g.ldc = T; g.sc = (int64_t)b * T; g.beta = scale;
+    }
+    HG_TRY(gemm(g, s, simt, wb ? "F = U Z + c Y" : "F = V Z", ST_GEMM_APPLY));
   }
   return HG_OK;
 }
@@ -607,6 +618,21 @@ hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const floa
                    reinterpret_cast<cudaStream_t>(stream), false);
 }
 
+hg_status hg_block_apply_woodbury(const float* Ut, const float* sigma, int32_t nb, int32_t b, int32_t k,
+                                  const float* Y, int32_t T, float mu, float* F, int32_t* d_status, void* ws,
+                                  size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (nb <= 0) return fail(HG_ERR_INVALID, "nb must be > 0");
+  HG_TRY(check_sizes((int64_t)nb * b, b, k, 0, T));
+  if (!Ut || !sigma || !d_status || (T > 0 && (!Y || !F))) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (!(mu > 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and > 0");
+  const Layout Lo = layout((int64_t)nb * b, 1, 0, b, k, T);
+  HG_TRY(check_ws(ws, ws_bytes, Lo.status));
+  return run_apply(Ut, sigma, nullptr, nb, b, k, Y, T, mu / (1.0f + mu), F, d_status,
+                   part_bufs(ws, Lo, nb, 0, b, k, T), reinterpret_cast<cudaStream_t>(stream), false, 1.0f + mu);
+}
+
 // Part count for hg_solve (HG_STREAMS, default 6, at most 8: with graph replay measured
 // 11.99 ms at configs[3] vs 12.11 / 12.29 / 12.56 / 12.05 with 4 / 3 / 2 / 8 parts) and the
 // auxiliary streams / events
@@ -697,6 +723,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, k, T);
   HG_TRY(check_ws(ws, ws_bytes, Lo.h_rowptr));
   const bool simt = (flags & HG_GEMM_SIMT) != 0;
+  const bool woodbury = (flags & HG_WOODBURY) != 0;
   int32_t* st = d_status;
   if (!st) {
     if (!(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
@@ -748,12 +775,13 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     const int64_t kb = (int64_t)blk0 * k * b;
     const Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, k, T);
     g_cur_part = p;
-    HG_TRY(run_assemble(H, mu, b, false, blk0, nbp, blocks, dvr, ws, Lo, ps[p]));
+    HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[p]));
     HG_TRY(run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, k, q, seed, simt, Ut + kb, sigma + (int64_t)blk0 * k,
                     Vt + kb, st, Bf, ps[p]));
     if (cps) HG_CU(cudaStreamWaitEvent(ps[p], ev_y[p], 0), "wait Y");
     HG_TRY(run_apply(Ut + kb, sigma + (int64_t)blk0 * k, Vt + kb, nbp, b, k, T > 0 ? Y + (int64_t)blk0 * b * T : Y, T,
-                     mu / (1.0f + mu), T > 0 ? F + (int64_t)blk0 * b * T : F, st, Bf, ps[p], simt));
+                     mu / (1.0f + mu), T > 0 ? F + (int64_t)blk0 * b * T : F, st, Bf, ps[p], simt,
+                     woodbury ? 1.0f + mu : 0.f));
     if (io.F_host && T > 0)
       HG_CU(cudaMemcpyAsync(io.F_host + (int64_t)blk0 * b * T, F + (int64_t)blk0 * b * T,
                             sizeof(float) * (size_t)nbp * b * T, cudaMemcpyDeviceToHost, ps[p]),

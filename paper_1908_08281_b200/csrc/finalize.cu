@@ -103,7 +103,31 @@ __global__ void k_inv_sigma(int nb, int k, const float* __restrict__ sigma, floa
   rs[i] = scale / s;
 }
 
+// Reading R2: rs[i][j] = c sigma_j / ((1+mu) - sigma_j), the Woodbury
+// weights of X_ii^-1 ~ I + U diag(sigma/((1+mu) - sigma)) U^T, times c = mu/(1+mu).
+__global__ void k_woodbury_scale(int nb, int k, const float* __restrict__ sigma, float c, float opm,
+                                 float* __restrict__ rs, int32_t* status) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nb * k) return;
+  const float s = sigma[i];
+  const float d = opm - s;
+  if (!isfinite(s) || !(d > 0.f)) {
+    hg_flag(status, isfinite(s) ? HGS_SINGULAR_SIGMA : HGS_NONFINITE);
+    rs[i] = 0.f;
+    return;
+  }
+  rs[i] = c * s / d;
+}
+
 }  // namespace
+
+cudaError_t launch_woodbury_scale(int nb, int k, const float* sigma, float c, float one_plus_mu, float* rs,
+                                  int32_t* status, cudaStream_t s, int* launches) {
+  const int64_t n = (int64_t)nb * k;
+  k_woodbury_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nb, k, sigma, c, one_plus_mu, rs, status);
+  ++*launches;
+  return cudaGetLastError();
+}
 
 // grid (nb, ceil(k/32)): a CTA normalises 32 columns of W_f and writes them as rows of Uk
 __global__ void __launch_bounds__(NT) k_unit_columns_t(int k, const float* __restrict__ Wf, float* __restrict__ Uk) {

@@ -46,6 +46,9 @@ struct EpiArgs {
   int a_mn, b_mn;
   int trunc_hi;   // 1: hi = the raw fp32 tile (tensor core truncates to tf32), lo = x - trunc(x)
   int lower;      // skip tiles entirely above the diagonal (GemmDesc::lower)
+  const float* C; // residual (row-major D only): D += beta * C
+  int64_t ldc, sc;
+  float beta;
 };
 
 constexpr int NEPI = 256;            // converter / epilogue threads (8 warps)
@@ -332,6 +335,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (n + 2 < ea.N) v.z *= csg[n + 2];
             if (n + 3 < ea.N) v.w *= csg[n + 3];
           }
+          if (ea.C) {
+            const float* crow = ea.C + (int64_t)g * ea.sc + (int64_t)(m0 + q * 32 + r) * ea.ldc;
+            if (vec && n + 3 < ea.N) {
+              const float4 cv = *reinterpret_cast<const float4*>(crow + n);
+              v.x = fmaf(ea.beta, cv.x, v.x); v.y = fmaf(ea.beta, cv.y, v.y);
+              v.z = fmaf(ea.beta, cv.z, v.z); v.w = fmaf(ea.beta, cv.w, v.w);
+            } else {
+              if (n < ea.N) v.x = fmaf(ea.beta, crow[n], v.x);
+              if (n + 1 < ea.N) v.y = fmaf(ea.beta, crow[n + 1], v.y);
+              if (n + 2 < ea.N) v.z = fmaf(ea.beta, crow[n + 2], v.z);
+              if (n + 3 < ea.N) v.w = fmaf(ea.beta, crow[n + 3], v.w);
+            }
+          }
           if (vec && n + 3 < ea.N) {
             *reinterpret_cast<float4*>(drow + n) = v;
           } else {
@@ -384,6 +400,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
         float v = acc[i][j] * ea.alpha;
         if (ea.rs) v *= ea.rs[(int64_t)g * ea.srs + m];
         if (ea.cs) v *= ea.cs[(int64_t)g * ea.scs + n];
+        if (ea.C) v = fmaf(ea.beta, ea.C[(int64_t)g * ea.sc + (int64_t)m * ea.ldc + n], v);
         if (ea.d_trans)
           Dg[(int64_t)n * ea.ldd + m] = v;
         else
@@ -455,6 +472,7 @@ const char* gemm_check(const GemmDesc& g) {
   if (g.batch > 1 && ((g.sa & 3) || (g.sb & 3))) return "gemm: batch strides must be multiples of 4";
   if (g.a_mn ? g.lda < g.M : g.lda < g.K) return "gemm: lda too small";
   if (g.b_mn ? g.ldb < g.N : g.ldb < g.K) return "gemm: ldb too small";
+  if (g.C && (g.d_trans || g.ldc < g.N)) return "gemm: residual C needs row-major D and ldc >= N";
   return nullptr;
 }
 
@@ -468,7 +486,7 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
     return (v && v[0] == 'r') ? 0 : 1;
   }();
   EpiArgs ea{g.M, g.N, g.K, g.D, g.ldd, g.sd, g.d_trans ? 1 : 0, g.alpha, g.rs, g.srs, g.cs, g.scs,
-             g.a_mn ? 1 : 0, g.b_mn ? 1 : 0, trunc_hi, g.lower ? 1 : 0};
+             g.a_mn ? 1 : 0, g.b_mn ? 1 : 0, trunc_hi, g.lower ? 1 : 0, g.C, g.ldc, g.sc, g.beta};
   if (simt) {
     dim3 grid((g.M + 63) / 64, (g.N + 63) / 64, g.batch);
     gemm_simt_kernel<<<grid, 256, 0, stream>>>(g.A, ea.a_mn, g.lda, g.sa, g.B, ea.b_mn, g.ldb, g.sb, ea);

@@ -3,7 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-// D_g(m,n) = alpha * rs_g[m] * cs_g[n] * sum_kk A_g(m,kk) B_g(kk,n),  g < batch
+// D_g(m,n) = alpha * rs_g[m] * cs_g[n] * sum_kk A_g(m,kk) B_g(kk,n) [+ beta * C_g(m,n)],  g < batch
 //   A_g(m,kk) = A[g*sa + (a_mn ? kk*lda + m : m*lda + kk)]   (a_mn: "M-major" storage)
 //   B_g(kk,n) = B[g*sb + (b_mn ? kk*ldb + n : n*ldb + kk)]
 //   d_trans ? D[g*sd + n*ldd + m] : D[g*sd + m*ldd + n]
@@ -26,6 +26,10 @@ struct GemmDesc {
   int bn_max = 256;   // widest N tile to use (smaller tiles = more CTAs for small outputs)
   bool lower = false; // symmetric result, consumer reads the lower triangle: skip output tiles
                       // entirely above the diagonal (n0 >= m0 + 128); those entries are left unset
+  // residual (row-major output only): D += beta * C_g, C_g(m,n) = C[g*sc + m*ldc + n]
+  const float* C = nullptr;
+  int64_t ldc = 0, sc = 0;
+  float beta = 0.f;
 };
 
 // Enqueue the GEMM; returns cudaSuccess or the launch error.  `simt` selects the

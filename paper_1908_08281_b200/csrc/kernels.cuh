@@ -37,6 +37,10 @@ cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float
 cudaError_t launch_inv_sigma(int nb, int k, const float* sigma, float scale, float* rs, int32_t* status,
                              cudaStream_t s, int* launches);
 
+// reading R2: rs[i][j] = c sigma_ij / ((1+mu) - sigma_ij)  (Woodbury weights)
+cudaError_t launch_woodbury_scale(int nb, int k, const float* sigma, float c, float one_plus_mu, float* rs,
+                                  int32_t* status, cudaStream_t s, int* launches);
+
 // debug counters (device globals): chol {near-identity, full}; jacobi {max sweeps, total sweeps, blocks}
 cudaError_t chol_debug(unsigned long long* out, bool reset);
 cudaError_t jacobi_debug(unsigned long long* out, bool reset);

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhgrsvd.so")
 
 HG_OK, HG_ERR_INVALID, HG_ERR_NUMERICAL, HG_ERR_CUDA = 0, 2, 3, 4
-HG_RAW_THETA, HG_SYNC, HG_GEMM_SIMT = 1 << 0, 1 << 1, 1 << 8
+HG_RAW_THETA, HG_SYNC, HG_WOODBURY, HG_GEMM_SIMT = 1 << 0, 1 << 1, 1 << 2, 1 << 8
 ST_FLAGS = {1: "isolated vertex", 2: "empty hyperedge", 4: "Cholesky breakdown", 8: "Jacobi sweep cap",
             16: "singular sigma", 32: "non-finite value", 64: "CG breakdown"}
 
@@ -50,6 +50,8 @@ _block_rsvd = _sig("hg_block_rsvd", ctypes.c_int, _P, _i32, _i32, _i32, _i32, _u
                    _P)
 _block_apply = _sig("hg_block_apply_inverse", ctypes.c_int, _P, _P, _P, _i32, _i32, _i32, _P, _i32, _f32, _P, _P, _P,
                     _sz, _P)
+_block_woodbury = _sig("hg_block_apply_woodbury", ctypes.c_int, _P, _P, _i32, _i32, _i32, _P, _i32, _f32, _P, _P,
+                       _P, _sz, _P)
 _solve = _sig("hg_solve", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _i32, _i32, _u64, _P, _i32, _P,
               _P, _u32, _P, _P, _sz, _P)
 _solve_host = _sig("hg_solve_host", ctypes.c_int, _i32, _i32, _i64, _P, _P, _P, _f32, _i32, _i32, _i32, _u64, _P,
@@ -68,7 +70,8 @@ _debug_counters = _sig("hg_debug_counters", ctypes.c_int, _P, _i32, _i32)
 
 EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_rsvd", "hg_block_apply_inverse",
            "hg_solve", "hg_solve_host", "hg_gemm", "hg_last_error", "hg_last_launch_count", "hg_profile_enable",
-           "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve")
+           "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve",
+           "hg_block_apply_woodbury")
 
 
 class HGError(RuntimeError):
@@ -241,8 +244,23 @@ def block_apply_inverse(Ut: torch.Tensor, sigma: torch.Tensor, Vt: torch.Tensor,
     return F, st
 
 
+def block_apply_woodbury(Ut: torch.Tensor, sigma: torch.Tensor, Y: torch.Tensor, mu: float, *,
+                         ws: Optional[Workspace] = None, status: Optional[torch.Tensor] = None, stream=None):
+    """Reading R2: F_i = c (Y_i + U_i diag(s/((1+mu)-s)) U_i^T Y_i) from the rSVD of Theta_ii."""
+    for t in (Ut, sigma, Y):
+        _dev(t, torch.float32)
+    nb, k, b = Ut.shape
+    T = Y.shape[1]
+    ws = ws or Workspace.for_sizes(nb * b, 1, 0, b, k, T)
+    F = torch.empty((nb * b, T), dtype=torch.float32, device=Y.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=Y.device)
+    _check(_block_woodbury(_ptr(Ut), _ptr(sigma), nb, b, k, _ptr(Y), T, mu, _ptr(F), _ptr(st), ws.ptr, ws.nbytes,
+                           _stream(stream)))
+    return F, st
+
+
 def solve(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, b: int, k: int, q: int, seed: int,
-          sync: bool = True, simt: bool = False, ws: Optional[Workspace] = None,
+          sync: bool = True, simt: bool = False, woodbury: bool = False, ws: Optional[Workspace] = None,
           F: Optional[torch.Tensor] = None, sigma: Optional[torch.Tensor] = None,
           status: Optional[torch.Tensor] = None, stream=None) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
     """The whole path from CSR H to F [N][T] (and sigma [N/b][k])."""
@@ -253,7 +271,7 @@ def solve(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, b: int, 
     F = F if F is not None else torch.empty((N, T), dtype=torch.float32, device=Y.device)
     sigma = sigma if sigma is not None else torch.empty((N // b, k), dtype=torch.float32, device=Y.device)
     st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=Y.device)
-    flags = (HG_SYNC if sync else 0) | (HG_GEMM_SIMT if simt else 0)
+    flags = (HG_SYNC if sync else 0) | (HG_GEMM_SIMT if simt else 0) | (HG_WOODBURY if woodbury else 0)
     inc = H.c()
     _check(_solve(ctypes.byref(inc), _ptr(w), mu, b, k, q, seed, _ptr(Y), T, _ptr(F), _ptr(sigma), flags, _ptr(st),
                   ws.ptr, ws.nbytes, _stream(stream)))
@@ -261,7 +279,7 @@ def solve(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, b: int, 
 
 
 def solve_host(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, seed: int, F=None, sigma=None,
-               ws: Optional[Workspace] = None, stream=None):
+               woodbury: bool = False, ws: Optional[Workspace] = None, stream=None):
     """End-to-end entry from HOST tensors (pinned for full copy bandwidth): returns F, sigma on the host."""
     N, T, E, nnz = row_ptr.numel() - 1, Y.shape[1], w.numel(), col_idx.numel()
     ws = ws or Workspace.for_sizes(N, E, nnz, b, k, T)
@@ -272,7 +290,7 @@ def solve_host(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, see
         if t.is_cuda or t.dtype != dt or not t.is_contiguous():
             raise ValueError("solve_host expects contiguous host tensors")
     _check(_solve_host(N, E, nnz, _ptr(row_ptr), _ptr(col_idx), _ptr(w), mu, b, k, q, seed, _ptr(Y), T, _ptr(F),
-                       _ptr(sigma), 0, ws.ptr, ws.nbytes, _stream(stream)))
+                       _ptr(sigma), HG_WOODBURY if woodbury else 0, ws.ptr, ws.nbytes, _stream(stream)))
     return F, sigma
 
 
