@@ -409,6 +409,56 @@ def run_ours(args):
             cg["rsvd_F_vs_full_solve_rel_fro"] = float(np.linalg.norm(Fr - Ff) / np.linalg.norm(Ff))
             cg["oracle_columns_s"] = ro.seconds
 
+    # SURVEY.md §8(f) NEXT-3, reading R2: Alg. 1 on Theta_ii + the Woodbury inverse of X_ii, same
+    # workload and timing; parity on sampled blocks; accuracy against the exact block solve and CG
+    r2 = None
+    if not args.no_r2:
+        F2 = torch.empty((c.N, c.T), dtype=torch.float32, device=dev)
+        s2 = torch.empty((c.nb, c.k), dtype=torch.float32, device=dev)
+
+        def r2_step():
+            hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, sync=False, woodbury=True, ws=ws, F=F2,
+                     sigma=s2, status=status, stream=stream)
+
+        for _ in range(3):
+            r2_step()
+        torch.cuda.synchronize(dev)
+        n_r2 = max(3, min(args.steps, 10))
+        r0_, r1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0_.record(stream)
+        for _ in range(n_r2):
+            r2_step()
+        r1_.record(stream)
+        torch.cuda.synchronize(dev)
+        r2_ms = max_over_ranks(r0_.elapsed_time(r1_) / n_r2, dev)
+        r2 = {"workload": "same H, w, Y, b, k, q; Alg. 1 on Theta_ii, F_i = c (Y_i + U diag(s/((1+mu)-s)) U^T Y_i)",
+              "solve_ms": r2_ms, "blocks_per_s": world * c.nb / (r2_ms / 1e3),
+              "status": int(status.item())}
+        if rank == 0:
+            import oracle
+            ro2 = oracle.solve(h.row_ptr, h.col_idx, h.w, h.Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed,
+                               blocks=[0, c.nb - 1], woodbury=True)
+            Fg2 = F2.double().cpu().numpy()
+            sg2 = s2.double().cpu().numpy()
+            fe, se, ex_r1, ex_r2 = 0.0, 0.0, 0.0, 0.0
+            Fr1 = Fh.double().numpy()
+            for s_, blk in enumerate(ro2.blocks):
+                rows = slice(blk * c.b, (blk + 1) * c.b)
+                fo = ro2.F[s_ * c.b:(s_ + 1) * c.b]
+                fe = max(fe, float(np.linalg.norm(Fg2[rows] - fo) / np.linalg.norm(fo)))
+                se = max(se, float(np.max(np.abs(sg2[blk] - ro2.sigma[s_]) / ro2.sigma[s_])))
+                Xo = oracle.theta_block(h.row_ptr, h.col_idx, h.w, c.b, blk, mu=c.mu)
+                ex = c.mu / (1 + c.mu) * np.linalg.solve(Xo, h.Y[rows].astype(np.float64))
+                ex_r2 = max(ex_r2, float(np.linalg.norm(Fg2[rows] - ex) / np.linalg.norm(ex)))
+                ex_r1 = max(ex_r1, float(np.linalg.norm(Fr1[rows] - ex) / np.linalg.norm(ex)))
+            r2["parity"] = {"blocks": ro2.blocks, "F_rel_fro": fe, "sigma_rel_max": se, "tol": {"F": 2e-5, "sigma": 1e-5},
+                            "ok": fe <= 2e-5 and se <= 1e-5}
+            r2["accuracy_vs_exact_block_solve"] = {"r2": ex_r2, "r1": ex_r1, "blocks": ro2.blocks}
+            if cg is not None:
+                Ff = Fc.double().cpu().numpy()
+                r2["accuracy_vs_full_solve"] = {"r2": float(np.linalg.norm(Fg2 - Ff) / np.linalg.norm(Ff)),
+                                                "r1": float(np.linalg.norm(Fr1 - Ff) / np.linalg.norm(Ff))}
+
     out = {
         "metric": "diag_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -426,7 +476,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "parity": parity,
         "cpu_baseline": cpu_base,
-        "next_rows": {"cg": cg},
+        "next_rows": {"cg": cg, "r2_woodbury": r2},
         "peaks": {"source": peak_src, "tf32_tflops_sustained": tf32_sust, "tf32_tflops_burst": tf32_burst,
                   "hbm_gbs": peaks["hbm_gbs"]},
     }
@@ -479,6 +529,7 @@ def main(argv=None):
     ap.add_argument("--q", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cg", action="store_true", help="skip the CG (NEXT-2) measurement")
+    ap.add_argument("--no-r2", action="store_true", help="skip the reading-R2 (NEXT-3) measurement")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
