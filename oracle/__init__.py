@@ -63,7 +63,9 @@ def lib() -> ctypes.CDLL:
                                P, P, P, P, P, P, cp, ci]
         L.or_solve.restype = ci
         L.or_solve_mode.argtypes = [i32, i32, P, P, P, dbl, i32, i32, i32, u64, P, i32, i32, P,
-                                    P, P, P, P, P, P, i32, cp, ci]
+                                    P, P, P, P, P, P, i32, i32, i32, cp, ci]
+        L.or_rsvd_block_ex.argtypes = [i32, i32, i32, i32, P, P, P, P, P, P, P]
+        L.or_rsvd_block_ex.restype = ci
         L.or_solve_mode.restype = ci
         L.or_apply_woodbury.argtypes = [i32, i32, i32, P, P, P, dbl, P]
         L.or_apply_woodbury.restype = None
@@ -164,15 +166,15 @@ def svd_wide(B: np.ndarray):
     return Ut, s, Vb
 
 
-def rsvd_block(X: np.ndarray, Omega: np.ndarray, q: int, want_S: bool = False):
-    """Alg. 1 on one block (l = k).  Returns U, sigma, V, resid[, S]."""
+def rsvd_block(X: np.ndarray, Omega: np.ndarray, q: int, want_S: bool = False, eq10: bool = False):
+    """Alg. 1 on one block (l = k; eq10: the Eq. 10 scheme).  Returns U, sigma, V, resid[, S]."""
     X = np.ascontiguousarray(X, np.float64)
     Om = np.ascontiguousarray(Omega, np.float64)
     m, k = Om.shape
     U, V, s = np.zeros((m, k)), np.zeros((m, k)), np.zeros(k)
     resid = np.zeros(1)
     S = np.zeros((m, k)) if want_S else None
-    st = lib().or_rsvd_block(m, k, q, _p(X), _p(Om), _p(U), _p(s), _p(V), _p(resid), _p(S))
+    st = lib().or_rsvd_block_ex(m, k, q, 1 if eq10 else 0, _p(X), _p(Om), _p(U), _p(s), _p(V), _p(resid), _p(S))
     if st != OK:
         raise OracleError(st, "SVD did not converge")
     if want_S:
@@ -221,10 +223,12 @@ def apply_woodbury(U, sigma, Y, mu: float) -> np.ndarray:
 
 def solve(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, seed: int,
           blocks: Optional[Sequence[int]] = None, want_UV: bool = False,
-          want_X: bool = False, woodbury: bool = False) -> SolveResult:
+          want_X: bool = False, woodbury: bool = False, p: int = 0, eq10: bool = False) -> SolveResult:
     """The whole path (degrees -> X_ii -> Alg. 1 -> Eq. 3/15 apply) on `blocks`.
 
     woodbury=True: reading R2 (Alg. 1 on Theta_ii, Woodbury apply).
+    p: oversampling, Alg. 1 at l = k + p columns then rank-k truncation.
+    eq10=True: the Eq. 10 power scheme instead of Alg. 1's per-step QR.
     F rows for block i are F[s*b:(s+1)*b] where s is i's position in `blocks`.
     """
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
@@ -246,7 +250,7 @@ def solve(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, seed: in
     t0 = time.perf_counter()
     st = lib().or_solve_mode(N, E, _p(row_ptr), _p(col_idx), _p(w), mu, b, k, q, seed, _p(Y), T, ns,
                              _p(sel), _p(F), _p(sigma), _p(U), _p(V), _p(resid), _p(X), 1 if woodbury else 0,
-                             err, 256)
+                             int(p), 1 if eq10 else 0, err, 256)
     dt = time.perf_counter() - t0
     if st != OK:
         raise OracleError(st, err.value.decode())

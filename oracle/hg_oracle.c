@@ -471,8 +471,19 @@ int or_svd_wide(int32_t k, int32_t m, const double* B, double* Ut, double* s, do
 /* Outputs U, V (m x k), sigma (k), and resid = ||X - S S^T X||_F (Eq. 7).     */
 /* Sign rule: the largest-|.| entry of each U column is >= 0 (V flips too).    */
 /* ------------------------------------------------------------------------ */
+int or_rsvd_block_ex(int32_t m, int32_t k, int32_t q, int32_t scheme, const double* X, const double* Omega,
+                     double* U, double* sigma, double* V, double* resid, double* S_out);
+
 int or_rsvd_block(int32_t m, int32_t k, int32_t q, const double* X, const double* Omega,
                   double* U, double* sigma, double* V, double* resid, double* S_out) {
+  return or_rsvd_block_ex(m, k, q, 0, X, Omega, U, sigma, V, resid, S_out);
+}
+
+/* scheme 0: Alg. 1 steps 2-3 (QR after every product).
+ * scheme 1: Eq. 10, Y = (X X^T)^pi X Omega formed first, then ONE QR
+ *           ("more sensitive to round-off errors").  Steps 4-6 are the same. */
+int or_rsvd_block_ex(int32_t m, int32_t k, int32_t q, int32_t scheme, const double* X, const double* Omega,
+                     double* U, double* sigma, double* V, double* resid, double* S_out) {
   size_t mk = (size_t)m * k, kk = (size_t)k * k, mm2 = (size_t)m * m;
   double* Y = (double*)malloc(sizeof(double) * mk);
   double* S = (double*)malloc(sizeof(double) * mk);
@@ -480,6 +491,15 @@ int or_rsvd_block(int32_t m, int32_t k, int32_t q, const double* X, const double
   double* R = (double*)malloc(sizeof(double) * kk);
   double* B = (double*)malloc(sizeof(double) * mk);
   double* Ut = (double*)malloc(sizeof(double) * kk);
+  if (scheme == 1) {
+    /* Eq. 10: Y = (X X^T)^pi X Omega, then S = qr(Y) */
+    mm(m, m, k, X, Omega, Y);
+    for (int it = 0; it < q; ++it) {
+      mtm(m, m, k, X, Y, St);                   /* X^T Y */
+      mm(m, m, k, X, St, Y);                    /* X X^T Y */
+    }
+    or_qr_householder(m, k, Y, S, R);
+  } else {
   /* step 2: Y0 = X Omega, Y0 = S0 R0 */
   mm(m, m, k, X, Omega, Y);
   or_qr_householder(m, k, Y, S, R);
@@ -489,6 +509,7 @@ int or_rsvd_block(int32_t m, int32_t k, int32_t q, const double* X, const double
     or_qr_householder(m, k, Y, St, R);
     mm(m, m, k, X, St, Y);
     or_qr_householder(m, k, Y, S, R);
+  }
   }
   /* step 4: B = S^T X (k x m) */
   mtm(k, m, m, S, X, B);
@@ -553,23 +574,30 @@ void or_apply_woodbury(int32_t m, int32_t k, int32_t T, const double* U, const d
 int or_solve_mode(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
                   double mu, int32_t b, int32_t k, int32_t q, uint64_t seed, const float* Y, int32_t T,
                   int32_t n_sel, const int32_t* sel, double* F, double* sigma, double* U_out, double* V_out,
-                  double* resid, double* X_out, int32_t mode, char* err, int errlen);
+                  double* resid, double* X_out, int32_t mode, int32_t p, int32_t scheme, char* err, int errlen);
 
 int or_solve(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
              double mu, int32_t b, int32_t k, int32_t q, uint64_t seed, const float* Y, int32_t T,
              int32_t n_sel, const int32_t* sel, double* F, double* sigma, double* U_out, double* V_out,
              double* resid, double* X_out, char* err, int errlen) {
   return or_solve_mode(N, E, row_ptr, col_idx, w, mu, b, k, q, seed, Y, T, n_sel, sel, F, sigma, U_out, V_out,
-                       resid, X_out, 0, err, errlen);
+                       resid, X_out, 0, 0, 0, err, errlen);
 }
 
 /* mode 0: reading R1 (Alg. 1 on X_ii, Eq. 15 apply); mode 1: reading R2 (Alg. 1 on Theta_ii,
- * Woodbury apply; X_out then holds the Theta_ii blocks the rSVD factored). */
+ * Woodbury apply; X_out then holds the Theta_ii blocks the rSVD factored).
+ * p: oversampling (l = k + pi): Alg. 1 runs with l = k + p columns (Omega is the
+ * global N x l Philox matrix), the rank-k truncation (top k singular triplets) is applied.
+ * scheme: 0 = Alg. 1, 1 = Eq. 10 (see or_rsvd_block_ex). */
 int or_solve_mode(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
                   double mu, int32_t b, int32_t k, int32_t q, uint64_t seed, const float* Y, int32_t T,
                   int32_t n_sel, const int32_t* sel, double* F, double* sigma, double* U_out, double* V_out,
-                  double* resid, double* X_out, int32_t mode, char* err, int errlen) {
+                  double* resid, double* X_out, int32_t mode, int32_t p, int32_t scheme, char* err, int errlen) {
   if (mode != 0 && mode != 1) { set_err(err, errlen, "mode must be 0 (R1) or 1 (R2)"); return OR_ERR_INVALID; }
+  if (p < 0 || k + p > b || (scheme != 0 && scheme != 1)) {
+    set_err(err, errlen, "need p >= 0, k + p <= b, scheme 0 or 1"); return OR_ERR_INVALID;
+  }
+  const int32_t l = k + p;
   if (N <= 0 || E <= 0 || b <= 0 || N % b != 0 || k < 1 || k > b || q < 0 || !(mu > 0.0) || T < 0) {
     set_err(err, errlen, "invalid arguments (need N % b == 0, 1 <= k <= b, q >= 0, mu > 0)");
     return OR_ERR_INVALID;
@@ -585,17 +613,24 @@ int or_solve_mode(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* c
 #pragma omp parallel for schedule(dynamic, 1)
   for (int s = 0; s < n_sel; ++s) {
     int blk = sel[s];
-    size_t bb = (size_t)b * b, bk = (size_t)b * k;
+    size_t bb = (size_t)b * b, bk = (size_t)b * k, bl = (size_t)b * l;
     double* X = (double*)malloc(sizeof(double) * bb);
-    double* Om = (double*)malloc(sizeof(double) * bk);
-    float* Omf = (float*)malloc(sizeof(float) * bk);
+    double* Om = (double*)malloc(sizeof(double) * bl);
+    float* Omf = (float*)malloc(sizeof(float) * bl);
+    double* Ul = (double*)malloc(sizeof(double) * bl);
+    double* Vl = (double*)malloc(sizeof(double) * bl);
+    double* sl = (double*)malloc(sizeof(double) * l);
     double* U = (double*)malloc(sizeof(double) * bk);
     double* V = (double*)malloc(sizeof(double) * bk);
     double* Yi = (double*)malloc(sizeof(double) * (size_t)b * (T > 0 ? T : 1));
     or_theta_block(b, blk, row_ptr, col_idx, w, dv, de, mode == 1 ? 0.0 : mu, X);
-    or_gaussian_f32(seed, (int64_t)blk * b * k, (int64_t)bk, Omf);
-    for (size_t i = 0; i < bk; ++i) Om[i] = (double)Omf[i];
-    int r = or_rsvd_block(b, k, q, X, Om, U, sigma + (size_t)s * k, V, resid ? resid + s : NULL, NULL);
+    or_gaussian_f32(seed, (int64_t)blk * b * l, (int64_t)bl, Omf);
+    for (size_t i = 0; i < bl; ++i) Om[i] = (double)Omf[i];
+    int r = or_rsvd_block_ex(b, l, q, scheme, X, Om, Ul, sl, Vl, resid ? resid + s : NULL, NULL);
+    /* rank-k truncation: the top k singular triplets (sigma is non-increasing) */
+    for (int i = 0; i < b; ++i)
+      for (int j = 0; j < k; ++j) { U[(int64_t)i * k + j] = Ul[(int64_t)i * l + j]; V[(int64_t)i * k + j] = Vl[(int64_t)i * l + j]; }
+    for (int j = 0; j < k; ++j) sigma[(size_t)s * k + j] = sl[j];
     if (r != OR_OK) {
 #pragma omp atomic write
       fail = r;
@@ -612,7 +647,7 @@ int or_solve_mode(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* c
     if (U_out) memcpy(U_out + (size_t)s * bk, U, sizeof(double) * bk);
     if (V_out) memcpy(V_out + (size_t)s * bk, V, sizeof(double) * bk);
     if (X_out) memcpy(X_out + (size_t)s * bb, X, sizeof(double) * bb);
-    free(X); free(Om); free(Omf); free(U); free(V); free(Yi);
+    free(X); free(Om); free(Omf); free(U); free(V); free(Yi); free(Ul); free(Vl); free(sl);
   }
   free(dv); free(de);
   if (fail) { set_err(err, errlen, "numerical failure (SVD non-convergence or singular sigma)"); return fail; }
