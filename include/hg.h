@@ -65,6 +65,8 @@ enum hg_status_flags {
 #define HG_SYNC (1u << 1)       /* hg_solve: synchronise `stream`, map *d_status to status  */
 #define HG_WOODBURY (1u << 2)   /* hg_solve(_host): reading R2, see  */
                                 /* hg_block_apply_woodbury                                     */
+#define HG_POWER_EQ10 (1u << 3) /* hg_block_rsvd(_ex) / hg_solve(_ex): the Eq. 10 scheme     */
+                                /* Y = (X X^T)^q X Omega, one QR at the end  */
 #define HG_GEMM_SIMT (1u << 8)  /* verification only: CUDA-core fp32 GEMMs, not tcgen05    */
 
 /* Hypergraph incidence H (H(v,e) = 1 iff v in e) in CSR over
@@ -118,6 +120,18 @@ hg_status hg_block_rsvd(const float* blocks, int32_t nb, int32_t b, int32_t k, i
                         uint32_t flags, float* Ut, float* sigma, float* Vt, int32_t* d_status, void* ws,
                         size_t ws_bytes, hg_stream_t stream);
 
+/* Alg. 1 with oversampling ("l = k + pi"): the
+ * factorisation runs at width l = k + p (Omega is the N x l Philox matrix) and the top k
+ * singular triplets are returned (rank-k truncation).  p >= 0, p % 4 == 0, l <= min(b, 512);
+ * p = 0 is hg_block_rsvd.  Workspace: hg_workspace_size_ex (= hg_workspace_size at k + p).
+ * flags: HG_POWER_EQ10 selects the Eq. 10 scheme (only for well-conditioned blocks such as
+ * X_ii, cond <= 2: for Theta_ii its (X X^T)^q X Omega exceeds fp32 range of accuracy, as the
+ * paper warns, "more sensitive to round-off errors"). */
+hg_status hg_block_rsvd_ex(const float* blocks, int32_t nb, int32_t b, int32_t k, int32_t p, int32_t q,
+                           uint64_t seed, uint32_t flags, float* Ut, float* sigma, float* Vt, int32_t* d_status,
+                           void* ws, size_t ws_bytes, hg_stream_t stream);
+hg_status hg_workspace_size_ex(int32_t N, int32_t E, int64_t nnz, int32_t b, int32_t k, int32_t p, int32_t T,
+                               size_t* bytes);
 /* Eq. 3 with Eq. 15 per block:
  *   F_i = scale * V_i diag(1/sigma_i) U_i^T Y_i,   Y_i = rows [ib,(i+1)b) of Y.
  *   Y, F [nb*b][T];  scale = mu/(1+mu) for Eq. 3.
@@ -155,6 +169,11 @@ hg_status hg_block_apply_woodbury(const float* Ut, const float* sigma, int32_t n
 hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
                    uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags,
                    int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
+/* hg_solve with oversampling p (see hg_block_rsvd_ex; the apply uses the top k triplets,
+ * sigma_out [N/b][k]); flags may add HG_POWER_EQ10 and HG_WOODBURY.  hg_solve = p = 0. */
+hg_status hg_solve_ex(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t p, int32_t q,
+                      uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags,
+                      int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
 
 /* hg_solve from HOST buffers (end-to-end entry): copies row_ptr, col_idx, w, Y
  * host->device, solves, copies F (and sigma_host if non-NULL) device->host,

@@ -114,7 +114,7 @@ constexpr size_t ALIGN = 256;
 
 struct Layout {
   size_t de = 0, eval = 0, dvr = 0, keys = 0, blocks = 0, P[4] = {0, 0, 0, 0}, Ut = 0, Vt = 0;
-  size_t G = 0, L = 0, Linv = 0, Wf = 0, Uk = 0, work = 0, sig = 0, sigma = 0, rs = 0, Z = 0, status = 0;
+  size_t G = 0, L = 0, Linv = 0, Wf = 0, Uk = 0, work = 0, sig = 0, sigma = 0, sigl = 0, rs = 0, Z = 0, status = 0;
   size_t h_rowptr = 0, h_col = 0, h_w = 0, h_Y = 0, h_F = 0;
   size_t total = 0;
 };
@@ -144,6 +144,7 @@ Layout layout(int64_t N, int64_t E, int64_t nnz, int64_t b, int64_t k, int64_t T
   L.work = take(4 * nb * k * k);
   L.sig = take(8 * nb * k + 4 * nb * k);
   L.sigma = take(4 * nb * k);
+  L.sigl = take(4 * nb * k);   // internal sigma of an oversampled (l = k + p) factorisation
   L.rs = take(4 * nb * k);
   L.Z = take(4 * nb * k * (T > 0 ? T : 1));
   L.status = take(4);
@@ -299,8 +300,10 @@ Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k,
 }
 
 // Alg. 1 on the nb blocks at X (global block index of the first: blk0, which keys Omega).
+// scheme 0: Alg. 1 (QR after every product); scheme 1: Eq. 10, Y = (X X^T)^q X Omega formed first
+// and orthonormalised once (shifted CholeskyQR3).
 hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64_t seed, bool simt, float* Ut,
-                   float* sigma, float* Vt, int32_t* st, const Bufs& Bf, cudaStream_t s) {
+                   float* sigma, float* Vt, int32_t* st, const Bufs& Bf, cudaStream_t s, int scheme = 0) {
   Rsvd R{nb, b, k, simt, s, X};
   float* P[4];
   for (int i = 0; i < 4; ++i) P[i] = Bf.P[i];
@@ -326,15 +329,29 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
   auto passes = [&](bool first, bool last) { return (first && 2 * k > b) ? 3 : ((last || full_qr) ? 2 : 1); };
   HG_TRY(R.power(P[0], P[1]));
   float* cur = nullptr;
-  HG_TRY(cholqr(R, P[1], P[0], G, Linv, work, st, passes(true, q == 0), &cur));
-  float* oth = (cur == P[1]) ? P[0] : P[1];
-  // loop i = 1..q: S~ = qr(X^T S), S = qr(X S~)
-  for (int it = 0; it < 2 * q; ++it) {
-    HG_TRY(R.power(cur, oth));
+  float* oth = nullptr;
+  if (scheme == 1) {
+    cur = P[1];
+    oth = P[0];
+    for (int it = 0; it < 2 * q; ++it) {   // (X X^T)^q X Omega, X^T = X (reading A12)
+      HG_TRY(R.power(cur, oth));
+      float* t = cur; cur = oth; oth = t;
+    }
     float* qn = nullptr;
-    HG_TRY(cholqr(R, oth, cur, G, Linv, work, st, passes(false, it == 2 * q - 1), &qn));
-    oth = (qn == oth) ? cur : oth;
+    HG_TRY(cholqr(R, cur, oth, G, Linv, work, st, 3, &qn));
+    oth = (qn == cur) ? oth : cur;
     cur = qn;
+  } else {
+    HG_TRY(cholqr(R, P[1], P[0], G, Linv, work, st, passes(true, q == 0), &cur));
+    oth = (cur == P[1]) ? P[0] : P[1];
+    // loop i = 1..q: S~ = qr(X^T S), S = qr(X S~)
+    for (int it = 0; it < 2 * q; ++it) {
+      HG_TRY(R.power(cur, oth));
+      float* qn = nullptr;
+      HG_TRY(cholqr(R, oth, cur, G, Linv, work, st, passes(false, it == 2 * q - 1), &qn));
+      oth = (qn == oth) ? cur : oth;
+      cur = qn;
+    }
   }
   // step 4: B = S^T X, stored as B [k][b] = (X S)^T
   float* Bt = oth;
@@ -380,33 +397,36 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
 // Eq. 3 with Eq. 15 (reading R1): F_i = scale V_i Sigma_i^-1 U_i^T Y_i.
 // woodbury_opm = 1 + mu > 0 selects reading R2 (blocks are Theta_ii): F_i = scale (Y_i + U_i D U_i^T Y_i),
 // D = diag(sigma / ((1+mu) - sigma)) -- the Woodbury inverse of I - U Sigma U^T/(1+mu).
+// Ut, Vt [nb][ldk][b] and sigma [nb][ldk] with ldk >= k: the first k triplets are used (ldk > k:
+// an oversampled factorisation truncated to rank k).
 hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb, int b, int k, const float* Y, int T,
                     float scale, float* F, int32_t* st, const Bufs& Bf, cudaStream_t s, bool simt,
-                    float woodbury_opm = 0.f) {
+                    float woodbury_opm = 0.f, int ldk = 0) {
   if (T == 0) return HG_OK;
+  if (ldk < k) ldk = k;
   const bool wb = woodbury_opm > 0.f;
   float* rs = Bf.rs;
   float* Z = Bf.Z;
   {
     ProfScope ps(ST_INV_SIGMA, s);
     if (wb)
-      HG_CU(launch_woodbury_scale(nb, k, sigma, scale, woodbury_opm, rs, st, s, &g_launches), "woodbury scale");
+      HG_CU(launch_woodbury_scale(nb, k, ldk, sigma, scale, woodbury_opm, rs, st, s, &g_launches), "woodbury scale");
     else
-      HG_CU(launch_inv_sigma(nb, k, sigma, scale, rs, st, s, &g_launches), "inv_sigma");
+      HG_CU(launch_inv_sigma(nb, k, ldk, sigma, scale, rs, st, s, &g_launches), "inv_sigma");
   }
   {  // Z = diag(rs) U^T Y_i   (k x T)
     GemmDesc g;
     g.M = k; g.N = T; g.K = b; g.batch = nb;
-    g.A = Ut; g.a_mn = false; g.lda = b; g.sa = (int64_t)k * b;
+    g.A = Ut; g.a_mn = false; g.lda = b; g.sa = (int64_t)ldk * b;
     g.B = Y; g.b_mn = true; g.ldb = T; g.sb = (int64_t)b * T;
     g.D = Z; g.d_trans = false; g.ldd = T; g.sd = (int64_t)k * T;
-    g.rs = rs; g.srs = k;
+    g.rs = rs; g.srs = ldk;
     HG_TRY(gemm(g, s, simt, "Z = Sigma^-1 U^T Y", ST_GEMM_APPLY));
   }
   {  // R1: F_i = V Z;  R2: F_i = U Z + scale Y_i   (b x T)
     GemmDesc g;
     g.M = b; g.N = T; g.K = k; g.batch = nb;
-    g.A = wb ? Ut : Vt; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
+    g.A = wb ? Ut : Vt; g.a_mn = true; g.lda = b; g.sa = (int64_t)ldk * b;
     g.B = Z; g.b_mn = true; g.ldb = T; g.sb = (int64_t)k * T;
     g.D = F; g.d_trans = false; g.ldd = T; g.sd = (int64_t)b * T;
     if (wb) {
@@ -566,6 +586,12 @@ hg_status hg_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t b, int32_
   return HG_OK;
 }
 
+hg_status hg_workspace_size_ex(int32_t N, int32_t E, int64_t nnz, int32_t b, int32_t k, int32_t p, int32_t T,
+                               size_t* bytes) {
+  if (p < 0 || p % 4) return fail(HG_ERR_INVALID, "oversampling p must be >= 0 and a multiple of 4 (p=%d)", p);
+  return hg_workspace_size(N, E, nnz, b, k + p, T, bytes);
+}
+
 hg_status hg_build_theta(const hg_incidence* H, const float* w, float mu, int32_t b, uint32_t flags, float* blocks,
                          float* dv_rsqrt, int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream) {
   g_err.clear();
@@ -589,18 +615,43 @@ hg_status hg_fill_gaussian(uint64_t seed, int32_t rows, int32_t cols, float* out
   return HG_OK;
 }
 
-hg_status hg_block_rsvd(const float* blocks, int32_t nb, int32_t b, int32_t k, int32_t q, uint64_t seed,
-                        uint32_t flags, float* Ut, float* sigma, float* Vt, int32_t* d_status, void* ws,
-                        size_t ws_bytes, hg_stream_t stream) {
+hg_status hg_block_rsvd_ex(const float* blocks, int32_t nb, int32_t b, int32_t k, int32_t p, int32_t q,
+                           uint64_t seed, uint32_t flags, float* Ut, float* sigma, float* Vt, int32_t* d_status,
+                           void* ws, size_t ws_bytes, hg_stream_t stream) {
   g_err.clear();
   g_launches = 0;
   if (nb <= 0) return fail(HG_ERR_INVALID, "nb must be > 0");
-  HG_TRY(check_sizes((int64_t)nb * b, b, k, q, 0));
+  if (p < 0 || p % 4) return fail(HG_ERR_INVALID, "oversampling p must be >= 0 and a multiple of 4 (p=%d)", p);
+  const int l = k + p;
+  HG_TRY(check_sizes((int64_t)nb * b, b, l, q, 0));
   if (!blocks || !Ut || !sigma || !Vt || !d_status) return fail(HG_ERR_INVALID, "NULL pointer argument");
-  const Layout Lo = layout((int64_t)nb * b, 1, 0, b, k, 0);
+  const Layout Lo = layout((int64_t)nb * b, 1, 0, b, l, 0);
   HG_TRY(check_ws(ws, ws_bytes, Lo.status));
-  return run_rsvd(blocks, nb, 0, b, k, q, seed, (flags & HG_GEMM_SIMT) != 0, Ut, sigma, Vt, d_status,
-                  part_bufs(ws, Lo, nb, 0, b, k, 0), reinterpret_cast<cudaStream_t>(stream));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int scheme = (flags & HG_POWER_EQ10) ? 1 : 0;
+  const bool simt = (flags & HG_GEMM_SIMT) != 0;
+  if (p == 0)
+    return run_rsvd(blocks, nb, 0, b, k, q, seed, simt, Ut, sigma, Vt, d_status, part_bufs(ws, Lo, nb, 0, b, k, 0), s,
+                    scheme);
+  // oversampled: factor at width l into the workspace, keep the top k triplets (rank-k truncation)
+  float* Ul = at<float>(ws, Lo.Ut);
+  float* Vl = at<float>(ws, Lo.Vt);
+  float* sl = at<float>(ws, Lo.sigl);
+  HG_TRY(run_rsvd(blocks, nb, 0, b, l, q, seed, simt, Ul, sl, Vl, d_status, part_bufs(ws, Lo, nb, 0, b, l, 0), s,
+                  scheme));
+  HG_CU(cudaMemcpy2DAsync(Ut, 4 * (size_t)k * b, Ul, 4 * (size_t)l * b, 4 * (size_t)k * b, nb, cudaMemcpyDeviceToDevice,
+                          s), "truncate U");
+  HG_CU(cudaMemcpy2DAsync(Vt, 4 * (size_t)k * b, Vl, 4 * (size_t)l * b, 4 * (size_t)k * b, nb, cudaMemcpyDeviceToDevice,
+                          s), "truncate V");
+  HG_CU(cudaMemcpy2DAsync(sigma, 4 * (size_t)k, sl, 4 * (size_t)l, 4 * (size_t)k, nb, cudaMemcpyDeviceToDevice, s),
+        "truncate sigma");
+  return HG_OK;
+}
+
+hg_status hg_block_rsvd(const float* blocks, int32_t nb, int32_t b, int32_t k, int32_t q, uint64_t seed,
+                        uint32_t flags, float* Ut, float* sigma, float* Vt, int32_t* d_status, void* ws,
+                        size_t ws_bytes, hg_stream_t stream) {
+  return hg_block_rsvd_ex(blocks, nb, b, k, 0, q, seed, flags, Ut, sigma, Vt, d_status, ws, ws_bytes, stream);
 }
 
 hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const float* Vt, int32_t nb, int32_t b,
@@ -712,18 +763,21 @@ static cudaStream_t copy_stream(hg_status* err) {
   return cs;
 }
 
-static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
-                            uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags,
-                            int32_t* d_status, void* ws, size_t ws_bytes, cudaStream_t s,
+static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t p,
+                            int32_t q, uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out,
+                            uint32_t flags, int32_t* d_status, void* ws, size_t ws_bytes, cudaStream_t s,
                             const HostIO& io = HostIO()) {
   HG_TRY(check_H(H));
-  HG_TRY(check_sizes(H->n_vertices, b, k, q, T));
+  if (p < 0 || p % 4) return fail(HG_ERR_INVALID, "oversampling p must be >= 0 and a multiple of 4 (p=%d)", p);
+  const int32_t l = k + p;   // Alg. 1 width; the apply uses the top k triplets
+  HG_TRY(check_sizes(H->n_vertices, b, l, q, T));
   if (!(mu > 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and > 0");
   if (!w || (T > 0 && (!Y || !F))) return fail(HG_ERR_INVALID, "NULL pointer argument");
-  const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, k, T);
+  const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, l, T);
   HG_TRY(check_ws(ws, ws_bytes, Lo.h_rowptr));
   const bool simt = (flags & HG_GEMM_SIMT) != 0;
   const bool woodbury = (flags & HG_WOODBURY) != 0;
+  const int scheme = (flags & HG_POWER_EQ10) ? 1 : 0;
   int32_t* st = d_status;
   if (!st) {
     if (!(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
@@ -734,7 +788,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   float* blocks = at<float>(ws, Lo.blocks);
   float* Ut = at<float>(ws, Lo.Ut);
   float* Vt = at<float>(ws, Lo.Vt);
-  float* sigma = sigma_out ? sigma_out : at<float>(ws, Lo.sigma);
+  float* sigma = (sigma_out && p == 0) ? sigma_out : at<float>(ws, p == 0 ? Lo.sigma : Lo.sigl);   // [nb][l]
   float* dvr = at<float>(ws, Lo.dvr);
   HG_TRY(run_degrees(H, w, dvr, st, ws, Lo, s));
   // Blocks are independent (reading A5): the assembly, rSVD and apply of disjoint block ranges run
@@ -761,34 +815,37 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     if (!ev_cps) HG_CU(cudaEventCreateWithFlags(&ev_cps, cudaEventDisableTiming), "event create");
     HG_CU(cudaEventRecord(ev_cps, s), "copy fork record");
     HG_CU(cudaStreamWaitEvent(cps, ev_cps, 0), "copy fork wait");
-    for (int p = 0; p < nparts; ++p) {
-      const int64_t r0 = (int64_t)nb * p / nparts * b, r1 = (int64_t)nb * (p + 1) / nparts * b;
-      if (!ev_y[p]) HG_CU(cudaEventCreateWithFlags(&ev_y[p], cudaEventDisableTiming), "event create");
+    for (int pt = 0; pt < nparts; ++pt) {
+      const int64_t r0 = (int64_t)nb * pt / nparts * b, r1 = (int64_t)nb * (pt + 1) / nparts * b;
+      if (!ev_y[pt]) HG_CU(cudaEventCreateWithFlags(&ev_y[pt], cudaEventDisableTiming), "event create");
       HG_CU(cudaMemcpyAsync(const_cast<float*>(Y) + r0 * T, io.Y_host + r0 * T, sizeof(float) * (size_t)(r1 - r0) * T,
                             cudaMemcpyHostToDevice, cps),
             "H2D Y");
-      HG_CU(cudaEventRecord(ev_y[p], cps), "Y event");
+      HG_CU(cudaEventRecord(ev_y[pt], cps), "Y event");
     }
   }
-  for (int p = 0; p < nparts; ++p) {
-    const int blk0 = (int)((int64_t)nb * p / nparts), nbp = (int)((int64_t)nb * (p + 1) / nparts) - blk0;
-    const int64_t kb = (int64_t)blk0 * k * b;
-    const Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, k, T);
-    g_cur_part = p;
-    HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[p]));
-    HG_TRY(run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, k, q, seed, simt, Ut + kb, sigma + (int64_t)blk0 * k,
-                    Vt + kb, st, Bf, ps[p]));
-    if (cps) HG_CU(cudaStreamWaitEvent(ps[p], ev_y[p], 0), "wait Y");
-    HG_TRY(run_apply(Ut + kb, sigma + (int64_t)blk0 * k, Vt + kb, nbp, b, k, T > 0 ? Y + (int64_t)blk0 * b * T : Y, T,
-                     mu / (1.0f + mu), T > 0 ? F + (int64_t)blk0 * b * T : F, st, Bf, ps[p], simt,
-                     woodbury ? 1.0f + mu : 0.f));
+  for (int pt = 0; pt < nparts; ++pt) {
+    const int blk0 = (int)((int64_t)nb * pt / nparts), nbp = (int)((int64_t)nb * (pt + 1) / nparts) - blk0;
+    const int64_t kb = (int64_t)blk0 * l * b;
+    const Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, l, T);
+    g_cur_part = pt;
+    HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[pt]));
+    HG_TRY(run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, l, q, seed, simt, Ut + kb, sigma + (int64_t)blk0 * l,
+                    Vt + kb, st, Bf, ps[pt], scheme));
+    if (cps) HG_CU(cudaStreamWaitEvent(ps[pt], ev_y[pt], 0), "wait Y");
+    HG_TRY(run_apply(Ut + kb, sigma + (int64_t)blk0 * l, Vt + kb, nbp, b, k, T > 0 ? Y + (int64_t)blk0 * b * T : Y, T,
+                     mu / (1.0f + mu), T > 0 ? F + (int64_t)blk0 * b * T : F, st, Bf, ps[pt], simt,
+                     woodbury ? 1.0f + mu : 0.f, l));
     if (io.F_host && T > 0)
       HG_CU(cudaMemcpyAsync(io.F_host + (int64_t)blk0 * b * T, F + (int64_t)blk0 * b * T,
-                            sizeof(float) * (size_t)nbp * b * T, cudaMemcpyDeviceToHost, ps[p]),
+                            sizeof(float) * (size_t)nbp * b * T, cudaMemcpyDeviceToHost, ps[pt]),
             "D2H F");
   }
   g_cur_part = 0;
   HG_TRY(join_streams(s, nparts, ps));
+  if (p > 0 && sigma_out)   // rank-k truncation of the oversampled sigma [nb][l] -> [nb][k]
+    HG_CU(cudaMemcpy2DAsync(sigma_out, 4 * (size_t)k, sigma, 4 * (size_t)l, 4 * (size_t)k, nb, cudaMemcpyDeviceToDevice,
+                            s), "truncate sigma");
   if (flags & HG_SYNC) {
     int32_t h = 0;
     HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
@@ -877,29 +934,30 @@ hg_status graph_run(const std::string& key, cudaStream_t s, Fn enqueue) {
 }  // namespace
 }  // extern "C++"
 
-hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q, uint64_t seed,
-                   const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags, int32_t* d_status, void* ws,
-                   size_t ws_bytes, hg_stream_t stream) {
+hg_status hg_solve_ex(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t p, int32_t q,
+                      uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags,
+                      int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream) {
   g_err.clear();
   g_launches = 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (!graphs_enabled(s))
-    return solve_impl(H, w, mu, b, k, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes, s);
+    return solve_impl(H, w, mu, b, k, p, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes, s);
   // host-side validation first (nothing is captured for an invalid call)
   HG_TRY(check_H(H));
-  HG_TRY(check_sizes(H->n_vertices, b, k, q, T));
-  const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, k, T);
+  if (p < 0 || p % 4) return fail(HG_ERR_INVALID, "oversampling p must be >= 0 and a multiple of 4 (p=%d)", p);
+  HG_TRY(check_sizes(H->n_vertices, b, k + p, q, T));
+  const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, k + p, T);
   HG_TRY(check_ws(ws, ws_bytes, Lo.h_rowptr));
   if (!d_status && !(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
   int32_t* st = d_status ? d_status : at<int32_t>(ws, Lo.status);
   std::string key = "solve|" + knob_env();
   key_add(key, *H);
-  key_add(key, w); key_add(key, mu); key_add(key, b); key_add(key, k); key_add(key, q); key_add(key, seed);
+  key_add(key, w); key_add(key, mu); key_add(key, b); key_add(key, k); key_add(key, p); key_add(key, q); key_add(key, seed);
   key_add(key, Y); key_add(key, T); key_add(key, F); key_add(key, sigma_out); key_add(key, flags & ~HG_SYNC);
   key_add(key, st); key_add(key, ws); key_add(key, ws_bytes); key_add(key, solve_parts());
   HG_TRY(graph_run(key, s, [&](cudaStream_t cs) -> hg_status {
     if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), cs), "memset status");
-    return solve_impl(H, w, mu, b, k, q, seed, Y, T, F, sigma_out, flags & ~HG_SYNC, st, ws, ws_bytes, cs);
+    return solve_impl(H, w, mu, b, k, p, q, seed, Y, T, F, sigma_out, flags & ~HG_SYNC, st, ws, ws_bytes, cs);
   }));
   if (flags & HG_SYNC) {
     int32_t h = 0;
@@ -909,6 +967,12 @@ hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, i
                        "Cholesky breakdown, 8 Jacobi cap, 16 singular sigma, 32 non-finite)", h);
   }
   return HG_OK;
+}
+
+hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q, uint64_t seed,
+                   const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags, int32_t* d_status, void* ws,
+                   size_t ws_bytes, hg_stream_t stream) {
+  return hg_solve_ex(H, w, mu, b, k, 0, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes, stream);
 }
 
 hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_ptr_host, const int32_t* col_idx_host,
@@ -941,7 +1005,7 @@ hg_status hg_solve_host(int32_t N, int32_t E, int64_t nnz, const int64_t* row_pt
   HostIO io;
   io.Y_host = Y_host;
   io.F_host = F_host;
-  HG_TRY(solve_impl(&H, d_w, mu, b, k, q, seed, d_Y, T, d_F, d_sig, flags & ~HG_SYNC, st, ws, ws_bytes, s, io));
+  HG_TRY(solve_impl(&H, d_w, mu, b, k, 0, q, seed, d_Y, T, d_F, d_sig, flags & ~HG_SYNC, st, ws, ws_bytes, s, io));
   if (sigma_host)
     HG_CU(cudaMemcpyAsync(sigma_host, d_sig, 4 * (size_t)nb * k, cudaMemcpyDeviceToHost, s), "D2H sigma");
   return HG_OK;

@@ -89,12 +89,17 @@ __global__ void __launch_bounds__(NT) k_rows(int b, int k, const float* __restri
   }
 }
 
-__global__ void k_inv_sigma(int nb, int k, const float* __restrict__ sigma, float scale, float* __restrict__ rs,
-                            int32_t* status) {
+// sigma, rs: [nb][ld], the first k of each row used (ld > k: oversampled, truncated to rank k)
+__global__ void k_inv_sigma(int nb, int k, int ld, const float* __restrict__ sigma, float scale,
+                            float* __restrict__ rs, int32_t* status) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)nb * k) return;
-  const int64_t blk = i / k;
-  const float s = sigma[i], s1 = sigma[blk * k];
+  if (i >= (int64_t)nb * ld) return;
+  const int64_t blk = i / ld;
+  if (i % ld >= k) {
+    rs[i] = 0.f;
+    return;
+  }
+  const float s = sigma[i], s1 = sigma[blk * ld];
   if (!isfinite(s) || !(s > 1e-6f * s1)) {
     hg_flag(status, isfinite(s) ? HGS_SINGULAR_SIGMA : HGS_NONFINITE);
     rs[i] = 0.f;
@@ -105,10 +110,14 @@ __global__ void k_inv_sigma(int nb, int k, const float* __restrict__ sigma, floa
 
 // Reading R2: rs[i][j] = c sigma_j / ((1+mu) - sigma_j), the Woodbury
 // weights of X_ii^-1 ~ I + U diag(sigma/((1+mu) - sigma)) U^T, times c = mu/(1+mu).
-__global__ void k_woodbury_scale(int nb, int k, const float* __restrict__ sigma, float c, float opm,
+__global__ void k_woodbury_scale(int nb, int k, int ld, const float* __restrict__ sigma, float c, float opm,
                                  float* __restrict__ rs, int32_t* status) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)nb * k) return;
+  if (i >= (int64_t)nb * ld) return;
+  if (i % ld >= k) {
+    rs[i] = 0.f;
+    return;
+  }
   const float s = sigma[i];
   const float d = opm - s;
   if (!isfinite(s) || !(d > 0.f)) {
@@ -121,10 +130,10 @@ __global__ void k_woodbury_scale(int nb, int k, const float* __restrict__ sigma,
 
 }  // namespace
 
-cudaError_t launch_woodbury_scale(int nb, int k, const float* sigma, float c, float one_plus_mu, float* rs,
+cudaError_t launch_woodbury_scale(int nb, int k, int ld, const float* sigma, float c, float one_plus_mu, float* rs,
                                   int32_t* status, cudaStream_t s, int* launches) {
-  const int64_t n = (int64_t)nb * k;
-  k_woodbury_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nb, k, sigma, c, one_plus_mu, rs, status);
+  const int64_t n = (int64_t)nb * ld;
+  k_woodbury_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nb, k, ld, sigma, c, one_plus_mu, rs, status);
   ++*launches;
   return cudaGetLastError();
 }
@@ -172,10 +181,10 @@ cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float
   return cudaGetLastError();
 }
 
-cudaError_t launch_inv_sigma(int nb, int k, const float* sigma, float scale, float* rs, int32_t* status,
+cudaError_t launch_inv_sigma(int nb, int k, int ld, const float* sigma, float scale, float* rs, int32_t* status,
                              cudaStream_t s, int* launches) {
-  const int64_t n = (int64_t)nb * k;
-  k_inv_sigma<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nb, k, sigma, scale, rs, status);
+  const int64_t n = (int64_t)nb * ld;
+  k_inv_sigma<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nb, k, ld, sigma, scale, rs, status);
   ++*launches;
   return cudaGetLastError();
 }

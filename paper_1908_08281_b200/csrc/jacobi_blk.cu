@@ -245,7 +245,7 @@ struct Cross4Scratch {
 
 template <int BW>
 __device__ int inner_sweep_cross4(const GramSrc<BW>& G, float* Q, double tol2, const Cross4Scratch& S, int lane, int h,
-                                  int aw, int bar_id) {
+                                  int aw, int bar_id, int npass) {
   constexpr int PW = 2 * BW, LDQ = JB<BW>::LDQ, QW = BW / 4;
   const int j0 = h * QW;
   const bool act = lane < PW;
@@ -278,7 +278,7 @@ __device__ int inner_sweep_cross4(const GramSrc<BW>& G, float* Q, double tol2, c
       if (stamp && r < 4) g_jb_iclk[12 * r + 3 * i + (h == aw ? 0 : (h == ((aw + 1) & 3) ? 1 : 2))] = clock64();
     };
 #pragma unroll 1
-    for (int r = 0; r < BW; ++r) {
+    for (int r = 0; r < BW * npass; ++r) {   // npass inner sweeps; slots return to column order every BW rounds
       ICLK(r, 0);
       // angles (warp aw, lane = pair a: rows a and pa = BW + (a + r) % BW)
       int rot = 0;
@@ -418,7 +418,7 @@ __host__ __device__ inline Layout make_layout(int k, int C) {
 
 template <int BW>
 __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, const float* __restrict__ L,
-                                                      float* __restrict__ Wf, int32_t* status, int w_is_l) {
+                                                      float* __restrict__ Wf, int32_t* status, int w_is_l, int npass) {
   using P = JB<BW>;
   constexpr int PW = P::PW, LDQ = P::LDQ, PACK = P::PACK, N4 = P::N4, UT = P::UT, NQB = P::NQB;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -527,7 +527,8 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
           const GramSrc<BW> Gsrc{Gp + (size_t)gi * PACK, C, nown * PACK};
           int rot_any = 0;
           if (!diag) {
-            rot_any = inner_sweep_cross4<BW>(Gsrc, Qw + (size_t)gi * PW * LDQ, tol2, S, lane, h, gi & 3, 1 + gi);
+            rot_any = inner_sweep_cross4<BW>(Gsrc, Qw + (size_t)gi * PW * LDQ, tol2, S, lane, h, gi & 3, 1 + gi,
+                                             npass);
           } else if (h < 2) {   // diagonal round: block I by warp 0, block J by warp 1
             int* rflag = reinterpret_cast<int*>(S.xg);
             const int rh = inner_sweep_diag<BW>(Gsrc, Qw + (size_t)gi * PW * LDQ, h * BW, tol2, S.csd + h * (BW / 2),
@@ -669,7 +670,12 @@ cudaError_t launch_bw(int nb, int k, const float* L, float* Wf, int32_t* status,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_jacobi_blk<BW>, k, C, tol, L, Wf, status, w_is_l);
+  static const int npass = [] {   // inner sweeps per outer round (HG_JACOBI_INNER, default 1)
+    const char* v = getenv("HG_JACOBI_INNER");
+    const int x = v ? atoi(v) : 1;
+    return x < 1 ? 1 : (x > 4 ? 4 : x);
+  }();
+  return cudaLaunchKernelEx(&cfg, k_jacobi_blk<BW>, k, C, tol, L, Wf, status, w_is_l, npass);
 }
 
 }  // namespace

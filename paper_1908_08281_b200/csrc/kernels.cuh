@@ -34,11 +34,12 @@ cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float
                             float* Vt, double* sig_raw, int32_t* perm, int32_t* status, cudaStream_t s,
                             int* launches);
 // apply prep: rs[i][j] = scale / sigma[i][j]; flags singular sigma
-cudaError_t launch_inv_sigma(int nb, int k, const float* sigma, float scale, float* rs, int32_t* status,
+// (sigma, rs are [nb][ld]; the first k per block are used, the rest of rs is zeroed)
+cudaError_t launch_inv_sigma(int nb, int k, int ld, const float* sigma, float scale, float* rs, int32_t* status,
                              cudaStream_t s, int* launches);
 
 // reading R2: rs[i][j] = c sigma_ij / ((1+mu) - sigma_ij)  (Woodbury weights)
-cudaError_t launch_woodbury_scale(int nb, int k, const float* sigma, float c, float one_plus_mu, float* rs,
+cudaError_t launch_woodbury_scale(int nb, int k, int ld, const float* sigma, float c, float one_plus_mu, float* rs,
                                   int32_t* status, cudaStream_t s, int* launches);
 
 // debug counters (device globals): chol {near-identity, full}; jacobi {max sweeps, total sweeps, blocks}

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhgrsvd.so")
 
 HG_OK, HG_ERR_INVALID, HG_ERR_NUMERICAL, HG_ERR_CUDA = 0, 2, 3, 4
-HG_RAW_THETA, HG_SYNC, HG_WOODBURY, HG_GEMM_SIMT = 1 << 0, 1 << 1, 1 << 2, 1 << 8
+HG_RAW_THETA, HG_SYNC, HG_WOODBURY, HG_POWER_EQ10, HG_GEMM_SIMT = 1 << 0, 1 << 1, 1 << 2, 1 << 3, 1 << 8
 ST_FLAGS = {1: "isolated vertex", 2: "empty hyperedge", 4: "Cholesky breakdown", 8: "Jacobi sweep cap",
             16: "singular sigma", 32: "non-finite value", 64: "CG breakdown"}
 
@@ -50,6 +50,12 @@ _block_rsvd = _sig("hg_block_rsvd", ctypes.c_int, _P, _i32, _i32, _i32, _i32, _u
                    _P)
 _block_apply = _sig("hg_block_apply_inverse", ctypes.c_int, _P, _P, _P, _i32, _i32, _i32, _P, _i32, _f32, _P, _P, _P,
                     _sz, _P)
+_workspace_size_ex = _sig("hg_workspace_size_ex", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, _i32, _i32,
+                          ctypes.POINTER(_sz))
+_block_rsvd_ex = _sig("hg_block_rsvd_ex", ctypes.c_int, _P, _i32, _i32, _i32, _i32, _i32, _u64, _u32, _P, _P, _P, _P,
+                      _P, _sz, _P)
+_solve_ex = _sig("hg_solve_ex", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _i32, _i32, _i32, _u64, _P,
+                 _i32, _P, _P, _u32, _P, _P, _sz, _P)
 _block_woodbury = _sig("hg_block_apply_woodbury", ctypes.c_int, _P, _P, _i32, _i32, _i32, _P, _i32, _f32, _P, _P,
                        _P, _sz, _P)
 _solve = _sig("hg_solve", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _i32, _i32, _u64, _P, _i32, _P,
@@ -71,7 +77,7 @@ _debug_counters = _sig("hg_debug_counters", ctypes.c_int, _P, _i32, _i32)
 EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_rsvd", "hg_block_apply_inverse",
            "hg_solve", "hg_solve_host", "hg_gemm", "hg_last_error", "hg_last_launch_count", "hg_profile_enable",
            "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve",
-           "hg_block_apply_woodbury")
+           "hg_block_apply_woodbury", "hg_workspace_size_ex", "hg_block_rsvd_ex", "hg_solve_ex")
 
 
 class HGError(RuntimeError):
@@ -153,9 +159,12 @@ def _dev(t: torch.Tensor, dtype) -> torch.Tensor:
     return t
 
 
-def workspace_size(N: int, E: int, nnz: int, b: int, k: int, T: int) -> int:
+def workspace_size(N: int, E: int, nnz: int, b: int, k: int, T: int, p: int = 0) -> int:
     out = _sz(0)
-    _check(_workspace_size(N, E, nnz, b, k, T, ctypes.byref(out)))
+    if p:
+        _check(_workspace_size_ex(N, E, nnz, b, k, p, T, ctypes.byref(out)))
+    else:
+        _check(_workspace_size(N, E, nnz, b, k, T, ctypes.byref(out)))
     return int(out.value)
 
 
@@ -169,8 +178,8 @@ class Workspace:
         self.nbytes = nbytes
 
     @classmethod
-    def for_sizes(cls, N, E, nnz, b, k, T, device=None):
-        return cls(workspace_size(N, E, nnz, b, k, T), device)
+    def for_sizes(cls, N, E, nnz, b, k, T, device=None, p: int = 0):
+        return cls(workspace_size(N, E, nnz, b, k, T, p), device)
 
 
 @dataclass
@@ -214,18 +223,21 @@ def fill_gaussian(seed: int, rows: int, cols: int, device="cuda", stream=None) -
     return out
 
 
-def block_rsvd(blocks: torch.Tensor, k: int, q: int, seed: int, *, simt: bool = False,
-               ws: Optional[Workspace] = None, status: Optional[torch.Tensor] = None, stream=None):
-    """Alg. 1 on each block: returns Ut [nb][k][b], sigma [nb][k], Vt [nb][k][b], status."""
+def block_rsvd(blocks: torch.Tensor, k: int, q: int, seed: int, *, simt: bool = False, p: int = 0,
+               eq10: bool = False, ws: Optional[Workspace] = None, status: Optional[torch.Tensor] = None,
+               stream=None):
+    """Alg. 1 on each block (oversampling p, Eq. 10 scheme with eq10): Ut [nb][k][b], sigma [nb][k],
+    Vt [nb][k][b], status."""
     _dev(blocks, torch.float32)
     nb, b, _ = blocks.shape
-    ws = ws or Workspace.for_sizes(nb * b, 1, 0, b, k, 0)
+    ws = ws or Workspace.for_sizes(nb * b, 1, 0, b, k, 0, p=p)
     Ut = torch.empty((nb, k, b), dtype=torch.float32, device=blocks.device)
     Vt = torch.empty_like(Ut)
     sigma = torch.empty((nb, k), dtype=torch.float32, device=blocks.device)
     st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=blocks.device)
-    _check(_block_rsvd(_ptr(blocks), nb, b, k, q, seed, HG_GEMM_SIMT if simt else 0, _ptr(Ut), _ptr(sigma), _ptr(Vt),
-                       _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
+    flags = (HG_GEMM_SIMT if simt else 0) | (HG_POWER_EQ10 if eq10 else 0)
+    _check(_block_rsvd_ex(_ptr(blocks), nb, b, k, p, q, seed, flags, _ptr(Ut), _ptr(sigma), _ptr(Vt),
+                          _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
     return Ut, sigma, Vt, st
 
 
@@ -260,21 +272,27 @@ def block_apply_woodbury(Ut: torch.Tensor, sigma: torch.Tensor, Y: torch.Tensor,
 
 
 def solve(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, b: int, k: int, q: int, seed: int,
-          sync: bool = True, simt: bool = False, woodbury: bool = False, ws: Optional[Workspace] = None,
+          sync: bool = True, simt: bool = False, woodbury: bool = False, p: int = 0, eq10: bool = False,
+          ws: Optional[Workspace] = None,
           F: Optional[torch.Tensor] = None, sigma: Optional[torch.Tensor] = None,
           status: Optional[torch.Tensor] = None, stream=None) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
     """The whole path from CSR H to F [N][T] (and sigma [N/b][k])."""
     _dev(w, torch.float32)
     _dev(Y, torch.float32)
     N, T = H.N, Y.shape[1]
-    ws = ws or Workspace.for_sizes(N, H.n_edges, H.nnz, b, k, T)
+    ws = ws or Workspace.for_sizes(N, H.n_edges, H.nnz, b, k, T, p=p)
     F = F if F is not None else torch.empty((N, T), dtype=torch.float32, device=Y.device)
     sigma = sigma if sigma is not None else torch.empty((N // b, k), dtype=torch.float32, device=Y.device)
     st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=Y.device)
-    flags = (HG_SYNC if sync else 0) | (HG_GEMM_SIMT if simt else 0) | (HG_WOODBURY if woodbury else 0)
+    flags = ((HG_SYNC if sync else 0) | (HG_GEMM_SIMT if simt else 0) | (HG_WOODBURY if woodbury else 0) |
+             (HG_POWER_EQ10 if eq10 else 0))
     inc = H.c()
-    _check(_solve(ctypes.byref(inc), _ptr(w), mu, b, k, q, seed, _ptr(Y), T, _ptr(F), _ptr(sigma), flags, _ptr(st),
-                  ws.ptr, ws.nbytes, _stream(stream)))
+    if p:
+        _check(_solve_ex(ctypes.byref(inc), _ptr(w), mu, b, k, p, q, seed, _ptr(Y), T, _ptr(F), _ptr(sigma), flags,
+                         _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
+    else:
+        _check(_solve(ctypes.byref(inc), _ptr(w), mu, b, k, q, seed, _ptr(Y), T, _ptr(F), _ptr(sigma), flags,
+                      _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
     return F, sigma, st
 
 
