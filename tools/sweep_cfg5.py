@@ -5,7 +5,10 @@ FP64 oracle on blocks {0, nb-1} (F rel-Frobenius, sigma rel), accuracy of the
 rank-k block inverse against the exact block solve c X_ii^-1 Y_i (FP64 LU) on
 the same blocks, and accuracy of the whole GPU F against the full solve
 F* = c X^-1 Y (FP64 block CG on the sparse operator; computed
-once: it does not depend on b, k, q).  One JSON line per point.
+once: it does not depend on b, k, q; the GPU CG of hg_cg_solve is checked against it).
+Each point is also run with reading R2 (HG_WOODBURY: Alg. 1 on Theta_ii + Woodbury, §8(f)
+NEXT-3): time, parity against the oracle's R2, accuracy against the same two references.
+One JSON line per point.
 
     python tools/sweep_cfg5.py [--points b,k,q ...] > profiles/r01_cfg5_sweep.jsonl
 """
@@ -78,8 +81,24 @@ def main():
     Y = torch.from_numpy(h.Y).cuda()
     t0 = time.time()
     Fstar, cg_it = full_solve_cg(h, base.mu)
-    print(json.dumps({"full_solve_cg": {"iterations": cg_it, "seconds": time.time() - t0,
-                                        "norm": float(np.linalg.norm(Fstar))}}), flush=True)
+    line = {"full_solve_cg": {"iterations": cg_it, "seconds": time.time() - t0, "norm": float(np.linalg.norm(Fstar))}}
+    # the GPU CG (tol 1e-6) on the same system, against the FP64 reference
+    Fc, itc, rrc, stc = hg.cg_solve(H, w, Y, mu=base.mu, max_iter=100, tol=1e-6)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(a.reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        hg.cg_solve(H, w, Y, mu=base.mu, max_iter=100, tol=1e-6, F=Fc, iters=itc, rel_res=rrc, status=stc,
+                    sync=False)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    line["gpu_cg"] = {"solve_ms": float(np.median(ts)), "iterations_max": int(itc.max().item()),
+                      "status": int(stc.item()),
+                      "rel_vs_fp64_full_solve": float(np.linalg.norm(Fc.double().cpu().numpy() - Fstar) /
+                                                      np.linalg.norm(Fstar))}
+    print(json.dumps(line), flush=True)
     for (b, k, q) in pts:
         c = base.with_(b=b, k=k, q=q)
         out = {"b": b, "k": k, "q": q, "nb": c.nb}
@@ -117,6 +136,36 @@ def main():
             out.update({"parity_F_rel": max(fe), "parity_sigma_rel": max(se), "parity_ok": max(fe) <= 2e-5 and
                         max(se) <= 1e-5 and out["status"] == 0,
                         "oracle_vs_exact_block_solve": max(acc), "oracle_s": time.time() - t0})
+            # reading R2 on the same point
+            F2, s2, st2 = hg.solve(H, w, Y, mu=c.mu, b=b, k=k, q=q, seed=0, ws=ws, sync=False, woodbury=True)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(a.reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                hg.solve(H, w, Y, mu=c.mu, b=b, k=k, q=q, seed=0, ws=ws, F=F2, sigma=s2, status=st2, sync=False,
+                         woodbury=True)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            t0 = time.time()
+            r2 = oracle.solve(h.row_ptr, h.col_idx, h.w, h.Y, mu=c.mu, b=b, k=k, q=q, seed=0, blocks=blocks,
+                              woodbury=True)
+            F2g = F2.double().cpu().numpy()
+            s2g = s2.double().cpu().numpy()
+            fe2, se2, acc2 = [], [], []
+            for s_, blk in enumerate(blocks):
+                fo = r2.F[s_ * b:(s_ + 1) * b]
+                fe2.append(float(np.linalg.norm(F2g[blk * b:(blk + 1) * b] - fo) / np.linalg.norm(fo)))
+                se2.append(float(np.max(np.abs(s2g[blk] - r2.sigma[s_]) / r2.sigma[s_])))
+                exact = 0.5 * np.linalg.solve(r.X[s_], h.Y[blk * b:(blk + 1) * b].astype(np.float64))
+                acc2.append(float(np.linalg.norm(fo - exact) / np.linalg.norm(exact)))
+            out["r2"] = {"status": int(st2.item()), "solve_ms": float(np.median(ts)),
+                         "parity_F_rel": max(fe2), "parity_sigma_rel": max(se2),
+                         "parity_ok": max(fe2) <= 2e-5 and max(se2) <= 1e-5 and int(st2.item()) == 0,
+                         "oracle_vs_exact_block_solve": max(acc2),
+                         "gpu_vs_full_solve": float(np.linalg.norm(F2g - Fstar) / np.linalg.norm(Fstar)),
+                         "oracle_s": time.time() - t0}
         except hg.HGError as e:
             out["error"] = str(e)
         print(json.dumps(out), flush=True)
