@@ -69,6 +69,12 @@ def lib() -> ctypes.CDLL:
         L.or_solve_mode.restype = ci
         L.or_apply_woodbury.argtypes = [i32, i32, i32, P, P, P, dbl, P]
         L.or_apply_woodbury.restype = None
+        L.or_weight_objective.argtypes = [i32, i32, P, P, P, P, i32, dbl, P, cp, ci]
+        L.or_weight_objective.restype = ci
+        L.or_weight_gradient.argtypes = [i32, i32, P, P, P, P, i32, dbl, P, cp, ci]
+        L.or_weight_gradient.restype = ci
+        L.or_weight_step.argtypes = [i32, P, P, P, dbl, cp, ci]
+        L.or_weight_step.restype = ci
         L.or_apply_X.argtypes = [i32, i32, P, P, P, P, P, dbl, P, P, P]
         L.or_apply_X.restype = None
         L.or_cg_solve.argtypes = [i32, i32, P, P, P, dbl, P, i32, i32, dbl, P, P, P, cp, ci]
@@ -296,3 +302,47 @@ def cg_solve(row_ptr, col_idx, w, Y, *, mu: float, max_iter: int, tol: float) ->
     if st != OK:
         raise OracleError(st, err.value.decode())
     return CGResult(F, iters, rel, dt, lib().or_num_threads())
+
+
+# ------------------------------------------ NEXT-4: hyperedge-weight update
+def _F2(F):
+    F = np.ascontiguousarray(F, np.float64)
+    return F[:, None] if F.ndim == 1 else F
+
+
+def weight_objective(row_ptr, col_idx, w, F, *, kappa: float) -> float:
+    """P(w) = sum_t f_t^T L(w) f_t + kappa ||w||^2 (degrees re-derived from w)."""
+    row_ptr, col_idx, w = _csr(row_ptr, col_idx, w)
+    F = _F2(F)
+    out = np.zeros(1)
+    err = ctypes.create_string_buffer(256)
+    st = lib().or_weight_objective(len(row_ptr) - 1, len(w), _p(row_ptr), _p(col_idx), _p(w), _p(F), F.shape[1],
+                                   kappa, _p(out), err, 256)
+    if st != OK:
+        raise OracleError(st, err.value.decode())
+    return float(out[0])
+
+
+def weight_gradient(row_ptr, col_idx, w, F, *, kappa: float) -> np.ndarray:
+    """Frozen-degree gradient -(1/delta(e)) sum_t (h_e^T Dv^-1/2 f_t)^2 + 2 kappa w_e."""
+    row_ptr, col_idx, w = _csr(row_ptr, col_idx, w)
+    F = _F2(F)
+    g = np.zeros(len(w))
+    err = ctypes.create_string_buffer(256)
+    st = lib().or_weight_gradient(len(row_ptr) - 1, len(w), _p(row_ptr), _p(col_idx), _p(w), _p(F), F.shape[1],
+                                  kappa, _p(g), err, 256)
+    if st != OK:
+        raise OracleError(st, err.value.decode())
+    return g
+
+
+def weight_step(w, active, grad, mu: float):
+    """One simplex-constrained steepest-descent step; returns (w, active) copies."""
+    w = np.array(w, np.float64)
+    active = np.array(active, np.int32)
+    grad = np.ascontiguousarray(grad, np.float64)
+    err = ctypes.create_string_buffer(256)
+    st = lib().or_weight_step(len(w), _p(w), _p(active), _p(grad), mu, err, 256)
+    if st != OK:
+        raise OracleError(st, err.value.decode())
+    return w, active

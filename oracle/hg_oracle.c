@@ -24,6 +24,9 @@
  *                       PAPER.md:40; Alg. 1 applied to the PSD low-rank part)
  *   or_solve            the whole path over a chosen subset of diagonal blocks (mode 0: reading R1,
  *                       Alg. 1 on X_ii + Eq. 15; mode 1: reading R2, Alg. 1 on Theta_ii + Woodbury)
+ *   or_weight_objective PAPER.md:46-52   P(w) = sum_t f_t^T L f_t + kappa ||w||^2, L = I - Theta(w) (NEXT-4)
+ *   or_weight_gradient  PAPER.md:56-58   frozen-degree gradient of P (SPEC.md gradient_frozen)
+ *   or_weight_step      PAPER.md:54-58   w <- w - mu grad on the simplex, clamped coordinates stay 0
  *   or_apply_X          PAPER.md:30-40   X p = p - (1/(1+theta)) Dv^-1/2 H W De^-1 H^T Dv^-1/2 p (matrix-free)
  *   or_cg_solve         PAPER.md:165-178 the paper's second approach: CG on Eq. 5, X f = theta/(1+theta) y
  *                                        (Eqs. 16-20), one independent CG per right-hand-side column
@@ -651,6 +654,95 @@ int or_solve_mode(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* c
   }
   free(dv); free(de);
   if (fail) { set_err(err, errlen, "numerical failure (SVD non-convergence or singular sigma)"); return fail; }
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4: the hyperedge-weight update, f fixed             */
+/* ------------------------------------------------------------------------ */
+/* s[e][t] = h_e^T Dv^-1/2 f_t = sum_{v in e} f_t[v] / sqrt(delta(v)), delta(v) from w. */
+static void edge_projections(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx,
+                             const double* dv, const double* F, int32_t T, double* S) {
+  for (int64_t i = 0; i < (int64_t)E * T; ++i) S[i] = 0.0;
+  for (int32_t v = 0; v < N; ++v) {
+    double r = 1.0 / sqrt(dv[v]);
+    for (int64_t q = row_ptr[v]; q < row_ptr[v + 1]; ++q) {
+      int32_t e = col_idx[q];
+      for (int32_t t = 0; t < T; ++t) S[(int64_t)e * T + t] += r * F[(int64_t)v * T + t];
+    }
+  }
+}
+
+/* P(w) = sum_t f_t^T L(w) f_t + kappa ||w||^2 with L = I - A(w) (Eq. 1 with w, degrees re-derived)
+ * (reading N1: the T columns of F are summed). */
+int or_weight_objective(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
+                        const double* F, int32_t T, double kappa, double* out, char* err, int errlen) {
+  double* dv = (double*)malloc(sizeof(double) * (size_t)N);
+  double* de = (double*)malloc(sizeof(double) * (size_t)E);
+  int st = or_degrees(N, E, row_ptr, col_idx, w, dv, de, err, errlen);
+  if (st != OR_OK) { free(dv); free(de); return st; }
+  double* S = (double*)malloc(sizeof(double) * (size_t)E * (T > 0 ? T : 1));
+  edge_projections(N, E, row_ptr, col_idx, dv, F, T, S);
+  double ff = 0.0, fAf = 0.0, ww = 0.0;
+  for (int64_t i = 0; i < (int64_t)N * T; ++i) ff += F[i] * F[i];
+  for (int32_t e = 0; e < E; ++e) {
+    double se = 0.0;
+    for (int32_t t = 0; t < T; ++t) se += S[(int64_t)e * T + t] * S[(int64_t)e * T + t];
+    fAf += (double)w[e] / de[e] * se;           /* f^T Dv^-1/2 H W De^-1 H^T Dv^-1/2 f */
+    ww += (double)w[e] * (double)w[e];
+  }
+  *out = ff - fAf + kappa * ww;
+  free(dv); free(de); free(S);
+  return OR_OK;
+}
+
+/* Frozen-degree gradient (SPEC.md gradient_frozen; PAPER.md:56-58 steepest descent on P):
+ * D_v, D_e held at the current w, so only the explicit W of Eq. 1 differentiates:
+ *   grad_e = -(1/delta(e)) sum_t (h_e^T Dv^-1/2 f_t)^2 + 2 kappa w_e. */
+int or_weight_gradient(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
+                       const double* F, int32_t T, double kappa, double* grad, char* err, int errlen) {
+  double* dv = (double*)malloc(sizeof(double) * (size_t)N);
+  double* de = (double*)malloc(sizeof(double) * (size_t)E);
+  int st = or_degrees(N, E, row_ptr, col_idx, w, dv, de, err, errlen);
+  if (st != OR_OK) { free(dv); free(de); return st; }
+  double* S = (double*)malloc(sizeof(double) * (size_t)E * (T > 0 ? T : 1));
+  edge_projections(N, E, row_ptr, col_idx, dv, F, T, S);
+  for (int32_t e = 0; e < E; ++e) {
+    double se = 0.0;
+    for (int32_t t = 0; t < T; ++t) se += S[(int64_t)e * T + t] * S[(int64_t)e * T + t];
+    grad[e] = -se / de[e] + 2.0 * kappa * (double)w[e];
+  }
+  free(dv); free(de); free(S);
+  return OR_OK;
+}
+
+/* One steepest-descent step on the simplex (Eq. 5's active constraints;
+ * SPEC.md steepest_descent_step), reading N2:
+ *   1. g_e -= mean of g over the free (non-clamped) coordinates   (G_1: 1^T w = 1 stays active)
+ *   2. g_e  = 0 on clamped coordinates                             (G_j, j > 1: w_e = 0 stays)
+ *   3. w   -= mu g
+ *   4. while a free coordinate is < 0: clamp every such one to 0 (it joins the active set) and
+ *      subtract the excess (sum w - 1) evenly from the remaining free coordinates.
+ * active[e] = 1 marks clamped coordinates (in/out).  Error if every coordinate is clamped. */
+int or_weight_step(int32_t E, double* w, int32_t* active, const double* grad, double mu, char* err, int errlen) {
+  int32_t nfree = 0;
+  double gm = 0.0;
+  for (int32_t e = 0; e < E; ++e) if (!active[e]) { gm += grad[e]; ++nfree; }
+  if (nfree == 0) { set_err(err, errlen, "every hyperedge weight is clamped (degenerate simplex)"); return OR_ERR_NUMERICAL; }
+  gm /= nfree;
+  for (int32_t e = 0; e < E; ++e) if (!active[e]) w[e] -= mu * (grad[e] - gm);
+  for (;;) {
+    int clamped = 0;
+    for (int32_t e = 0; e < E; ++e)
+      if (!active[e] && w[e] < 0.0) { w[e] = 0.0; active[e] = 1; ++clamped; }
+    if (!clamped) break;
+    double sum = 0.0;
+    nfree = 0;
+    for (int32_t e = 0; e < E; ++e) { sum += w[e]; if (!active[e]) ++nfree; }
+    if (nfree == 0) { set_err(err, errlen, "every hyperedge weight is clamped (degenerate simplex)"); return OR_ERR_NUMERICAL; }
+    double ex = (sum - 1.0) / nfree;
+    for (int32_t e = 0; e < E; ++e) if (!active[e]) w[e] -= ex;
+  }
   return OR_OK;
 }
 
