@@ -57,7 +57,8 @@ enum hg_status_flags {
   HG_ST_JACOBI_CAP = 1 << 3,      /* one-sided Jacobi did not converge in the sweep cap      */
   HG_ST_SINGULAR_SIGMA = 1 << 4,  /* sigma_j <= 1e-6 sigma_1 at apply      */
   HG_ST_NONFINITE = 1 << 5,       /* NaN/Inf met                                             */
-  HG_ST_CG_BREAKDOWN = 1 << 6     /* hg_cg_solve: p^T X p <= 0 (X is SPD: corrupt input only)  */
+  HG_ST_CG_BREAKDOWN = 1 << 6,    /* hg_cg_solve: p^T X p <= 0 (X is SPD: corrupt input only)  */
+  HG_ST_SIMPLEX_DEGENERATE = 1 << 7 /* hg_weight_step: every hyperedge weight clamped to 0     */
 };
 
 /* flags */
@@ -209,6 +210,22 @@ hg_status hg_cg_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t T, int
 hg_status hg_cg_solve(const hg_incidence* H, const float* w, float mu, const float* Y, int32_t T, int32_t max_iter,
                       float tol, float* F, int32_t* iters, float* rel_res, uint32_t flags, int32_t* d_status,
                       void* ws, size_t ws_bytes, hg_stream_t stream);
+/* ---- NEXT-4: the hyperedge-weight update with f fixed.
+ * P(w) = sum_t f_t^T L f_t + kappa ||w||^2, L = I - Theta(w) (reading N1: the T columns of F are
+ * summed).  hg_weight_gradient: the frozen-degree gradient (D_v, D_e held at the current w)
+ *   grad_e = -(1/delta(e)) sum_t (sum_{v in e} f_t[v] / sqrt(delta(v)))^2 + 2 kappa w_e
+ *   H, w as for hg_solve; F [N][T] (T % 4 == 0); grad [E] out.
+ *   Workspace: hg_cg_workspace_size(N, E, nnz, T, 0) (the CSC of H is rebuilt per call).
+ * hg_weight_step: one steepest-descent step w <- w - mu g on the simplex 1^T w = 1, w >= 0
+ * (reading N2): g made mean-free over the free coordinates and zero on clamped ones
+ * (active[e] = 1), then negative free coordinates are clamped to 0 (joining the active set)
+ * and the excess mass removed evenly from the remaining free ones, until none is negative.
+ *   w [E] fp32 in/out, active [E] int32 in/out, grad [E].  One CTA; fp64 reductions.
+ * Device errors: HG_ST_SIMPLEX_DEGENERATE (every coordinate clamped). */
+hg_status hg_weight_gradient(const hg_incidence* H, const float* w, const float* F, int32_t T, float kappa,
+                             float* grad, int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
+hg_status hg_weight_step(int32_t E, float* w, int32_t* active, const float* grad, float mu, int32_t* d_status,
+                         hg_stream_t stream);
 /* Verification export of the batched GEMM the path runs on (3xTF32 on
  * tcgen05, or fp32 CUDA cores with HG_GEMM_SIMT):
  *   for g < batch: D_g(m,n) = alpha * rs_g[m] * cs_g[n] * sum_kk A_g(m,kk) B_g(kk,n)

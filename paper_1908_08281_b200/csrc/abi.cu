@@ -1136,6 +1136,38 @@ hg_status hg_cg_solve(const hg_incidence* H, const float* w, float mu, const flo
   return HG_OK;
 }
 
+// ---------------------------------------------------------------- NEXT-4
+hg_status hg_weight_gradient(const hg_incidence* H, const float* w, const float* F, int32_t T, float kappa,
+                             float* grad, int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  HG_TRY(check_H(H));
+  if (T < 1 || T % 4) return fail(HG_ERR_INVALID, "T must be >= 1 and a multiple of 4 (T=%d)", T);
+  if (!w || !F || !grad || !d_status) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (!std::isfinite(kappa)) return fail(HG_ERR_INVALID, "kappa must be finite");
+  if (H->nnz >= INT32_MAX) return fail(HG_ERR_INVALID, "nnz must be < 2^31");
+  const CgLayout L = cg_layout(H->n_vertices, H->n_edges, H->nnz, T, 0);
+  HG_TRY(check_ws(ws, ws_bytes, L.total));
+  CgArgs a;
+  a.N = H->n_vertices; a.E = H->n_edges; a.nnz = H->nnz; a.row_ptr = H->row_ptr; a.col_idx = H->col_idx;
+  a.w = w; a.mu = 1.f; a.Y = nullptr; a.T = T; a.max_iter = 0; a.tol = 0.f; a.F = const_cast<float*>(F);
+  a.iters_out = nullptr; a.rel_out = nullptr; a.status = d_status; a.ws = ws;
+  HG_CU(launch_weight_gradient(a, kappa, grad, reinterpret_cast<cudaStream_t>(stream), &g_launches), "weight gradient");
+  return HG_OK;
+}
+
+hg_status hg_weight_step(int32_t E, float* w, int32_t* active, const float* grad, float mu, int32_t* d_status,
+                         hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (E <= 0) return fail(HG_ERR_INVALID, "E must be > 0");
+  if (!w || !active || !grad || !d_status) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (!(mu >= 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and >= 0");
+  HG_CU(launch_weight_step(E, w, active, grad, mu, d_status, reinterpret_cast<cudaStream_t>(stream), &g_launches),
+        "weight step");
+  return HG_OK;
+}
+
 hg_status hg_gemm(int32_t M, int32_t N, int32_t K, int32_t batch, const float* A, int32_t a_mn, int64_t lda,
                   int64_t sa, const float* B, int32_t b_mn, int64_t ldb, int64_t sb, float* D, int32_t d_trans,
                   int64_t ldd, int64_t sd, float alpha, const float* rs, int64_t srs, const float* cs, int64_t scs,

@@ -519,6 +519,132 @@ __global__ void __launch_bounds__(NT) k_cg_out(CgDev d, float* __restrict__ Fo, 
   }
 }
 
+// ------------------------------------------------------------------ NEXT-4
+// Frozen-degree gradient of P(w) = sum_t f_t^T L f_t + kappa ||w||^2 (oracle or_weight_gradient):
+//   grad_e = -(1/delta(e)) sum_t s_{e,t}^2 + 2 kappa w_e,   s_{e,t} = sum_{v in e} r_v F[v][t].
+// One warp per CSC work item; columns in chunks of 128 (a float4 per lane) straight from the
+// caller's [N][T] F.  Single-chunk edges finish here; chunks of larger edges go to partial
+// slots [slot][Tp] that k_wgrad_big adds in chunk order before squaring (deterministic).
+__global__ void __launch_bounds__(NT) k_wgrad_items(int T, int Tp, const float* __restrict__ F,
+                                                    const float* __restrict__ dvr, const int32_t* __restrict__ csc,
+                                                    const int4* __restrict__ items, const int32_t* __restrict__ totals,
+                                                    const int32_t* __restrict__ de, const float* __restrict__ w,
+                                                    float kappa, float* __restrict__ part, float* __restrict__ grad) {
+  const int lane = threadIdx.x & 31;
+  const int item = blockIdx.x * NW + (threadIdx.x >> 5);
+  if (item >= totals[0]) return;
+  const int4 it = items[item];
+  double sq = 0.0;
+  for (int c0 = 0; c0 < T; c0 += 128) {
+    const int c = c0 + 4 * lane;
+    const bool on = c < T;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int base = it.y; base < it.z; base += 32) {
+      const int j = base + lane;
+      const int myv = j < it.z ? csc[j] : 0;
+      const float myr = j < it.z ? dvr[myv] : 0.f;
+      const int cnt = min(32, it.z - base);
+      for (int u0 = 0; u0 < cnt; u0 += 8) {
+        float4 x[8];
+        float r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int v = __shfl_sync(~0u, myv, (u0 + u) & 31);
+          r[u] = __shfl_sync(~0u, myr, (u0 + u) & 31);
+          x[u] = (on && u0 + u < cnt) ? __ldg(reinterpret_cast<const float4*>(F + (size_t)v * T + c))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = f4_fma(r[u], x[u], acc);
+      }
+    }
+    if (it.w >= 0) {
+      if (on) *reinterpret_cast<float4*>(part + (size_t)it.w * Tp + c) = acc;
+    } else {
+      sq += (double)acc.x * acc.x + (double)acc.y * acc.y + (double)acc.z * acc.z + (double)acc.w * acc.w;
+    }
+  }
+  if (it.w < 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(~0u, sq, o);
+    if (lane == 0) grad[it.x] = (float)(-sq / (double)de[it.x] + 2.0 * (double)kappa * (double)w[it.x]);
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_wgrad_big(int T, int Tp, const int4* __restrict__ bigs,
+                                                  const int32_t* __restrict__ totals, const int32_t* __restrict__ de,
+                                                  const float* __restrict__ w, float kappa,
+                                                  const float* __restrict__ part, float* __restrict__ grad) {
+  const int lane = threadIdx.x & 31;
+  const int bi = blockIdx.x * NW + (threadIdx.x >> 5);
+  if (bi >= totals[1]) return;
+  const int4 b = bigs[bi];
+  double sq = 0.0;
+  for (int c = 4 * lane; c < T; c += 128) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < b.z; ++j) {
+      const float4 x = *reinterpret_cast<const float4*>(part + (size_t)(b.y + j) * Tp + c);
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    sq += (double)acc.x * acc.x + (double)acc.y * acc.y + (double)acc.z * acc.z + (double)acc.w * acc.w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(~0u, sq, o);
+  if (lane == 0) grad[b.x] = (float)(-sq / (double)de[b.x] + 2.0 * (double)kappa * (double)w[b.x]);
+}
+
+// One simplex-constrained steepest-descent step (oracle or_weight_step, reading N2), one
+// CTA, fp64 fixed-order reductions: mean-free gradient over the free coordinates, w -= mu g,
+// then clamp negative free coordinates to 0 (they join the active set) and remove the excess
+// mass evenly from the remaining free ones, until none is negative.
+__device__ double block_sum_d(double v, double* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(~0u, v, o);
+  __syncthreads();
+  if (lane == 0) sm[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sm[i];
+  return t;
+}
+
+__global__ void __launch_bounds__(1024) k_weight_step(int E, float* __restrict__ w, int32_t* __restrict__ active,
+                                                      const float* __restrict__ grad, float mu, int32_t* status) {
+  __shared__ double sm[32];
+  double gs = 0.0, nf = 0.0;
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (!active[e]) { gs += grad[e]; nf += 1.0; }
+  gs = block_sum_d(gs, sm);
+  nf = block_sum_d(nf, sm);
+  if (nf == 0.0) {
+    if (threadIdx.x == 0) hg_flag(status, HGS_SIMPLEX_DEGENERATE);
+    return;
+  }
+  const double gm = gs / nf;
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (!active[e]) w[e] = (float)((double)w[e] - (double)mu * ((double)grad[e] - gm));
+  for (int round = 0; round < E + 1; ++round) {
+    __syncthreads();
+    double clamped = 0.0;
+    for (int e = threadIdx.x; e < E; e += blockDim.x)
+      if (!active[e] && w[e] < 0.f) { w[e] = 0.f; active[e] = 1; clamped += 1.0; }
+    clamped = block_sum_d(clamped, sm);
+    if (clamped == 0.0) break;
+    double sum = 0.0, fr = 0.0;
+    for (int e = threadIdx.x; e < E; e += blockDim.x) { sum += w[e]; if (!active[e]) fr += 1.0; }
+    sum = block_sum_d(sum, sm);
+    fr = block_sum_d(fr, sm);
+    if (fr == 0.0) {
+      if (threadIdx.x == 0) hg_flag(status, HGS_SIMPLEX_DEGENERATE);
+      return;
+    }
+    const double ex = (sum - 1.0) / fr;
+    for (int e = threadIdx.x; e < E; e += blockDim.x)
+      if (!active[e]) w[e] = (float)((double)w[e] - ex);
+  }
+}
+
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
 }  // namespace
@@ -625,14 +751,13 @@ cudaError_t body(const CgDev& d, const CgLayout& L, cudaGraphConditionalHandle h
   return cudaGetLastError();
 }
 
-template <int LPR>
-cudaError_t prologue(const CgArgs& a, const CgDev& d, const CgLayout& L, cudaStream_t s, int* launches) {
+// degrees (r = delta(v)^-1/2, w_e/delta(e)) and the sorted CSC of H with its CH-chunk work items
+cudaError_t setup_csc(const CgArgs& a, const CgLayout& L, cudaStream_t s, int* launches) {
   void* ws = a.ws;
   cudaError_t e = launch_degrees(a.N, a.E, a.nnz, a.row_ptr, a.col_idx, a.w, at<int32_t>(ws, L.de),
                                  at<float>(ws, L.eval), at<float>(ws, L.dvr), a.status, s, launches);
   if (e != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(at<int32_t>(ws, L.cursor), 0, 4 * (size_t)a.E, s)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(d.ctl, 0, 4 * (size_t)(a.max_iter + 3), s)) != cudaSuccess) return e;
   int32_t* col_ptr = at<int32_t>(ws, L.col_ptr);
   k_cg_scan<<<1, 1024, 0, s>>>(a.E, at<int32_t>(ws, L.de), col_ptr, at<int32_t>(ws, L.item_ptr),
                                at<int32_t>(ws, L.slot_ptr), at<int32_t>(ws, L.big_ptr), at<int32_t>(ws, L.totals));
@@ -646,10 +771,19 @@ cudaError_t prologue(const CgArgs& a, const CgDev& d, const CgLayout& L, cudaStr
                                                                      at<int32_t>(ws, L.csc));
   k_cg_items<<<gE, 256, 0, s>>>(a.E, col_ptr, at<int32_t>(ws, L.item_ptr), at<int32_t>(ws, L.slot_ptr),
                                 at<int32_t>(ws, L.big_ptr), at<int4>(ws, L.items), at<int4>(ws, L.bigs));
+  *launches += 6;
+  return cudaGetLastError();
+}
+
+template <int LPR>
+cudaError_t prologue(const CgArgs& a, const CgDev& d, const CgLayout& L, cudaStream_t s, int* launches) {
+  cudaError_t e = cudaMemsetAsync(d.ctl, 0, 4 * (size_t)(a.max_iter + 3), s);
+  if (e != cudaSuccess) return e;
+  if ((e = setup_csc(a, L, s, launches)) != cudaSuccess) return e;
   const dim3 gr(L.nparts, L.ns);
   k_cg_init<LPR><<<gr, NT, 0, s>>>(d, a.Y);
   k_cg_scalars<4 * LPR><<<L.ns, 512, 0, s>>>(d, 0);
-  *launches += 8;
+  *launches += 2;
   return cudaGetLastError();
 }
 
@@ -689,4 +823,27 @@ cudaError_t launch_cg(const CgArgs& a, const CgGraphHook* hook, cudaStream_t s, 
     case 16: return run_cg_t<16>(a, L, hook, s, launches);
     default: return run_cg_t<8>(a, L, hook, s, launches);
   }
+}
+
+// NEXT-4 entry points; a.F is the caller's F [N][T], a.ws a CG workspace.
+cudaError_t launch_weight_gradient(const CgArgs& a, float kappa, float* grad, cudaStream_t s, int* launches) {
+  const CgLayout L = cg_layout(a.N, a.E, a.nnz, a.T, 0);
+  cudaError_t e = setup_csc(a, L, s, launches);
+  if (e != cudaSuccess) return e;
+  const int Tp = L.ns * L.TS;   // partial-slot pitch (the CG partial buffer holds max_slots x Tp)
+  k_wgrad_items<<<(unsigned)((L.max_items + NW - 1) / NW), NT, 0, s>>>(
+      a.T, Tp, a.F, at<float>(a.ws, L.dvr), at<int32_t>(a.ws, L.csc), at<int4>(a.ws, L.items),
+      at<int32_t>(a.ws, L.totals), at<int32_t>(a.ws, L.de), a.w, kappa, at<float>(a.ws, L.part), grad);
+  k_wgrad_big<<<(unsigned)((L.max_big + NW - 1) / NW), NT, 0, s>>>(
+      a.T, Tp, at<int4>(a.ws, L.bigs), at<int32_t>(a.ws, L.totals), at<int32_t>(a.ws, L.de), a.w, kappa,
+      at<float>(a.ws, L.part), grad);
+  *launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_weight_step(int E, float* w, int32_t* active, const float* grad, float mu, int32_t* status,
+                               cudaStream_t s, int* launches) {
+  k_weight_step<<<1, 1024, 0, s>>>(E, w, active, grad, mu, status);
+  ++*launches;
+  return cudaGetLastError();
 }

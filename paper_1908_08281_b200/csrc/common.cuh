@@ -23,6 +23,7 @@ enum : int32_t {
   HGS_SINGULAR_SIGMA = 1 << 4,    // sigma_j <= sigma_1 * 1e-6 at apply
   HGS_NONFINITE = 1 << 5,         // NaN/Inf
   HGS_CG_BREAKDOWN = 1 << 6,      // CG: p^T X p <= 0 (X is SPD, so only on corrupt input)
+  HGS_SIMPLEX_DEGENERATE = 1 << 7,  // weight step: every hyperedge weight clamped to 0
 };
 
 __device__ __forceinline__ void hg_flag(int32_t* st, int32_t f) {

@@ -96,3 +96,8 @@ struct CgGraphHook {
 int cg_lanes(int T);
 CgLayout cg_layout(int64_t N, int64_t E, int64_t nnz, int64_t T, int64_t max_iter);
 cudaError_t launch_cg(const CgArgs& a, const CgGraphHook* hook, cudaStream_t s, int* launches);
+// NEXT-4: frozen-degree gradient (a.F = F [N][T] read-only, a.ws a CG
+// workspace of hg_cg_workspace_size(N, E, nnz, T, 0)) and one simplex step
+cudaError_t launch_weight_gradient(const CgArgs& a, float kappa, float* grad, cudaStream_t s, int* launches);
+cudaError_t launch_weight_step(int E, float* w, int32_t* active, const float* grad, float mu, int32_t* status,
+                               cudaStream_t s, int* launches);

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libhgrsvd.so")
 HG_OK, HG_ERR_INVALID, HG_ERR_NUMERICAL, HG_ERR_CUDA = 0, 2, 3, 4
 HG_RAW_THETA, HG_SYNC, HG_WOODBURY, HG_POWER_EQ10, HG_GEMM_SIMT = 1 << 0, 1 << 1, 1 << 2, 1 << 3, 1 << 8
 ST_FLAGS = {1: "isolated vertex", 2: "empty hyperedge", 4: "Cholesky breakdown", 8: "Jacobi sweep cap",
-            16: "singular sigma", 32: "non-finite value", 64: "CG breakdown"}
+            16: "singular sigma", 32: "non-finite value", 64: "CG breakdown", 128: "degenerate simplex"}
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1908_08281_b200.build` "
@@ -67,6 +67,9 @@ _gemm = _sig("hg_gemm", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i32, _i64, _i
 _cg_workspace_size = _sig("hg_cg_workspace_size", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, ctypes.POINTER(_sz))
 _cg_solve = _sig("hg_cg_solve", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _P, _i32, _i32, _f32, _P, _P, _P,
                  _u32, _P, _P, _sz, _P)
+_weight_gradient = _sig("hg_weight_gradient", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _P, _i32, _f32, _P, _P,
+                        _P, _sz, _P)
+_weight_step = _sig("hg_weight_step", ctypes.c_int, _i32, _P, _P, _P, _f32, _P, _P)
 _last_error = _sig("hg_last_error", ctypes.c_char_p)
 _prof_enable = _sig("hg_profile_enable", ctypes.c_int, _i32)
 _prof_collect = _sig("hg_profile_collect", ctypes.c_int, _i32, _P, _P, _P, ctypes.POINTER(_i32))
@@ -77,7 +80,8 @@ _debug_counters = _sig("hg_debug_counters", ctypes.c_int, _P, _i32, _i32)
 EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_rsvd", "hg_block_apply_inverse",
            "hg_solve", "hg_solve_host", "hg_gemm", "hg_last_error", "hg_last_launch_count", "hg_profile_enable",
            "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve",
-           "hg_block_apply_woodbury", "hg_workspace_size_ex", "hg_block_rsvd_ex", "hg_solve_ex")
+           "hg_block_apply_woodbury", "hg_workspace_size_ex", "hg_block_rsvd_ex", "hg_solve_ex",
+           "hg_weight_gradient", "hg_weight_step")
 
 
 class HGError(RuntimeError):
@@ -345,6 +349,32 @@ def cg_solve(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, max_i
     _check(_cg_solve(ctypes.byref(inc), _ptr(w), mu, _ptr(Y), T, max_iter, tol, _ptr(F), _ptr(iters), _ptr(rel_res),
                      HG_SYNC if sync else 0, _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
     return F, iters, rel_res, st
+
+
+def weight_gradient(H: Incidence, w: torch.Tensor, F: torch.Tensor, *, kappa: float, ws: Optional[Workspace] = None,
+                    grad: Optional[torch.Tensor] = None, status: Optional[torch.Tensor] = None, stream=None):
+    """NEXT-4 frozen-degree gradient of P(w): returns grad [E], status."""
+    _dev(w, torch.float32)
+    _dev(F, torch.float32)
+    N, T = F.shape
+    ws = ws or Workspace(cg_workspace_size(N, H.n_edges, H.nnz, T, 0), F.device)
+    grad = grad if grad is not None else torch.empty(H.n_edges, dtype=torch.float32, device=F.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=F.device)
+    inc = H.c()
+    _check(_weight_gradient(ctypes.byref(inc), _ptr(w), _ptr(F), T, kappa, _ptr(grad), _ptr(st), ws.ptr, ws.nbytes,
+                            _stream(stream)))
+    return grad, st
+
+
+def weight_step(w: torch.Tensor, active: torch.Tensor, grad: torch.Tensor, mu: float, *,
+                status: Optional[torch.Tensor] = None, stream=None):
+    """One simplex-constrained steepest-descent step, in place on w and active; returns status."""
+    _dev(w, torch.float32)
+    _dev(active, torch.int32)
+    _dev(grad, torch.float32)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=w.device)
+    _check(_weight_step(w.numel(), _ptr(w), _ptr(active), _ptr(grad), mu, _ptr(st), _stream(stream)))
+    return st
 
 
 def incidence_to_device(row_ptr, col_idx, n_edges: int, device="cuda") -> Incidence:
