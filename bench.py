@@ -459,6 +459,43 @@ def run_ours(args):
                 r2["accuracy_vs_full_solve"] = {"r2": float(np.linalg.norm(Fg2 - Ff) / np.linalg.norm(Ff)),
                                                 "r1": float(np.linalg.norm(Fr1 - Ff) / np.linalg.norm(Ff))}
 
+    # the hyperedge-weight update with f = the CG solution
+    wts = None
+    if cg is not None and not args.no_weights:
+        kappa = 1.0
+        wg = torch.empty(h.E, dtype=torch.float32, device=dev)
+        for _ in range(3):
+            hg.weight_gradient(H, w, Fc, kappa=kappa, ws=cws, grad=wg, status=status, stream=stream)
+        torch.cuda.synchronize(dev)
+        n_w = max(3, min(args.steps, 10))
+        w0_, w1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0_.record(stream)
+        for _ in range(n_w):
+            hg.weight_gradient(H, w, Fc, kappa=kappa, ws=cws, grad=wg, status=status, stream=stream)
+        w1_.record(stream)
+        torch.cuda.synchronize(dev)
+        g_ms = w0_.elapsed_time(w1_) / n_w
+        ws_ = (w / w.sum()).contiguous()
+        act = torch.zeros(h.E, dtype=torch.int32, device=dev)
+        s0_, s1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0_.record(stream)
+        for _ in range(n_w):
+            hg.weight_step(ws_, act, wg, 1e-9, status=status, stream=stream)
+        s1_.record(stream)
+        torch.cuda.synchronize(dev)
+        st_ms = s0_.elapsed_time(s1_) / n_w
+        gather = h.nnz * c.T * 4.0
+        wts = {"workload": "grad_e of P(w) = sum_t f_t^T L f_t + kappa||w||^2 at F = the CG solution, kappa 1; "
+                           "one simplex step",
+               "gradient_ms": g_ms, "step_ms": st_ms, "gather_bytes": gather,
+               "gather_GBps": gather / (g_ms / 1e3) / 1e9, "status": int(status.item())}
+        if rank == 0:
+            import oracle
+            go = oracle.weight_gradient(h.row_ptr, h.col_idx, h.w, Fc.double().cpu().numpy(), kappa=kappa)
+            gg = wg.double().cpu().numpy()
+            err = float(np.max(np.abs(gg - go)) / np.max(np.abs(go)))
+            wts["parity"] = {"grad_max_rel": err, "tol": 1e-5, "ok": err <= 1e-5}
+
     out = {
         "metric": "diag_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -476,7 +513,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "parity": parity,
         "cpu_baseline": cpu_base,
-        "next_rows": {"cg": cg, "r2_woodbury": r2},
+        "next_rows": {"cg": cg, "r2_woodbury": r2, "weights": wts},
         "peaks": {"source": peak_src, "tf32_tflops_sustained": tf32_sust, "tf32_tflops_burst": tf32_burst,
                   "hbm_gbs": peaks["hbm_gbs"]},
     }
@@ -530,6 +567,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cg", action="store_true", help="skip the CG (NEXT-2) measurement")
     ap.add_argument("--no-r2", action="store_true", help="skip the reading-R2 (NEXT-3) measurement")
+    ap.add_argument("--no-weights", action="store_true", help="skip the weight-update (NEXT-4) measurement")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
