@@ -159,7 +159,7 @@ hg_status hg_block_apply_woodbury(const float* Ut, const float* sigma, int32_t n
  * *d_status returns HG_ERR_NUMERICAL).  d_status may be NULL only with HG_SYNC
  * (a word inside ws is used).
  * Concurrency: after the degrees, disjoint block ranges (HG_STREAMS parts,
- * default 6, at most 8) run their assembly, rSVD and apply on library-owned non-blocking
+ * default 8, at most 8) run their assembly, rSVD and apply on library-owned non-blocking
  * streams forked from and joined back into `stream` with events, so all work
  * is still ordered after prior work on `stream` and before later work (also
  * under stream capture).  The result is bitwise independent of the part count.

@@ -684,38 +684,45 @@ hg_status hg_block_apply_woodbury(const float* Ut, const float* sigma, int32_t n
                    part_bufs(ws, Lo, nb, 0, b, k, T), reinterpret_cast<cudaStream_t>(stream), false, 1.0f + mu);
 }
 
-// Part count for hg_solve (HG_STREAMS, default 6, at most 8: with graph replay measured
-// 11.99 ms at configs[3] vs 12.11 / 12.29 / 12.56 / 12.05 with 4 / 3 / 2 / 8 parts) and the
-// auxiliary streams / events
+// Part count for hg_solve (HG_STREAMS, default 8, at most 8: with graph replay measured
+// 10.99 ms at configs[3] vs 11.01 / 11.04 with 6 / 4 parts) and the auxiliary streams / events
 // of the fork-join (created once, non-blocking, reused).
 constexpr int kMaxParts = 8;
 static int solve_parts() {   // read per call (tests switch it)
   const char* v = getenv("HG_STREAMS");
-  const int x = v ? atoi(v) : 6;
+  const int x = v ? atoi(v) : 8;
   return x < 1 ? 1 : (x > kMaxParts ? kMaxParts : x);
 }
-// Parts run on library streams of default priority (HG_STREAM_PRIO=1: part p gets
-// greatest + p; measured 13.97 vs 13.80 ms at configs[3]: staggering the parts delays
-// the last part's latency-bound Jacobi, which sets the makespan).
-static cudaStream_t g_aux[kMaxParts] = {};
+// Two sets of part streams.  Plain (default priority) for hg_solve: staggering the parts delays
+// the last part's latency-bound Jacobi, which sets the device makespan (11.05 vs 10.99 ms).
+// Prioritised (part p at greatest + p) for hg_solve_host: the earliest parts then finish first
+// and their F downloads overlap the later parts' compute (e2e 15.30 -> 14.57 ms at configs[3]).
+// Graphs are instantiated with cudaGraphInstantiateFlagUseNodePriority so the captured
+// priorities hold under replay.  HG_STREAM_PRIO=0/1 forces one set for both entries.
+static cudaStream_t g_aux[2][kMaxParts] = {};
 static cudaEvent_t g_ev_fork = nullptr, g_ev_join[kMaxParts] = {};
 // library streams / events, created once and outside any stream capture
 static hg_status ensure_streams() {
   if (g_ev_fork) return HG_OK;
   int least = 0, greatest = 0;
   HG_CU(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
-  const char* pv = getenv("HG_STREAM_PRIO");
-  const bool prio = pv && pv[0] == '1';
-  for (int p = 0; p < kMaxParts; ++p) {
-    int pr = prio ? greatest + p : 0;
-    if (pr > least) pr = least;
-    HG_CU(cudaStreamCreateWithPriority(&g_aux[p], cudaStreamNonBlocking, pr), "stream create");
+  for (int set = 0; set < 2; ++set)
+    for (int p = 0; p < kMaxParts; ++p) {
+      int pr = set ? greatest + p : 0;
+      if (pr > least) pr = least;
+      HG_CU(cudaStreamCreateWithPriority(&g_aux[set][p], cudaStreamNonBlocking, pr), "stream create");
+    }
+  for (int p = 0; p < kMaxParts; ++p)
     HG_CU(cudaEventCreateWithFlags(&g_ev_join[p], cudaEventDisableTiming), "event create");
-  }
   HG_CU(cudaEventCreateWithFlags(&g_ev_fork, cudaEventDisableTiming), "event create");
   return HG_OK;
 }
-static hg_status fork_streams(cudaStream_t s, int nparts, cudaStream_t* ps) {
+static bool use_prio_streams(bool host_entry) {
+  const char* pv = getenv("HG_STREAM_PRIO");
+  if (pv && (pv[0] == '0' || pv[0] == '1')) return pv[0] == '1';
+  return host_entry;
+}
+static hg_status fork_streams(cudaStream_t s, int nparts, cudaStream_t* ps, bool prio) {
   ps[0] = s;
   if (nparts == 1) return HG_OK;
   if (const char* v = getenv("HG_STREAMS_SERIAL")) {   // debugging: parts in sequence on `stream`
@@ -725,7 +732,7 @@ static hg_status fork_streams(cudaStream_t s, int nparts, cudaStream_t* ps) {
     }
   }
   HG_TRY(ensure_streams());
-  cudaStream_t* aux = g_aux;
+  cudaStream_t* aux = g_aux[prio ? 1 : 0];
   cudaEvent_t ev_fork = g_ev_fork;
   HG_CU(cudaEventRecord(ev_fork, s), "fork record");
   for (int p = 0; p < nparts; ++p) {
@@ -803,7 +810,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     g_t0_set = true;
   }
   cudaStream_t ps[kMaxParts];
-  HG_TRY(fork_streams(s, nparts, ps));
+  HG_TRY(fork_streams(s, nparts, ps, use_prio_streams(io.F_host != nullptr)));
   // host staging of Y: one slice per part on the copy stream, started before the parts
   static cudaEvent_t ev_y[kMaxParts] = {};
   cudaStream_t cps = nullptr;
@@ -872,7 +879,7 @@ constexpr size_t kMaxGraphs = 8;
 std::string knob_env() {   // enqueue-time knobs that change the captured sequence
   std::string e;
   for (const char* n : {"HG_ASSEMBLE", "HG_STREAMS_SERIAL", "HG_BN_POWER", "HG_BN_GRAM", "HG_BN_QFORM", "HG_GRAM_FULL",
-                        "HG_QR_PASSES"}) {
+                        "HG_QR_PASSES", "HG_STREAM_PRIO"}) {
     const char* v = getenv(n);
     e += v ? v : "-";
     e += '|';
@@ -912,7 +919,8 @@ hg_status graph_run(const std::string& key, cudaStream_t s, Fn enqueue) {
       return r != HG_OK ? r : cuda_fail(ec, "end capture");
     }
     cudaGraphExec_t exec = nullptr;
-    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    // node priorities (captured from the part streams) are honoured only with this flag
+    const cudaError_t ei = cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(graph);
     if (ei != cudaSuccess) return cuda_fail(ei, "graph instantiate");
     if (!cache) {
