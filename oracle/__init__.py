@@ -69,6 +69,12 @@ def lib() -> ctypes.CDLL:
         L.or_solve_mode.restype = ci
         L.or_apply_woodbury.argtypes = [i32, i32, i32, P, P, P, dbl, P]
         L.or_apply_woodbury.restype = None
+        L.or_theta_offblock.argtypes = [i32, i32, i32, P, P, P, P, P, P]
+        L.or_theta_offblock.restype = None
+        L.or_lowrank_inverse.argtypes = [i32, i32, i32, P, P, dbl, P]
+        L.or_lowrank_inverse.restype = ci
+        L.or_solve_schur.argtypes = [i32, i32, P, P, P, dbl, i32, i32, i32, u64, P, i32, i32, P, P, cp, ci]
+        L.or_solve_schur.restype = ci
         L.or_weight_objective.argtypes = [i32, i32, P, P, P, P, i32, dbl, P, cp, ci]
         L.or_weight_objective.restype = ci
         L.or_weight_gradient.argtypes = [i32, i32, P, P, P, P, i32, dbl, P, cp, ci]
@@ -346,3 +352,45 @@ def weight_step(w, active, grad, mu: float):
     if st != OK:
         raise OracleError(st, err.value.decode())
     return w, active
+
+
+# ------------------------------------------ NEXT-1: 2x2 Schur-complement inverse
+def theta_offblock(row_ptr, col_idx, w, b: int, bi: int, bj: int) -> np.ndarray:
+    """Theta restricted to rows of block bi and columns of block bj (Eq. 1), fp64 b x b."""
+    row_ptr, col_idx, w = _csr(row_ptr, col_idx, w)
+    dv, de = degrees(row_ptr, col_idx, w)
+    out = np.zeros((b, b))
+    lib().or_theta_offblock(b, bi, bj, _p(row_ptr), _p(col_idx), _p(w), _p(dv), _p(de), _p(out))
+    return out
+
+
+def lowrank_inverse(K, Omega, q: int, mu: float) -> np.ndarray:
+    """(I - K/(1+mu))^-1 ~ I + U diag(s/((1+mu)-s)) U^T from Alg. 1 on PSD K (reading R2)."""
+    K = np.ascontiguousarray(K, np.float64)
+    Om = np.ascontiguousarray(Omega, np.float64)
+    m, k = Om.shape
+    out = np.zeros((m, m))
+    st = lib().or_lowrank_inverse(m, k, q, _p(K), _p(Om), mu, _p(out))
+    if st != OK:
+        raise OracleError(st, "SVD did not converge")
+    return out
+
+
+def solve_schur(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, seed: int,
+                superblocks: Optional[Sequence[int]] = None):
+    """One Eq. 12 level over super-blocks of 2b (blocks 2s, 2s+1); returns (F [n*2b][T], superblocks, seconds)."""
+    row_ptr, col_idx, w = _csr(row_ptr, col_idx, w)
+    Y = np.ascontiguousarray(Y, np.float32)
+    N, E = len(row_ptr) - 1, len(w)
+    T = Y.shape[1]
+    ns = N // (2 * b) if b > 0 else 0
+    sel = np.asarray(range(ns) if superblocks is None else superblocks, dtype=np.int32)
+    F = np.zeros((len(sel) * 2 * b, T))
+    err = ctypes.create_string_buffer(256)
+    t0 = time.perf_counter()
+    st = lib().or_solve_schur(N, E, _p(row_ptr), _p(col_idx), _p(w), mu, b, k, q, seed, _p(Y), T, len(sel),
+                              _p(sel), _p(F), err, 256)
+    dt = time.perf_counter() - t0
+    if st != OK:
+        raise OracleError(st, err.value.decode())
+    return F, list(map(int, sel)), dt

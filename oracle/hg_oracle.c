@@ -24,6 +24,10 @@
  *                       PAPER.md:40; Alg. 1 applied to the PSD low-rank part)
  *   or_solve            the whole path over a chosen subset of diagonal blocks (mode 0: reading R1,
  *                       Alg. 1 on X_ii + Eq. 15; mode 1: reading R2, Alg. 1 on Theta_ii + Woodbury)
+ *   or_theta_offblock   PAPER.md:32-34   Eq. 1 off-diagonal block Theta_ij (rows of block i, columns of block j)
+ *   or_lowrank_inverse  NEXT-3 reading R2: (I - K/(1+theta))^-1 ~ I + U diag(s/((1+theta)-s)) U^T, Alg. 1 on K
+ *   or_solve_schur      PAPER.md:127-154 Eqs. 11-14 (NEXT-1): one 2x2 Schur level over pairs of adjacent
+ *                       diagonal blocks, X11^-1, X22^-1, Z1^-1, Z2^-1 by rSVD (reading R2)
  *   or_weight_objective PAPER.md:46-52   P(w) = sum_t f_t^T L f_t + kappa ||w||^2, L = I - Theta(w) (NEXT-4)
  *   or_weight_gradient  PAPER.md:56-58   frozen-degree gradient of P (SPEC.md gradient_frozen)
  *   or_weight_step      PAPER.md:54-58   w <- w - mu grad on the simplex, clamped coordinates stay 0
@@ -566,6 +570,136 @@ void or_apply_woodbury(int32_t m, int32_t k, int32_t T, const double* U, const d
   mm(m, k, T, U, Z, F);                           /* U D U^T Y */
   for (int64_t i = 0; i < (int64_t)m * T; ++i) F[i] = c * (Y[i] + F[i]);
   free(Z);
+}
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-1: the 2x2 Schur-complement inverse (Eqs. 11-14)   */
+/* ------------------------------------------------------------------------ */
+/* Theta_ij[u][v] = dv_u^-1/2 dv_v^-1/2 sum_e H(u,e) w(e)/delta(e) H(v,e), u in block bi, v in block bj. */
+void or_theta_offblock(int32_t b, int32_t bi, int32_t bj, const int64_t* row_ptr, const int32_t* col_idx,
+                       const float* w, const double* dv, const double* de, double* out) {
+  int64_t bu = (int64_t)bi * b, bv = (int64_t)bj * b;
+  for (int32_t u = 0; u < b; ++u)
+    for (int32_t v = 0; v < b; ++v) {
+      int64_t pu = row_ptr[bu + u], eu = row_ptr[bu + u + 1];
+      int64_t pv = row_ptr[bv + v], ev = row_ptr[bv + v + 1];
+      double acc = 0.0;
+      while (pu < eu && pv < ev) {
+        if (col_idx[pu] < col_idx[pv]) ++pu;
+        else if (col_idx[pu] > col_idx[pv]) ++pv;
+        else { int32_t e = col_idx[pu]; acc += (double)w[e] / de[e]; ++pu; ++pv; }
+      }
+      out[(int64_t)u * b + v] = acc / sqrt(dv[bu + u]) / sqrt(dv[bv + v]);
+    }
+}
+
+/* Reading R2 on a general block: for S = I - K/(1+mu) with K symmetric PSD (m x m), Alg. 1 on K
+ * (rank k, q passes, Omega given) gives K ~ U diag(s) U^T and, by Woodbury,
+ *   S^-1 ~ Ainv = I + U diag(s_j / ((1+mu) - s_j)) U^T   (dense m x m out). */
+int or_lowrank_inverse(int32_t m, int32_t k, int32_t q, const double* K, const double* Omega, double mu,
+                       double* Ainv) {
+  double* U = (double*)malloc(sizeof(double) * (size_t)m * k);
+  double* V = (double*)malloc(sizeof(double) * (size_t)m * k);
+  double* sg = (double*)malloc(sizeof(double) * (size_t)k);
+  int st = or_rsvd_block(m, k, q, K, Omega, U, sg, V, NULL, NULL);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      double a = (i == j) ? 1.0 : 0.0;
+      for (int t = 0; t < k; ++t) a += U[(int64_t)i * k + t] * (sg[t] / ((1.0 + mu) - sg[t])) * U[(int64_t)j * k + t];
+      Ainv[(int64_t)i * m + j] = a;
+    }
+  free(U); free(V); free(sg);
+  return st;
+}
+
+/* One level of Eq. 12 on the super-block of diagonal blocks (2s, 2s+1) (reading S1):
+ *   X_s = [[X11, X12], [X21, X22]],  X_ij = delta_ij I - Theta_ij/(1+mu)
+ *   Z1 = X11 - X12 X22^-1 X21,  Z2 = X22 - X21 X11^-1 X12               (Eqs. 13-14)
+ *   X_s^-1 = [[Z1^-1, -X11^-1 X12 Z2^-1], [-Z2^-1 X21 X11^-1, Z2^-1]]   (Eq. 12)
+ * with X11^-1, X22^-1, Z1^-1, Z2^-1 "by randomized SVD", reading R2: each
+ * is I - K/(1+mu) with K PSD -- K11 = Theta11, K_Z1 = Theta11 + Theta12 X22^-1 Theta21/(1+mu)
+ * (since X12 = -Theta12/(1+mu)) -- inverted by or_lowrank_inverse; Omega for X11 and Z1 is
+ * block 2s's rows of the N x k Philox matrix, for X22 and Z2 block 2s+1's (reading S3).
+ * F_s = c X_s^-1 Y_s, c = mu/(1+mu) (Eq. 3).  sel[n_sel] are super-block indices; F is
+ * [n_sel * 2b][T] in sel order. */
+int or_solve_schur(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
+                   double mu, int32_t b, int32_t k, int32_t q, uint64_t seed, const float* Y, int32_t T,
+                   int32_t n_sel, const int32_t* sel, double* F, char* err, int errlen) {
+  if (N <= 0 || E <= 0 || b <= 0 || N % (2 * b) != 0 || k < 1 || k > b || q < 0 || !(mu > 0.0) || T < 0) {
+    set_err(err, errlen, "invalid arguments (need N % 2b == 0, 1 <= k <= b, q >= 0, mu > 0)");
+    return OR_ERR_INVALID;
+  }
+  for (int i = 0; i < n_sel; ++i)
+    if (sel[i] < 0 || sel[i] >= N / (2 * b)) { set_err(err, errlen, "super-block out of range"); return OR_ERR_INVALID; }
+  double* dv = (double*)malloc(sizeof(double) * (size_t)N);
+  double* de = (double*)malloc(sizeof(double) * (size_t)E);
+  int st = or_degrees(N, E, row_ptr, col_idx, w, dv, de, err, errlen);
+  if (st != OR_OK) { free(dv); free(de); return st; }
+  const double c = mu / (1.0 + mu), ip = 1.0 / (1.0 + mu);
+  int fail = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int s = 0; s < n_sel; ++s) {
+    const int i1 = 2 * sel[s], i2 = i1 + 1;
+    size_t bb = (size_t)b * b, bk = (size_t)b * k, bt = (size_t)b * (T > 0 ? T : 1);
+    double *T11 = malloc(sizeof(double) * bb), *T22 = malloc(sizeof(double) * bb), *T12 = malloc(sizeof(double) * bb);
+    double *T21 = malloc(sizeof(double) * bb), *A11 = malloc(sizeof(double) * bb), *A22 = malloc(sizeof(double) * bb);
+    double *Z1i = malloc(sizeof(double) * bb), *Z2i = malloc(sizeof(double) * bb), *W1 = malloc(sizeof(double) * bb);
+    double *K1 = malloc(sizeof(double) * bb), *K2 = malloc(sizeof(double) * bb);
+    double *O1 = malloc(sizeof(double) * bk), *O2 = malloc(sizeof(double) * bk);
+    float* Of = malloc(sizeof(float) * bk);
+    double *Y1 = malloc(sizeof(double) * bt), *Y2 = malloc(sizeof(double) * bt), *G = malloc(sizeof(double) * bt);
+    double *H = malloc(sizeof(double) * bt), *P = malloc(sizeof(double) * bt);
+    or_theta_block(b, i1, row_ptr, col_idx, w, dv, de, 0.0, T11);
+    or_theta_block(b, i2, row_ptr, col_idx, w, dv, de, 0.0, T22);
+    or_theta_offblock(b, i1, i2, row_ptr, col_idx, w, dv, de, T12);
+    or_theta_offblock(b, i2, i1, row_ptr, col_idx, w, dv, de, T21);   /* = T12^T, computed literally */
+    or_gaussian_f32(seed, (int64_t)i1 * b * k, (int64_t)bk, Of);
+    for (size_t i = 0; i < bk; ++i) O1[i] = (double)Of[i];
+    or_gaussian_f32(seed, (int64_t)i2 * b * k, (int64_t)bk, Of);
+    for (size_t i = 0; i < bk; ++i) O2[i] = (double)Of[i];
+    int r = 0;
+    r |= or_lowrank_inverse(b, k, q, T11, O1, mu, A11);                /* X11^-1 */
+    r |= or_lowrank_inverse(b, k, q, T22, O2, mu, A22);                /* X22^-1 */
+    /* K_Z1 = Theta11 + Theta12 X22^-1 Theta21 / (1+mu);  K_Z2 = Theta22 + Theta21 X11^-1 Theta12 / (1+mu) */
+    mm(b, b, b, A22, T21, W1);
+    mm(b, b, b, T12, W1, K1);
+    for (size_t i = 0; i < bb; ++i) K1[i] = T11[i] + ip * K1[i];
+    mm(b, b, b, A11, T12, W1);
+    mm(b, b, b, T21, W1, K2);
+    for (size_t i = 0; i < bb; ++i) K2[i] = T22[i] + ip * K2[i];
+    r |= or_lowrank_inverse(b, k, q, K1, O1, mu, Z1i);                 /* Z1^-1 */
+    r |= or_lowrank_inverse(b, k, q, K2, O2, mu, Z2i);                 /* Z2^-1 */
+    if (r) {
+#pragma omp atomic write
+      fail = OR_ERR_NUMERICAL;
+    }
+    for (int i = 0; i < b; ++i)
+      for (int t = 0; t < T; ++t) {
+        Y1[(int64_t)i * T + t] = (double)Y[((int64_t)i1 * b + i) * T + t];
+        Y2[(int64_t)i * T + t] = (double)Y[((int64_t)i2 * b + i) * T + t];
+      }
+    double* F1 = F + (size_t)s * 2 * b * T;
+    double* F2 = F1 + (size_t)b * T;
+    if (T > 0) {
+      /* top: Z1^-1 Y1 - X11^-1 X12 Z2^-1 Y2 = Z1^-1 Y1 + X11^-1 Theta12 Z2^-1 Y2 / (1+mu) */
+      mm(b, b, T, Z2i, Y2, G);
+      mm(b, b, T, T12, G, H);
+      mm(b, b, T, A11, H, P);
+      mm(b, b, T, Z1i, Y1, G);
+      for (size_t i = 0; i < (size_t)b * T; ++i) F1[i] = c * (G[i] + ip * P[i]);
+      /* bottom: -Z2^-1 X21 X11^-1 Y1 + Z2^-1 Y2 = Z2^-1 (Y2 + Theta21 X11^-1 Y1 / (1+mu)) */
+      mm(b, b, T, A11, Y1, G);
+      mm(b, b, T, T21, G, H);
+      for (size_t i = 0; i < (size_t)b * T; ++i) H[i] = Y2[i] + ip * H[i];
+      mm(b, b, T, Z2i, H, P);
+      for (size_t i = 0; i < (size_t)b * T; ++i) F2[i] = c * P[i];
+    }
+    free(T11); free(T22); free(T12); free(T21); free(A11); free(A22); free(Z1i); free(Z2i); free(W1);
+    free(K1); free(K2); free(O1); free(O2); free(Of); free(Y1); free(Y2); free(G); free(H); free(P);
+  }
+  free(dv); free(de);
+  if (fail) { set_err(err, errlen, "numerical failure in a randomized SVD"); return fail; }
+  return OR_OK;
 }
 
 /* ------------------------------------------------------------------------ */
