@@ -210,6 +210,21 @@ hg_status hg_cg_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t T, int
 hg_status hg_cg_solve(const hg_incidence* H, const float* w, float mu, const float* Y, int32_t T, int32_t max_iter,
                       float tol, float* F, int32_t* iters, float* rel_res, uint32_t flags, int32_t* d_status,
                       void* ws, size_t ws_bytes, hg_stream_t stream);
+/* ---- NEXT-1: one level of the 2x2 Schur-complement inverse (PAPER.md:127-154,
+ * Eqs. 11-14) over super-blocks of two adjacent diagonal blocks (2s, 2s+1), reading S1:
+ *   X_s = [[X11, X12], [X21, X22]],  Z1 = X11 - X12 X22^-1 X21,  Z2 = X22 - X21 X11^-1 X12,
+ *   X_s^-1 = [[Z1^-1, -X11^-1 X12 Z2^-1], [-Z2^-1 X21 X11^-1, Z2^-1]],   F_s = c X_s^-1 Y_s,
+ * with X11^-1, X22^-1, Z1^-1, Z2^-1 "by randomized SVD" in reading R2: each is
+ * I - K/(1+mu) with K PSD (K = Theta_ii; K_Z1 = Theta11 + Theta12 X22^-1 Theta21/(1+mu), ...),
+ * factored by Alg. 1 (rank k, q passes) and inverted by Woodbury.  Omega for X11 and Z1 is block
+ * 2s's rows of the N x k Philox matrix, for X22 and Z2 block 2s+1's (reading S3).
+ *   N % 2b == 0; other sizes as hg_solve; Y, F [N][T]; flags HG_SYNC.
+ * Workspace: hg_schur_workspace_size.  Device errors as hg_solve. */
+hg_status hg_schur_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t b, int32_t k, int32_t T,
+                                  size_t* bytes);
+hg_status hg_solve_schur(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
+                         uint64_t seed, const float* Y, int32_t T, float* F, uint32_t flags, int32_t* d_status,
+                         void* ws, size_t ws_bytes, hg_stream_t stream);
 /* ---- NEXT-4: the hyperedge-weight update with f fixed.
  * P(w) = sum_t f_t^T L f_t + kappa ||w||^2, L = I - Theta(w) (reading N1: the T columns of F are
  * summed).  hg_weight_gradient: the frozen-degree gradient (D_v, D_e held at the current w)

@@ -1144,6 +1144,213 @@ hg_status hg_cg_solve(const hg_incidence* H, const float* w, float mu, const flo
   return HG_OK;
 }
 
+// ---------------------------------------------------------------- NEXT-1
+extern "C++" {
+namespace {
+struct SchurLayout {
+  Layout R;      // degrees, Theta_ii blocks and the rSVD part buffers (offsets into ws)
+  CgLayout C;    // CSC of H, at ws + cg_off
+  size_t cg_off = 0, th12 = 0, ainv = 0, w = 0, kz = 0, utl = 0, sigl = 0, rsl = 0, wt = 0, utz = 0, sigz = 0,
+         rsz = 0, zt = 0, t1 = 0, t2 = 0, total = 0;
+};
+SchurLayout schur_layout(int64_t N, int64_t E, int64_t nnz, int64_t b, int64_t k, int64_t T) {
+  SchurLayout S;
+  S.R = layout(N, E, nnz, b, k, T);
+  S.C = cg_layout(N, E, nnz, 4, 0);
+  size_t off = S.R.total;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + ALIGN - 1) / ALIGN * ALIGN;
+    return o;
+  };
+  const int64_t nb = N / b, ns = nb / 2, Tt = T > 0 ? T : 1;
+  S.cg_off = take(S.C.total);
+  S.th12 = take(4 * ns * b * b);
+  S.ainv = take(4 * nb * b * b);
+  S.w = take(4 * ns * b * b);
+  S.kz = take(4 * nb * b * b);
+  S.utl = take(4 * nb * k * b);
+  S.sigl = take(4 * nb * k);
+  S.rsl = take(4 * nb * k);
+  S.wt = take(4 * nb * k * b);
+  S.utz = take(4 * nb * k * b);
+  S.sigz = take(4 * nb * k);
+  S.rsz = take(4 * nb * k);
+  S.zt = take(4 * ns * k * Tt);
+  S.t1 = take(4 * ns * b * Tt);
+  S.t2 = take(4 * ns * b * Tt);
+  S.total = off;
+  return S;
+}
+}  // namespace
+}  // extern "C++"
+
+hg_status hg_schur_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t b, int32_t k, int32_t T, size_t* bytes) {
+  g_err.clear();
+  if (!bytes) return fail(HG_ERR_INVALID, "bytes is NULL");
+  HG_TRY(check_sizes(N, b, k, 0, T));
+  if (E <= 0 || nnz < 0 || nnz >= INT32_MAX) return fail(HG_ERR_INVALID, "need E > 0 and 0 <= nnz < 2^31");
+  if ((N / b) % 2) return fail(HG_ERR_INVALID, "hg_solve_schur needs an even number of blocks (N %% 2b == 0)");
+  *bytes = schur_layout(N, E, nnz, b, k, T).total;
+  return HG_OK;
+}
+
+hg_status hg_solve_schur(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
+                         uint64_t seed, const float* Y, int32_t T, float* F, uint32_t flags, int32_t* d_status,
+                         void* ws, size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  HG_TRY(check_H(H));
+  HG_TRY(check_sizes(H->n_vertices, b, k, q, T));
+  if (T < 1) return fail(HG_ERR_INVALID, "T must be >= 1");
+  if ((H->n_vertices / b) % 2) return fail(HG_ERR_INVALID, "hg_solve_schur needs N %% 2b == 0");
+  if (!(mu > 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and > 0");
+  if (!w || !Y || !F) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (H->nnz >= INT32_MAX) return fail(HG_ERR_INVALID, "nnz must be < 2^31");
+  if (!d_status && !(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
+  const int64_t N = H->n_vertices, nb = N / b, ns = nb / 2, bb = (int64_t)b * b, kb = (int64_t)k * b,
+                bT = (int64_t)b * T, kT = (int64_t)k * T;
+  const SchurLayout S = schur_layout(N, H->n_edges, H->nnz, b, k, T);
+  HG_TRY(check_ws(ws, ws_bytes, S.total));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int32_t* st = d_status ? d_status : at<int32_t>(ws, S.R.status);
+  if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), s), "memset status");
+  const float opm = 1.0f + mu, ip = 1.0f / opm, c = mu / opm;
+  float* blocks = at<float>(ws, S.R.blocks);
+  float* th12 = at<float>(ws, S.th12);
+  float* ainv = at<float>(ws, S.ainv);
+  float* W = at<float>(ws, S.w);
+  float* KZ = at<float>(ws, S.kz);
+  float* UtL = at<float>(ws, S.utl);
+  float* sigL = at<float>(ws, S.sigl);
+  float* rsL = at<float>(ws, S.rsl);
+  float* Wt = at<float>(ws, S.wt);
+  float* UtZ = at<float>(ws, S.utz);
+  float* sigZ = at<float>(ws, S.sigz);
+  float* rsZ = at<float>(ws, S.rsz);
+  float* Zt = at<float>(ws, S.zt);
+  float* T1 = at<float>(ws, S.t1);
+  float* T2 = at<float>(ws, S.t2);
+  float* Vscratch = at<float>(ws, S.R.Vt);
+  // 1. Theta_ii (raw) and the off-diagonal Theta_{2s,2s+1} from the sorted CSC
+  float* dvr = at<float>(ws, S.R.dvr);
+  HG_TRY(run_degrees(H, w, dvr, st, ws, S.R, s));
+  HG_TRY(run_assemble(H, mu, b, true, 0, (int)nb, blocks, dvr, ws, S.R, s));
+  void* cws = static_cast<char*>(ws) + S.cg_off;
+  CgArgs ca;
+  ca.N = (int)N; ca.E = H->n_edges; ca.nnz = H->nnz; ca.row_ptr = H->row_ptr; ca.col_idx = H->col_idx; ca.w = w;
+  ca.mu = mu; ca.Y = nullptr; ca.T = 4; ca.max_iter = 0; ca.tol = 0.f; ca.F = nullptr; ca.iters_out = nullptr;
+  ca.rel_out = nullptr; ca.status = st; ca.ws = cws;
+  {
+    ProfScope ps(ST_ASSEMBLE, s);
+    HG_CU(launch_csc_setup(ca, s, &g_launches), "CSC");
+    HG_CU(launch_theta_offblock((int)ns, b, H->row_ptr, H->col_idx, at<int32_t>(cws, S.C.col_ptr),
+                                at<int32_t>(cws, S.C.csc), at<float>(cws, S.C.eval), at<float>(cws, S.C.dvr), th12, s,
+                                &g_launches),
+          "off-diagonal Theta");
+  }
+  // 2. leaves: Alg. 1 on Theta_ii, X_ii^-1 ~ I + U diag(s/((1+mu)-s)) U^T (reading R2), materialised
+  const Bufs Bf = part_bufs(ws, S.R, (int)nb, 0, b, k, T);
+  HG_TRY(run_rsvd(blocks, (int)nb, 0, b, k, q, seed, false, UtL, sigL, Vscratch, st, Bf, s));
+  HG_CU(launch_woodbury_scale((int)nb, k, k, sigL, 1.f, opm, rsL, st, s, &g_launches), "woodbury weights");
+  HG_CU(launch_scale_rows((int)nb, k, b, rsL, UtL, Wt, s, &g_launches), "scale rows");
+  auto G = [&](int M, int Nn, int K, int batch) {
+    GemmDesc g;
+    g.M = M; g.N = Nn; g.K = K; g.batch = batch;
+    return g;
+  };
+  {
+    GemmDesc g = G(b, b, k, (int)nb);   // A_ii = W_t^T U_t (+ I below)
+    g.A = Wt; g.a_mn = true; g.lda = b; g.sa = kb;
+    g.B = UtL; g.b_mn = true; g.ldb = b; g.sb = kb;
+    g.D = ainv; g.ldd = b; g.sd = bb;
+    HG_TRY(gemm(g, s, false, "X_ii^-1"));
+  }
+  HG_CU(launch_add_identity((int)nb, b, ainv, s, &g_launches), "identity");
+  // 3. Schur Grams K_Z1 = Theta11 + Theta12 A22 Theta21/(1+mu), K_Z2 = Theta22 + Theta21 A11 Theta12/(1+mu)
+  {
+    GemmDesc g = G(b, b, b, (int)ns);   // W = A22 Theta12^T
+    g.A = ainv + bb; g.a_mn = false; g.lda = b; g.sa = 2 * bb;
+    g.B = th12; g.b_mn = false; g.ldb = b; g.sb = bb;
+    g.D = W; g.ldd = b; g.sd = bb;
+    HG_TRY(gemm(g, s, false, "A22 Theta21"));
+  }
+  {
+    GemmDesc g = G(b, b, b, (int)ns);   // K_Z1 = Theta12 W / (1+mu) + Theta11
+    g.A = th12; g.a_mn = false; g.lda = b; g.sa = bb;
+    g.B = W; g.b_mn = true; g.ldb = b; g.sb = bb;
+    g.D = KZ; g.ldd = b; g.sd = 2 * bb;
+    g.alpha = ip; g.C = blocks; g.ldc = b; g.sc = 2 * bb; g.beta = 1.f;
+    HG_TRY(gemm(g, s, false, "K_Z1"));
+  }
+  {
+    GemmDesc g = G(b, b, b, (int)ns);   // W = A11 Theta12
+    g.A = ainv; g.a_mn = false; g.lda = b; g.sa = 2 * bb;
+    g.B = th12; g.b_mn = true; g.ldb = b; g.sb = bb;
+    g.D = W; g.ldd = b; g.sd = bb;
+    HG_TRY(gemm(g, s, false, "A11 Theta12"));
+  }
+  {
+    GemmDesc g = G(b, b, b, (int)ns);   // K_Z2 = Theta12^T W / (1+mu) + Theta22
+    g.A = th12; g.a_mn = true; g.lda = b; g.sa = bb;
+    g.B = W; g.b_mn = true; g.ldb = b; g.sb = bb;
+    g.D = KZ + bb; g.ldd = b; g.sd = 2 * bb;
+    g.alpha = ip; g.C = blocks + bb; g.ldc = b; g.sc = 2 * bb; g.beta = 1.f;
+    HG_TRY(gemm(g, s, false, "K_Z2"));
+  }
+  HG_CU(launch_symmetrize((int)nb, b, KZ, s, &g_launches), "symmetrize");
+  // 4. Z1^-1, Z2^-1 by Alg. 1 on K_Z (slot 2s: Z1, 2s+1: Z2; Omega keyed by the slot's block)
+  HG_TRY(run_rsvd(KZ, (int)nb, 0, b, k, q, seed, false, UtZ, sigZ, Vscratch, st, Bf, s));
+  HG_CU(launch_woodbury_scale((int)nb, k, k, sigZ, 1.f, opm, rsZ, st, s, &g_launches), "woodbury weights");
+  // 5. apply Eq. 12 to Y_s = [Y1; Y2] (super-block s: rows 2s b .. 2s b + 2b)
+  //    wb: Out = beta (Yin + U D U^T Yin) with Z_t = beta D U^T Yin (GEMM with row scale), Out = U Z_t + beta Yin
+  auto wb = [&](const float* Ut, const float* rs, const float* Yin, int64_t ys, float* Out, int64_t os,
+                float beta) -> hg_status {
+    {
+      GemmDesc g = G(k, T, b, (int)ns);
+      g.A = Ut; g.a_mn = false; g.lda = b; g.sa = 2 * kb;
+      g.B = Yin; g.b_mn = true; g.ldb = T; g.sb = ys;
+      g.D = Zt; g.ldd = T; g.sd = kT;
+      g.rs = rs; g.srs = 2 * k; g.alpha = beta;
+      HG_TRY(gemm(g, s, false, "Schur apply D U^T Y", ST_GEMM_APPLY));
+    }
+    GemmDesc g = G(b, T, k, (int)ns);
+    g.A = Ut; g.a_mn = true; g.lda = b; g.sa = 2 * kb;
+    g.B = Zt; g.b_mn = true; g.ldb = T; g.sb = kT;
+    g.D = Out; g.ldd = T; g.sd = os;
+    g.C = Yin; g.ldc = T; g.sc = ys; g.beta = beta;
+    return gemm(g, s, false, "Schur apply U Z + Y", ST_GEMM_APPLY);
+  };
+  HG_TRY(wb(UtZ + kb, rsZ + k, Y + bT, 2 * bT, T1, bT, 1.f));   // T1 = Z2^-1 Y2
+  {
+    GemmDesc g = G(b, T, b, (int)ns);   // T2 = Theta12 T1
+    g.A = th12; g.a_mn = false; g.lda = b; g.sa = bb;
+    g.B = T1; g.b_mn = true; g.ldb = T; g.sb = bT;
+    g.D = T2; g.ldd = T; g.sd = bT;
+    HG_TRY(gemm(g, s, false, "Theta12 Z2^-1 Y2", ST_GEMM_APPLY));
+  }
+  HG_TRY(wb(UtL, rsL, T2, bT, T1, bT, 1.f));                    // T1 = A11 Theta12 Z2^-1 Y2
+  HG_TRY(wb(UtZ, rsZ, Y, 2 * bT, T2, bT, 1.f));                 // T2 = Z1^-1 Y1
+  HG_CU(launch_axpby((int)ns, bT, c, ip, T2, bT, T1, bT, F, 2 * bT, s, &g_launches), "F1");   // F1
+  HG_TRY(wb(UtL, rsL, Y, 2 * bT, T1, bT, 1.f));                 // T1 = A11 Y1
+  {
+    GemmDesc g = G(b, T, b, (int)ns);   // T2 = Theta21 T1 / (1+mu) + Y2
+    g.A = th12; g.a_mn = true; g.lda = b; g.sa = bb;
+    g.B = T1; g.b_mn = true; g.ldb = T; g.sb = bT;
+    g.D = T2; g.ldd = T; g.sd = bT;
+    g.alpha = ip; g.C = Y + bT; g.ldc = T; g.sc = 2 * bT; g.beta = 1.f;
+    HG_TRY(gemm(g, s, false, "Y2 + Theta21 A11 Y1", ST_GEMM_APPLY));
+  }
+  HG_TRY(wb(UtZ + kb, rsZ + k, T2, bT, F + bT, 2 * bT, c));     // F2 = c Z2^-1 T2
+  if (flags & HG_SYNC) {
+    int32_t h = 0;
+    HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
+    HG_CU(cudaStreamSynchronize(s), "synchronize");
+    if (h) return fail(HG_ERR_NUMERICAL, "device status 0x%x", h);
+  }
+  return HG_OK;
+}
+
 // ---------------------------------------------------------------- NEXT-4
 hg_status hg_weight_gradient(const hg_incidence* H, const float* w, const float* F, int32_t T, float kappa,
                              float* grad, int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream) {

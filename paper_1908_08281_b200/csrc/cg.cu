@@ -847,3 +847,7 @@ cudaError_t launch_weight_step(int E, float* w, int32_t* active, const float* gr
   ++*launches;
   return cudaGetLastError();
 }
+
+cudaError_t launch_csc_setup(const CgArgs& a, cudaStream_t s, int* launches) {
+  return setup_csc(a, cg_layout(a.N, a.E, a.nnz, a.T, 0), s, launches);
+}

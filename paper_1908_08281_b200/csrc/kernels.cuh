@@ -101,3 +101,16 @@ cudaError_t launch_cg(const CgArgs& a, const CgGraphHook* hook, cudaStream_t s, 
 cudaError_t launch_weight_gradient(const CgArgs& a, float kappa, float* grad, cudaStream_t s, int* launches);
 cudaError_t launch_weight_step(int E, float* w, int32_t* active, const float* grad, float mu, int32_t* status,
                                cudaStream_t s, int* launches);
+
+// schur.cu -- NEXT-1: the non-GEMM pieces of one Eq. 12 level
+cudaError_t launch_theta_offblock(int ns, int b, const int64_t* row_ptr, const int32_t* col, const int32_t* col_ptr,
+                                  const int32_t* csc, const float* eval, const float* dvr, float* out, cudaStream_t s,
+                                  int* launches);
+cudaError_t launch_scale_rows(int nb, int k, int b, const float* d, const float* Ut, float* Wt, cudaStream_t s,
+                              int* launches);
+cudaError_t launch_add_identity(int nb, int b, float* A, cudaStream_t s, int* launches);
+cudaError_t launch_symmetrize(int nb, int b, float* K, cudaStream_t s, int* launches);
+cudaError_t launch_axpby(int ns, int64_t len, float c, float g, const float* P, int64_t pp, const float* Q, int64_t pq,
+                         float* F, int64_t pf, cudaStream_t s, int* launches);
+// cg.cu: degrees + the sorted CSC of H (for the off-diagonal assembly); a.ws is a CG workspace
+cudaError_t launch_csc_setup(const CgArgs& a, cudaStream_t s, int* launches);

@@ -70,6 +70,9 @@ _cg_solve = _sig("hg_cg_solve", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f
 _weight_gradient = _sig("hg_weight_gradient", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _P, _i32, _f32, _P, _P,
                         _P, _sz, _P)
 _weight_step = _sig("hg_weight_step", ctypes.c_int, _i32, _P, _P, _P, _f32, _P, _P)
+_schur_ws = _sig("hg_schur_workspace_size", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, _i32, ctypes.POINTER(_sz))
+_solve_schur = _sig("hg_solve_schur", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _i32, _i32, _u64, _P,
+                    _i32, _P, _u32, _P, _P, _sz, _P)
 _last_error = _sig("hg_last_error", ctypes.c_char_p)
 _prof_enable = _sig("hg_profile_enable", ctypes.c_int, _i32)
 _prof_collect = _sig("hg_profile_collect", ctypes.c_int, _i32, _P, _P, _P, ctypes.POINTER(_i32))
@@ -81,7 +84,8 @@ EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_
            "hg_solve", "hg_solve_host", "hg_gemm", "hg_last_error", "hg_last_launch_count", "hg_profile_enable",
            "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve",
            "hg_block_apply_woodbury", "hg_workspace_size_ex", "hg_block_rsvd_ex", "hg_solve_ex",
-           "hg_weight_gradient", "hg_weight_step")
+           "hg_weight_gradient", "hg_weight_step", "hg_schur_workspace_size",
+           "hg_solve_schur")
 
 
 class HGError(RuntimeError):
@@ -375,6 +379,28 @@ def weight_step(w: torch.Tensor, active: torch.Tensor, grad: torch.Tensor, mu: f
     st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=w.device)
     _check(_weight_step(w.numel(), _ptr(w), _ptr(active), _ptr(grad), mu, _ptr(st), _stream(stream)))
     return st
+
+
+def schur_workspace_size(N: int, E: int, nnz: int, b: int, k: int, T: int) -> int:
+    out = _sz(0)
+    _check(_schur_ws(N, E, nnz, b, k, T, ctypes.byref(out)))
+    return int(out.value)
+
+
+def solve_schur(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, b: int, k: int, q: int, seed: int,
+                sync: bool = True, ws: Optional[Workspace] = None, F: Optional[torch.Tensor] = None,
+                status: Optional[torch.Tensor] = None, stream=None):
+    """NEXT-1: one Eq. 12 level over pairs of adjacent blocks (reading R2 inverses): returns F, status."""
+    _dev(w, torch.float32)
+    _dev(Y, torch.float32)
+    N, T = H.N, Y.shape[1]
+    ws = ws or Workspace(schur_workspace_size(N, H.n_edges, H.nnz, b, k, T), Y.device)
+    F = F if F is not None else torch.empty((N, T), dtype=torch.float32, device=Y.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=Y.device)
+    inc = H.c()
+    _check(_solve_schur(ctypes.byref(inc), _ptr(w), mu, b, k, q, seed, _ptr(Y), T, _ptr(F), HG_SYNC if sync else 0,
+                        _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
+    return F, st
 
 
 def incidence_to_device(row_ptr, col_idx, n_edges: int, device="cuda") -> Incidence:
