@@ -459,6 +459,45 @@ def run_ours(args):
                 r2["accuracy_vs_full_solve"] = {"r2": float(np.linalg.norm(Fg2 - Ff) / np.linalg.norm(Ff)),
                                                 "r1": float(np.linalg.norm(Fr1 - Ff) / np.linalg.norm(Ff))}
 
+    # one Eq. 12 Schur level over pairs of adjacent blocks (reading R2 inverses)
+    sch = None
+    if not args.no_schur and c.nb % 2 == 0:
+        sws = hg.Workspace(hg.schur_workspace_size(c.N, h.E, h.nnz, c.b, c.k, c.T), device=dev)
+        Fs = torch.empty((c.N, c.T), dtype=torch.float32, device=dev)
+        for _ in range(2):
+            hg.solve_schur(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, sync=False, ws=sws, F=Fs, status=status,
+                           stream=stream)
+        sch_launches = hg.last_launch_count()
+        torch.cuda.synchronize(dev)
+        n_s = max(3, min(args.steps, 5))
+        h0_, h1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0_.record(stream)
+        for _ in range(n_s):
+            hg.solve_schur(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, sync=False, ws=sws, F=Fs, status=status,
+                           stream=stream)
+        h1_.record(stream)
+        torch.cuda.synchronize(dev)
+        sch_ms = max_over_ranks(h0_.elapsed_time(h1_) / n_s, dev)
+        sch = {"workload": "same H, w, Y, b, k, q; one Eq. 12 level over super-blocks (2s, 2s+1) of 2b, "
+                           "X11^-1, X22^-1, Z1^-1, Z2^-1 by Alg. 1 + Woodbury (reading R2)",
+               "solve_ms": sch_ms, "launches_per_solve": sch_launches, "status": int(status.item())}
+        del sws
+        if rank == 0:
+            import oracle
+            Fo, sel, osec = oracle.solve_schur(h.row_ptr, h.col_idx, h.w, h.Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed,
+                                               superblocks=[0])
+            Fsg = Fs.double().cpu().numpy()
+            rows = slice(0, 2 * c.b)
+            pe = float(np.linalg.norm(Fsg[rows] - Fo) / np.linalg.norm(Fo))
+            sch["parity"] = {"superblocks": sel, "F_rel_fro": pe, "tol": 2e-5, "ok": pe <= 2e-5}
+            Xs = oracle.theta_block(h.row_ptr, h.col_idx, h.w, 2 * c.b, 0, mu=c.mu)
+            ex = c.mu / (1 + c.mu) * np.linalg.solve(Xs, h.Y[rows].astype(np.float64))
+            sch["accuracy_vs_exact_superblock_solve"] = float(np.linalg.norm(Fsg[rows] - ex) / np.linalg.norm(ex))
+            if cg is not None:
+                Ff = Fc.double().cpu().numpy()
+                sch["accuracy_vs_full_solve"] = float(np.linalg.norm(Fsg - Ff) / np.linalg.norm(Ff))
+            sch["oracle_superblock_s"] = osec
+
     # the hyperedge-weight update with f = the CG solution
     wts = None
     if cg is not None and not args.no_weights:
@@ -513,7 +552,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "parity": parity,
         "cpu_baseline": cpu_base,
-        "next_rows": {"cg": cg, "r2_woodbury": r2, "weights": wts},
+        "next_rows": {"cg": cg, "r2_woodbury": r2, "schur": sch, "weights": wts},
         "peaks": {"source": peak_src, "tf32_tflops_sustained": tf32_sust, "tf32_tflops_burst": tf32_burst,
                   "hbm_gbs": peaks["hbm_gbs"]},
     }
@@ -568,6 +607,7 @@ def main(argv=None):
     ap.add_argument("--no-cg", action="store_true", help="skip the CG (NEXT-2) measurement")
     ap.add_argument("--no-r2", action="store_true", help="skip the reading-R2 (NEXT-3) measurement")
     ap.add_argument("--no-weights", action="store_true", help="skip the weight-update (NEXT-4) measurement")
+    ap.add_argument("--no-schur", action="store_true", help="skip the Schur-complement (NEXT-1) measurement")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
