@@ -208,7 +208,7 @@ def test_solve_parity_config4_sampled_blocks(inputs):
     check_against_oracle(h, c, F, sigma, [0, c.nb // 2, c.nb - 1], Ut, Vt)
 
 
-CFG5_SUBSET = [(512, 64, 1), (512, 256, 4), (1024, 128, 2), (1024, 512, 1), (2048, 256, 1)]
+CFG5_SUBSET = [(512, 64, 1), (512, 256, 4), (1024, 128, 2), (1024, 512, 1), (2048, 256, 1), (512, 512, 1)]
 
 
 @pytest.mark.parametrize("b,k,q", CFG5_SUBSET)
@@ -366,3 +366,19 @@ def test_qr_passes_knob_both_parity_green(inputs, cfg, monkeypatch):
     check_against_oracle(h, c, F1, s1, blocks)
     check_against_oracle(h, c, F2, s2, blocks)
     assert rel(F1.double().cpu().numpy(), F2.double().cpu().numpy()) <= 1e-5
+
+
+def test_solve_without_rhs_returns_sigma_only(inputs):
+    """T = 0 (no right-hand sides): the factorisation runs, sigma matches the oracle, F is empty."""
+    hg = hgm()
+    h = inputs(2)
+    c = CONFIGS[2]
+    H, w, _ = dev_inputs(h)
+    Y0 = torch.empty((c.N, 0), dtype=torch.float32, device="cuda")
+    F, sigma, st = hg.solve(H, w, Y0, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    assert int(st.item()) == 0 and F.numel() == 0
+    r = oracle.solve(h.row_ptr, h.col_idx, h.w, np.zeros((c.N, 0), np.float32), mu=c.mu, b=c.b, k=c.k, q=c.q,
+                     seed=c.seed, blocks=[0, c.nb - 1])
+    sg = sigma.double().cpu().numpy()
+    for s_, blk in enumerate(r.blocks):
+        assert np.max(np.abs(sg[blk] - r.sigma[s_]) / r.sigma[s_]) <= SIG_TOL
