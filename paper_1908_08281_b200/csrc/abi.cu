@@ -699,8 +699,9 @@ static int solve_parts() {   // read per call (tests switch it)
 // and their F downloads overlap the later parts' compute (e2e 15.30 -> 14.57 ms at configs[3]).
 // Graphs are instantiated with cudaGraphInstantiateFlagUseNodePriority so the captured
 // priorities hold under replay.  HG_STREAM_PRIO=0/1 forces one set for both entries.
-static cudaStream_t g_aux[2][kMaxParts] = {};
-static cudaEvent_t g_ev_fork = nullptr, g_ev_join[kMaxParts] = {};
+// per host thread (concurrent hg_solve calls from different threads never share events)
+static thread_local cudaStream_t g_aux[2][kMaxParts] = {};
+static thread_local cudaEvent_t g_ev_fork = nullptr, g_ev_join[kMaxParts] = {};
 // library streams / events, created once and outside any stream capture
 static hg_status ensure_streams() {
   if (g_ev_fork) return HG_OK;
@@ -759,7 +760,7 @@ struct HostIO {
 };
 
 static cudaStream_t copy_stream(hg_status* err) {
-  static cudaStream_t cs = nullptr;
+  static thread_local cudaStream_t cs = nullptr;
   if (!cs) {
     cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
@@ -812,13 +813,13 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   cudaStream_t ps[kMaxParts];
   HG_TRY(fork_streams(s, nparts, ps, use_prio_streams(io.F_host != nullptr)));
   // host staging of Y: one slice per part on the copy stream, started before the parts
-  static cudaEvent_t ev_y[kMaxParts] = {};
+  static thread_local cudaEvent_t ev_y[kMaxParts] = {};
   cudaStream_t cps = nullptr;
   if (io.Y_host && T > 0) {
     hg_status err = HG_OK;
     cps = copy_stream(&err);
     if (!cps) return err;
-    static cudaEvent_t ev_cps = nullptr;   // fork the copy stream from `s` (joins a capture)
+    static thread_local cudaEvent_t ev_cps = nullptr;   // fork the copy stream from `s` (joins a capture)
     if (!ev_cps) HG_CU(cudaEventCreateWithFlags(&ev_cps, cudaEventDisableTiming), "event create");
     HG_CU(cudaEventRecord(ev_cps, s), "copy fork record");
     HG_CU(cudaStreamWaitEvent(cps, ev_cps, 0), "copy fork wait");

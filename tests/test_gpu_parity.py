@@ -382,3 +382,38 @@ def test_solve_without_rhs_returns_sigma_only(inputs):
     sg = sigma.double().cpu().numpy()
     for s_, blk in enumerate(r.blocks):
         assert np.max(np.abs(sg[blk] - r.sigma[s_]) / r.sigma[s_]) <= SIG_TOL
+
+
+def test_concurrent_host_threads_distinct_workspaces(inputs):
+    """hg_solve from two host threads at once (distinct workspaces, streams and outputs) gives the
+    single-thread bits: the library's part streams and fork/join events are per host thread."""
+    import threading
+    hg = hgm()
+    h = inputs(2)
+    c = CONFIGS[2]
+    H, w, Y = dev_inputs(h)
+    F0, s0, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    torch.cuda.synchronize()
+    results, errors = {}, []
+
+    def worker(i):
+        try:
+            st = torch.cuda.Stream()
+            ws = hg.Workspace.for_sizes(c.N, h.E, h.nnz, c.b, c.k, c.T)
+            with torch.cuda.stream(st):
+                for _ in range(3):
+                    F, s, status = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed, ws=ws, stream=st)
+            st.synchronize()
+            results[i] = (F, s, int(status.item()))
+        except Exception as e:   # surfaced below
+            errors.append(e)
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for i in range(2):
+        F, s, status = results[i]
+        assert status == 0 and torch.equal(F, F0) and torch.equal(s, s0)
