@@ -751,6 +751,25 @@ static hg_status join_streams(cudaStream_t s, int nparts, const cudaStream_t* ps
   return HG_OK;
 }
 
+// Alg. 1 on nb blocks split into stream parts (as hg_solve's): part p factors its block range with
+// its own part buffers on a forked stream; joined back into s.  Results are those of one run_rsvd
+// over all blocks (Omega is keyed by the global block index).
+static hg_status run_rsvd_parts(const float* X, int nb, int b, int k, int q, uint64_t seed, float* Ut, float* sigma,
+                                float* Vt, int32_t* st, void* ws, const Layout& Lo, int T, cudaStream_t s) {
+  const int nparts = g_prof_mode == 1 ? 1 : std::max(1, std::min(solve_parts(), nb));
+  cudaStream_t ps[kMaxParts];
+  HG_TRY(fork_streams(s, nparts, ps, false));
+  for (int pt = 0; pt < nparts; ++pt) {
+    const int blk0 = (int)((int64_t)nb * pt / nparts), nbp = (int)((int64_t)nb * (pt + 1) / nparts) - blk0;
+    const int64_t kb = (int64_t)blk0 * k * b;
+    g_cur_part = pt;
+    HG_TRY(run_rsvd(X + (int64_t)blk0 * b * b, nbp, blk0, b, k, q, seed, false, Ut + kb, sigma + (int64_t)blk0 * k,
+                    Vt + kb, st, part_bufs(ws, Lo, nb, blk0, b, k, T), ps[pt]));
+  }
+  g_cur_part = 0;
+  return join_streams(s, nparts, ps);
+}
+
 // Host staging for hg_solve_host: Y's rows are uploaded per part on a library copy
 // stream (the part waits only before its apply, so the upload overlaps the rSVD) and each
 // part downloads its F rows right after its apply (overlapping the other parts' work).
@@ -1196,26 +1215,11 @@ hg_status hg_schur_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t b, 
   return HG_OK;
 }
 
-hg_status hg_solve_schur(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
-                         uint64_t seed, const float* Y, int32_t T, float* F, uint32_t flags, int32_t* d_status,
-                         void* ws, size_t ws_bytes, hg_stream_t stream) {
-  g_err.clear();
-  g_launches = 0;
-  HG_TRY(check_H(H));
-  HG_TRY(check_sizes(H->n_vertices, b, k, q, T));
-  if (T < 1) return fail(HG_ERR_INVALID, "T must be >= 1");
-  if ((H->n_vertices / b) % 2) return fail(HG_ERR_INVALID, "hg_solve_schur needs N %% 2b == 0");
-  if (!(mu > 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and > 0");
-  if (!w || !Y || !F) return fail(HG_ERR_INVALID, "NULL pointer argument");
-  if (H->nnz >= INT32_MAX) return fail(HG_ERR_INVALID, "nnz must be < 2^31");
-  if (!d_status && !(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
+static hg_status schur_impl(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
+                            uint64_t seed, const float* Y, int32_t T, float* F, int32_t* st, void* ws,
+                            const SchurLayout& S, cudaStream_t s) {
   const int64_t N = H->n_vertices, nb = N / b, ns = nb / 2, bb = (int64_t)b * b, kb = (int64_t)k * b,
                 bT = (int64_t)b * T, kT = (int64_t)k * T;
-  const SchurLayout S = schur_layout(N, H->n_edges, H->nnz, b, k, T);
-  HG_TRY(check_ws(ws, ws_bytes, S.total));
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  int32_t* st = d_status ? d_status : at<int32_t>(ws, S.R.status);
-  if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), s), "memset status");
   const float opm = 1.0f + mu, ip = 1.0f / opm, c = mu / opm;
   float* blocks = at<float>(ws, S.R.blocks);
   float* th12 = at<float>(ws, S.th12);
@@ -1251,8 +1255,7 @@ hg_status hg_solve_schur(const hg_incidence* H, const float* w, float mu, int32_
           "off-diagonal Theta");
   }
   // 2. leaves: Alg. 1 on Theta_ii, X_ii^-1 ~ I + U diag(s/((1+mu)-s)) U^T (reading R2), materialised
-  const Bufs Bf = part_bufs(ws, S.R, (int)nb, 0, b, k, T);
-  HG_TRY(run_rsvd(blocks, (int)nb, 0, b, k, q, seed, false, UtL, sigL, Vscratch, st, Bf, s));
+  HG_TRY(run_rsvd_parts(blocks, (int)nb, b, k, q, seed, UtL, sigL, Vscratch, st, ws, S.R, T, s));
   HG_CU(launch_woodbury_scale((int)nb, k, k, sigL, 1.f, opm, rsL, st, s, &g_launches), "woodbury weights");
   HG_CU(launch_scale_rows((int)nb, k, b, rsL, UtL, Wt, s, &g_launches), "scale rows");
   auto G = [&](int M, int Nn, int K, int batch) {
@@ -1301,7 +1304,7 @@ hg_status hg_solve_schur(const hg_incidence* H, const float* w, float mu, int32_
   }
   HG_CU(launch_symmetrize((int)nb, b, KZ, s, &g_launches), "symmetrize");
   // 4. Z1^-1, Z2^-1 by Alg. 1 on K_Z (slot 2s: Z1, 2s+1: Z2; Omega keyed by the slot's block)
-  HG_TRY(run_rsvd(KZ, (int)nb, 0, b, k, q, seed, false, UtZ, sigZ, Vscratch, st, Bf, s));
+  HG_TRY(run_rsvd_parts(KZ, (int)nb, b, k, q, seed, UtZ, sigZ, Vscratch, st, ws, S.R, T, s));
   HG_CU(launch_woodbury_scale((int)nb, k, k, sigZ, 1.f, opm, rsZ, st, s, &g_launches), "woodbury weights");
   // 5. apply Eq. 12 to Y_s = [Y1; Y2] (super-block s: rows 2s b .. 2s b + 2b)
   //    wb: Out = beta (Yin + U D U^T Yin) with Z_t = beta D U^T Yin (GEMM with row scale), Out = U Z_t + beta Yin
@@ -1343,6 +1346,40 @@ hg_status hg_solve_schur(const hg_incidence* H, const float* w, float mu, int32_
     HG_TRY(gemm(g, s, false, "Y2 + Theta21 A11 Y1", ST_GEMM_APPLY));
   }
   HG_TRY(wb(UtZ + kb, rsZ + k, T2, bT, F + bT, 2 * bT, c));     // F2 = c Z2^-1 T2
+  return HG_OK;
+}
+
+hg_status hg_solve_schur(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
+                         uint64_t seed, const float* Y, int32_t T, float* F, uint32_t flags, int32_t* d_status,
+                         void* ws, size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  HG_TRY(check_H(H));
+  HG_TRY(check_sizes(H->n_vertices, b, k, q, T));
+  if (T < 1) return fail(HG_ERR_INVALID, "T must be >= 1");
+  if ((H->n_vertices / b) % 2) return fail(HG_ERR_INVALID, "hg_solve_schur needs N %% 2b == 0");
+  if (!(mu > 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and > 0");
+  if (!w || !Y || !F) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (H->nnz >= INT32_MAX) return fail(HG_ERR_INVALID, "nnz must be < 2^31");
+  if (!d_status && !(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
+  const SchurLayout S = schur_layout(H->n_vertices, H->n_edges, H->nnz, b, k, T);
+  HG_TRY(check_ws(ws, ws_bytes, S.total));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int32_t* st = d_status ? d_status : at<int32_t>(ws, S.R.status);
+  if (graphs_enabled(s) && !g_prof_on) {
+    std::string key = "schur|" + knob_env();
+    key_add(key, *H);
+    key_add(key, w); key_add(key, mu); key_add(key, b); key_add(key, k); key_add(key, q); key_add(key, seed);
+    key_add(key, Y); key_add(key, T); key_add(key, F); key_add(key, st); key_add(key, ws); key_add(key, ws_bytes);
+    key_add(key, solve_parts());
+    HG_TRY(graph_run(key, s, [&](cudaStream_t cs) -> hg_status {
+      if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), cs), "memset status");
+      return schur_impl(H, w, mu, b, k, q, seed, Y, T, F, st, ws, S, cs);
+    }));
+  } else {
+    if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), s), "memset status");
+    HG_TRY(schur_impl(H, w, mu, b, k, q, seed, Y, T, F, st, ws, S, s));
+  }
   if (flags & HG_SYNC) {
     int32_t h = 0;
     HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
