@@ -320,6 +320,12 @@ def test_deterministic_and_host_entry(inputs):
     assert torch.equal(Fh, F1.cpu()) and torch.equal(sh, s1.cpu())
     F3, _, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=1)
     assert not torch.equal(F1, F3)
+    # reading R2 through the host entry (prioritised part streams) gives the device entry's bits
+    Fw, sw, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0, woodbury=True)
+    Fhw, shw = hg.solve_host(torch.from_numpy(h.row_ptr), torch.from_numpy(h.col_idx), torch.from_numpy(h.w),
+                             torch.from_numpy(h.Y).pin_memory(), mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0,
+                             woodbury=True)
+    assert torch.equal(Fhw, Fw.cpu()) and torch.equal(shw, sw.cpu())
 
 
 def test_simt_verification_path_agrees(inputs):
