@@ -302,7 +302,17 @@ __device__ __forceinline__ void assemble_rows_walk(int b, int nu, int nseg, int6
 #pragma unroll
           for (int sg = 0; sg < NSEG_MAX; ++sg) {
             if (sg >= nseg) break;
-            for (int m = rg[sg].x; m < rg[sg].y; ++m) stage[d++] = K[m];
+            const int m0 = rg[sg].x, m1 = rg[sg].y;
+            int m = m0;
+            for (; m + 8 <= m1; m += 8) {   // eight independent loads in flight per lane
+              uint32_t x[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) x[i] = K[m + i];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) stage[d + i] = x[i];
+              d += 8;
+            }
+            for (; m < m1; ++m) stage[d++] = K[m];
           }
         }
         __syncwarp();
