@@ -34,4 +34,6 @@ for i, v in enumerate(clk):
         nm = f"panel {p} " + ("start" if ph == 0 else ("trsm done" if ph == 1 else "update done"))
     if nm is None and 42 <= i < 60:
         nm = f"trtri col {i - 42}"
+    if nm is None:
+        nm = f"stamp {i}"
     print(f"{i:3d} {nm:22s} {v - t0:9d}")
