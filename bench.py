@@ -13,7 +13,9 @@ all ranks; the per-block inputs (256 MiB of X blocks, 250 MiB of Y) exceed the
 
 One JSON line on rank 0.  Ranks (torchrun) run
 independent problems (Omega seed = rank): weak scaling, no collective on the
-data path; the step time is the max over ranks.
+data path; the step time is the max over ranks.  --shard: one problem, rank r
+solves its contiguous block range (hg_solve_blocks) and F is all-gathered
+(strong scaling; the e2e key then times the full problem per rank).
 
 --impl reference times the FP64 CPU oracle (oracle/, the stand-in reference:
 there is no reference implementation, only the paper) on a bounded sample of
@@ -62,6 +64,30 @@ def max_over_ranks(x: float, device=None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def shard_range(nb: int, rank: int, world: int):
+    """Contiguous diagonal-block range [begin, begin + count) of one rank:
+    blocks are independent, so a problem shards over ranks with no collective on the data path."""
+    b0 = nb * rank // world
+    return b0, nb * (rank + 1) // world - b0
+
+
+def allgather_rows(F_local, row0: int, nrows: int, world: int):
+    """The optional exchange of a sharded solve: every rank's F rows [row0, row0 + nrows) gathered
+    into the full F on every rank (NCCL over NVLink on GPUs; gloo in the CPU tests)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return F_local[row0:row0 + nrows]
+    counts = [None] * world
+    dist.all_gather_object(counts, (row0, nrows))
+    mx = max(n for _, n in counts)   # collectives need equal sizes: pad to the largest share
+    mine = torch.zeros((mx, F_local.shape[1]), dtype=F_local.dtype, device=F_local.device)
+    mine[:nrows] = F_local[row0:row0 + nrows]
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    return torch.cat([parts[r][:n] for r, (_, n) in enumerate(counts)], 0)
 
 
 # ---------------------------------------------------------------- clocks
@@ -185,7 +211,10 @@ def run_ours(args):
 
     c = workload_config(args)
     h = make_input(c)
-    seed = rank                                     # independent problem per rank
+    # default: an independent problem per rank (weak scaling); --shard: ONE problem, rank r solves
+    # its contiguous block range (hg_solve_blocks) and F is all-gathered (strong scaling)
+    shard = bool(args.shard) and world > 1
+    seed = 0 if shard else rank
     H = hg.incidence_to_device(h.row_ptr, h.col_idx, h.E, device=dev)
     w = torch.from_numpy(h.w).to(dev)
     Y = torch.from_numpy(h.Y).to(dev)
@@ -195,9 +224,17 @@ def run_ours(args):
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    sb0, scnt = shard_range(c.nb, rank, world) if shard else (0, c.nb)
+    sig_sh = torch.empty((scnt, c.k), dtype=torch.float32, device=dev)
+
     def step():
-        hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, sync=False, ws=ws, F=F, sigma=sigma,
-                 status=status, stream=stream)
+        if shard:
+            hg.solve_blocks(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, blk_begin=sb0, blk_count=scnt,
+                            sync=False, ws=ws, F=F, sigma=sig_sh, status=status, stream=stream)
+            allgather_rows(F, sb0 * c.b, scnt * c.b, world)
+        else:
+            hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, sync=False, ws=ws, F=F, sigma=sigma,
+                     status=status, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -217,7 +254,7 @@ def run_ours(args):
     barrier()
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms_local, dev)
-    value = world * c.nb / (ms / 1e3)
+    value = (c.nb if shard else world * c.nb) / (ms / 1e3)
 
     # per-stage attribution: the same steps with per-stage CUDA events on the stream
     hg.debug_counters(reset=True)
@@ -538,7 +575,7 @@ def run_ours(args):
     out = {
         "metric": "diag_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config_json(c),
         "solve_ms": ms, "blocks_per_s_per_gpu": c.nb / (ms / 1e3),
         "gemm_useful_tflops": gemm_useful_tflops,
@@ -608,6 +645,9 @@ def main(argv=None):
     ap.add_argument("--no-r2", action="store_true", help="skip the reading-R2 (NEXT-3) measurement")
     ap.add_argument("--no-weights", action="store_true", help="skip the weight-update (NEXT-4) measurement")
     ap.add_argument("--no-schur", action="store_true", help="skip the Schur-complement (NEXT-1) measurement")
+    ap.add_argument("--shard", action="store_true",
+                    help="N > 1: one problem sharded by block ranges over the ranks + an all-gather of F "
+                         "(strong scaling) instead of an independent problem per rank (weak scaling)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

@@ -176,6 +176,16 @@ hg_status hg_solve_ex(const hg_incidence* H, const float* w, float mu, int32_t b
                       uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags,
                       int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
 
+/* hg_solve restricted to the diagonal blocks [blk_begin, blk_begin + blk_count) -- one rank's
+ * share of a problem sharded over GPUs (blocks are independent, so ranks
+ * need no collective; the optional exchange is an all-gather of F).  Y and F are the full
+ * [N][T] arrays: only the range's rows are read / written.  sigma_out [blk_count][k] or NULL.
+ * Results are bitwise those of hg_solve for the same blocks (Omega is keyed by the global
+ * block index). */
+hg_status hg_solve_blocks(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
+                          uint64_t seed, int32_t blk_begin, int32_t blk_count, const float* Y, int32_t T, float* F,
+                          float* sigma_out, uint32_t flags, int32_t* d_status, void* ws, size_t ws_bytes,
+                          hg_stream_t stream);
 /* hg_solve from HOST buffers (end-to-end entry): copies row_ptr, col_idx, w, Y
  * host->device, solves, copies F (and sigma_host if non-NULL) device->host,
  * synchronises.  ws (device) is caller-provided as above; host buffers should

@@ -790,10 +790,12 @@ static cudaStream_t copy_stream(hg_status* err) {
   return cs;
 }
 
+// Blocks [rb0, rb0 + rcnt) of the N/b diagonal blocks (rcnt < 0: all); F rows of other blocks are
+// not touched; sigma_out, when given, is [rcnt][k].
 static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t p,
                             int32_t q, uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out,
                             uint32_t flags, int32_t* d_status, void* ws, size_t ws_bytes, cudaStream_t s,
-                            const HostIO& io = HostIO()) {
+                            const HostIO& io = HostIO(), int32_t rb0 = 0, int32_t rcnt = -1) {
   HG_TRY(check_H(H));
   if (p < 0 || p % 4) return fail(HG_ERR_INVALID, "oversampling p must be >= 0 and a multiple of 4 (p=%d)", p);
   const int32_t l = k + p;   // Alg. 1 width; the apply uses the top k triplets
@@ -812,10 +814,16 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), s), "memset status");
   }
   const int nb = H->n_vertices / b;
+  if (rcnt < 0) { rb0 = 0; rcnt = nb; }
+  if (rb0 < 0 || rcnt < 1 || rb0 + rcnt > nb)
+    return fail(HG_ERR_INVALID, "block range [%d, %d) outside [0, %d)", rb0, rb0 + rcnt, nb);
   float* blocks = at<float>(ws, Lo.blocks);
   float* Ut = at<float>(ws, Lo.Ut);
   float* Vt = at<float>(ws, Lo.Vt);
-  float* sigma = (sigma_out && p == 0) ? sigma_out : at<float>(ws, p == 0 ? Lo.sigma : Lo.sigl);   // [nb][l]
+  // sigma of global block i at sigma + (i - soff) l: the caller's [rcnt][k] array, or the workspace's [nb][l]
+  const bool sig_user = sigma_out && p == 0;
+  float* sigma = sig_user ? sigma_out : at<float>(ws, p == 0 ? Lo.sigma : Lo.sigl);
+  const int soff = sig_user ? rb0 : 0;
   float* dvr = at<float>(ws, Lo.dvr);
   HG_TRY(run_degrees(H, w, dvr, st, ws, Lo, s));
   // Blocks are independent (reading A5): the assembly, rSVD and apply of disjoint block ranges run
@@ -823,7 +831,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   // part's latency-bound Cholesky / Jacobi leave idle.  Bitwise the same result for
   // any part count (Omega is keyed by the global block index).  One part while the
   // stage profiler is on (per-stage attribution needs sequential stages).
-  const int nparts = g_prof_mode == 1 ? 1 : std::max(1, std::min(solve_parts(), nb));
+  const int nparts = g_prof_mode == 1 ? 1 : std::max(1, std::min(solve_parts(), rcnt));
   if (g_prof_mode == 2 && !g_t0_set) {
     if (!g_t0) HG_CU(cudaEventCreate(&g_t0), "event create");
     prof_record(g_t0, s);
@@ -843,7 +851,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     HG_CU(cudaEventRecord(ev_cps, s), "copy fork record");
     HG_CU(cudaStreamWaitEvent(cps, ev_cps, 0), "copy fork wait");
     for (int pt = 0; pt < nparts; ++pt) {
-      const int64_t r0 = (int64_t)nb * pt / nparts * b, r1 = (int64_t)nb * (pt + 1) / nparts * b;
+      const int64_t r0 = (rb0 + (int64_t)rcnt * pt / nparts) * b, r1 = (rb0 + (int64_t)rcnt * (pt + 1) / nparts) * b;
       if (!ev_y[pt]) HG_CU(cudaEventCreateWithFlags(&ev_y[pt], cudaEventDisableTiming), "event create");
       HG_CU(cudaMemcpyAsync(const_cast<float*>(Y) + r0 * T, io.Y_host + r0 * T, sizeof(float) * (size_t)(r1 - r0) * T,
                             cudaMemcpyHostToDevice, cps),
@@ -852,15 +860,17 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     }
   }
   for (int pt = 0; pt < nparts; ++pt) {
-    const int blk0 = (int)((int64_t)nb * pt / nparts), nbp = (int)((int64_t)nb * (pt + 1) / nparts) - blk0;
+    const int blk0 = rb0 + (int)((int64_t)rcnt * pt / nparts);
+    const int nbp = rb0 + (int)((int64_t)rcnt * (pt + 1) / nparts) - blk0;
     const int64_t kb = (int64_t)blk0 * l * b;
     const Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, l, T);
     g_cur_part = pt;
     HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[pt]));
-    HG_TRY(run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, l, q, seed, simt, Ut + kb, sigma + (int64_t)blk0 * l,
+    HG_TRY(run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, l, q, seed, simt, Ut + kb,
+                    sigma + (int64_t)(blk0 - soff) * l,
                     Vt + kb, st, Bf, ps[pt], scheme));
     if (cps) HG_CU(cudaStreamWaitEvent(ps[pt], ev_y[pt], 0), "wait Y");
-    HG_TRY(run_apply(Ut + kb, sigma + (int64_t)blk0 * l, Vt + kb, nbp, b, k, T > 0 ? Y + (int64_t)blk0 * b * T : Y, T,
+    HG_TRY(run_apply(Ut + kb, sigma + (int64_t)(blk0 - soff) * l, Vt + kb, nbp, b, k, T > 0 ? Y + (int64_t)blk0 * b * T : Y, T,
                      mu / (1.0f + mu), T > 0 ? F + (int64_t)blk0 * b * T : F, st, Bf, ps[pt], simt,
                      woodbury ? 1.0f + mu : 0.f, l));
     if (io.F_host && T > 0)
@@ -870,9 +880,9 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   }
   g_cur_part = 0;
   HG_TRY(join_streams(s, nparts, ps));
-  if (p > 0 && sigma_out)   // rank-k truncation of the oversampled sigma [nb][l] -> [nb][k]
-    HG_CU(cudaMemcpy2DAsync(sigma_out, 4 * (size_t)k, sigma, 4 * (size_t)l, 4 * (size_t)k, nb, cudaMemcpyDeviceToDevice,
-                            s), "truncate sigma");
+  if (p > 0 && sigma_out)   // rank-k truncation of the oversampled sigma [nb][l] -> [rcnt][k]
+    HG_CU(cudaMemcpy2DAsync(sigma_out, 4 * (size_t)k, sigma + (int64_t)rb0 * l, 4 * (size_t)l, 4 * (size_t)k, rcnt,
+                            cudaMemcpyDeviceToDevice, s), "truncate sigma");
   if (flags & HG_SYNC) {
     int32_t h = 0;
     HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
@@ -962,14 +972,16 @@ hg_status graph_run(const std::string& key, cudaStream_t s, Fn enqueue) {
 }  // namespace
 }  // extern "C++"
 
-hg_status hg_solve_ex(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t p, int32_t q,
-                      uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags,
-                      int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream) {
+extern "C++" static hg_status solve_entry(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k,
+                                          int32_t p, int32_t q, uint64_t seed, const float* Y, int32_t T, float* F,
+                                          float* sigma_out, uint32_t flags, int32_t* d_status, void* ws,
+                                          size_t ws_bytes, hg_stream_t stream, int32_t rb0, int32_t rcnt) {
   g_err.clear();
   g_launches = 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (!graphs_enabled(s))
-    return solve_impl(H, w, mu, b, k, p, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes, s);
+    return solve_impl(H, w, mu, b, k, p, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes, s, HostIO(),
+                      rb0, rcnt);
   // host-side validation first (nothing is captured for an invalid call)
   HG_TRY(check_H(H));
   if (p < 0 || p % 4) return fail(HG_ERR_INVALID, "oversampling p must be >= 0 and a multiple of 4 (p=%d)", p);
@@ -977,15 +989,19 @@ hg_status hg_solve_ex(const hg_incidence* H, const float* w, float mu, int32_t b
   const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, k + p, T);
   HG_TRY(check_ws(ws, ws_bytes, Lo.h_rowptr));
   if (!d_status && !(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
+  if (rcnt >= 0 && (rb0 < 0 || rcnt < 1 || rb0 + rcnt > H->n_vertices / b))
+    return fail(HG_ERR_INVALID, "block range [%d, %d) outside [0, %d)", rb0, rb0 + rcnt, H->n_vertices / b);
   int32_t* st = d_status ? d_status : at<int32_t>(ws, Lo.status);
   std::string key = "solve|" + knob_env();
+  key_add(key, rb0); key_add(key, rcnt);
   key_add(key, *H);
   key_add(key, w); key_add(key, mu); key_add(key, b); key_add(key, k); key_add(key, p); key_add(key, q); key_add(key, seed);
   key_add(key, Y); key_add(key, T); key_add(key, F); key_add(key, sigma_out); key_add(key, flags & ~HG_SYNC);
   key_add(key, st); key_add(key, ws); key_add(key, ws_bytes); key_add(key, solve_parts());
   HG_TRY(graph_run(key, s, [&](cudaStream_t cs) -> hg_status {
     if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), cs), "memset status");
-    return solve_impl(H, w, mu, b, k, p, q, seed, Y, T, F, sigma_out, flags & ~HG_SYNC, st, ws, ws_bytes, cs);
+    return solve_impl(H, w, mu, b, k, p, q, seed, Y, T, F, sigma_out, flags & ~HG_SYNC, st, ws, ws_bytes, cs,
+                      HostIO(), rb0, rcnt);
   }));
   if (flags & HG_SYNC) {
     int32_t h = 0;
@@ -995,6 +1011,24 @@ hg_status hg_solve_ex(const hg_incidence* H, const float* w, float mu, int32_t b
                        "Cholesky breakdown, 8 Jacobi cap, 16 singular sigma, 32 non-finite)", h);
   }
   return HG_OK;
+}
+
+hg_status hg_solve_ex(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t p, int32_t q,
+                      uint64_t seed, const float* Y, int32_t T, float* F, float* sigma_out, uint32_t flags,
+                      int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream) {
+  return solve_entry(H, w, mu, b, k, p, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes, stream, 0, -1);
+}
+
+hg_status hg_solve_blocks(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
+                          uint64_t seed, int32_t blk_begin, int32_t blk_count, const float* Y, int32_t T, float* F,
+                          float* sigma_out, uint32_t flags, int32_t* d_status, void* ws, size_t ws_bytes,
+                          hg_stream_t stream) {
+  if (blk_count < 1) {
+    g_err.clear();
+    return fail(HG_ERR_INVALID, "blk_count must be >= 1");
+  }
+  return solve_entry(H, w, mu, b, k, 0, q, seed, Y, T, F, sigma_out, flags, d_status, ws, ws_bytes, stream, blk_begin,
+                     blk_count);
 }
 
 hg_status hg_solve(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q, uint64_t seed,

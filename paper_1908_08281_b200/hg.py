@@ -56,6 +56,8 @@ _block_rsvd_ex = _sig("hg_block_rsvd_ex", ctypes.c_int, _P, _i32, _i32, _i32, _i
                       _P, _sz, _P)
 _solve_ex = _sig("hg_solve_ex", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _i32, _i32, _i32, _u64, _P,
                  _i32, _P, _P, _u32, _P, _P, _sz, _P)
+_solve_blocks = _sig("hg_solve_blocks", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _i32, _i32, _u64,
+                     _i32, _i32, _P, _i32, _P, _P, _u32, _P, _P, _sz, _P)
 _block_woodbury = _sig("hg_block_apply_woodbury", ctypes.c_int, _P, _P, _i32, _i32, _i32, _P, _i32, _f32, _P, _P,
                        _P, _sz, _P)
 _solve = _sig("hg_solve", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _i32, _i32, _u64, _P, _i32, _P,
@@ -85,7 +87,7 @@ EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_
            "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve",
            "hg_block_apply_woodbury", "hg_workspace_size_ex", "hg_block_rsvd_ex", "hg_solve_ex",
            "hg_weight_gradient", "hg_weight_step", "hg_schur_workspace_size",
-           "hg_solve_schur")
+           "hg_solve_schur", "hg_solve_blocks")
 
 
 class HGError(RuntimeError):
@@ -301,6 +303,24 @@ def solve(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, b: int, 
     else:
         _check(_solve(ctypes.byref(inc), _ptr(w), mu, b, k, q, seed, _ptr(Y), T, _ptr(F), _ptr(sigma), flags,
                       _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
+    return F, sigma, st
+
+
+def solve_blocks(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, b: int, k: int, q: int, seed: int,
+                 blk_begin: int, blk_count: int, sync: bool = True, ws: Optional[Workspace] = None,
+                 F: Optional[torch.Tensor] = None, sigma: Optional[torch.Tensor] = None,
+                 status: Optional[torch.Tensor] = None, stream=None):
+    """hg_solve on blocks [blk_begin, blk_begin + blk_count) (one rank's share); F is the full [N][T]."""
+    _dev(w, torch.float32)
+    _dev(Y, torch.float32)
+    N, T = H.N, Y.shape[1]
+    ws = ws or Workspace.for_sizes(N, H.n_edges, H.nnz, b, k, T)
+    F = F if F is not None else torch.zeros((N, T), dtype=torch.float32, device=Y.device)
+    sigma = sigma if sigma is not None else torch.empty((blk_count, k), dtype=torch.float32, device=Y.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=Y.device)
+    inc = H.c()
+    _check(_solve_blocks(ctypes.byref(inc), _ptr(w), mu, b, k, q, seed, blk_begin, blk_count, _ptr(Y), T, _ptr(F),
+                         _ptr(sigma), HG_SYNC if sync else 0, _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
     return F, sigma, st
 
 

@@ -69,3 +69,39 @@ def test_reference_arm_json_line(monkeypatch, capsys):
     line = json.loads(capsys.readouterr().out.strip())
     assert line["impl"] == "reference" and line["unit"] == "blocks/s" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "oracle" and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _shard_worker(rank, world, port, q):
+    os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    import torch
+    import bench
+    import torch.distributed as dist
+    bench.dist_setup("gloo")
+    nb, b, T = 7, 4, 3
+    b0, cnt = bench.shard_range(nb, rank, world)
+    # each rank fills only its blocks' rows of F (as hg_solve_blocks does); the all-gather assembles F
+    F = torch.zeros(nb * b, T)
+    F[b0 * b:(b0 + cnt) * b] = torch.arange(b0 * b * T, (b0 + cnt) * b * T, dtype=torch.float32).reshape(-1, T)
+    full = bench.allgather_rows(F, b0 * b, cnt * b, world)
+    q.put((rank, b0, cnt, full.numpy().tolist()))
+    dist.destroy_process_group()
+
+
+def test_sharded_blocks_and_allgather_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    # disjoint contiguous ranges covering every block
+    assert [(x[1], x[2]) for x in res] == [(0, 3), (3, 4)]
+    import numpy as np
+    want = np.arange(7 * 4 * 3, dtype=np.float32).reshape(-1, 3)
+    for x in res:
+        assert np.array_equal(np.array(x[3], np.float32), want)

@@ -423,3 +423,24 @@ def test_concurrent_host_threads_distinct_workspaces(inputs):
     for i in range(2):
         F, s, status = results[i]
         assert status == 0 and torch.equal(F, F0) and torch.equal(s, s0)
+
+
+def test_solve_blocks_shards_equal_full_solve(inputs):
+    """hg_solve_blocks on disjoint block ranges (one rank's share each) reproduces hg_solve's bits."""
+    import bench
+    hg = hgm()
+    h = inputs(2)
+    c = CONFIGS[2]
+    H, w, Y = dev_inputs(h)
+    F0, s0, _ = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    F = torch.zeros_like(F0)
+    sig = []
+    for r in range(3):
+        b0, cnt = bench.shard_range(c.nb, r, 3)
+        _, s, st = hg.solve_blocks(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed, blk_begin=b0, blk_count=cnt,
+                                   F=F)
+        assert int(st.item()) == 0
+        sig.append(s)
+    assert torch.equal(F, F0) and torch.equal(torch.cat(sig, 0), s0)
+    with pytest.raises(hg.HGError):
+        hg.solve_blocks(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed, blk_begin=c.nb - 1, blk_count=2)
