@@ -122,3 +122,17 @@ def test_cg_full_size_sampled_columns():
     o5 = oracle.cg_solve(h.row_ptr, h.col_idx, h.w, np.ascontiguousarray(h.Y[:, cols]), mu=CONFIGS[i].mu,
                          max_iter=5, tol=0.0)
     assert rel(F5[:, cols], o5.F) <= F_TOL
+
+
+def test_cg_flags_isolated_vertex_and_empty_edge():
+    hg = hgm()
+    rp = np.array([0, 2, 3, 4, 4], np.int64)    # vertex 3 isolated; hyperedge 2 empty
+    ci = np.array([0, 1, 0, 1], np.int32)
+    H = hg.incidence_to_device(rp, ci, 3)
+    w = torch.ones(3, device="cuda")
+    with pytest.raises(hg.HGError) as e:
+        hg.cg_solve(H, w, torch.ones(4, 4, device="cuda"), mu=1.0, max_iter=5, tol=0.0)
+    assert e.value.status == hg.HG_ERR_NUMERICAL
+    _, st = hg.weight_gradient(H, w, torch.ones(4, 4, device="cuda"), kappa=1.0)
+    torch.cuda.synchronize()
+    assert int(st.item()) & 1 and int(st.item()) & 2
