@@ -27,19 +27,20 @@ def csr(edges_of_vertex):
 
 
 def test_objective_spec_examples():
-    # SPEC.md objective: f = 0 -> kappa ||w||^2
+    # SPEC.md:387 objective: f = 0 -> kappa ||w||^2
     rp, ci = csr([[0, 1], [0, 2], [0, 3]])          # 3 vertices, edge 0 holds all, edges 1-3
     w = np.array([0.4, 0.3, 0.2, 0.1], np.float32)
     assert oracle.weight_objective(rp, ci, w, np.zeros(3), kappa=2.0) == pytest.approx(2.0 * np.sum(w.astype(float) ** 2))
-    # 2-vertex / 1-edge toy, w = (1), f = (1, -1), kappa = 0 -> 2
+    # SPEC.md:388 2-vertex / 1-edge toy, w = (1), f = (1, -1), kappa = 0 -> 2
     rp2, ci2 = csr([[0], [0]])
     assert oracle.weight_objective(rp2, ci2, np.ones(1, np.float32), np.array([1.0, -1.0]), kappa=0.0) == pytest.approx(2.0)
-    # n = 4, w = (1, 0, 0, 0), kappa = 1, f = 0 -> 1 (every vertex lies on edge 0, so degrees stay positive)
+    # SPEC.md:389 n = 4, w = (1, 0, 0, 0), kappa = 1, f = 0 -> 1 (every vertex lies on edge 0)
     w4 = np.array([1, 0, 0, 0], np.float32)
     assert oracle.weight_objective(rp, ci, w4, np.zeros(3), kappa=1.0) == pytest.approx(1.0)
 
 
 def test_gradient_spec_examples():
+    # SPEC.md:396 (f = 0 -> 2 kappa w) and SPEC.md:397 (toy, f = (1, 1), w = (1), kappa = 0 -> -2)
     rp, ci = csr([[0, 1], [0, 2], [0, 3]])
     w = np.array([0.4, 0.3, 0.2, 0.1], np.float32)
     np.testing.assert_allclose(oracle.weight_gradient(rp, ci, w, np.zeros(3), kappa=1.5), 3.0 * w.astype(float))
@@ -79,6 +80,7 @@ def test_gradient_matches_finite_differences():
 
 
 def test_step_spec_examples():
+    # SPEC.md:406, 407 (n = 2 cases), SPEC.md:405 (constant gradient annihilated)
     w, a = oracle.weight_step([0.5, 0.5], [0, 0], [1.0, -1.0], 0.1)
     np.testing.assert_allclose(w, [0.4, 0.6], atol=1e-15)
     w, a = oracle.weight_step([0.05, 0.95], [0, 0], [1.0, -1.0], 0.1)
@@ -99,7 +101,7 @@ def test_step_invariants_and_large_kappa_uniform():
         w, a = oracle.weight_step(w, a, rng.standard_normal(E), 0.05)
         assert abs(w.sum() - 1.0) <= 1e-12 and w.min() >= 0.0
         assert np.all(w[a == 1] == 0.0)
-    # kappa -> infinity: gradient 2 kappa w, step 0.25/kappa halves the distance to uniform
+    # SPEC.md:414 kappa -> infinity: gradient 2 kappa w, step 0.25/kappa halves the distance to uniform
     h = make_tiny(8, 4, 2, 1, K=2, n_tag=3)
     E = len(h.w)
     w = h.w.astype(np.float64) / h.w.sum()
