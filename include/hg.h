@@ -251,6 +251,12 @@ hg_status hg_weight_gradient(const hg_incidence* H, const float* w, const float*
                              float* grad, int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
 hg_status hg_weight_step(int32_t E, float* w, int32_t* active, const float* grad, float mu, int32_t* d_status,
                          hg_stream_t stream);
+/* The objective P(w) = sum_t f_t^T L f_t + kappa ||w||^2 at the w the gradient was taken at (degrees
+ * from w): since P is linear in w at fixed degrees apart from the penalty,
+ *   P(w) = ||F||^2 + w^T grad(w) - kappa ||w||^2   (grad from hg_weight_gradient at the same w).
+ *   F [N][T]; out: one fp64 (device); ws: >= 296 doubles of device scratch.  Fixed-order sums. */
+hg_status hg_weight_objective(const float* F, int32_t N, int32_t T, int32_t E, const float* w, const float* grad,
+                              float kappa, double* out, void* ws, size_t ws_bytes, hg_stream_t stream);
 /* Verification export of the batched GEMM the path runs on (3xTF32 on
  * tcgen05, or fp32 CUDA cores with HG_GEMM_SIMT):
  *   for g < batch: D_g(m,n) = alpha * rs_g[m] * cs_g[n] * sum_kk A_g(m,kk) B_g(kk,n)

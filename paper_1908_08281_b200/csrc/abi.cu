@@ -1443,6 +1443,19 @@ hg_status hg_weight_gradient(const hg_incidence* H, const float* w, const float*
   return HG_OK;
 }
 
+hg_status hg_weight_objective(const float* F, int32_t N, int32_t T, int32_t E, const float* w, const float* grad,
+                              float kappa, double* out, void* ws, size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (N <= 0 || T < 0 || E <= 0) return fail(HG_ERR_INVALID, "need N > 0, T >= 0, E > 0");
+  if (!F || !w || !grad || !out) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  HG_TRY(check_ws(ws, ws_bytes, 296 * sizeof(double)));
+  HG_CU(launch_weight_objective((int64_t)N * T, F, E, w, grad, kappa, static_cast<double*>(ws), out,
+                                reinterpret_cast<cudaStream_t>(stream), &g_launches),
+        "weight objective");
+  return HG_OK;
+}
+
 hg_status hg_weight_step(int32_t E, float* w, int32_t* active, const float* grad, float mu, int32_t* d_status,
                          hg_stream_t stream) {
   g_err.clear();

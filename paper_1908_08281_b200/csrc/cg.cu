@@ -645,6 +645,37 @@ __global__ void __launch_bounds__(1024) k_weight_step(int E, float* __restrict__
   }
 }
 
+// P(w) = ||F||^2 - sum_e (w_e/delta(e)) sum_t s_{e,t}^2 + kappa ||w||^2 from the gradient at the same
+// w: w_e (2 kappa w_e - grad_e) = w_e sum_t s^2 / delta(e), so P = ||F||^2 + w^T grad - kappa ||w||^2.
+// Fixed-order fp64 sums: per-CTA partials, then one CTA adds them in order.
+__global__ void __launch_bounds__(256) k_wobj_partial(int64_t nF, const float* __restrict__ F, int E,
+                                                      const float* __restrict__ w, const float* __restrict__ grad,
+                                                      float kappa, double* __restrict__ part) {
+  __shared__ double sm[8];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nF; i += (int64_t)gridDim.x * blockDim.x)
+    acc += (double)F[i] * (double)F[i];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+    acc += (double)w[e] * (double)grad[e] - (double)kappa * (double)w[e] * (double)w[e];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(~0u, acc, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t += sm[i];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_wobj_final(int n, const double* __restrict__ part, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += part[i];
+    *out = t;
+  }
+}
+
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
 }  // namespace
@@ -850,4 +881,14 @@ cudaError_t launch_weight_step(int E, float* w, int32_t* active, const float* gr
 
 cudaError_t launch_csc_setup(const CgArgs& a, cudaStream_t s, int* launches) {
   return setup_csc(a, cg_layout(a.N, a.E, a.nnz, a.T, 0), s, launches);
+}
+
+// out[0] = P(w) (fp64, device) from grad = the frozen-degree gradient at w; part: >= 296 doubles scratch
+cudaError_t launch_weight_objective(int64_t nF, const float* F, int E, const float* w, const float* grad, float kappa,
+                                    double* part, double* out, cudaStream_t s, int* launches) {
+  constexpr int NB = 296;   // 2 CTAs per SM
+  k_wobj_partial<<<NB, 256, 0, s>>>(nF, F, E, w, grad, kappa, part);
+  k_wobj_final<<<1, 32, 0, s>>>(NB, part, out);
+  *launches += 2;
+  return cudaGetLastError();
 }

@@ -114,3 +114,5 @@ cudaError_t launch_axpby(int ns, int64_t len, float c, float g, const float* P, 
                          float* F, int64_t pf, cudaStream_t s, int* launches);
 // cg.cu: degrees + the sorted CSC of H (for the off-diagonal assembly); a.ws is a CG workspace
 cudaError_t launch_csc_setup(const CgArgs& a, cudaStream_t s, int* launches);
+cudaError_t launch_weight_objective(int64_t nF, const float* F, int E, const float* w, const float* grad, float kappa,
+                                    double* part, double* out, cudaStream_t s, int* launches);

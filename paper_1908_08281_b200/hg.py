@@ -71,6 +71,7 @@ _cg_solve = _sig("hg_cg_solve", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f
                  _u32, _P, _P, _sz, _P)
 _weight_gradient = _sig("hg_weight_gradient", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _P, _i32, _f32, _P, _P,
                         _P, _sz, _P)
+_weight_objective = _sig("hg_weight_objective", ctypes.c_int, _P, _i32, _i32, _i32, _P, _P, _f32, _P, _P, _sz, _P)
 _weight_step = _sig("hg_weight_step", ctypes.c_int, _i32, _P, _P, _P, _f32, _P, _P)
 _schur_ws = _sig("hg_schur_workspace_size", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, _i32, ctypes.POINTER(_sz))
 _solve_schur = _sig("hg_solve_schur", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _i32, _i32, _u64, _P,
@@ -87,7 +88,7 @@ EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_
            "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve",
            "hg_block_apply_woodbury", "hg_workspace_size_ex", "hg_block_rsvd_ex", "hg_solve_ex",
            "hg_weight_gradient", "hg_weight_step", "hg_schur_workspace_size",
-           "hg_solve_schur", "hg_solve_blocks")
+           "hg_solve_schur", "hg_solve_blocks", "hg_weight_objective")
 
 
 class HGError(RuntimeError):
@@ -421,6 +422,45 @@ def solve_schur(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, b:
     _check(_solve_schur(ctypes.byref(inc), _ptr(w), mu, b, k, q, seed, _ptr(Y), T, _ptr(F), HG_SYNC if sync else 0,
                         _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
     return F, st
+
+
+def weight_objective(F: torch.Tensor, w: torch.Tensor, grad: torch.Tensor, *, kappa: float, stream=None) -> float:
+    """P(w) = ||F||^2 + w^T grad - kappa ||w||^2 (grad from weight_gradient at this w), computed on the device."""
+    for t in (F, w, grad):
+        _dev(t, torch.float32)
+    out = torch.zeros(1, dtype=torch.float64, device=F.device)
+    scratch = torch.empty(296, dtype=torch.float64, device=F.device)
+    _check(_weight_objective(_ptr(F), F.shape[0], F.shape[1], w.numel(), _ptr(w), _ptr(grad), kappa, _ptr(out),
+                             _ptr(scratch), scratch.numel() * 8, _stream(stream)))
+    return float(out.item())
+
+
+def learn_weights(H: Incidence, w0: torch.Tensor, F: torch.Tensor, *, kappa: float, mu: float, steps: int,
+                  ws: Optional[Workspace] = None):
+    """NEXT-4 driver (SPEC.md learn_weights): with F fixed, `steps` accepted simplex steps of steepest descent
+    on P(w); a step that increases P is rejected and mu halved.  Every step runs in the library's kernels
+    (gradient, step, objective); this loop only decides accept / reject.  Returns (w, active, trace of P, mu)."""
+    N, T = F.shape
+    ws = ws or Workspace(cg_workspace_size(N, H.n_edges, H.nnz, T, 0), F.device)
+    w = (w0 / w0.sum()).contiguous()
+    active = torch.zeros(H.n_edges, dtype=torch.int32, device=F.device)
+    g, st = weight_gradient(H, w, F, kappa=kappa, ws=ws)
+    P = weight_objective(F, w, g, kappa=kappa)
+    trace = [P]
+    done, tries = 0, 0
+    while done < steps and tries < 8 * steps:
+        tries += 1
+        w_try, a_try = w.clone(), active.clone()
+        st = weight_step(w_try, a_try, g, mu)
+        g_try, st2 = weight_gradient(H, w_try, F, kappa=kappa, ws=ws)
+        P_try = weight_objective(F, w_try, g_try, kappa=kappa)
+        if int(st.item()) != 0 or int(st2.item()) != 0 or not (P_try <= P):
+            mu *= 0.5
+            continue
+        w, active, g, P = w_try, a_try, g_try, P_try
+        trace.append(P)
+        done += 1
+    return w, active, trace, mu
 
 
 def incidence_to_device(row_ptr, col_idx, n_edges: int, device="cuda") -> Incidence:

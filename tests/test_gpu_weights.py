@@ -105,3 +105,48 @@ def test_weight_step_with_clamping_matches_oracle():
     assert 0 < ao.sum() < h.E
     assert np.array_equal(a.cpu().numpy(), ao)
     assert np.max(np.abs(w.double().cpu().numpy() - wo)) <= 1e-6 * np.max(wo) + 1e-9
+
+
+def oracle_learn(h, w0, F, kappa, mu, steps):
+    w = w0 / w0.sum()
+    a = np.zeros(len(w), np.int32)
+    g = oracle.weight_gradient(h.row_ptr, h.col_idx, w.astype(np.float32), F, kappa=kappa)
+    P = oracle.weight_objective(h.row_ptr, h.col_idx, w.astype(np.float32), F, kappa=kappa)
+    trace, done, tries = [P], 0, 0
+    while done < steps and tries < 8 * steps:
+        tries += 1
+        wt, at = oracle.weight_step(w, a, g, mu)
+        try:
+            gt = oracle.weight_gradient(h.row_ptr, h.col_idx, wt.astype(np.float32), F, kappa=kappa)
+            Pt = oracle.weight_objective(h.row_ptr, h.col_idx, wt.astype(np.float32), F, kappa=kappa)
+        except oracle.OracleError:
+            mu *= 0.5
+            continue
+        if not Pt <= P:
+            mu *= 0.5
+            continue
+        w, a, g, P = wt, at, gt, Pt
+        trace.append(P)
+        done += 1
+    return w, a, trace
+
+
+def test_weight_objective_and_learn_loop_match_oracle():
+    hg = hgm()
+    h, H, w0, Y = get(1)
+    c = CONFIGS[1]
+    F, _, _, _ = hg.cg_solve(H, w0, Y, mu=c.mu, max_iter=30, tol=1e-6)
+    Fh = F.double().cpu().numpy()
+    kappa = 0.5
+    w = (w0 / w0.sum()).contiguous()
+    g, _ = hg.weight_gradient(H, w, F, kappa=kappa)
+    P = hg.weight_objective(F, w, g, kappa=kappa)
+    Po = oracle.weight_objective(h.row_ptr, h.col_idx, w.cpu().numpy(), Fh, kappa=kappa)
+    assert abs(P - Po) <= 1e-5 * abs(Po)
+    wg, ag, trace, _ = hg.learn_weights(H, w0, F, kappa=kappa, mu=1e-4, steps=6)
+    wo, ao, traceo = oracle_learn(h, h.w.astype(np.float64), Fh, kappa, 1e-4, 6)
+    assert len(trace) == len(traceo) == 7
+    assert all(trace[i + 1] <= trace[i] for i in range(6))
+    np.testing.assert_allclose(trace, traceo, rtol=1e-5)
+    assert np.array_equal(ag.cpu().numpy(), ao)
+    assert np.max(np.abs(wg.double().cpu().numpy() - wo)) <= 1e-5 * np.max(wo)

@@ -112,3 +112,16 @@ def test_step_invariants_and_large_kappa_uniform():
         g = oracle.weight_gradient(h.row_ptr, h.col_idx, w.astype(np.float32), F, kappa=kappa)
         w, a = oracle.weight_step(w, a, g, 0.25 / kappa)
     np.testing.assert_allclose(w, 1.0 / E, atol=1e-3)
+
+
+def test_objective_gradient_identity():
+    # P is linear in w at fixed degrees apart from the penalty, so at the gradient's own w:
+    # P(w) = ||F||^2 + w^T grad(w) - kappa ||w||^2  (the identity hg_weight_objective uses)
+    h = make_tiny(8, 4, 2, 1, K=2, n_tag=3)
+    rng = np.random.default_rng(12)
+    F = rng.standard_normal((8, 3))
+    for kappa in (0.0, 0.7):
+        g = oracle.weight_gradient(h.row_ptr, h.col_idx, h.w, F, kappa=kappa)
+        w = h.w.astype(np.float64)
+        P = oracle.weight_objective(h.row_ptr, h.col_idx, h.w, F, kappa=kappa)
+        assert P == pytest.approx(np.sum(F * F) + w @ g - kappa * w @ w, rel=1e-12)
