@@ -463,6 +463,27 @@ def learn_weights(H: Incidence, w0: torch.Tensor, F: torch.Tensor, *, kappa: flo
     return w, active, trace, mu
 
 
+def adaptive_learning(H: Incidence, w0: torch.Tensor, Y: torch.Tensor, *, mu: float, kappa: float, outer: int = 2,
+                      weight_steps: int = 5, step: float = 1e-4, solver: str = "cg", b: int = 0, k: int = 0,
+                      q: int = 0, seed: int = 0, cg_tol: float = 1e-6, cg_max_iter: int = 100):
+    """The paper's alternation (Table 2): solve Eq. 3 for F with the current w (the CG of
+    PAPER.md:165-178, or the block rSVD path with solver="rsvd"), then update w with F fixed
+    (learn_weights), `outer` times.  Returns (F, w, history) with history[i] = (P before, P after) of
+    outer pass i.  Composition of library calls only."""
+    w = (w0 / w0.sum()).contiguous()
+    hist = []
+    F = None
+    for _ in range(outer):
+        if solver == "cg":
+            F, _, _, _ = cg_solve(H, w, Y, mu=mu, max_iter=cg_max_iter, tol=cg_tol)
+        else:
+            F, _, _ = solve(H, w, Y, mu=mu, b=b, k=k, q=q, seed=seed)
+        w_new, _, trace, step = learn_weights(H, w, F, kappa=kappa, mu=step, steps=weight_steps)
+        hist.append((trace[0], trace[-1]))
+        w = w_new
+    return F, w, hist
+
+
 def incidence_to_device(row_ptr, col_idx, n_edges: int, device="cuda") -> Incidence:
     return Incidence(torch.as_tensor(row_ptr, dtype=torch.int64).to(device).contiguous(),
                      torch.as_tensor(col_idx, dtype=torch.int32).to(device).contiguous(), int(n_edges))
