@@ -97,3 +97,31 @@ def test_woodbury_accuracy_vs_exact_block_solve():
         X = oracle.theta_block(h.row_ptr, h.col_idx, h.w, c.b, blk, mu=c.mu)
         ex = c.mu / (1 + c.mu) * np.linalg.solve(X, h.Y[blk * c.b:(blk + 1) * c.b].astype(float))
         assert rel(Fg[blk * c.b:(blk + 1) * c.b], ex) <= 5e-2
+
+
+def test_woodbury_rank_deficient_theta_blocks():
+    """Degenerate case: Theta_ii of rank 2 < k (every vertex of a block lies on the same two
+    hyperedges).  Alg. 1's extra directions carry sigma ~ 0, so their Woodbury weights vanish and F is
+    still determined; the GPU's shifted CholeskyQR must not break down or produce non-finite values."""
+    hg = hgm()
+    b, nblk, T = 16, 2, 4
+    rows = []
+    for blk in range(nblk):
+        for v in range(b):
+            es = [2 * blk] + ([2 * blk + 1] if v < b // 2 else [])
+            rows.append(es)
+    rp = np.array([0] + list(np.cumsum([len(r) for r in rows])), np.int64)
+    ci = np.array([e for r in rows for e in r], np.int32)
+    w = np.array([1.0, 0.5, 1.5, 1.0], np.float32)
+    Y = np.random.default_rng(0).integers(0, 2, (b * nblk, T)).astype(np.float32)
+    H = hg.incidence_to_device(rp, ci, 4)
+    F, sigma, st = hg.solve(H, torch.from_numpy(w).cuda(), torch.from_numpy(Y).cuda(), mu=1.0, b=b, k=8, q=1,
+                            seed=0, woodbury=True)
+    assert int(st.item()) == 0 and bool(torch.isfinite(F).all())
+    r = oracle.solve(rp, ci, w, Y, mu=1.0, b=b, k=8, q=1, seed=0, woodbury=True)
+    assert rel(F.double().cpu().numpy(), r.F) <= F_TOL
+    # exact: Theta_ii has rank 2 <= k, so the Woodbury inverse is exact (the block solve)
+    for blk in range(nblk):
+        X = oracle.theta_block(rp, ci, w, b, blk, mu=1.0)
+        ex = 0.5 * np.linalg.solve(X, Y[blk * b:(blk + 1) * b].astype(float))
+        assert rel(F[blk * b:(blk + 1) * b].double().cpu().numpy(), ex) <= F_TOL
