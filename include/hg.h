@@ -8,7 +8,15 @@
  *   2. hg_block_rsvd           per block, Alg. 1 with l = k, pi = q
  *   3. hg_block_apply_inverse  F_i = scale * V_i Sigma_i^-1 U_i^T Y_i      (Eq. 3,
  *                                                                           PAPER.md:160-163 Eq. 15)
- *   hg_solve = 1 -> 2 -> 3 from the CSR incidence to F.
+ *   hg_solve = 1 -> 2 -> 3 from the CSR incidence to F (hg_solve_host: from host buffers;
+ *   hg_solve_blocks: one block range, a rank's share of a sharded problem).
+ *
+ * Beyond the hot path (each against the same FP64 oracle):
+ *   hg_solve_ex / hg_block_rsvd_ex  oversampling l = k + p, Eq. 10 scheme
+ *   HG_WOODBURY, hg_block_apply_woodbury  reading R2: Alg. 1 on Theta_ii
+ *   hg_solve_schur                  one 2x2 Schur level, Eqs. 11-14
+ *   hg_cg_solve                     CG on Eq. 5, Eqs. 16-20
+ *   hg_weight_gradient / _step / _objective  the hyperedge-weight update
  *
  * Conventions for every entry point:
  *   - Pointers are DEVICE pointers owned by the caller unless a name says
@@ -17,7 +25,9 @@
  *   - Work is enqueued on `stream` and is asynchronous unless stated.  The
  *     library never allocates device memory on these calls: scratch comes
  *     from the caller's workspace `ws` (size from hg_workspace_size, 256-byte
- *     aligned).  Distinct workspaces make concurrent calls thread-safe.
+ *     aligned; CG / Schur entries have their own size queries).  Distinct
+ *     workspaces make concurrent calls thread-safe (the library's part
+ *     streams and events are per host thread).
  *   - Host-side validation failures return HG_ERR_INVALID synchronously and
  *     enqueue nothing.  Data-dependent failures found on the device are OR-ed
  *     as bit flags into the caller's device word *d_status (0 = ok; the
