@@ -78,17 +78,26 @@ __global__ void k_add_identity(int nb, int b, float* __restrict__ A) {
   A[(blk * b + r) * b + r] += 1.f;
 }
 
-// K = (K + K^T)/2 per b x b block; thread (r, c) with r < c writes both entries
-__global__ void k_symmetrize(int b, float* __restrict__ K) {
-  float* Kb = K + (size_t)blockIdx.y * b * b;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)b * b;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(i / b), c = (int)(i % b);
-    if (r < c) {
-      const float v = 0.5f * (Kb[(size_t)r * b + c] + Kb[(size_t)c * b + r]);
-      Kb[(size_t)r * b + c] = v;
-      Kb[(size_t)c * b + r] = v;
-    }
+// K = (K + K^T)/2 per b x b block: CTA per pair of mirrored 32 x 32 tiles (ti <= tj), both staged in
+// shared memory so every global access is a coalesced row segment
+__global__ void __launch_bounds__(256) k_symmetrize(int b, float* __restrict__ K) {
+  __shared__ float A[32][33], B[32][33];
+  const int ti = blockIdx.x, tj = blockIdx.y;
+  if (ti > tj) return;
+  float* Kb = K + (size_t)blockIdx.z * b * b;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    const int gi = ti * 32 + r, gj = tj * 32 + r;
+    A[r][tx] = (gi < b && tj * 32 + tx < b) ? Kb[(size_t)gi * b + tj * 32 + tx] : 0.f;   // tile (ti, tj)
+    B[r][tx] = (gj < b && ti * 32 + tx < b) ? Kb[(size_t)gj * b + ti * 32 + tx] : 0.f;   // tile (tj, ti)
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int gi = ti * 32 + r, gj = tj * 32 + r;
+    const float v = 0.5f * (A[r][tx] + B[tx][r]);      // (ti*32 + r, tj*32 + tx)
+    const float u = 0.5f * (B[r][tx] + A[tx][r]);      // (tj*32 + r, ti*32 + tx)
+    if (gi < b && tj * 32 + tx < b) Kb[(size_t)gi * b + tj * 32 + tx] = v;
+    if (gj < b && ti * 32 + tx < b) Kb[(size_t)gj * b + ti * 32 + tx] = u;
   }
 }
 
@@ -134,8 +143,8 @@ cudaError_t launch_add_identity(int nb, int b, float* A, cudaStream_t s, int* la
 }
 
 cudaError_t launch_symmetrize(int nb, int b, float* K, cudaStream_t s, int* launches) {
-  const dim3 grid((unsigned)std::min<int64_t>(((int64_t)b * b + 255) / 256, 256), nb);
-  k_symmetrize<<<grid, 256, 0, s>>>(b, K);
+  const int nt = (b + 31) / 32;
+  k_symmetrize<<<dim3(nt, nt, nb), 256, 0, s>>>(b, K);
   ++*launches;
   return cudaGetLastError();
 }
