@@ -528,46 +528,53 @@ __global__ void __launch_bounds__(NT) k_cg_out(CgDev d, float* __restrict__ Fo, 
 __global__ void __launch_bounds__(NT) k_wgrad_items(int T, int Tp, const float* __restrict__ F,
                                                     const float* __restrict__ dvr, const int32_t* __restrict__ csc,
                                                     const int4* __restrict__ items, const int32_t* __restrict__ totals,
-                                                    const int32_t* __restrict__ de, const float* __restrict__ w,
-                                                    float kappa, float* __restrict__ part, float* __restrict__ grad) {
+                                                    float* __restrict__ part, double* __restrict__ sqpart) {
+  // grid (items, column chunks of 128): the chunk is the slow dimension, so the CTAs in flight
+  // gather rows of one 512-byte-wide column slice of F, which stays in L2
   const int lane = threadIdx.x & 31;
   const int item = blockIdx.x * NW + (threadIdx.x >> 5);
   if (item >= totals[0]) return;
   const int4 it = items[item];
-  double sq = 0.0;
-  for (int c0 = 0; c0 < T; c0 += 128) {
-    const int c = c0 + 4 * lane;
-    const bool on = c < T;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int base = it.y; base < it.z; base += 32) {
-      const int j = base + lane;
-      const int myv = j < it.z ? csc[j] : 0;
-      const float myr = j < it.z ? dvr[myv] : 0.f;
-      const int cnt = min(32, it.z - base);
-      for (int u0 = 0; u0 < cnt; u0 += 8) {
-        float4 x[8];
-        float r[8];
+  const int c = blockIdx.y * 128 + 4 * lane;
+  const bool on = c < T;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int base = it.y; base < it.z; base += 32) {
+    const int j = base + lane;
+    const int myv = j < it.z ? csc[j] : 0;
+    const float myr = j < it.z ? dvr[myv] : 0.f;
+    const int cnt = min(32, it.z - base);
+    for (int u0 = 0; u0 < cnt; u0 += 8) {
+      float4 x[8];
+      float r[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int v = __shfl_sync(~0u, myv, (u0 + u) & 31);
-          r[u] = __shfl_sync(~0u, myr, (u0 + u) & 31);
-          x[u] = (on && u0 + u < cnt) ? __ldg(reinterpret_cast<const float4*>(F + (size_t)v * T + c))
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc = f4_fma(r[u], x[u], acc);
+      for (int u = 0; u < 8; ++u) {
+        const int v = __shfl_sync(~0u, myv, (u0 + u) & 31);
+        r[u] = __shfl_sync(~0u, myr, (u0 + u) & 31);
+        x[u] = (on && u0 + u < cnt) ? __ldg(reinterpret_cast<const float4*>(F + (size_t)v * T + c))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-    }
-    if (it.w >= 0) {
-      if (on) *reinterpret_cast<float4*>(part + (size_t)it.w * Tp + c) = acc;
-    } else {
-      sq += (double)acc.x * acc.x + (double)acc.y * acc.y + (double)acc.z * acc.z + (double)acc.w * acc.w;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = f4_fma(r[u], x[u], acc);
     }
   }
-  if (it.w < 0) {
+  if (it.w >= 0) {
+    if (on) *reinterpret_cast<float4*>(part + (size_t)it.w * Tp + c) = acc;
+  } else {
+    double sq = (double)acc.x * acc.x + (double)acc.y * acc.y + (double)acc.z * acc.z + (double)acc.w * acc.w;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(~0u, sq, o);
-    if (lane == 0) grad[it.x] = (float)(-sq / (double)de[it.x] + 2.0 * (double)kappa * (double)w[it.x]);
+    if (lane == 0) sqpart[(size_t)it.x * gridDim.y + blockIdx.y] = sq;
+  }
+}
+
+// single-chunk edges: grad_e from the per-chunk sums of squares, added in chunk order
+__global__ void k_wgrad_small(int E, int nch, const int32_t* __restrict__ de, const float* __restrict__ w, float kappa,
+                              const double* __restrict__ sqpart, float* __restrict__ grad) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    if (de[e] > CH || de[e] == 0) continue;   // multi-chunk edges: k_wgrad_big
+    double sq = 0.0;
+    for (int ch = 0; ch < nch; ++ch) sq += sqpart[(size_t)e * nch + ch];
+    grad[e] = (float)(-sq / (double)de[e] + 2.0 * (double)kappa * (double)w[e]);
   }
 }
 
@@ -718,6 +725,7 @@ CgLayout cg_layout(int64_t N, int64_t E, int64_t nnz, int64_t T, int64_t max_ite
   L.R = take(vec);
   L.F = take(vec);
   L.XP = take(vec);
+  L.sqpart = take(8 * (size_t)E * ((T + 127) / 128));   // weight gradient: per-edge, per-chunk sums
   L.Q = take(4 * (size_t)ns * E * TS);
   L.part = take(4 * (size_t)ns * max_slots * TS);
   L.red = take(4 * (size_t)ns * nparts * TS);
@@ -862,13 +870,17 @@ cudaError_t launch_weight_gradient(const CgArgs& a, float kappa, float* grad, cu
   cudaError_t e = setup_csc(a, L, s, launches);
   if (e != cudaSuccess) return e;
   const int Tp = L.ns * L.TS;   // partial-slot pitch (the CG partial buffer holds max_slots x Tp)
-  k_wgrad_items<<<(unsigned)((L.max_items + NW - 1) / NW), NT, 0, s>>>(
+  const int nch = (a.T + 127) / 128;
+  double* sqpart = at<double>(a.ws, L.sqpart);   // [E][nch]
+  k_wgrad_items<<<dim3((unsigned)((L.max_items + NW - 1) / NW), nch), NT, 0, s>>>(
       a.T, Tp, a.F, at<float>(a.ws, L.dvr), at<int32_t>(a.ws, L.csc), at<int4>(a.ws, L.items),
-      at<int32_t>(a.ws, L.totals), at<int32_t>(a.ws, L.de), a.w, kappa, at<float>(a.ws, L.part), grad);
+      at<int32_t>(a.ws, L.totals), at<float>(a.ws, L.part), sqpart);
+  k_wgrad_small<<<(unsigned)std::min<int64_t>((a.E + 255) / 256, 148 * 8), 256, 0, s>>>(
+      a.E, nch, at<int32_t>(a.ws, L.de), a.w, kappa, sqpart, grad);
   k_wgrad_big<<<(unsigned)((L.max_big + NW - 1) / NW), NT, 0, s>>>(
       a.T, Tp, at<int4>(a.ws, L.bigs), at<int32_t>(a.ws, L.totals), at<int32_t>(a.ws, L.de), a.w, kappa,
       at<float>(a.ws, L.part), grad);
-  *launches += 2;
+  *launches += 3;
   return cudaGetLastError();
 }
 

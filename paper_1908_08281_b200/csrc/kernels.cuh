@@ -82,7 +82,7 @@ struct CgLayout {
   int TS, ns, nparts;
   int64_t max_items, max_big;
   size_t de, eval, dvr, col_ptr, item_ptr, slot_ptr, big_ptr, cursor, totals, csc_tmp, csc, items, bigs;
-  size_t P, R, F, XP, Q, part, red, rr, rr0, alpha, beta, active, iters, ctl, status, total;
+  size_t P, R, F, XP, sqpart, Q, part, red, rr, rr0, alpha, beta, active, iters, ctl, status, total;
 };
 // Graph mode: begin() creates the WHILE node's handle in the graph being captured; open_body()
 // adds the conditional node after the captured work so far and returns a stream capturing into
