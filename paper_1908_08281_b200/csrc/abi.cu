@@ -894,7 +894,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
 }
 
 // CUDA-graph cache of hg_solve / hg_solve_host: the whole multi-stream launch sequence
-// (6 parts of ~67 kernels, their fork/join events, the host copies) is captured once per
+// (8 parts of ~51 kernels, their fork/join events, the host copies) is captured once per
 // distinct argument set and replayed with one cudaGraphLaunch on the caller's stream.
 // Enqueued directly, the parts cost ~1.1-1.5 ms of host time and start ~0.4 ms apart.
 extern "C++" {
