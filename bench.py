@@ -363,21 +363,21 @@ def run_ours(args):
     h2d = (c.N + 1) * 8 + h.nnz * 4 + h.E * 4 + c.N * c.T * 4
     d2h = c.N * c.T * 4 + c.nb * c.k * 4
 
-    # parity of the timed output on sampled blocks (rank 0; oracle = FP64 CPU)
-    parity = None
-    cpu_base = None
-    if rank == 0:
-        sel = [0, c.nb - 1]
-        t_or = time.perf_counter()
+    # Every use of the FP64 oracle below is deferred into the cpu_baseline leg (cpu_baseline_leg, run
+    # once after all GPU timing on rank 0): the CPU baseline timing itself and the parity / accuracy
+    # references of the timed outputs.  Nothing on the GPU path depends on it.
+    leg = []
+    result = {"parity": None, "cpu_baseline": None}
+
+    def leg_main():
         r = oracle_sample(h, c, 2, seed=seed) if c.nb > 1 else oracle_sample(h, c, 1, seed=seed)
         Fg = Fh.double().numpy()
         sg = sh.double().numpy()
         ferr = max(float(np.linalg.norm(Fg[blk * c.b:(blk + 1) * c.b] - r.F[s_ * c.b:(s_ + 1) * c.b]) /
                          np.linalg.norm(r.F[s_ * c.b:(s_ + 1) * c.b])) for s_, blk in enumerate(r.blocks))
         serr = max(float(np.max(np.abs(sg[blk] - r.sigma[s_]) / r.sigma[s_])) for s_, blk in enumerate(r.blocks))
-        parity = {"blocks": r.blocks, "F_rel_fro": ferr, "sigma_rel_max": serr, "tol": {"F": 2e-5, "sigma": 1e-5},
-                  "ok": ferr <= 2e-5 and serr <= 1e-5}
-        del t_or, sel
+        result["parity"] = {"blocks": r.blocks, "F_rel_fro": ferr, "sigma_rel_max": serr,
+                            "tol": {"F": 2e-5, "sigma": 1e-5}, "ok": ferr <= 2e-5 and serr <= 1e-5}
         if world == 1 and not args.no_cpu_baseline:
             nthreads = cores()
             n_s = max(1, min(c.nb, nthreads))
@@ -394,6 +394,9 @@ def run_ours(args):
                 cpu_base["value_1thread"] = 1.0 / r1.seconds
             finally:
                 oracle.set_num_threads(nthreads)
+            result["cpu_baseline"] = cpu_base
+
+    leg.append(leg_main)
 
     # the paper's second approach (CG on Eq. 5) on the
     # same workload, timed the same way (CUDA events, resident inputs), parity on sampled columns
@@ -431,7 +434,7 @@ def run_ours(args):
               "rel_res_max": float(rrc.max().item()), "launches_per_solve": cg_launches,
               "gather_bytes_per_solve": gather, "gather_GBps": gather / (cg_ms / 1e3) / 1e9,
               "note": "gathers are L2-resident (slice-major layout); see DESIGN.md §10"}
-        if rank == 0:
+        def leg_cg():
             import oracle
             cols = np.array([0, 1, c.T // 2, c.T - 1])
             ro = oracle.cg_solve(h.row_ptr, h.col_idx, h.w, np.ascontiguousarray(h.Y[:, cols]), mu=c.mu,
@@ -445,6 +448,8 @@ def run_ours(args):
             Ff = Fc.double().cpu().numpy()
             cg["rsvd_F_vs_full_solve_rel_fro"] = float(np.linalg.norm(Fr - Ff) / np.linalg.norm(Ff))
             cg["oracle_columns_s"] = ro.seconds
+
+        leg.append(leg_cg)
 
     # SURVEY.md §8(f) NEXT-3, reading R2: Alg. 1 on Theta_ii + the Woodbury inverse of X_ii, same
     # workload and timing; parity on sampled blocks; accuracy against the exact block solve and CG
@@ -471,7 +476,7 @@ def run_ours(args):
         r2 = {"workload": "same H, w, Y, b, k, q; Alg. 1 on Theta_ii, F_i = c (Y_i + U diag(s/((1+mu)-s)) U^T Y_i)",
               "solve_ms": r2_ms, "blocks_per_s": world * c.nb / (r2_ms / 1e3),
               "status": int(status.item())}
-        if rank == 0:
+        def leg_r2():
             import oracle
             ro2 = oracle.solve(h.row_ptr, h.col_idx, h.w, h.Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed,
                                blocks=[0, c.nb - 1], woodbury=True)
@@ -496,6 +501,8 @@ def run_ours(args):
                 r2["accuracy_vs_full_solve"] = {"r2": float(np.linalg.norm(Fg2 - Ff) / np.linalg.norm(Ff)),
                                                 "r1": float(np.linalg.norm(Fr1 - Ff) / np.linalg.norm(Ff))}
 
+        leg.append(leg_r2)
+
     # one Eq. 12 Schur level over pairs of adjacent blocks (reading R2 inverses)
     sch = None
     if not args.no_schur and c.nb % 2 == 0:
@@ -519,7 +526,7 @@ def run_ours(args):
                            "X11^-1, X22^-1, Z1^-1, Z2^-1 by Alg. 1 + Woodbury (reading R2)",
                "solve_ms": sch_ms, "launches_per_solve": sch_launches, "status": int(status.item())}
         del sws
-        if rank == 0:
+        def leg_schur():
             import oracle
             Fo, sel, osec = oracle.solve_schur(h.row_ptr, h.col_idx, h.w, h.Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed,
                                                superblocks=[0])
@@ -534,6 +541,8 @@ def run_ours(args):
                 Ff = Fc.double().cpu().numpy()
                 sch["accuracy_vs_full_solve"] = float(np.linalg.norm(Fsg - Ff) / np.linalg.norm(Ff))
             sch["oracle_superblock_s"] = osec
+
+        leg.append(leg_schur)
 
     # the hyperedge-weight update with f = the CG solution
     wts = None
@@ -565,12 +574,23 @@ def run_ours(args):
                            "one simplex step",
                "gradient_ms": g_ms, "step_ms": st_ms, "gather_bytes": gather,
                "gather_GBps": gather / (g_ms / 1e3) / 1e9, "status": int(status.item())}
-        if rank == 0:
+        def leg_weights():
             import oracle
             go = oracle.weight_gradient(h.row_ptr, h.col_idx, h.w, Fc.double().cpu().numpy(), kappa=kappa)
             gg = wg.double().cpu().numpy()
             err = float(np.max(np.abs(gg - go)) / np.max(np.abs(go)))
             wts["parity"] = {"grad_max_rel": err, "tol": 1e-5, "ok": err <= 1e-5}
+
+        leg.append(leg_weights)
+
+    def cpu_baseline_leg():
+        """The oracle (FP64 CPU), run once on rank 0 after all GPU timing: baseline + parity references."""
+        for task in leg:
+            task()
+
+    if rank == 0:
+        cpu_baseline_leg()
+    parity, cpu_base = result["parity"], result["cpu_baseline"]
 
     out = {
         "metric": "diag_blocks_per_s", "value": value, "unit": "blocks/s", "n_gpus": world,
