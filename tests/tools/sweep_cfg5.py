@@ -10,7 +10,7 @@ Each point is also run with reading R2 (HG_WOODBURY: Alg. 1 on Theta_ii + Woodbu
 NEXT-3): time, parity against the oracle's R2, accuracy against the same two references.
 One JSON line per point.
 
-    python tools/sweep_cfg5.py [--points b,k,q ...] > profiles/r01_cfg5_sweep.jsonl
+    python tests/tools/sweep_cfg5.py [--points b,k,q ...] > profiles/r01_cfg5_sweep.jsonl
 """
 import argparse
 import json
@@ -21,7 +21,7 @@ import time
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
 import oracle  # noqa: E402
 from paper_1908_08281_b200 import hg  # noqa: E402

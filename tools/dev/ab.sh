@@ -10,5 +10,5 @@ for i in $(seq $reps); do
 done
 for v in new old; do
   d=.; [ $v = old ] && d=_ab_old
-  echo "== $v stages (HG_STREAMS=1)"; (cd $d && HG_STREAMS=1 python tools/stage_probe.py 1 --no-parity 2>&1 | tail -14)
+  echo "== $v stages (HG_STREAMS=1)"; (cd $d && HG_STREAMS=1 python tests/tools/stage_probe.py 1 --no-parity 2>&1 | tail -14)
 done
