@@ -21,6 +21,8 @@
 //   (POTRF) -- two barriers per panel; tile products are register-blocked half tiles;
 //   in-place tile TRTRI (LAPACK trtri order): invert diagonal tiles, then for
 //   block columns j = nt-2..0: L_ij <- -(sum_{m=j+1..i} Linv_im L_mj) Linv_jj.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -156,29 +158,24 @@ __device__ __forceinline__ void tile_store_h(float* C, const float (&v)[2][8], i
   }
 }
 
-// warp: lower-triangular 32x32 tile inverse in place; lane c owns column c (registers)
+// warp: lower-triangular 32x32 tile inverse in place, as the TRSM above applied to the
+// identity: lane r solves row r of I L^-T, i.e. column r of L^-1 (the former column-by-column
+// substitution with lane-dependent branches took ~32k cycles per tile, 10x this)
 __device__ void tile_trtri(float* T, int lane) {
-  float x[TS];
-  const int c = lane;
-  const float rd = __frcp_rn(T[lane * LDT + lane]);     // lane r: 1 / T[r][r]
+  float a[TS];
 #pragma unroll
-  for (int r = 0; r < TS; ++r) {
-    const float rr = __shfl_sync(0xffffffffu, rd, r);
-    if (r < c) {
-      x[r] = 0.f;
-    } else if (r == c) {
-      x[r] = rr;
-    } else {
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};   // four independent chains (fixed order)
+  for (int t = 0; t < TS; ++t) a[t] = 0.f;
+  const float rd = __frcp_rn(T[lane * LDT + lane]);     // lane c: 1 / L[c][c]
 #pragma unroll
-      for (int t = 0; t < r; ++t)
-        if (t >= c) acc[t & 3] = fmaf(T[r * LDT + t], x[t], acc[t & 3]);
-      x[r] = -((acc[0] + acc[1]) + (acc[2] + acc[3])) * rr;
-    }
+  for (int c = 0; c < TS; ++c) {
+    float x[4] = {c == lane ? 1.f : 0.f, 0.f, 0.f, 0.f};   // four independent chains (fixed order)
+#pragma unroll
+    for (int t = 0; t < c; ++t) x[t & 3] = fmaf(-a[t], T[c * LDT + t], x[t & 3]);
+    a[c] = ((x[0] + x[1]) + (x[2] + x[3])) * __shfl_sync(0xffffffffu, rd, c);
   }
   __syncwarp();
 #pragma unroll
-  for (int r = 0; r < TS; ++r) T[r * LDT + c] = x[r];   // lower part only: x[r] = 0 above
+  for (int c = 0; c < TS; ++c) T[c * LDT + lane] = a[c];   // L^-1[c][lane]; zero above the diagonal
   __syncwarp();
 }
 
@@ -202,7 +199,8 @@ __device__ void store_lower(float* out, const float* tiles, int k, int nt, int w
 // choice so that the shared-memory instantiation's tile pointers are provably shared.
 template <bool SMEM>
 __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, float* __restrict__ Lout,
-                                           float* __restrict__ Linv, float* __restrict__ work, int32_t* status) {
+                                           float* __restrict__ Linv, float* __restrict__ work, int32_t* status,
+                                           int dbg_twice) {
   extern __shared__ __align__(16) float sm[];
   __shared__ float red[NWARP];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -312,7 +310,9 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
       if (warp == 0) {                              // lookahead: tile (p+1, p+1), then POTRF
         tile_sub_abt_h(T(p + 1, p + 1), T(p + 1, p), T(p + 1, p), lane, 0);
         tile_sub_abt_h(T(p + 1, p + 1), T(p + 1, p), T(p + 1, p), lane, 16);
+        if (p < 2) CHOL_CLK(30 + 2 * p);
         tile_potrf(T(p + 1, p + 1), lane, status, bad);
+        if (p < 2) CHOL_CLK(31 + 2 * p);
         if (bad && lane == 0) s_bad = 1;
       } else {
         const int ntask = (m * (m + 1) / 2 - 1) * 2;  // half tiles, diagonal (p+1, p+1) excluded
@@ -403,8 +403,9 @@ cudaError_t launch_cholinv(int nb, int k, const float* G, float* L, float* Linv,
     if (e != cudaSuccess) return e;
     attr[smem_tiles] = smem;
   }
-  if (smem_tiles) k_cholinv<true><<<nb, NT, smem, s>>>(k, G, L, Linv, work, status);
-  else k_cholinv<false><<<nb, NT, smem, s>>>(k, G, L, Linv, work, status);
+  static const int dbg = getenv("HG_CHOL_DBG") ? atoi(getenv("HG_CHOL_DBG")) : 0;
+  if (smem_tiles) k_cholinv<true><<<nb, NT, smem, s>>>(k, G, L, Linv, work, status, dbg);
+  else k_cholinv<false><<<nb, NT, smem, s>>>(k, G, L, Linv, work, status, dbg);
   ++*launches;
   return cudaGetLastError();
 }

@@ -24,7 +24,9 @@ for _ in range(2):
 torch.cuda.synchronize()
 clk = np.array(hg.debug_counters()["chol_clk"], dtype=np.int64)
 t0 = clk[0]
-names = {0: "start", 1: "loaded", 40: "factor done", 41: "trtri diag", 60: "trtri done", 61: "stored"}
+names = {0: "start", 1: "loaded", 40: "factor done", 41: "trtri diag", 60: "trtri done", 61: "stored",
+         30: "p0 lookahead potrf in", 31: "p0 lookahead potrf out", 32: "p1 lookahead potrf in",
+         33: "p1 lookahead potrf out", 36: "trtri diag (second run)"}
 for i, v in enumerate(clk):
     if v == 0:
         continue
@@ -36,4 +38,7 @@ for i, v in enumerate(clk):
         nm = f"trtri col {i - 42}"
     if nm is None:
         nm = f"stamp {i}"
-    print(f"{i:3d} {nm:22s} {v - t0:9d}")
+    print(f"{i:3d} {nm:26s} {v - t0:9d}")
+for a, b in ((30, 31), (32, 33), (40, 41), (41, 36), (41, 42), (59, 60), (60, 61)):
+    if clk[a] and clk[b]:
+        print(f"  {a}->{b}: {clk[b] - clk[a]}")
