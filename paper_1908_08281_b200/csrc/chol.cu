@@ -21,6 +21,8 @@
 //   (POTRF) -- two barriers per panel; tile products are register-blocked half tiles;
 //   in-place tile TRTRI (LAPACK trtri order): invert diagonal tiles, then for
 //   block columns j = nt-2..0: L_ij <- -(sum_{m=j+1..i} Linv_im L_mj) Linv_jj.
+//   (Recursive doubling -- B <- -C^-1 (B A^-1) per 2m x 2m tile block, log2(nt) levels of
+//   two register-held product phases -- measured the same 82k cycles at k = 256, not adopted.)
 #include <cstdlib>
 
 #include "common.cuh"
@@ -180,8 +182,27 @@ __device__ void tile_trtri(float* T, int lane) {
 }
 
 // warps write the full k x k row-major matrix (zeros above the diagonal) from the
-// lower tiles: warp per (tile row, tile column, 8-row slab), lanes = columns
+// lower tiles: float4 rows when k % 4 == 0 (17.0k cycles at k = 256 vs 18.4k for the
+// scalar form); else warp per (tile row, tile column, 8-row slab), lanes = columns
 __device__ void store_lower(float* out, const float* tiles, int k, int nt, int warp, int lane) {
+  if ((k & 3) == 0) {   // float4 rows: lane covers columns 4 lane .. 4 lane + 3 of a 128-column slab
+    const int nq = (k + 127) / 128;
+    for (int task = warp; task < k * nq; task += NWARP) {
+      const int r = task / nq, c = (task % nq) * 128 + 4 * lane;
+      if (c >= k) continue;
+      const int i = r / TS, j = c / TS;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j <= i) {
+        v = *reinterpret_cast<const float4*>(tiles + (int64_t)tidx(i, j) * TILE + (r % TS) * LDT + c % TS);
+        if (c + 0 > r) v.x = 0.f;
+        if (c + 1 > r) v.y = 0.f;
+        if (c + 2 > r) v.z = 0.f;
+        if (c + 3 > r) v.w = 0.f;
+      }
+      *reinterpret_cast<float4*>(out + (int64_t)r * k + c) = v;
+    }
+    return;
+  }
   for (int task = warp; task < nt * nt * 4; task += NWARP) {
     const int tl = task >> 2, rq = (task & 3) * 8;
     const int i = tl / nt, j = tl % nt;
@@ -200,7 +221,7 @@ __device__ void store_lower(float* out, const float* tiles, int k, int nt, int w
 template <bool SMEM>
 __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, float* __restrict__ Lout,
                                            float* __restrict__ Linv, float* __restrict__ work, int32_t* status,
-                                           int dbg_twice) {
+                                           int opts) {
   extern __shared__ __align__(16) float sm[];
   __shared__ float red[NWARP];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -316,7 +337,11 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
         if (bad && lane == 0) s_bad = 1;
       } else {
         const int ntask = (m * (m + 1) / 2 - 1) * 2;  // half tiles, diagonal (p+1, p+1) excluded
-        for (int task = warp - 1; task < ntask; task += NWARP - 1) {
+        // warps on warp 0's SM sub-partition (warp % 4 == 0) skip the trailing update when
+        // opts & 1, so the lookahead POTRF chain does not share its scheduler with them
+        const int nw = (opts & 1) ? NWARP - NWARP / 4 : NWARP - 1;
+        const int tw = (opts & 1) ? warp - (warp >> 2) - 1 : warp - 1;
+        for (int task = ((opts & 1) && (warp & 3) == 0) ? ntask : tw; task < ntask; task += nw) {
           const int w = (task >> 1) + 1;
           int a = 0;
           while ((a + 1) * (a + 2) / 2 <= w) ++a;
@@ -403,7 +428,8 @@ cudaError_t launch_cholinv(int nb, int k, const float* G, float* L, float* Linv,
     if (e != cudaSuccess) return e;
     attr[smem_tiles] = smem;
   }
-  static const int dbg = getenv("HG_CHOL_DBG") ? atoi(getenv("HG_CHOL_DBG")) : 0;
+  // opts bit 0 (HG_CHOL_OPTS, default 1): lookahead warp alone on its sub-partition (see the panel loop)
+  static const int dbg = getenv("HG_CHOL_OPTS") ? atoi(getenv("HG_CHOL_OPTS")) : 1;
   if (smem_tiles) k_cholinv<true><<<nb, NT, smem, s>>>(k, G, L, Linv, work, status, dbg);
   else k_cholinv<false><<<nb, NT, smem, s>>>(k, G, L, Linv, work, status, dbg);
   ++*launches;
