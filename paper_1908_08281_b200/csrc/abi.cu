@@ -866,9 +866,17 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     const Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, l, T);
     g_cur_part = pt;
     HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[pt]));
-    HG_TRY(run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, l, q, seed, simt, Ut + kb,
-                    sigma + (int64_t)(blk0 - soff) * l,
-                    Vt + kb, st, Bf, ps[pt], scheme));
+    // host entry: part 0's Jacobi on twice as many SMs (64-row cluster CTAs) -- its F is the
+    // first download, and the download (~4.7 ms at configs[3]) is what the e2e waits for after
+    // it (13.81 -> 13.52 ms e2e; on the device-only path the same costs 10.44 -> 10.61 ms).
+    // HG_JACOBI_WIDE = bitmask of parts overrides the default (1 with host buffers, else 0).
+    static const int wide_env = getenv("HG_JACOBI_WIDE") ? atoi(getenv("HG_JACOBI_WIDE")) : -1;
+    const int wide = wide_env >= 0 ? wide_env : (io.F_host ? 1 : 0);
+    jacobi_rows_hint(((wide >> pt) & 1) ? 64 : 0);
+    hg_status rs = run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, l, q, seed, simt, Ut + kb,
+                            sigma + (int64_t)(blk0 - soff) * l, Vt + kb, st, Bf, ps[pt], scheme);
+    jacobi_rows_hint(0);
+    HG_TRY(rs);
     if (cps) HG_CU(cudaStreamWaitEvent(ps[pt], ev_y[pt], 0), "wait Y");
     HG_TRY(run_apply(Ut + kb, sigma + (int64_t)(blk0 - soff) * l, Vt + kb, nbp, b, k, T > 0 ? Y + (int64_t)blk0 * b * T : Y, T,
                      mu / (1.0f + mu), T > 0 ? F + (int64_t)blk0 * b * T : F, st, Bf, ps[pt], simt,

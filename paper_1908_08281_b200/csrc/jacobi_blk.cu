@@ -645,11 +645,14 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
   if (C > 1) cluster_barrier_jb();
 }
 
+thread_local int g_rows_hint = 0;
+
 template <int BW>
 cudaError_t launch_bw(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s, double tol,
                       int w_is_l) {
-  // rows per CTA: 128 up to k = 256 (one CTA per SM for configs[3]), 64 beyond
-  const int rt = k <= 256 ? 128 : 64;
+  // rows per CTA: 128 up to k = 256 (one CTA per SM for configs[3]), 64 beyond; a caller's
+  // hint (jacobi_rows_hint) overrides it for one launch (wider clusters: shorter per-block latency)
+  const int rt = g_rows_hint > 0 ? g_rows_hint : (k <= 256 ? 128 : 64);
   const int C = (k + rt - 1) / rt;
   if (C > 8) return cudaErrorInvalidValue;
   const Layout Lo = make_layout<BW>(k, C);
@@ -697,6 +700,8 @@ cudaError_t jacobi_blk_debug(unsigned long long* out, bool reset) {
 }
 
 double jacobi_tol(int k);
+
+void jacobi_rows_hint(int rows) { g_rows_hint = rows; }
 
 // Block width 16 (32 x 32 inner problems) by default; HG_JACOBI_BW=8 selects 8 columns
 // (measured slower at configs[3]: 12.4 vs 8.4 ms -- inner rounds are latency-bound, so

@@ -50,6 +50,8 @@ cudaError_t jacobi_clocks(long long* out);
 cudaError_t launch_jacobi_blk(int nb, int k, const float* L, float* Wf, int32_t* status, cudaStream_t s,
                               int* launches);
 cudaError_t jacobi_blk_debug(unsigned long long* out, bool reset);
+// rows per cluster CTA for the next block-Jacobi launches of this thread (0: default)
+void jacobi_rows_hint(int rows);
 cudaError_t jacobi_blk_clocks(long long* out);
 
 // true when launch_jacobi orthogonalises the columns of L (then U~ = unit columns of W_f)
