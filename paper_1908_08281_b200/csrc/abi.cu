@@ -872,7 +872,8 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     // HG_JACOBI_WIDE = bitmask of parts overrides the default (1 with host buffers, else 0).
     static const int wide_env = getenv("HG_JACOBI_WIDE") ? atoi(getenv("HG_JACOBI_WIDE")) : -1;
     const int wide = wide_env >= 0 ? wide_env : (io.F_host ? 1 : 0);
-    jacobi_rows_hint(((wide >> pt) & 1) ? 64 : 0);
+    static const int wide_rows = getenv("HG_JACOBI_WIDE_ROWS") ? atoi(getenv("HG_JACOBI_WIDE_ROWS")) : 64;
+    jacobi_rows_hint(((wide >> pt) & 1) ? wide_rows : 0);
     hg_status rs = run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, l, q, seed, simt, Ut + kb,
                             sigma + (int64_t)(blk0 - soff) * l, Vt + kb, st, Bf, ps[pt], scheme);
     jacobi_rows_hint(0);
