@@ -307,6 +307,13 @@ hg_status hg_profile_timeline(int32_t max_rec, int32_t* stage, int32_t* part, do
  * out[85..132] block-Jacobi inner-round stamps (a reset call enables them). */
 hg_status hg_debug_counters(int64_t* out, int32_t n, int32_t reset);
 
+/* Debug, only meaningful in a build with -DHG_JB_SWEEPMAX (else the values stay 0):
+ * out == NULL clears the per-sweep maxima and switches recording on (on != 0) or off;
+ * else copies them out: out[64 * 40] floats, slot (blk, sweep) = largest
+ * a_pq^2 / (a_pp a_qq) that block slot blk (blockIdx within a launch) saw in that
+ * sweep of the block Jacobi (stopping rule).  Returns a cudaError_t value. */
+int hg_debug_jacobi_sweepmax(float* out, int on);
+
 /* Number of kernels the last hg_* call on this host thread enqueued. */
 int32_t hg_last_launch_count(void);
 

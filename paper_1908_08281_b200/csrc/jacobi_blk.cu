@@ -4,7 +4,8 @@
 // Same rotations as the scalar cyclic method (jacobi.cu): every column pair
 // (p, q) is visited once per sweep and rotated by the angle that zeroes its 2x2
 // Gram [[a_pp, a_pq], [a_pq, a_qq]] while |a_pq| > tol sqrt(a_pp a_qq); the
-// sweep loop stops after a sweep without rotations.  What changes is the data
+// sweep loop stops after a sweep in which no |a_pq| / sqrt(a_pp a_qq) exceeded
+// 4 tol (its rotations above tol are still applied; reading A16 in DESIGN.md).  What changes is the data
 // movement.  Columns are grouped in blocks of BW; an outer round pairs blocks
 // (I, J) by a round-robin tournament (nblk - 1 rounds), plus one "diagonal"
 // round for the pairs inside each block:
@@ -34,6 +35,15 @@ __device__ unsigned long long g_jb_dbg[3];   // [0] max sweeps, [1] total sweeps
 __device__ long long g_jb_clk[16];           // block 0 / rank 0 / thread 0: sweep 1, outer rounds 0-1
 __device__ long long g_jb_iclk[48];          // inner rounds 0-3 of block 0, pair 0, sweep 1, outer round 0
 __device__ int g_jb_iclk_on;                 // set by the caller of the stamps (debug)
+// debug (build with -DHG_JB_SWEEPMAX, tools/jacobi_sweepmax.py): per block and sweep, the largest
+// a_pq^2 / (a_pp a_qq) seen (float bits); compiled out otherwise
+__device__ unsigned g_jb_smax[64 * 40];
+__device__ int g_jb_smax_on;
+__device__ __forceinline__ void jb_meas(unsigned* slot, double apq, double app, double aqq) {
+#ifdef HG_JB_SWEEPMAX
+  if (slot) atomicMax(slot, __float_as_uint((float)(apq * apq / (app * aqq))));
+#endif
+}
 #define JB_CLK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0 && sweep == 1 && ro < 2) g_jb_clk[(i) + 8 * ro] = clock64(); } while (0)
 
 __device__ __forceinline__ void cluster_barrier_jb() {
@@ -136,7 +146,8 @@ template <int BW>
 __device__ __forceinline__ int diag_col(int s, int r) { return s == 0 ? 0 : 1 + (s - 1 + r) % (BW - 1); }
 
 template <int BW>
-__device__ int inner_sweep_diag(const GramSrc<BW>& G, float* Q, int base, double tol2, double2* cs, int lane) {
+__device__ int inner_sweep_diag(const GramSrc<BW>& G, float* Q, int base, double tol2, double stop2, double2* cs,
+                                int lane, unsigned* smax) {
   constexpr int PW = 2 * BW, LDQ = JB<BW>::LDQ;
   const bool act = lane < BW;
   const int row = base + (act ? lane : 0);
@@ -159,7 +170,7 @@ __device__ int inner_sweep_diag(const GramSrc<BW>& G, float* Q, int base, double
     }
     if (__ballot_sync(0xffffffffu, need) == 0u) return 0;
   }
-  int rot_any = 0;
+  int rot_any = 0, big = 0;
 #pragma unroll 1
   for (int r = 0; r < BW - 1; ++r) {
     int pa = lane, pj = 0, pslot = 0;
@@ -178,6 +189,8 @@ __device__ int inner_sweep_diag(const GramSrc<BW>& G, float* Q, int base, double
     const double aqq = __shfl_sync(0xffffffffu, d, pa);
     float c = 1.f, s = 0.f;
     double dp = d, dq = aqq;
+    if (first) jb_meas(smax, apq, d, aqq);
+    big |= first && apq * apq > stop2 * d * aqq;
     if (first && apq * apq > tol2 * d * aqq) jrot(d, aqq, apq, c, s, dp, dq);
     const float c_o = __shfl_sync(0xffffffffu, c, pa);
     const float s_o = __shfl_sync(0xffffffffu, s, pa);
@@ -215,7 +228,7 @@ __device__ int inner_sweep_diag(const GramSrc<BW>& G, float* Q, int base, double
     for (int j = 1; j < BW - 1; ++j) g[j] = g[j + 1];
     g[BW - 1] = t0;
   }
-  return rot_any;
+  return rot_any | (__ballot_sync(0xffffffffu, big) != 0u ? 2 : 0);
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -240,12 +253,12 @@ struct Cross4Scratch {
   double2* csd;   // [BW] (c, s) fp64
   float* xq;      // [4][32] Q slot exchange
   float2* csf;    // [BW] (c, s) fp32
-  int* flags;     // [2] "round rotates" (by round parity) | [4] per-warp "needs a sweep"
+  int* flags;     // [2] "round rotates" (by round parity) | [4] per-warp "needs a sweep" | [1] "above stop"
 };
 
 template <int BW>
 __device__ int inner_sweep_cross4(const GramSrc<BW>& G, float* Q, double tol2, const Cross4Scratch& S, int lane, int h,
-                                  int aw, int bar_id, int npass) {
+                                  int aw, int bar_id, int npass, double stop2, unsigned* smax) {
   constexpr int PW = 2 * BW, LDQ = JB<BW>::LDQ, QW = BW / 4;
   const int j0 = h * QW;
   const bool act = lane < PW;
@@ -260,13 +273,17 @@ __device__ int inner_sweep_cross4(const GramSrc<BW>& G, float* Q, double tol2, c
   }
   if (h == 0 && act) S.dsm[lane] = G(lane, lane);
   if (lane < BW && lane / QW == h) S.apq[lane] = gJ[lane - j0];   // round 0: pair a = slot (a, BW + a)
+  if (h == 0 && lane == 0) S.flags[6] = 0;                        // "a measure above the stop threshold"
   named_bar(bar_id, 128);
   // no cross entry above the threshold: no round can rotate (G never changes), skip
   int need = 0;
   if (lane < BW) {
     const double da = S.dsm[lane];
 #pragma unroll
-    for (int i = 0; i < QW; ++i) need |= gJ[i] * gJ[i] > tol2 * da * S.dsm[BW + j0 + i];
+    for (int i = 0; i < QW; ++i) {
+      need |= gJ[i] * gJ[i] > tol2 * da * S.dsm[BW + j0 + i];
+      jb_meas(smax, gJ[i], da, S.dsm[BW + j0 + i]);
+    }
   }
   need = __ballot_sync(0xffffffffu, need) != 0u;
   if (lane == 0) S.flags[2 + h] = need;
@@ -286,6 +303,8 @@ __device__ int inner_sweep_cross4(const GramSrc<BW>& G, float* Q, double tol2, c
         const int pa = BW + (lane + r) % BW;
         const double apq = S.apq[lane], app = S.dsm[lane], aqq = S.dsm[pa];
         float c = 1.f, sn = 0.f;
+        if (r < BW) jb_meas(smax, apq, app, aqq);
+        if (r < BW && apq * apq > stop2 * app * aqq) S.flags[6] = 1;
         if (apq * apq > tol2 * app * aqq) {
           double dp, dq;
           jrot(app, aqq, apq, c, sn, dp, dq);
@@ -365,7 +384,7 @@ __device__ int inner_sweep_cross4(const GramSrc<BW>& G, float* Q, double tol2, c
       qrow[(BW + j0 + i) ^ sw] = qJ[i];
     }
   }
-  return rot_any;
+  return rot_any | (S.flags[6] ? 2 : 0);
 }
 
 // per-owned-pair scratch (doubles): dsm [PW] | apq [BW] | xg [4 x 32] | csd [BW x 2] |
@@ -418,7 +437,8 @@ __host__ __device__ inline Layout make_layout(int k, int C) {
 
 template <int BW>
 __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, const float* __restrict__ L,
-                                                      float* __restrict__ Wf, int32_t* status, int w_is_l, int npass) {
+                                                      float* __restrict__ Wf, int32_t* status, int w_is_l, int npass,
+                                                      double stop_f) {
   using P = JB<BW>;
   constexpr int PW = P::PW, LDQ = P::LDQ, PACK = P::PACK, N4 = P::N4, UT = P::UT, NQB = P::NQB;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -436,7 +456,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
   double* JS = reinterpret_cast<double*>(smem_raw + Lo.offJ);    // [nown][JSCR]: cs | dsm | xch
   int* flag = reinterpret_cast<int*>(smem_raw + Lo.offF);        // [Pb] rotated-this-round
   const int t = threadIdx.x;
-  const double tol2 = tol * tol;
+  const double tol2 = tol * tol, stop2 = tol2 * stop_f * stop_f;
   const float* Lb = L + (int64_t)blk * k * k;
 
   for (int i = t; i < R * ldw; i += NT) {
@@ -455,6 +475,11 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
   bool converged = false;
   for (; sweep < MAX_SWEEPS && !converged; ++sweep) {
     int any = 0;
+#ifdef HG_JB_SWEEPMAX
+    unsigned* smax = (g_jb_smax_on && blk < 64 && sweep < 40) ? &g_jb_smax[blk * 40 + sweep] : nullptr;
+#else
+    unsigned* smax = nullptr;
+#endif
     for (int ro = 0; ro < nblk; ++ro) {
       const bool diag = (ro == nblk - 1);
       JB_CLK(0);
@@ -528,11 +553,11 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
           int rot_any = 0;
           if (!diag) {
             rot_any = inner_sweep_cross4<BW>(Gsrc, Qw + (size_t)gi * PW * LDQ, tol2, S, lane, h, gi & 3, 1 + gi,
-                                             npass);
+                                             npass, stop2, smax);
           } else if (h < 2) {   // diagonal round: block I by warp 0, block J by warp 1
             int* rflag = reinterpret_cast<int*>(S.xg);
-            const int rh = inner_sweep_diag<BW>(Gsrc, Qw + (size_t)gi * PW * LDQ, h * BW, tol2, S.csd + h * (BW / 2),
-                                                lane);
+            const int rh = inner_sweep_diag<BW>(Gsrc, Qw + (size_t)gi * PW * LDQ, h * BW, tol2, stop2,
+                                                S.csd + h * (BW / 2), lane, smax);
             if (lane == 0) rflag[h] = rh;
             named_bar(1 + gi, 64);
             rot_any = rflag[0] | rflag[1];
@@ -557,7 +582,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
         for (int e = t; e < npair * PW * F4; e += NT) {   // fetch Q (owner's smem) as float4 rows
           const int pp = e / (PW * F4), rem = e % (PW * F4), a = rem / F4, c4 = rem % F4;
           const int g = g0 + pp;
-          if (!flag[g]) continue;
+          if (!(flag[g] & 1)) continue;
           const int owner = g % C, slot = g / C;
           const float* src = Qw + (size_t)slot * PW * LDQ + a * LDQ + 4 * c4;
           const float4 v = (owner == rank) ? *reinterpret_cast<const float4*>(src) : ld_cluster_f4(src, owner);
@@ -577,7 +602,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
           tk[nt_mine] = task;
           const int pp = task / (rq_n * F4), rem = task % (rq_n * F4), rq = rem / F4, cq = rem % F4;
           const int g = g0 + pp;
-          if (!flag[g]) continue;
+          if (!(flag[g] & 1)) continue;
           int I, J;
           blocks_of(ro, g, I, J);
           const float* Qp = Qb + (size_t)pp * PW * LDQ;
@@ -615,7 +640,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
           const int task = tk[m];
           const int pp = task / (rq_n * F4), rem = task % (rq_n * F4), rq = rem / F4, cq = rem % F4;
           const int g = g0 + pp;
-          if (!flag[g]) continue;
+          if (!(flag[g] & 1)) continue;
           int I, J;
           blocks_of(ro, g, I, J);
           const int col = colof(4 * cq, I, J);
@@ -626,7 +651,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
         }
         __syncthreads();
       }
-      for (int g = 0; g < Pb; ++g) any |= flag[g];
+      for (int g = 0; g < Pb; ++g) any |= flag[g] >> 1;   // a measure above the stop threshold
       JB_CLK(5);
     }
     converged = (any == 0);
@@ -678,7 +703,18 @@ cudaError_t launch_bw(int nb, int k, const float* L, float* Wf, int32_t* status,
     const int x = v ? atoi(v) : 1;
     return x < 1 ? 1 : (x > 4 ? 4 : x);
   }();
-  return cudaLaunchKernelEx(&cfg, k_jacobi_blk<BW>, k, C, tol, L, Wf, status, w_is_l, npass);
+  // stop rule: the sweep loop ends after a sweep whose largest rotation measure
+  // |a_pq| / sqrt(a_pp a_qq) is <= stop_f * tol (HG_JACOBI_STOP = stop_f, default 4; 1 = "a sweep
+  // without rotations").  Measured at configs[3] (tools/jacobi_sweepmax.py): the per-sweep maximum
+  // falls 2e-3 ... 4e-5, 2e-6, then sits at 5.0-5.3e-7 -- the fp32 Gram noise floor, just above
+  // tol = 5e-7 -- for the last 2-3 sweeps, which only rotate noise: 10.2 -> 8.1 sweeps, F and sigma
+  // errors unchanged (6.2e-6 / 6.1e-7)
+  static const double stop_f = [] {
+    const char* v = getenv("HG_JACOBI_STOP");
+    const double x = v ? atof(v) : 4.0;
+    return x < 1.0 ? 1.0 : x;
+  }();
+  return cudaLaunchKernelEx(&cfg, k_jacobi_blk<BW>, k, C, tol, L, Wf, status, w_is_l, npass, stop_f);
 }
 
 }  // namespace
@@ -702,6 +738,15 @@ cudaError_t jacobi_blk_debug(unsigned long long* out, bool reset) {
 double jacobi_tol(int k);
 
 void jacobi_rows_hint(int rows) { g_rows_hint = rows; }
+
+// debug: switch the per-sweep maximum rotation measure on (and clear it) / read it
+extern "C" int hg_debug_jacobi_sweepmax(float* out, int on) {
+  if (out) return (int)cudaMemcpyFromSymbol(out, g_jb_smax, sizeof(g_jb_smax));
+  static unsigned z[64 * 40] = {};
+  cudaError_t e = cudaMemcpyToSymbol(g_jb_smax, z, sizeof z);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_jb_smax_on, &on, sizeof(int));
+  return (int)e;
+}
 
 // Block width 16 (32 x 32 inner problems) by default; HG_JACOBI_BW=8 selects 8 columns
 // (measured slower at configs[3]: 12.4 vs 8.4 ms -- inner rounds are latency-bound, so

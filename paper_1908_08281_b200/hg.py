@@ -88,7 +88,7 @@ EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_
            "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve",
            "hg_block_apply_woodbury", "hg_workspace_size_ex", "hg_block_rsvd_ex", "hg_solve_ex",
            "hg_weight_gradient", "hg_weight_step", "hg_schur_workspace_size",
-           "hg_solve_schur", "hg_solve_blocks", "hg_weight_objective")
+           "hg_solve_schur", "hg_solve_blocks", "hg_weight_objective", "hg_debug_jacobi_sweepmax")
 
 
 class HGError(RuntimeError):
@@ -113,6 +113,24 @@ def debug_counters(reset: bool = False) -> dict:
     return {"chol_near_identity": int(out[0]), "chol_full": int(out[1]), "jacobi_max_sweeps": int(out[2]),
             "jacobi_total_sweeps": int(out[3]), "jacobi_blocks": int(out[4]), "chol_clk": out[5:69].tolist(),
             "jac_clk": out[69:85].tolist(), "jac_inner_clk": out[85:133].tolist()}
+
+
+def debug_jacobi_sweepmax(on=None):
+    """Per-sweep maximum block-Jacobi rotation measure (only in a -DHG_JB_SWEEPMAX build).
+    on=True/False: clear and switch recording on/off; on=None: return float32 [64, 40] of
+    |a_pq| / sqrt(a_pp a_qq) (block slot, sweep)."""
+    import numpy as np
+    fn = _lib.hg_debug_jacobi_sweepmax
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    fn.restype = ctypes.c_int
+    if on is not None:
+        if fn(None, int(bool(on))) != 0:
+            raise HGError(HG_ERR_CUDA, "hg_debug_jacobi_sweepmax")
+        return None
+    out = np.zeros(64 * 40, dtype=np.float32)
+    if fn(out.ctypes.data, 0) != 0:
+        raise HGError(HG_ERR_CUDA, "hg_debug_jacobi_sweepmax")
+    return np.sqrt(out.reshape(64, 40))
 
 
 STAGES = ("degrees", "assemble", "omega", "gemm_power", "gemm_gram", "gemm_qform", "gemm_svd", "gemm_apply",
