@@ -238,6 +238,8 @@ struct Rsvd {
     g.B = Linv; g.b_mn = false; g.ldb = k; g.sb = (int64_t)k * k;
     g.D = Q_t; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
     g.bn_max = bn_env("HG_BN_QFORM", 256);
+    static const bool tri = !getenv("HG_QFORM_FULL");   // Linv is lower: B(kk, n) = Linv(n, kk) upper
+    g.b_upper = tri;
     return gemm(g, s, simt, "Q = Y R^-1", ST_GEMM_QFORM);
   }
 };

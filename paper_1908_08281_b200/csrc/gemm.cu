@@ -49,6 +49,7 @@ struct EpiArgs {
   const float* C; // residual (row-major D only): D += beta * C
   int64_t ldc, sc;
   float beta;
+  int b_upper;    // B(kk, n) = 0 for kk > n (GemmDesc::b_upper): per k-block, MMAs over n >= kk only
 };
 
 constexpr int NEPI = 256;            // converter / epilogue threads (8 warps)
@@ -185,18 +186,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         mbar_wait(&conv_bar[s], ph);
         tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(buf * BN);
+        // b_upper: columns n < kb * BK of this k-block are zero in B -- the MMAs cover
+        // n >= nlo only (N = BN - nlo, TMEM columns and B rows offset by nlo; K-major B rows
+        // are 128 B, nlo a multiple of 16); the drain masks what a chunk never wrote
+        const int nlo = ea.b_upper ? (max(0, kb * BK - n0) & ~15) : 0;
+        if (nlo >= BN) {
+          mma_commit(&empty_bar[s]);
+          if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == num_kb - 1) mma_commit(&tfull_bar[buf]);
+          continue;
+        }
+        const uint32_t idk = nlo ? make_idesc(BN - nlo, ea.a_mn, ea.b_mn) : idesc;
+        const uint32_t d = tmem + (uint32_t)(buf * BN + nlo);
         const uint32_t ahi = smem_u32(sA_hi(s)), alo = smem_u32(sA_lo(s));
-        const uint32_t bhi = smem_u32(sB_hi(s)), blo = smem_u32(sB_lo(s));
+        const uint32_t bhi = smem_u32(sB_hi(s)) + nlo * 128, blo = smem_u32(sB_lo(s)) + nlo * 128;
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
           const uint64_t dah = umma_desc(ahi + kk * a_kstep, a_lbo, a_sbo, a_lay);
           const uint64_t dal = umma_desc(alo + kk * a_kstep, a_lbo, a_sbo, a_lay);
           const uint64_t dbh = umma_desc(bhi + kk * b_kstep, b_lbo, b_sbo, b_lay);
           const uint64_t dbl = umma_desc(blo + kk * b_kstep, b_lbo, b_sbo, b_lay);
-          mma_tf32(d, dal, dbh, idesc, (first && kk == 0) ? 0u : 1u);
-          mma_tf32(d, dah, dbl, idesc, 1);
-          mma_tf32(d, dah, dbh, idesc, 1);
+          mma_tf32(d, dal, dbh, idk, (first && kk == 0) ? 0u : 1u);
+          mma_tf32(d, dah, dbl, idk, 1);
+          mma_tf32(d, dah, dbh, idk, 1);
         }
         mma_commit(&empty_bar[s]);
         if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == num_kb - 1) mma_commit(&tfull_bar[buf]);
@@ -214,12 +225,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(&tfull_bar[buf], (dch >> 1) & 1);
       tc_fence_after();
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * C::HALF);
+      // b_upper: tile columns below the chunk's first k-block's nlo were never written by it
+      const int clo = ea.b_upper ? min(BN, max(0, dch * CHUNK_KB * BK - n0) & ~15) - h * C::HALF : 0;
 #pragma unroll
       for (int j0 = 0; j0 < C::HALF; j0 += 16) {
         float v[16];
         tmem_ld16(ta + j0, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[j0 + i] += v[i];
+        for (int i = 0; i < 16; ++i) acc[j0 + i] += (j0 + i >= clo) ? v[i] : 0.f;
       }
       tc_fence_before();
       __syncwarp();
@@ -234,6 +247,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       float4* al = reinterpret_cast<float4*>(sA_lo(s));
       float4* bh = reinterpret_cast<float4*>(sB_hi(s));
       float4* bl = reinterpret_cast<float4*>(sB_lo(s));
+      // b_upper: B rows (n) below this k-block's nlo are never read by the MMAs -- not split
+      const int b0 = ea.b_upper ? min(BN, max(0, kb * BK - n0) & ~15) * (BK / 4) : 0;
       if (ea.trunc_hi) {
 #pragma unroll
         for (int i = t; i < BM * BK / 4; i += NEPI) {
@@ -241,7 +256,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           al[i] = make_float4(trunc_lo(x.x), trunc_lo(x.y), trunc_lo(x.z), trunc_lo(x.w));
         }
 #pragma unroll
-        for (int i = t; i < BN * BK / 4; i += NEPI) {
+        for (int i = b0 + t; i < BN * BK / 4; i += NEPI) {
           const float4 x = bh[i];
           bl[i] = make_float4(trunc_lo(x.x), trunc_lo(x.y), trunc_lo(x.z), trunc_lo(x.w));
         }
@@ -254,7 +269,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           al[i] = l;
         }
 #pragma unroll
-        for (int i = t; i < BN * BK / 4; i += NEPI) {
+        for (int i = b0 + t; i < BN * BK / 4; i += NEPI) {
           float4 x = bh[i];
           float4 l = split_hi(x);
           bh[i] = x;
@@ -486,7 +501,8 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
     return (v && v[0] == 'r') ? 0 : 1;
   }();
   EpiArgs ea{g.M, g.N, g.K, g.D, g.ldd, g.sd, g.d_trans ? 1 : 0, g.alpha, g.rs, g.srs, g.cs, g.scs,
-             g.a_mn ? 1 : 0, g.b_mn ? 1 : 0, trunc_hi, g.lower ? 1 : 0, g.C, g.ldc, g.sc, g.beta};
+             g.a_mn ? 1 : 0, g.b_mn ? 1 : 0, trunc_hi, g.lower ? 1 : 0, g.C, g.ldc, g.sc, g.beta,
+             (g.b_upper && !g.b_mn) ? 1 : 0};
   if (simt) {
     dim3 grid((g.M + 63) / 64, (g.N + 63) / 64, g.batch);
     gemm_simt_kernel<<<grid, 256, 0, stream>>>(g.A, ea.a_mn, g.lda, g.sa, g.B, ea.b_mn, g.ldb, g.sb, ea);

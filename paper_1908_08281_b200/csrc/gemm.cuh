@@ -30,6 +30,9 @@ struct GemmDesc {
   const float* C = nullptr;
   int64_t ldc = 0, sc = 0;
   float beta = 0.f;
+  // B(kk, n) = 0 for kk > n (e.g. B = Linv^T): the tensor-core kernel skips the zero
+  // part of each k-block's MMAs (K-major B only; ignored otherwise -- still correct)
+  bool b_upper = false;
 };
 
 // Enqueue the GEMM; returns cudaSuccess or the launch error.  `simt` selects the
