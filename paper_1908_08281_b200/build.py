@@ -27,9 +27,22 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+STAMP = LIB + ".stamp"
+
+
+def _stamp() -> str:
+    """What the library was compiled with: a library built with other flags (e.g. debug defines
+    through HG_NVCC_EXTRA) is never silently reused."""
+    extra = os.environ.get("HG_NVCC_EXTRA", "").split()
+    return " ".join(ARCH + FLAGS + extra + SOURCES)
+
+
 def _stale() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return True
+    with open(STAMP) as f:
+        if f.read() != _stamp():
+            return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "hg.h")]
     return any(os.path.getmtime(d) > t for d in deps)
@@ -60,6 +73,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + " ".join(cmd) + "\n" + r.stdout)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(_stamp())
     return LIB
 
 

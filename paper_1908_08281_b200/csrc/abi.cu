@@ -868,12 +868,12 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     const Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, l, T);
     g_cur_part = pt;
     HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[pt]));
-    // host entry: part 0's Jacobi on twice as many SMs (64-row cluster CTAs) -- its F is the
-    // first download, and the download (~4.7 ms at configs[3]) is what the e2e waits for after
-    // it (13.81 -> 13.52 ms e2e; on the device-only path the same costs 10.44 -> 10.61 ms).
-    // HG_JACOBI_WIDE = bitmask of parts overrides the default (1 with host buffers, else 0).
-    static const int wide_env = getenv("HG_JACOBI_WIDE") ? atoi(getenv("HG_JACOBI_WIDE")) : -1;
-    const int wide = wide_env >= 0 ? wide_env : (io.F_host ? 1 : 0);
+    // HG_JACOBI_WIDE = bitmask of parts whose Jacobi runs on 64-row cluster CTAs (twice the SMs
+    // per block: a shorter per-block latency for that part).  Off by default in BOTH entries: the
+    // cluster width changes the order of the Jacobi's Gram partial sums, so a wide part's bits
+    // differ from the narrow one's (within the tolerances) and the host entry would no longer
+    // reproduce the device entry bit for bit.
+    static const int wide = getenv("HG_JACOBI_WIDE") ? atoi(getenv("HG_JACOBI_WIDE")) : 0;
     static const int wide_rows = getenv("HG_JACOBI_WIDE_ROWS") ? atoi(getenv("HG_JACOBI_WIDE_ROWS")) : 64;
     jacobi_rows_hint(((wide >> pt) & 1) ? wide_rows : 0);
     hg_status rs = run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, l, q, seed, simt, Ut + kb,

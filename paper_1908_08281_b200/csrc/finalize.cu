@@ -81,7 +81,10 @@ __global__ void __launch_bounds__(NT) k_rows(int b, int k, const float* __restri
   __syncthreads();
   const float sgn = (u[bi[0]] < 0.f) ? -1.f : 1.f;
   const double sv = sig[(int64_t)blk * k + j];
-  const float vs = (float)((double)sgn / sv);
+  const double smax = sig[(int64_t)blk * k + perm[(int64_t)blk * k]];
+  // v_j = B^T u_j / sigma_j; a zero (or noise-level) sigma_j of a rank-deficient block has no
+  // defined v_j: write 0 instead of inf/NaN (the R1 apply flags such a sigma, k_inv_sigma)
+  const float vs = (sv > 1e-7 * smax && sv > 0.0) ? (float)((double)sgn / sv) : 0.f;
   const float* v = Vw_t + src;
   for (int i = threadIdx.x; i < b; i += NT) {
     Ut[dst + i] = sgn * u[i];

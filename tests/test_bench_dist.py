@@ -105,3 +105,54 @@ def test_sharded_blocks_and_allgather_gloo_world2():
     want = np.arange(7 * 4 * 3, dtype=np.float32).reshape(-1, 3)
     for x in res:
         assert np.array_equal(np.array(x[3], np.float32), want)
+
+
+def test_bench_gpus2_spawns_ranks_and_shards_gloo(monkeypatch, capfd):
+    """`bench.py --gpus 2` without torchrun spawns its two ranks itself (torch.distributed.run on
+    127.0.0.1); the harness self-test shards configs[0]'s blocks, all-gathers F and sigma over gloo
+    and reports the max over ranks."""
+    import json
+    import bench
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        monkeypatch.delenv(k, raising=False)
+    rc = bench.main(["--gpus", "2", "--selftest-dist", "--config", "2"])
+    out = capfd.readouterr().out
+    assert rc == 0, out
+    line = json.loads([ln for ln in out.splitlines() if ln.startswith("{")][-1])
+    assert line["selftest"] == "dist" and line["ok"] and line["n_gpus"] == 2
+    assert line["shards"] == [[0, 8], [8, 8]] and line["ms_per_step_max"] == 2.0
+
+
+def test_allgather_uneven_and_inplace_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_uneven_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = [q.get(timeout=10) for _ in range(3)]
+    assert all(r[1] for r in res), res
+
+
+def _uneven_worker(rank, world, port, q):
+    os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank),
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    import torch
+    import bench
+    import torch.distributed as dist
+    bench.dist_setup("gloo")
+    ok = True
+    for nb in (7, 6):   # uneven shares (padded path) and equal shares (all_gather_into_tensor)
+        b, T = 2, 3
+        b0, cnt = bench.shard_range(nb, rank, world)
+        F = torch.full((nb * b, T), -1.0)
+        F[b0 * b:(b0 + cnt) * b] = rank
+        out = torch.empty_like(F)
+        bench.allgather_rows(F, b0 * b, cnt * b, world, counts=bench.shard_rows(nb, b, world), out=out)
+        want = torch.cat([torch.full((bench.shard_range(nb, r, world)[1] * b, T), float(r)) for r in range(world)])
+        ok &= bool(torch.equal(out, want))
+    q.put((rank, ok))
+    dist.destroy_process_group()

@@ -208,18 +208,65 @@ def test_solve_parity_config4_sampled_blocks(inputs):
     check_against_oracle(h, c, F, sigma, [0, c.nb // 2, c.nb - 1], Ut, Vt)
 
 
-CFG5_SUBSET = [(512, 64, 1), (512, 256, 4), (1024, 128, 2), (1024, 512, 1), (2048, 256, 1), (512, 512, 1)]
+def test_solve_parity_config4_every_stream_part(inputs):
+    """configs[3] through hg_solve (the bench entry: 8 stream parts of 8 blocks on forked streams,
+    CUDA-graph replay): one block per part (0, 8, ..., 56) and the last block, against the oracle."""
+    hg = hgm()
+    h = inputs(4)
+    c = CONFIGS[4]
+    H, w, Y = dev_inputs(h)
+    F, sigma, st = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    assert int(st.item()) == 0
+    check_against_oracle(h, c, F, sigma, list(range(0, c.nb, 8)) + [c.nb - 1])
 
 
-@pytest.mark.parametrize("b,k,q", CFG5_SUBSET)
-def test_solve_parity_config5_points(inputs, b, k, q):
+def _cfg5_cost(p):
+    b, k, q = p
+    return b * b * k * (q + 1) + b * k * k * (2 * q + 1)
+
+
+@pytest.fixture(scope="module")
+def cfg5_oracle(inputs):
+    """The FP64 oracle on blocks {0, nb-1} of all 36 configs[4] points, computed once as one
+    parallel batch (host threads x 2 OpenMP threads each, largest points first)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    h = inputs(5)
+    ncores = len(os.sched_getaffinity(0))
+
+    def run(p):
+        b, k, q = p
+        oracle.set_num_threads(2)   # per host thread (OpenMP ICV): 2 blocks per point
+        nb = CONFIGS[5].N // b
+        return p, oracle.solve(h.row_ptr, h.col_idx, h.w, h.Y, mu=CONFIGS[5].mu, b=b, k=k, q=q,
+                               seed=CONFIGS[5].seed, blocks=[0, nb - 1])
+
+    pts = sorted(cfg5_points(), key=_cfg5_cost, reverse=True)
+    with ThreadPoolExecutor(max_workers=max(1, ncores // 2)) as ex:
+        res = dict(ex.map(run, pts))
+    oracle.set_num_threads(ncores)
+    return res
+
+
+@pytest.mark.parametrize("b,k,q", cfg5_points())
+def test_solve_parity_config5_all_points(inputs, cfg5_oracle, b, k, q):
+    """Every configs[4] (b, k, q) point (36) through hg_solve: F <= 2e-5 and sigma <= 1e-5 against
+    the FP64 oracle on the first and last block (north_star: parity on all five configs)."""
     hg = hgm()
     h = inputs(5)
     c = CONFIGS[5].with_(b=b, k=k, q=q)
-    assert (b, k, q) in cfg5_points()
     H, w, Y = dev_inputs(h)
     F, sigma, st = hg.solve(H, w, Y, mu=c.mu, b=b, k=k, q=q, seed=c.seed)
-    check_against_oracle(h, c, F, sigma, [0, c.nb - 1])
+    assert int(st.item()) == 0
+    r = cfg5_oracle[(b, k, q)]
+    Fg = F.double().cpu().numpy()
+    sg = sigma.double().cpu().numpy()
+    for s_, blk in enumerate(r.blocks):
+        fo = r.F[s_ * b:(s_ + 1) * b]
+        fe = rel(Fg[blk * b:(blk + 1) * b], fo)
+        se = float(np.max(np.abs(sg[blk] - r.sigma[s_]) / r.sigma[s_]))
+        assert fe <= F_TOL and se <= SIG_TOL, (blk, fe, se)
+        assert np.all(np.diff(sg[blk]) <= 0)
 
 
 def test_tiny_inputs_and_k_equals_b():
@@ -326,6 +373,20 @@ def test_deterministic_and_host_entry(inputs):
                              torch.from_numpy(h.Y).pin_memory(), mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0,
                              woodbury=True)
     assert torch.equal(Fhw, Fw.cpu()) and torch.equal(shw, sw.cpu())
+
+
+def test_host_entry_bitwise_equal_at_k256(inputs):
+    """configs[3] (k = 256, 2-CTA Jacobi clusters): the host entry (prioritised part streams, Y
+    uploads and F downloads per part) gives the device entry's bits."""
+    hg = hgm()
+    h = inputs(4)
+    c = CONFIGS[4]
+    H, w, Y = dev_inputs(h)
+    F1, s1, st = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)
+    assert int(st.item()) == 0
+    Fh, sh = hg.solve_host(torch.from_numpy(h.row_ptr), torch.from_numpy(h.col_idx), torch.from_numpy(h.w),
+                           torch.from_numpy(h.Y).pin_memory(), mu=c.mu, b=c.b, k=c.k, q=c.q, seed=0)
+    assert torch.equal(Fh, F1.cpu()) and torch.equal(sh, s1.cpu())
 
 
 def test_simt_verification_path_agrees(inputs):

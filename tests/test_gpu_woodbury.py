@@ -125,3 +125,9 @@ def test_woodbury_rank_deficient_theta_blocks():
         X = oracle.theta_block(rp, ci, w, b, blk, mu=1.0)
         ex = 0.5 * np.linalg.solve(X, Y[blk * b:(blk + 1) * b].astype(float))
         assert rel(F[blk * b:(blk + 1) * b].double().cpu().numpy(), ex) <= F_TOL
+    # the factorisation itself stays finite: the right vectors of the (near-)zero sigma are written
+    # as 0, not inf/NaN (finalize.cu k_rows)
+    X, _, _ = hg.build_theta(H, torch.from_numpy(w).cuda(), 1.0, b, raw=True)
+    Ut, sg, Vt, st2 = hg.block_rsvd(X, 8, 1, 0)
+    torch.cuda.synchronize()
+    assert bool(torch.isfinite(Ut).all()) and bool(torch.isfinite(Vt).all()) and bool(torch.isfinite(sg).all())
