@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhgrsvd.so")
-SOURCES = ["abi.cu", "gemm.cu", "theta.cu", "philox.cu", "chol.cu", "jacobi.cu", "jacobi_blk.cu", "finalize.cu", "cg.cu", "schur.cu"]
+SOURCES = ["abi.cu", "gemm.cu", "theta.cu", "philox.cu", "chol.cu", "jacobi.cu", "jacobi_blk.cu", "finalize.cu", "cg.cu", "schur.cu", "eig.cu"]
 HEADERS = ["common.cuh", "gemm.cuh", "kernels.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-warn-spills"]

@@ -1,0 +1,688 @@
+// eig.cu -- eigen-preconditioner of the one-sided Jacobi SVD (Alg. 1 step 5).
+//
+// The Jacobi of jacobi_blk.cu orthogonalises the columns of W = L (B B^T = L L^T):
+// W J = U~ Sigma.  Started from W = L it needs 8-9 sweeps on the configs, because
+// the singular values of B are tightly clustered (sigma(X_ii) in [theta/(1+theta), 1],
+// the top k of them within ~2%: SURVEY.md App. A).  Started from W0 = L J0, where J0
+// is an orthogonal approximation of the eigenvectors of A = L^T L (the right singular
+// vectors of L), the columns of W0 are already orthogonal to ~fp32 rounding and one
+// sweep (a check that rotates little or nothing) finishes ("Jacobi
+// preconditioner"; the mixed-precision Jacobi idea: an SVD computed cheaply in
+// lower accuracy preconditions the accurate one-sided Jacobi).  The preconditioner
+// only changes where the Jacobi starts, not what it converges to: the result is the
+// Jacobi's, whatever the quality of J0, as long as J0 is orthogonal -- which the
+// CholeskyQR2 after these kernels guarantees (abi.cu).
+//
+// J0 here (all fp32; deviations from exactness only cost Jacobi rotations):
+//   k_sytrd_eig  one CTA per block: Householder tridiagonalisation Q^T A Q = T with
+//                the lower triangle of A in shared-memory 32x32 tiles; eigenvalues of T
+//                by Sturm bisection; eigenvectors Z of T by inverse iteration (thread
+//                per eigenvalue);
+//   k_orgtr      Q = H_0 H_1 ... H_{k-3} formed explicitly (stored transposed);
+//   then (abi.cu) J0^T = diag(s) (Q Z)^T on the tensor cores, CholeskyQR2.
+#include <cfloat>
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+constexpr int INV_IT = 3;         // inverse iterations per eigenvector
+
+__device__ long long g_eig_clk[32];  // debug: phase clock stamps of block 0 (hg_debug_eig_clocks)
+#define EIG_CLK(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_eig_clk[i] = clock64(); } while (0)
+// steps 0, 64, 128, 192 of the tridiagonalisation: stamps at (b), after (b), after (c), after (c2), after (d)
+#define EIG_SCLK(i) do { if ((j & 63) == 0 && j < 256) EIG_CLK(8 + 5 * (j >> 6) + (i)); } while (0)
+
+__host__ __device__ inline int tix(int I, int J) { return I * (I + 1) / 2 + J; }   // lower tile (I >= J)
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// deterministic start vector of the inverse iteration for eigenvalue i, in [-1, 1)
+__device__ __forceinline__ float start_vec(int r, int i) {
+  uint32_t h = (uint32_t)r * 0x9E3779B1u ^ ((uint32_t)i * 0x85EBCA77u + 0x165667B1u);
+  h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+  return (float)(h >> 8) * (2.0f / 16777216.0f) - 1.0f;
+}
+
+// Number of eigenvalues of the (normalised) tridiagonal T below x: sign changes of the Sturm
+// sequence p_0 = 1, p_1 = d_0 - x, p_{i+1} = (d_i - x) p_i - e_{i-1}^2 p_{i-1} (Golub & Van Loan
+// §8.4.1), in the division-free three-term form; |d|, e^2 <= ~1 after normalisation, so |p| grows
+// by at most ~3^8 between the exact power-of-two rescalings every 8 steps.  An exact zero p_i
+// counts one change over the pair (p_{i-1}, p_i, p_{i+1} = -e^2 p_{i-1}) whichever its sign bit.
+// d, e2s: shared, 16-byte aligned, e2s[i] = e_{i-1}^2 (e2s[0] = 0), zero-padded to a multiple of 8.
+__device__ __forceinline__ int sturm_count(const float* __restrict__ d, const float* __restrict__ e2s, int k, float x) {
+  float p0 = 0.f, p1 = 1.f;   // p_{-1}, p_0
+  int cnt = 0;
+  for (int i0 = 0; i0 < k; i0 += 8) {
+    const int n = min(8, k - i0);
+    const float4 da = *reinterpret_cast<const float4*>(d + i0), db = *reinterpret_cast<const float4*>(d + i0 + 4);
+    const float4 ea = *reinterpret_cast<const float4*>(e2s + i0), eb = *reinterpret_cast<const float4*>(e2s + i0 + 4);
+    const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+    const float ev[8] = {ea.x, ea.y, ea.z, ea.w, eb.x, eb.y, eb.z, eb.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q < n) {
+        const float p2 = fmaf(dv[q] - x, p1, -ev[q] * p0);
+        cnt += (__float_as_uint(p2) ^ __float_as_uint(p1)) >> 31;
+        p0 = p1;
+        p1 = p2;
+      }
+    }
+    const float m = fmaxf(fabsf(p0), fabsf(p1));
+    const int ex = ((__float_as_int(m) >> 23) & 0xff) - 127;
+    if (ex > 48 || (ex < -48 && m != 0.f)) {
+      const float sc = __int_as_float((127 - ex) << 23);
+      p0 *= sc;
+      p1 *= sc;
+    }
+  }
+  return cnt;
+}
+
+// ---------------------------------------------------------------- tridiagonalisation
+// One CTA per block, 2 tiles of 32x32 per warp held in registers (lane = tile row): the lower
+// triangle of A never leaves the register file.  Householder tridiagonalisation (Golub & Van Loan
+// Alg. 8.3.1, unblocked, LAPACK sytd2 form: x = A[j+1:, j]; H_j = I - tau v v^T, H_j x = beta e1;
+// p = tau A22 v; w = p - (tau/2)(p^T v) v; A22 -= v w^T + w v^T), four block barriers per step:
+//   (b) y' = A22 z on the raw column z = A[j+1:, j] (A22 v = s (A22 z - beta A22 e_1), s = 1/(alpha -
+//       beta), so the product need not wait for the norm): row part per tile, and for strictly lower
+//       tiles the transposed part by a butterfly reduce-scatter across the lanes;
+//   (c) Householder scalars (every thread), v, y = A22 v, y^T v;      (c2) w;
+//   (d) rank-2 update in registers; the owners of the next two columns publish them (and the next
+//       column's norm partials) to shared memory.
+// Tiles are listed by tile column J descending, so the trailing tiles of a step are a prefix of the
+// list; tile p lives in slot p / NWT of warp p % NWT (the longest-lived tiles spread over all warps).
+constexpr int NSLOT = 2;
+
+__host__ __device__ inline int sytrd_warps(int ntl) {
+  const int nt = ntl * (ntl + 1) / 2;
+  return (nt + NSLOT - 1) / NSLOT;
+}
+
+struct TrdSmem {   // offsets in 4-byte words
+  int zs, xs2, vs, ws, ys, yrow, ycol, nrm, red, dsc, tl, total;
+};
+__host__ __device__ inline TrdSmem trd_smem(int ntl) {
+  TrdSmem S;
+  int off = 0;
+  const int nt = ntl * (ntl + 1) / 2, KP = 32 * ntl;
+  S.zs = off; off += KP;
+  S.xs2 = off; off += KP;
+  S.vs = off; off += KP;
+  S.ws = off; off += KP;
+  S.ys = off; off += KP;
+  S.yrow = off; off += nt * 32;
+  S.ycol = off; off += nt * 32;
+  S.nrm = off; off += 8;
+  S.red = off; off += 32;
+  S.dsc = off; off += 4;
+  S.tl = off; off += nt;
+  S.total = off;
+  return S;
+}
+
+__device__ __forceinline__ float sel32(const float* a, int c) {   // a[c], c warp-uniform, static register indices
+  float v = a[0];
+#pragma unroll
+  for (int i = 1; i < 32; ++i) v = (c == i) ? a[i] : v;
+  return v;
+}
+
+__global__ void __launch_bounds__(576, 1) k_sytrd(int k, int ntl, const float* __restrict__ A, float* __restrict__ Hv,
+                                                  float* __restrict__ tau_out, float* __restrict__ d_out,
+                                                  float* __restrict__ e_out) {
+  extern __shared__ __align__(16) float sm[];
+  const TrdSmem S = trd_smem(ntl);
+  float* zs = sm + S.zs;     // column j, rows > j (0 elsewhere)
+  float* xs2 = sm + S.xs2;   // column j + 1, rows >= j + 1
+  float* vs = sm + S.vs;
+  float* ws = sm + S.ws;
+  float* ys = sm + S.ys;
+  float* yrow = sm + S.yrow;
+  float* ycol = sm + S.ycol;
+  float* nrm = sm + S.nrm;   // partial sums of squares of column j, rows >= j + 2, per tile row
+  float* red = sm + S.red;
+  float* dsc = sm + S.dsc;   // A(j, j)
+  int* tl = reinterpret_cast<int*>(sm + S.tl);
+  const int blk = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int NT = blockDim.x, NWT = NT >> 5;
+  const int KP = 32 * ntl, nt = ntl * (ntl + 1) / 2;
+  const float* Ab = A + (int64_t)blk * k * k;
+  float* Hb = Hv + (int64_t)blk * k * k;
+  float* tb = tau_out + (int64_t)blk * k;
+  EIG_CLK(0);
+  if (t == 0) {
+    int a = 0;
+    for (int J = ntl - 1; J >= 0; --J)
+      for (int I = J; I < ntl; ++I) tl[a++] = I | (J << 8);
+  }
+  for (int i = t; i < KP; i += NT) { zs[i] = 0.f; xs2[i] = 0.f; vs[i] = 0.f; ws[i] = 0.f; ys[i] = 0.f; }
+  if (t < 32) red[t] = 0.f;
+  if (t < 8) nrm[t] = 0.f;
+  __syncthreads();
+  // registers: slot s = tile p = warp + NWT s
+  float a[NSLOT][32];
+  int tI[NSLOT], tJ[NSLOT];
+#pragma unroll
+  for (int s = 0; s < NSLOT; ++s) {
+    const int p = warp + NWT * s;
+    tI[s] = p < nt ? (tl[p] & 0xff) : 0;
+    tJ[s] = p < nt ? (tl[p] >> 8) : 0;
+    const int r = 32 * tI[s] + lane;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const int cc = 32 * tJ[s] + c;
+      float v = 0.f;
+      if (p < nt && r < k && cc < k) v = (r >= cc) ? Ab[(int64_t)r * k + cc] : Ab[(int64_t)cc * k + r];
+      a[s][c] = v;
+    }
+  }
+  // publish column jn (rows > jn, its diagonal, its norm partials over rows >= jn + 2) and column
+  // jn + 1 (rows >= jn + 1) from the registers of the tiles holding them
+  auto emit = [&](int jn, int nact) {
+#pragma unroll
+    for (int s = 0; s < NSLOT; ++s) {
+      const int p = warp + NWT * s;
+      if (p >= nact) continue;
+      const int r = 32 * tI[s] + lane;
+      if (tJ[s] == (jn >> 5)) {
+        const float v = sel32(a[s], jn & 31);
+        zs[r] = (r > jn && r < k) ? v : 0.f;
+        if (r == jn) dsc[0] = v;
+        const float x = (r >= jn + 2 && r < k) ? v : 0.f;
+        const float q = warp_sum_f(x * x);
+        if (lane == 0) nrm[tI[s]] = q;
+      }
+      if (jn + 1 < k && tJ[s] == ((jn + 1) >> 5)) {
+        const float v = sel32(a[s], (jn + 1) & 31);
+        xs2[r] = (r >= jn + 1 && r < k) ? v : 0.f;
+      }
+    }
+  };
+  emit(0, nt);
+  __syncthreads();
+  EIG_CLK(1);
+
+  for (int j = 0; j + 2 < k; ++j) {
+    const int t0 = (j + 1) >> 5, ntr = ntl - t0;
+    const int nrow = ntr * (ntr + 1) / 2;
+    EIG_SCLK(0);
+    // (b) y' = A22 z
+#pragma unroll
+    for (int s = 0; s < NSLOT; ++s) {
+      const int p = warp + NWT * s;
+      if (p >= nrow) continue;
+      const int I = tI[s], J = tJ[s], ti = tix(I, J);
+      const float* zJ = zs + 32 * J;
+      float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 z4 = *reinterpret_cast<const float4*>(zJ + 4 * c4);
+        acc0 = fmaf(a[s][4 * c4 + 0], z4.x, acc0);
+        acc1 = fmaf(a[s][4 * c4 + 1], z4.y, acc1);
+        acc0 = fmaf(a[s][4 * c4 + 2], z4.z, acc0);
+        acc1 = fmaf(a[s][4 * c4 + 3], z4.w, acc1);
+      }
+      yrow[ti * 32 + lane] = acc0 + acc1;
+      if (I > J) {   // transposed half: lane L <- sum_r a[r][L] z_r (butterfly reduce-scatter)
+        const float zl = zs[32 * I + lane];
+        float h16[16], h8[8], h4[4], h2[2];
+        {
+          const bool up = lane & 16;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float lo = a[s][i] * zl, hi = a[s][i + 16] * zl;
+            h16[i] = (up ? hi : lo) + __shfl_xor_sync(0xffffffffu, up ? lo : hi, 16);
+          }
+        }
+        {
+          const bool up = lane & 8;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            h8[i] = (up ? h16[i + 8] : h16[i]) + __shfl_xor_sync(0xffffffffu, up ? h16[i] : h16[i + 8], 8);
+        }
+        {
+          const bool up = lane & 4;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            h4[i] = (up ? h8[i + 4] : h8[i]) + __shfl_xor_sync(0xffffffffu, up ? h8[i] : h8[i + 4], 4);
+        }
+        {
+          const bool up = lane & 2;
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            h2[i] = (up ? h4[i + 2] : h4[i]) + __shfl_xor_sync(0xffffffffu, up ? h4[i] : h4[i + 2], 2);
+        }
+        const bool up = lane & 1;
+        ycol[ti * 32 + lane] = (up ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, up ? h2[0] : h2[1], 1);
+      }
+    }
+    __syncthreads();
+    EIG_SCLK(1);
+    // (c) Householder scalars (every thread, fp32), v, y = A22 v, y^T v partials
+    float xn2 = 0.f;
+    {   // nrm[0..7]: independent loads, tile rows < (j + 2) / 32 masked
+      const float4 n0 = *reinterpret_cast<const float4*>(nrm), n1 = *reinterpret_cast<const float4*>(nrm + 4);
+      const int i0 = (j + 2) >> 5;
+      xn2 = ((i0 <= 0 ? n0.x : 0.f) + (i0 <= 1 ? n0.y : 0.f)) + ((i0 <= 2 ? n0.z : 0.f) + (i0 <= 3 ? n0.w : 0.f)) +
+            (((i0 <= 4 && ntl > 4) ? n1.x : 0.f) + ((i0 <= 5 && ntl > 5) ? n1.y : 0.f)) +
+            (((i0 <= 6 && ntl > 6) ? n1.z : 0.f) + ((i0 <= 7 && ntl > 7) ? n1.w : 0.f));
+    }
+    const float alpha = zs[j + 1];
+    float beta = alpha, tau = 0.f, scal = 0.f;
+    if (xn2 > 0.f) {
+      beta = -copysignf(sqrtf(fmaf(alpha, alpha, xn2)), alpha);
+      tau = __fdividef(beta - alpha, beta);
+      scal = __fdividef(1.f, alpha - beta);
+    }
+    float dot = 0.f;
+    for (int r = t; r < KP; r += NT) {
+      float v = 0.f, y = 0.f;
+      if (r > j && r < k) {
+        const int I = r >> 5, rr = r & 31;
+        float yq[16];   // independent loads (static bounds, predicated), then a fixed-order sum
+#pragma unroll
+        for (int J = 0; J < 8; ++J) yq[J] = (J >= t0 && J <= I) ? yrow[tix(I, J) * 32 + rr] : 0.f;
+#pragma unroll
+        for (int I2 = 1; I2 < 8; ++I2) yq[7 + I2] = (I2 > I && I2 < ntl) ? ycol[tix(I2, I) * 32 + rr] : 0.f;
+        yq[15] = 0.f;
+#pragma unroll
+        for (int h = 8; h; h >>= 1)
+#pragma unroll
+          for (int i = 0; i < h; ++i) yq[i] += yq[i + h];
+        const float yp = yq[0];
+        v = (r == j + 1) ? 1.f : zs[r] * scal;
+        y = scal * fmaf(-beta, xs2[r], yp);
+      }
+      vs[r] = v;
+      ys[r] = y;
+      if (r < k) Hb[(int64_t)j * k + r] = v;
+      dot = fmaf(y, v, dot);
+    }
+    if (t == 0) {
+      d_out[(int64_t)blk * k + j] = dsc[0];
+      e_out[(int64_t)blk * k + j] = beta;
+      tb[j] = tau;
+    }
+    dot = warp_sum_f(dot);
+    if (lane == 0) red[warp] = dot;
+    __syncthreads();
+    EIG_SCLK(2);
+    if (tau == 0.f) {   // H_j = I (uniform): no update; publish the next columns of A as it is
+      emit(j + 1, nrow);
+      __syncthreads();
+      continue;
+    }
+    float yv = 0.f;
+#pragma unroll
+    for (int w4 = 0; w4 < 20; w4 += 4) {   // <= 18 warps; red[NWT..19] are zero
+      const float4 q = *reinterpret_cast<const float4*>(red + w4);
+      yv += (q.x + q.y) + (q.z + q.w);
+    }
+    const float Kc = 0.5f * tau * tau * yv;   // w = tau y - (tau^2 / 2)(y^T v) v, formed on the fly below
+    EIG_SCLK(3);
+    // (d) A22 -= v w^T + w v^T (no FMA contraction: the two products are summed in either order, so
+    //     diagonal tiles stay exactly symmetric); publish columns j + 1, j + 2
+#pragma unroll
+    for (int s = 0; s < NSLOT; ++s) {
+      const int p = warp + NWT * s;
+      if (p >= nrow) continue;
+      const int I = tI[s], J = tJ[s];
+      const float vr = vs[32 * I + lane], wr = fmaf(tau, ys[32 * I + lane], -Kc * vr);
+      const float* vJ = vs + 32 * J;
+      const float* yJ = ys + 32 * J;
+      auto wq = [&](const float4& v4, const float4& y4) {
+        return make_float4(fmaf(tau, y4.x, -Kc * v4.x), fmaf(tau, y4.y, -Kc * v4.y), fmaf(tau, y4.z, -Kc * v4.z),
+                           fmaf(tau, y4.w, -Kc * v4.w));
+      };
+      if (I == J) {
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const float4 v4 = *reinterpret_cast<const float4*>(vJ + 4 * c4);
+          const float4 w4 = wq(v4, *reinterpret_cast<const float4*>(yJ + 4 * c4));
+          a[s][4 * c4 + 0] = __fsub_rn(a[s][4 * c4 + 0], __fadd_rn(__fmul_rn(vr, w4.x), __fmul_rn(wr, v4.x)));
+          a[s][4 * c4 + 1] = __fsub_rn(a[s][4 * c4 + 1], __fadd_rn(__fmul_rn(vr, w4.y), __fmul_rn(wr, v4.y)));
+          a[s][4 * c4 + 2] = __fsub_rn(a[s][4 * c4 + 2], __fadd_rn(__fmul_rn(vr, w4.z), __fmul_rn(wr, v4.z)));
+          a[s][4 * c4 + 3] = __fsub_rn(a[s][4 * c4 + 3], __fadd_rn(__fmul_rn(vr, w4.w), __fmul_rn(wr, v4.w)));
+        }
+      } else {   // strictly lower tile: no symmetry to keep, two FMAs per entry
+#pragma unroll
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const float4 v4 = *reinterpret_cast<const float4*>(vJ + 4 * c4);
+          const float4 w4 = wq(v4, *reinterpret_cast<const float4*>(yJ + 4 * c4));
+          a[s][4 * c4 + 0] = fmaf(-vr, w4.x, fmaf(-wr, v4.x, a[s][4 * c4 + 0]));
+          a[s][4 * c4 + 1] = fmaf(-vr, w4.y, fmaf(-wr, v4.y, a[s][4 * c4 + 1]));
+          a[s][4 * c4 + 2] = fmaf(-vr, w4.z, fmaf(-wr, v4.z, a[s][4 * c4 + 2]));
+          a[s][4 * c4 + 3] = fmaf(-vr, w4.w, fmaf(-wr, v4.w, a[s][4 * c4 + 3]));
+        }
+      }
+    }
+    emit(j + 1, nrow);
+    __syncthreads();
+    EIG_SCLK(4);
+  }
+  // the last 2x2 (or 1x1) block: d_{k-2}, e_{k-2}, d_{k-1}
+  if (t == 0) {
+    float* db = d_out + (int64_t)blk * k;
+    float* eb = e_out + (int64_t)blk * k;
+    const int j = k >= 2 ? k - 2 : 0;
+    db[j] = dsc[0];
+    if (k >= 2) {
+      eb[k - 2] = zs[k - 1];
+      db[k - 1] = xs2[k - 1];
+      tb[k - 2] = 0.f;
+    }
+    eb[k - 1] = 0.f;
+    tb[k - 1] = 0.f;
+  }
+  EIG_CLK(2);
+}
+
+// ---------------------------------------------------------------- eigenpairs of T
+// One CTA per block, thread per eigenvalue.  (1) T / tn (tn = max |Gershgorin bound|): the
+// division-free Sturm counts stay in range; eigenvectors are unchanged.  (2) Eigenvalues: Sturm-count
+// scans (one point per thread) narrow the interval holding the spectrum, then each thread bisects
+// from its scan bracket to fp32 resolution.  (3) Eigenvectors: INV_IT steps of inverse iteration
+// (LAPACK gttrf/gtts2 elimination with partial pivoting; factors through global scratch, prefetched
+// 8 rows ahead).  Out: Z [nb][k][k] (column i = the unnormalised eigenvector of the i-th smallest
+// eigenvalue), scale [nb][k] (1 / ||Z[:, i]||).
+constexpr int EIG_NT = 256;
+constexpr int SEG = 16;           // inverse iteration: rows per checkpoint segment
+constexpr int SCAN_PASSES = 2;
+
+__device__ __forceinline__ float e_in_scaled(const float* e_in, int blk, int k, int i) {
+  return i < k - 1 ? e_in[(int64_t)blk * k + i] : 0.f;
+}
+
+__global__ void __launch_bounds__(EIG_NT) k_trideig(int k, const float* __restrict__ d_in, const float* __restrict__ e_in,
+                                                    float* __restrict__ Z, float* __restrict__ scale_out) {
+  extern __shared__ float ckpt[];   // [ceil((k-1)/SEG)][3][EIG_NT] inverse-iteration checkpoints
+  __shared__ __align__(16) float d[256];
+  __shared__ __align__(16) float e[256];
+  __shared__ __align__(16) float e2[256];
+  __shared__ int cnt[EIG_NT];
+  __shared__ float red[2 * (EIG_NT / 32)];
+  const int blk = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  constexpr int NWE = EIG_NT / 32;
+  for (int i = t; i < 256; i += EIG_NT) {
+    d[i] = i < k ? d_in[(int64_t)blk * k + i] : 0.f;
+    e[i] = i < k - 1 ? e_in[(int64_t)blk * k + i] : 0.f;
+  }
+  __syncthreads();
+  EIG_CLK(3);
+  float gmin = FLT_MAX, gmax = -FLT_MAX;
+  for (int i = t; i < k; i += EIG_NT) {
+    const float em = i > 0 ? fabsf(e[i - 1]) : 0.f, ep = i < k - 1 ? fabsf(e[i]) : 0.f;
+    gmin = fminf(gmin, d[i] - em - ep);
+    gmax = fmaxf(gmax, d[i] + em + ep);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    gmin = fminf(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
+    gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+  }
+  if (lane == 0) { red[warp] = gmin; red[NWE + warp] = gmax; }
+  __syncthreads();
+  gmin = red[0];
+  gmax = red[NWE];
+  for (int w = 1; w < NWE; ++w) { gmin = fminf(gmin, red[w]); gmax = fmaxf(gmax, red[NWE + w]); }
+  float tn = fmaxf(fabsf(gmin), fabsf(gmax));
+  if (!(tn > 0.f) || !isfinite(tn)) tn = 1.f;
+  const float itn = 1.f / tn;
+  __syncthreads();
+  __syncthreads();
+  for (int i = t; i < 256; i += EIG_NT) {
+    d[i] *= itn;
+    e[i] *= itn;
+    const float em = i > 0 ? e_in_scaled(e_in, blk, k, i - 1) * itn : 0.f;
+    e2[i] = em * em;   // e2[i] = e_{i-1}^2 (the Sturm recurrence's shifted layout)
+  }
+  __syncthreads();
+  const float pad = 4.f * FLT_EPSILON;
+  float glo = gmin * itn - pad, ghi = gmax * itn + pad;
+  auto pt = [&](float lo_, float hi_, int m) { return lo_ + (hi_ - lo_) * (float)(m + 1) / (float)(EIG_NT + 1); };
+  for (int pass = 0; pass < SCAN_PASSES; ++pass) {
+    cnt[t] = sturm_count(d, e2, k, pt(glo, ghi, t));
+    __syncthreads();
+    if (pass + 1 == SCAN_PASSES) break;
+    // occupied part: from the last point with count 0 to the first with count k (counts are
+    // non-decreasing in x up to rounding; binary searches)
+    int a = 0, b = EIG_NT;
+    while (a < b) { const int m = (a + b) >> 1; if (cnt[m] > 0) b = m; else a = m + 1; }
+    const int f0 = a;
+    a = 0; b = EIG_NT;
+    while (a < b) { const int m = (a + b) >> 1; if (cnt[m] >= k) b = m; else a = m + 1; }
+    const int fk = a;
+    const float nlo = f0 > 0 ? pt(glo, ghi, f0 - 1) : glo;
+    const float nhi = fk < EIG_NT ? pt(glo, ghi, fk) : ghi;
+    __syncthreads();
+    glo = nlo;
+    ghi = nhi;
+  }
+  if (t >= k) return;
+  float lo, hi;
+  {
+    int a = 0, b = EIG_NT;   // first scan point with count > t
+    while (a < b) { const int m = (a + b) >> 1; if (cnt[m] > t) b = m; else a = m + 1; }
+    lo = a > 0 ? pt(glo, ghi, a - 1) : glo;
+    hi = a < EIG_NT ? pt(glo, ghi, a) : ghi;
+  }
+  for (int it = 0; it < 40; ++it) {
+    const float mid = 0.5f * (lo + hi);
+    if (!(mid > lo && mid < hi)) break;   // fp32 resolution
+    if (sturm_count(d, e2, k, mid) > t) hi = mid;
+    else lo = mid;
+  }
+  const float lam = 0.5f * (lo + hi);
+  EIG_CLK(4);
+
+  // Inverse iteration without factor storage: the forward elimination keeps a checkpoint of its
+  // working row (w0, w1, rhs) every SEG rows in shared memory; the back substitution walks the
+  // segments from the last, recomputing each segment's U rows from its checkpoint into registers.
+  // The right-hand side of iteration it >= 1 is the previous iterate (Z, read ahead of the rows the
+  // back substitution overwrites).
+  const float eps_piv = FLT_EPSILON;   // replaces an exactly zero pivot (T normalised: ||T|| ~ 1)
+  float* Zb = Z + (int64_t)blk * k * k;   // [row][k]: column t = this eigenvector
+  float* ck = ckpt + t;                   // [seg][3][EIG_NT]
+  float rscale = 1.f;
+  // one elimination step on rows (r, r + 1): working row (w0, w1 | rw) against row r + 1 (a0, a1, a2 | ra);
+  // returns the U row (1/u0, u1, u2, ru)
+  auto elim = [&](int r, float& w0, float& w1, float& rw, float ra) {
+    const float a0 = e[r], a1 = d[r + 1] - lam, a2 = e[r + 1];
+    float4 f;
+    if (fabsf(w0) >= fabsf(a0)) {   // pivot: the working row
+      if (w0 == 0.f) w0 = eps_piv;
+      const float l = __fdividef(a0, w0);
+      f = make_float4(__fdividef(1.f, w0), w1, 0.f, rw);
+      w0 = fmaf(-l, w1, a1);
+      w1 = a2;
+      rw = fmaf(-l, rw, ra);
+    } else {                         // interchange: pivot on row r + 1
+      const float l = __fdividef(w0, a0);
+      f = make_float4(__fdividef(1.f, a0), a1, a2, ra);
+      w0 = fmaf(-l, a1, w1);
+      w1 = -l * a2;
+      rw = fmaf(-l, ra, rw);
+    }
+    return f;
+  };
+  for (int it = 0; it < INV_IT; ++it) {
+    auto rhs = [&](int r) { return r < k ? (it == 0 ? start_vec(r, t) : Zb[(int64_t)r * k + t] * rscale) : 0.f; };
+    // forward: rows 0 .. k-2 (step r eliminates row r + 1), checkpoints before steps 0, SEG, 2 SEG, ...
+    float rb[SEG], nb[SEG];
+#pragma unroll
+    for (int q = 0; q < SEG; ++q) rb[q] = rhs(1 + q);
+    float w0 = d[0] - lam, w1 = k > 1 ? e[0] : 0.f, rw = rhs(0);
+    for (int base = 0; base + 1 < k; base += SEG) {
+#pragma unroll
+      for (int q = 0; q < SEG; ++q) nb[q] = rhs(base + SEG + 1 + q);   // next segment's right-hand sides
+      ck[(base / SEG) * 3 * EIG_NT] = w0;
+      ck[(base / SEG) * 3 * EIG_NT + EIG_NT] = w1;
+      ck[(base / SEG) * 3 * EIG_NT + 2 * EIG_NT] = rw;
+#pragma unroll
+      for (int q = 0; q < SEG; ++q)
+        if (base + q + 1 < k) elim(base + q, w0, w1, rw, rb[q]);
+#pragma unroll
+      for (int q = 0; q < SEG; ++q) rb[q] = nb[q];
+    }
+    if (w0 == 0.f) w0 = eps_piv;
+    float x1 = rw / w0, x2 = 0.f;   // x_{r+1}, x_{r+2}
+    const float xlast = x1;
+    float nrm2 = x1 * x1;
+    // backward, segment by segment
+    const int nseg = (k - 1 + SEG - 1) / SEG;
+#pragma unroll
+    for (int q = 0; q < SEG; ++q) rb[q] = rhs((nseg - 1) * SEG + 1 + q);
+    for (int sg = nseg - 1; sg >= 0; --sg) {
+      const int base = sg * SEG;
+      if (sg > 0) {
+#pragma unroll
+        for (int q = 0; q < SEG; ++q) nb[q] = rhs(base - SEG + 1 + q);   // read before this segment writes
+      }
+      float u0[SEG], u1[SEG], u2[SEG], ru[SEG];
+      float sw0 = ck[sg * 3 * EIG_NT], sw1 = ck[sg * 3 * EIG_NT + EIG_NT], srw = ck[sg * 3 * EIG_NT + 2 * EIG_NT];
+#pragma unroll
+      for (int q = 0; q < SEG; ++q) {
+        if (base + q + 1 < k) {
+          const float4 f = elim(base + q, sw0, sw1, srw, rb[q]);
+          u0[q] = f.x; u1[q] = f.y; u2[q] = f.z; ru[q] = f.w;
+        }
+      }
+#pragma unroll
+      for (int q = SEG - 1; q >= 0; --q) {
+        const int r = base + q;
+        if (r + 1 < k) {
+          const float x = (ru[q] - u1[q] * x1 - u2[q] * x2) * u0[q];
+          Zb[(int64_t)r * k + t] = x;
+          nrm2 = fmaf(x, x, nrm2);
+          x2 = x1;
+          x1 = x;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < SEG; ++q) rb[q] = nb[q];
+    }
+    Zb[(int64_t)(k - 1) * k + t] = xlast;
+    rscale = nrm2 > 0.f ? rsqrtf(nrm2) : 0.f;
+    EIG_CLK(5 + it);
+  }
+  scale_out[(int64_t)blk * k + t] = rscale;
+}
+
+// Q^T with Q = H_0 H_1 ... H_{k-3} (LAPACK orgtr, backward accumulation): column c of Q is
+// H_0 ... H_{c-1} e_c (H_j e_c = e_c for j >= c), applied from the inside out.  Warp per 8 columns
+// (lane = rows lane + 32 s), no block barrier; out[c][r] = Q[r][c].
+template <int RPL>
+__global__ void __launch_bounds__(128) k_orgtr(int k, const float* __restrict__ Hv, const float* __restrict__ tau,
+                                               float* __restrict__ Qt) {
+  const int blk = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = (blockIdx.y * 4 + warp) * 8;
+  if (c0 >= k) return;
+  const float* Hb = Hv + (int64_t)blk * k * k;
+  const float* tb = tau + (int64_t)blk * k;
+  float z[RPL][8];
+#pragma unroll
+  for (int s = 0; s < RPL; ++s)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) z[s][q] = (lane + 32 * s == c0 + q) ? 1.f : 0.f;
+  const int jtop = min(k - 3, c0 + 6);   // the largest j < the warp's largest column
+  float vn[RPL];
+  auto loadv = [&](int j, float* v) {
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {
+      const int r = lane + 32 * s;
+      v[s] = (j >= 0 && r < k) ? Hb[(int64_t)j * k + r] : 0.f;
+    }
+  };
+  loadv(jtop, vn);
+  for (int j = jtop; j >= 0; --j) {
+    float v[RPL];
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) v[s] = vn[s];
+    loadv(j - 1, vn);   // prefetch
+    const float tj = tb[j];
+    if (tj == 0.f) continue;
+    const int s0 = (j + 1) >> 5;   // rows <= j: v = 0
+    float dot[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int s = 0; s < RPL; ++s)
+      if (s >= s0)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dot[q] = fmaf(v[s], z[s][q], dot[q]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dot[q] += __shfl_xor_sync(0xffffffffu, dot[q], o);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dot[q] *= -tj;
+#pragma unroll
+    for (int s = 0; s < RPL; ++s)
+      if (s >= s0)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) z[s][q] = fmaf(dot[q], v[s], z[s][q]);
+  }
+  float* ob = Qt + (int64_t)blk * k * k;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (c0 + q >= k) continue;
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {
+      const int r = lane + 32 * s;
+      if (r < k) ob[(int64_t)(c0 + q) * k + r] = z[s][q];
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int hg_debug_eig_clocks(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_eig_clk, sizeof(g_eig_clk));
+}
+
+// per block: tau [k], scale [k], d [k], e [k] (a multiple of 4 floats: 16-byte aligned per part)
+size_t eig_scratch_floats(int k) { return ((size_t)4 * k + 3) / 4 * 4; }
+
+bool eig_precond_supported(int k) { return k >= 1 && k <= 256; }
+
+cudaError_t launch_eig_precond(int nb, int k, const float* A, float* Hv, float* Z, float* scratch, float* Qt,
+                               const float** scale, cudaStream_t s, int* launches) {
+  if (!eig_precond_supported(k)) return cudaErrorInvalidValue;
+  const int ntl = (k + 31) / 32;
+  float* tau = scratch;                         // [nb][k]
+  float* sc = scratch + (size_t)nb * k;         // [nb][k]
+  float* dd = scratch + (size_t)2 * nb * k;     // [nb][k]
+  float* ee = scratch + (size_t)3 * nb * k;     // [nb][k]
+  *scale = sc;
+  const TrdSmem S = trd_smem(ntl);
+  const size_t smem = (size_t)S.total * 4;
+  k_sytrd<<<nb, 32 * sytrd_warps(ntl), smem, s>>>(k, ntl, A, Hv, tau, dd, ee);
+  ++*launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t ck_bytes = (size_t)((k - 1 + SEG - 1) / SEG + 1) * 3 * EIG_NT * 4;
+  e = cudaFuncSetAttribute(k_trideig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ck_bytes);
+  if (e != cudaSuccess) return e;
+  k_trideig<<<nb, EIG_NT, ck_bytes, s>>>(k, dd, ee, Z, sc);
+  ++*launches;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const dim3 grid(nb, (k + 31) / 32);
+  switch (ntl) {
+    case 1: k_orgtr<1><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 2: k_orgtr<2><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 3: k_orgtr<3><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 4: k_orgtr<4><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 5: k_orgtr<5><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 6: k_orgtr<6><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 7: k_orgtr<7><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    default: k_orgtr<8><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+  }
+  ++*launches;
+  return cudaGetLastError();
+}

@@ -118,3 +118,13 @@ cudaError_t launch_axpby(int ns, int64_t len, float c, float g, const float* P, 
 cudaError_t launch_csc_setup(const CgArgs& a, cudaStream_t s, int* launches);
 cudaError_t launch_weight_objective(int64_t nF, const float* F, int E, const float* w, const float* grad, float kappa,
                                     double* part, double* out, cudaStream_t s, int* launches);
+
+// eig.cu -- eigen-preconditioner of the Jacobi (k <= 256): from A = L^T L [nb][k][k] (lower triangle
+// read): Q^T A Q = T tridiagonal (Hv: Householder vectors, [nb][k][k]), Z [nb][k][k] column i = the
+// (unnormalised) eigenvector of T for its i-th smallest eigenvalue, *scale -> [nb][k] its 1/norm, and
+// Qt [nb][k][k] = Q^T.  The approximate eigenvectors of A are the columns of Q Z diag(scale).
+// scratch: eig_scratch_floats(k) floats per block (16-byte aligned).
+bool eig_precond_supported(int k);
+size_t eig_scratch_floats(int k);
+cudaError_t launch_eig_precond(int nb, int k, const float* A, float* Hv, float* Z, float* scratch, float* Qt,
+                               const float** scale, cudaStream_t s, int* launches);

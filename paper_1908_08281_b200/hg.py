@@ -134,7 +134,7 @@ def debug_jacobi_sweepmax(on=None):
 
 
 STAGES = ("degrees", "assemble", "omega", "gemm_power", "gemm_gram", "gemm_qform", "gemm_svd", "gemm_apply",
-          "cholinv", "jacobi", "finalize", "inv_sigma")
+          "cholinv", "jacobi", "finalize", "inv_sigma", "cg", "eig_precond")
 
 
 def profile_enable(on=True):

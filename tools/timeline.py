@@ -17,7 +17,8 @@ from paper_1908_08281_b200 import hg  # noqa: E402
 from synth.hypergraph import CONFIGS, make_input  # noqa: E402
 
 LETTER = {"degrees": "d", "assemble": "A", "omega": "o", "gemm_power": "P", "gemm_gram": "g", "gemm_qform": "q",
-          "gemm_svd": "s", "gemm_apply": "a", "cholinv": "C", "jacobi": "J", "finalize": "f", "inv_sigma": "i"}
+          "gemm_svd": "s", "gemm_apply": "a", "cholinv": "C", "jacobi": "J", "finalize": "f", "inv_sigma": "i",
+          "eig_precond": "E"}
 
 
 def main():
