@@ -385,32 +385,86 @@ __global__ void __launch_bounds__(576, 1) k_sytrd(int k, int ntl, const float* _
 }
 
 // ---------------------------------------------------------------- eigenpairs of T
-// One CTA per block, thread per eigenvalue.  (1) T / tn (tn = max |Gershgorin bound|): the
-// division-free Sturm counts stay in range; eigenvectors are unchanged.  (2) Eigenvalues: Sturm-count
-// scans (one point per thread) narrow the interval holding the spectrum, then each thread bisects
-// from its scan bracket to fp32 resolution.  (3) Eigenvectors: INV_IT steps of inverse iteration
-// (LAPACK gttrf/gtts2 elimination with partial pivoting; factors through global scratch, prefetched
-// 8 rows ahead).  Out: Z [nb][k][k] (column i = the unnormalised eigenvector of the i-th smallest
-// eigenvalue), scale [nb][k] (1 / ||Z[:, i]||).
-constexpr int EIG_NT = 256;
+// CTAs of EIG_NT threads, ceil(k / EIG_NT) per block, thread per eigenvalue.  (1) T / tn (tn = max
+// |Gershgorin bound|): the division-free Sturm counts stay in range; eigenvectors are unchanged.
+// (2) Eigenvalues: two scans of NSCAN Sturm counts (4 points per thread) narrow the interval holding
+// the spectrum and bracket every eigenvalue, then each thread bisects to fp32 resolution.
+// (3) Eigenvectors: INV_IT steps of inverse iteration from a pseudo-random start (LAPACK gttrf/gtts2
+// elimination with partial pivoting, branch-free), the iterate in shared memory, the U rows
+// recomputed per SEG-row segment from checkpoints of the forward elimination.
+// Out: Z [nb][k][k], column i = the unit eigenvector of the i-th smallest eigenvalue; scale = 1.
+constexpr int EIG_NT = 64;
 constexpr int SEG = 16;           // inverse iteration: rows per checkpoint segment
-constexpr int SCAN_PASSES = 2;
+constexpr int NSCAN = 256;        // Sturm-count scan points (4 per thread)
 
-__device__ __forceinline__ float e_in_scaled(const float* e_in, int blk, int k, int i) {
-  return i < k - 1 ? e_in[(int64_t)blk * k + i] : 0.f;
+struct TdSmem {   // offsets in 4-byte words
+  int d, e, e2, cnt, red, ck, xs, total;
+};
+__host__ __device__ inline TdSmem td_smem(int k) {
+  TdSmem S;
+  int off = 0;
+  const int kp = (k + 7) / 8 * 8, nseg = (k - 1 + SEG - 1) / SEG + 1;
+  S.d = off; off += kp;
+  S.e = off; off += kp;
+  S.e2 = off; off += kp;
+  S.cnt = off; off += NSCAN;
+  S.red = off; off += 8;
+  S.ck = off; off += nseg * 3 * EIG_NT;
+  S.xs = off; off += k * EIG_NT;
+  S.total = off;
+  return S;
+}
+
+// Sturm counts at 4 points (shared loads of d, e2s amortised over the points)
+__device__ __forceinline__ void sturm_count4(const float* __restrict__ d, const float* __restrict__ e2s, int k,
+                                             const float x[4], int cnt[4]) {
+  float p0[4], p1[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) { p0[u] = 0.f; p1[u] = 1.f; cnt[u] = 0; }
+  for (int i0 = 0; i0 < k; i0 += 8) {
+    const int n = min(8, k - i0);
+    const float4 da = *reinterpret_cast<const float4*>(d + i0), db = *reinterpret_cast<const float4*>(d + i0 + 4);
+    const float4 ea = *reinterpret_cast<const float4*>(e2s + i0), eb = *reinterpret_cast<const float4*>(e2s + i0 + 4);
+    const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+    const float ev[8] = {ea.x, ea.y, ea.z, ea.w, eb.x, eb.y, eb.z, eb.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q < n) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float p2 = fmaf(dv[q] - x[u], p1[u], -ev[q] * p0[u]);
+          cnt[u] += (__float_as_uint(p2) ^ __float_as_uint(p1[u])) >> 31;
+          p0[u] = p1[u];
+          p1[u] = p2;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float m = fmaxf(fabsf(p0[u]), fabsf(p1[u]));
+      const int ex = ((__float_as_int(m) >> 23) & 0xff) - 127;
+      if (ex > 48 || (ex < -48 && m != 0.f)) {
+        const float sc = __int_as_float((127 - ex) << 23);
+        p0[u] *= sc;
+        p1[u] *= sc;
+      }
+    }
+  }
 }
 
 __global__ void __launch_bounds__(EIG_NT) k_trideig(int k, const float* __restrict__ d_in, const float* __restrict__ e_in,
                                                     float* __restrict__ Z, float* __restrict__ scale_out) {
-  extern __shared__ float ckpt[];   // [ceil((k-1)/SEG)][3][EIG_NT] inverse-iteration checkpoints
-  __shared__ __align__(16) float d[256];
-  __shared__ __align__(16) float e[256];
-  __shared__ __align__(16) float e2[256];
-  __shared__ int cnt[EIG_NT];
-  __shared__ float red[2 * (EIG_NT / 32)];
+  extern __shared__ __align__(16) float tsm[];
+  const TdSmem S = td_smem(k);
+  float* d = tsm + S.d;
+  float* e = tsm + S.e;
+  float* e2 = tsm + S.e2;   // e2[i] = e_{i-1}^2 (the Sturm recurrence's shifted layout), e2[0] = 0
+  int* cnt = reinterpret_cast<int*>(tsm + S.cnt);
+  float* red = tsm + S.red;
   const int blk = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  constexpr int NWE = EIG_NT / 32;
-  for (int i = t; i < 256; i += EIG_NT) {
+  const int ev_i = blockIdx.y * EIG_NT + t;   // this thread's eigenvalue index
+  const int kp = (k + 7) / 8 * 8;
+  for (int i = t; i < kp; i += EIG_NT) {
     d[i] = i < k ? d_in[(int64_t)blk * k + i] : 0.f;
     e[i] = i < k - 1 ? e_in[(int64_t)blk * k + i] : 0.f;
   }
@@ -427,124 +481,119 @@ __global__ void __launch_bounds__(EIG_NT) k_trideig(int k, const float* __restri
     gmin = fminf(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
     gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
   }
-  if (lane == 0) { red[warp] = gmin; red[NWE + warp] = gmax; }
+  if (lane == 0) { red[warp] = gmin; red[4 + warp] = gmax; }
   __syncthreads();
-  gmin = red[0];
-  gmax = red[NWE];
-  for (int w = 1; w < NWE; ++w) { gmin = fminf(gmin, red[w]); gmax = fmaxf(gmax, red[NWE + w]); }
+  gmin = fminf(red[0], red[1]);
+  gmax = fmaxf(red[4], red[5]);
   float tn = fmaxf(fabsf(gmin), fabsf(gmax));
   if (!(tn > 0.f) || !isfinite(tn)) tn = 1.f;
   const float itn = 1.f / tn;
+  for (int i = t; i < kp; i += EIG_NT) {
+    const float em = (i > 0 && i < k) ? e_in[(int64_t)blk * k + i - 1] * itn : 0.f;
+    e2[i] = em * em;
+  }
   __syncthreads();
-  __syncthreads();
-  for (int i = t; i < 256; i += EIG_NT) {
+  for (int i = t; i < kp; i += EIG_NT) {
     d[i] *= itn;
     e[i] *= itn;
-    const float em = i > 0 ? e_in_scaled(e_in, blk, k, i - 1) * itn : 0.f;
-    e2[i] = em * em;   // e2[i] = e_{i-1}^2 (the Sturm recurrence's shifted layout)
   }
   __syncthreads();
   const float pad = 4.f * FLT_EPSILON;
   float glo = gmin * itn - pad, ghi = gmax * itn + pad;
-  auto pt = [&](float lo_, float hi_, int m) { return lo_ + (hi_ - lo_) * (float)(m + 1) / (float)(EIG_NT + 1); };
-  for (int pass = 0; pass < SCAN_PASSES; ++pass) {
-    cnt[t] = sturm_count(d, e2, k, pt(glo, ghi, t));
+  auto pt = [&](float lo_, float hi_, int m) { return lo_ + (hi_ - lo_) * (float)(m + 1) / (float)(NSCAN + 1); };
+  for (int pass = 0; pass < 2; ++pass) {
+    float xq[4];
+    int cq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xq[u] = pt(glo, ghi, 4 * t + u);
+    sturm_count4(d, e2, k, xq, cq);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cnt[4 * t + u] = cq[u];
     __syncthreads();
-    if (pass + 1 == SCAN_PASSES) break;
+    if (pass == 1) break;
     // occupied part: from the last point with count 0 to the first with count k (counts are
     // non-decreasing in x up to rounding; binary searches)
-    int a = 0, b = EIG_NT;
+    int a = 0, b = NSCAN;
     while (a < b) { const int m = (a + b) >> 1; if (cnt[m] > 0) b = m; else a = m + 1; }
     const int f0 = a;
-    a = 0; b = EIG_NT;
+    a = 0; b = NSCAN;
     while (a < b) { const int m = (a + b) >> 1; if (cnt[m] >= k) b = m; else a = m + 1; }
     const int fk = a;
     const float nlo = f0 > 0 ? pt(glo, ghi, f0 - 1) : glo;
-    const float nhi = fk < EIG_NT ? pt(glo, ghi, fk) : ghi;
+    const float nhi = fk < NSCAN ? pt(glo, ghi, fk) : ghi;
     __syncthreads();
     glo = nlo;
     ghi = nhi;
   }
-  if (t >= k) return;
+  if (ev_i >= k) return;   // no barrier below
   float lo, hi;
   {
-    int a = 0, b = EIG_NT;   // first scan point with count > t
-    while (a < b) { const int m = (a + b) >> 1; if (cnt[m] > t) b = m; else a = m + 1; }
+    int a = 0, b = NSCAN;   // first scan point with count > ev_i
+    while (a < b) { const int m = (a + b) >> 1; if (cnt[m] > ev_i) b = m; else a = m + 1; }
     lo = a > 0 ? pt(glo, ghi, a - 1) : glo;
-    hi = a < EIG_NT ? pt(glo, ghi, a) : ghi;
+    hi = a < NSCAN ? pt(glo, ghi, a) : ghi;
   }
   for (int it = 0; it < 40; ++it) {
     const float mid = 0.5f * (lo + hi);
     if (!(mid > lo && mid < hi)) break;   // fp32 resolution
-    if (sturm_count(d, e2, k, mid) > t) hi = mid;
+    if (sturm_count(d, e2, k, mid) > ev_i) hi = mid;
     else lo = mid;
   }
   const float lam = 0.5f * (lo + hi);
   EIG_CLK(4);
 
-  // Inverse iteration without factor storage: the forward elimination keeps a checkpoint of its
-  // working row (w0, w1, rhs) every SEG rows in shared memory; the back substitution walks the
-  // segments from the last, recomputing each segment's U rows from its checkpoint into registers.
-  // The right-hand side of iteration it >= 1 is the previous iterate (Z, read ahead of the rows the
-  // back substitution overwrites).
+  // Inverse iteration.  The iterate lives in shared memory (xs[row][thread]); the forward elimination
+  // keeps a checkpoint of its working row (w0, w1, rhs) every SEG rows and the back substitution walks
+  // the segments from the last, recomputing each segment's U rows into registers.  A segment reads
+  // the right-hand sides of rows base + 1 .. base + SEG, the first of the next segment's rows (already
+  // overwritten by the new iterate) is carried over in a register.
   const float eps_piv = FLT_EPSILON;   // replaces an exactly zero pivot (T normalised: ||T|| ~ 1)
-  float* Zb = Z + (int64_t)blk * k * k;   // [row][k]: column t = this eigenvector
-  float* ck = ckpt + t;                   // [seg][3][EIG_NT]
-  float rscale = 1.f;
-  // one elimination step on rows (r, r + 1): working row (w0, w1 | rw) against row r + 1 (a0, a1, a2 | ra);
-  // returns the U row (1/u0, u1, u2, ru)
+  float* xs = tsm + S.xs + t;          // xs[r * EIG_NT]
+  float* ck = tsm + S.ck + t;          // [seg][3][EIG_NT]
+  // one elimination step on rows (r, r + 1) (branch-free partial pivoting): working row (w0, w1 | rw)
+  // against row r + 1 (e_r, d_{r+1} - lam, e_{r+1} | ra); returns the U row (1/u0, u1, u2, ru)
   auto elim = [&](int r, float& w0, float& w1, float& rw, float ra) {
     const float a0 = e[r], a1 = d[r + 1] - lam, a2 = e[r + 1];
-    float4 f;
-    if (fabsf(w0) >= fabsf(a0)) {   // pivot: the working row
-      if (w0 == 0.f) w0 = eps_piv;
-      const float l = __fdividef(a0, w0);
-      f = make_float4(__fdividef(1.f, w0), w1, 0.f, rw);
-      w0 = fmaf(-l, w1, a1);
-      w1 = a2;
-      rw = fmaf(-l, rw, ra);
-    } else {                         // interchange: pivot on row r + 1
-      const float l = __fdividef(w0, a0);
-      f = make_float4(__fdividef(1.f, a0), a1, a2, ra);
-      w0 = fmaf(-l, a1, w1);
-      w1 = -l * a2;
-      rw = fmaf(-l, ra, rw);
-    }
+    const bool pv = fabsf(w0) >= fabsf(a0);
+    float den = pv ? w0 : a0;
+    if (den == 0.f) den = eps_piv;
+    const float inv = __fdividef(1.f, den);
+    const float l = (pv ? a0 : w0) * inv;
+    const float4 f = make_float4(inv, pv ? w1 : a1, pv ? 0.f : a2, pv ? rw : ra);
+    const float n0 = fmaf(-l, pv ? w1 : a1, pv ? a1 : w1);
+    const float n1 = pv ? a2 : -l * a2;
+    rw = fmaf(-l, pv ? rw : ra, pv ? ra : rw);
+    w0 = n0;
+    w1 = n1;
     return f;
   };
+  for (int r = 0; r < k; ++r) xs[r * EIG_NT] = start_vec(r, ev_i);
+  const int nseg = (k - 1 + SEG - 1) / SEG;
+  float rscale = 1.f;
   for (int it = 0; it < INV_IT; ++it) {
-    auto rhs = [&](int r) { return r < k ? (it == 0 ? start_vec(r, t) : Zb[(int64_t)r * k + t] * rscale) : 0.f; };
-    // forward: rows 0 .. k-2 (step r eliminates row r + 1), checkpoints before steps 0, SEG, 2 SEG, ...
-    float rb[SEG], nb[SEG];
-#pragma unroll
-    for (int q = 0; q < SEG; ++q) rb[q] = rhs(1 + q);
-    float w0 = d[0] - lam, w1 = k > 1 ? e[0] : 0.f, rw = rhs(0);
-    for (int base = 0; base + 1 < k; base += SEG) {
-#pragma unroll
-      for (int q = 0; q < SEG; ++q) nb[q] = rhs(base + SEG + 1 + q);   // next segment's right-hand sides
-      ck[(base / SEG) * 3 * EIG_NT] = w0;
-      ck[(base / SEG) * 3 * EIG_NT + EIG_NT] = w1;
-      ck[(base / SEG) * 3 * EIG_NT + 2 * EIG_NT] = rw;
+    float w0 = d[0] - lam, w1 = k > 1 ? e[0] : 0.f, rw = xs[0] * rscale;
+    for (int sg = 0; sg < nseg; ++sg) {
+      const int base = sg * SEG;
+      ck[sg * 3 * EIG_NT] = w0;
+      ck[sg * 3 * EIG_NT + EIG_NT] = w1;
+      ck[sg * 3 * EIG_NT + 2 * EIG_NT] = rw;
 #pragma unroll
       for (int q = 0; q < SEG; ++q)
-        if (base + q + 1 < k) elim(base + q, w0, w1, rw, rb[q]);
-#pragma unroll
-      for (int q = 0; q < SEG; ++q) rb[q] = nb[q];
+        if (base + q + 1 < k) elim(base + q, w0, w1, rw, xs[(base + q + 1) * EIG_NT] * rscale);
     }
     if (w0 == 0.f) w0 = eps_piv;
     float x1 = rw / w0, x2 = 0.f;   // x_{r+1}, x_{r+2}
     const float xlast = x1;
     float nrm2 = x1 * x1;
-    // backward, segment by segment
-    const int nseg = (k - 1 + SEG - 1) / SEG;
-#pragma unroll
-    for (int q = 0; q < SEG; ++q) rb[q] = rhs((nseg - 1) * SEG + 1 + q);
+    const int top = (nseg - 1) * SEG + SEG;
+    float carry = top < k ? xs[top * EIG_NT] * rscale : 0.f;
     for (int sg = nseg - 1; sg >= 0; --sg) {
       const int base = sg * SEG;
-      if (sg > 0) {
+      float rb[SEG];
 #pragma unroll
-        for (int q = 0; q < SEG; ++q) nb[q] = rhs(base - SEG + 1 + q);   // read before this segment writes
-      }
+      for (int q = 0; q < SEG - 1; ++q) rb[q] = (base + q + 1 < k) ? xs[(base + q + 1) * EIG_NT] * rscale : 0.f;
+      rb[SEG - 1] = carry;
+      carry = xs[base * EIG_NT] * rscale;   // row base's right-hand side, for segment sg - 1
       float u0[SEG], u1[SEG], u2[SEG], ru[SEG];
       float sw0 = ck[sg * 3 * EIG_NT], sw1 = ck[sg * 3 * EIG_NT + EIG_NT], srw = ck[sg * 3 * EIG_NT + 2 * EIG_NT];
 #pragma unroll
@@ -559,20 +608,20 @@ __global__ void __launch_bounds__(EIG_NT) k_trideig(int k, const float* __restri
         const int r = base + q;
         if (r + 1 < k) {
           const float x = (ru[q] - u1[q] * x1 - u2[q] * x2) * u0[q];
-          Zb[(int64_t)r * k + t] = x;
+          xs[r * EIG_NT] = x;
           nrm2 = fmaf(x, x, nrm2);
           x2 = x1;
           x1 = x;
         }
       }
-#pragma unroll
-      for (int q = 0; q < SEG; ++q) rb[q] = nb[q];
     }
-    Zb[(int64_t)(k - 1) * k + t] = xlast;
+    xs[(k - 1) * EIG_NT] = xlast;
     rscale = nrm2 > 0.f ? rsqrtf(nrm2) : 0.f;
     EIG_CLK(5 + it);
   }
-  scale_out[(int64_t)blk * k + t] = rscale;
+  float* Zb = Z + (int64_t)blk * k * k;   // [row][k]: column ev_i = this eigenvector
+  for (int r = 0; r < k; ++r) Zb[(int64_t)r * k + ev_i] = xs[r * EIG_NT] * rscale;
+  scale_out[(int64_t)blk * k + ev_i] = 1.f;
 }
 
 // Q^T with Q = H_0 H_1 ... H_{k-3} (LAPACK orgtr, backward accumulation): column c of Q is
@@ -665,10 +714,10 @@ cudaError_t launch_eig_precond(int nb, int k, const float* A, float* Hv, float* 
   ++*launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const size_t ck_bytes = (size_t)((k - 1 + SEG - 1) / SEG + 1) * 3 * EIG_NT * 4;
-  e = cudaFuncSetAttribute(k_trideig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ck_bytes);
+  const size_t td_bytes = (size_t)td_smem(k).total * 4;
+  e = cudaFuncSetAttribute(k_trideig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)td_bytes);
   if (e != cudaSuccess) return e;
-  k_trideig<<<nb, EIG_NT, ck_bytes, s>>>(k, dd, ee, Z, sc);
+  k_trideig<<<dim3(nb, (k + EIG_NT - 1) / EIG_NT), EIG_NT, td_bytes, s>>>(k, dd, ee, Z, sc);
   ++*launches;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
