@@ -372,6 +372,288 @@ __global__ void __launch_bounds__(ROWS_NT) k_assemble_rows(int blk0, int b, cons
                      blocks + (int64_t)blk * b * b, acc, stage, lane, warp);
 }
 
+
+// ---------------------------------------------------------------------------
+// Per-block radix assembly (default when E < 2^17 and a block's incidences fit in shared
+// memory; other blocks take the hashed-tile kernel, problems with E >= 2^17 the segmented path).
+//   k_block_sort: one CTA per block.  The block's incidences (u, e) as keys e << 15 | idx
+//   (idx = position in the block's CSR range) are stably radix-sorted by e (LSD, 3 passes of
+//   6/6/5 bits, warp-ordered chunks, ranks by __match_any_sync: deterministic), so each edge's
+//   members in the block become one run, in ascending vertex order.  Out: memb[p0 + j] = the
+//   block-local vertex of sorted entry j; rng[p] = the run [start, end) (relative to p0) of the
+//   members of incidence p's edge.
+//   k_assemble_rows2: one CTA per (block, 16 rows), a warp per row u walks u's edges in
+//   ascending order and adds w_e/delta(e) to acc[u][v] for the members v.  Heavy edges (>= 32
+//   members in the block) with all lanes; a run of light edges as one batch of (edge, member)
+//   pairs -- pairs with the same v are applied by one lane, in ascending edge order, to the
+//   running acc[v]: every entry sees exactly the sequence of fp32 additions of the edge-by-edge
+//   walk (bitwise equal to k_assemble and k_assemble_rows; blocks bitwise symmetric).
+constexpr int BR_NT = 1024;
+constexpr int BR_NW = BR_NT / 32;
+constexpr int BR_IDXB = 15;                  // idx bits of a key
+constexpr int BR_CAP = 25600;                // incidences per block (2 x 100 KB key buffers)
+constexpr int R2_NT = 512;                   // k_assemble_rows2: one warp per row
+constexpr int R2_ROWS = R2_NT / 32;
+constexpr int HEAVY = 32;                    // members of an edge in the block for the all-lanes path
+
+__global__ void __launch_bounds__(BR_NT, 1) k_block_sort(int blk0, int b, const int64_t* __restrict__ row_ptr,
+                                                         const int32_t* __restrict__ col, uint32_t* __restrict__ memb,
+                                                         int2* __restrict__ rng, int32_t* __restrict__ overflow) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint32_t* kA = reinterpret_cast<uint32_t*>(smem_raw);                    // [BR_CAP]
+  uint32_t* kB = kA + BR_CAP;                                              // [BR_CAP]
+  int* vp = reinterpret_cast<int*>(kB + BR_CAP);                           // [b + 1] CSR offsets rel. p0
+  int* hist = vp + 2049;                                                   // [64][BR_NW]
+  int* wtot = hist + 64 * BR_NW;                                           // [BR_NW]
+  const int blk = blk0 + blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t vb = (int64_t)blk * b;
+  const int64_t p0 = row_ptr[vb];
+  const int64_t n64 = row_ptr[vb + b] - p0;
+  if (n64 > BR_CAP) {   // handled by the hashed-tile kernel
+    if (t == 0) overflow[blk] = 1;
+    return;
+  }
+  const int n = (int)n64;
+  for (int i = t; i <= b; i += BR_NT) vp[i] = (int)(row_ptr[vb + i] - p0);
+  for (int i = t; i < n; i += BR_NT) kA[i] = ((uint32_t)col[p0 + i] << BR_IDXB) | (uint32_t)i;
+  __syncthreads();
+  // LSD passes over the edge bits [15, 21), [21, 27), [27, 32)
+  const int chunk = (n + BR_NW - 1) / BR_NW;
+  const int c0 = warp * chunk, c1 = min(n, c0 + chunk);
+  uint32_t* src = kA;
+  uint32_t* dst = kB;
+  for (int pass = 0; pass < 3; ++pass) {
+    const int shift = BR_IDXB + 6 * pass, nb = pass < 2 ? 64 : 32;
+    for (int i = t; i < 64 * BR_NW; i += BR_NT) hist[i] = 0;
+    __syncthreads();
+    for (int g = c0; g < c1; g += 32) {   // per-warp digit counts (no atomics: one leader per digit)
+      const int i = g + lane;
+      const unsigned act = __ballot_sync(0xffffffffu, i < c1);
+      if (i < c1) {
+        const int dg = (int)((src[i] >> shift) & (nb - 1));
+        const unsigned m = __match_any_sync(act, dg);
+        if (lane == __ffs(m) - 1) hist[dg * BR_NW + warp] += __popc(m);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // exclusive scan over (digit, warp) in digit-major order: 2048 entries, 2 per thread
+    {
+      const int i0 = 2 * t;
+      const int a0 = hist[i0], a1 = hist[i0 + 1];
+      int s = a0 + a1, x = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wtot[warp] = x;
+      __syncthreads();
+      int pre = 0;
+      for (int w = 0; w < warp; ++w) pre += wtot[w];
+      const int ex = pre + x - s;
+      hist[i0] = ex;
+      hist[i0 + 1] = ex + a0;
+    }
+    __syncthreads();
+    for (int g = c0; g < c1; g += 32) {   // stable scatter
+      const int i = g + lane;
+      const unsigned act = __ballot_sync(0xffffffffu, i < c1);
+      int dg = 0, pos = 0;
+      unsigned m = 0;
+      uint32_t key = 0;
+      if (i < c1) {
+        key = src[i];
+        dg = (int)((key >> shift) & (nb - 1));
+        m = __match_any_sync(act, dg);
+        pos = hist[dg * BR_NW + warp] + __popc(m & ((1u << lane) - 1u));
+      }
+      __syncwarp();
+      if (i < c1) {
+        dst[pos] = key;
+        if (lane == __ffs(m) - 1) hist[dg * BR_NW + warp] += __popc(m);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    uint32_t* tmp = src; src = dst; dst = tmp;
+  }
+  // src: sorted.  Runs of equal edge: start flags, then per entry its run [rs, re) by a block max-scan
+  // of starts (forward) and min-scan of ends (backward); contiguous chunks per thread.
+  const int per = (n + BR_NT - 1) / BR_NT;
+  const int j0 = t * per, j1 = min(n, j0 + per);
+  int last_start = -1;                 // the last run start within this thread's chunk
+  for (int j = j0; j < j1; ++j)
+    if (j == 0 || (src[j] >> BR_IDXB) != (src[j - 1] >> BR_IDXB)) last_start = j;
+  int first_start = n;                 // the first run start strictly after this thread's chunk start
+  for (int j = j1 - 1; j >= j0; --j)
+    if (j == 0 || (src[j] >> BR_IDXB) != (src[j - 1] >> BR_IDXB)) first_start = j;
+  // inclusive max-scan of last_start over threads, exclusive min-scan (from the right) of first_start
+  int mx = last_start, mn = first_start;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, mx, o);
+    if (lane >= o) mx = max(mx, y);
+    const int z = __shfl_down_sync(0xffffffffu, mn, o);
+    if (lane + o < 32) mn = min(mn, z);
+  }
+  __syncthreads();   // hist / wtot reuse below
+  int* wmax = hist;
+  int* wmin = hist + BR_NW;
+  if (lane == 31) wmax[warp] = mx;
+  if (lane == 0) wmin[warp] = mn;
+  __syncthreads();
+  int before = -1, after = n;   // last start before my chunk / first start after my chunk
+  for (int w = 0; w < warp; ++w) before = max(before, wmax[w]);
+  for (int w = warp + 1; w < BR_NW; ++w) after = min(after, wmin[w]);
+  {
+    const int xm = __shfl_up_sync(0xffffffffu, mx, 1);
+    if (lane > 0) before = max(before, xm);
+    const int xn = __shfl_down_sync(0xffffffffu, mn, 1);
+    if (lane < 31) after = min(after, xn);
+  }
+  // walk the chunk: rs = current run start, re = next run start
+  int rs = before;
+  int re_next = after;   // first start after the chunk
+  // ends: for j in chunk, re = the next start > j: scan backward
+  for (int j = j1 - 1; j >= j0; --j) {
+    const bool st = (j == 0 || (src[j] >> BR_IDXB) != (src[j - 1] >> BR_IDXB));
+    dst[j] = (uint32_t)re_next;        // run end of entry j (dst is free now)
+    if (st) re_next = j;
+  }
+  for (int j = j0; j < j1; ++j) {
+    const uint32_t key = src[j];
+    if (j == 0 || (key >> BR_IDXB) != (src[j - 1] >> BR_IDXB)) rs = j;
+    const int idx = (int)(key & ((1u << BR_IDXB) - 1u));
+    int lo = 0, hi = b;                // vertex of incidence idx: vp[lo] <= idx < vp[lo + 1]
+    while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (vp[mid] <= idx) lo = mid; else hi = mid; }
+    memb[p0 + j] = (uint32_t)lo;
+    rng[p0 + idx] = make_int2(rs, (int)dst[j]);
+  }
+}
+
+__global__ void __launch_bounds__(R2_NT) k_assemble_rows2(int blk0, int b, const int64_t* __restrict__ row_ptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const uint32_t* __restrict__ memb,
+                                                          const int2* __restrict__ rng,
+                                                          const float* __restrict__ eval,
+                                                          const float* __restrict__ dvr, float inv1pmu, int raw,
+                                                          float* __restrict__ blocks,
+                                                          const int32_t* __restrict__ overflow) {
+  const int blk = blk0 + blockIdx.x;
+  if (overflow[blk]) return;                      // handled by the hashed-tile kernel
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  float* acc = reinterpret_cast<float*>(smem_raw);   // [R2_ROWS][b]
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  float* stc = reinterpret_cast<float*>(smem_raw + (size_t)R2_ROWS * b * 4) + warp * 32;   // per-warp pair values
+  const int64_t base = (int64_t)blk * b;
+  const int u0 = blockIdx.y * R2_ROWS;
+  const int uu = u0 + warp;
+  for (int i = t; i < R2_ROWS * b; i += R2_NT) acc[i] = 0.f;
+  __syncthreads();
+  if (uu >= b) return;
+  const int64_t p0 = row_ptr[base];
+  const uint32_t* M = memb + p0;
+  float* arow = acc + (size_t)warp * b;
+  const int64_t q0 = row_ptr[base + uu], q1 = row_ptr[base + uu + 1];
+  for (int64_t c0 = q0; c0 < q1; c0 += 32) {
+    const int ne = (int)((q1 - c0) < 32 ? (q1 - c0) : 32);
+    float val = 0.f;
+    int rs = 0, len = 0;
+    if (lane < ne) {
+      const int2 r = rng[c0 + lane];
+      rs = r.x;
+      len = r.y - r.x;
+      val = eval[col[c0 + lane]];
+    }
+    const unsigned heavy = __ballot_sync(0xffffffffu, lane < ne && len >= HEAVY);
+    int i = 0;
+    while (i < ne) {
+      if ((heavy >> i) & 1u) {   // heavy edge: all lanes, distinct members
+        const float c = __shfl_sync(0xffffffffu, val, i);
+        const int s = __shfl_sync(0xffffffffu, rs, i), l = __shfl_sync(0xffffffffu, len, i);
+        int m = lane;
+        for (; m + 96 < l; m += 128) {   // four loads in flight
+          const uint32_t v0 = M[s + m], v1 = M[s + m + 32], v2 = M[s + m + 64], v3 = M[s + m + 96];
+          arow[v0] += c;
+          arow[v1] += c;
+          arow[v2] += c;
+          arow[v3] += c;
+        }
+        for (; m < l; m += 32) arow[M[s + m]] += c;
+        __syncwarp();
+        ++i;
+        continue;
+      }
+      // a run of light edges [i, i1): (edge, member) pairs in ascending edge order
+      const unsigned hv = heavy & ~((2u << i) - 1u);   // heavy edges after i
+      const int i1 = hv ? (__ffs(hv) - 1) : ne;
+      const int ln = (lane >= i && lane < i1) ? len : 0;
+      int incl = ln;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      for (int q0p = 0; q0p < total; q0p += 32) {
+        const int q = q0p + lane;
+        // edge of pair q: the first lane with incl > q (binary search over the lanes' prefixes)
+        int lo = 0;
+#pragma unroll
+        for (int st = 16; st; st >>= 1) {
+          const int y = __shfl_sync(0xffffffffu, incl, lo + st - 1);
+          if (y <= q) lo += st;
+        }
+        const int ex = __shfl_sync(0xffffffffu, incl - ln, lo & 31);
+        const int s = __shfl_sync(0xffffffffu, rs, lo & 31);
+        const float c = __shfl_sync(0xffffffffu, val, lo & 31);
+        const bool act = q < total;
+        const uint32_t v = act ? M[s + (q - ex)] : 0xffffffffu;
+        stc[lane] = c;
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        __syncwarp();
+        if (act) {
+          const unsigned m = __match_any_sync(am, v);
+          if (lane == __ffs(m) - 1) {   // leader: this v's pairs in ascending edge order
+            float x = arow[v];
+            unsigned mm = m;
+            while (mm) {
+              const int l = __ffs(mm) - 1;
+              mm &= mm - 1;
+              x += stc[l];
+            }
+            arow[v] = x;
+          }
+        }
+        __syncwarp();
+      }
+      i = i1;
+    }
+  }
+  __syncwarp();
+  const float du = dvr[base + uu];
+  float* orow = blocks + (int64_t)blk * b * b + (int64_t)uu * b;
+  const float* dv = dvr + base;
+  for (int v4 = lane; v4 < b / 4; v4 += 32) {
+    const float4 a = *reinterpret_cast<const float4*>(arow + 4 * v4);
+    const float4 r = *reinterpret_cast<const float4*>(dv + 4 * v4);
+    const int v = 4 * v4;
+    float4 o;
+    o.x = (du * r.x) * a.x;
+    o.y = (du * r.y) * a.y;
+    o.z = (du * r.z) * a.z;
+    o.w = (du * r.w) * a.w;
+    if (!raw) {
+      o.x = ((uu == v + 0) ? 1.0f : 0.0f) - o.x * inv1pmu;
+      o.y = ((uu == v + 1) ? 1.0f : 0.0f) - o.y * inv1pmu;
+      o.z = ((uu == v + 2) ? 1.0f : 0.0f) - o.z * inv1pmu;
+      o.w = ((uu == v + 3) ? 1.0f : 0.0f) - o.w * inv1pmu;
+    }
+    *reinterpret_cast<float4*>(orow + v) = o;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_degrees(int N, int E, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
@@ -407,10 +689,33 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
                                       al256((size_t)nb_total * 4));
   // HG_ASSEMBLE=tiles forces the hashed-tile kernel (verification: both paths are bit-identical)
   const char* force = getenv("HG_ASSEMBLE");
-  const bool sorted_ok = (uint64_t)E * (uint64_t)b < (1ull << 32) && b <= 4 * SEG_V && !(force && force[0] == 't');
-  cudaError_t e = cudaMemsetAsync(overflow + blk0, sorted_ok ? 0 : 1, sizeof(int32_t) * nb, s);
+  const bool tiles = force && force[0] == 't';
+  const bool radix_ok = E < (1 << 17) && b <= 2048 && !tiles && !(force && force[0] == 's');
+  const bool sorted_ok = (uint64_t)E * (uint64_t)b < (1ull << 32) && b <= 4 * SEG_V && !tiles;
+  cudaError_t e = cudaMemsetAsync(overflow + blk0, (radix_ok || sorted_ok) ? 0 : 1, sizeof(int32_t) * nb, s);
   if (e != cudaSuccess) return e;
-  if (sorted_ok) {
+  if (radix_ok) {
+    // per-block radix sort + batched row walk (HG_ASSEMBLE=segments: the segmented path below)
+    const size_t ssmem = (size_t)2 * BR_CAP * 4 + 2049 * 4 + 64 * BR_NW * 4 + BR_NW * 4;
+    static bool attr0 = false;
+    if (!attr0) {
+      e = cudaFuncSetAttribute(k_block_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+      if (e != cudaSuccess) return e;
+      attr0 = true;
+    }
+    k_block_sort<<<nb, BR_NT, ssmem, s>>>(blk0, b, row_ptr, col_idx, keys, rng, overflow);
+    const size_t smem = (size_t)R2_ROWS * b * 4 + (size_t)R2_ROWS * 32 * 4;
+    static size_t attr3 = 0;
+    if (smem > attr3) {
+      e = cudaFuncSetAttribute(k_assemble_rows2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr3 = smem;
+    }
+    k_assemble_rows2<<<dim3(nb, (b + R2_ROWS - 1) / R2_ROWS), R2_NT, smem, s>>>(
+        blk0, b, row_ptr, col_idx, keys, rng, edge_val, dv_rsqrt, 1.0f / (1.0f + mu), raw_theta ? 1 : 0, blocks,
+        overflow);
+    *launches += 2;
+  } else if (sorted_ok) {
     const int nseg = (b + SEG_V - 1) / SEG_V;
     const size_t ssmem = (size_t)(SEG_V + 2) * 8 + (size_t)SEG_CAP * 4;
     static bool attr1 = false;

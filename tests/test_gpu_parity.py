@@ -116,8 +116,8 @@ def test_theta_blocks_parity(inputs, cfg):
 
 @pytest.mark.parametrize("cfg", [1, 2, 4])
 def test_assembly_paths_bit_identical(inputs, cfg, monkeypatch):
-    """The sorted-CSC row kernel and the hashed-tile kernel add the same terms in
-    the same order (ascending edge id per (u, v)): identical bits."""
+    """The radix-sorted row kernel (default), the segment-sorted row kernel and the hashed-tile
+    kernel add the same terms in the same order (ascending edge id per (u, v)): identical bits."""
     hg = hgm()
     h = inputs(cfg)
     c = CONFIGS[cfg]
@@ -126,9 +126,12 @@ def test_assembly_paths_bit_identical(inputs, cfg, monkeypatch):
     X1, _, s1 = hg.build_theta(H, w, c.mu, c.b)
     monkeypatch.setenv("HG_ASSEMBLE", "tiles")
     X2, _, s2 = hg.build_theta(H, w, c.mu, c.b)
+    monkeypatch.setenv("HG_ASSEMBLE", "segments")   # the per-segment bitonic-sort path
+    X3, _, s3 = hg.build_theta(H, w, c.mu, c.b)
     monkeypatch.delenv("HG_ASSEMBLE")
-    assert int(s1.item()) == 0 and int(s2.item()) == 0
+    assert int(s1.item()) == 0 and int(s2.item()) == 0 and int(s3.item()) == 0
     assert torch.equal(X1, X2)
+    assert torch.equal(X1, X3)
 
 
 def test_theta_error_flags():
