@@ -132,7 +132,7 @@ Layout layout(int64_t N, int64_t E, int64_t nnz, int64_t b, int64_t k, int64_t T
   L.de = take(4 * E);
   L.eval = take(4 * E);
   L.dvr = take(4 * N);
-  L.keys = take(assemble_keys_bytes(nnz, (int)nb));
+  L.keys = take(assemble_keys_bytes(nnz, (int)nb, (int)E));
   L.blocks = take(4 * nb * b * b);
   for (int i = 0; i < 4; ++i) L.P[i] = take(4 * nb * k * b);
   L.Ut = take(4 * nb * k * b);
@@ -491,12 +491,17 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
   return HG_OK;
 }
 
-hg_status run_degrees(const hg_incidence* H, const float* w, float* dvr, int32_t* st, void* ws, const Layout& Lo,
-                      cudaStream_t s) {
+// degrees and, for the grouped assembly, the (block, edge) grouping of the incidences of
+// all N/b blocks -- both before the stream parts fork
+hg_status run_degrees(const hg_incidence* H, const float* w, int b, float* dvr, int32_t* st, void* ws,
+                      const Layout& Lo, cudaStream_t s) {
   ProfScope ps(ST_DEGREES, s);
   HG_CU(launch_degrees(H->n_vertices, H->n_edges, H->nnz, H->row_ptr, H->col_idx, w, at<int32_t>(ws, Lo.de),
                        at<float>(ws, Lo.eval), dvr, st, s, &g_launches),
         "degrees");
+  HG_CU(launch_assemble_group(H->n_vertices / b, b, H->n_edges, H->nnz, H->row_ptr, H->col_idx,
+                              at<void>(ws, Lo.keys), s, &g_launches),
+        "assembly grouping");
   return HG_OK;
 }
 
@@ -513,7 +518,7 @@ hg_status run_assemble(const hg_incidence* H, float mu, int b, bool raw, int blk
 hg_status run_theta(const hg_incidence* H, const float* w, float mu, int b, bool raw, float* blocks, float* dvr_out,
                     int32_t* st, void* ws, const Layout& Lo, cudaStream_t s) {
   float* dvr = dvr_out ? dvr_out : at<float>(ws, Lo.dvr);
-  HG_TRY(run_degrees(H, w, dvr, st, ws, Lo, s));
+  HG_TRY(run_degrees(H, w, b, dvr, st, ws, Lo, s));
   return run_assemble(H, mu, b, raw, 0, H->n_vertices / b, blocks, dvr, ws, Lo, s);
 }
 
@@ -655,7 +660,7 @@ hg_status hg_build_theta(const hg_incidence* H, const float* w, float mu, int32_
   if (!(mu > 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and > 0");
   if (!w || !blocks || !d_status) return fail(HG_ERR_INVALID, "NULL pointer argument");
   const Layout Lo = layout(H->n_vertices, H->n_edges, H->nnz, b, 4, 0);
-  HG_TRY(check_ws(ws, ws_bytes, Lo.keys + assemble_keys_bytes(H->nnz, H->n_vertices / b)));
+  HG_TRY(check_ws(ws, ws_bytes, Lo.keys + assemble_keys_bytes(H->nnz, H->n_vertices / b, H->n_edges)));
   return run_theta(H, w, mu, b, (flags & HG_RAW_THETA) != 0, blocks, dv_rsqrt, d_status, ws, Lo,
                    reinterpret_cast<cudaStream_t>(stream));
 }
@@ -879,7 +884,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   float* sigma = sig_user ? sigma_out : at<float>(ws, p == 0 ? Lo.sigma : Lo.sigl);
   const int soff = sig_user ? rb0 : 0;
   float* dvr = at<float>(ws, Lo.dvr);
-  HG_TRY(run_degrees(H, w, dvr, st, ws, Lo, s));
+  HG_TRY(run_degrees(H, w, b, dvr, st, ws, Lo, s));
   // Blocks are independent (reading A5): the assembly, rSVD and apply of disjoint block ranges run
   // on forked streams, so one part's tensor-core GEMMs fill the SMs that the other
   // part's latency-bound Cholesky / Jacobi leave idle.  Bitwise the same result for
@@ -1336,7 +1341,7 @@ static hg_status schur_impl(const hg_incidence* H, const float* w, float mu, int
   float* Vscratch = at<float>(ws, S.R.Vt);
   // 1. Theta_ii (raw) and the off-diagonal Theta_{2s,2s+1} from the sorted CSC
   float* dvr = at<float>(ws, S.R.dvr);
-  HG_TRY(run_degrees(H, w, dvr, st, ws, S.R, s));
+  HG_TRY(run_degrees(H, w, b, dvr, st, ws, S.R, s));
   HG_TRY(run_assemble(H, mu, b, true, 0, (int)nb, blocks, dvr, ws, S.R, s));
   void* cws = static_cast<char*>(ws) + S.cg_off;
   CgArgs ca;

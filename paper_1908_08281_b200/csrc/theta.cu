@@ -654,6 +654,202 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows2(int blk0, int b, const
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Grouped assembly (default when nb * E <= GRP_MAX): the incidences of all blocks are grouped
+// by (block, edge) once per solve, before the stream parts fork:
+//   k_grp_count   cnt[blk][e] = |e n block|                      (atomic counts, thread per vertex)
+//   k_grp_scan    start[blk][e] = p0(blk) + sum_{e' < e} cnt[blk][e']  (CTA per block; the block's
+//                 members land in its own CSR range), cur = start
+//   k_grp_fill    memb[atomicAdd(cur[blk][e], 1)] = block-local vertex   (after it: cur = end)
+// so the members of edge e in block blk are memb[start .. cur).  The order inside a run is not
+// deterministic and does not matter: an edge contributes one addition to each (u, v), and the
+// row walk orders the contributions to one (u, v) by edge (k_assemble_rows3 = k_assemble_rows2
+// with these runs).
+constexpr int64_t GRP_MAX = 1ll << 26;       // nb * E counters per array
+
+// warp per vertex, lane per incidence
+__global__ void k_grp_count(int N, int b, int E, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                            int32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  for (int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < N; v += (gridDim.x * blockDim.x) >> 5) {
+    int32_t* cb = cnt + (int64_t)(v / b) * E;
+    const int64_t p1 = row_ptr[v + 1];
+    for (int64_t p = row_ptr[v] + lane; p < p1; p += 32) atomicAdd(&cb[col[p]], 1);
+  }
+}
+
+// CTA per block: exclusive scan of cnt[blk][0..E) (coalesced: warp w scans the w-th contiguous
+// segment in 32-entry chunks with a carry), offset by the block's first incidence
+__global__ void __launch_bounds__(1024) k_grp_scan(int b, int E, const int64_t* __restrict__ row_ptr,
+                                                   int32_t* __restrict__ start, int32_t* __restrict__ cur) {
+  __shared__ int wsum[32];
+  const int blk = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int32_t* st = start + (int64_t)blk * E;
+  int32_t* cu = cur + (int64_t)blk * E;
+  const int seg = (E + 31) / 32;
+  const int s0 = warp * seg, s1 = min(E, s0 + seg);
+  int tot = 0;
+  for (int e = s0 + lane; e < s1; e += 32) tot += st[e];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if (lane == 0) wsum[warp] = tot;
+  __syncthreads();
+  int carry = (int)row_ptr[(int64_t)blk * b];
+  for (int w = 0; w < warp; ++w) carry += wsum[w];
+  for (int e0 = s0; e0 < s1; e0 += 32) {
+    const int e = e0 + lane;
+    const int c = e < s1 ? st[e] : 0;
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (e < s1) {
+      st[e] = carry + x - c;
+      cu[e] = carry + x - c;
+    }
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+}
+
+// warp per vertex, lane per incidence
+__global__ void k_grp_fill(int N, int b, int E, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                           int32_t* __restrict__ cur, uint32_t* __restrict__ memb) {
+  const int lane = threadIdx.x & 31;
+  for (int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < N; v += (gridDim.x * blockDim.x) >> 5) {
+    int32_t* cb = cur + (int64_t)(v / b) * E;
+    const uint32_t vl = (uint32_t)(v % b);
+    const int64_t p1 = row_ptr[v + 1];
+    for (int64_t p = row_ptr[v] + lane; p < p1; p += 32) memb[atomicAdd(&cb[col[p]], 1)] = vl;
+  }
+}
+
+__global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, int E, const int64_t* __restrict__ row_ptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const uint32_t* __restrict__ memb,
+                                                          const int32_t* __restrict__ gstart,
+                                                          const int32_t* __restrict__ gend,
+                                                          const float* __restrict__ eval,
+                                                          const float* __restrict__ dvr, float inv1pmu, int raw,
+                                                          float* __restrict__ blocks) {
+  const int blk = blk0 + blockIdx.x;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  float* acc = reinterpret_cast<float*>(smem_raw);                                  // [R2_ROWS][b]
+  float* dvs = acc + (size_t)R2_ROWS * b;                                           // [b]
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  float* stc = dvs + b + warp * 32;                                                 // per-warp pair values
+  const int64_t base = (int64_t)blk * b;
+  const int u0 = blockIdx.y * R2_ROWS;
+  const int uu = u0 + warp;
+  for (int i = t; i < R2_ROWS * b; i += R2_NT) acc[i] = 0.f;
+  for (int i = t; i < b; i += R2_NT) dvs[i] = dvr[base + i];
+  __syncthreads();
+  if (uu >= b) return;
+  const int32_t* gs = gstart + (int64_t)blk * E;
+  const int32_t* ge = gend + (int64_t)blk * E;
+  float* arow = acc + (size_t)warp * b;
+  const int64_t q0 = row_ptr[base + uu], q1 = row_ptr[base + uu + 1];
+  for (int64_t c0 = q0; c0 < q1; c0 += 32) {
+    const int ne = (int)((q1 - c0) < 32 ? (q1 - c0) : 32);
+    float val = 0.f;
+    int rs = 0, len = 0;
+    if (lane < ne) {
+      const int e = col[c0 + lane];
+      rs = gs[e];
+      len = ge[e] - rs;
+      val = eval[e];
+    }
+    const unsigned heavy = __ballot_sync(0xffffffffu, lane < ne && len >= HEAVY);
+    int i = 0;
+    while (i < ne) {
+      if ((heavy >> i) & 1u) {   // heavy edge: all lanes, distinct members
+        const float c = __shfl_sync(0xffffffffu, val, i);
+        const int s = __shfl_sync(0xffffffffu, rs, i), l = __shfl_sync(0xffffffffu, len, i);
+        const uint32_t* Ms = memb + s;
+        int m = lane;
+        for (; m + 96 < l; m += 128) {   // four loads in flight
+          const uint32_t v0 = Ms[m], v1 = Ms[m + 32], v2 = Ms[m + 64], v3 = Ms[m + 96];
+          arow[v0] += c;
+          arow[v1] += c;
+          arow[v2] += c;
+          arow[v3] += c;
+        }
+        for (; m < l; m += 32) arow[Ms[m]] += c;
+        __syncwarp();
+        ++i;
+        continue;
+      }
+      // a run of light edges [i, i1): (edge, member) pairs in ascending edge order; the pairs of one
+      // v are applied by one lane in that order (the same fp32 additions as edge by edge)
+      const unsigned hv = heavy & ~((2u << i) - 1u);
+      const int i1 = hv ? (__ffs(hv) - 1) : ne;
+      const int ln = (lane >= i && lane < i1) ? len : 0;
+      int incl = ln;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      for (int qb = 0; qb < total; qb += 32) {
+        const int q = qb + lane;
+        int lo = 0;   // the first lane with incl > q
+#pragma unroll
+        for (int st = 16; st; st >>= 1) {
+          const int y = __shfl_sync(0xffffffffu, incl, lo + st - 1);
+          if (y <= q) lo += st;
+        }
+        const int ex = __shfl_sync(0xffffffffu, incl - ln, lo & 31);
+        const int s = __shfl_sync(0xffffffffu, rs, lo & 31);
+        const float c = __shfl_sync(0xffffffffu, val, lo & 31);
+        const bool act = q < total;
+        const uint32_t v = act ? memb[s + (q - ex)] : 0xffffffffu;
+        stc[lane] = c;
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        __syncwarp();
+        if (act) {
+          const unsigned mk = __match_any_sync(am, v);
+          if (lane == __ffs(mk) - 1) {
+            float x = arow[v];
+            unsigned mm = mk;
+            while (mm) {
+              const int l = __ffs(mm) - 1;
+              mm &= mm - 1;
+              x += stc[l];
+            }
+            arow[v] = x;
+          }
+        }
+        __syncwarp();
+      }
+      i = i1;
+    }
+  }
+  __syncwarp();
+  const float du = dvs[uu];
+  float* orow = blocks + (int64_t)blk * b * b + (int64_t)uu * b;
+#pragma unroll 4
+  for (int v4 = lane; v4 < b / 4; v4 += 32) {
+    const float4 a = *reinterpret_cast<const float4*>(arow + 4 * v4);
+    const float4 r = *reinterpret_cast<const float4*>(dvs + 4 * v4);
+    const int v = 4 * v4;
+    float4 o;
+    o.x = (du * r.x) * a.x;
+    o.y = (du * r.y) * a.y;
+    o.z = (du * r.z) * a.z;
+    o.w = (du * r.w) * a.w;
+    if (!raw) {
+      o.x = ((uu == v + 0) ? 1.0f : 0.0f) - o.x * inv1pmu;
+      o.y = ((uu == v + 1) ? 1.0f : 0.0f) - o.y * inv1pmu;
+      o.z = ((uu == v + 2) ? 1.0f : 0.0f) - o.z * inv1pmu;
+      o.w = ((uu == v + 3) ? 1.0f : 0.0f) - o.w * inv1pmu;
+    }
+    *reinterpret_cast<float4*>(orow + v) = o;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_degrees(int N, int E, int64_t nnz, const int64_t* row_ptr, const int32_t* col_idx,
@@ -672,10 +868,37 @@ cudaError_t launch_degrees(int N, int E, int64_t nnz, const int64_t* row_ptr, co
   return cudaGetLastError();
 }
 
-// keys [nnz] u32 | overflow [nb] i32 | member ranges [nnz][NSEG_MAX] int2 (256-byte aligned parts)
+// keys [nnz] u32 | overflow [nb] i32 | member ranges [nnz][NSEG_MAX] int2 | grouped path: run
+// starts [nb][E] i32, run ends [nb][E] i32 (256-byte aligned parts)
 static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
-size_t assemble_keys_bytes(int64_t nnz, int nb) {
-  return al256((size_t)nnz * 4) + al256((size_t)nb * 4) + (size_t)nnz * NSEG_MAX * sizeof(int2) + 256;
+bool assemble_grouped(int nb, int E) {
+  const char* force = getenv("HG_ASSEMBLE");
+  return (int64_t)nb * E <= GRP_MAX && !(force && force[0] != 'g');
+}
+static size_t grp_off(int64_t nnz, int nb) {
+  return al256((size_t)nnz * 4) + al256((size_t)nb * 4) + al256((size_t)nnz * NSEG_MAX * sizeof(int2));
+}
+size_t assemble_keys_bytes(int64_t nnz, int nb, int E) {
+  size_t g = (int64_t)nb * E <= GRP_MAX ? 2 * al256((size_t)nb * E * 4) : 0;   // whatever HG_ASSEMBLE says
+  return grp_off(nnz, nb) + g + 256;
+}
+
+// Grouped path, once per solve for all nb_total blocks (before the stream parts fork)
+cudaError_t launch_assemble_group(int nb_total, int b, int E, int64_t nnz, const int64_t* row_ptr,
+                                  const int32_t* col_idx, void* keys_ws, cudaStream_t s, int* launches) {
+  if (!assemble_grouped(nb_total, E)) return cudaSuccess;
+  uint32_t* memb = reinterpret_cast<uint32_t*>(keys_ws);
+  int32_t* gstart = reinterpret_cast<int32_t*>(static_cast<char*>(keys_ws) + grp_off(nnz, nb_total));
+  int32_t* gcur = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(gstart) + al256((size_t)nb_total * E * 4));
+  const int N = nb_total * b;
+  cudaError_t e = cudaMemsetAsync(gstart, 0, (size_t)nb_total * E * 4, s);
+  if (e != cudaSuccess) return e;
+  const int grid = (int)(((int64_t)N * 32 + 255) / 256 < 148 * 32 ? ((int64_t)N * 32 + 255) / 256 : 148 * 32);
+  k_grp_count<<<grid, 256, 0, s>>>(N, b, E, row_ptr, col_idx, gstart);
+  k_grp_scan<<<nb_total, 1024, 0, s>>>(b, E, row_ptr, gstart, gcur);
+  k_grp_fill<<<grid, 256, 0, s>>>(N, b, E, row_ptr, col_idx, gcur, memb);
+  *launches += 3;
+  return cudaGetLastError();
 }
 
 // keys: nnz uint32 + nb int32 overflow flags (workspace).  E*b must be < 2^32 for the
@@ -690,6 +913,24 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
   // HG_ASSEMBLE=tiles forces the hashed-tile kernel (verification: both paths are bit-identical)
   const char* force = getenv("HG_ASSEMBLE");
   const bool tiles = force && force[0] == 't';
+  if (assemble_grouped(nb_total, E)) {   // grouped by launch_assemble_group: the row walk only
+    const int32_t* gstart =
+        reinterpret_cast<const int32_t*>(static_cast<const char*>(keys_ws) + grp_off(nnz, nb_total));
+    const int32_t* gend = reinterpret_cast<const int32_t*>(reinterpret_cast<const char*>(gstart) +
+                                                           al256((size_t)nb_total * E * 4));
+    const size_t smem = (size_t)R2_ROWS * b * 4 + (size_t)b * 4 + (size_t)R2_ROWS * 32 * 4;
+    static size_t attr4 = 0;
+    if (smem > attr4) {
+      cudaError_t e = cudaFuncSetAttribute(k_assemble_rows3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr4 = smem;
+    }
+    k_assemble_rows3<<<dim3(nb, (b + R2_ROWS - 1) / R2_ROWS), R2_NT, smem, s>>>(
+        blk0, b, E, row_ptr, col_idx, keys, gstart, gend, edge_val, dv_rsqrt, 1.0f / (1.0f + mu), raw_theta ? 1 : 0,
+        blocks);
+    ++*launches;
+    return cudaGetLastError();
+  }
   const bool radix_ok = E < (1 << 17) && b <= 2048 && !tiles && !(force && force[0] == 's');
   const bool sorted_ok = (uint64_t)E * (uint64_t)b < (1ull << 32) && b <= 4 * SEG_V && !tiles;
   cudaError_t e = cudaMemsetAsync(overflow + blk0, (radix_ok || sorted_ok) ? 0 : 1, sizeof(int32_t) * nb, s);
