@@ -496,12 +496,15 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
 hg_status run_degrees(const hg_incidence* H, const float* w, int b, float* dvr, int32_t* st, void* ws,
                       const Layout& Lo, cudaStream_t s) {
   ProfScope ps(ST_DEGREES, s);
-  HG_CU(launch_degrees(H->n_vertices, H->n_edges, H->nnz, H->row_ptr, H->col_idx, w, at<int32_t>(ws, Lo.de),
-                       at<float>(ws, Lo.eval), dvr, st, s, &g_launches),
-        "degrees");
-  HG_CU(launch_assemble_group(H->n_vertices / b, b, H->n_edges, H->nnz, H->row_ptr, H->col_idx,
-                              at<void>(ws, Lo.keys), s, &g_launches),
-        "assembly grouping");
+  if (assemble_grouped(H->n_vertices / b, H->n_edges))
+    HG_CU(launch_degrees_grouped(H->n_vertices / b, b, H->n_edges, H->nnz, H->row_ptr, H->col_idx, w,
+                                 at<int32_t>(ws, Lo.de), at<float>(ws, Lo.eval), dvr, st, at<void>(ws, Lo.keys), s,
+                                 &g_launches),
+          "degrees + assembly grouping");
+  else
+    HG_CU(launch_degrees(H->n_vertices, H->n_edges, H->nnz, H->row_ptr, H->col_idx, w, at<int32_t>(ws, Lo.de),
+                         at<float>(ws, Lo.eval), dvr, st, s, &g_launches),
+          "degrees");
   return HG_OK;
 }
 

@@ -11,11 +11,12 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
                             const int32_t* col_idx, const float* edge_val, const float* dv_rsqrt, float mu,
                             bool raw_theta, float* blocks, void* keys_ws, cudaStream_t s, int* launches);
 size_t assemble_keys_bytes(int64_t nnz, int nb, int E);
-// grouped assembly (default when nb * E is small enough): group the incidences of all nb_total blocks
-// by (block, edge) once per solve, before launch_assemble of any block range; no-op otherwise
+// grouped assembly (default when nb * E is small enough): degrees and the (block, edge) grouping of the
+// incidences of all nb_total blocks once per solve (instead of launch_degrees), before launch_assemble
 bool assemble_grouped(int nb, int E);
-cudaError_t launch_assemble_group(int nb_total, int b, int E, int64_t nnz, const int64_t* row_ptr,
-                                  const int32_t* col_idx, void* keys_ws, cudaStream_t s, int* launches);
+cudaError_t launch_degrees_grouped(int nb_total, int b, int E, int64_t nnz, const int64_t* row_ptr,
+                                   const int32_t* col_idx, const float* w, int32_t* de_cnt, float* edge_val,
+                                   float* dv_rsqrt, int32_t* status, void* keys_ws, cudaStream_t s, int* launches);
 
 // philox.cu -- Alg. 1 step 1, reading A6
 // panel: out[i][c][m] = Omega[i*b + m][c] (Omega is N x k, normal index r*k + c)

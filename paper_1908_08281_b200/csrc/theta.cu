@@ -673,20 +673,22 @@ __global__ void k_grp_count(int N, int b, int E, const int64_t* __restrict__ row
                             int32_t* __restrict__ cnt) {
   const int lane = threadIdx.x & 31;
   for (int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < N; v += (gridDim.x * blockDim.x) >> 5) {
-    int32_t* cb = cnt + (int64_t)(v / b) * E;
+    int32_t* cb = cnt + (int64_t)(v / b) * (E + 1);
     const int64_t p1 = row_ptr[v + 1];
     for (int64_t p = row_ptr[v] + lane; p < p1; p += 32) atomicAdd(&cb[col[p]], 1);
   }
 }
 
 // CTA per block: exclusive scan of cnt[blk][0..E) (coalesced: warp w scans the w-th contiguous
-// segment in 32-entry chunks with a carry), offset by the block's first incidence
+// segment in 32-entry chunks with a carry), offset by the block's first incidence; rows of E + 1
+// entries, the last = the block's end (so edge e's run is [start[e], start[e + 1]))
 __global__ void __launch_bounds__(1024) k_grp_scan(int b, int E, const int64_t* __restrict__ row_ptr,
                                                    int32_t* __restrict__ start, int32_t* __restrict__ cur) {
   __shared__ int wsum[32];
   const int blk = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  int32_t* st = start + (int64_t)blk * E;
-  int32_t* cu = cur + (int64_t)blk * E;
+  int32_t* st = start + (int64_t)blk * (E + 1);
+  int32_t* cu = cur + (int64_t)blk * (E + 1);
+  if (t == 0) st[E] = (int)row_ptr[(int64_t)(blk + 1) * b];
   const int seg = (E + 31) / 32;
   const int s0 = warp * seg, s1 = min(E, s0 + seg);
   int tot = 0;
@@ -714,23 +716,45 @@ __global__ void __launch_bounds__(1024) k_grp_scan(int b, int E, const int64_t* 
   }
 }
 
-// warp per vertex, lane per incidence
+// warp per vertex, lane per incidence: memb[cursor++] = the vertex; rng[p] = its edge's run in the block
 __global__ void k_grp_fill(int N, int b, int E, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                           int32_t* __restrict__ cur, uint32_t* __restrict__ memb) {
+                           const int32_t* __restrict__ start, int32_t* __restrict__ cur, uint32_t* __restrict__ memb,
+                           int2* __restrict__ rng) {
   const int lane = threadIdx.x & 31;
   for (int v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < N; v += (gridDim.x * blockDim.x) >> 5) {
-    int32_t* cb = cur + (int64_t)(v / b) * E;
+    const int64_t off = (int64_t)(v / b) * (E + 1);
     const uint32_t vl = (uint32_t)(v % b);
     const int64_t p1 = row_ptr[v + 1];
-    for (int64_t p = row_ptr[v] + lane; p < p1; p += 32) memb[atomicAdd(&cb[col[p]], 1)] = vl;
+    for (int64_t p = row_ptr[v] + lane; p < p1; p += 32) {
+      const int e = col[p];
+      memb[atomicAdd(&cur[off + e], 1)] = vl;
+      rng[p] = make_int2(start[off + e], start[off + e + 1]);
+    }
   }
 }
 
-__global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, int E, const int64_t* __restrict__ row_ptr,
+// delta(e) = sum over blocks of |e n block| (no hot-address atomics), w_e / delta(e)
+__global__ void k_grp_degree(int nb, int E, const int32_t* __restrict__ cnt, const float* __restrict__ w,
+                             int32_t* __restrict__ de, float* __restrict__ val, int32_t* status) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  int c = 0;
+  for (int i = 0; i < nb; ++i) c += cnt[(int64_t)i * (E + 1) + e];
+  de[e] = c;
+  if (c == 0) {
+    hg_flag(status, HGS_EMPTY_EDGE);
+    val[e] = 0.f;
+    return;
+  }
+  const float v = w[e] / (float)c;
+  if (!isfinite(v)) hg_flag(status, HGS_NONFINITE);
+  val[e] = v;
+}
+
+__global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, const int64_t* __restrict__ row_ptr,
                                                           const int32_t* __restrict__ col,
                                                           const uint32_t* __restrict__ memb,
-                                                          const int32_t* __restrict__ gstart,
-                                                          const int32_t* __restrict__ gend,
+                                                          const int2* __restrict__ rng,
                                                           const float* __restrict__ eval,
                                                           const float* __restrict__ dvr, float inv1pmu, int raw,
                                                           float* __restrict__ blocks) {
@@ -747,8 +771,6 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, int E
   for (int i = t; i < b; i += R2_NT) dvs[i] = dvr[base + i];
   __syncthreads();
   if (uu >= b) return;
-  const int32_t* gs = gstart + (int64_t)blk * E;
-  const int32_t* ge = gend + (int64_t)blk * E;
   float* arow = acc + (size_t)warp * b;
   const int64_t q0 = row_ptr[base + uu], q1 = row_ptr[base + uu + 1];
   for (int64_t c0 = q0; c0 < q1; c0 += 32) {
@@ -756,10 +778,10 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, int E
     float val = 0.f;
     int rs = 0, len = 0;
     if (lane < ne) {
-      const int e = col[c0 + lane];
-      rs = gs[e];
-      len = ge[e] - rs;
-      val = eval[e];
+      const int2 r = rng[c0 + lane];
+      rs = r.x;
+      len = r.y - r.x;
+      val = eval[col[c0 + lane]];
     }
     const unsigned heavy = __ballot_sync(0xffffffffu, lane < ne && len >= HEAVY);
     int i = 0;
@@ -879,25 +901,37 @@ static size_t grp_off(int64_t nnz, int nb) {
   return al256((size_t)nnz * 4) + al256((size_t)nb * 4) + al256((size_t)nnz * NSEG_MAX * sizeof(int2));
 }
 size_t assemble_keys_bytes(int64_t nnz, int nb, int E) {
-  size_t g = (int64_t)nb * E <= GRP_MAX ? 2 * al256((size_t)nb * E * 4) : 0;   // whatever HG_ASSEMBLE says
+  size_t g = (int64_t)nb * E <= GRP_MAX ? 2 * al256((size_t)nb * (E + 1) * 4) : 0;   // whatever HG_ASSEMBLE says
   return grp_off(nnz, nb) + g + 256;
 }
 
-// Grouped path, once per solve for all nb_total blocks (before the stream parts fork)
-cudaError_t launch_assemble_group(int nb_total, int b, int E, int64_t nnz, const int64_t* row_ptr,
-                                  const int32_t* col_idx, void* keys_ws, cudaStream_t s, int* launches) {
-  if (!assemble_grouped(nb_total, E)) return cudaSuccess;
+static int32_t* grp_start(void* keys_ws, int64_t nnz, int nb) {
+  return reinterpret_cast<int32_t*>(static_cast<char*>(keys_ws) + grp_off(nnz, nb));
+}
+static int32_t* grp_cur(void* keys_ws, int64_t nnz, int nb, int E) {
+  return reinterpret_cast<int32_t*>(reinterpret_cast<char*>(grp_start(keys_ws, nnz, nb)) +
+                                    al256((size_t)nb * (E + 1) * 4));
+}
+
+// Grouped path: degrees and the (block, edge) grouping of all nb_total blocks, once per
+// solve before the stream parts fork (replaces launch_degrees when assemble_grouped(nb_total, E))
+cudaError_t launch_degrees_grouped(int nb_total, int b, int E, int64_t nnz, const int64_t* row_ptr,
+                                   const int32_t* col_idx, const float* w, int32_t* de_cnt, float* edge_val,
+                                   float* dv_rsqrt, int32_t* status, void* keys_ws, cudaStream_t s, int* launches) {
   uint32_t* memb = reinterpret_cast<uint32_t*>(keys_ws);
-  int32_t* gstart = reinterpret_cast<int32_t*>(static_cast<char*>(keys_ws) + grp_off(nnz, nb_total));
-  int32_t* gcur = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(gstart) + al256((size_t)nb_total * E * 4));
+  int2* rng = reinterpret_cast<int2*>(static_cast<char*>(keys_ws) + al256((size_t)nnz * 4) + al256((size_t)nb_total * 4));
+  int32_t* gstart = grp_start(keys_ws, nnz, nb_total);
+  int32_t* gcur = grp_cur(keys_ws, nnz, nb_total, E);
   const int N = nb_total * b;
-  cudaError_t e = cudaMemsetAsync(gstart, 0, (size_t)nb_total * E * 4, s);
+  cudaError_t e = cudaMemsetAsync(gstart, 0, (size_t)nb_total * (E + 1) * 4, s);
   if (e != cudaSuccess) return e;
   const int grid = (int)(((int64_t)N * 32 + 255) / 256 < 148 * 32 ? ((int64_t)N * 32 + 255) / 256 : 148 * 32);
   k_grp_count<<<grid, 256, 0, s>>>(N, b, E, row_ptr, col_idx, gstart);
+  k_grp_degree<<<(E + 255) / 256, 256, 0, s>>>(nb_total, E, gstart, w, de_cnt, edge_val, status);
+  k_vertex_deg<<<(N + 255) / 256, 256, 0, s>>>(N, row_ptr, col_idx, w, dv_rsqrt, status);
   k_grp_scan<<<nb_total, 1024, 0, s>>>(b, E, row_ptr, gstart, gcur);
-  k_grp_fill<<<grid, 256, 0, s>>>(N, b, E, row_ptr, col_idx, gcur, memb);
-  *launches += 3;
+  k_grp_fill<<<grid, 256, 0, s>>>(N, b, E, row_ptr, col_idx, gstart, gcur, memb, rng);
+  *launches += 5;
   return cudaGetLastError();
 }
 
@@ -913,11 +947,7 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
   // HG_ASSEMBLE=tiles forces the hashed-tile kernel (verification: both paths are bit-identical)
   const char* force = getenv("HG_ASSEMBLE");
   const bool tiles = force && force[0] == 't';
-  if (assemble_grouped(nb_total, E)) {   // grouped by launch_assemble_group: the row walk only
-    const int32_t* gstart =
-        reinterpret_cast<const int32_t*>(static_cast<const char*>(keys_ws) + grp_off(nnz, nb_total));
-    const int32_t* gend = reinterpret_cast<const int32_t*>(reinterpret_cast<const char*>(gstart) +
-                                                           al256((size_t)nb_total * E * 4));
+  if (assemble_grouped(nb_total, E)) {   // grouped by launch_degrees_grouped: the row walk only
     const size_t smem = (size_t)R2_ROWS * b * 4 + (size_t)b * 4 + (size_t)R2_ROWS * 32 * 4;
     static size_t attr4 = 0;
     if (smem > attr4) {
@@ -926,8 +956,7 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
       attr4 = smem;
     }
     k_assemble_rows3<<<dim3(nb, (b + R2_ROWS - 1) / R2_ROWS), R2_NT, smem, s>>>(
-        blk0, b, E, row_ptr, col_idx, keys, gstart, gend, edge_val, dv_rsqrt, 1.0f / (1.0f + mu), raw_theta ? 1 : 0,
-        blocks);
+        blk0, b, row_ptr, col_idx, keys, rng, edge_val, dv_rsqrt, 1.0f / (1.0f + mu), raw_theta ? 1 : 0, blocks);
     ++*launches;
     return cudaGetLastError();
   }
