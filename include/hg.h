@@ -78,6 +78,10 @@ enum hg_status_flags {
                                 /* hg_block_apply_woodbury                                     */
 #define HG_POWER_EQ10 (1u << 3) /* hg_block_rsvd(_ex) / hg_solve(_ex): the Eq. 10 scheme     */
                                 /* Y = (X X^T)^q X Omega, one QR at the end  */
+#define HG_GENERAL (1u << 4)    /* hg_block_rsvd(_ex): blocks need not be symmetric -- the X^T   */
+                                /* products of Alg. 1 use the literal transpose   */
+#define HG_UV_BK (1u << 5)      /* hg_block_rsvd / hg_block_apply_inverse_ex: U, V [nb][b][k]    */
+                                /* (column j = u_j) instead of the transposed Ut, Vt [nb][k][b]  */
 #define HG_GEMM_SIMT (1u << 8)  /* verification only: CUDA-core fp32 GEMMs, not tcgen05    */
 
 /* Hypergraph incidence H (H(v,e) = 1 iff v in e) in CSR over
@@ -122,10 +126,13 @@ hg_status hg_fill_gaussian(uint64_t seed, int32_t rows, int32_t cols, float* out
  *   Y0 = X Omega, S0 = qr(Y0); for i = 1..q: S~ = qr(X^T S), S = qr(X S~);
  *   B = S^T X; B = U~ Sigma V^T; U = S U~.
  * X_ii^T = X_ii is assumed (hg_build_theta writes bitwise-symmetric blocks;
- * reading A12).  QR is CholeskyQR2; the SVD is one-sided Jacobi.
- *   blocks [nb][b][b]   input blocks (symmetric)
+ * reading A12) unless flags has HG_GENERAL, which multiplies by the literal X^T in
+ * the S~ = qr(X^T S) and B = S^T X steps.  QR is CholeskyQR2; the SVD is one-sided
+ * Jacobi started from an eigen-preconditioner for k <= 256.
+ *   blocks [nb][b][b]   input blocks (symmetric unless HG_GENERAL)
  *   1 <= k <= min(b, 512); b % 4 == 0 and k % 4 == 0 (16-byte TMA row strides)
- *   Ut, Vt [nb][k][b]   out, U_i^T and V_i^T;  sigma [nb][k] out, non-increasing
+ *   Ut, Vt [nb][k][b]   out, U_i^T and V_i^T (HG_UV_BK: U, V [nb][b][k]);
+ *   sigma [nb][k] out, non-increasing
  * Device errors: HG_ST_CHOL_BREAKDOWN, HG_ST_JACOBI_CAP, HG_ST_NONFINITE. */
 hg_status hg_block_rsvd(const float* blocks, int32_t nb, int32_t b, int32_t k, int32_t q, uint64_t seed,
                         uint32_t flags, float* Ut, float* sigma, float* Vt, int32_t* d_status, void* ws,
@@ -146,10 +153,16 @@ hg_status hg_workspace_size_ex(int32_t N, int32_t E, int64_t nnz, int32_t b, int
 /* Eq. 3 with Eq. 15 per block:
  *   F_i = scale * V_i diag(1/sigma_i) U_i^T Y_i,   Y_i = rows [ib,(i+1)b) of Y.
  *   Y, F [nb*b][T];  scale = mu/(1+mu) for Eq. 3.
+ *   T >= 0 arbitrary (T % 4 != 0: Y and F pass through 16-byte-pitched workspace copies).
  * Device errors: HG_ST_SINGULAR_SIGMA (sigma_j <= 1e-6 sigma_1; reading A14). */
 hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const float* Vt, int32_t nb, int32_t b,
                                  int32_t k, const float* Y, int32_t T, float scale, float* F,
                                  int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
+/* hg_block_apply_inverse with flags: HG_UV_BK takes U, V [nb][b][k] (hg_block_rsvd with HG_UV_BK);
+ * HG_GEMM_SIMT as for hg_gemm. */
+hg_status hg_block_apply_inverse_ex(const float* U, const float* sigma, const float* V, int32_t nb, int32_t b,
+                                    int32_t k, const float* Y, int32_t T, float scale, float* F, uint32_t flags,
+                                    int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
 
 /* Reading R2 (the paper calls the X blocks "low-rank", PAPER.md:102,
  * 138, yet X = I - Theta/(1+mu) is full-rank, its low-rank part being Theta): given the
@@ -261,6 +274,11 @@ hg_status hg_weight_gradient(const hg_incidence* H, const float* w, const float*
                              float* grad, int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
 hg_status hg_weight_step(int32_t E, float* w, int32_t* active, const float* grad, float mu, int32_t* d_status,
                          hg_stream_t stream);
+/* Projection of a starting weight vector onto the simplex's affine hull, w_out = w / (1^T w), the start
+ * of the constrained iteration of PAPER.md:50-52 (1^T w = 1, w >= 0).  w, w_out [E] (may alias).  One
+ * CTA, fixed-order fp64 sum.  Device errors: HG_ST_SIMPLEX_DEGENERATE (a negative or non-finite w_e, or
+ * 1^T w <= 0; w_out = w then). */
+hg_status hg_weight_normalize(int32_t E, const float* w, float* w_out, int32_t* d_status, hg_stream_t stream);
 /* The objective P(w) = sum_t f_t^T L f_t + kappa ||w||^2 at the w the gradient was taken at (degrees
  * from w): since P is linear in w at fixed degrees apart from the penalty,
  *   P(w) = ||F||^2 + w^T grad(w) - kappa ||w||^2   (grad from hg_weight_gradient at the same w).

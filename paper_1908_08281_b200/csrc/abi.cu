@@ -115,7 +115,7 @@ constexpr size_t ALIGN = 256;
 struct Layout {
   size_t de = 0, eval = 0, dvr = 0, keys = 0, blocks = 0, P[4] = {0, 0, 0, 0}, Ut = 0, Vt = 0;
   size_t G = 0, L = 0, Linv = 0, Wf = 0, Uk = 0, work = 0, eig = 0, sig = 0, sigma = 0, sigl = 0, rs = 0, Z = 0,
-         status = 0;
+         Yp = 0, Fp = 0, status = 0;
   size_t h_rowptr = 0, h_col = 0, h_w = 0, h_Y = 0, h_F = 0;
   size_t total = 0;
 };
@@ -148,7 +148,12 @@ Layout layout(int64_t N, int64_t E, int64_t nnz, int64_t b, int64_t k, int64_t T
   L.sigma = take(4 * nb * k);
   L.sigl = take(4 * nb * k);   // internal sigma of an oversampled (l = k + p) factorisation
   L.rs = take(4 * nb * k);
-  L.Z = take(4 * nb * k * (T > 0 ? T : 1));
+  const int64_t T4 = (T + 3) / 4 * 4;   // T % 4 != 0: Y, F go through 16-byte-pitched copies
+  L.Z = take(4 * nb * k * (T > 0 ? T4 : 1));
+  if (T % 4) {
+    L.Yp = take(4 * N * T4);
+    L.Fp = take(4 * N * T4);
+  }
   L.status = take(4);
   L.h_rowptr = take(8 * (N + 1));
   L.h_col = take(4 * (nnz > 0 ? nnz : 1));
@@ -172,7 +177,7 @@ hg_status check_sizes(int64_t N, int64_t b, int64_t k, int64_t q, int64_t T) {
   if (k % 4) return fail(HG_ERR_INVALID, "k must be a multiple of 4 (k=%lld)", (long long)k);
   if (k > 512) return fail(HG_ERR_INVALID, "k > 512 is not supported (k=%lld)", (long long)k);
   if (q < 0) return fail(HG_ERR_INVALID, "q must be >= 0 (q=%lld)", (long long)q);
-  if (T < 0 || (T % 4)) return fail(HG_ERR_INVALID, "T must be >= 0 and a multiple of 4 (T=%lld)", (long long)T);
+  if (T < 0) return fail(HG_ERR_INVALID, "T must be >= 0 (T=%lld)", (long long)T);
   if (N / b > 65535) return fail(HG_ERR_INVALID, "more than 65535 blocks");
   return HG_OK;
 }
@@ -209,12 +214,14 @@ struct Rsvd {
   bool simt;
   cudaStream_t s;
   const float* X;
+  bool general = false;   // HG_GENERAL: X^T products use the literal transpose (else X^T = X, reading A12)
 
-  // out_t = (X P)^T  with P given as P_t [k][b] (X symmetric: X^T P = X P, reading A12)
-  hg_status power(const float* P_t, float* out_t) const {
+  // out_t = (X P)^T  with P given as P_t [k][b]; trans: (X^T P)^T, the literal X^T only when general
+  // (X symmetric: X^T P = X P, reading A12)
+  hg_status power(const float* P_t, float* out_t, bool trans = false) const {
     GemmDesc g;
     g.M = b; g.N = k; g.K = b; g.batch = nb;
-    g.A = X; g.a_mn = false; g.lda = b; g.sa = (int64_t)b * b;
+    g.A = X; g.a_mn = trans && general; g.lda = b; g.sa = (int64_t)b * b;
     g.B = P_t; g.b_mn = false; g.ldb = b; g.sb = (int64_t)k * b;
     g.D = out_t; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
     g.bn_max = bn_env("HG_BN_POWER", 256);
@@ -287,7 +294,7 @@ hg_status cholqr(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* L
 // problem (parts run concurrently on different streams; see solve_impl).
 struct Bufs {
   float* P[4];
-  float *G, *L, *Linv, *Wf, *Uk, *work, *eig, *rs, *Z;
+  float *G, *L, *Linv, *Wf, *Uk, *work, *eig, *rs, *Z, *Yp, *Fp;
   double* sig;
   int32_t* perm;
 };
@@ -303,7 +310,10 @@ Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k,
   B.work = at<float>(ws, Lo.work) + kk;
   B.eig = eig_precond_supported(k) ? at<float>(ws, Lo.eig) + (int64_t)blk0 * eig_scratch_floats(k) : nullptr;
   B.rs = at<float>(ws, Lo.rs) + k1;
-  B.Z = at<float>(ws, Lo.Z) + k1 * (T > 0 ? T : 1);
+  const int64_t T4 = (T + 3) / 4 * 4;
+  B.Z = at<float>(ws, Lo.Z) + k1 * (T > 0 ? T4 : 1);
+  B.Yp = (T % 4) ? at<float>(ws, Lo.Yp) + (int64_t)blk0 * b * T4 : nullptr;
+  B.Fp = (T % 4) ? at<float>(ws, Lo.Fp) + (int64_t)blk0 * b * T4 : nullptr;
   double* sig0 = at<double>(ws, Lo.sig);
   B.sig = sig0 + k1;
   B.perm = reinterpret_cast<int32_t*>(sig0 + (int64_t)nb_total * k) + k1;
@@ -314,8 +324,9 @@ Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k,
 // scheme 0: Alg. 1 (QR after every product); scheme 1: Eq. 10, Y = (X X^T)^q X Omega formed first
 // and orthonormalised once (shifted CholeskyQR3).
 hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64_t seed, bool simt, float* Ut,
-                   float* sigma, float* Vt, int32_t* st, const Bufs& Bf, cudaStream_t s, int scheme = 0) {
-  Rsvd R{nb, b, k, simt, s, X};
+                   float* sigma, float* Vt, int32_t* st, const Bufs& Bf, cudaStream_t s, int scheme = 0,
+                   bool general = false, bool uv_bk = false) {
+  Rsvd R{nb, b, k, simt, s, X, general};
   float* P[4];
   for (int i = 0; i < 4; ++i) P[i] = Bf.P[i];
   float* G = Bf.G;
@@ -344,8 +355,8 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
   if (scheme == 1) {
     cur = P[1];
     oth = P[0];
-    for (int it = 0; it < 2 * q; ++it) {   // (X X^T)^q X Omega, X^T = X (reading A12)
-      HG_TRY(R.power(cur, oth));
+    for (int it = 0; it < 2 * q; ++it) {   // (X X^T)^q X Omega (X^T = X unless HG_GENERAL, reading A12)
+      HG_TRY(R.power(cur, oth, it % 2 == 0));
       float* t = cur; cur = oth; oth = t;
     }
     float* qn = nullptr;
@@ -357,16 +368,16 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
     oth = (cur == P[1]) ? P[0] : P[1];
     // loop i = 1..q: S~ = qr(X^T S), S = qr(X S~)
     for (int it = 0; it < 2 * q; ++it) {
-      HG_TRY(R.power(cur, oth));
+      HG_TRY(R.power(cur, oth, it % 2 == 0));
       float* qn = nullptr;
       HG_TRY(cholqr(R, oth, cur, G, Linv, work, st, passes(false, it == 2 * q - 1), &qn));
       oth = (qn == oth) ? cur : oth;
       cur = qn;
     }
   }
-  // step 4: B = S^T X, stored as B [k][b] = (X S)^T
+  // step 4: B = S^T X, stored as B [k][b] = (X^T S)^T
   float* Bt = oth;
-  HG_TRY(R.power(cur, Bt));
+  HG_TRY(R.power(cur, Bt, true));
   // step 5: SVD of B via B B^T = L L^T and one-sided Jacobi (W = L, or W = L^T; jacobi.cu)
   HG_TRY(R.gram(Bt, G));
   const bool on_l = jacobi_on_l();
@@ -443,7 +454,8 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
   }
   {
     ProfScope ps(ST_FINALIZE, s);
-    HG_CU(launch_finalize(nb, b, k, P[2], P[3], Ut, sigma, Vt, sig, Bf.perm, st, s, &g_launches), "finalize");
+    HG_CU(launch_finalize(nb, b, k, P[2], P[3], Ut, sigma, Vt, sig, Bf.perm, st, s, &g_launches, uv_bk),
+          "finalize");
   }
   return HG_OK;
 }
@@ -455,9 +467,23 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
 // an oversampled factorisation truncated to rank k).
 hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb, int b, int k, const float* Y, int T,
                     float scale, float* F, int32_t* st, const Bufs& Bf, cudaStream_t s, bool simt,
-                    float woodbury_opm = 0.f, int ldk = 0) {
+                    float woodbury_opm = 0.f, int ldk = 0, bool uv_bk = false) {
   if (T == 0) return HG_OK;
   if (ldk < k) ldk = k;
+  if (T % 4) {   // the GEMMs need 16-byte row pitches: run on zero-padded [rows][T4] copies of Y and F
+    const int T4 = (T + 3) / 4 * 4;
+    const size_t rows = (size_t)nb * b;
+    HG_CU(cudaMemsetAsync(Bf.Yp, 0, rows * T4 * 4, s), "pad Y");
+    HG_CU(cudaMemcpy2DAsync(Bf.Yp, (size_t)T4 * 4, Y, (size_t)T * 4, (size_t)T * 4, rows, cudaMemcpyDeviceToDevice, s),
+          "pad Y");
+    Bufs B2 = Bf;
+    B2.Yp = nullptr;
+    B2.Fp = nullptr;
+    HG_TRY(run_apply(Ut, sigma, Vt, nb, b, k, Bf.Yp, T4, scale, Bf.Fp, st, B2, s, simt, woodbury_opm, ldk, uv_bk));
+    HG_CU(cudaMemcpy2DAsync(F, (size_t)T * 4, Bf.Fp, (size_t)T4 * 4, (size_t)T * 4, rows, cudaMemcpyDeviceToDevice, s),
+          "unpad F");
+    return HG_OK;
+  }
   const bool wb = woodbury_opm > 0.f;
   float* rs = Bf.rs;
   float* Z = Bf.Z;
@@ -471,7 +497,7 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
   {  // Z = diag(rs) U^T Y_i   (k x T)
     GemmDesc g;
     g.M = k; g.N = T; g.K = b; g.batch = nb;
-    g.A = Ut; g.a_mn = false; g.lda = b; g.sa = (int64_t)ldk * b;
+    g.A = Ut; g.a_mn = uv_bk; g.lda = uv_bk ? ldk : b; g.sa = (int64_t)ldk * b;   // HG_UV_BK: U [b][ldk]
     g.B = Y; g.b_mn = true; g.ldb = T; g.sb = (int64_t)b * T;
     g.D = Z; g.d_trans = false; g.ldd = T; g.sd = (int64_t)k * T;
     g.rs = rs; g.srs = ldk;
@@ -480,7 +506,7 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
   {  // R1: F_i = V Z;  R2: F_i = U Z + scale Y_i   (b x T)
     GemmDesc g;
     g.M = b; g.N = T; g.K = k; g.batch = nb;
-    g.A = wb ? Ut : Vt; g.a_mn = true; g.lda = b; g.sa = (int64_t)ldk * b;
+    g.A = wb ? Ut : Vt; g.a_mn = !uv_bk; g.lda = uv_bk ? ldk : b; g.sa = (int64_t)ldk * b;
     g.B = Z; g.b_mn = true; g.ldb = T; g.sb = (int64_t)k * T;
     g.D = F; g.d_trans = false; g.ldd = T; g.sd = (int64_t)b * T;
     if (wb) {
@@ -692,15 +718,17 @@ hg_status hg_block_rsvd_ex(const float* blocks, int32_t nb, int32_t b, int32_t k
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int scheme = (flags & HG_POWER_EQ10) ? 1 : 0;
   const bool simt = (flags & HG_GEMM_SIMT) != 0;
+  const bool general = (flags & HG_GENERAL) != 0, uv_bk = (flags & HG_UV_BK) != 0;
   if (p == 0)
     return run_rsvd(blocks, nb, 0, b, k, q, seed, simt, Ut, sigma, Vt, d_status, part_bufs(ws, Lo, nb, 0, b, k, 0), s,
-                    scheme);
+                    scheme, general, uv_bk);
+  if (uv_bk) return fail(HG_ERR_INVALID, "HG_UV_BK is not supported with oversampling (p > 0)");
   // oversampled: factor at width l into the workspace, keep the top k triplets (rank-k truncation)
   float* Ul = at<float>(ws, Lo.Ut);
   float* Vl = at<float>(ws, Lo.Vt);
   float* sl = at<float>(ws, Lo.sigl);
   HG_TRY(run_rsvd(blocks, nb, 0, b, l, q, seed, simt, Ul, sl, Vl, d_status, part_bufs(ws, Lo, nb, 0, b, l, 0), s,
-                  scheme));
+                  scheme, general));
   HG_CU(cudaMemcpy2DAsync(Ut, 4 * (size_t)k * b, Ul, 4 * (size_t)l * b, 4 * (size_t)k * b, nb, cudaMemcpyDeviceToDevice,
                           s), "truncate U");
   HG_CU(cudaMemcpy2DAsync(Vt, 4 * (size_t)k * b, Vl, 4 * (size_t)l * b, 4 * (size_t)k * b, nb, cudaMemcpyDeviceToDevice,
@@ -729,6 +757,23 @@ hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const floa
   HG_TRY(check_ws(ws, ws_bytes, Lo.status));
   return run_apply(Ut, sigma, Vt, nb, b, k, Y, T, scale, F, d_status, part_bufs(ws, Lo, nb, 0, b, k, T),
                    reinterpret_cast<cudaStream_t>(stream), false);
+}
+
+hg_status hg_block_apply_inverse_ex(const float* U, const float* sigma, const float* V, int32_t nb, int32_t b,
+                                    int32_t k, const float* Y, int32_t T, float scale, float* F, uint32_t flags,
+                                    int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (nb <= 0) return fail(HG_ERR_INVALID, "nb must be > 0");
+  HG_TRY(check_sizes((int64_t)nb * b, b, k, 0, T));
+  if (!U || !sigma || !V || !d_status || (T > 0 && (!Y || !F))) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (!std::isfinite(scale)) return fail(HG_ERR_INVALID, "scale must be finite");
+  if (flags & ~(HG_UV_BK | HG_GEMM_SIMT)) return fail(HG_ERR_INVALID, "unsupported flags 0x%x", flags);
+  const Layout Lo = layout((int64_t)nb * b, 1, 0, b, k, T);
+  HG_TRY(check_ws(ws, ws_bytes, Lo.status));
+  return run_apply(U, sigma, V, nb, b, k, Y, T, scale, F, d_status, part_bufs(ws, Lo, nb, 0, b, k, T),
+                   reinterpret_cast<cudaStream_t>(stream), (flags & HG_GEMM_SIMT) != 0, 0.f, 0,
+                   (flags & HG_UV_BK) != 0);
 }
 
 hg_status hg_block_apply_woodbury(const float* Ut, const float* sigma, int32_t nb, int32_t b, int32_t k,
@@ -1524,6 +1569,16 @@ hg_status hg_weight_objective(const float* F, int32_t N, int32_t T, int32_t E, c
   HG_CU(launch_weight_objective((int64_t)N * T, F, E, w, grad, kappa, static_cast<double*>(ws), out,
                                 reinterpret_cast<cudaStream_t>(stream), &g_launches),
         "weight objective");
+  return HG_OK;
+}
+
+hg_status hg_weight_normalize(int32_t E, const float* w, float* w_out, int32_t* d_status, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (E <= 0) return fail(HG_ERR_INVALID, "E must be > 0");
+  if (!w || !w_out || !d_status) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  HG_CU(launch_weight_normalize(E, w, w_out, d_status, reinterpret_cast<cudaStream_t>(stream), &g_launches),
+        "weight normalize");
   return HG_OK;
 }
 

@@ -652,6 +652,26 @@ __global__ void __launch_bounds__(1024) k_weight_step(int E, float* __restrict__
   }
 }
 
+// Start of the weight iteration on the simplex 1^T w = 1, w >= 0 (Eq. optprob):
+// w_out = w / (1^T w), the sum in a fixed order in fp64.  A negative, non-finite or all-zero w flags
+// HGS_SIMPLEX_DEGENERATE (w_out then = w).
+__global__ void __launch_bounds__(1024) k_weight_normalize(int E, const float* __restrict__ w, float* __restrict__ wo,
+                                                           int32_t* status) {
+  __shared__ double sm[32];
+  double s = 0.0, bad = 0.0;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const float x = w[e];
+    s += x;
+    if (!(x >= 0.f) || !isfinite(x)) bad += 1.0;
+  }
+  s = block_sum_d(s, sm);
+  bad = block_sum_d(bad, sm);
+  const bool ok = bad == 0.0 && s > 0.0;
+  if (!ok && threadIdx.x == 0) hg_flag(status, HGS_SIMPLEX_DEGENERATE);
+  const double inv = ok ? 1.0 / s : 1.0;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) wo[e] = (float)((double)w[e] * inv);
+}
+
 // P(w) = ||F||^2 - sum_e (w_e/delta(e)) sum_t s_{e,t}^2 + kappa ||w||^2 from the gradient at the same
 // w: w_e (2 kappa w_e - grad_e) = w_e sum_t s^2 / delta(e), so P = ||F||^2 + w^T grad - kappa ||w||^2.
 // Fixed-order fp64 sums: per-CTA partials, then one CTA adds them in order.
@@ -881,6 +901,13 @@ cudaError_t launch_weight_gradient(const CgArgs& a, float kappa, float* grad, cu
       a.T, Tp, at<int4>(a.ws, L.bigs), at<int32_t>(a.ws, L.totals), at<int32_t>(a.ws, L.de), a.w, kappa,
       at<float>(a.ws, L.part), grad);
   *launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_weight_normalize(int E, const float* w, float* wo, int32_t* status, cudaStream_t s,
+                                    int* launches) {
+  k_weight_normalize<<<1, 1024, 0, s>>>(E, w, wo, status);
+  ++*launches;
   return cudaGetLastError();
 }
 

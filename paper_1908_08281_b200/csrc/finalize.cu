@@ -54,7 +54,7 @@ __global__ void k_rank(int k, const double* __restrict__ sig, int32_t* __restric
 __global__ void __launch_bounds__(NT) k_rows(int b, int k, const float* __restrict__ Vw_t,
                                              const float* __restrict__ Uw_t, const int32_t* __restrict__ perm,
                                              const double* __restrict__ sig, float* __restrict__ Ut,
-                                             float* __restrict__ Vt) {
+                                             float* __restrict__ Vt, int uv_bk) {
   __shared__ float bv[NT / 32];
   __shared__ int bi[NT / 32];
   const int blk = blockIdx.x / k, jj = blockIdx.x % k;
@@ -86,6 +86,14 @@ __global__ void __launch_bounds__(NT) k_rows(int b, int k, const float* __restri
   // defined v_j: write 0 instead of inf/NaN (the R1 apply flags such a sigma, k_inv_sigma)
   const float vs = (sv > 1e-7 * smax && sv > 0.0) ? (float)((double)sgn / sv) : 0.f;
   const float* v = Vw_t + src;
+  if (uv_bk) {   // HG_UV_BK: U, V [nb][b][k] (column jj of U_i, V_i)
+    const int64_t ob = (int64_t)blk * b * k + jj;
+    for (int i = threadIdx.x; i < b; i += NT) {
+      Ut[ob + (int64_t)i * k] = sgn * u[i];
+      Vt[ob + (int64_t)i * k] = v[i] * vs;
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < b; i += NT) {
     Ut[dst + i] = sgn * u[i];
     Vt[dst + i] = v[i] * vs;
@@ -176,10 +184,10 @@ cudaError_t launch_unit_columns_t(int nb, int k, const float* Wf, float* Uk, cud
 
 cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float* Uw_t, float* Ut, float* sigma,
                             float* Vt, double* sig_raw, int32_t* perm, int32_t* status, cudaStream_t s,
-                            int* launches) {
+                            int* launches, bool uv_bk) {
   k_colnorm<<<nb * k, NT, 0, s>>>(b, Vw_t, sig_raw);
   k_rank<<<nb, 256, 0, s>>>(k, sig_raw, perm, sigma, status);
-  k_rows<<<nb * k, NT, 0, s>>>(b, k, Vw_t, Uw_t, perm, sig_raw, Ut, Vt);
+  k_rows<<<nb * k, NT, 0, s>>>(b, k, Vw_t, Uw_t, perm, sig_raw, Ut, Vt, uv_bk ? 1 : 0);
   *launches += 3;
   return cudaGetLastError();
 }

@@ -38,7 +38,7 @@ cudaError_t launch_jacobi(int nb, int k, const float* L, float* Wf, int32_t* sta
 // finalize.cu -- sigma_j = ||V_w column j|| (fp64), sort, normalise, sign rule
 cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float* Uw_t, float* Ut, float* sigma,
                             float* Vt, double* sig_raw, int32_t* perm, int32_t* status, cudaStream_t s,
-                            int* launches);
+                            int* launches, bool uv_bk = false);
 // apply prep: rs[i][j] = scale / sigma[i][j]; flags singular sigma
 // (sigma, rs are [nb][ld]; the first k per block are used, the rest of rs is zeroed)
 cudaError_t launch_inv_sigma(int nb, int k, int ld, const float* sigma, float scale, float* rs, int32_t* status,
@@ -109,6 +109,8 @@ cudaError_t launch_cg(const CgArgs& a, const CgGraphHook* hook, cudaStream_t s, 
 cudaError_t launch_weight_gradient(const CgArgs& a, float kappa, float* grad, cudaStream_t s, int* launches);
 cudaError_t launch_weight_step(int E, float* w, int32_t* active, const float* grad, float mu, int32_t* status,
                                cudaStream_t s, int* launches);
+cudaError_t launch_weight_normalize(int E, const float* w, float* wo, int32_t* status, cudaStream_t s,
+                                    int* launches);
 
 // schur.cu -- NEXT-1: the non-GEMM pieces of one Eq. 12 level
 cudaError_t launch_theta_offblock(int ns, int b, const int64_t* row_ptr, const int32_t* col, const int32_t* col_ptr,

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libhgrsvd.so")
 
 HG_OK, HG_ERR_INVALID, HG_ERR_NUMERICAL, HG_ERR_CUDA = 0, 2, 3, 4
 HG_RAW_THETA, HG_SYNC, HG_WOODBURY, HG_POWER_EQ10, HG_GEMM_SIMT = 1 << 0, 1 << 1, 1 << 2, 1 << 3, 1 << 8
+HG_GENERAL, HG_UV_BK = 1 << 4, 1 << 5
 ST_FLAGS = {1: "isolated vertex", 2: "empty hyperedge", 4: "Cholesky breakdown", 8: "Jacobi sweep cap",
             16: "singular sigma", 32: "non-finite value", 64: "CG breakdown", 128: "degenerate simplex"}
 
@@ -73,6 +74,9 @@ _weight_gradient = _sig("hg_weight_gradient", ctypes.c_int, ctypes.POINTER(_Inci
                         _P, _sz, _P)
 _weight_objective = _sig("hg_weight_objective", ctypes.c_int, _P, _i32, _i32, _i32, _P, _P, _f32, _P, _P, _sz, _P)
 _weight_step = _sig("hg_weight_step", ctypes.c_int, _i32, _P, _P, _P, _f32, _P, _P)
+_weight_normalize = _sig("hg_weight_normalize", ctypes.c_int, _i32, _P, _P, _P, _P)
+_block_apply_ex = _sig("hg_block_apply_inverse_ex", ctypes.c_int, _P, _P, _P, _i32, _i32, _i32, _P, _i32, _f32, _P,
+                       _u32, _P, _P, _sz, _P)
 _schur_ws = _sig("hg_schur_workspace_size", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, _i32, ctypes.POINTER(_sz))
 _solve_schur = _sig("hg_solve_schur", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _i32, _i32, _u64, _P,
                     _i32, _P, _u32, _P, _P, _sz, _P)
@@ -88,7 +92,8 @@ EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_
            "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve",
            "hg_block_apply_woodbury", "hg_workspace_size_ex", "hg_block_rsvd_ex", "hg_solve_ex",
            "hg_weight_gradient", "hg_weight_step", "hg_schur_workspace_size",
-           "hg_solve_schur", "hg_solve_blocks", "hg_weight_objective", "hg_debug_jacobi_sweepmax")
+           "hg_solve_schur", "hg_solve_blocks", "hg_weight_objective", "hg_debug_jacobi_sweepmax",
+           "hg_block_apply_inverse_ex", "hg_weight_normalize")
 
 
 class HGError(RuntimeError):
@@ -253,18 +258,21 @@ def fill_gaussian(seed: int, rows: int, cols: int, device="cuda", stream=None) -
 
 
 def block_rsvd(blocks: torch.Tensor, k: int, q: int, seed: int, *, simt: bool = False, p: int = 0,
-               eq10: bool = False, ws: Optional[Workspace] = None, status: Optional[torch.Tensor] = None,
-               stream=None):
-    """Alg. 1 on each block (oversampling p, Eq. 10 scheme with eq10): Ut [nb][k][b], sigma [nb][k],
-    Vt [nb][k][b], status."""
+               eq10: bool = False, general: bool = False, uv_bk: bool = False, ws: Optional[Workspace] = None,
+               status: Optional[torch.Tensor] = None, stream=None):
+    """Alg. 1 on each block (oversampling p, Eq. 10 scheme with eq10; general: literal X^T products for
+    non-symmetric blocks): Ut [nb][k][b], sigma [nb][k], Vt [nb][k][b], status -- with uv_bk the first and
+    third are U, V [nb][b][k]."""
     _dev(blocks, torch.float32)
     nb, b, _ = blocks.shape
     ws = ws or Workspace.for_sizes(nb * b, 1, 0, b, k, 0, p=p)
-    Ut = torch.empty((nb, k, b), dtype=torch.float32, device=blocks.device)
+    shape = (nb, b, k) if uv_bk else (nb, k, b)
+    Ut = torch.empty(shape, dtype=torch.float32, device=blocks.device)
     Vt = torch.empty_like(Ut)
     sigma = torch.empty((nb, k), dtype=torch.float32, device=blocks.device)
     st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=blocks.device)
-    flags = (HG_GEMM_SIMT if simt else 0) | (HG_POWER_EQ10 if eq10 else 0)
+    flags = (HG_GEMM_SIMT if simt else 0) | (HG_POWER_EQ10 if eq10 else 0) | (HG_GENERAL if general else 0) | \
+        (HG_UV_BK if uv_bk else 0)
     _check(_block_rsvd_ex(_ptr(blocks), nb, b, k, p, q, seed, flags, _ptr(Ut), _ptr(sigma), _ptr(Vt),
                           _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
     return Ut, sigma, Vt, st
@@ -282,6 +290,23 @@ def block_apply_inverse(Ut: torch.Tensor, sigma: torch.Tensor, Vt: torch.Tensor,
     st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=Y.device)
     _check(_block_apply(_ptr(Ut), _ptr(sigma), _ptr(Vt), nb, b, k, _ptr(Y), T, scale, _ptr(F), _ptr(st), ws.ptr,
                         ws.nbytes, _stream(stream)))
+    return F, st
+
+
+def block_apply_inverse_ex(U: torch.Tensor, sigma: torch.Tensor, V: torch.Tensor, Y: torch.Tensor, scale: float, *,
+                           uv_bk: bool = False, ws: Optional[Workspace] = None,
+                           status: Optional[torch.Tensor] = None, stream=None):
+    """block_apply_inverse with U, V in either layout: uv_bk -> [nb][b][k], else [nb][k][b]."""
+    for t in (U, sigma, V, Y):
+        _dev(t, torch.float32)
+    nb = U.shape[0]
+    b, k = (U.shape[1], U.shape[2]) if uv_bk else (U.shape[2], U.shape[1])
+    T = Y.shape[1]
+    ws = ws or Workspace.for_sizes(nb * b, 1, 0, b, k, T)
+    F = torch.empty((nb * b, T), dtype=torch.float32, device=Y.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=Y.device)
+    _check(_block_apply_ex(_ptr(U), _ptr(sigma), _ptr(V), nb, b, k, _ptr(Y), T, scale, _ptr(F),
+                           HG_UV_BK if uv_bk else 0, _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
     return F, st
 
 
@@ -420,6 +445,15 @@ def weight_step(w: torch.Tensor, active: torch.Tensor, grad: torch.Tensor, mu: f
     return st
 
 
+def weight_normalize(w: torch.Tensor, *, status: Optional[torch.Tensor] = None, stream=None):
+    """w / (1^T w) on the device (the start of the simplex iteration); returns (w_out, status)."""
+    _dev(w, torch.float32)
+    wo = torch.empty_like(w)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=w.device)
+    _check(_weight_normalize(w.numel(), _ptr(w), _ptr(wo), _ptr(st), _stream(stream)))
+    return wo, st
+
+
 def schur_workspace_size(N: int, E: int, nnz: int, b: int, k: int, T: int) -> int:
     out = _sz(0)
     _check(_schur_ws(N, E, nnz, b, k, T, ctypes.byref(out)))
@@ -460,7 +494,9 @@ def learn_weights(H: Incidence, w0: torch.Tensor, F: torch.Tensor, *, kappa: flo
     (gradient, step, objective); this loop only decides accept / reject.  Returns (w, active, trace of P, mu)."""
     N, T = F.shape
     ws = ws or Workspace(cg_workspace_size(N, H.n_edges, H.nnz, T, 0), F.device)
-    w = (w0 / w0.sum()).contiguous()
+    w, st0 = weight_normalize(w0.contiguous())
+    if int(st0.item()) != 0:
+        raise HGError(HG_ERR_NUMERICAL, "w0 is not a valid start for the simplex (negative, non-finite or zero sum)")
     active = torch.zeros(H.n_edges, dtype=torch.int32, device=F.device)
     g, st = weight_gradient(H, w, F, kappa=kappa, ws=ws)
     P = weight_objective(F, w, g, kappa=kappa)
@@ -488,7 +524,9 @@ def adaptive_learning(H: Incidence, w0: torch.Tensor, Y: torch.Tensor, *, mu: fl
     PAPER.md:165-178, or the block rSVD path with solver="rsvd"), then update w with F fixed
     (learn_weights), `outer` times.  Returns (F, w, history) with history[i] = (P before, P after) of
     outer pass i.  Composition of library calls only."""
-    w = (w0 / w0.sum()).contiguous()
+    w, st0 = weight_normalize(w0.contiguous())
+    if int(st0.item()) != 0:
+        raise HGError(HG_ERR_NUMERICAL, "w0 is not a valid start for the simplex (negative, non-finite or zero sum)")
     hist = []
     F = None
     for _ in range(outer):

@@ -28,6 +28,12 @@ def test_library_exports_every_declared_symbol():
     assert set(hg.EXPORTS) == set(names)
 
 
+def test_ragged_T_is_accepted():
+    """T % 4 != 0 is valid (Y, F pass through 16-byte-pitched workspace copies), and costs more workspace."""
+    from paper_1908_08281_b200 import hg
+    assert hg.workspace_size(128, 10, 10, 64, 8, 7) > hg.workspace_size(128, 10, 10, 64, 8, 8)
+
+
 def test_host_validation_is_synchronous_and_invalid():
     from paper_1908_08281_b200 import hg
     with pytest.raises(hg.HGError) as e:
@@ -35,7 +41,7 @@ def test_host_validation_is_synchronous_and_invalid():
     assert e.value.status == hg.HG_ERR_INVALID and "N % b" in str(e.value)
     for args in [(128, 10, 10, 64, 72, 0),                 # k > b
                  (128, 10, 10, 64, 6, 0),                  # k % 4
-                 (128, 10, 10, 64, 8, 6),                  # T % 4
+                 (128, 10, 10, 64, 8, -1),                 # T < 0
                  (1024, 10, 10, 1024, 1024, 0)]:           # k > 512
         with pytest.raises(hg.HGError) as e:
             hg.workspace_size(*args)
