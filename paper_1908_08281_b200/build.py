@@ -14,6 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhgrsvd.so")
+LIB_CHECK = os.path.join(HERE, "libhgrsvd_check.so")   # -DHG_BOUNDS_CHECK (device index checks)
 SOURCES = ["abi.cu", "gemm.cu", "theta.cu", "philox.cu", "chol.cu", "jacobi.cu", "jacobi_blk.cu", "finalize.cu", "cg.cu", "schur.cu", "eig.cu"]
 HEADERS = ["common.cuh", "gemm.cuh", "kernels.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -27,37 +28,37 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-STAMP = LIB + ".stamp"
-
-
-def _stamp() -> str:
+def _stamp(check: bool) -> str:
     """What the library was compiled with: a library built with other flags (e.g. debug defines
     through HG_NVCC_EXTRA) is never silently reused."""
-    extra = os.environ.get("HG_NVCC_EXTRA", "").split()
+    extra = os.environ.get("HG_NVCC_EXTRA", "").split() + (["-DHG_BOUNDS_CHECK"] if check else [])
     return " ".join(ARCH + FLAGS + extra + SOURCES)
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+def _stale(lib: str, check: bool) -> bool:
+    stamp = lib + ".stamp"
+    if not os.path.exists(lib) or not os.path.exists(stamp):
         return True
-    with open(STAMP) as f:
-        if f.read() != _stamp():
+    with open(stamp) as f:
+        if f.read() != _stamp(check):
             return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "hg.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    objdir = os.path.join(HERE, "build")
+def _build_one(lib: str, check: bool, force: bool, verbose: bool) -> str:
+    if not force and not _stale(lib, check):
+        return lib
+    objdir = os.path.join(HERE, "build_check" if check else "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    extra = os.environ.get("HG_NVCC_EXTRA", "").split()   # debug defines, e.g. -DHG_JB_SWEEPMAX
+    if check:
+        extra = extra + ["-DHG_BOUNDS_CHECK"]
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        extra = os.environ.get("HG_NVCC_EXTRA", "").split()   # debug defines, e.g. -DHG_JB_SWEEPMAX
         cmd = [nvcc(), *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
@@ -67,15 +68,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stdout.write(out)
         if p.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + out)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + " ".join(cmd) + "\n" + r.stdout)
-    os.replace(tmp, LIB)
-    with open(STAMP, "w") as f:
-        f.write(_stamp())
-    return LIB
+    os.replace(tmp, lib)
+    with open(lib + ".stamp", "w") as f:
+        f.write(_stamp(check))
+    return lib
+
+
+def build(force: bool = False, verbose: bool = False, check: bool = True) -> str:
+    """libhgrsvd.so and (check=True) its bounds-checked twin libhgrsvd_check.so (HG_LIB=check)."""
+    lib = _build_one(LIB, False, force, verbose)
+    if check:
+        _build_one(LIB_CHECK, True, force, verbose)
+    return lib
 
 
 if __name__ == "__main__":

@@ -272,7 +272,10 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   CHOL_CLK(0);
   float* tiles = SMEM ? sm : work + (int64_t)blockIdx.x * ((int64_t)ntiles * TILE);
   float* temp = SMEM ? sm + (int64_t)ntiles * TILE : sm;   // [nt-1] tiles in shared memory
-  auto T = [&](int i, int j) { return tiles + (int64_t)tidx(i, j) * TILE; };
+  auto T = [&](int i, int j) {
+    HG_DCHECK(i >= 0 && j >= 0 && j <= i && i < nt);
+    return tiles + (int64_t)tidx(i, j) * TILE;
+  };
 
   // Shifted retry (shifted CholeskyQR): if a pivot is <= 0 -- the fp32 Gram of an
   // ill-conditioned Y (e.g. X Omega with k = b, cond ~ 1e4) is numerically

@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include "../../include/hg.h"
 
@@ -25,6 +26,23 @@ enum : int32_t {
   HGS_CG_BREAKDOWN = 1 << 6,      // CG: p^T X p <= 0 (X is SPD, so only on corrupt input)
   HGS_SIMPLEX_DEGENERATE = 1 << 7,  // weight step: every hyperedge weight clamped to 0
 };
+
+// Bounds checks of the HG_BOUNDS_CHECK build (libhgrsvd_check.so): a violated index condition prints
+// its location and traps (the CUDA context reports an illegal instruction); compiled out otherwise.
+#ifdef HG_BOUNDS_CHECK
+#define HG_DCHECK(c)                                                                    \
+  do {                                                                                  \
+    if (!(c)) {                                                                         \
+      printf("HG_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             (int)blockIdx.x, (int)threadIdx.x);                                        \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define HG_DCHECK(c) \
+  do {               \
+  } while (0)
+#endif
 
 __device__ __forceinline__ void hg_flag(int32_t* st, int32_t f) {
   if (st) atomicOr(st, f);

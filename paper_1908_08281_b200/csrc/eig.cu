@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(576, 1) k_sytrd(int k, int ntl, const float* _
 #pragma unroll
   for (int s = 0; s < NSLOT; ++s) {
     const int p = warp + NWT * s;
+    HG_DCHECK(NWT * NSLOT >= nt);
     tI[s] = p < nt ? (tl[p] & 0xff) : 0;
     tJ[s] = p < nt ? (tl[p] >> 8) : 0;
     const int r = 32 * tI[s] + lane;
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(576, 1) k_sytrd(int k, int ntl, const float* _
       const int p = warp + NWT * s;
       if (p >= nrow) continue;
       const int I = tI[s], J = tJ[s], ti = tix(I, J);
+      HG_DCHECK(J <= I && I < ntl && ti < nt);
       const float* zJ = zs + 32 * J;
       float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
@@ -549,6 +551,7 @@ __global__ void __launch_bounds__(EIG_NT) k_trideig(int k, const float* __restri
   // overwritten by the new iterate) is carried over in a register.
   const float eps_piv = FLT_EPSILON;   // replaces an exactly zero pivot (T normalised: ||T|| ~ 1)
   float* xs = tsm + S.xs + t;          // xs[r * EIG_NT]
+  HG_DCHECK(S.xs + (k - 1) * EIG_NT + EIG_NT <= S.total);
   float* ck = tsm + S.ck + t;          // [seg][3][EIG_NT]
   // one elimination step on rows (r, r + 1) (branch-free partial pivoting): working row (w0, w1 | rw)
   // against row r + 1 (e_r, d_{r+1} - lam, e_{r+1} | ra); returns the U row (1/u0, u1, u2, ru)

@@ -309,8 +309,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         float* dcol = Dg + mw0 + 4 * l4;
         for (int j = lane >> 3; j < C::HALF; j += 4) {
           const int n = nb0 + j;
-          if (n < ea.N)
+          if (n < ea.N) {
+            HG_DCHECK(mw0 + 4 * l4 + 3 < ea.ldd);
             *reinterpret_cast<float4*>(dcol + (int64_t)n * ea.ldd) = *reinterpret_cast<const float4*>(st + j * TP + 4 * l4);
+          }
         }
       } else if (m < ea.M) {
 #pragma unroll

@@ -523,6 +523,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
             for (int j = 0; j < 4; ++j) accd[i][j] += acc[i][j];
         }
         const int owner = g % C, slot = g / C;
+        HG_DCHECK(slot < nown && owner < C);
         float* dst = Gp + ((size_t)rank * nown + slot) * PACK;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -584,6 +585,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
           const int g = g0 + pp;
           if (!(flag[g] & 1)) continue;
           const int owner = g % C, slot = g / C;
+          HG_DCHECK(slot < nown && pp < NQB && a < PW);
           const float* src = Qw + (size_t)slot * PW * LDQ + a * LDQ + 4 * c4;
           const float4 v = (owner == rank) ? *reinterpret_cast<const float4*>(src) : ld_cluster_f4(src, owner);
           const int sw = qsw(a);   // un-swizzle (see qsw): out[i] = v[i ^ sw]
@@ -605,6 +607,7 @@ __global__ void __launch_bounds__(NT, 1) k_jacobi_blk(int k, int C, double tol, 
           if (!(flag[g] & 1)) continue;
           int I, J;
           blocks_of(ro, g, I, J);
+          HG_DCHECK(4 * rq + 3 < R && BW * J + BW <= ldw && BW * I + BW <= ldw && pp < NQB);
           const float* Qp = Qb + (size_t)pp * PW * LDQ;
 #pragma unroll
           for (int i = 0; i < 4; ++i)

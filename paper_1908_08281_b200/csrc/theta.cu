@@ -727,7 +727,10 @@ __global__ void k_grp_fill(int N, int b, int E, const int64_t* __restrict__ row_
     const int64_t p1 = row_ptr[v + 1];
     for (int64_t p = row_ptr[v] + lane; p < p1; p += 32) {
       const int e = col[p];
-      memb[atomicAdd(&cur[off + e], 1)] = vl;
+      HG_DCHECK(e >= 0 && e < E);
+      const int pos = atomicAdd(&cur[off + e], 1);
+      HG_DCHECK(pos < start[off + e + 1]);
+      memb[pos] = vl;
       rng[p] = make_int2(start[off + e], start[off + e + 1]);
     }
   }
@@ -790,6 +793,7 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, const
         const float c = __shfl_sync(0xffffffffu, val, i);
         const int s = __shfl_sync(0xffffffffu, rs, i), l = __shfl_sync(0xffffffffu, len, i);
         const uint32_t* Ms = memb + s;
+        HG_DCHECK(s >= row_ptr[base] && s + l <= row_ptr[base + b]);
         int m = lane;
         for (; m + 96 < l; m += 128) {   // four loads in flight
           const uint32_t v0 = Ms[m], v1 = Ms[m + 32], v2 = Ms[m + 64], v3 = Ms[m + 96];
@@ -798,7 +802,10 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, const
           arow[v2] += c;
           arow[v3] += c;
         }
-        for (; m < l; m += 32) arow[Ms[m]] += c;
+        for (; m < l; m += 32) {
+          HG_DCHECK(Ms[m] < (uint32_t)b);
+          arow[Ms[m]] += c;
+        }
         __syncwarp();
         ++i;
         continue;
@@ -828,6 +835,7 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, const
         const float c = __shfl_sync(0xffffffffu, val, lo & 31);
         const bool act = q < total;
         const uint32_t v = act ? memb[s + (q - ex)] : 0xffffffffu;
+        HG_DCHECK(!act || (v < (uint32_t)b && s + (q - ex) < row_ptr[base + b]));
         stc[lane] = c;
         const unsigned am = __ballot_sync(0xffffffffu, act);
         __syncwarp();

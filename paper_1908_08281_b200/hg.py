@@ -14,7 +14,9 @@ from typing import Optional, Tuple
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhgrsvd.so")
+# HG_LIB=check loads the bounds-checked build (libhgrsvd_check.so: device traps on index violations,
+# the substitute for compute-sanitizer, which is closed on this pool)
+LIB_PATH = os.path.join(_HERE, "libhgrsvd_check.so" if os.environ.get("HG_LIB") == "check" else "libhgrsvd.so")
 
 HG_OK, HG_ERR_INVALID, HG_ERR_NUMERICAL, HG_ERR_CUDA = 0, 2, 3, 4
 HG_RAW_THETA, HG_SYNC, HG_WOODBURY, HG_POWER_EQ10, HG_GEMM_SIMT = 1 << 0, 1 << 1, 1 << 2, 1 << 3, 1 << 8

@@ -69,3 +69,20 @@ def test_cg_host_validation():
     a = hg.cg_workspace_size(512, 548, 4937, 20, 10)
     b = hg.cg_workspace_size(512, 548, 4937, 200, 10)
     assert 0 < a < b
+
+
+def test_bounds_checked_build_has_the_checks():
+    """libhgrsvd_check.so (HG_LIB=check, the compute-sanitizer substitute) carries the HG_DCHECK traps."""
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump):
+        pytest.skip("cuobjdump not available")
+    counts = []
+    for name in ("libhgrsvd.so", "libhgrsvd_check.so"):
+        path = os.path.join(root, "paper_1908_08281_b200", name)
+        assert os.path.exists(path), path
+        sass = subprocess.run([cuobjdump, "-sass", path], capture_output=True, text=True).stdout
+        counts.append(sass.count("BPT.TRAP"))
+    assert counts[1] > counts[0] + 20, counts
