@@ -386,6 +386,205 @@ __global__ void __launch_bounds__(576, 1) k_sytrd(int k, int ntl, const float* _
   EIG_CLK(2);
 }
 
+// ---------------------------------------------------------------- tridiagonalisation, 256 < k <= 512
+// The same algorithm as k_sytrd with the lower tiles of A in global scratch (L2-resident; 136 tiles of
+// 32 x 32 at k = 512 do not fit in one SM's registers or shared memory): 1024 threads, task lists by
+// tile column as in k_sytrd, the transposed half of the product by column tasks (lane = tile column,
+// coalesced), the rank-2 update with lane = tile column (coalesced stores).  Vectors in shared memory.
+constexpr int BIG_NT = 1024;
+constexpr int BIG_NW = BIG_NT / 32;
+constexpr int BIG_MAXNTL = 16;
+
+struct BigSmem {   // offsets in 4-byte words
+  int vs, ys, yrow, ycol, nrm, red, tl_incl, tl_strict, total;
+};
+__host__ __device__ inline BigSmem big_smem(int ntl) {
+  BigSmem S;
+  int off = 0;
+  const int nt = ntl * (ntl + 1) / 2, KP = 32 * ntl;
+  S.vs = off; off += KP;
+  S.ys = off; off += KP;
+  S.yrow = off; off += nt * 32;
+  S.ycol = off; off += nt * 32;
+  S.nrm = off; off += BIG_MAXNTL;
+  S.red = off; off += BIG_NW;
+  S.tl_incl = off; off += nt;
+  S.tl_strict = off; off += nt;
+  S.total = off;
+  return S;
+}
+
+__global__ void __launch_bounds__(BIG_NT, 1) k_sytrd_big(int k, int ntl, const float* __restrict__ A,
+                                                         float* __restrict__ tiles, float* __restrict__ Hv,
+                                                         float* __restrict__ tau_out, float* __restrict__ d_out,
+                                                         float* __restrict__ e_out) {
+  extern __shared__ __align__(16) float sm[];
+  const BigSmem S = big_smem(ntl);
+  float* vs = sm + S.vs;
+  float* ys = sm + S.ys;
+  float* yrow = sm + S.yrow;
+  float* ycol = sm + S.ycol;
+  float* nrm = sm + S.nrm;
+  float* red = sm + S.red;
+  int* tl_incl = reinterpret_cast<int*>(sm + S.tl_incl);
+  int* tl_strict = reinterpret_cast<int*>(sm + S.tl_strict);
+  const int blk = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int KP = 32 * ntl, nt = ntl * (ntl + 1) / 2;
+  const float* Ab = A + (int64_t)blk * k * k;
+  float* T = tiles + (int64_t)blk * nt * 1024;   // tile ti at T + ti * 1024, row-major 32 x 32
+  float* Hb = Hv + (int64_t)blk * k * k;
+  float* tb = tau_out + (int64_t)blk * k;
+  EIG_CLK(0);
+  auto At = [&](int r, int c) -> float& {   // element (r, c), r >= c or inside a diagonal tile
+    return T[tix(r >> 5, c >> 5) * 1024 + (r & 31) * 32 + (c & 31)];
+  };
+  for (int idx = t; idx < nt * 1024; idx += BIG_NT) {
+    const int ti = idx >> 10, rr = (idx >> 5) & 31, cc = idx & 31;
+    int I = 0;
+    while (tix(I + 1, 0) <= ti) ++I;
+    const int J = ti - tix(I, 0);
+    const int r = 32 * I + rr, c = 32 * J + cc;
+    float v = 0.f;
+    if (r < k && c < k) v = (r >= c) ? Ab[(int64_t)r * k + c] : Ab[(int64_t)c * k + r];
+    T[idx] = v;
+  }
+  if (t == 0) {
+    int a = 0, b = 0;
+    for (int J = ntl - 1; J >= 0; --J)
+      for (int I = J; I < ntl; ++I) {
+        tl_incl[a++] = I | (J << 8);
+        if (I > J) tl_strict[b++] = I | (J << 8);
+      }
+  }
+  for (int i = t; i < KP; i += BIG_NT) { vs[i] = 0.f; ys[i] = 0.f; }
+  if (t < BIG_MAXNTL) nrm[t] = 0.f;
+  __syncthreads();
+  if (warp < ntl) {   // norm partials of column 0 (rows >= 2), one per tile row
+    const int r = 32 * warp + lane;
+    const float x = (r >= 2 && r < k) ? At(r, 0) : 0.f;
+    const float s = warp_sum_f(x * x);
+    if (lane == 0) nrm[warp] = s;
+  }
+  __syncthreads();
+  EIG_CLK(1);
+  for (int j = 0; j + 2 < k; ++j) {
+    const int t0 = (j + 1) >> 5, ntr = ntl - t0, jt = j >> 5, cj = j & 31;
+    const int nrow = ntr * (ntr + 1) / 2, nstr = ntr * (ntr - 1) / 2;
+    // (b) y' = A22 z, z = column j masked to rows > j
+    for (int task = warp; task < nrow + nstr; task += BIG_NW) {
+      const bool rowmode = task < nrow;
+      const int ij = rowmode ? tl_incl[task] : tl_strict[task - nrow];
+      const int I = ij & 0xff, J = ij >> 8, ti = tix(I, J);
+      HG_DCHECK(J <= I && I < ntl);
+      const float* Tt = T + ti * 1024;
+      const int zr = 32 * (rowmode ? J : I) + lane;
+      const float zl = (zr > j && zr < k) ? T[tix(zr >> 5, jt) * 1024 + lane * 32 + cj] : 0.f;
+      float acc0 = 0.f, acc1 = 0.f;
+      if (rowmode) {
+        const float* row = Tt + lane * 32;
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          acc0 = fmaf(row[c], __shfl_sync(0xffffffffu, zl, c), acc0);
+          acc1 = fmaf(row[c + 1], __shfl_sync(0xffffffffu, zl, c + 1), acc1);
+        }
+        yrow[ti * 32 + lane] = acc0 + acc1;
+      } else {
+#pragma unroll
+        for (int r = 0; r < 32; r += 2) {
+          acc0 = fmaf(Tt[r * 32 + lane], __shfl_sync(0xffffffffu, zl, r), acc0);
+          acc1 = fmaf(Tt[(r + 1) * 32 + lane], __shfl_sync(0xffffffffu, zl, r + 1), acc1);
+        }
+        ycol[ti * 32 + lane] = acc0 + acc1;
+      }
+    }
+    __syncthreads();
+    // (c) Householder scalars, v, y = A22 v, y^T v
+    float xn2 = 0.f;
+    for (int I = (j + 2) >> 5; I < ntl; ++I) xn2 += nrm[I];
+    const float alpha = At(j + 1, j);
+    float beta = alpha, tau = 0.f, scal = 0.f;
+    if (xn2 > 0.f) {
+      beta = -copysignf(sqrtf(fmaf(alpha, alpha, xn2)), alpha);
+      tau = __fdividef(beta - alpha, beta);
+      scal = __fdividef(1.f, alpha - beta);
+    }
+    float dot = 0.f;
+    for (int r = t; r < KP; r += BIG_NT) {
+      float v = 0.f, y = 0.f;
+      if (r > j && r < k) {
+        const int I = r >> 5, rr = r & 31;
+        float yp = 0.f;
+        for (int J = t0; J <= I; ++J) yp += yrow[tix(I, J) * 32 + rr];
+        for (int I2 = I + 1; I2 < ntl; ++I2) yp += ycol[tix(I2, I) * 32 + rr];
+        v = (r == j + 1) ? 1.f : At(r, j) * scal;
+        y = scal * fmaf(-beta, At(r, j + 1), yp);
+      }
+      vs[r] = v;
+      ys[r] = y;
+      if (r < k) Hb[(int64_t)j * k + r] = v;
+      dot = fmaf(y, v, dot);
+    }
+    if (t == 0) {
+      d_out[(int64_t)blk * k + j] = At(j, j);
+      e_out[(int64_t)blk * k + j] = beta;
+      tb[j] = tau;
+    }
+    dot = warp_sum_f(dot);
+    if (lane == 0) red[warp] = dot;
+    __syncthreads();
+    const int J1 = t0, c1 = (j + 1) & 31;
+    if (tau == 0.f) {   // H_j = I: no update; the next column's norm from A as it is
+      if (warp < ntl) {
+        const int r = 32 * warp + lane;
+        const float x = (r >= j + 3 && r < k && warp >= J1) ? At(r, j + 1) : 0.f;
+        const float s = warp_sum_f(x * x);
+        if (lane == 0) nrm[warp] = s;
+      }
+      __syncthreads();
+      continue;
+    }
+    float yv = 0.f;
+    for (int w = 0; w < BIG_NW; ++w) yv += red[w];
+    const float Kc = 0.5f * tau * tau * yv;
+    // (d) A22 -= v w^T + w v^T, lane = tile column (coalesced); w = tau y - Kc v formed on the fly; the
+    //     warps on tile column J1 accumulate the norm partials of column j + 1 (rows >= j + 3)
+    for (int task = warp; task < nrow; task += BIG_NW) {
+      const int ij = tl_incl[task];
+      const int I = ij & 0xff, J = ij >> 8;
+      float* Tt = T + tix(I, J) * 1024;
+      const int cg = 32 * J + lane;
+      const float vc = vs[cg], wc = fmaf(tau, ys[cg], -Kc * vc);
+      float part = 0.f;
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) {
+        const int rg = 32 * I + r;
+        const float vr = vs[rg], wr = fmaf(tau, ys[rg], -Kc * vr);
+        const float a = __fsub_rn(Tt[r * 32 + lane], __fadd_rn(__fmul_rn(vr, wc), __fmul_rn(wr, vc)));
+        Tt[r * 32 + lane] = a;
+        if (J == J1 && lane == c1 && rg >= j + 3 && rg < k) part = fmaf(a, a, part);
+      }
+      if (J == J1) {
+        const float s = warp_sum_f(part);
+        if (lane == 0) nrm[I] = s;
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    float* db = d_out + (int64_t)blk * k;
+    float* eb = e_out + (int64_t)blk * k;
+    if (k >= 2) {
+      db[k - 2] = At(k - 2, k - 2);
+      eb[k - 2] = At(k - 1, k - 2);
+      tb[k - 2] = 0.f;
+    }
+    db[k - 1] = At(k - 1, k - 1);
+    eb[k - 1] = 0.f;
+    tb[k - 1] = 0.f;
+  }
+  EIG_CLK(2);
+}
+
 // ---------------------------------------------------------------- eigenpairs of T
 // CTAs of EIG_NT threads, ceil(k / EIG_NT) per block, thread per eigenvalue.  (1) T / tn (tn = max
 // |Gershgorin bound|): the division-free Sturm counts stay in range; eigenvectors are unchanged.
@@ -628,22 +827,22 @@ __global__ void __launch_bounds__(EIG_NT) k_trideig(int k, const float* __restri
 }
 
 // Q^T with Q = H_0 H_1 ... H_{k-3} (LAPACK orgtr, backward accumulation): column c of Q is
-// H_0 ... H_{c-1} e_c (H_j e_c = e_c for j >= c), applied from the inside out.  Warp per 8 columns
+// H_0 ... H_{c-1} e_c (H_j e_c = e_c for j >= c), applied from the inside out.  Warp per CPW columns
 // (lane = rows lane + 32 s), no block barrier; out[c][r] = Q[r][c].
-template <int RPL>
+template <int RPL, int CPW>
 __global__ void __launch_bounds__(128) k_orgtr(int k, const float* __restrict__ Hv, const float* __restrict__ tau,
                                                float* __restrict__ Qt) {
   const int blk = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c0 = (blockIdx.y * 4 + warp) * 8;
+  const int c0 = (blockIdx.y * 4 + warp) * CPW;
   if (c0 >= k) return;
   const float* Hb = Hv + (int64_t)blk * k * k;
   const float* tb = tau + (int64_t)blk * k;
-  float z[RPL][8];
+  float z[RPL][CPW];
 #pragma unroll
   for (int s = 0; s < RPL; ++s)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) z[s][q] = (lane + 32 * s == c0 + q) ? 1.f : 0.f;
-  const int jtop = min(k - 3, c0 + 6);   // the largest j < the warp's largest column
+    for (int q = 0; q < CPW; ++q) z[s][q] = (lane + 32 * s == c0 + q) ? 1.f : 0.f;
+  const int jtop = min(k - 3, c0 + CPW - 2);   // the largest j < the warp's largest column
   float vn[RPL];
   auto loadv = [&](int j, float* v) {
 #pragma unroll
@@ -661,27 +860,29 @@ __global__ void __launch_bounds__(128) k_orgtr(int k, const float* __restrict__ 
     const float tj = tb[j];
     if (tj == 0.f) continue;
     const int s0 = (j + 1) >> 5;   // rows <= j: v = 0
-    float dot[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float dot[CPW];
+#pragma unroll
+    for (int q = 0; q < CPW; ++q) dot[q] = 0.f;
 #pragma unroll
     for (int s = 0; s < RPL; ++s)
       if (s >= s0)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) dot[q] = fmaf(v[s], z[s][q], dot[q]);
+        for (int q = 0; q < CPW; ++q) dot[q] = fmaf(v[s], z[s][q], dot[q]);
 #pragma unroll
     for (int o = 16; o; o >>= 1)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) dot[q] += __shfl_xor_sync(0xffffffffu, dot[q], o);
+      for (int q = 0; q < CPW; ++q) dot[q] += __shfl_xor_sync(0xffffffffu, dot[q], o);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) dot[q] *= -tj;
+    for (int q = 0; q < CPW; ++q) dot[q] *= -tj;
 #pragma unroll
     for (int s = 0; s < RPL; ++s)
       if (s >= s0)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) z[s][q] = fmaf(dot[q], v[s], z[s][q]);
+        for (int q = 0; q < CPW; ++q) z[s][q] = fmaf(dot[q], v[s], z[s][q]);
   }
   float* ob = Qt + (int64_t)blk * k * k;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < CPW; ++q) {
     if (c0 + q >= k) continue;
 #pragma unroll
     for (int s = 0; s < RPL; ++s) {
@@ -697,10 +898,15 @@ extern "C" int hg_debug_eig_clocks(long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_eig_clk, sizeof(g_eig_clk));
 }
 
-// per block: tau [k], scale [k], d [k], e [k] (a multiple of 4 floats: 16-byte aligned per part)
-size_t eig_scratch_floats(int k) { return ((size_t)4 * k + 3) / 4 * 4; }
+// per block: tau [k], scale [k], d [k], e [k] (a multiple of 4 floats: 16-byte aligned per part), and for
+// k > 256 the lower tiles of A for k_sytrd_big (nt x 32 x 32)
+static int big_ntl(int k) { return k > 256 ? (k + 31) / 32 : 0; }
+size_t eig_scratch_floats(int k) {
+  const size_t ntl = big_ntl(k);
+  return ((size_t)4 * k + 3) / 4 * 4 + ntl * (ntl + 1) / 2 * 1024;
+}
 
-bool eig_precond_supported(int k) { return k >= 1 && k <= 256; }
+bool eig_precond_supported(int k) { return k >= 1 && k <= 512; }
 
 cudaError_t launch_eig_precond(int nb, int k, const float* A, float* Hv, float* Z, float* scratch, float* Qt,
                                const float** scale, cudaStream_t s, int* launches) {
@@ -711,11 +917,19 @@ cudaError_t launch_eig_precond(int nb, int k, const float* A, float* Hv, float* 
   float* dd = scratch + (size_t)2 * nb * k;     // [nb][k]
   float* ee = scratch + (size_t)3 * nb * k;     // [nb][k]
   *scale = sc;
-  const TrdSmem S = trd_smem(ntl);
-  const size_t smem = (size_t)S.total * 4;
-  k_sytrd<<<nb, 32 * sytrd_warps(ntl), smem, s>>>(k, ntl, A, Hv, tau, dd, ee);
+  cudaError_t e;
+  if (ntl <= 8) {   // k <= 256: register-resident tiles
+    const TrdSmem S = trd_smem(ntl);
+    k_sytrd<<<nb, 32 * sytrd_warps(ntl), (size_t)S.total * 4, s>>>(k, ntl, A, Hv, tau, dd, ee);
+  } else {          // 256 < k <= 512: tiles in (L2-resident) global scratch after d, e
+    const size_t smem = (size_t)big_smem(ntl).total * 4;
+    e = cudaFuncSetAttribute(k_sytrd_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    float* tiles = scratch + ((size_t)4 * nb * k + 3) / 4 * 4;
+    k_sytrd_big<<<nb, BIG_NT, smem, s>>>(k, ntl, A, tiles, Hv, tau, dd, ee);
+  }
   ++*launches;
-  cudaError_t e = cudaGetLastError();
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const size_t td_bytes = (size_t)td_smem(k).total * 4;
   e = cudaFuncSetAttribute(k_trideig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)td_bytes);
@@ -724,16 +938,18 @@ cudaError_t launch_eig_precond(int nb, int k, const float* A, float* Hv, float* 
   ++*launches;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const dim3 grid(nb, (k + 31) / 32);
+  const dim3 grid(nb, (k + 31) / 32), grid16(nb, (k + 15) / 16);
   switch (ntl) {
-    case 1: k_orgtr<1><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
-    case 2: k_orgtr<2><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
-    case 3: k_orgtr<3><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
-    case 4: k_orgtr<4><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
-    case 5: k_orgtr<5><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
-    case 6: k_orgtr<6><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
-    case 7: k_orgtr<7><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
-    default: k_orgtr<8><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 1: k_orgtr<1, 8><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 2: k_orgtr<2, 8><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 3: k_orgtr<3, 8><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 4: k_orgtr<4, 8><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 5: k_orgtr<5, 8><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 6: k_orgtr<6, 8><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 7: k_orgtr<7, 8><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 8: k_orgtr<8, 8><<<grid, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    case 9: case 10: case 11: case 12: k_orgtr<12, 4><<<grid16, 128, 0, s>>>(k, Hv, tau, Qt); break;
+    default: k_orgtr<16, 4><<<grid16, 128, 0, s>>>(k, Hv, tau, Qt); break;
   }
   ++*launches;
   return cudaGetLastError();

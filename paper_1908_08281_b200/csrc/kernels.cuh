@@ -127,7 +127,7 @@ cudaError_t launch_csc_setup(const CgArgs& a, cudaStream_t s, int* launches);
 cudaError_t launch_weight_objective(int64_t nF, const float* F, int E, const float* w, const float* grad, float kappa,
                                     double* part, double* out, cudaStream_t s, int* launches);
 
-// eig.cu -- eigen-preconditioner of the Jacobi (k <= 256): from A = L^T L [nb][k][k] (lower triangle
+// eig.cu -- eigen-preconditioner of the Jacobi (k <= 512): from A = L^T L [nb][k][k] (lower triangle
 // read): Q^T A Q = T tridiagonal (Hv: Householder vectors, [nb][k][k]), Z [nb][k][k] column i = the
 // (unnormalised) eigenvector of T for its i-th smallest eigenvalue, *scale -> [nb][k] its 1/norm, and
 // Qt [nb][k][k] = Q^T.  The approximate eigenvectors of A are the columns of Q Z diag(scale).

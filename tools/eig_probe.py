@@ -19,9 +19,13 @@ from synth.hypergraph import CONFIGS, make_input  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--b", type=int)
+    ap.add_argument("--k", type=int)
+    ap.add_argument("--q", type=int)
     a = ap.parse_args()
     os.environ["HG_STREAMS"] = "1"
     c = CONFIGS[a.config]
+    c = c.with_(**{n: getattr(a, n) for n in ("b", "k", "q") if getattr(a, n) is not None})
     h = make_input(c)
     H = hg.incidence_to_device(h.row_ptr, h.col_idx, h.E)
     w = torch.from_numpy(h.w).cuda()
