@@ -74,6 +74,8 @@ def lib() -> ctypes.CDLL:
         L.or_lowrank_inverse.argtypes = [i32, i32, i32, P, P, dbl, P]
         L.or_lowrank_inverse.restype = ci
         L.or_solve_schur.argtypes = [i32, i32, P, P, P, dbl, i32, i32, i32, u64, P, i32, i32, P, P, cp, ci]
+        L.or_solve_nested.argtypes = [i32, i32, P, P, P, dbl, i32, i32, i32, i32, u64, P, i32, i32, P, P, cp, ci]
+        L.or_solve_nested.restype = ci
         L.or_solve_schur.restype = ci
         L.or_weight_objective.argtypes = [i32, i32, P, P, P, P, i32, dbl, P, cp, ci]
         L.or_weight_objective.restype = ci
@@ -374,6 +376,28 @@ def lowrank_inverse(K, Omega, q: int, mu: float) -> np.ndarray:
     if st != OK:
         raise OracleError(st, "SVD did not converge")
     return out
+
+
+def solve_nested(row_ptr, col_idx, w, Y, *, mu: float, b: int, levels: int, k: int, q: int, seed: int,
+                 superblocks: Optional[Sequence[int]] = None):
+    """Nested tessellation: Eq. 12 recursively inside super-blocks of m = 2^levels b, leaves
+    b x b, level-l Schur complements at rank k 2^(l-1); returns (F [n*m][T], superblocks, seconds)."""
+    row_ptr, col_idx, w = _csr(row_ptr, col_idx, w)
+    Y = np.ascontiguousarray(Y, np.float32)
+    N, E = len(row_ptr) - 1, len(w)
+    T = Y.shape[1]
+    m = b << levels
+    ns = N // m if m > 0 else 0
+    sel = np.asarray(range(ns) if superblocks is None else superblocks, dtype=np.int32)
+    F = np.zeros((len(sel) * m, T))
+    err = ctypes.create_string_buffer(256)
+    t0 = time.perf_counter()
+    st = lib().or_solve_nested(N, E, _p(row_ptr), _p(col_idx), _p(w), mu, b, levels, k, q, seed, _p(Y), T,
+                               len(sel), _p(sel), _p(F), err, 256)
+    dt = time.perf_counter() - t0
+    if st != OK:
+        raise OracleError(st, err.value.decode())
+    return F, list(map(int, sel)), dt
 
 
 def solve_schur(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, seed: int,

@@ -28,6 +28,8 @@
  *   or_lowrank_inverse  NEXT-3 reading R2: (I - K/(1+theta))^-1 ~ I + U diag(s/((1+theta)-s)) U^T, Alg. 1 on K
  *   or_solve_schur      PAPER.md:127-154 Eqs. 11-14 (NEXT-1): one 2x2 Schur level over pairs of adjacent
  *                       diagonal blocks, X11^-1, X22^-1, Z1^-1, Z2^-1 by rSVD (reading R2)
+ *   or_solve_nested     PAPER.md:155-156 (NEXT-1): the nested tessellation, Eq. 12 recursively inside
+ *                       super-blocks of 2^L b vertices, leaves and Schur complements by reading R2
  *   or_weight_objective PAPER.md:46-52   P(w) = sum_t f_t^T L f_t + kappa ||w||^2, L = I - Theta(w) (NEXT-4)
  *   or_weight_gradient  PAPER.md:56-58   frozen-degree gradient of P (SPEC.md gradient_frozen)
  *   or_weight_step      PAPER.md:54-58   w <- w - mu grad on the simplex, clamped coordinates stay 0
@@ -696,6 +698,125 @@ int or_solve_schur(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* 
     }
     free(T11); free(T22); free(T12); free(T21); free(A11); free(A22); free(Z1i); free(Z2i); free(W1);
     free(K1); free(K2); free(O1); free(O2); free(Of); free(Y1); free(Y2); free(G); free(H); free(P);
+  }
+  free(dv); free(de);
+  if (fail) { set_err(err, errlen, "numerical failure in a randomized SVD"); return fail; }
+  return OR_OK;
+}
+
+/* Nested tessellation ("nested tessellations of submatrices created along the main
+ * diagonal"; reading S4 in DESIGN.md): the inverse of a super-block of m = 2^L b vertices by Eq. 12
+ * applied recursively to its diagonal halves down to b x b leaves.  A node of n = 2^l b vertices
+ * starting at vertex r0 (l >= 1, halves of h = n/2):
+ *   A11 = inverse of the first half, A22 = of the second (the recursion; leaves by reading R2 with
+ *   rank k and Omega = rows [r0, r0+b) of the N x k Philox matrix);
+ *   Theta11, Theta22 = the halves' Theta blocks, Theta12 = Theta[first half, second half], Theta21
+ *   literally (or_theta_offblock with block size h);
+ *   K_Z1 = Theta11 + Theta12 A22 Theta21/(1+mu), K_Z2 = Theta22 + Theta21 A11 Theta12/(1+mu)
+ *   (Eqs. 13-14 with X12 = -Theta12/(1+mu), reading S2); Z1^-1, Z2^-1 by or_lowrank_inverse at rank
+ *   k_l = k 2^(l-1) (the same rank-to-dimension ratio k/b at every level, reading S5) with Omega =
+ *   rows [r0, r0+h) resp. [r0+h, r0+n) of the N x k_l Philox matrix (reading S3 generalised);
+ *   node inverse (Eq. 12, X12 = -Theta12/(1+mu), X21 = -Theta21/(1+mu)):
+ *     [[Z1^-1, A11 Theta12 Z2^-1/(1+mu)], [Z2^-1 Theta21 A11/(1+mu), Z2^-1]].
+ * Writes the node's inverse Ainv and Theta block (both n x n, dense). */
+static int nested_node(int32_t N, int32_t l, int64_t r0, int32_t b, int32_t k, int32_t q, uint64_t seed, double mu,
+                       const int64_t* row_ptr, const int32_t* col_idx, const float* w, const double* dv,
+                       const double* de, double* Ainv, double* Th) {
+  const int64_t n = (int64_t)b << l;
+  if (l == 0) {
+    double* Om = (double*)malloc(sizeof(double) * (size_t)b * k);
+    float* Of = (float*)malloc(sizeof(float) * (size_t)b * k);
+    or_theta_block(b, (int32_t)(r0 / b), row_ptr, col_idx, w, dv, de, 0.0, Th);
+    or_gaussian_f32(seed, r0 * k, (int64_t)b * k, Of);
+    for (int64_t i = 0; i < (int64_t)b * k; ++i) Om[i] = (double)Of[i];
+    int st = or_lowrank_inverse(b, k, q, Th, Om, mu, Ainv);
+    free(Om); free(Of);
+    return st;
+  }
+  const int64_t h = n / 2, hh = h * h;
+  const int32_t kl = k << (l - 1);
+  const double ip = 1.0 / (1.0 + mu);
+  double *A11 = malloc(sizeof(double) * hh), *A22 = malloc(sizeof(double) * hh);
+  double *T11 = malloc(sizeof(double) * hh), *T22 = malloc(sizeof(double) * hh);
+  double *T12 = malloc(sizeof(double) * hh), *T21 = malloc(sizeof(double) * hh);
+  double *W1 = malloc(sizeof(double) * hh), *K1 = malloc(sizeof(double) * hh), *K2 = malloc(sizeof(double) * hh);
+  double *Z1i = malloc(sizeof(double) * hh), *Z2i = malloc(sizeof(double) * hh);
+  double *O1 = malloc(sizeof(double) * h * kl), *O2 = malloc(sizeof(double) * h * kl);
+  float* Of = malloc(sizeof(float) * h * kl);
+  int st = nested_node(N, l - 1, r0, b, k, q, seed, mu, row_ptr, col_idx, w, dv, de, A11, T11);
+  st |= nested_node(N, l - 1, r0 + h, b, k, q, seed, mu, row_ptr, col_idx, w, dv, de, A22, T22);
+  or_theta_offblock((int32_t)h, (int32_t)(r0 / h), (int32_t)(r0 / h + 1), row_ptr, col_idx, w, dv, de, T12);
+  or_theta_offblock((int32_t)h, (int32_t)(r0 / h + 1), (int32_t)(r0 / h), row_ptr, col_idx, w, dv, de, T21);
+  mm((int)h, (int)h, (int)h, A22, T21, W1);
+  mm((int)h, (int)h, (int)h, T12, W1, K1);
+  for (int64_t i = 0; i < hh; ++i) K1[i] = T11[i] + ip * K1[i];
+  mm((int)h, (int)h, (int)h, A11, T12, W1);
+  mm((int)h, (int)h, (int)h, T21, W1, K2);
+  for (int64_t i = 0; i < hh; ++i) K2[i] = T22[i] + ip * K2[i];
+  or_gaussian_f32(seed, r0 * kl, h * kl, Of);
+  for (int64_t i = 0; i < h * kl; ++i) O1[i] = (double)Of[i];
+  or_gaussian_f32(seed, (r0 + h) * kl, h * kl, Of);
+  for (int64_t i = 0; i < h * kl; ++i) O2[i] = (double)Of[i];
+  st |= or_lowrank_inverse((int32_t)h, kl, q, K1, O1, mu, Z1i);
+  st |= or_lowrank_inverse((int32_t)h, kl, q, K2, O2, mu, Z2i);
+  /* top-right A11 Theta12 Z2^-1 / (1+mu) -> K1 (scratch); bottom-left Z2^-1 Theta21 A11 / (1+mu) -> K2 */
+  mm((int)h, (int)h, (int)h, A11, T12, W1);
+  mm((int)h, (int)h, (int)h, W1, Z2i, K1);
+  mm((int)h, (int)h, (int)h, Z2i, T21, W1);
+  mm((int)h, (int)h, (int)h, W1, A11, K2);
+  for (int64_t i = 0; i < h; ++i)
+    for (int64_t j = 0; j < h; ++j) {
+      Ainv[i * n + j] = Z1i[i * h + j];
+      Ainv[i * n + h + j] = ip * K1[i * h + j];
+      Ainv[(h + i) * n + j] = ip * K2[i * h + j];
+      Ainv[(h + i) * n + h + j] = Z2i[i * h + j];
+      Th[i * n + j] = T11[i * h + j];
+      Th[i * n + h + j] = T12[i * h + j];
+      Th[(h + i) * n + j] = T21[i * h + j];
+      Th[(h + i) * n + h + j] = T22[i * h + j];
+    }
+  free(A11); free(A22); free(T11); free(T22); free(T12); free(T21); free(W1); free(K1); free(K2); free(Z1i);
+  free(Z2i); free(O1); free(O2); free(Of);
+  return st;
+}
+
+/* F_s = c A_s^-1 Y_s (Eq. 3) for the selected super-blocks s of m = 2^L b vertices (nested_node at
+ * level L); F is [n_sel * m][T] in sel order.  Constraints: L >= 1, N % m == 0, 1 <= k <= b. */
+int or_solve_nested(int32_t N, int32_t E, const int64_t* row_ptr, const int32_t* col_idx, const float* w,
+                    double mu, int32_t b, int32_t L, int32_t k, int32_t q, uint64_t seed, const float* Y, int32_t T,
+                    int32_t n_sel, const int32_t* sel, double* F, char* err, int errlen) {
+  const int64_t m = (int64_t)b << (L > 0 ? L : 0);
+  if (N <= 0 || E <= 0 || b <= 0 || L < 1 || L > 8 || N % m != 0 || k < 1 || k > b || q < 0 || !(mu > 0.0) ||
+      T < 0) {
+    set_err(err, errlen, "invalid arguments (need L >= 1, N % (2^L b) == 0, 1 <= k <= b, q >= 0, mu > 0)");
+    return OR_ERR_INVALID;
+  }
+  for (int i = 0; i < n_sel; ++i)
+    if (sel[i] < 0 || sel[i] >= N / m) { set_err(err, errlen, "super-block out of range"); return OR_ERR_INVALID; }
+  double* dv = (double*)malloc(sizeof(double) * (size_t)N);
+  double* de = (double*)malloc(sizeof(double) * (size_t)E);
+  int st = or_degrees(N, E, row_ptr, col_idx, w, dv, de, err, errlen);
+  if (st != OR_OK) { free(dv); free(de); return st; }
+  const double c = mu / (1.0 + mu);
+  int fail = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int s = 0; s < n_sel; ++s) {
+    double* Ainv = (double*)malloc(sizeof(double) * (size_t)(m * m));
+    double* Th = (double*)malloc(sizeof(double) * (size_t)(m * m));
+    const int64_t r0 = (int64_t)sel[s] * m;
+    int r = nested_node(N, L, r0, b, k, q, seed, mu, row_ptr, col_idx, w, dv, de, Ainv, Th);
+    if (r) {
+#pragma omp atomic write
+      fail = OR_ERR_NUMERICAL;
+    }
+    double* Fs = F + (size_t)s * m * T;
+    for (int64_t i = 0; i < m; ++i)
+      for (int t = 0; t < T; ++t) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < m; ++j) acc += Ainv[i * m + j] * (double)Y[(r0 + j) * T + t];
+        Fs[i * T + t] = c * acc;
+      }
+    free(Ainv); free(Th);
   }
   free(dv); free(de);
   if (fail) { set_err(err, errlen, "numerical failure in a randomized SVD"); return fail; }
