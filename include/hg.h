@@ -258,6 +258,23 @@ hg_status hg_schur_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t b, 
 hg_status hg_solve_schur(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
                          uint64_t seed, const float* Y, int32_t T, float* F, uint32_t flags, int32_t* d_status,
                          void* ws, size_t ws_bytes, hg_stream_t stream);
+/* ---- NEXT-1: the nested tessellation ("nested tessellations of
+ * submatrices created along the main diagonal"), reading S4: Eq. 12 applied recursively inside super-
+ * blocks of m = 2^levels b vertices down to b x b leaves.  A node of n = 2^l b vertices (l >= 1) takes
+ * its halves' inverses A11, A22 from the level below, Theta12 between its halves, the Schur complements
+ *   K_Z1 = Theta11 + Theta12 A22 Theta21/(1+mu),  K_Z2 = Theta22 + Theta21 A11 Theta12/(1+mu)
+ * (Eqs. 13-14, X = I - Theta/(1+mu)), inverts Z1 = I - K_Z1/(1+mu), Z2 likewise by Alg. 1 at rank
+ * k_l = k 2^(l-1) + Woodbury (reading R2; Omega = the halves' rows of the N x k_l Philox matrix), and
+ * materialises its inverse [[Z1^-1, A11 Theta12 Z2^-1/(1+mu)], [(.)^T, Z2^-1]] (Eq. 12); leaves by
+ * Alg. 1 on Theta_ii at rank k.  F_s = mu/(1+mu) A_s^-1 Y_s (Eq. 3).  levels = 1 is hg_solve_schur's
+ * one-level scheme; k = b makes every inverse exact (the super-block solve).
+ *   1 <= levels <= 6, N % (2^levels b) == 0, 1 <= k <= b, k 2^(levels-1) <= 512, T % 4 == 0.
+ *   Workspace: hg_nested_workspace_size (dense node matrices: ~4 N 2^levels b floats).  flags: HG_SYNC. */
+hg_status hg_nested_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t b, int32_t levels, int32_t k, int32_t T,
+                                   size_t* bytes);
+hg_status hg_solve_nested(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t levels, int32_t k,
+                          int32_t q, uint64_t seed, const float* Y, int32_t T, float* F, uint32_t flags,
+                          int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);
 /* ---- NEXT-4: the hyperedge-weight update with f fixed.
  * P(w) = sum_t f_t^T L f_t + kappa ||w||^2, L = I - Theta(w) (reading N1: the T columns of F are
  * summed).  hg_weight_gradient: the frozen-degree gradient (D_v, D_e held at the current w)

@@ -1499,6 +1499,222 @@ static hg_status schur_impl(const hg_incidence* H, const float* w, float mu, int
   return HG_OK;
 }
 
+// ---------------------------------------------------------------- NEXT-1: nested tessellation
+// PAPER.md:155-156 (reading S4): Eq. 12 recursively inside super-blocks of m = 2^L b
+// vertices, leaves b x b, the level-l Schur complements (h = 2^(l-1) b) at rank k_l = k 2^(l-1), all
+// inverses by reading R2 (Alg. 1 on the PSD K + Woodbury) and materialised dense, level by level over
+// all nodes at once (batched GEMMs, the rSVDs in the stream parts).
+extern "C++" {
+namespace {
+struct NestedLayout {
+  Layout R;      // degrees, keys, rSVD part buffers sized for the top level (h_L, k_L)
+  CgLayout C;    // CSC of H
+  Layout Rk;     // R with its assembly keys region sized for the N/b leaves
+  size_t cg_off = 0, keys = 0, th[2] = {0, 0}, ai[2] = {0, 0}, off = 0, zinv = 0, tr = 0, wsc = 0, ut = 0, sig = 0,
+         rs = 0, wt = 0, total = 0;
+};
+NestedLayout nested_layout(int64_t N, int64_t E, int64_t nnz, int64_t b, int64_t L, int64_t k, int64_t T) {
+  NestedLayout S;
+  const int64_t hL = b << (L - 1), kL = k << (L - 1);
+  S.R = layout(N, E, nnz, hL, kL, T);
+  S.C = cg_layout(N, E, nnz, 4, 0);
+  size_t off = S.R.total;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + ALIGN - 1) / ALIGN * ALIGN;
+    return o;
+  };
+  S.cg_off = take(S.C.total);
+  S.keys = take(assemble_keys_bytes(nnz, (int)(N / b), (int)E));
+  S.Rk = S.R;
+  S.Rk.keys = S.keys;
+  for (int i = 0; i < 2; ++i) {
+    S.th[i] = take(4 * N * 2 * hL);   // node Theta of a level (N x n floats)
+    S.ai[i] = take(4 * N * 2 * hL);   // node inverse of a level
+  }
+  S.off = take(4 * N * hL / 2);       // Theta_12 of every node [nn][h][h]
+  S.zinv = take(4 * N * hL);          // Z1^-1, Z2^-1 [2nn][h][h]
+  S.tr = take(4 * N * hL / 2);        // top-right quadrants [nn][h][h]
+  S.wsc = take(4 * N * hL / 2);       // GEMM scratch [nn][h][h]
+  S.ut = take(4 * N * kL);            // U^T of the level's rSVDs [slots][k_l][h]
+  S.sig = take(4 * (N / b) * k);      // [slots][k_l]: (N / h_l) k_l = N k / b
+  S.rs = take(4 * (N / b) * k);
+  S.wt = take(4 * N * kL);
+  S.total = off;
+  return S;
+}
+}  // namespace
+}  // extern "C++"
+
+hg_status hg_nested_workspace_size(int32_t N, int32_t E, int64_t nnz, int32_t b, int32_t levels, int32_t k, int32_t T,
+                                   size_t* bytes) {
+  g_err.clear();
+  if (!bytes) return fail(HG_ERR_INVALID, "bytes is NULL");
+  if (levels < 1 || levels > 6) return fail(HG_ERR_INVALID, "levels must be in [1, 6] (levels=%d)", levels);
+  HG_TRY(check_sizes(N, b, k, 0, T));
+  if (T % 4) return fail(HG_ERR_INVALID, "hg_solve_nested needs T %% 4 == 0 (T=%d)", T);
+  if (E <= 0 || nnz < 0 || nnz >= INT32_MAX) return fail(HG_ERR_INVALID, "need E > 0 and 0 <= nnz < 2^31");
+  if (N % ((int64_t)b << levels)) return fail(HG_ERR_INVALID, "N %% (2^levels b) != 0");
+  if (((int64_t)k << (levels - 1)) > 512)
+    return fail(HG_ERR_INVALID, "the top-level Schur rank k 2^(levels-1) must be <= 512");
+  *bytes = nested_layout(N, E, nnz, b, levels, k, T).total;
+  return HG_OK;
+}
+
+static hg_status nested_impl(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t L, int32_t k,
+                             int32_t q, uint64_t seed, const float* Y, int32_t T, float* F, int32_t* st, void* ws,
+                             const NestedLayout& S, cudaStream_t s) {
+  const int64_t N = H->n_vertices;
+  const float opm = 1.0f + mu, ip = 1.0f / opm, c = mu / opm;
+  float* thc = at<float>(ws, S.th[0]);
+  float* thn = at<float>(ws, S.th[1]);
+  float* aic = at<float>(ws, S.ai[0]);
+  float* ain = at<float>(ws, S.ai[1]);
+  float* off = at<float>(ws, S.off);
+  float* KZ = at<float>(ws, S.R.blocks);
+  float* Zi = at<float>(ws, S.zinv);
+  float* TR = at<float>(ws, S.tr);
+  float* Wsc = at<float>(ws, S.wsc);
+  float* Ut = at<float>(ws, S.ut);
+  float* sg = at<float>(ws, S.sig);
+  float* rs = at<float>(ws, S.rs);
+  float* Wt = at<float>(ws, S.wt);
+  float* Vscratch = at<float>(ws, S.R.Vt);
+  auto G = [&](int M, int Nn, int K, int batch) {
+    GemmDesc g;
+    g.M = M; g.N = Nn; g.K = K; g.batch = batch;
+    return g;
+  };
+  // R2 inverse of nb PSD-K slots (h x h): I + U diag(s/((1+mu)-s)) U^T -> out [nb][h][h]
+  auto lowrank_inverse = [&](const float* Kb, int nb, int h, int kl, float* out) -> hg_status {
+    HG_TRY(run_rsvd_parts(Kb, nb, h, kl, q, seed, Ut, sg, Vscratch, st, ws, S.R, T, s));
+    HG_CU(launch_woodbury_scale(nb, kl, kl, sg, 1.f, opm, rs, st, s, &g_launches), "woodbury weights");
+    HG_CU(launch_scale_rows(nb, kl, h, rs, Ut, Wt, s, &g_launches), "scale rows");
+    GemmDesc g = G(h, h, kl, nb);   // W_t^T U_t
+    g.A = Wt; g.a_mn = true; g.lda = h; g.sa = (int64_t)kl * h;
+    g.B = Ut; g.b_mn = true; g.ldb = h; g.sb = (int64_t)kl * h;
+    g.D = out; g.ldd = h; g.sd = (int64_t)h * h;
+    HG_TRY(gemm(g, s, false, "I + U D U^T"));
+    HG_CU(launch_add_identity(nb, h, out, s, &g_launches), "identity");
+    return HG_OK;
+  };
+  // leaves: Theta_ii (raw), their inverses
+  float* dvr = at<float>(ws, S.R.dvr);
+  HG_TRY(run_degrees(H, w, b, dvr, st, ws, S.Rk, s));
+  HG_TRY(run_assemble(H, mu, b, true, 0, (int)(N / b), thc, dvr, ws, S.Rk, s));
+  void* cws = static_cast<char*>(ws) + S.cg_off;
+  CgArgs ca;
+  ca.N = (int)N; ca.E = H->n_edges; ca.nnz = H->nnz; ca.row_ptr = H->row_ptr; ca.col_idx = H->col_idx; ca.w = w;
+  ca.mu = mu; ca.Y = nullptr; ca.T = 4; ca.max_iter = 0; ca.tol = 0.f; ca.F = nullptr; ca.iters_out = nullptr;
+  ca.rel_out = nullptr; ca.status = st; ca.ws = cws;
+  {
+    ProfScope ps(ST_ASSEMBLE, s);
+    HG_CU(launch_csc_setup(ca, s, &g_launches), "CSC");
+  }
+  HG_TRY(lowrank_inverse(thc, (int)(N / b), b, k, aic));
+  for (int l = 1; l <= L; ++l) {
+    const int h = b << (l - 1), kl = k << (l - 1);
+    const int64_t n = 2 * (int64_t)h, nn = N / n, hh = (int64_t)h * h;
+    {
+      ProfScope ps(ST_ASSEMBLE, s);   // Theta_12 of every node: rows of its first half, columns of its second
+      HG_CU(launch_theta_offblock((int)nn, h, H->row_ptr, H->col_idx, at<int32_t>(cws, S.C.col_ptr),
+                                  at<int32_t>(cws, S.C.csc), at<float>(cws, S.C.eval), at<float>(cws, S.C.dvr), off, s,
+                                  &g_launches),
+            "off-diagonal Theta");
+    }
+    {   // K_Z1 = Theta11 + Theta12 (A22 Theta21) / (1+mu)
+      GemmDesc g = G(h, h, h, (int)nn);
+      g.A = aic + hh; g.a_mn = false; g.lda = h; g.sa = 2 * hh;
+      g.B = off; g.b_mn = false; g.ldb = h; g.sb = hh;
+      g.D = Wsc; g.ldd = h; g.sd = hh;
+      HG_TRY(gemm(g, s, false, "A22 Theta21"));
+      GemmDesc g2 = G(h, h, h, (int)nn);
+      g2.A = off; g2.a_mn = false; g2.lda = h; g2.sa = hh;
+      g2.B = Wsc; g2.b_mn = true; g2.ldb = h; g2.sb = hh;
+      g2.D = KZ; g2.ldd = h; g2.sd = 2 * hh;
+      g2.alpha = ip; g2.C = thc; g2.ldc = h; g2.sc = 2 * hh; g2.beta = 1.f;
+      HG_TRY(gemm(g2, s, false, "K_Z1"));
+    }
+    {   // K_Z2 = Theta22 + Theta21 (A11 Theta12) / (1+mu)
+      GemmDesc g = G(h, h, h, (int)nn);
+      g.A = aic; g.a_mn = false; g.lda = h; g.sa = 2 * hh;
+      g.B = off; g.b_mn = true; g.ldb = h; g.sb = hh;
+      g.D = Wsc; g.ldd = h; g.sd = hh;
+      HG_TRY(gemm(g, s, false, "A11 Theta12"));
+      GemmDesc g2 = G(h, h, h, (int)nn);
+      g2.A = off; g2.a_mn = true; g2.lda = h; g2.sa = hh;
+      g2.B = Wsc; g2.b_mn = true; g2.ldb = h; g2.sb = hh;
+      g2.D = KZ + hh; g2.ldd = h; g2.sd = 2 * hh;
+      g2.alpha = ip; g2.C = thc + hh; g2.ldc = h; g2.sc = 2 * hh; g2.beta = 1.f;
+      HG_TRY(gemm(g2, s, false, "K_Z2"));
+    }
+    HG_CU(launch_symmetrize((int)(2 * nn), h, KZ, s, &g_launches), "symmetrize");
+    // Z1^-1 (slot 2s), Z2^-1 (slot 2s+1): Omega rows of the N x k_l Philox matrix (reading S3, S5)
+    HG_TRY(lowrank_inverse(KZ, (int)(2 * nn), h, kl, Zi));
+    {   // top-right A11 Theta12 Z2^-1 / (1+mu): Wsc = A11 Theta12 is still there from K_Z2
+      GemmDesc g2 = G(h, h, h, (int)nn);
+      g2.A = Wsc; g2.a_mn = false; g2.lda = h; g2.sa = hh;
+      g2.B = Zi + hh; g2.b_mn = true; g2.ldb = h; g2.sb = 2 * hh;
+      g2.D = TR; g2.ldd = h; g2.sd = hh;
+      g2.alpha = ip;
+      HG_TRY(gemm(g2, s, false, "A11 Theta12 Z2^-1"));
+    }
+    HG_CU(launch_place_node((int)nn, h, Zi, 2 * hh, Zi + hh, 2 * hh, TR, hh, ain, s, &g_launches), "node inverse");
+    if (l < L)
+      HG_CU(launch_place_node((int)nn, h, thc, 2 * hh, thc + hh, 2 * hh, off, hh, thn, s, &g_launches), "node Theta");
+    std::swap(aic, ain);
+    std::swap(thc, thn);
+  }
+  // F_s = c A_s^-1 Y_s (Eq. 3), super-blocks of m = 2^L b
+  const int64_t m = (int64_t)b << L;
+  GemmDesc g = G((int)m, T, (int)m, (int)(N / m));
+  g.A = aic; g.a_mn = false; g.lda = m; g.sa = m * m;
+  g.B = Y; g.b_mn = true; g.ldb = T; g.sb = m * T;
+  g.D = F; g.ldd = T; g.sd = m * T;
+  g.alpha = c;
+  return gemm(g, s, false, "F = c A^-1 Y", ST_GEMM_APPLY);
+}
+
+hg_status hg_solve_nested(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t levels, int32_t k,
+                          int32_t q, uint64_t seed, const float* Y, int32_t T, float* F, uint32_t flags,
+                          int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  HG_TRY(check_H(H));
+  size_t need = 0;
+  HG_TRY(hg_nested_workspace_size(H->n_vertices, H->n_edges, H->nnz, b, levels, k, T, &need));
+  if (T < 1) return fail(HG_ERR_INVALID, "T must be >= 1");
+  if (q < 0) return fail(HG_ERR_INVALID, "q must be >= 0");
+  if (!(mu > 0.f) || !std::isfinite(mu)) return fail(HG_ERR_INVALID, "mu must be finite and > 0");
+  if (!w || !Y || !F) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (!d_status && !(flags & HG_SYNC)) return fail(HG_ERR_INVALID, "d_status may be NULL only with HG_SYNC");
+  const NestedLayout S = nested_layout(H->n_vertices, H->n_edges, H->nnz, b, levels, k, T);
+  HG_TRY(check_ws(ws, ws_bytes, S.total));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int32_t* st = d_status ? d_status : at<int32_t>(ws, S.R.status);
+  if (graphs_enabled(s) && !g_prof_on) {
+    std::string key = "nested|" + knob_env();
+    key_add(key, *H);
+    key_add(key, w); key_add(key, mu); key_add(key, b); key_add(key, levels); key_add(key, k); key_add(key, q);
+    key_add(key, seed); key_add(key, Y); key_add(key, T); key_add(key, F); key_add(key, st); key_add(key, ws);
+    key_add(key, ws_bytes); key_add(key, solve_parts());
+    HG_TRY(graph_run(key, s, [&](cudaStream_t cs) -> hg_status {
+      if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), cs), "memset status");
+      return nested_impl(H, w, mu, b, levels, k, q, seed, Y, T, F, st, ws, S, cs);
+    }));
+  } else {
+    if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), s), "memset status");
+    HG_TRY(nested_impl(H, w, mu, b, levels, k, q, seed, Y, T, F, st, ws, S, s));
+  }
+  if (flags & HG_SYNC) {
+    int32_t h = 0;
+    HG_CU(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s), "status readback");
+    HG_CU(cudaStreamSynchronize(s), "synchronize");
+    if (h) return fail(HG_ERR_NUMERICAL, "device status 0x%x", h);
+  }
+  return HG_OK;
+}
+
 hg_status hg_solve_schur(const hg_incidence* H, const float* w, float mu, int32_t b, int32_t k, int32_t q,
                          uint64_t seed, const float* Y, int32_t T, float* F, uint32_t flags, int32_t* d_status,
                          void* ws, size_t ws_bytes, hg_stream_t stream) {

@@ -120,6 +120,9 @@ cudaError_t launch_scale_rows(int nb, int k, int b, const float* d, const float*
                               int* launches);
 cudaError_t launch_add_identity(int nb, int b, float* A, cudaStream_t s, int* launches);
 cudaError_t launch_symmetrize(int nb, int b, float* K, cudaStream_t s, int* launches);
+// nested tessellation: out[s] (2h x 2h) = [[TL[s], TR[s]], [TR[s]^T, BR[s]]] (batch strides sTL, sBR, sTR)
+cudaError_t launch_place_node(int nn, int h, const float* TL, int64_t sTL, const float* BR, int64_t sBR, const float* TR,
+                              int64_t sTR, float* out, cudaStream_t s, int* launches);
 cudaError_t launch_axpby(int ns, int64_t len, float c, float g, const float* P, int64_t pp, const float* Q, int64_t pq,
                          float* F, int64_t pf, cudaStream_t s, int* launches);
 // cg.cu: degrees + the sorted CSC of H (for the off-diagonal assembly); a.ws is a CG workspace

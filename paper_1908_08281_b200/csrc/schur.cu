@@ -111,6 +111,22 @@ __global__ void k_axpby(int ns, int64_t len, float c, float g, const float* __re
   }
 }
 
+// Node of the nested tessellation (2h x 2h, row-major) from its quadrants: top-left TL, bottom-right
+// BR, top-right TR and bottom-left TR^T (the node inverse and the node Theta are symmetric).
+__global__ void k_place_node(int nn, int h, const float* __restrict__ TL, int64_t sTL, const float* __restrict__ BR,
+                             int64_t sBR, const float* __restrict__ TR, int64_t sTR, float* __restrict__ out) {
+  const int64_t n = 2 * (int64_t)h, per = n * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nn * per; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = i / per, rc = i % per, r = rc / n, c = rc % n;
+    float v;
+    if (r < h && c < h) v = TL[s * sTL + r * h + c];
+    else if (r >= h && c >= h) v = BR[s * sBR + (r - h) * h + (c - h)];
+    else if (r < h) v = TR[s * sTR + r * h + (c - h)];
+    else v = TR[s * sTR + c * h + (r - h)];
+    out[i] = v;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_theta_offblock(int ns, int b, const int64_t* row_ptr, const int32_t* col, const int32_t* col_ptr,
@@ -153,6 +169,15 @@ cudaError_t launch_axpby(int ns, int64_t len, float c, float g, const float* P, 
                          float* F, int64_t pf, cudaStream_t s, int* launches) {
   const int64_t n = (int64_t)ns * len;
   k_axpby<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, s>>>(ns, len, c, g, P, pp, Q, pq, F, pf);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_place_node(int nn, int h, const float* TL, int64_t sTL, const float* BR, int64_t sBR, const float* TR,
+                              int64_t sTR, float* out, cudaStream_t s, int* launches) {
+  const int64_t n = (int64_t)nn * 4 * h * h;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 32);
+  k_place_node<<<grid, 256, 0, s>>>(nn, h, TL, sTL, BR, sBR, TR, sTR, out);
   ++*launches;
   return cudaGetLastError();
 }

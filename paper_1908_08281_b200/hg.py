@@ -77,6 +77,9 @@ _weight_gradient = _sig("hg_weight_gradient", ctypes.c_int, ctypes.POINTER(_Inci
 _weight_objective = _sig("hg_weight_objective", ctypes.c_int, _P, _i32, _i32, _i32, _P, _P, _f32, _P, _P, _sz, _P)
 _weight_step = _sig("hg_weight_step", ctypes.c_int, _i32, _P, _P, _P, _f32, _P, _P)
 _weight_normalize = _sig("hg_weight_normalize", ctypes.c_int, _i32, _P, _P, _P, _P)
+_nested_ws = _sig("hg_nested_workspace_size", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, _i32, _i32, ctypes.POINTER(_sz))
+_solve_nested = _sig("hg_solve_nested", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _i32, _i32, _i32, _i32, _u64,
+                     _P, _i32, _P, _u32, _P, _P, _sz, _P)
 _block_apply_ex = _sig("hg_block_apply_inverse_ex", ctypes.c_int, _P, _P, _P, _i32, _i32, _i32, _P, _i32, _f32, _P,
                        _u32, _P, _P, _sz, _P)
 _schur_ws = _sig("hg_schur_workspace_size", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, _i32, ctypes.POINTER(_sz))
@@ -95,7 +98,7 @@ EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_
            "hg_block_apply_woodbury", "hg_workspace_size_ex", "hg_block_rsvd_ex", "hg_solve_ex",
            "hg_weight_gradient", "hg_weight_step", "hg_schur_workspace_size",
            "hg_solve_schur", "hg_solve_blocks", "hg_weight_objective", "hg_debug_jacobi_sweepmax",
-           "hg_block_apply_inverse_ex", "hg_weight_normalize")
+           "hg_block_apply_inverse_ex", "hg_weight_normalize", "hg_nested_workspace_size", "hg_solve_nested")
 
 
 class HGError(RuntimeError):
@@ -478,6 +481,37 @@ def solve_schur(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, b:
     return F, st
 
 
+def nested_workspace_size(N: int, E: int, nnz: int, b: int, levels: int, k: int, T: int) -> int:
+    n = _sz(0)
+    _check(_nested_ws(N, E, nnz, b, levels, k, T, ctypes.byref(n)))
+    return n.value
+
+
+def solve_nested(H: Incidence, w: torch.Tensor, Y: torch.Tensor, *, mu: float, b: int, levels: int, k: int, q: int,
+                 seed: int, sync: bool = True, ws: Optional[Workspace] = None, F: Optional[torch.Tensor] = None,
+                 status: Optional[torch.Tensor] = None, stream=None):
+    """NEXT-1: the nested tessellation (Eq. 12 recursively inside super-blocks of b * 2^levels): returns F, status."""
+    _dev(w, torch.float32)
+    _dev(Y, torch.float32)
+    N, T = Y.shape
+    ws = ws or Workspace(nested_workspace_size(N, H.n_edges, H.nnz, b, levels, k, T), Y.device)
+    F = F if F is not None else torch.empty((N, T), dtype=torch.float32, device=Y.device)
+    st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=Y.device)
+    inc = H.c()
+    _check(_solve_nested(ctypes.byref(inc), _ptr(w), mu, b, levels, k, q, seed, _ptr(Y), T, _ptr(F),
+                         HG_SYNC if sync else 0, _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
+    return F, st
+
+
+def tessellate(super_block: int, threshold: int):
+    """SPEC.md tessellate on a super-block of `super_block` vertices: midpoint splits until the leaf
+    dimension is <= threshold (reading S6 of the 50 -> 500 schedule); returns (b, levels)."""
+    levels = 0
+    while (super_block >> levels) > threshold and (super_block >> levels) % 2 == 0:
+        levels += 1
+    return super_block >> levels, levels
+
+
 def weight_objective(F: torch.Tensor, w: torch.Tensor, grad: torch.Tensor, *, kappa: float, stream=None) -> float:
     """P(w) = ||F||^2 + w^T grad - kappa ||w||^2 (grad from weight_gradient at this w), computed on the device."""
     for t in (F, w, grad):
@@ -521,11 +555,14 @@ def learn_weights(H: Incidence, w0: torch.Tensor, F: torch.Tensor, *, kappa: flo
 
 def adaptive_learning(H: Incidence, w0: torch.Tensor, Y: torch.Tensor, *, mu: float, kappa: float, outer: int = 2,
                       weight_steps: int = 5, step: float = 1e-4, solver: str = "cg", b: int = 0, k: int = 0,
-                      q: int = 0, seed: int = 0, cg_tol: float = 1e-6, cg_max_iter: int = 100):
+                      q: int = 0, seed: int = 0, cg_tol: float = 1e-6, cg_max_iter: int = 100,
+                      super_block: int = 1024, thresholds=(50, 500), rank_ratio: float = 0.25):
     """The paper's alternation (Table 2): solve Eq. 3 for F with the current w (the CG of
-    PAPER.md:165-178, or the block rSVD path with solver="rsvd"), then update w with F fixed
-    (learn_weights), `outer` times.  Returns (F, w, history) with history[i] = (P before, P after) of
-    outer pass i.  Composition of library calls only."""
+    PAPER.md:165-178, the block rSVD path with solver="rsvd", or the nested tessellation with
+    solver="nested": super-blocks of `super_block` vertices tessellated down to leaves <= thresholds[i] in
+    outer pass i -- the paper's 50 -> 500 schedule, reading S6 -- leaf rank rank_ratio * b),
+    then update w with F fixed (learn_weights), `outer` times.  Returns (F, w, history) with history[i] =
+    (P before, P after) of outer pass i.  Composition of library calls only."""
     w, st0 = weight_normalize(w0.contiguous())
     if int(st0.item()) != 0:
         raise HGError(HG_ERR_NUMERICAL, "w0 is not a valid start for the simplex (negative, non-finite or zero sum)")
@@ -534,6 +571,12 @@ def adaptive_learning(H: Incidence, w0: torch.Tensor, Y: torch.Tensor, *, mu: fl
     for _ in range(outer):
         if solver == "cg":
             F, _, _, _ = cg_solve(H, w, Y, mu=mu, max_iter=cg_max_iter, tol=cg_tol)
+        elif solver == "nested":
+            bl, lv = tessellate(super_block, thresholds[min(len(hist), len(thresholds) - 1)])
+            lv = min(max(lv, 1), 6)
+            bl = super_block >> lv
+            kl = max(4, int(round(bl * rank_ratio / 4)) * 4)
+            F, _ = solve_nested(H, w, Y, mu=mu, b=bl, levels=lv, k=min(kl, bl), q=q, seed=seed)
         else:
             F, _, _ = solve(H, w, Y, mu=mu, b=b, k=k, q=q, seed=seed)
         w_new, _, trace, step = learn_weights(H, w, F, kappa=kappa, mu=step, steps=weight_steps)

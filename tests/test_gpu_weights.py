@@ -152,7 +152,7 @@ def test_weight_objective_and_learn_loop_match_oracle():
     assert np.max(np.abs(wg.double().cpu().numpy() - wo)) <= 1e-5 * np.max(wo)
 
 
-@pytest.mark.parametrize("solver", ["cg", "rsvd"])
+@pytest.mark.parametrize("solver", ["cg", "rsvd", "nested"])
 def test_adaptive_learning_alternation(solver):
     """Two outer passes of solve F -> learn w: every weight phase lowers its objective
     and the weights stay on the simplex (the solves and steps themselves are checked above)."""
@@ -160,7 +160,7 @@ def test_adaptive_learning_alternation(solver):
     h, H, w0, Y = get(1)
     c = CONFIGS[1]
     F, w, hist = hg.adaptive_learning(H, w0, Y, mu=c.mu, kappa=0.5, outer=2, weight_steps=3, step=1e-4,
-                                      solver=solver, b=c.b, k=c.k, q=c.q)
+                                      solver=solver, b=c.b, k=c.k, q=c.q, super_block=c.N)
     assert len(hist) == 2 and all(after <= before for before, after in hist)
     wn = w.double().cpu().numpy()
     assert abs(wn.sum() - 1.0) <= 1e-5 and wn.min() >= 0.0
