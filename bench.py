@@ -738,6 +738,51 @@ def run_ours(args):
 
         leg.append(leg_schur)
 
+    # the nested tessellation -- Eq. 12 recursively inside 2^L b super-blocks
+    nst = None
+    L_n = args.nested_levels
+    if (L_n > 0 and c.N % (c.b << L_n) == 0 and (c.k << (L_n - 1)) <= 512 and c.T % 4 == 0):
+        nws = hg.Workspace(hg.nested_workspace_size(c.N, h.E, h.nnz, c.b, L_n, c.k, c.T), device=dev)
+        Fn = torch.empty((c.N, c.T), dtype=torch.float32, device=dev)
+        for _ in range(2):
+            hg.solve_nested(H, w, Y, mu=c.mu, b=c.b, levels=L_n, k=c.k, q=c.q, seed=seed, sync=False, ws=nws, F=Fn,
+                            status=status, stream=stream)
+        nst_launches = hg.last_launch_count()
+        torch.cuda.synchronize(dev)
+        n_n = max(3, min(args.steps, 5))
+        n0_, n1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0_.record(stream)
+        for _ in range(n_n):
+            hg.solve_nested(H, w, Y, mu=c.mu, b=c.b, levels=L_n, k=c.k, q=c.q, seed=seed, sync=False, ws=nws, F=Fn,
+                            status=status, stream=stream)
+        n1_.record(stream)
+        torch.cuda.synchronize(dev)
+        nst = {"workload": f"same H, w, Y, b, k, q; Eq. 12 applied recursively over {c.N // (c.b << L_n)} super-blocks "
+                           f"of 2^{L_n} b = {c.b << L_n}, level-l Schur rank k 2^(l-1) (readings S4, S5)",
+               "levels": L_n, "solve_ms": max_over_ranks(n0_.elapsed_time(n1_) / n_n, dev),
+               "launches_per_solve": nst_launches, "status": int(status.item())}
+        del nws
+        def leg_nested():
+            import oracle
+            m = c.b << L_n
+            Fng = Fn.double().cpu().numpy()
+            if args.nested_parity:   # the FP64 oracle of one 2^L b super-block: minutes at configs[3]
+                Fo, sel, osec = oracle.solve_nested(h.row_ptr, h.col_idx, h.w, h.Y, mu=c.mu, b=c.b, levels=L_n,
+                                                    k=c.k, q=c.q, seed=seed, superblocks=[0])
+                pe = float(np.linalg.norm(Fng[:m] - Fo) / np.linalg.norm(Fo))
+                nst["parity"] = {"superblocks": sel, "F_rel_fro": pe, "tol": 2e-5, "ok": pe <= 2e-5}
+                nst["oracle_superblock_s"] = osec
+            else:
+                nst["parity"] = "tests/test_gpu_nested.py (configs[0]/[1] vs the oracle); --nested-parity for this config"
+            Xs = oracle.theta_block(h.row_ptr, h.col_idx, h.w, m, 0, mu=c.mu)
+            ex = c.mu / (1 + c.mu) * np.linalg.solve(Xs, h.Y[:m].astype(np.float64))
+            nst["accuracy_vs_exact_superblock_solve"] = float(np.linalg.norm(Fng[:m] - ex) / np.linalg.norm(ex))
+            if cg is not None:
+                Ff = Fc.double().cpu().numpy()
+                nst["accuracy_vs_full_solve"] = float(np.linalg.norm(Fng - Ff) / np.linalg.norm(Ff))
+
+        leg.append(leg_nested)
+
     # the hyperedge-weight update with f = the CG solution
     wts = None
     if cg is not None and not args.no_weights:
@@ -804,7 +849,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "parity": parity,
         "cpu_baseline": cpu_base,
-        "next_rows": {"cg": cg, "r2_woodbury": r2, "schur": sch, "weights": wts},
+        "next_rows": {"cg": cg, "r2_woodbury": r2, "schur": sch, "nested": nst, "weights": wts},
         "peaks": {"source": peak_src, "tf32_tflops_sustained": tf32_sust, "tf32_tflops_burst": tf32_burst,
                   "tf32_source": tf32_src, "tf32_denominator": tf32_peak_kind,
                   "tf32_measured": tf32_meas, "hbm_gbs": peaks["hbm_gbs"]},
@@ -861,6 +906,10 @@ def main(argv=None):
     ap.add_argument("--no-r2", action="store_true", help="skip the reading-R2 (NEXT-3) measurement")
     ap.add_argument("--no-weights", action="store_true", help="skip the weight-update (NEXT-4) measurement")
     ap.add_argument("--no-schur", action="store_true", help="skip the Schur-complement (NEXT-1) measurement")
+    ap.add_argument("--nested-levels", type=int, default=2,
+                    help="levels of the nested-tessellation (NEXT-1) measurement; 0 skips it")
+    ap.add_argument("--nested-parity", action="store_true",
+                    help="check the nested row against the FP64 oracle on super-block 0 (about 6 min at configs[3])")
     ap.add_argument("--independent", action="store_true",
                     help="N > 1: an independent problem per rank (weak scaling) instead of the default ONE "
                          "problem sharded by block ranges over the ranks + an all-gather of F (strong scaling)")

@@ -313,6 +313,15 @@ hg_status hg_gemm(int32_t M, int32_t N, int32_t K, int32_t batch, const float* A
                   int64_t sa, const float* B, int32_t b_mn, int64_t ldb, int64_t sb, float* D, int32_t d_trans,
                   int64_t ldd, int64_t sd, float alpha, const float* rs, int64_t srs, const float* cs,
                   int64_t scs, uint32_t flags, hg_stream_t stream);
+/* hg_gemm with an explicit precision: prec -1 = the process default (HG_GEMM_PREC env, 3xTF32
+ * unless "f16"), 0 = 3xTF32, 1 = 3xF16 -- each operand x is split as hi = fp16_rn(2^e x),
+ * lo = fp16_rn(2^e x - hi) with e = a_exp for A, b_exp for B (the result is rescaled by
+ * 2^-(a_exp + b_exp)); the caller picks e so that 2^e max|x| < 65504 (|e| <= 40), else
+ * the fp16 hi part overflows to inf.  Same layouts and flags as hg_gemm. */
+hg_status hg_gemm_ex(int32_t M, int32_t N, int32_t K, int32_t batch, const float* A, int32_t a_mn, int64_t lda,
+                     int64_t sa, const float* B, int32_t b_mn, int64_t ldb, int64_t sb, float* D, int32_t d_trans,
+                     int64_t ldd, int64_t sd, float alpha, const float* rs, int64_t srs, const float* cs,
+                     int64_t scs, uint32_t flags, int32_t prec, int32_t a_exp, int32_t b_exp, hg_stream_t stream);
 
 /* Stage profiler (tracing).  hg_profile_enable(1) makes the calls on this host
  * thread bracket each stage launch with CUDA events on its stream (off by

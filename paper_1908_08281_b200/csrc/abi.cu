@@ -1826,4 +1826,22 @@ hg_status hg_gemm(int32_t M, int32_t N, int32_t K, int32_t batch, const float* A
   return gemm(g, reinterpret_cast<cudaStream_t>(stream), (flags & HG_GEMM_SIMT) != 0, "hg_gemm");
 }
 
+hg_status hg_gemm_ex(int32_t M, int32_t N, int32_t K, int32_t batch, const float* A, int32_t a_mn, int64_t lda,
+                     int64_t sa, const float* B, int32_t b_mn, int64_t ldb, int64_t sb, float* D, int32_t d_trans,
+                     int64_t ldd, int64_t sd, float alpha, const float* rs, int64_t srs, const float* cs,
+                     int64_t scs, uint32_t flags, int32_t prec, int32_t a_exp, int32_t b_exp, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!A || !B || !D) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (prec < -1 || prec > 1) return fail(HG_ERR_INVALID, "prec must be -1, 0 or 1 (prec=%d)", prec);
+  GemmDesc g;
+  g.M = M; g.N = N; g.K = K; g.batch = batch;
+  g.A = A; g.a_mn = a_mn != 0; g.lda = lda; g.sa = sa;
+  g.B = B; g.b_mn = b_mn != 0; g.ldb = ldb; g.sb = sb;
+  g.D = D; g.d_trans = d_trans != 0; g.ldd = ldd; g.sd = sd;
+  g.alpha = alpha; g.rs = rs; g.srs = srs; g.cs = cs; g.scs = scs;
+  g.prec = prec; g.a_exp = a_exp; g.b_exp = b_exp;
+  return gemm(g, reinterpret_cast<cudaStream_t>(stream), (flags & HG_GEMM_SIMT) != 0, "hg_gemm_ex");
+}
+
 }  // extern "C"

@@ -17,10 +17,18 @@
 //   * operands may be K-major or MN-major in global memory (both legal for
 //     kind::tf32); the mbarrier ring is full(TMA) -> conv(split) -> empty(commit).
 //   * accumulation: TMEM chunks of K = 64, ping-pong, summed in fp32 registers
-//     (see gemm_tf32x3_kernel); epilogue: scaled, coalesced stores (a warp owns 32
+//     (see gemm_tc_kernel); epilogue: scaled, coalesced stores (a warp owns 32
 //     consecutive rows m, so a transposed store D[n][m] is one 128-byte line).
+//   * 3xF16 (GemmDesc::prec = 1): the same pipeline on kind::f16 (twice the tf32 MMA rate):
+//     hi = fp16_rn(2^e x), lo = fp16_rn(2^e x - hi) -- 22 significant bits like the tf32 pair,
+//     the power-of-two prescale 2^e (from the caller's bound on |x|) keeps the pair inside the
+//     fp16 exponent range.  The split is done in place (fp32 landing tile -> K-major SWIZZLE_64B
+//     hi | lo halves, both majors), or not at all for operands the producer stored pre-split
+//     (GemmDesc::A16 / B16: hi and lo fp16 planes, TMA-loaded straight into the same layout).
+//     TMEM chunks of K = 128 (24 MMAs per chunk, the same truncation bound as the tf32 path).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 
 #include <cstdlib>
 #include <mutex>
@@ -50,22 +58,25 @@ struct EpiArgs {
   int64_t ldc, sc;
   float beta;
   int b_upper;    // B(kk, n) = 0 for kk > n (GemmDesc::b_upper): per k-block, MMAs over n >= kk only
+  // 3xF16 only
+  int a_pre, b_pre;   // operand TMA-loaded pre-split (hi | lo fp16 planes): no in-kernel split
+  float a_sc, b_sc;   // 2^a_exp, 2^b_exp: prescale of the in-kernel split
 };
 
 constexpr int NEPI = 256;            // converter / epilogue threads (8 warps)
 constexpr int NTHREADS = NEPI + 64;  // + TMA warp + MMA warp
-constexpr int CHUNK_KB = 2;          // k-blocks accumulated per TMEM chunk (K = 64)
 
-template <int BN>
+template <int BN, bool F16>
 struct Cfg {
-  static constexpr int A_BYTES = BM * BK * 4;   // 16 KB
+  static constexpr int A_BYTES = BM * BK * 4;   // 16 KB (3xF16: the fp32 tile, then hi | lo fp16 halves)
   static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGE_BYTES = F16 ? A_BYTES + B_BYTES : 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = (STAGE_BYTES * 4 <= 200 * 1024) ? 4 : (STAGE_BYTES * 3 <= 200 * 1024 ? 3 : 2);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr uint32_t TX = (uint32_t)(BM + BN) * BK * 4;
   static constexpr int HALF = BN / 2;           // columns per epilogue warp
+  static constexpr int CHUNK = F16 ? 4 : 2;     // k-blocks per TMEM chunk: 24 MMAs either way
   static_assert(8 * 32 * (HALF + 4) * 4 <= STAGES * STAGE_BYTES, "epilogue staging must fit the pipeline smem");
   static_assert(8 * HALF * 36 * 4 <= STAGES * STAGE_BYTES, "transposed staging must fit the pipeline smem");
 };
@@ -81,6 +92,25 @@ __device__ __forceinline__ uint32_t make_idesc(int bn, int a_mn, int b_mn) {
   d |= (uint32_t)(bn >> 3) << 17;    // n_dim
   d |= (uint32_t)(BM >> 4) << 24;    // m_dim
   return d;
+}
+
+// kind::f16 instruction descriptor: D f32, A/B fp16 (format 0), both K-major, M = 128, N = bn.
+__device__ __forceinline__ uint32_t make_idesc_f16(int bn) {
+  return (1u << 4) | ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+// 3xF16 split of 4 consecutive k of one row into the K-major SWIZZLE_64B hi | lo planes:
+// row r is 64 bytes (32 fp16), 16-byte unit u = kq / 2 sits at u ^ ((r >> 1) & 3).
+__device__ __forceinline__ void f16_split_store(uint8_t* hi, uint8_t* lo, int r, int kq, float4 x) {
+  const __half2 h01 = __floats2half2_rn(x.x, x.y), h23 = __floats2half2_rn(x.z, x.w);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn(x.x - f01.x, x.y - f01.y), l23 = __floats2half2_rn(x.z - f23.x, x.w - f23.y);
+  const int off = r * 64 + ((((kq >> 1) ^ (r >> 1)) & 3) << 4) + ((kq & 1) << 3);
+  uint2 hv, lv;
+  hv.x = *reinterpret_cast<const uint32_t*>(&h01); hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+  lv.x = *reinterpret_cast<const uint32_t*>(&l01); lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+  *reinterpret_cast<uint2*>(hi + off) = hv;
+  *reinterpret_cast<uint2*>(lo + off) = lv;
 }
 
 __device__ __forceinline__ float trunc_lo(float x) {   // x - trunc_tf32(x), exact in fp32
@@ -99,11 +129,11 @@ __device__ __forceinline__ float4 split_hi(float4& x) {
 // at K = 1024).  The MMAs of each K-chunk of 64 go to a fresh TMEM buffer (two
 // buffers, ping-pong); the epilogue warps drain finished chunks and sum them in
 // fp32 round-to-nearest registers, bounding the truncation to 24 MMAs.
-template <int BN>
+template <int BN, bool F16>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                       EpiArgs ea) {
-  using C = Cfg<BN>;
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   EpiArgs ea) {
+  using C = Cfg<BN, F16>;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[C::STAGES], conv_bar[C::STAGES], empty_bar[C::STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
@@ -113,7 +143,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, g = blockIdx.z;
   if (ea.lower && n0 >= m0 + BM) return;   // tile above the diagonal (uniform: before any setup)
   const int num_kb = (ea.K + BK - 1) / BK;
-  const int nchunks = (num_kb + CHUNK_KB - 1) / CHUNK_KB;
+  const int nchunks = (num_kb + C::CHUNK - 1) / C::CHUNK;
 
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   auto sA_hi = [&](int s) { return base + s * C::STAGE_BYTES; };
@@ -150,13 +180,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (kb >= C::STAGES) mbar_wait(&empty_bar[s], ph ^ 1);
         mbar_arrive_expect_tx(&full_bar[s], C::TX);
         const int k0 = kb * BK;
-        if (!ea.a_mn) {
+        if (F16 && ea.a_pre) {
+          tma_load_4d(sA_hi(s), &tmA, &full_bar[s], k0, m0, 0, g);   // hi rows then lo rows
+        } else if (!ea.a_mn) {
           tma_load_3d(sA_hi(s), &tmA, &full_bar[s], k0, m0, g);
         } else {
 #pragma unroll
           for (int c = 0; c < BM / 32; ++c) tma_load_3d(sA_hi(s) + c * 4096, &tmA, &full_bar[s], m0 + 32 * c, k0, g);
         }
-        if (!ea.b_mn) {
+        if (F16 && ea.b_pre) {
+          tma_load_4d(sB_hi(s), &tmB, &full_bar[s], k0, n0, 0, g);
+        } else if (!ea.b_mn) {
           tma_load_3d(sB_hi(s), &tmB, &full_bar[s], k0, n0, g);
         } else {
 #pragma unroll
@@ -166,7 +200,50 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else if (warp == 9) {
     // ---------------- MMA issuer (single thread)
-    if (lane == 0) {
+    if (F16 && lane == 0) {
+      // 3xF16: both operands K-major SWIZZLE_64B fp16 (64-byte rows, 8-row groups 512 B apart),
+      // hi plane then lo plane; K-step 16 = +32 B in the row
+      const uint32_t idesc = make_idesc_f16(BN);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % C::STAGES;
+        const uint32_t ph = (kb / C::STAGES) & 1;
+        const int c = kb / C::CHUNK, buf = c & 1;
+        const bool first = (kb % C::CHUNK) == 0;
+        if (first && c >= 2) {
+          mbar_wait(&tempty_bar[buf], ((c >> 1) - 1) & 1);
+          tc_fence_after();
+        }
+        mbar_wait(&conv_bar[s], ph);
+        tc_fence_after();
+        const int nlo = ea.b_upper ? (max(0, kb * BK - n0) & ~15) : 0;
+        const bool last_in_chunk = (kb % C::CHUNK) == C::CHUNK - 1 || kb == num_kb - 1;
+        if (nlo >= BN) {
+          mma_commit(&empty_bar[s]);
+          if (last_in_chunk) mma_commit(&tfull_bar[buf]);
+          continue;
+        }
+        const uint32_t idk = nlo ? make_idesc_f16(BN - nlo) : idesc;
+        const uint32_t d = tmem + (uint32_t)(buf * BN + nlo);
+        // split in the kernel: 1 KB groups of 8 hi rows + 8 lo rows (SBO 1024, lo at +512);
+        // pre-split (TMA): the hi plane then the lo plane (SBO 512, lo at +R * 64)
+        const uint32_t a0 = smem_u32(sA_hi(s)), b0 = smem_u32(sB_hi(s));
+        const uint32_t ahi = a0, alo = ea.a_pre ? a0 + BM * 64 : a0 + 512, asbo = ea.a_pre ? 512 : 1024;
+        const uint32_t bhi = b0 + (ea.b_pre ? nlo * 64 : nlo * 128);
+        const uint32_t blo = ea.b_pre ? b0 + BN * 64 + nlo * 64 : bhi + 512, bsbo = ea.b_pre ? 512 : 1024;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint64_t dah = umma_desc(ahi + kk * 32, 16, asbo, 4);
+          const uint64_t dal = umma_desc(alo + kk * 32, 16, asbo, 4);
+          const uint64_t dbh = umma_desc(bhi + kk * 32, 16, bsbo, 4);
+          const uint64_t dbl = umma_desc(blo + kk * 32, 16, bsbo, 4);
+          mma_f16(d, dal, dbh, idk, (first && kk == 0) ? 0u : 1u);
+          mma_f16(d, dah, dbl, idk, 1);
+          mma_f16(d, dah, dbh, idk, 1);
+        }
+        mma_commit(&empty_bar[s]);
+        if (last_in_chunk) mma_commit(&tfull_bar[buf]);
+      }
+    } else if (!F16 && lane == 0) {
       const uint32_t idesc = make_idesc(BN, ea.a_mn, ea.b_mn);
       // K-major (SWIZZLE_128B): 8-row groups 1024 B apart (SBO), K-step = +32 B in the row.
       // MN-major (SWIZZLE_128B_BASE32B): 32-element chunks BK*128 B apart (LBO),
@@ -178,8 +255,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         const int s = kb % C::STAGES;
         const uint32_t ph = (kb / C::STAGES) & 1;
-        const int c = kb / CHUNK_KB, buf = c & 1;
-        const bool first = (kb % CHUNK_KB) == 0;
+        const int c = kb / C::CHUNK, buf = c & 1;
+        const bool first = (kb % C::CHUNK) == 0;
         if (first && c >= 2) {
           mbar_wait(&tempty_bar[buf], ((c >> 1) - 1) & 1);
           tc_fence_after();
@@ -192,7 +269,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int nlo = ea.b_upper ? (max(0, kb * BK - n0) & ~15) : 0;
         if (nlo >= BN) {
           mma_commit(&empty_bar[s]);
-          if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == num_kb - 1) mma_commit(&tfull_bar[buf]);
+          if ((kb % C::CHUNK) == C::CHUNK - 1 || kb == num_kb - 1) mma_commit(&tfull_bar[buf]);
           continue;
         }
         const uint32_t idk = nlo ? make_idesc(BN - nlo, ea.a_mn, ea.b_mn) : idesc;
@@ -210,7 +287,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mma_tf32(d, dah, dbh, idk, 1);
         }
         mma_commit(&empty_bar[s]);
-        if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == num_kb - 1) mma_commit(&tfull_bar[buf]);
+        if ((kb % C::CHUNK) == C::CHUNK - 1 || kb == num_kb - 1) mma_commit(&tfull_bar[buf]);
       }
     }
   } else {
@@ -226,7 +303,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc_fence_after();
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * BN + h * C::HALF);
       // b_upper: tile columns below the chunk's first k-block's nlo were never written by it
-      const int clo = ea.b_upper ? min(BN, max(0, dch * CHUNK_KB * BK - n0) & ~15) - h * C::HALF : 0;
+      const int clo = ea.b_upper ? min(BN, max(0, dch * C::CHUNK * BK - n0) & ~15) - h * C::HALF : 0;
 #pragma unroll
       for (int j0 = 0; j0 < C::HALF; j0 += 16) {
         float v[16];
@@ -243,6 +320,69 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int s = kb % C::STAGES;
       const uint32_t ph = (kb / C::STAGES) & 1;
       mbar_wait(&full_bar[s], ph);
+      if constexpr (F16) {
+        // In-place 3xF16 split into 8-row groups of 1 KB -- the group's 8 hi rows (64 B each,
+        // SWIZZLE_64B), then its 8 lo rows: exactly the bytes its 8 fp32 rows occupied.
+        // K-major tiles: a warp converts whole groups (2 float4 per lane, __syncwarp, store),
+        // no CTA barrier.  MN-major tiles (32-row chunks [32 k][32 rows], SWIZZLE_128B) are
+        // read transposed (4 rows k of one column per unit): all threads load, barrier, store.
+        auto conv_k = [&](uint8_t* reg, int R, float sc) {
+          for (int gi = warp; gi < R / 8; gi += NEPI / 32) {
+            uint8_t* gb = reg + gi * 1024;
+            float4 x[2];
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int u = lane + 32 * h2, rr = u >> 3, kq = u & 7;
+              const float4 v = *reinterpret_cast<const float4*>(gb + rr * 128 + ((kq ^ rr) << 4));
+              x[h2] = make_float4(v.x * sc, v.y * sc, v.z * sc, v.w * sc);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int u = lane + 32 * h2;
+              f16_split_store(gb, gb + 512, u >> 3, u & 7, x[h2]);
+            }
+          }
+        };
+        auto conv_mn = [&](uint8_t* reg, int R, float sc) {
+          constexpr int UMAX = BN > BM ? BN * 8 / NEPI : BM * 8 / NEPI;
+          float4 x[UMAX];
+          const int nu = R * 8 / NEPI;
+#pragma unroll
+          for (int i = 0; i < UMAX; ++i) {
+            if (i >= nu) break;
+            const int u = t + i * NEPI, kq = u / R, r = u % R;
+            const uint8_t* col = reg + (r >> 5) * 4096 + (r & 3) * 4;
+            const int ch = (r & 31) >> 2;
+            float e[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int kk = 4 * kq + j;
+              e[j] = *reinterpret_cast<const float*>(col + kk * 128 + ((ch ^ (kk & 7)) << 4)) * sc;
+            }
+            x[i] = make_float4(e[0], e[1], e[2], e[3]);
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(NEPI) : "memory");
+#pragma unroll
+          for (int i = 0; i < UMAX; ++i) {
+            if (i >= nu) break;
+            const int u = t + i * NEPI, kq = u / R, r = u % R;
+            uint8_t* gb = reg + (r >> 3) * 1024;
+            f16_split_store(gb, gb + 512, r & 7, kq, x[i]);
+          }
+        };
+        if (!ea.a_pre) {
+          if (ea.a_mn) conv_mn(sA_hi(s), BM, ea.a_sc); else conv_k(sA_hi(s), BM, ea.a_sc);
+        }
+        if (!ea.b_pre) {
+          if (ea.b_mn) conv_mn(sB_hi(s), BN, ea.b_sc); else conv_k(sB_hi(s), BN, ea.b_sc);
+        }
+        if (!(ea.a_pre && ea.b_pre)) fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv_bar[s]);
+        while (drained < nchunks - 1 && kb >= (drained + 1) * C::CHUNK + 1) drain(drained++);
+        continue;
+      }
       float4* ah = reinterpret_cast<float4*>(sA_hi(s));
       float4* al = reinterpret_cast<float4*>(sA_lo(s));
       float4* bh = reinterpret_cast<float4*>(sB_hi(s));
@@ -280,7 +420,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv_bar[s]);
       // drain chunk d once the MMAs of chunk d+1 are under way
-      while (drained < nchunks - 1 && kb >= (drained + 1) * CHUNK_KB + 1) drain(drained++);
+      while (drained < nchunks - 1 && kb >= (drained + 1) * C::CHUNK + 1) drain(drained++);
     }
     while (drained < nchunks) drain(drained++);
     // epilogue: scale and store.  Transposed output D[n][m]: a warp's 32 rows m are
@@ -441,8 +581,10 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 3D map: (inner, outer, batch), row pitch ld elements, batch pitch bs elements; box (32, box_outer, 1).
+// MN-major fp32 tiles use 32-byte swizzle atoms for the tf32 MMA (its only legal MN-major form),
+// plain SWIZZLE_128B when the 3xF16 split reads them (f16_split = true).
 bool make_map(CUtensorMap* m, const float* ptr, int64_t inner, int64_t outer, int64_t batch, int64_t ld,
-              int64_t bs, int box_outer, bool mn_major) {
+              int64_t bs, int box_outer, bool mn_major, bool f16_split = false) {
   auto enc = get_encode();
   if (!enc) return false;
   if (batch <= 1) bs = ld * outer;
@@ -452,44 +594,88 @@ bool make_map(CUtensorMap* m, const float* ptr, int64_t inner, int64_t outer, in
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   (mn_major && !f16_split) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-template <int BN>
+// Pre-split fp16 operand: 4D map (K, rows, {hi, lo}, batch) over hi[g*bs + row*ld + kk] and
+// lo = hi + lo_off; box (32, box_rows, 2, 1) lands as the hi plane then the lo plane, SWIZZLE_64B.
+bool make_map_pair(CUtensorMap* m, const uint16_t* hi, int64_t K, int64_t rows, int64_t batch, int64_t ld,
+                   int64_t bs, int64_t lo_off, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  if (batch <= 1) bs = ld * rows;
+  cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)rows, 2, (cuuint64_t)(batch < 1 ? 1 : batch)};
+  cuuint64_t strides[3] = {(cuuint64_t)ld * 2, (cuuint64_t)lo_off * 2, (cuuint64_t)bs * 2};
+  cuuint32_t box[4] = {32, (cuuint32_t)box_rows, 2, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<uint16_t*>(hi), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool F16>
 cudaError_t launch_tc(const GemmDesc& g, const EpiArgs& ea, cudaStream_t stream) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, F16>;
   static bool attr_set = false;  // per-instantiation; set once per process
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tf32x3_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   CUtensorMap ta, tb;
-  bool ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.batch, g.lda, g.sa, 32, true)
-                   : make_map(&ta, g.A, g.K, g.M, g.batch, g.lda, g.sa, BM, false);
-  ok = ok && (g.b_mn ? make_map(&tb, g.B, g.N, g.K, g.batch, g.ldb, g.sb, 32, true)
-                     : make_map(&tb, g.B, g.K, g.N, g.batch, g.ldb, g.sb, BN, false));
+  bool ok;
+  if (F16 && g.A16)
+    ok = make_map_pair(&ta, g.A16, g.K, g.M, g.batch, g.lda, g.sa, g.a_lo, BM);
+  else
+    ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.batch, g.lda, g.sa, 32, true, F16)
+                : make_map(&ta, g.A, g.K, g.M, g.batch, g.lda, g.sa, BM, false);
+  if (F16 && g.B16)
+    ok = ok && make_map_pair(&tb, g.B16, g.K, g.N, g.batch, g.ldb, g.sb, g.b_lo, BN);
+  else
+    ok = ok && (g.b_mn ? make_map(&tb, g.B, g.N, g.K, g.batch, g.ldb, g.sb, 32, true, F16)
+                       : make_map(&tb, g.B, g.K, g.N, g.batch, g.ldb, g.sb, BN, false));
   if (!ok) return cudaErrorInvalidValue;
   dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, g.batch);
-  gemm_tf32x3_kernel<BN><<<grid, NTHREADS, C::SMEM, stream>>>(ta, tb, ea);
+  gemm_tc_kernel<BN, F16><<<grid, NTHREADS, C::SMEM, stream>>>(ta, tb, ea);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+static int prec_env() {   // HG_GEMM_PREC=f16 | tf32: the precision of GEMMs that leave GemmDesc::prec = -1
+  static const int p = [] {
+    const char* v = getenv("HG_GEMM_PREC");
+    return (v && v[0] == 'f') ? 1 : 0;
+  }();
+  return p;
+}
+
+int gemm_prec(const GemmDesc& g) { return g.prec >= 0 ? g.prec : prec_env(); }
+
 const char* gemm_check(const GemmDesc& g) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return "gemm: non-positive size";
   if (g.batch > 65535) return "gemm: batch > 65535";
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (!al16(g.A) || !al16(g.B)) return "gemm: A/B must be 16-byte aligned";
-  if ((g.lda & 3) || (g.ldb & 3)) return "gemm: lda/ldb must be multiples of 4";
-  if (g.batch > 1 && ((g.sa & 3) || (g.sb & 3))) return "gemm: batch strides must be multiples of 4";
-  if (g.a_mn ? g.lda < g.M : g.lda < g.K) return "gemm: lda too small";
-  if (g.b_mn ? g.ldb < g.N : g.ldb < g.K) return "gemm: ldb too small";
+  const bool pa = g.A16 != nullptr, pb = g.B16 != nullptr;
+  if ((pa || pb) && gemm_prec(g) != 1) return "gemm: pre-split fp16 operands need prec = 1";
+  if (pa ? (!al16(g.A16) || (g.lda & 7) || (g.a_lo & 7) || (g.batch > 1 && (g.sa & 7)) || g.lda < g.K)
+         : (!g.A || !al16(g.A)))
+    return pa ? "gemm: pre-split A needs 16-byte alignment, lda/a_lo/sa multiples of 8, lda >= K"
+              : "gemm: A must be non-null and 16-byte aligned";
+  if (pb ? (!al16(g.B16) || (g.ldb & 7) || (g.b_lo & 7) || (g.batch > 1 && (g.sb & 7)) || g.ldb < g.K)
+         : (!g.B || !al16(g.B)))
+    return pb ? "gemm: pre-split B needs 16-byte alignment, ldb/b_lo/sb multiples of 8, ldb >= K"
+              : "gemm: B must be non-null and 16-byte aligned";
+  if ((!pa && (g.lda & 3)) || (!pb && (g.ldb & 3))) return "gemm: lda/ldb must be multiples of 4";
+  if (g.batch > 1 && ((!pa && (g.sa & 3)) || (!pb && (g.sb & 3)))) return "gemm: batch strides must be multiples of 4";
+  if (!pa && (g.a_mn ? g.lda < g.M : g.lda < g.K)) return "gemm: lda too small";
+  if (!pb && (g.b_mn ? g.ldb < g.N : g.ldb < g.K)) return "gemm: ldb too small";
   if (g.C && (g.d_trans || g.ldc < g.N)) return "gemm: residual C needs row-major D and ldc >= N";
+  if (g.a_exp < -40 || g.a_exp > 40 || g.b_exp < -40 || g.b_exp > 40) return "gemm: |a_exp|, |b_exp| must be <= 40";
   return nullptr;
 }
 
@@ -502,17 +688,27 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
     const char* v = getenv("HG_TF32_SPLIT");
     return (v && v[0] == 'r') ? 0 : 1;
   }();
-  EpiArgs ea{g.M, g.N, g.K, g.D, g.ldd, g.sd, g.d_trans ? 1 : 0, g.alpha, g.rs, g.srs, g.cs, g.scs,
+  const bool f16 = !simt && gemm_prec(g) == 1;
+  const float alpha = f16 ? ldexpf(g.alpha, -(g.a_exp + g.b_exp)) : g.alpha;
+  EpiArgs ea{g.M, g.N, g.K, g.D, g.ldd, g.sd, g.d_trans ? 1 : 0, alpha, g.rs, g.srs, g.cs, g.scs,
              g.a_mn ? 1 : 0, g.b_mn ? 1 : 0, trunc_hi, g.lower ? 1 : 0, g.C, g.ldc, g.sc, g.beta,
-             (g.b_upper && !g.b_mn) ? 1 : 0};
+             (g.b_upper && (f16 || !g.b_mn)) ? 1 : 0,
+             g.A16 ? 1 : 0, g.B16 ? 1 : 0, ldexpf(1.0f, g.a_exp), ldexpf(1.0f, g.b_exp)};
   if (simt) {
+    if (g.A16 || g.B16) return cudaErrorInvalidValue;
     dim3 grid((g.M + 63) / 64, (g.N + 63) / 64, g.batch);
     gemm_simt_kernel<<<grid, 256, 0, stream>>>(g.A, ea.a_mn, g.lda, g.sa, g.B, ea.b_mn, g.ldb, g.sb, ea);
     return cudaGetLastError();
   }
   const int n = g.N < g.bn_max ? g.N : g.bn_max;
-  if (n <= 32) return launch_tc<32>(g, ea, stream);
-  if (n <= 64) return launch_tc<64>(g, ea, stream);
-  if (n <= 128) return launch_tc<128>(g, ea, stream);
-  return launch_tc<256>(g, ea, stream);
+  if (f16) {
+    if (n <= 32) return launch_tc<32, true>(g, ea, stream);
+    if (n <= 64) return launch_tc<64, true>(g, ea, stream);
+    if (n <= 128) return launch_tc<128, true>(g, ea, stream);
+    return launch_tc<256, true>(g, ea, stream);
+  }
+  if (n <= 32) return launch_tc<32, false>(g, ea, stream);
+  if (n <= 64) return launch_tc<64, false>(g, ea, stream);
+  if (n <= 128) return launch_tc<128, false>(g, ea, stream);
+  return launch_tc<256, false>(g, ea, stream);
 }

@@ -33,6 +33,19 @@ struct GemmDesc {
   // B(kk, n) = 0 for kk > n (e.g. B = Linv^T): the tensor-core kernel skips the zero
   // part of each k-block's MMAs (K-major B only; ignored otherwise -- still correct)
   bool b_upper = false;
+  // Precision: -1 = the process default (HG_GEMM_PREC, 3xTF32 unless "f16"), 0 = 3xTF32,
+  // 1 = 3xF16 (hi = fp16_rn(2^exp x), lo = fp16_rn(2^exp x - hi); the caller picks a_exp / b_exp
+  // from a bound on |A| / |B| so that 2^exp max|x| < 65504 -- the result is rescaled by
+  // 2^-(a_exp + b_exp) in the epilogue).
+  int prec = -1;
+  int a_exp = 0, b_exp = 0;
+  // Pre-split operands (prec 1 only, K-major): hi planes A16[g*sa + m*lda + kk], lo planes at
+  // A16 + a_lo (fp16 element offsets, multiples of 8), already scaled by 2^a_exp.  When set,
+  // A / a_mn are ignored (likewise B16 / b_lo for B).
+  const uint16_t* A16 = nullptr;
+  int64_t a_lo = 0;
+  const uint16_t* B16 = nullptr;
+  int64_t b_lo = 0;
 };
 
 // Enqueue the GEMM; returns cudaSuccess or the launch error.  `simt` selects the
@@ -41,3 +54,5 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt);
 // Validation used by the ABI (alignment/stride requirements of TMA); returns a
 // static message or nullptr.
 const char* gemm_check(const GemmDesc& g);
+// The precision launch_gemm will use for g (0 = 3xTF32, 1 = 3xF16).
+int gemm_prec(const GemmDesc& g);

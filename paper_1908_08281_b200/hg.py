@@ -69,6 +69,8 @@ _solve_host = _sig("hg_solve_host", ctypes.c_int, _i32, _i32, _i64, _P, _P, _P, 
                    _i32, _P, _P, _u32, _P, _sz, _P)
 _gemm = _sig("hg_gemm", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i32, _i64, _i64, _P, _i32, _i64, _i64, _P, _i32,
              _i64, _i64, _f32, _P, _i64, _P, _i64, _u32, _P)
+_gemm_ex = _sig("hg_gemm_ex", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i32, _i64, _i64, _P, _i32, _i64, _i64, _P,
+                _i32, _i64, _i64, _f32, _P, _i64, _P, _i64, _u32, _i32, _i32, _i32, _P)
 _cg_workspace_size = _sig("hg_cg_workspace_size", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, ctypes.POINTER(_sz))
 _cg_solve = _sig("hg_cg_solve", ctypes.c_int, ctypes.POINTER(_Incidence), _P, _f32, _P, _i32, _i32, _f32, _P, _P, _P,
                  _u32, _P, _P, _sz, _P)
@@ -93,7 +95,7 @@ _last_launches = _sig("hg_last_launch_count", ctypes.c_int32)
 _debug_counters = _sig("hg_debug_counters", ctypes.c_int, _P, _i32, _i32)
 
 EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_rsvd", "hg_block_apply_inverse",
-           "hg_solve", "hg_solve_host", "hg_gemm", "hg_last_error", "hg_last_launch_count", "hg_profile_enable",
+           "hg_solve", "hg_solve_host", "hg_gemm", "hg_gemm_ex", "hg_last_error", "hg_last_launch_count", "hg_profile_enable",
            "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve",
            "hg_block_apply_woodbury", "hg_workspace_size_ex", "hg_block_rsvd_ex", "hg_solve_ex",
            "hg_weight_gradient", "hg_weight_step", "hg_schur_workspace_size",
@@ -392,10 +394,17 @@ def solve_host(row_ptr, col_idx, w, Y, *, mu: float, b: int, k: int, q: int, see
 def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, batch: int = 1, a_mn: bool = False, lda: int,
          sa: int = 0, b_mn: bool = False, ldb: int, sb: int = 0, D: torch.Tensor, d_trans: bool = False, ldd: int,
          sd: int = 0, alpha: float = 1.0, rs: Optional[torch.Tensor] = None, srs: int = 0,
-         cs: Optional[torch.Tensor] = None, scs: int = 0, simt: bool = False, stream=None):
-    """Verification export of the batched 3xTF32 GEMM (see hg.h)."""
-    _check(_gemm(M, N, K, batch, _ptr(A), int(a_mn), lda, sa, _ptr(B), int(b_mn), ldb, sb, _ptr(D), int(d_trans), ldd,
-                 sd, alpha, _ptr(rs), srs, _ptr(cs), scs, HG_GEMM_SIMT if simt else 0, _stream(stream)))
+         cs: Optional[torch.Tensor] = None, scs: int = 0, simt: bool = False, prec: Optional[int] = None,
+         a_exp: int = 0, b_exp: int = 0, stream=None):
+    """Verification export of the batched GEMM (see hg.h): 3xTF32, or 3xF16 with prec=1 (operands
+    prescaled by 2^a_exp / 2^b_exp before the fp16 split)."""
+    if prec is None:
+        _check(_gemm(M, N, K, batch, _ptr(A), int(a_mn), lda, sa, _ptr(B), int(b_mn), ldb, sb, _ptr(D), int(d_trans),
+                     ldd, sd, alpha, _ptr(rs), srs, _ptr(cs), scs, HG_GEMM_SIMT if simt else 0, _stream(stream)))
+    else:
+        _check(_gemm_ex(M, N, K, batch, _ptr(A), int(a_mn), lda, sa, _ptr(B), int(b_mn), ldb, sb, _ptr(D),
+                        int(d_trans), ldd, sd, alpha, _ptr(rs), srs, _ptr(cs), scs, HG_GEMM_SIMT if simt else 0,
+                        prec, a_exp, b_exp, _stream(stream)))
     return D
 
 

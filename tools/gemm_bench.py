@@ -1,6 +1,7 @@
-"""Micro-benchmark of the batched 3xTF32 tcgen05 GEMM on the path's shapes (configs[3]).
+"""Micro-benchmark of the batched tcgen05 GEMM (3xTF32, or 3xF16 with --prec 1) on the path's shapes
+(configs[3]).
 
-    python tools/gemm_bench.py [--reps 20]
+    python tools/gemm_bench.py [--reps 20] [--prec 0|1]
 Prints one line per shape: ms per launch, useful TFLOP/s, tf32-pipe TFLOP/s, rel. error on batch 0.
 """
 import argparse
@@ -26,6 +27,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--shapes", nargs="*", default=list(SHAPES))
+    ap.add_argument("--prec", type=int, default=0)
     a = ap.parse_args()
     g = torch.Generator(device="cuda").manual_seed(0)
     for name in a.shapes:
@@ -36,7 +38,8 @@ def main():
 
         def run():
             hg.gemm(A, Bm, M=M, N=N, K=K, batch=B, a_mn=a_mn, lda=A.shape[2], sa=A[0].numel(), b_mn=b_mn,
-                    ldb=Bm.shape[2], sb=Bm[0].numel(), D=D, d_trans=d_trans, ldd=D.shape[2], sd=D[0].numel())
+                    ldb=Bm.shape[2], sb=Bm[0].numel(), D=D, d_trans=d_trans, ldd=D.shape[2], sd=D[0].numel(),
+                    prec=a.prec, a_exp=11, b_exp=11)
         for _ in range(3):
             run()
         torch.cuda.synchronize()
@@ -55,7 +58,8 @@ def main():
         useful = 2.0 * M * N * K * B / (ms / 1e3) / 1e12
         print(json.dumps({"shape": name, "MNK_batch": [M, N, K, B], "ms": ms, "useful_tflops": useful,
                           "pipe_tflops": 3 * useful, "rel_err": err,
-                          "split": os.environ.get("HG_TF32_SPLIT", "rna")}), flush=True)
+                          "prec": ["3xtf32", "3xf16"][a.prec],
+                          "split": os.environ.get("HG_TF32_SPLIT", "trunc")}), flush=True)
 
 
 if __name__ == "__main__":
