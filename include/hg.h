@@ -82,6 +82,11 @@ enum hg_status_flags {
                                 /* products of Alg. 1 use the literal transpose   */
 #define HG_UV_BK (1u << 5)      /* hg_block_rsvd / hg_block_apply_inverse_ex: U, V [nb][b][k]    */
                                 /* (column j = u_j) instead of the transposed Ut, Vt [nb][k][b]  */
+#define HG_X_UNIT (1u << 6)     /* hg_block_rsvd(_ex): the caller guarantees |X_ij| <= 1 and     */
+                                /* ||X_ii||_2 <= 1 (true of hg_build_theta's X_ii and Theta_ii):  */
+                                /* enables the 3xF16 power products and Grams the solve entries  */
+                                /* use (off: 3xTF32).  Needs b % 8 == 0 */
+                                /* and no HG_GENERAL; ignored otherwise.                          */
 #define HG_GEMM_SIMT (1u << 8)  /* verification only: CUDA-core fp32 GEMMs, not tcgen05    */
 
 /* Hypergraph incidence H (H(v,e) = 1 iff v in e) in CSR over
@@ -322,6 +327,18 @@ hg_status hg_gemm_ex(int32_t M, int32_t N, int32_t K, int32_t batch, const float
                      int64_t sa, const float* B, int32_t b_mn, int64_t ldb, int64_t sb, float* D, int32_t d_trans,
                      int64_t ldd, int64_t sd, float alpha, const float* rs, int64_t srs, const float* cs,
                      int64_t scs, uint32_t flags, int32_t prec, int32_t a_exp, int32_t b_exp, hg_stream_t stream);
+
+/* Verification exports of the 3xF16 pre-split operand path.  hg_f16_split: hi[r*ldo + c] =
+ * fp16_rn(2^exp x[r*ld + c]), lo = fp16_rn(2^exp x - hi) (fp16 bit patterns; cols % 8 == 0).
+ * hg_gemm_f16pre: D = alpha A B with both operands pre-split and K-major: A_g(m,kk) =
+ * 2^-a_exp (A16[g*sa + m*lda + kk] + A16[a_lo + g*sa + m*lda + kk]) (likewise B with n for m);
+ * lda, ldb, sa, sb, a_lo, b_lo multiples of 8 (fp16 elements). */
+hg_status hg_f16_split(const float* x, int64_t rows, int32_t cols, int64_t ld, int32_t exp, uint16_t* hi,
+                       uint16_t* lo, int64_t ldo, hg_stream_t stream);
+hg_status hg_gemm_f16pre(int32_t M, int32_t N, int32_t K, int32_t batch, const uint16_t* A16, int64_t a_lo,
+                         int64_t lda, int64_t sa, int32_t a_exp, const uint16_t* B16, int64_t b_lo, int64_t ldb,
+                         int64_t sb, int32_t b_exp, float* D, int32_t d_trans, int64_t ldd, int64_t sd, float alpha,
+                         hg_stream_t stream);
 
 /* Stage profiler (tracing).  hg_profile_enable(1) makes the calls on this host
  * thread bracket each stage launch with CUDA events on its stream (off by

@@ -114,6 +114,7 @@ constexpr size_t ALIGN = 256;
 
 struct Layout {
   size_t de = 0, eval = 0, dvr = 0, keys = 0, blocks = 0, P[4] = {0, 0, 0, 0}, Ut = 0, Vt = 0;
+  size_t X16 = 0, P16[4] = {0, 0, 0, 0};   // 3xF16 pre-split twins of the blocks and the panels (hi | lo planes)
   size_t G = 0, L = 0, Linv = 0, Wf = 0, Uk = 0, work = 0, eig = 0, sig = 0, sigma = 0, sigl = 0, rs = 0, Z = 0,
          Yp = 0, Fp = 0, status = 0;
   size_t h_rowptr = 0, h_col = 0, h_w = 0, h_Y = 0, h_F = 0;
@@ -135,6 +136,8 @@ Layout layout(int64_t N, int64_t E, int64_t nnz, int64_t b, int64_t k, int64_t T
   L.keys = take(assemble_keys_bytes(nnz, (int)nb, (int)E));
   L.blocks = take(4 * nb * b * b);
   for (int i = 0; i < 4; ++i) L.P[i] = take(4 * nb * k * b);
+  L.X16 = take(4 * nb * b * b);
+  for (int i = 0; i < 4; ++i) L.P16[i] = take(4 * nb * k * b);
   L.Ut = take(4 * nb * k * b);
   L.Vt = take(4 * nb * k * b);
   L.G = take(4 * nb * k * k);
@@ -209,12 +212,41 @@ static int bn_env(const char* name, int dflt) {
   return x >= 256 ? 256 : x >= 128 ? 128 : x >= 64 ? 64 : 32;
 }
 
+// 3xF16 bookkeeping of the rSVD panels: which fp32 panels carry a
+// valid pre-split twin (hi | lo fp16 planes), the power-of-two exponent it was scaled by, and a
+// bound on its column 2-norms.  Products X P have |(X P)_ij| <= ||x_i|| ||p_j|| <= cb(P) since
+// ||X||_2 <= 1 (X = I - Theta/(1+mu), 0 <= eig(Theta) <= 1), so the exponent of every twin follows
+// from bounds, not from the data: Omega |z| <= 8.7 (Box-Muller on 53-bit uniforms, philox.cu),
+// orthonormalised panels ||q_j|| <= 2.
+constexpr int kNoTwin = -99;
+struct Twins {
+  const float* f[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint16_t* h[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t lo = 0;
+  int exp[4] = {kNoTwin, kNoTwin, kNoTwin, kNoTwin};
+  float cb[4] = {0.f, 0.f, 0.f, 0.f};
+  int find(const float* p) const {
+    for (int i = 0; i < 4; ++i)
+      if (f[i] == p) return i;
+    return -1;
+  }
+  bool valid(int i) const { return i >= 0 && exp[i] != kNoTwin; }
+};
+// largest e <= 14 with 2^e * 1.01 * bound < 65504 (fp16 max)
+static int f16_exp(float bound) {
+  const int e = (int)floorf(log2f(65504.f / (1.01f * bound)));
+  return e < 14 ? e : 14;
+}
+
 struct Rsvd {
   int nb, b, k;
   bool simt;
   cudaStream_t s;
   const float* X;
   bool general = false;   // HG_GENERAL: X^T products use the literal transpose (else X^T = X, reading A12)
+  const uint16_t* X16 = nullptr;   // pre-split X (exponent 14, |X_ij| <= 1): 3xF16 power products
+  int64_t x_lo = 0;
+  Twins* tw = nullptr;
 
   // out_t = (X P)^T  with P given as P_t [k][b]; trans: (X^T P)^T, the literal X^T only when general
   // (X symmetric: X^T P = X P, reading A12)
@@ -225,6 +257,21 @@ struct Rsvd {
     g.B = P_t; g.b_mn = false; g.ldb = b; g.sb = (int64_t)k * b;
     g.D = out_t; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
     g.bn_max = bn_env("HG_BN_POWER", 256);
+    const int i = tw ? tw->find(P_t) : -1, o = tw ? tw->find(out_t) : -1;
+    const bool f16 = X16 && tw && tw->valid(i) && !simt;
+    if (f16) {   // both operands pre-split: no in-kernel split, kind::f16 at twice the tf32 rate
+      g.prec = 1;
+      g.A16 = X16; g.a_lo = x_lo; g.a_exp = 14;
+      g.B16 = tw->h[i]; g.b_lo = tw->lo; g.b_exp = tw->exp[i];
+    }
+    if (o >= 0) {
+      tw->exp[o] = kNoTwin;
+      if (f16) {   // |(X P)_ij| <= cb(P); the column norms do not grow either
+        g.D16 = tw->h[o]; g.d_lo = tw->lo; g.d_exp = f16_exp(tw->cb[i]);
+        tw->exp[o] = g.d_exp;
+        tw->cb[o] = tw->cb[i];
+      }
+    }
     return gemm(g, s, simt, "power product X*S", ST_GEMM_POWER);
   }
   // G = P^T P (k x k)
@@ -237,6 +284,11 @@ struct Rsvd {
     // symmetric: 128-wide tiles on and below the diagonal only (k_cholinv reads the lower triangle)
     g.bn_max = bn_env("HG_BN_GRAM", 128);
     g.lower = !getenv("HG_GRAM_FULL");
+    const int i = tw ? tw->find(P_t) : -1;
+    if (tw && tw->valid(i) && !simt) {
+      g.prec = 1;
+      g.A16 = g.B16 = tw->h[i]; g.a_lo = g.b_lo = tw->lo; g.a_exp = g.b_exp = tw->exp[i];
+    }
     return gemm(g, s, simt, "Gram P^T P", ST_GEMM_GRAM);
   }
   // Q = P L^-T  ->  Q_t
@@ -249,6 +301,15 @@ struct Rsvd {
     g.bn_max = bn_env("HG_BN_QFORM", 256);
     static const bool tri = !getenv("HG_QFORM_FULL");   // Linv is lower: B(kk, n) = Linv(n, kk) upper
     g.b_upper = tri;
+    const int o = tw ? tw->find(Q_t) : -1;
+    if (o >= 0) {   // the orthonormalised panel's twin for the next power product / Gram: ||q_j|| <= 2
+      tw->exp[o] = kNoTwin;
+      if (!simt) {
+        g.D16 = tw->h[o]; g.d_lo = tw->lo; g.d_exp = f16_exp(2.f);
+        tw->exp[o] = g.d_exp;
+        tw->cb[o] = 2.f;
+      }
+    }
     return gemm(g, s, simt, "Q = Y R^-1", ST_GEMM_QFORM);
   }
 };
@@ -262,6 +323,13 @@ struct Rsvd {
 static int qr_passes_env() {   // read per call (tests switch it)
   const char* v = getenv("HG_QR_PASSES");
   return v ? atoi(v) : 1;
+}
+
+// 3xF16 power products and Grams (pre-split X and panels) on unless
+// HG_GEMM_F16=0 (read per call: tests switch it); the pre-split planes need b % 8 == 0.
+static bool f16_on(int b, bool simt) {
+  const char* v = getenv("HG_GEMM_F16");
+  return !simt && b % 8 == 0 && !(v && v[0] == '0');
 }
 
 // Jacobi preconditioner (eig.cu) on unless HG_JACOBI_PRE=0 (read per call: tests switch it)
@@ -294,6 +362,8 @@ hg_status cholqr(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* L
 // problem (parts run concurrently on different streams; see solve_impl).
 struct Bufs {
   float* P[4];
+  uint16_t* P16[4];   // pre-split twins of P (hi plane; lo plane p16_lo fp16 elements further)
+  int64_t p16_lo;
   float *G, *L, *Linv, *Wf, *Uk, *work, *eig, *rs, *Z, *Yp, *Fp;
   double* sig;
   int32_t* perm;
@@ -302,6 +372,8 @@ Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k,
   Bufs B;
   const int64_t kb = (int64_t)blk0 * k * b, kk = (int64_t)blk0 * k * k, k1 = (int64_t)blk0 * k;
   for (int i = 0; i < 4; ++i) B.P[i] = at<float>(ws, Lo.P[i]) + kb;
+  for (int i = 0; i < 4; ++i) B.P16[i] = at<uint16_t>(ws, Lo.P16[i]) + kb;
+  B.p16_lo = (int64_t)nb_total * k * b;
   B.G = at<float>(ws, Lo.G) + kk;
   B.L = at<float>(ws, Lo.L) + kk;
   B.Linv = at<float>(ws, Lo.Linv) + kk;
@@ -325,8 +397,19 @@ Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k,
 // and orthonormalised once (shifted CholeskyQR3).
 hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64_t seed, bool simt, float* Ut,
                    float* sigma, float* Vt, int32_t* st, const Bufs& Bf, cudaStream_t s, int scheme = 0,
-                   bool general = false, bool uv_bk = false) {
+                   bool general = false, bool uv_bk = false, const uint16_t* X16 = nullptr, int64_t x_lo = 0) {
   Rsvd R{nb, b, k, simt, s, X, general};
+  Twins tw;
+  if (X16 && !simt && !general) {
+    for (int i = 0; i < 4; ++i) {
+      tw.f[i] = Bf.P[i];
+      tw.h[i] = Bf.P16[i];
+    }
+    tw.lo = Bf.p16_lo;
+    R.X16 = X16;
+    R.x_lo = x_lo;
+    R.tw = &tw;
+  }
   float* P[4];
   for (int i = 0; i < 4; ++i) P[i] = Bf.P[i];
   float* G = Bf.G;
@@ -341,6 +424,12 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
   {
     ProfScope ps(ST_OMEGA, s);
     HG_CU(launch_omega_panels(seed, blk0, nb, b, k, P[0], s, &g_launches), "omega");
+    if (R.tw) {   // |Omega_ij| <= 8.7: the twin for the first 3xF16 power product
+      tw.exp[0] = f16_exp(8.7f);
+      tw.cb[0] = 8.7f * sqrtf((float)b);
+      HG_CU(launch_f16_split(P[0], (int64_t)nb * k, b, b, tw.exp[0], tw.h[0], tw.h[0] + tw.lo, b, s), "omega split");
+      ++g_launches;
+    }
   }
   // Passes per QR: the final basis S (used by B = S^T X and U = S U~) gets
   // CholeskyQR2; an intermediate basis is only multiplied by X next, so one CholeskyQR pass
@@ -451,6 +540,7 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
     g.B = Uk; g.b_mn = false; g.ldb = k; g.sb = (int64_t)k * k;
     g.D = P[2 + w]; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
     HG_TRY(gemm(g, s, simt, w == 0 ? "V = B^T U~" : "U = S U~"));
+    if (R.tw) tw.exp[2 + w] = kNoTwin;
   }
   {
     ProfScope ps(ST_FINALIZE, s);
@@ -719,16 +809,23 @@ hg_status hg_block_rsvd_ex(const float* blocks, int32_t nb, int32_t b, int32_t k
   const int scheme = (flags & HG_POWER_EQ10) ? 1 : 0;
   const bool simt = (flags & HG_GEMM_SIMT) != 0;
   const bool general = (flags & HG_GENERAL) != 0, uv_bk = (flags & HG_UV_BK) != 0;
+  // HG_X_UNIT: the caller's bound |X_ij| <= 1, ||X||_2 <= 1 makes the 3xF16 twins safe (as in hg_solve)
+  uint16_t* x16 = ((flags & HG_X_UNIT) && !general && f16_on(b, simt)) ? at<uint16_t>(ws, Lo.X16) : nullptr;
+  const int64_t x_lo = (int64_t)nb * b * b;
+  if (x16) {
+    HG_CU(launch_f16_split(blocks, (int64_t)nb * b, b, b, 14, x16, x16 + x_lo, b, s), "blocks split");
+    ++g_launches;
+  }
   if (p == 0)
     return run_rsvd(blocks, nb, 0, b, k, q, seed, simt, Ut, sigma, Vt, d_status, part_bufs(ws, Lo, nb, 0, b, k, 0), s,
-                    scheme, general, uv_bk);
+                    scheme, general, uv_bk, x16, x_lo);
   if (uv_bk) return fail(HG_ERR_INVALID, "HG_UV_BK is not supported with oversampling (p > 0)");
   // oversampled: factor at width l into the workspace, keep the top k triplets (rank-k truncation)
   float* Ul = at<float>(ws, Lo.Ut);
   float* Vl = at<float>(ws, Lo.Vt);
   float* sl = at<float>(ws, Lo.sigl);
   HG_TRY(run_rsvd(blocks, nb, 0, b, l, q, seed, simt, Ul, sl, Vl, d_status, part_bufs(ws, Lo, nb, 0, b, l, 0), s,
-                  scheme, general));
+                  scheme, general, false, x16, x_lo));
   HG_CU(cudaMemcpy2DAsync(Ut, 4 * (size_t)k * b, Ul, 4 * (size_t)l * b, 4 * (size_t)k * b, nb, cudaMemcpyDeviceToDevice,
                           s), "truncate U");
   HG_CU(cudaMemcpy2DAsync(Vt, 4 * (size_t)k * b, Vl, 4 * (size_t)l * b, 4 * (size_t)k * b, nb, cudaMemcpyDeviceToDevice,
@@ -973,6 +1070,16 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     const Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, l, T);
     g_cur_part = pt;
     HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[pt]));
+    // the 3xF16 twin of the part's blocks: |X_ij| <= 1 (and |Theta_ij| <= 1), exponent 14
+    uint16_t* x16 = f16_on(b, simt) ? at<uint16_t>(ws, Lo.X16) : nullptr;
+    const int64_t x_lo = (int64_t)nb * b * b;
+    if (x16) {
+      ProfScope psx(ST_ASSEMBLE, ps[pt]);
+      x16 += (int64_t)blk0 * b * b;
+      HG_CU(launch_f16_split(blocks + (int64_t)blk0 * b * b, (int64_t)nbp * b, b, b, 14, x16, x16 + x_lo, b, ps[pt]),
+            "blocks split");
+      ++g_launches;
+    }
     // HG_JACOBI_WIDE = bitmask of parts whose Jacobi runs on 64-row cluster CTAs (twice the SMs
     // per block: a shorter per-block latency for that part).  Off by default in BOTH entries: the
     // cluster width changes the order of the Jacobi's Gram partial sums, so a wide part's bits
@@ -982,7 +1089,8 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     static const int wide_rows = getenv("HG_JACOBI_WIDE_ROWS") ? atoi(getenv("HG_JACOBI_WIDE_ROWS")) : 64;
     jacobi_rows_hint(((wide >> pt) & 1) ? wide_rows : 0);
     hg_status rs = run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, l, q, seed, simt, Ut + kb,
-                            sigma + (int64_t)(blk0 - soff) * l, Vt + kb, st, Bf, ps[pt], scheme);
+                            sigma + (int64_t)(blk0 - soff) * l, Vt + kb, st, Bf, ps[pt], scheme, false, false, x16,
+                            x_lo);
     jacobi_rows_hint(0);
     HG_TRY(rs);
     if (cps) HG_CU(cudaStreamWaitEvent(ps[pt], ev_y[pt], 0), "wait Y");
@@ -1025,7 +1133,7 @@ constexpr size_t kMaxGraphs = 8;
 std::string knob_env() {   // enqueue-time knobs that change the captured sequence
   std::string e;
   for (const char* n : {"HG_ASSEMBLE", "HG_STREAMS_SERIAL", "HG_BN_POWER", "HG_BN_GRAM", "HG_BN_QFORM", "HG_GRAM_FULL",
-                        "HG_QR_PASSES", "HG_STREAM_PRIO"}) {
+                        "HG_QR_PASSES", "HG_STREAM_PRIO", "HG_GEMM_F16", "HG_JACOBI_PRE"}) {
     const char* v = getenv(n);
     e += v ? v : "-";
     e += '|';
@@ -1842,6 +1950,35 @@ hg_status hg_gemm_ex(int32_t M, int32_t N, int32_t K, int32_t batch, const float
   g.alpha = alpha; g.rs = rs; g.srs = srs; g.cs = cs; g.scs = scs;
   g.prec = prec; g.a_exp = a_exp; g.b_exp = b_exp;
   return gemm(g, reinterpret_cast<cudaStream_t>(stream), (flags & HG_GEMM_SIMT) != 0, "hg_gemm_ex");
+}
+
+hg_status hg_f16_split(const float* x, int64_t rows, int32_t cols, int64_t ld, int32_t exp, uint16_t* hi,
+                       uint16_t* lo, int64_t ldo, hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!x || !hi || !lo) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (rows < 0 || cols < 0 || (cols & 7) || (ld & 3) || (ldo & 7) || ld < cols || ldo < cols)
+    return fail(HG_ERR_INVALID, "need cols %% 8 == 0, ld %% 4 == 0, ldo %% 8 == 0, ld, ldo >= cols");
+  HG_CU(launch_f16_split(x, rows, cols, ld, exp, hi, lo, ldo, reinterpret_cast<cudaStream_t>(stream)), "f16 split");
+  ++g_launches;
+  return HG_OK;
+}
+
+hg_status hg_gemm_f16pre(int32_t M, int32_t N, int32_t K, int32_t batch, const uint16_t* A16, int64_t a_lo,
+                         int64_t lda, int64_t sa, int32_t a_exp, const uint16_t* B16, int64_t b_lo, int64_t ldb,
+                         int64_t sb, int32_t b_exp, float* D, int32_t d_trans, int64_t ldd, int64_t sd, float alpha,
+                         hg_stream_t stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!A16 || !B16 || !D) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  GemmDesc g;
+  g.M = M; g.N = N; g.K = K; g.batch = batch;
+  g.A16 = A16; g.a_lo = a_lo; g.lda = lda; g.sa = sa; g.a_exp = a_exp;
+  g.B16 = B16; g.b_lo = b_lo; g.ldb = ldb; g.sb = sb; g.b_exp = b_exp;
+  g.D = D; g.d_trans = d_trans != 0; g.ldd = ldd; g.sd = sd;
+  g.alpha = alpha;
+  g.prec = 1;
+  return gemm(g, reinterpret_cast<cudaStream_t>(stream), false, "hg_gemm_f16pre");
 }
 
 }  // extern "C"

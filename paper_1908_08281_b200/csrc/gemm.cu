@@ -30,6 +30,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -61,6 +62,11 @@ struct EpiArgs {
   // 3xF16 only
   int a_pre, b_pre;   // operand TMA-loaded pre-split (hi | lo fp16 planes): no in-kernel split
   float a_sc, b_sc;   // 2^a_exp, 2^b_exp: prescale of the in-kernel split
+  // optional pre-split copy of the (transposed) output for a later 3xF16 GEMM: hi / lo planes of
+  // fp16_rn(2^d_exp D) at D16[g*sd + n*ldd + m] and D16 + d_lo (both precisions)
+  uint16_t* D16;
+  int64_t d_lo;
+  float d_sc;
 };
 
 constexpr int NEPI = 256;            // converter / epilogue threads (8 warps)
@@ -113,6 +119,15 @@ __device__ __forceinline__ void f16_split_store(uint8_t* hi, uint8_t* lo, int r,
   *reinterpret_cast<uint2*>(lo + off) = lv;
 }
 
+__device__ __forceinline__ void split4(float4 x, float sc, uint2& hv, uint2& lv) {
+  x = make_float4(x.x * sc, x.y * sc, x.z * sc, x.w * sc);
+  const __half2 h01 = __floats2half2_rn(x.x, x.y), h23 = __floats2half2_rn(x.z, x.w);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn(x.x - f01.x, x.y - f01.y), l23 = __floats2half2_rn(x.z - f23.x, x.w - f23.y);
+  hv.x = *reinterpret_cast<const uint32_t*>(&h01); hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+  lv.x = *reinterpret_cast<const uint32_t*>(&l01); lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+}
+
 __device__ __forceinline__ float trunc_lo(float x) {   // x - trunc_tf32(x), exact in fp32
   return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
@@ -148,7 +163,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   auto sA_hi = [&](int s) { return base + s * C::STAGE_BYTES; };
   auto sA_lo = [&](int s) { return base + s * C::STAGE_BYTES + C::A_BYTES; };
-  auto sB_hi = [&](int s) { return base + s * C::STAGE_BYTES + 2 * C::A_BYTES; };
+  // 3xF16: [A tile | B tile] per stage (each split in place); 3xTF32: [A hi | A lo | B hi | B lo]
+  auto sB_hi = [&](int s) { return base + s * C::STAGE_BYTES + (F16 ? 1 : 2) * C::A_BYTES; };
   auto sB_lo = [&](int s) { return base + s * C::STAGE_BYTES + 2 * C::A_BYTES + C::B_BYTES; };
 
   if (warp == 8 && lane == 0) {
@@ -451,7 +467,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int n = nb0 + j;
           if (n < ea.N) {
             HG_DCHECK(mw0 + 4 * l4 + 3 < ea.ldd);
-            *reinterpret_cast<float4*>(dcol + (int64_t)n * ea.ldd) = *reinterpret_cast<const float4*>(st + j * TP + 4 * l4);
+            const float4 v = *reinterpret_cast<const float4*>(st + j * TP + 4 * l4);
+            *reinterpret_cast<float4*>(dcol + (int64_t)n * ea.ldd) = v;
+            if (ea.D16) {
+              uint2 hv, lv;
+              split4(v, ea.d_sc, hv, lv);
+              uint16_t* d16 = ea.D16 + (int64_t)g * ea.sd + (int64_t)n * ea.ldd + mw0 + 4 * l4;
+              *reinterpret_cast<uint2*>(d16) = hv;
+              *reinterpret_cast<uint2*>(d16 + ea.d_lo) = lv;
+            }
           }
         }
       } else if (m < ea.M) {
@@ -462,6 +486,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             float val = acc[j] * rsv;
             if (ea.cs) val *= ea.cs[(int64_t)g * ea.scs + n];
             Dg[(int64_t)n * ea.ldd + m] = val;
+            if (ea.D16) {
+              const float x = val * ea.d_sc;
+              const __half hh = __float2half_rn(x);
+              const __half ll = __float2half_rn(x - __half2float(hh));
+              uint16_t* d16 = ea.D16 + (int64_t)g * ea.sd + (int64_t)n * ea.ldd + m;
+              d16[0] = *reinterpret_cast<const uint16_t*>(&hh);
+              d16[ea.d_lo] = *reinterpret_cast<const uint16_t*>(&ll);
+            }
           }
         }
       }
@@ -564,6 +596,34 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
           Dg[(int64_t)m * ea.ldd + n] = v;
       }
     }
+}
+
+// ------------------------------------------------------------------ pre-split producer
+// hi[i] = fp16_rn(2^e x[i]), lo[i] = fp16_rn(2^e x[i] - hi[i]) over rows x cols (row pitch ld for x,
+// ldo for hi / lo); 8 elements per thread (16-byte fp16 stores).
+__global__ void __launch_bounds__(256) k_f16_split(const float* __restrict__ x, int64_t rows, int cols, int64_t ld,
+                                                   float sc, uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
+                                                   int64_t ldo) {
+  const int c8 = cols / 8;
+  const int64_t n = rows * c8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / c8;
+    const int c = (int)(i % c8) * 8;
+    const float4 a = *reinterpret_cast<const float4*>(x + r * ld + c);
+    const float4 b = *reinterpret_cast<const float4*>(x + r * ld + c + 4);
+    const float v[8] = {a.x * sc, a.y * sc, a.z * sc, a.w * sc, b.x * sc, b.y * sc, b.z * sc, b.w * sc};
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __half2 hh = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
+      const float2 hf = __half22float2(hh);
+      const __half2 ll = __floats2half2_rn(v[2 * j] - hf.x, v[2 * j + 1] - hf.y);
+      h[j] = *reinterpret_cast<const uint32_t*>(&hh);
+      l[j] = *reinterpret_cast<const uint32_t*>(&ll);
+    }
+    *reinterpret_cast<uint4*>(hi + r * ldo + c) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(lo + r * ldo + c) = make_uint4(l[0], l[1], l[2], l[3]);
+  }
 }
 
 // ------------------------------------------------------------------ host
@@ -675,7 +735,10 @@ const char* gemm_check(const GemmDesc& g) {
   if (!pa && (g.a_mn ? g.lda < g.M : g.lda < g.K)) return "gemm: lda too small";
   if (!pb && (g.b_mn ? g.ldb < g.N : g.ldb < g.K)) return "gemm: ldb too small";
   if (g.C && (g.d_trans || g.ldc < g.N)) return "gemm: residual C needs row-major D and ldc >= N";
-  if (g.a_exp < -40 || g.a_exp > 40 || g.b_exp < -40 || g.b_exp > 40) return "gemm: |a_exp|, |b_exp| must be <= 40";
+  if (g.a_exp < -40 || g.a_exp > 40 || g.b_exp < -40 || g.b_exp > 40 || g.d_exp < -40 || g.d_exp > 40)
+    return "gemm: |a_exp|, |b_exp|, |d_exp| must be <= 40";
+  if (g.D16 && (!g.d_trans || !al16(g.D16) || (g.ldd & 3) || (g.d_lo & 3) || (g.batch > 1 && (g.sd & 3))))
+    return "gemm: the pre-split output D16 needs d_trans, 16-byte alignment, ldd/d_lo/sd multiples of 4";
   return nullptr;
 }
 
@@ -693,7 +756,8 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
   EpiArgs ea{g.M, g.N, g.K, g.D, g.ldd, g.sd, g.d_trans ? 1 : 0, alpha, g.rs, g.srs, g.cs, g.scs,
              g.a_mn ? 1 : 0, g.b_mn ? 1 : 0, trunc_hi, g.lower ? 1 : 0, g.C, g.ldc, g.sc, g.beta,
              (g.b_upper && (f16 || !g.b_mn)) ? 1 : 0,
-             g.A16 ? 1 : 0, g.B16 ? 1 : 0, ldexpf(1.0f, g.a_exp), ldexpf(1.0f, g.b_exp)};
+             g.A16 ? 1 : 0, g.B16 ? 1 : 0, ldexpf(1.0f, g.a_exp), ldexpf(1.0f, g.b_exp),
+             g.D16, g.d_lo, ldexpf(1.0f, g.d_exp)};
   if (simt) {
     if (g.A16 || g.B16) return cudaErrorInvalidValue;
     dim3 grid((g.M + 63) / 64, (g.N + 63) / 64, g.batch);
@@ -711,4 +775,14 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
   if (n <= 64) return launch_tc<64, false>(g, ea, stream);
   if (n <= 128) return launch_tc<128, false>(g, ea, stream);
   return launch_tc<256, false>(g, ea, stream);
+}
+
+cudaError_t launch_f16_split(const float* x, int64_t rows, int cols, int64_t ld, int exp, uint16_t* hi, uint16_t* lo,
+                             int64_t ldo, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  if ((cols & 7) || (ld & 3) || (ldo & 7)) return cudaErrorInvalidValue;
+  const int64_t n = rows * (cols / 8);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_f16_split<<<grid, 256, 0, stream>>>(x, rows, cols, ld, ldexpf(1.0f, exp), hi, lo, ldo);
+  return cudaGetLastError();
 }

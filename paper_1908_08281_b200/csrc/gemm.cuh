@@ -46,6 +46,12 @@ struct GemmDesc {
   int64_t a_lo = 0;
   const uint16_t* B16 = nullptr;
   int64_t b_lo = 0;
+  // Optional pre-split copy of a transposed output (d_trans only, either precision): hi / lo
+  // planes of fp16_rn(2^d_exp D) at D16[g*sd + n*ldd + m] and D16 + d_lo -- the B16 / A16 form
+  // of a later 3xF16 GEMM that reads D K-major.
+  uint16_t* D16 = nullptr;
+  int64_t d_lo = 0;
+  int d_exp = 0;
 };
 
 // Enqueue the GEMM; returns cudaSuccess or the launch error.  `simt` selects the
@@ -56,3 +62,7 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt);
 const char* gemm_check(const GemmDesc& g);
 // The precision launch_gemm will use for g (0 = 3xTF32, 1 = 3xF16).
 int gemm_prec(const GemmDesc& g);
+// Pre-split producer for 3xF16 operands: hi = fp16_rn(2^exp x), lo = fp16_rn(2^exp x - hi) over a
+// rows x cols fp32 matrix (row pitch ld) into hi / lo planes of row pitch ldo (cols % 8 == 0).
+cudaError_t launch_f16_split(const float* x, int64_t rows, int cols, int64_t ld, int exp, uint16_t* hi, uint16_t* lo,
+                             int64_t ldo, cudaStream_t stream);

@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libhgrsvd_check.so" if os.environ.get("HG_LIB") 
 
 HG_OK, HG_ERR_INVALID, HG_ERR_NUMERICAL, HG_ERR_CUDA = 0, 2, 3, 4
 HG_RAW_THETA, HG_SYNC, HG_WOODBURY, HG_POWER_EQ10, HG_GEMM_SIMT = 1 << 0, 1 << 1, 1 << 2, 1 << 3, 1 << 8
-HG_GENERAL, HG_UV_BK = 1 << 4, 1 << 5
+HG_GENERAL, HG_UV_BK, HG_X_UNIT = 1 << 4, 1 << 5, 1 << 6
 ST_FLAGS = {1: "isolated vertex", 2: "empty hyperedge", 4: "Cholesky breakdown", 8: "Jacobi sweep cap",
             16: "singular sigma", 32: "non-finite value", 64: "CG breakdown", 128: "degenerate simplex"}
 
@@ -69,6 +69,9 @@ _solve_host = _sig("hg_solve_host", ctypes.c_int, _i32, _i32, _i64, _P, _P, _P, 
                    _i32, _P, _P, _u32, _P, _sz, _P)
 _gemm = _sig("hg_gemm", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i32, _i64, _i64, _P, _i32, _i64, _i64, _P, _i32,
              _i64, _i64, _f32, _P, _i64, _P, _i64, _u32, _P)
+_f16_split = _sig("hg_f16_split", ctypes.c_int, _P, _i64, _i32, _i64, _i32, _P, _P, _i64, _P)
+_gemm_f16pre = _sig("hg_gemm_f16pre", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i64, _i64, _i64, _i32, _P, _i64, _i64,
+                    _i64, _i32, _P, _i32, _i64, _i64, _f32, _P)
 _gemm_ex = _sig("hg_gemm_ex", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i32, _i64, _i64, _P, _i32, _i64, _i64, _P,
                 _i32, _i64, _i64, _f32, _P, _i64, _P, _i64, _u32, _i32, _i32, _i32, _P)
 _cg_workspace_size = _sig("hg_cg_workspace_size", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, ctypes.POINTER(_sz))
@@ -95,7 +98,7 @@ _last_launches = _sig("hg_last_launch_count", ctypes.c_int32)
 _debug_counters = _sig("hg_debug_counters", ctypes.c_int, _P, _i32, _i32)
 
 EXPORTS = ("hg_workspace_size", "hg_build_theta", "hg_fill_gaussian", "hg_block_rsvd", "hg_block_apply_inverse",
-           "hg_solve", "hg_solve_host", "hg_gemm", "hg_gemm_ex", "hg_last_error", "hg_last_launch_count", "hg_profile_enable",
+           "hg_solve", "hg_solve_host", "hg_gemm", "hg_gemm_ex", "hg_f16_split", "hg_gemm_f16pre", "hg_last_error", "hg_last_launch_count", "hg_profile_enable",
            "hg_profile_collect", "hg_profile_timeline", "hg_debug_counters", "hg_cg_workspace_size", "hg_cg_solve",
            "hg_block_apply_woodbury", "hg_workspace_size_ex", "hg_block_rsvd_ex", "hg_solve_ex",
            "hg_weight_gradient", "hg_weight_step", "hg_schur_workspace_size",
@@ -265,11 +268,12 @@ def fill_gaussian(seed: int, rows: int, cols: int, device="cuda", stream=None) -
 
 
 def block_rsvd(blocks: torch.Tensor, k: int, q: int, seed: int, *, simt: bool = False, p: int = 0,
-               eq10: bool = False, general: bool = False, uv_bk: bool = False, ws: Optional[Workspace] = None,
-               status: Optional[torch.Tensor] = None, stream=None):
+               eq10: bool = False, general: bool = False, uv_bk: bool = False, x_unit: bool = False,
+               ws: Optional[Workspace] = None, status: Optional[torch.Tensor] = None, stream=None):
     """Alg. 1 on each block (oversampling p, Eq. 10 scheme with eq10; general: literal X^T products for
     non-symmetric blocks): Ut [nb][k][b], sigma [nb][k], Vt [nb][k][b], status -- with uv_bk the first and
-    third are U, V [nb][b][k]."""
+    third are U, V [nb][b][k].  x_unit: the caller guarantees |X_ij| <= 1 and ||X_ii||_2 <= 1 (blocks from
+    build_theta): the 3xF16 power products of the solve entries (HG_X_UNIT)."""
     _dev(blocks, torch.float32)
     nb, b, _ = blocks.shape
     ws = ws or Workspace.for_sizes(nb * b, 1, 0, b, k, 0, p=p)
@@ -279,7 +283,7 @@ def block_rsvd(blocks: torch.Tensor, k: int, q: int, seed: int, *, simt: bool = 
     sigma = torch.empty((nb, k), dtype=torch.float32, device=blocks.device)
     st = status if status is not None else torch.zeros(1, dtype=torch.int32, device=blocks.device)
     flags = (HG_GEMM_SIMT if simt else 0) | (HG_POWER_EQ10 if eq10 else 0) | (HG_GENERAL if general else 0) | \
-        (HG_UV_BK if uv_bk else 0)
+        (HG_UV_BK if uv_bk else 0) | (HG_X_UNIT if x_unit else 0)
     _check(_block_rsvd_ex(_ptr(blocks), nb, b, k, p, q, seed, flags, _ptr(Ut), _ptr(sigma), _ptr(Vt),
                           _ptr(st), ws.ptr, ws.nbytes, _stream(stream)))
     return Ut, sigma, Vt, st
@@ -405,6 +409,28 @@ def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, batch: int
         _check(_gemm_ex(M, N, K, batch, _ptr(A), int(a_mn), lda, sa, _ptr(B), int(b_mn), ldb, sb, _ptr(D),
                         int(d_trans), ldd, sd, alpha, _ptr(rs), srs, _ptr(cs), scs, HG_GEMM_SIMT if simt else 0,
                         prec, a_exp, b_exp, _stream(stream)))
+    return D
+
+
+def f16_split(x: torch.Tensor, exp: int, stream=None):
+    """Verification export: the 3xF16 pre-split of a 2D/3D fp32 tensor (last dim % 8 == 0) into
+    (hi, lo) int16 tensors holding fp16 bit patterns of 2^exp x and 2^exp x - hi."""
+    _dev(x, torch.float32)
+    cols = x.shape[-1]
+    rows = x.numel() // cols
+    hi = torch.empty(x.shape, dtype=torch.int16, device=x.device)
+    lo = torch.empty_like(hi)
+    _check(_f16_split(_ptr(x), rows, cols, cols, exp, _ptr(hi), _ptr(lo), cols, _stream(stream)))
+    return hi, lo
+
+
+def gemm_f16pre(A16: torch.Tensor, a_lo: int, B16: torch.Tensor, b_lo: int, *, M: int, N: int, K: int, batch: int,
+                lda: int, sa: int, a_exp: int, ldb: int, sb: int, b_exp: int, D: torch.Tensor, d_trans: bool = False,
+                ldd: int, sd: int = 0, alpha: float = 1.0, stream=None):
+    """Verification export: 3xF16 GEMM on pre-split K-major operands (hi planes at A16 / B16, lo planes
+    a_lo / b_lo fp16 elements further on)."""
+    _check(_gemm_f16pre(M, N, K, batch, _ptr(A16), a_lo, lda, sa, a_exp, _ptr(B16), b_lo, ldb, sb, b_exp, _ptr(D),
+                        int(d_trans), ldd, sd, alpha, _stream(stream)))
     return D
 
 

@@ -187,11 +187,17 @@ def test_solve_parity_configs_1_to_3(inputs, cfg):
     c = CONFIGS[cfg]
     H, w, Y = dev_inputs(h)
     X, _, _ = hg.build_theta(H, w, c.mu, c.b)
-    Ut, sigma, Vt, st = hg.block_rsvd(X, c.k, c.q, c.seed)
+    # x_unit: build_theta's blocks satisfy |X_ij| <= 1, ||X_ii|| <= 1 -- the 3xF16 products hg_solve uses
+    Ut, sigma, Vt, st = hg.block_rsvd(X, c.k, c.q, c.seed, x_unit=True)
     F, st2 = hg.block_apply_inverse(Ut, sigma, Vt, Y, c.mu / (1 + c.mu))
     torch.cuda.synchronize()
     assert int(st.item()) == 0 and int(st2.item()) == 0
     check_against_oracle(h, c, F, sigma, list(range(c.nb)), Ut, Vt)
+    # the 3xTF32 products (no x_unit) meet the same bar
+    Ut0, sigma0, Vt0, st0 = hg.block_rsvd(X, c.k, c.q, c.seed)
+    F0, _ = hg.block_apply_inverse(Ut0, sigma0, Vt0, Y, c.mu / (1 + c.mu))
+    assert int(st0.item()) == 0
+    check_against_oracle(h, c, F0, sigma0, list(range(c.nb)), Ut0, Vt0)
     # the composite entry point gives the same bits
     F2, sigma2, st3 = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
     assert int(st3.item()) == 0

@@ -56,7 +56,7 @@ def test_woodbury_solve_parity(cfg):
     check(h, c, F, sigma, list(range(c.nb)))
     # the three entry points in sequence give the same bits as the composite
     Th, _, _ = hg.build_theta(H, w, c.mu, c.b, raw=True)
-    Ut, s2, Vt, st2 = hg.block_rsvd(Th, c.k, c.q, c.seed)
+    Ut, s2, Vt, st2 = hg.block_rsvd(Th, c.k, c.q, c.seed, x_unit=True)   # Theta_ii: |.| <= 1, ||.|| <= 1
     F2, st3 = hg.block_apply_woodbury(Ut, s2, Y, c.mu)
     torch.cuda.synchronize()
     assert int(st2.item()) == 0 and int(st3.item()) == 0

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--shapes", nargs="*", default=list(SHAPES))
     ap.add_argument("--prec", type=int, default=0)
+    ap.add_argument("--pre", action="store_true", help="3xF16 with both operands pre-split (K-major shapes only)")
     a = ap.parse_args()
     g = torch.Generator(device="cuda").manual_seed(0)
     for name in a.shapes:
@@ -36,10 +37,23 @@ def main():
         Bm = torch.randn(B, *((K, N) if b_mn else (N, K)), device="cuda", generator=g)
         D = torch.empty(B, *((N, M) if d_trans else (M, N)), device="cuda")
 
-        def run():
-            hg.gemm(A, Bm, M=M, N=N, K=K, batch=B, a_mn=a_mn, lda=A.shape[2], sa=A[0].numel(), b_mn=b_mn,
-                    ldb=Bm.shape[2], sb=Bm[0].numel(), D=D, d_trans=d_trans, ldd=D.shape[2], sd=D[0].numel(),
-                    prec=a.prec, a_exp=11, b_exp=11)
+        if a.pre:
+            if a_mn or b_mn:
+                continue
+            ah, al = hg.f16_split(A, 11)
+            bh, bl = hg.f16_split(Bm, 11)
+            A16 = torch.cat([ah.flatten(), al.flatten()])
+            B16 = torch.cat([bh.flatten(), bl.flatten()])
+
+            def run():
+                hg.gemm_f16pre(A16, ah.numel(), B16, bh.numel(), M=M, N=N, K=K, batch=B, lda=A.shape[2],
+                               sa=A[0].numel(), a_exp=11, ldb=Bm.shape[2], sb=Bm[0].numel(), b_exp=11, D=D,
+                               d_trans=d_trans, ldd=D.shape[2], sd=D[0].numel())
+        else:
+            def run():
+                hg.gemm(A, Bm, M=M, N=N, K=K, batch=B, a_mn=a_mn, lda=A.shape[2], sa=A[0].numel(), b_mn=b_mn,
+                        ldb=Bm.shape[2], sb=Bm[0].numel(), D=D, d_trans=d_trans, ldd=D.shape[2], sd=D[0].numel(),
+                        prec=a.prec, a_exp=11, b_exp=11)
         for _ in range(3):
             run()
         torch.cuda.synchronize()
@@ -58,7 +72,7 @@ def main():
         useful = 2.0 * M * N * K * B / (ms / 1e3) / 1e12
         print(json.dumps({"shape": name, "MNK_batch": [M, N, K, B], "ms": ms, "useful_tflops": useful,
                           "pipe_tflops": 3 * useful, "rel_err": err,
-                          "prec": ["3xtf32", "3xf16"][a.prec],
+                          "prec": ["3xtf32", "3xf16"][a.prec] + ("-presplit" if a.pre else ""),
                           "split": os.environ.get("HG_TF32_SPLIT", "trunc")}), flush=True)
 
 
