@@ -259,6 +259,9 @@ struct Rsvd {
     g.bn_max = bn_env("HG_BN_POWER", 256);
     const int i = tw ? tw->find(P_t) : -1, o = tw ? tw->find(out_t) : -1;
     const bool f16 = X16 && tw && tw->valid(i) && !simt;
+    // X16 set: the fp32 blocks may not exist (the assembly wrote only the twin) -- every panel a
+    // power product reads (Omega, qform and power outputs) carries a twin by construction
+    if (X16 && !f16) return fail(HG_ERR_INVALID, "internal: power product operand panel without a 3xF16 twin");
     if (f16) {   // both operands pre-split: no in-kernel split, kind::f16 at twice the tf32 rate
       g.prec = 1;
       g.A16 = X16; g.a_lo = x_lo; g.a_exp = 14;
@@ -423,12 +426,12 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
   // Alg. 1 step 1-2: Omega, Y0 = X Omega, S0 = qr(Y0)
   {
     ProfScope ps(ST_OMEGA, s);
-    HG_CU(launch_omega_panels(seed, blk0, nb, b, k, P[0], s, &g_launches), "omega");
-    if (R.tw) {   // |Omega_ij| <= 8.7: the twin for the first 3xF16 power product
+    if (R.tw) {   // |Omega_ij| <= 8.7: only the twin, for the first 3xF16 power product
       tw.exp[0] = f16_exp(8.7f);
       tw.cb[0] = 8.7f * sqrtf((float)b);
-      HG_CU(launch_f16_split(P[0], (int64_t)nb * k, b, b, tw.exp[0], tw.h[0], tw.h[0] + tw.lo, b, s), "omega split");
-      ++g_launches;
+      HG_CU(launch_omega_panels(seed, blk0, nb, b, k, P[0], s, &g_launches, tw.h[0], tw.lo, tw.exp[0]), "omega");
+    } else {
+      HG_CU(launch_omega_panels(seed, blk0, nb, b, k, P[0], s, &g_launches), "omega");
     }
   }
   // Passes per QR: the final basis S (used by B = S^T X and U = S U~) gets
@@ -626,10 +629,12 @@ hg_status run_degrees(const hg_incidence* H, const float* w, int b, float* dvr, 
 
 // Eq. 1 blocks [blk0, blk0 + nb) of the N/b diagonal blocks (degrees already computed)
 hg_status run_assemble(const hg_incidence* H, float mu, int b, bool raw, int blk0, int nb, float* blocks,
-                       const float* dvr, void* ws, const Layout& Lo, cudaStream_t s) {
+                       const float* dvr, void* ws, const Layout& Lo, cudaStream_t s, uint16_t* x16 = nullptr,
+                       int64_t x_lo = 0) {
   ProfScope ps(ST_ASSEMBLE, s);
   HG_CU(launch_assemble(blk0, nb, H->n_vertices / b, b, H->n_edges, H->nnz, H->row_ptr, H->col_idx,
-                        at<float>(ws, Lo.eval), dvr, mu, raw, blocks, at<void>(ws, Lo.keys), s, &g_launches),
+                        at<float>(ws, Lo.eval), dvr, mu, raw, blocks, at<void>(ws, Lo.keys), s, &g_launches, x16,
+                        x_lo, x16 != nullptr),
         "assemble");
   return HG_OK;
 }
@@ -1069,17 +1074,12 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     const int64_t kb = (int64_t)blk0 * l * b;
     const Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, l, T);
     g_cur_part = pt;
-    HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[pt]));
-    // the 3xF16 twin of the part's blocks: |X_ij| <= 1 (and |Theta_ij| <= 1), exponent 14
+    // with the 3xF16 products the assembly writes the blocks' twin (|X_ij|, |Theta_ij| <= 1: exponent 14)
+    // instead of fp32 blocks -- nothing downstream reads those
     uint16_t* x16 = f16_on(b, simt) ? at<uint16_t>(ws, Lo.X16) : nullptr;
     const int64_t x_lo = (int64_t)nb * b * b;
-    if (x16) {
-      ProfScope psx(ST_ASSEMBLE, ps[pt]);
-      x16 += (int64_t)blk0 * b * b;
-      HG_CU(launch_f16_split(blocks + (int64_t)blk0 * b * b, (int64_t)nbp * b, b, b, 14, x16, x16 + x_lo, b, ps[pt]),
-            "blocks split");
-      ++g_launches;
-    }
+    HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[pt], x16, x_lo));
+    if (x16) x16 += (int64_t)blk0 * b * b;
     // HG_JACOBI_WIDE = bitmask of parts whose Jacobi runs on 64-row cluster CTAs (twice the SMs
     // per block: a shorter per-block latency for that part).  Off by default in BOTH entries: the
     // cluster width changes the order of the Jacobi's Gram partial sums, so a wide part's bits

@@ -3,6 +3,8 @@
 // (Salmon et al., SC'11) keyed by (seed, 0); raw block j uses counter
 // (j+1, 0, 0, 0) and yields normals 4j..4j+3 by Box-Muller in fp64, rounded to
 // fp32 (reading A6).  Normal n of the global N x k matrix is entry (n / k, n % k).
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -52,7 +54,9 @@ __global__ void k_gauss(uint64_t seed, int64_t total, float* __restrict__ out) {
 // Panels: block i (global blk0 + i) gets out[(i*k + c)*b + m] = Omega[(blk0+i)*b + m][c].
 // k % 4 == 0, so normals 4j..4j+3 share a row: a thread owns (m, c..c+3) and a warp
 // covers 32 consecutive m, i.e. every store instruction writes one 128-byte line.
-__global__ void k_gauss_panel(uint64_t seed, int64_t blk0, int b, int k, float* __restrict__ out) {
+// out16 (3xF16 twin, instead of out): hi / lo fp16 planes of 2^exp Omega at out16[i] and out16[lo + i].
+__global__ void k_gauss_panel(uint64_t seed, int64_t blk0, int b, int k, float* __restrict__ out,
+                              uint16_t* __restrict__ out16, int64_t lo, float sc) {
   const int local = blockIdx.x * blockDim.x + threadIdx.x;   // (c/4) * b + m
   if (local >= b * (k / 4)) return;
   const int m = local % b, c = 4 * (local / b);
@@ -60,17 +64,28 @@ __global__ void k_gauss_panel(uint64_t seed, int64_t blk0, int b, int k, float* 
   const int64_t r = (blk0 + i) * b + m;
   float z[4];
   normals4(seed, r * (k / 4) + c / 4, z);
-  float* o = out + (i * k + c) * b + m;
+  const int64_t o = (i * k + c) * b + m;
+  if (out16) {
 #pragma unroll
-  for (int t = 0; t < 4; ++t) o[(int64_t)t * b] = z[t];
+    for (int t = 0; t < 4; ++t) {
+      const float x = z[t] * sc;
+      const __half h = __float2half_rn(x);
+      const __half l = __float2half_rn(x - __half2float(h));
+      out16[o + (int64_t)t * b] = __half_as_ushort(h);
+      out16[lo + o + (int64_t)t * b] = __half_as_ushort(l);
+    }
+    return;
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) out[o + (int64_t)t * b] = z[t];
 }
 
 }  // namespace
 
 cudaError_t launch_omega_panels(uint64_t seed, int blk0, int nb, int b, int k, float* out, cudaStream_t s,
-                                int* launches) {
+                                int* launches, uint16_t* out16, int64_t lo, int exp) {
   const int per = b * (k / 4);
-  k_gauss_panel<<<dim3((per + 255) / 256, nb), 256, 0, s>>>(seed, blk0, b, k, out);
+  k_gauss_panel<<<dim3((per + 255) / 256, nb), 256, 0, s>>>(seed, blk0, b, k, out, out16, lo, ldexpf(1.f, exp));
   ++*launches;
   return cudaGetLastError();
 }

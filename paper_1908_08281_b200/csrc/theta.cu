@@ -16,8 +16,11 @@
 // Traffic: the b x b block is written once (4 b^2 bytes per block; HBM-write bound).
 #include <cstdlib>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+#include "gemm.cuh"
 
 cudaError_t launch_assemble_tiles(int blk0, int nb, int b, const int64_t* row_ptr, const int32_t* col_idx,
                                   const float* edge_val, const float* dv_rsqrt, float mu, bool raw_theta,
@@ -760,7 +763,8 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, const
                                                           const int2* __restrict__ rng,
                                                           const float* __restrict__ eval,
                                                           const float* __restrict__ dvr, float inv1pmu, int raw,
-                                                          float* __restrict__ blocks) {
+                                                          float* __restrict__ blocks, uint16_t* __restrict__ x16,
+                                                          int64_t x_lo) {
   const int blk = blk0 + blockIdx.x;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   float* acc = reinterpret_cast<float*>(smem_raw);                                  // [R2_ROWS][b]
@@ -859,7 +863,8 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, const
   }
   __syncwarp();
   const float du = dvs[uu];
-  float* orow = blocks + (int64_t)blk * b * b + (int64_t)uu * b;
+  const int64_t ooff = (int64_t)blk * b * b + (int64_t)uu * b;
+  float* orow = blocks ? blocks + ooff : nullptr;
 #pragma unroll 4
   for (int v4 = lane; v4 < b / 4; v4 += 32) {
     const float4 a = *reinterpret_cast<const float4*>(arow + 4 * v4);
@@ -876,7 +881,19 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, const
       o.z = ((uu == v + 2) ? 1.0f : 0.0f) - o.z * inv1pmu;
       o.w = ((uu == v + 3) ? 1.0f : 0.0f) - o.w * inv1pmu;
     }
-    *reinterpret_cast<float4*>(orow + v) = o;
+    if (orow) *reinterpret_cast<float4*>(orow + v) = o;
+    if (x16) {   // the 3xF16 twin, exponent 14 (|X_ij|, |Theta_ij| <= 1): hi / lo fp16 planes
+      const __half2 h01 = __floats2half2_rn(o.x * 16384.f, o.y * 16384.f);
+      const __half2 h23 = __floats2half2_rn(o.z * 16384.f, o.w * 16384.f);
+      const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+      const __half2 l01 = __floats2half2_rn(o.x * 16384.f - f01.x, o.y * 16384.f - f01.y);
+      const __half2 l23 = __floats2half2_rn(o.z * 16384.f - f23.x, o.w * 16384.f - f23.y);
+      uint2 hv, lv;
+      hv.x = *reinterpret_cast<const uint32_t*>(&h01); hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+      lv.x = *reinterpret_cast<const uint32_t*>(&l01); lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+      *reinterpret_cast<uint2*>(x16 + ooff + v) = hv;
+      *reinterpret_cast<uint2*>(x16 + x_lo + ooff + v) = lv;
+    }
   }
 }
 
@@ -947,7 +964,8 @@ cudaError_t launch_degrees_grouped(int nb_total, int b, int E, int64_t nnz, cons
 // sorted path (32-bit keys); otherwise every block takes the hashed-tile kernel.
 cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_t nnz, const int64_t* row_ptr,
                             const int32_t* col_idx, const float* edge_val, const float* dv_rsqrt, float mu,
-                            bool raw_theta, float* blocks, void* keys_ws, cudaStream_t s, int* launches) {
+                            bool raw_theta, float* blocks, void* keys_ws, cudaStream_t s, int* launches,
+                            uint16_t* x16, int64_t x_lo, bool skip_f32) {
   uint32_t* keys = reinterpret_cast<uint32_t*>(keys_ws);
   int32_t* overflow = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(keys_ws) + al256((size_t)nnz * 4));
   int2* rng = reinterpret_cast<int2*>(reinterpret_cast<char*>(keys_ws) + al256((size_t)nnz * 4) +
@@ -964,7 +982,8 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
       attr4 = smem;
     }
     k_assemble_rows3<<<dim3(nb, (b + R2_ROWS - 1) / R2_ROWS), R2_NT, smem, s>>>(
-        blk0, b, row_ptr, col_idx, keys, rng, edge_val, dv_rsqrt, 1.0f / (1.0f + mu), raw_theta ? 1 : 0, blocks);
+        blk0, b, row_ptr, col_idx, keys, rng, edge_val, dv_rsqrt, 1.0f / (1.0f + mu), raw_theta ? 1 : 0,
+        (x16 && skip_f32) ? nullptr : blocks, x16, x_lo);
     ++*launches;
     return cudaGetLastError();
   }
@@ -1015,8 +1034,13 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
         overflow);
     *launches += 2;
   }
-  return launch_assemble_tiles(blk0, nb, b, row_ptr, col_idx, edge_val, dv_rsqrt, mu, raw_theta, blocks, overflow, s,
-                               launches);
+  e = launch_assemble_tiles(blk0, nb, b, row_ptr, col_idx, edge_val, dv_rsqrt, mu, raw_theta, blocks, overflow, s,
+                            launches);
+  if (e != cudaSuccess || !x16) return e;
+  // the other assembly paths write fp32 only: split the part's blocks into the twin afterwards
+  const int64_t off = (int64_t)blk0 * b * b;
+  ++*launches;
+  return launch_f16_split(blocks + off, (int64_t)nb * b, b, b, 14, x16 + off, x16 + x_lo + off, b, s);
 }
 
 cudaError_t launch_assemble_tiles(int blk0, int nb, int b, const int64_t* row_ptr, const int32_t* col_idx,
