@@ -398,6 +398,296 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
   CHOL_CLK(61);
 }
 
+// ================================================================== k_cholinv2 (k <= 256)
+// All 16 warps share every phase (no single-warp tile loops on the critical path):
+//   per panel p:  warp 0 factors the diagonal tile (row per lane, the pivot column broadcast
+//                 through a double-buffered shared column -- no shuffle chains) and inverts it,
+//                 D_p = L_pp^-1 (kept beside the tiles);
+//                 all warps: L_ip = A_ip D_p^T (TRSM as a product, i > p), then the trailing
+//                 update A_ij -= L_ip L_jp^T -- 16-row half-tile units, 4 x 4 outputs per lane,
+//                 float4 operand rows (8 LDS.128 per 64 FMA, conflict-free);
+//   triangular inverse: X_ii = D_i, then block columns j = nt-2 .. 0: T_i = sum_{m=j+1..i} X_im L_mj
+//                 into the (then free) D area, X_ij = -T_i D_j -- the LAPACK trtri order, in place.
+constexpr int NT2 = 512, NW2 = NT2 / 32;
+
+// out[r][c] (op)= sum_t A[r][t] * B[c][t] over one 16-row half tile (rows r0 .. r0 + 15); lane = (rg, cg):
+// rows r0 + rg + 4 ii, columns cg + 8 jj.  mode 0: out = acc, 1: out -= acc.  Operands may alias out
+// (every lane computes before any lane stores).
+__device__ __forceinline__ void half_abt(float* out, const float* A, const float* B, int lane, int r0, int mode) {
+  const int rg = lane >> 3, cg = lane & 7;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
+  for (int t = 0; t < TS; t += 4) {
+    float4 a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float4*>(A + (r0 + rg + 4 * i) * LDT + t);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const float4*>(B + (cg + 8 * j) * LDT + t);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[i][j] = fmaf(a[i].x, b[j].x, acc[i][j]);
+        acc[i][j] = fmaf(a[i].y, b[j].y, acc[i][j]);
+        acc[i][j] = fmaf(a[i].z, b[j].z, acc[i][j]);
+        acc[i][j] = fmaf(a[i].w, b[j].w, acc[i][j]);
+      }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float* o = out + (r0 + rg + 4 * i) * LDT + cg + 8 * j;
+      *o = mode ? *o - acc[i][j] : acc[i][j];
+    }
+  __syncwarp();
+}
+
+// acc[r][c] += sum_t A[r][t] * B[t][c] over a 16-row half tile; lane = (rg, cg): rows r0 + rg + 4 ii,
+// columns 4 cg .. 4 cg + 3 (B rows read as float4: 8 lanes cover one 128-byte row)
+__device__ __forceinline__ void half_ab_acc(float (&acc)[4][4], const float* A, const float* B, int lane, int r0) {
+  const int rg = lane >> 3, cg = lane & 7;
+#pragma unroll 2
+  for (int t = 0; t < TS; t += 4) {
+    float4 a[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float4*>(A + (r0 + rg + 4 * i) * LDT + t);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4 bv = *reinterpret_cast<const float4*>(B + (t + u) * LDT + 4 * cg);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float av = u == 0 ? a[i].x : u == 1 ? a[i].y : u == 2 ? a[i].z : a[i].w;
+        acc[i][0] = fmaf(av, bv.x, acc[i][0]);
+        acc[i][1] = fmaf(av, bv.y, acc[i][1]);
+        acc[i][2] = fmaf(av, bv.z, acc[i][2]);
+        acc[i][3] = fmaf(av, bv.w, acc[i][3]);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void half_store(float* out, const float (&acc)[4][4], int lane, int r0, float sign) {
+  const int rg = lane >> 3, cg = lane & 7;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    *reinterpret_cast<float4*>(out + (r0 + rg + 4 * i) * LDT + 4 * cg) =
+        make_float4(sign * acc[i][0], sign * acc[i][1], sign * acc[i][2], sign * acc[i][3]);
+}
+
+// warp: Cholesky of the 32 x 32 tile T in place (lower; zeros written above the diagonal) and its
+// inverse into Dt (lower, zeros above).  Row per lane; the scaled pivot column is published through
+// colbuf (two 32-float buffers, alternating) and read back as float4 broadcasts.
+__device__ void diag_factor(float* T, float* Dt, float* colbuf, int lane, bool& bad) {
+  float a[TS];
+#pragma unroll
+  for (int t = 0; t < TS; ++t) a[t] = T[lane * LDT + t];
+#pragma unroll
+  for (int c = 0; c < TS; ++c) {
+    float d = __shfl_sync(0xffffffffu, a[c], c);
+    if (!(d > 0.f) || !isfinite(d)) {
+      bad = true;
+      d = 1.f;
+    }
+    float inv = rsqrtf(d);
+    inv = inv * fmaf(-0.5f * d * inv, inv, 1.5f);
+    if (lane == c) a[c] = d * inv;
+    if (lane > c) a[c] *= inv;
+    float* cb = colbuf + (c & 1) * TS;
+    cb[lane] = a[c];
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < TS / 4; ++q) {
+      if (4 * q + 3 <= c) continue;   // compile-time (c unrolled): only the quads past the pivot
+      const float4 v = *reinterpret_cast<const float4*>(cb + 4 * q);
+      const float cv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int l = 4 * q + u;
+        if (l > c && lane >= l) a[l] = fmaf(-a[c], cv[u], a[l]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < TS; ++t) T[lane * LDT + t] = (t <= lane) ? a[t] : 0.f;
+  __syncwarp();
+  // D = L^-1: lane r solves row r of I L^-T = column r of L^-1 (four independent FMA chains)
+  float x[TS];
+  const float rd = __frcp_rn(T[lane * LDT + lane]);
+#pragma unroll
+  for (int c = 0; c < TS; ++c) {
+    float y[4] = {c == lane ? 1.f : 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int t = 0; t < c; ++t) y[t & 3] = fmaf(-x[t], T[c * LDT + t], y[t & 3]);
+    x[c] = ((y[0] + y[1]) + (y[2] + y[3])) * __shfl_sync(0xffffffffu, rd, c);
+  }
+#pragma unroll
+  for (int c = 0; c < TS; ++c) Dt[c * LDT + lane] = x[c];   // D[c][lane]; zero above the diagonal
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(NT2, 1) k_cholinv2(int k, const float* __restrict__ G, float* __restrict__ Lout,
+                                                     float* __restrict__ Linv, int32_t* status) {
+  extern __shared__ __align__(16) float sm[];
+  __shared__ float red[NW2];
+  __shared__ __align__(16) float colbuf[2 * TS];
+  __shared__ int s_bad;
+  __shared__ float s_shift;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nt = (k + TS - 1) / TS;
+  const int ntiles = nt * (nt + 1) / 2;
+  const int64_t off = (int64_t)blockIdx.x * k * k;
+  const float* Gb = G + off;
+  float* Lb = Lout ? Lout + off : nullptr;
+  float* Ib = Linv ? Linv + off : nullptr;
+  float* tiles = sm;                                   // [ntiles][TILE] lower tiles
+  float* dti = sm + (int64_t)ntiles * TILE;            // [nt][TILE]: D_p, then the trtri temporaries
+  auto T = [&](int i, int j) { return tiles + (int64_t)tidx(i, j) * TILE; };
+  auto D = [&](int i) { return dti + (int64_t)i * TILE; };
+  CHOL_CLK(0);
+
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (t == 0) {
+      s_bad = 0;
+      float dmax = 0.f;
+      if (attempt == 1)
+        for (int i = 0; i < k; ++i) dmax = fmaxf(dmax, Gb[(int64_t)i * k + i]);
+      s_shift = attempt == 1 ? 1e-5f * dmax : 0.f;
+    }
+    __syncthreads();
+    const float shift = s_shift;
+    // load the lower tiles as float4 rows (identity padding beyond k) and measure max|G - I|
+    float emax = 0.f;
+    for (int task = t; task < ntiles * TS * 8; task += NT2) {
+      const int tl = task >> 8, r = (task >> 3) & 31, c4 = task & 7;
+      int i = 0;
+      while ((i + 1) * (i + 2) / 2 <= tl) ++i;
+      const int j = tl - i * (i + 1) / 2;
+      const int R = i * TS + r, C = j * TS + 4 * c4;
+      float4 v;
+      if (R < k && C < k) {
+        v = *reinterpret_cast<const float4*>(Gb + (int64_t)R * k + C);
+      } else {
+        v = make_float4(R == C ? 1.f : 0.f, R == C + 1 ? 1.f : 0.f, R == C + 2 ? 1.f : 0.f, R == C + 3 ? 1.f : 0.f);
+      }
+      const float e4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (C + u <= R && R < k) {
+          const float e = fabsf(e4[u] - (R == C + u ? 1.f : 0.f));
+          emax = fmaxf(emax, isfinite(e4[u]) ? e : INFINITY);
+        }
+      if (shift != 0.f) {
+        if (R == C) v.x += shift;
+        if (R == C + 1) v.y += shift;
+        if (R == C + 2) v.z += shift;
+        if (R == C + 3) v.w += shift;
+      }
+      *reinterpret_cast<float4*>(tiles + (int64_t)tl * TILE + r * LDT + 4 * c4) = v;
+    }
+    if (attempt == 0) {
+      for (int o = 16; o; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+      if (lane == 0) red[warp] = emax;
+      __syncthreads();
+      float E = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW2; ++w) E = fmaxf(E, red[w]);
+      if (!isfinite(E) && t == 0) hg_flag(status, HGS_NONFINITE);
+      if (t == 0) atomicAdd(&g_chol_dbg[E <= NEAR_ID_TOL ? 0 : 1], 1ull);
+      if (E <= NEAR_ID_TOL) {   // second CholeskyQR pass: first-order factor from the tiles
+        for (int task = t; task < k * (k / 4); task += NT2) {
+          const int r = task / (k / 4), c = 4 * (task % (k / 4));
+          const int i = r / TS, j = c / TS;
+          float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (j <= i) g = *reinterpret_cast<const float4*>(T(i, j) + (r % TS) * LDT + c % TS);
+          const float gv[4] = {g.x, g.y, g.z, g.w};
+          float l[4], li[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int cc = c + u;
+            if (cc > r) { l[u] = 0.f; li[u] = 0.f; }
+            else if (cc == r) { const float e = 0.5f * (gv[u] - 1.f); l[u] = 1.f + e; li[u] = 1.f - e; }
+            else { l[u] = gv[u]; li[u] = -gv[u]; }
+          }
+          if (Lb) *reinterpret_cast<float4*>(Lb + (int64_t)r * k + c) = make_float4(l[0], l[1], l[2], l[3]);
+          if (Ib) *reinterpret_cast<float4*>(Ib + (int64_t)r * k + c) = make_float4(li[0], li[1], li[2], li[3]);
+        }
+        return;
+      }
+    }
+    __syncthreads();
+    CHOL_CLK(1);
+
+    // ---- right-looking Cholesky, panel width 32
+    bool bad = false;
+    for (int p = 0; p < nt; ++p) {
+      CHOL_CLK(2 + 3 * p);
+      if (warp == 0) {
+        diag_factor(T(p, p), D(p), colbuf, lane, bad);
+        if (bad && lane == 0) s_bad = 1;
+      }
+      __syncthreads();
+      CHOL_CLK(3 + 3 * p);
+      const int m = nt - 1 - p;
+      for (int u = warp; u < 2 * m; u += NW2) {   // L_ip = A_ip D_p^T
+        const int i = p + 1 + (u >> 1);
+        half_abt(T(i, p), T(i, p), D(p), lane, (u & 1) * 16, 0);
+      }
+      __syncthreads();
+      CHOL_CLK(4 + 3 * p);
+      const int nu = m * (m + 1);                  // half tiles of the trailing lower tiles
+      for (int u = warp; u < nu; u += NW2) {
+        const int w = u >> 1;
+        int a = 0;
+        while ((a + 1) * (a + 2) / 2 <= w) ++a;
+        const int b = w - a * (a + 1) / 2;
+        const int i = p + 1 + a, j = p + 1 + b;
+        half_abt(T(i, j), T(i, p), T(j, p), lane, (u & 1) * 16, 1);
+      }
+      __syncthreads();
+    }
+    if (!s_bad) break;
+    if (attempt == 1 && t == 0) hg_flag(status, HGS_CHOL_BREAKDOWN);
+    __syncthreads();
+  }
+  CHOL_CLK(40);
+
+  if (Lb) store_lower(Lb, tiles, k, nt, warp, lane);
+  if (!Ib) return;
+  // ---- triangular inverse in place: X_ii = D_i; columns j = nt-2 .. 0
+  for (int task = t; task < nt * TS * 8; task += NT2) {
+    const int i = task >> 8, r = (task >> 3) & 31, c4 = task & 7;
+    *reinterpret_cast<float4*>(T(i, i) + r * LDT + 4 * c4) = *reinterpret_cast<const float4*>(D(i) + r * LDT + 4 * c4);
+  }
+  __syncthreads();
+  CHOL_CLK(41);
+  for (int j = nt - 2; j >= 0; --j) {
+    const int dn = nt - 1 - j;
+    for (int u = warp; u < 2 * dn; u += NW2) {     // T_i = sum_{m=j+1..i} X_im L_mj  -> D area
+      const int i = j + 1 + (u >> 1), r0 = (u & 1) * 16;
+      float acc[4][4] = {};
+      for (int mm = j + 1; mm <= i; ++mm) half_ab_acc(acc, T(i, mm), T(mm, j), lane, r0);
+      half_store(D(i - j - 1), acc, lane, r0, 1.f);
+    }
+    __syncthreads();
+    for (int u = warp; u < 2 * dn; u += NW2) {     // X_ij = -T_i X_jj
+      const int i = j + 1 + (u >> 1), r0 = (u & 1) * 16;
+      float acc[4][4] = {};
+      half_ab_acc(acc, D(i - j - 1), T(j, j), lane, r0);
+      half_store(T(i, j), acc, lane, r0, -1.f);
+    }
+    __syncthreads();
+  }
+  CHOL_CLK(60);
+  store_lower(Ib, tiles, k, nt, warp, lane);
+  CHOL_CLK(61);
+}
+
 }  // namespace
 
 cudaError_t chol_clocks(long long* out) { return cudaMemcpyFromSymbol(out, g_chol_clk, sizeof(g_chol_clk)); }
@@ -430,6 +720,20 @@ cudaError_t launch_cholinv(int nb, int k, const float* G, float* L, float* Linv,
                         : cudaFuncSetAttribute(k_cholinv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr[smem_tiles] = smem;
+  }
+  // k <= 256: the all-warps kernel (HG_CHOL_V1=1: the single-warp-tile kernel below)
+  static const bool v1 = getenv("HG_CHOL_V1") && getenv("HG_CHOL_V1")[0] == '1';
+  if (nt <= 8 && !v1) {
+    const size_t sm2 = (size_t)(nt * (nt + 1) / 2 + nt) * TILE * sizeof(float);
+    static size_t attr2 = 0;
+    if (sm2 > 48 * 1024 && sm2 > attr2) {
+      cudaError_t e = cudaFuncSetAttribute(k_cholinv2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      if (e != cudaSuccess) return e;
+      attr2 = sm2;
+    }
+    k_cholinv2<<<nb, NT2, sm2, s>>>(k, G, L, Linv, status);
+    ++*launches;
+    return cudaGetLastError();
   }
   // opts bit 0 (HG_CHOL_OPTS, default 1): lookahead warp alone on its sub-partition (see the panel loop)
   static const int dbg = getenv("HG_CHOL_OPTS") ? atoi(getenv("HG_CHOL_OPTS")) : 1;
