@@ -165,6 +165,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// One lane of a converged warp (elect.sync): the warp runs its role loop with uniform control flow
+// and only the tcgen05 / TMA instructions sit under this predicate, so their operands stay in
+// uniform registers (under `if (lane == 0)` every UTCHMMA was wrapped in a per-lane R2UR loop and
+// the single issuing thread, not the tensor pipe, bounded the main loop).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // UMMA shared-memory descriptor (sm100 version bits); start, lbo, sbo in bytes
 // (encoded >> 4).  layout: 2 = SWIZZLE_128B (16-byte atoms, 8-row period; the
 // K-major form), 1 = SWIZZLE_128B_BASE32B (32-byte atoms, 4-row period; the
@@ -178,6 +192,18 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)1 << 46;   // descriptor version (sm100)
   d |= (uint64_t)(layout & 7) << 61;
   return d;
+}
+
+// The same descriptor from its two 32-bit words: lo = (start >> 4) | (lbo >> 4) << 16 (the start
+// field advances by bytes >> 4 with no carry inside shared memory), hi = (sbo >> 4) | version | layout.
+__device__ __forceinline__ uint32_t umma_desc_lo(uint32_t saddr, uint32_t lbo) {
+  return ((saddr >> 4) & 0x3FFF) | (((lbo >> 4) & 0x3FFF) << 16);
+}
+__device__ __forceinline__ uint32_t umma_desc_hi(uint32_t sbo, uint32_t layout) {
+  return ((sbo >> 4) & 0x3FFF) | (1u << 14) | ((layout & 7) << 29);
+}
+__device__ __forceinline__ uint64_t umma_desc2(uint32_t lo, uint32_t hi) {
+  return ((uint64_t)hi << 32) | lo;
 }
 
 // tf32 rounding (round-to-nearest, ties away): value stays an fp32 bit pattern.

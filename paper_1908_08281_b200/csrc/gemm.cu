@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (ea.lower && n0 >= m0 + BM) return;   // tile above the diagonal (uniform: before any setup)
   const int num_kb = (ea.K + BK - 1) / BK;
   const int nchunks = (num_kb + C::CHUNK - 1) / C::CHUNK;
+  const bool pre_ab = F16 && ea.a_pre && ea.b_pre;   // no in-kernel split at all
 
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   auto sA_hi = [&](int s) { return base + s * C::STAGE_BYTES; };
@@ -188,12 +189,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t tmem = tmem_base_sh;
 
   if (warp == 8) {
-    // ---------------- TMA producer
-    if (lane == 0) {
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % C::STAGES;
-        const uint32_t ph = (kb / C::STAGES) & 1;
-        if (kb >= C::STAGES) mbar_wait(&empty_bar[s], ph ^ 1);
+    // ---------------- TMA producer: converged warp, one elected lane issues
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % C::STAGES;
+      const uint32_t ph = (kb / C::STAGES) & 1;
+      if (kb >= C::STAGES) mbar_wait(&empty_bar[s], ph ^ 1);
+      if (elect_one()) {
         mbar_arrive_expect_tx(&full_bar[s], C::TX);
         const int k0 = kb * BK;
         if (F16 && ea.a_pre) {
@@ -213,98 +214,73 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int c = 0; c < BN / 32; ++c) tma_load_3d(sB_hi(s) + c * 4096, &tmB, &full_bar[s], n0 + 32 * c, k0, g);
         }
       }
+      __syncwarp();
     }
   } else if (warp == 9) {
-    // ---------------- MMA issuer (single thread)
-    if (F16 && lane == 0) {
-      // 3xF16: both operands K-major SWIZZLE_64B fp16 (64-byte rows, 8-row groups 512 B apart),
-      // hi plane then lo plane; K-step 16 = +32 B in the row
-      const uint32_t idesc = make_idesc_f16(BN);
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % C::STAGES;
-        const uint32_t ph = (kb / C::STAGES) & 1;
-        const int c = kb / C::CHUNK, buf = c & 1;
-        const bool first = (kb % C::CHUNK) == 0;
-        if (first && c >= 2) {
-          mbar_wait(&tempty_bar[buf], ((c >> 1) - 1) & 1);
-          tc_fence_after();
-        }
-        mbar_wait(&conv_bar[s], ph);
+    // ---------------- MMA issuer: the warp stays converged, one elected lane issues (under
+    // `if (lane == 0)` every UTCHMMA sat in a per-lane R2UR loop); descriptors from 32-bit words
+    const uint32_t sbase = smem_u32(base);
+    // 3xF16: both operands K-major SWIZZLE_64B fp16 (64-byte rows, 8-row groups 512 B apart),
+    // hi plane then lo plane; K-step 16 = +32 B in the row.
+    // split in the kernel: 1 KB groups of 8 hi rows + 8 lo rows (SBO 1024, lo at +512);
+    // pre-split (TMA): the hi plane then the lo plane (SBO 512, lo at +R * 64)
+    // 3xTF32, K-major (SWIZZLE_128B): 8-row groups 1024 B apart (SBO), K-step = +32 B in the row.
+    // MN-major (SWIZZLE_128B_BASE32B): 32-element chunks BK*128 B apart (LBO),
+    // 4-row groups 512 B apart (SBO), K-step = +1024 B (8 rows).
+    const uint32_t idesc = F16 ? make_idesc_f16(BN) : make_idesc(BN, ea.a_mn, ea.b_mn);
+    const uint32_t a_lbo = (!F16 && ea.a_mn) ? BK * 128 : 16, b_lbo = (!F16 && ea.b_mn) ? BK * 128 : 16;
+    const uint32_t a_hiw = F16 ? umma_desc_hi(ea.a_pre ? 512 : 1024, 4) : umma_desc_hi(ea.a_mn ? 512 : 1024, ea.a_mn ? 1 : 2);
+    const uint32_t b_hiw = F16 ? umma_desc_hi(ea.b_pre ? 512 : 1024, 4) : umma_desc_hi(ea.b_mn ? 512 : 1024, ea.b_mn ? 1 : 2);
+    // offsets (in 16-byte units) of the lo operands from the hi ones and of a K-step; bytes per B row n
+    const uint32_t a_lo_off = (F16 ? (ea.a_pre ? BM * 64 : 512) : C::A_BYTES) >> 4;
+    const uint32_t b_lo_off = (F16 ? (ea.b_pre ? BN * 64 : 512) : C::B_BYTES) >> 4;
+    const uint32_t a_kstep = (F16 ? 32 : (ea.a_mn ? 1024 : 32)) >> 4, b_kstep = (F16 ? 32 : (ea.b_mn ? 1024 : 32)) >> 4;
+    const uint32_t b_row = (F16 && ea.b_pre) ? 64 : 128;
+    constexpr int KSTEPS = F16 ? BK / 16 : BK / 8;
+    for (int kb = 0; kb < num_kb; ++kb) {
+      const int s = kb % C::STAGES;
+      const uint32_t ph = (kb / C::STAGES) & 1;
+      const int c = kb / C::CHUNK, buf = c & 1;
+      const bool first = (kb % C::CHUNK) == 0;
+      if (first && c >= 2) {
+        mbar_wait(&tempty_bar[buf], ((c >> 1) - 1) & 1);
         tc_fence_after();
-        const int nlo = ea.b_upper ? (max(0, kb * BK - n0) & ~15) : 0;
-        const bool last_in_chunk = (kb % C::CHUNK) == C::CHUNK - 1 || kb == num_kb - 1;
-        if (nlo >= BN) {
-          mma_commit(&empty_bar[s]);
-          if (last_in_chunk) mma_commit(&tfull_bar[buf]);
-          continue;
-        }
-        const uint32_t idk = nlo ? make_idesc_f16(BN - nlo) : idesc;
-        const uint32_t d = tmem + (uint32_t)(buf * BN + nlo);
-        // split in the kernel: 1 KB groups of 8 hi rows + 8 lo rows (SBO 1024, lo at +512);
-        // pre-split (TMA): the hi plane then the lo plane (SBO 512, lo at +R * 64)
-        const uint32_t a0 = smem_u32(sA_hi(s)), b0 = smem_u32(sB_hi(s));
-        const uint32_t ahi = a0, alo = ea.a_pre ? a0 + BM * 64 : a0 + 512, asbo = ea.a_pre ? 512 : 1024;
-        const uint32_t bhi = b0 + (ea.b_pre ? nlo * 64 : nlo * 128);
-        const uint32_t blo = ea.b_pre ? b0 + BN * 64 + nlo * 64 : bhi + 512, bsbo = ea.b_pre ? 512 : 1024;
+      }
+      // both operands pre-split: the TMA-landed tile is the MMA operand as it stands -- wait for
+      // the TMA itself (the epilogue warps only drain)
+      mbar_wait(pre_ab ? &full_bar[s] : &conv_bar[s], ph);
+      tc_fence_after();
+      // b_upper: columns n < kb * BK of this k-block are zero in B -- the MMAs cover
+      // n >= nlo only (N = BN - nlo, TMEM columns and B rows offset by nlo, a multiple of 16);
+      // the drain masks what a chunk never wrote
+      const int nlo = ea.b_upper ? (max(0, kb * BK - n0) & ~15) : 0;
+      const bool last_in_chunk = (kb % C::CHUNK) == C::CHUNK - 1 || kb == num_kb - 1;
+      if (elect_one()) {
+        if (nlo < BN) {
+          const uint32_t idk = nlo ? (F16 ? make_idesc_f16(BN - nlo) : make_idesc(BN - nlo, ea.a_mn, ea.b_mn)) : idesc;
+          const uint32_t d = tmem + (uint32_t)(buf * BN + nlo);
+          const uint32_t st0 = sbase + s * C::STAGE_BYTES;
+          const uint32_t a0 = umma_desc_lo(st0, a_lbo);
+          const uint32_t b0 = umma_desc_lo(st0 + (F16 ? 1 : 2) * C::A_BYTES + nlo * b_row, b_lbo);
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          const uint64_t dah = umma_desc(ahi + kk * 32, 16, asbo, 4);
-          const uint64_t dal = umma_desc(alo + kk * 32, 16, asbo, 4);
-          const uint64_t dbh = umma_desc(bhi + kk * 32, 16, bsbo, 4);
-          const uint64_t dbl = umma_desc(blo + kk * 32, 16, bsbo, 4);
-          mma_f16(d, dal, dbh, idk, (first && kk == 0) ? 0u : 1u);
-          mma_f16(d, dah, dbl, idk, 1);
-          mma_f16(d, dah, dbh, idk, 1);
+          for (int kk = 0; kk < KSTEPS; ++kk) {
+            const uint64_t dah = umma_desc2(a0 + kk * a_kstep, a_hiw), dal = umma_desc2(a0 + a_lo_off + kk * a_kstep, a_hiw);
+            const uint64_t dbh = umma_desc2(b0 + kk * b_kstep, b_hiw), dbl = umma_desc2(b0 + b_lo_off + kk * b_kstep, b_hiw);
+            if constexpr (F16) {
+              mma_f16(d, dal, dbh, idk, (first && kk == 0) ? 0u : 1u);
+              mma_f16(d, dah, dbl, idk, 1);
+              mma_f16(d, dah, dbh, idk, 1);
+            } else {
+              mma_tf32(d, dal, dbh, idk, (first && kk == 0) ? 0u : 1u);
+              mma_tf32(d, dah, dbl, idk, 1);
+              mma_tf32(d, dah, dbh, idk, 1);
+            }
+          }
         }
         mma_commit(&empty_bar[s]);
         if (last_in_chunk) mma_commit(&tfull_bar[buf]);
       }
-    } else if (!F16 && lane == 0) {
-      const uint32_t idesc = make_idesc(BN, ea.a_mn, ea.b_mn);
-      // K-major (SWIZZLE_128B): 8-row groups 1024 B apart (SBO), K-step = +32 B in the row.
-      // MN-major (SWIZZLE_128B_BASE32B): 32-element chunks BK*128 B apart (LBO),
-      // 4-row groups 512 B apart (SBO), K-step = +1024 B (8 rows).
-      const uint32_t a_lbo = ea.a_mn ? BK * 128 : 16, b_lbo = ea.b_mn ? BK * 128 : 16;
-      const uint32_t a_sbo = ea.a_mn ? 512 : 1024, b_sbo = ea.b_mn ? 512 : 1024;
-      const uint32_t a_lay = ea.a_mn ? 1 : 2, b_lay = ea.b_mn ? 1 : 2;
-      const uint32_t a_kstep = ea.a_mn ? 1024 : 32, b_kstep = ea.b_mn ? 1024 : 32;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % C::STAGES;
-        const uint32_t ph = (kb / C::STAGES) & 1;
-        const int c = kb / C::CHUNK, buf = c & 1;
-        const bool first = (kb % C::CHUNK) == 0;
-        if (first && c >= 2) {
-          mbar_wait(&tempty_bar[buf], ((c >> 1) - 1) & 1);
-          tc_fence_after();
-        }
-        mbar_wait(&conv_bar[s], ph);
-        tc_fence_after();
-        // b_upper: columns n < kb * BK of this k-block are zero in B -- the MMAs cover
-        // n >= nlo only (N = BN - nlo, TMEM columns and B rows offset by nlo; K-major B rows
-        // are 128 B, nlo a multiple of 16); the drain masks what a chunk never wrote
-        const int nlo = ea.b_upper ? (max(0, kb * BK - n0) & ~15) : 0;
-        if (nlo >= BN) {
-          mma_commit(&empty_bar[s]);
-          if ((kb % C::CHUNK) == C::CHUNK - 1 || kb == num_kb - 1) mma_commit(&tfull_bar[buf]);
-          continue;
-        }
-        const uint32_t idk = nlo ? make_idesc(BN - nlo, ea.a_mn, ea.b_mn) : idesc;
-        const uint32_t d = tmem + (uint32_t)(buf * BN + nlo);
-        const uint32_t ahi = smem_u32(sA_hi(s)), alo = smem_u32(sA_lo(s));
-        const uint32_t bhi = smem_u32(sB_hi(s)) + nlo * 128, blo = smem_u32(sB_lo(s)) + nlo * 128;
-#pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t dah = umma_desc(ahi + kk * a_kstep, a_lbo, a_sbo, a_lay);
-          const uint64_t dal = umma_desc(alo + kk * a_kstep, a_lbo, a_sbo, a_lay);
-          const uint64_t dbh = umma_desc(bhi + kk * b_kstep, b_lbo, b_sbo, b_lay);
-          const uint64_t dbl = umma_desc(blo + kk * b_kstep, b_lbo, b_sbo, b_lay);
-          mma_tf32(d, dal, dbh, idk, (first && kk == 0) ? 0u : 1u);
-          mma_tf32(d, dah, dbl, idk, 1);
-          mma_tf32(d, dah, dbh, idk, 1);
-        }
-        mma_commit(&empty_bar[s]);
-        if ((kb % C::CHUNK) == C::CHUNK - 1 || kb == num_kb - 1) mma_commit(&tfull_bar[buf]);
-      }
+      __syncwarp();
     }
   } else {
     // ---------------- warps 0-7: tf32 hi/lo split, chunk drains, epilogue
@@ -332,7 +308,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (lane == 0) mbar_arrive(&tempty_bar[buf]);
     };
     int drained = 0;
-    for (int kb = 0; kb < num_kb; ++kb) {
+    for (int kb = pre_ab ? num_kb : 0; kb < num_kb; ++kb) {
       const int s = kb % C::STAGES;
       const uint32_t ph = (kb / C::STAGES) & 1;
       mbar_wait(&full_bar[s], ph);
