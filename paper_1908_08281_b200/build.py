@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhgrsvd.so")
 LIB_CHECK = os.path.join(HERE, "libhgrsvd_check.so")   # -DHG_BOUNDS_CHECK (device index checks)
-SOURCES = ["abi.cu", "gemm.cu", "theta.cu", "philox.cu", "chol.cu", "jacobi.cu", "jacobi_blk.cu", "finalize.cu", "cg.cu", "schur.cu", "eig.cu"]
+SOURCES = ["abi.cu", "gemm.cu", "theta.cu", "philox.cu", "chol.cu", "jacobi.cu", "jacobi_blk.cu", "finalize.cu", "cg.cu", "schur.cu", "eig.cu", "apply.cu"]
 HEADERS = ["common.cuh", "gemm.cuh", "kernels.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-warn-spills"]

@@ -116,7 +116,7 @@ struct Layout {
   size_t de = 0, eval = 0, dvr = 0, keys = 0, blocks = 0, P[4] = {0, 0, 0, 0}, Ut = 0, Vt = 0;
   size_t X16 = 0, P16[4] = {0, 0, 0, 0};   // 3xF16 pre-split twins of the blocks and the panels (hi | lo planes)
   size_t G = 0, L = 0, Linv = 0, Wf = 0, Uk = 0, work = 0, eig = 0, sig = 0, sigma = 0, sigl = 0, rs = 0, Z = 0,
-         Yp = 0, Fp = 0, status = 0;
+         Yp = 0, Fp = 0, amax = 0, status = 0;
   size_t h_rowptr = 0, h_col = 0, h_w = 0, h_Y = 0, h_F = 0;
   size_t total = 0;
 };
@@ -157,6 +157,7 @@ Layout layout(int64_t N, int64_t E, int64_t nnz, int64_t b, int64_t k, int64_t T
     L.Yp = take(4 * N * T4);
     L.Fp = take(4 * N * T4);
   }
+  L.amax = take(apply_fused_amax_bytes((int)nb));   // fused apply: per-block max|Y_i|, max|U_i|, max|V_i|
   L.status = take(4);
   L.h_rowptr = take(8 * (N + 1));
   L.h_col = take(4 * (nnz > 0 ? nnz : 1));
@@ -370,6 +371,8 @@ struct Bufs {
   float *G, *L, *Linv, *Wf, *Uk, *work, *eig, *rs, *Z, *Yp, *Fp;
   double* sig;
   int32_t* perm;
+  uint32_t* amax;   // fused apply: [3][amax_ld] exponent words, this part's first block at [0]
+  int amax_ld;
 };
 Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k, int T) {
   Bufs B;
@@ -392,6 +395,8 @@ Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k,
   double* sig0 = at<double>(ws, Lo.sig);
   B.sig = sig0 + k1;
   B.perm = reinterpret_cast<int32_t*>(sig0 + (int64_t)nb_total * k) + k1;
+  B.amax = at<uint32_t>(ws, Lo.amax) + blk0;
+  B.amax_ld = nb_total;
   return B;
 }
 
@@ -560,7 +565,7 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
 // an oversampled factorisation truncated to rank k).
 hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb, int b, int k, const float* Y, int T,
                     float scale, float* F, int32_t* st, const Bufs& Bf, cudaStream_t s, bool simt,
-                    float woodbury_opm = 0.f, int ldk = 0, bool uv_bk = false) {
+                    float woodbury_opm = 0.f, int ldk = 0, bool uv_bk = false, bool uv_unit = false) {
   if (T == 0) return HG_OK;
   if (ldk < k) ldk = k;
   if (T % 4) {   // the GEMMs need 16-byte row pitches: run on zero-padded [rows][T4] copies of Y and F
@@ -572,12 +577,28 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
     Bufs B2 = Bf;
     B2.Yp = nullptr;
     B2.Fp = nullptr;
-    HG_TRY(run_apply(Ut, sigma, Vt, nb, b, k, Bf.Yp, T4, scale, Bf.Fp, st, B2, s, simt, woodbury_opm, ldk, uv_bk));
+    HG_TRY(run_apply(Ut, sigma, Vt, nb, b, k, Bf.Yp, T4, scale, Bf.Fp, st, B2, s, simt, woodbury_opm, ldk, uv_bk, uv_unit));
     HG_CU(cudaMemcpy2DAsync(F, (size_t)T * 4, Bf.Fp, (size_t)T4 * 4, (size_t)T * 4, rows, cudaMemcpyDeviceToDevice, s),
           "unpad F");
     return HG_OK;
   }
   const bool wb = woodbury_opm > 0.f;
+  // The fused kernel (apply.cu): c / sigma, both products and the k x T intermediate in one launch;
+  // U, V go in as 3xF16 twins (panel-twin scratch, free after the rSVD).  uv_unit: the factors come
+  // from this library's finalize (unit vectors, exponent 14); otherwise their maxima are measured.
+  if (!wb && !simt && !uv_bk && Bf.P16[0] && apply_fused_supported(b, k, ldk, T, Ut, Vt, Y, F)) {
+    {
+      ProfScope ps(ST_INV_SIGMA, s);   // apply prep: exponents and twins
+      HG_CU(launch_apply_prep(Ut, Vt, nb, b, k, ldk, Y, T, Bf.P16[0], Bf.P16[1], Bf.p16_lo, Bf.amax, Bf.amax_ld,
+                              uv_unit, s, &g_launches),
+            "apply prep");
+    }
+    ProfScope ps(ST_GEMM_APPLY, s);
+    HG_CU(launch_apply_fused(sigma, nb, b, k, ldk, Y, T, scale, F, st, Bf.P16[0], Bf.P16[1], Bf.p16_lo, Bf.amax,
+                             Bf.amax_ld, s, &g_launches),
+          "fused apply");
+    return HG_OK;
+  }
   float* rs = Bf.rs;
   float* Z = Bf.Z;
   {
@@ -1096,7 +1117,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     if (cps) HG_CU(cudaStreamWaitEvent(ps[pt], ev_y[pt], 0), "wait Y");
     HG_TRY(run_apply(Ut + kb, sigma + (int64_t)(blk0 - soff) * l, Vt + kb, nbp, b, k, T > 0 ? Y + (int64_t)blk0 * b * T : Y, T,
                      mu / (1.0f + mu), T > 0 ? F + (int64_t)blk0 * b * T : F, st, Bf, ps[pt], simt,
-                     woodbury ? 1.0f + mu : 0.f, l));
+                     woodbury ? 1.0f + mu : 0.f, l, false, true));
     if (io.F_host && T > 0)
       HG_CU(cudaMemcpyAsync(io.F_host + (int64_t)blk0 * b * T, F + (int64_t)blk0 * b * T,
                             sizeof(float) * (size_t)nbp * b * T, cudaMemcpyDeviceToHost, ps[pt]),

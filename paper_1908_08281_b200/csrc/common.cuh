@@ -5,6 +5,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 #include <cstdio>
 
@@ -211,4 +212,27 @@ __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
+}
+
+// 3xF16 split of 4 consecutive k of one row into the K-major SWIZZLE_64B hi | lo planes:
+// row r is 64 bytes (32 fp16), 16-byte unit u = kq / 2 sits at u ^ ((r >> 1) & 3).
+__device__ __forceinline__ void f16_split_store(uint8_t* hi, uint8_t* lo, int r, int kq, float4 x) {
+  const __half2 h01 = __floats2half2_rn(x.x, x.y), h23 = __floats2half2_rn(x.z, x.w);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn(x.x - f01.x, x.y - f01.y), l23 = __floats2half2_rn(x.z - f23.x, x.w - f23.y);
+  const int off = r * 64 + ((((kq >> 1) ^ (r >> 1)) & 3) << 4) + ((kq & 1) << 3);
+  uint2 hv, lv;
+  hv.x = *reinterpret_cast<const uint32_t*>(&h01); hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+  lv.x = *reinterpret_cast<const uint32_t*>(&l01); lv.y = *reinterpret_cast<const uint32_t*>(&l23);
+  *reinterpret_cast<uint2*>(hi + off) = hv;
+  *reinterpret_cast<uint2*>(lo + off) = lv;
+}
+
+__device__ __forceinline__ void split4(float4 x, float sc, uint2& hv, uint2& lv) {
+  x = make_float4(x.x * sc, x.y * sc, x.z * sc, x.w * sc);
+  const __half2 h01 = __floats2half2_rn(x.x, x.y), h23 = __floats2half2_rn(x.z, x.w);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn(x.x - f01.x, x.y - f01.y), l23 = __floats2half2_rn(x.z - f23.x, x.w - f23.y);
+  hv.x = *reinterpret_cast<const uint32_t*>(&h01); hv.y = *reinterpret_cast<const uint32_t*>(&h23);
+  lv.x = *reinterpret_cast<const uint32_t*>(&l01); lv.y = *reinterpret_cast<const uint32_t*>(&l23);
 }

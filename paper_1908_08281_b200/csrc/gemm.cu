@@ -105,29 +105,6 @@ __device__ __forceinline__ uint32_t make_idesc_f16(int bn) {
   return (1u << 4) | ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
-// 3xF16 split of 4 consecutive k of one row into the K-major SWIZZLE_64B hi | lo planes:
-// row r is 64 bytes (32 fp16), 16-byte unit u = kq / 2 sits at u ^ ((r >> 1) & 3).
-__device__ __forceinline__ void f16_split_store(uint8_t* hi, uint8_t* lo, int r, int kq, float4 x) {
-  const __half2 h01 = __floats2half2_rn(x.x, x.y), h23 = __floats2half2_rn(x.z, x.w);
-  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-  const __half2 l01 = __floats2half2_rn(x.x - f01.x, x.y - f01.y), l23 = __floats2half2_rn(x.z - f23.x, x.w - f23.y);
-  const int off = r * 64 + ((((kq >> 1) ^ (r >> 1)) & 3) << 4) + ((kq & 1) << 3);
-  uint2 hv, lv;
-  hv.x = *reinterpret_cast<const uint32_t*>(&h01); hv.y = *reinterpret_cast<const uint32_t*>(&h23);
-  lv.x = *reinterpret_cast<const uint32_t*>(&l01); lv.y = *reinterpret_cast<const uint32_t*>(&l23);
-  *reinterpret_cast<uint2*>(hi + off) = hv;
-  *reinterpret_cast<uint2*>(lo + off) = lv;
-}
-
-__device__ __forceinline__ void split4(float4 x, float sc, uint2& hv, uint2& lv) {
-  x = make_float4(x.x * sc, x.y * sc, x.z * sc, x.w * sc);
-  const __half2 h01 = __floats2half2_rn(x.x, x.y), h23 = __floats2half2_rn(x.z, x.w);
-  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-  const __half2 l01 = __floats2half2_rn(x.x - f01.x, x.y - f01.y), l23 = __floats2half2_rn(x.z - f23.x, x.w - f23.y);
-  hv.x = *reinterpret_cast<const uint32_t*>(&h01); hv.y = *reinterpret_cast<const uint32_t*>(&h23);
-  lv.x = *reinterpret_cast<const uint32_t*>(&l01); lv.y = *reinterpret_cast<const uint32_t*>(&l23);
-}
-
 __device__ __forceinline__ float trunc_lo(float x) {   // x - trunc_tf32(x), exact in fp32
   return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
@@ -681,6 +658,15 @@ cudaError_t launch_tc(const GemmDesc& g, const EpiArgs& ea, cudaStream_t stream)
 }
 
 }  // namespace
+
+bool hg_tma_map_f32(CUtensorMap* m, const float* ptr, int64_t inner, int64_t outer, int64_t batch, int64_t ld,
+                    int64_t bs, int box_outer, bool mn_major, bool f16_split) {
+  return make_map(m, ptr, inner, outer, batch, ld, bs, box_outer, mn_major, f16_split);
+}
+bool hg_tma_map_pair(CUtensorMap* m, const uint16_t* hi, int64_t K, int64_t rows, int64_t batch, int64_t ld,
+                     int64_t bs, int64_t lo_off, int box_rows) {
+  return make_map_pair(m, hi, K, rows, batch, ld, bs, lo_off, box_rows);
+}
 
 static int prec_env() {   // HG_GEMM_PREC=f16 | tf32: the precision of GEMMs that leave GemmDesc::prec = -1
   static const int p = [] {
