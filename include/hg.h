@@ -328,17 +328,18 @@ hg_status hg_gemm_ex(int32_t M, int32_t N, int32_t K, int32_t batch, const float
                      int64_t ldd, int64_t sd, float alpha, const float* rs, int64_t srs, const float* cs,
                      int64_t scs, uint32_t flags, int32_t prec, int32_t a_exp, int32_t b_exp, hg_stream_t stream);
 
-/* Verification exports of the 3xF16 pre-split operand path.  hg_f16_split: hi[r*ldo + c] =
- * fp16_rn(2^exp x[r*ld + c]), lo = fp16_rn(2^exp x - hi) (fp16 bit patterns; cols % 8 == 0).
- * hg_gemm_f16pre: D = alpha A B with both operands pre-split and K-major: A_g(m,kk) =
- * 2^-a_exp (A16[g*sa + m*lda + kk] + A16[a_lo + g*sa + m*lda + kk]) (likewise B with n for m);
- * lda, ldb, sa, sb, a_lo, b_lo multiples of 8 (fp16 elements). */
-hg_status hg_f16_split(const float* x, int64_t rows, int32_t cols, int64_t ld, int32_t exp, uint16_t* hi,
-                       uint16_t* lo, int64_t ldo, hg_stream_t stream);
-hg_status hg_gemm_f16pre(int32_t M, int32_t N, int32_t K, int32_t batch, const uint16_t* A16, int64_t a_lo,
-                         int64_t lda, int64_t sa, int32_t a_exp, const uint16_t* B16, int64_t b_lo, int64_t ldb,
-                         int64_t sb, int32_t b_exp, float* D, int32_t d_trans, int64_t ldd, int64_t sd, float alpha,
-                         hg_stream_t stream);
+/* Verification exports of the 3xF16 twin-operand path.  hg_f16_split: out16 = the twin of the dense
+ * rows x cols fp32 matrix x (row pitch ld; cols % 32 == 0): element o = r*cols + c has its hi half
+ * fp16_rn(2^exp x) at out16[2 o - (o % 32)] and its lo half fp16_rn(2^exp x - hi) 32 entries further
+ * (fp16 bit patterns; out16 holds 2 rows cols entries) -- per 32 elements the 32 hi then the 32 lo, so a
+ * 64 x R TMA box lands as the tensor core's 128-byte operand rows.
+ * hg_gemm_f16pre: D = alpha 2^-(a_exp + b_exp) A B with both operands given as twins of the K-major
+ * arrays A[g*sa + m*lda + kk], B[g*sb + n*ldb + kk]; lda, ldb, sa, sb multiples of 32. */
+hg_status hg_f16_split(const float* x, int64_t rows, int32_t cols, int64_t ld, int32_t exp, uint16_t* out16,
+                       hg_stream_t stream);
+hg_status hg_gemm_f16pre(int32_t M, int32_t N, int32_t K, int32_t batch, const uint16_t* A16, int64_t lda,
+                         int64_t sa, int32_t a_exp, const uint16_t* B16, int64_t ldb, int64_t sb, int32_t b_exp,
+                         float* D, int32_t d_trans, int64_t ldd, int64_t sd, float alpha, hg_stream_t stream);
 
 /* Stage profiler (tracing).  hg_profile_enable(1) makes the calls on this host
  * thread bracket each stage launch with CUDA events on its stream (off by

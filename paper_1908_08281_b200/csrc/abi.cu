@@ -265,13 +265,13 @@ struct Rsvd {
     if (X16 && !f16) return fail(HG_ERR_INVALID, "internal: power product operand panel without a 3xF16 twin");
     if (f16) {   // both operands pre-split: no in-kernel split, kind::f16 at twice the tf32 rate
       g.prec = 1;
-      g.A16 = X16; g.a_lo = x_lo; g.a_exp = 14;
-      g.B16 = tw->h[i]; g.b_lo = tw->lo; g.b_exp = tw->exp[i];
+      g.A16 = X16; g.a_exp = 14;
+      g.B16 = tw->h[i]; g.b_exp = tw->exp[i];
     }
     if (o >= 0) {
       tw->exp[o] = kNoTwin;
       if (f16) {   // |(X P)_ij| <= cb(P); the column norms do not grow either
-        g.D16 = tw->h[o]; g.d_lo = tw->lo; g.d_exp = f16_exp(tw->cb[i]);
+        g.D16 = tw->h[o]; g.d_exp = f16_exp(tw->cb[i]);
         tw->exp[o] = g.d_exp;
         tw->cb[o] = tw->cb[i];
       }
@@ -291,7 +291,7 @@ struct Rsvd {
     const int i = tw ? tw->find(P_t) : -1;
     if (tw && tw->valid(i) && !simt) {
       g.prec = 1;
-      g.A16 = g.B16 = tw->h[i]; g.a_lo = g.b_lo = tw->lo; g.a_exp = g.b_exp = tw->exp[i];
+      g.A16 = g.B16 = tw->h[i]; g.a_exp = g.b_exp = tw->exp[i];
     }
     return gemm(g, s, simt, "Gram P^T P", ST_GEMM_GRAM);
   }
@@ -309,7 +309,7 @@ struct Rsvd {
     if (o >= 0) {   // the orthonormalised panel's twin for the next power product / Gram: ||q_j|| <= 2
       tw->exp[o] = kNoTwin;
       if (!simt) {
-        g.D16 = tw->h[o]; g.d_lo = tw->lo; g.d_exp = f16_exp(2.f);
+        g.D16 = tw->h[o]; g.d_exp = f16_exp(2.f);
         tw->exp[o] = g.d_exp;
         tw->cb[o] = 2.f;
       }
@@ -333,7 +333,7 @@ static int qr_passes_env() {   // read per call (tests switch it)
 // HG_GEMM_F16=0 (read per call: tests switch it); the pre-split planes need b % 8 == 0.
 static bool f16_on(int b, bool simt) {
   const char* v = getenv("HG_GEMM_F16");
-  return !simt && b % 8 == 0 && !(v && v[0] == '0');
+  return !simt && b % 32 == 0 && !(v && v[0] == '0');   // twins: rows of whole 32-element groups (tw_off)
 }
 
 // Jacobi preconditioner (eig.cu) on unless HG_JACOBI_PRE=0 (read per call: tests switch it)
@@ -366,7 +366,7 @@ hg_status cholqr(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* L
 // problem (parts run concurrently on different streams; see solve_impl).
 struct Bufs {
   float* P[4];
-  uint16_t* P16[4];   // pre-split twins of P (hi plane; lo plane p16_lo fp16 elements further)
+  uint16_t* P16[4];   // 3xF16 twins of P (common.cuh tw_off layout: 2 fp16 per element)
   int64_t p16_lo;
   float *G, *L, *Linv, *Wf, *Uk, *work, *eig, *rs, *Z, *Yp, *Fp;
   double* sig;
@@ -378,7 +378,7 @@ Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k,
   Bufs B;
   const int64_t kb = (int64_t)blk0 * k * b, kk = (int64_t)blk0 * k * k, k1 = (int64_t)blk0 * k;
   for (int i = 0; i < 4; ++i) B.P[i] = at<float>(ws, Lo.P[i]) + kb;
-  for (int i = 0; i < 4; ++i) B.P16[i] = at<uint16_t>(ws, Lo.P16[i]) + kb;
+  for (int i = 0; i < 4; ++i) B.P16[i] = at<uint16_t>(ws, Lo.P16[i]) + 2 * kb;   // twin of the part's panels (tw_off)
   B.p16_lo = (int64_t)nb_total * k * b;
   B.G = at<float>(ws, Lo.G) + kk;
   B.L = at<float>(ws, Lo.L) + kk;
@@ -589,12 +589,12 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
   if (!wb && !simt && !uv_bk && Bf.P16[0] && apply_fused_supported(b, k, ldk, T, Ut, Vt, Y, F)) {
     {
       ProfScope ps(ST_INV_SIGMA, s);   // apply prep: exponents and twins
-      HG_CU(launch_apply_prep(Ut, Vt, nb, b, k, ldk, Y, T, Bf.P16[0], Bf.P16[1], Bf.p16_lo, Bf.amax, Bf.amax_ld,
+      HG_CU(launch_apply_prep(Ut, Vt, nb, b, k, ldk, Y, T, Bf.P16[0], Bf.P16[1], Bf.amax, Bf.amax_ld,
                               uv_unit, s, &g_launches),
             "apply prep");
     }
     ProfScope ps(ST_GEMM_APPLY, s);
-    HG_CU(launch_apply_fused(sigma, nb, b, k, ldk, Y, T, scale, F, st, Bf.P16[0], Bf.P16[1], Bf.p16_lo, Bf.amax,
+    HG_CU(launch_apply_fused(sigma, nb, b, k, ldk, Y, T, scale, F, st, Bf.P16[0], Bf.P16[1], Bf.amax,
                              Bf.amax_ld, s, &g_launches),
           "fused apply");
     return HG_OK;
@@ -839,7 +839,7 @@ hg_status hg_block_rsvd_ex(const float* blocks, int32_t nb, int32_t b, int32_t k
   uint16_t* x16 = ((flags & HG_X_UNIT) && !general && f16_on(b, simt)) ? at<uint16_t>(ws, Lo.X16) : nullptr;
   const int64_t x_lo = (int64_t)nb * b * b;
   if (x16) {
-    HG_CU(launch_f16_split(blocks, (int64_t)nb * b, b, b, 14, x16, x16 + x_lo, b, s), "blocks split");
+    HG_CU(launch_f16_split(blocks, (int64_t)nb * b, b, b, 14, x16, s), "blocks split");
     ++g_launches;
   }
   if (p == 0)
@@ -1100,7 +1100,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     uint16_t* x16 = f16_on(b, simt) ? at<uint16_t>(ws, Lo.X16) : nullptr;
     const int64_t x_lo = (int64_t)nb * b * b;
     HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[pt], x16, x_lo));
-    if (x16) x16 += (int64_t)blk0 * b * b;
+    if (x16) x16 += 2 * (int64_t)blk0 * b * b;
     // HG_JACOBI_WIDE = bitmask of parts whose Jacobi runs on 64-row cluster CTAs (twice the SMs
     // per block: a shorter per-block latency for that part).  Off by default in BOTH entries: the
     // cluster width changes the order of the Jacobi's Gram partial sums, so a wide part's bits
@@ -1973,29 +1973,28 @@ hg_status hg_gemm_ex(int32_t M, int32_t N, int32_t K, int32_t batch, const float
   return gemm(g, reinterpret_cast<cudaStream_t>(stream), (flags & HG_GEMM_SIMT) != 0, "hg_gemm_ex");
 }
 
-hg_status hg_f16_split(const float* x, int64_t rows, int32_t cols, int64_t ld, int32_t exp, uint16_t* hi,
-                       uint16_t* lo, int64_t ldo, hg_stream_t stream) {
+hg_status hg_f16_split(const float* x, int64_t rows, int32_t cols, int64_t ld, int32_t exp, uint16_t* out16,
+                       hg_stream_t stream) {
   g_err.clear();
   g_launches = 0;
-  if (!x || !hi || !lo) return fail(HG_ERR_INVALID, "NULL pointer argument");
-  if (rows < 0 || cols < 0 || (cols & 7) || (ld & 3) || (ldo & 7) || ld < cols || ldo < cols)
-    return fail(HG_ERR_INVALID, "need cols %% 8 == 0, ld %% 4 == 0, ldo %% 8 == 0, ld, ldo >= cols");
-  HG_CU(launch_f16_split(x, rows, cols, ld, exp, hi, lo, ldo, reinterpret_cast<cudaStream_t>(stream)), "f16 split");
+  if (!x || !out16) return fail(HG_ERR_INVALID, "NULL pointer argument");
+  if (rows < 0 || cols < 0 || (cols & 31) || (ld & 3) || ld < cols)
+    return fail(HG_ERR_INVALID, "need cols %% 32 == 0, ld %% 4 == 0, ld >= cols");
+  HG_CU(launch_f16_split(x, rows, cols, ld, exp, out16, reinterpret_cast<cudaStream_t>(stream)), "f16 split");
   ++g_launches;
   return HG_OK;
 }
 
-hg_status hg_gemm_f16pre(int32_t M, int32_t N, int32_t K, int32_t batch, const uint16_t* A16, int64_t a_lo,
-                         int64_t lda, int64_t sa, int32_t a_exp, const uint16_t* B16, int64_t b_lo, int64_t ldb,
-                         int64_t sb, int32_t b_exp, float* D, int32_t d_trans, int64_t ldd, int64_t sd, float alpha,
-                         hg_stream_t stream) {
+hg_status hg_gemm_f16pre(int32_t M, int32_t N, int32_t K, int32_t batch, const uint16_t* A16, int64_t lda,
+                         int64_t sa, int32_t a_exp, const uint16_t* B16, int64_t ldb, int64_t sb, int32_t b_exp,
+                         float* D, int32_t d_trans, int64_t ldd, int64_t sd, float alpha, hg_stream_t stream) {
   g_err.clear();
   g_launches = 0;
   if (!A16 || !B16 || !D) return fail(HG_ERR_INVALID, "NULL pointer argument");
   GemmDesc g;
   g.M = M; g.N = N; g.K = K; g.batch = batch;
-  g.A16 = A16; g.a_lo = a_lo; g.lda = lda; g.sa = sa; g.a_exp = a_exp;
-  g.B16 = B16; g.b_lo = b_lo; g.ldb = ldb; g.sb = sb; g.b_exp = b_exp;
+  g.A16 = A16; g.lda = lda; g.sa = sa; g.a_exp = a_exp;
+  g.B16 = B16; g.ldb = ldb; g.sb = sb; g.b_exp = b_exp;
   g.D = D; g.d_trans = d_trans != 0; g.ldd = ldd; g.sd = sd;
   g.alpha = alpha;
   g.prec = 1;

@@ -9,12 +9,14 @@
 //      as the K-major B operand of the second product -- the k x T intermediate never leaves the SM
 //   3. F_i[m-tile] = V_i[m-tile] Z    (128 x 128, K = k) for the b/128 row tiles, TMEM double-buffered
 //      so tile mt's drain + store overlaps tile mt+1's MMAs.
-// Operands: U as the pre-split fp16 twin of Ut [k][b] (K-major B of product 1), V as the pre-split
-// twin of V [b][k] (K-major A of product 2) -- both TMA-loaded as MMA operands as they stand; Y tiles
-// land as fp32 [32 rows][32 columns] chunks and are split in place by the 8 epilogue warps (the
-// transposing split of gemm.cu's MN-major path).  Exponents: 2^e_y from max|Y_i| per block (k_absmax,
-// so results do not depend on the part / shard split), 2^14 for orthonormal U, V inside hg_solve
-// (from max|U_i|, max|V_i| for caller-provided factors).
+// Operands: U as the 3xF16 twin (common.cuh tw_off) of Ut [k][b] (K-major B of product 1), V as the twin
+// of V [b][k] (K-major operand of product 2) -- both TMA-loaded into 128-byte SWIZZLE_128B rows
+// [hi 32 k | lo 32 k] and read by the MMAs as they stand; Y tiles land as fp32 [32 rows][32 columns]
+// chunks and are split in place into the same row layout by the 8 epilogue warps (a transposing split);
+// Z is written in that layout too.  (64-byte SWIZZLE_64B rows halve the tensor core's operand fetch
+// rate, gemm.cu.)  Exponents: 2^e_y from max|Y_i| per block (k_absmax, so results do not depend on the
+// part / shard split), 2^14 for orthonormal U, V inside hg_solve (from max|U_i|, max|V_i| for
+// caller-provided factors).
 // Precision is that of the other 3xF16 products: 22 significant bits per operand, fp32 accumulation
 // in chunks of 24 MMAs summed in registers.
 #include <cuda.h>
@@ -29,27 +31,27 @@
 
 bool hg_tma_map_f32(CUtensorMap* m, const float* ptr, int64_t inner, int64_t outer, int64_t batch, int64_t ld,
                     int64_t bs, int box_outer, bool mn_major, bool f16_split);
-bool hg_tma_map_pair(CUtensorMap* m, const uint16_t* hi, int64_t K, int64_t rows, int64_t batch, int64_t ld,
-                     int64_t bs, int64_t lo_off, int box_rows);
+bool hg_tma_map_twin(CUtensorMap* m, const uint16_t* tw, int64_t K, int64_t rows, int64_t batch, int64_t ld,
+                     int64_t bs, int box_rows);
 
 namespace {
 
 constexpr int TN = 128;   // RHS columns per CTA = MMA M of product 1, N of product 2
-constexpr int BK = 32;    // K elements per pipeline stage (64-byte fp16 rows, SWIZZLE_64B)
+constexpr int BK = 32;    // K elements per pipeline stage (128-byte rows: 32 hi | 32 lo fp16, SWIZZLE_128B)
 constexpr int NEPI = 256, NTHREADS = NEPI + 64;
-constexpr int S1 = 3, S2 = 3;
+constexpr int S1 = 4, S2 = 4;   // both rings are latency-bound: as many bytes in flight as shared memory holds
 
 template <int KP>
 struct ACfg {
   static constexpr int A1 = TN * BK * 4;                 // Y tile: fp32 landing = hi | lo fp16 after the split
-  static constexpr int B1 = KP * BK * 4;                 // U twin: hi plane then lo plane
+  static constexpr int B1 = KP * BK * 4;                 // U twin: KP rows [hi | lo]
   static constexpr int STAGE1 = A1 + B1;
-  static constexpr int ZS = TN * KP * 4;                 // Z as hi | lo fp16 k-blocks (aliases the product-1 ring)
-  static constexpr int R1 = S1 * STAGE1 > ZS ? S1 * STAGE1 : ZS;
-  static constexpr int A2 = 128 * BK * 4;                // V twin tile: hi plane then lo plane
-  static constexpr int R2 = S2 * A2;
-  static constexpr int R3 = 8 * 32 * 20 * 4;             // per-warp F staging, 32 rows x 16 columns (pitch 20)
-  static constexpr int SMEM = R1 + R2 + R3 + 1024;
+  static constexpr int ZS = TN * KP * 4;                 // Z as hi | lo fp16 k-blocks
+  static constexpr int A2 = 128 * BK * 4;                // V twin tile: 128 rows [hi | lo]
+  // one ring: product 1 uses S1 stages of it; afterwards Z sits in its first ZS bytes and the V tiles
+  // of product 2 cycle through S2 stages behind Z
+  static constexpr int RING = S1 * STAGE1 > ZS + S2 * A2 ? S1 * STAGE1 : ZS + S2 * A2;
+  static constexpr int SMEM = RING + 1024;
   static constexpr int NKB2 = KP / BK;
   static constexpr int NCH2 = (NKB2 + 3) / 4;            // TMEM chunks of product 2 (24 MMAs each)
   static constexpr int HALF = KP / 2;                    // Z columns per epilogue thread
@@ -94,6 +96,22 @@ __device__ __forceinline__ void split8(const float* x, float sc, uint4& hv, uint
   lv = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
+#ifdef HG_APPLY_CLK
+// debug build (-DHG_APPLY_CLK): %globaltimer stamps of the phases of the first 160 CTAs
+__device__ unsigned long long g_aclk[160 * 32];
+__device__ __forceinline__ void aclk(int slot) {
+  const int c = blockIdx.y * gridDim.x + blockIdx.x;
+  if (c < 160 && slot < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_aclk[c * 32 + slot] = t;
+  }
+}
+#define ACLK(cond, slot) do { if (cond) aclk(slot); } while (0)
+#else
+#define ACLK(cond, slot) do { } while (0)
+#endif
+
 template <int KP>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_apply_fused(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmU,
@@ -108,12 +126,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * TN, g = blockIdx.y;
+  ACLK(threadIdx.x == 0, 0);
   const int nkb1 = (aa.b + BK - 1) / BK, nch1 = (nkb1 + 3) / 4;
   const int nmt = (aa.b + 127) / 128;
 
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* r2 = base + C::R1;
-  uint8_t* r3 = r2 + C::R2;
+  uint8_t* r2 = base + C::ZS;
 
   if (warp == 8 && lane == 0) {
     tma_prefetch(&tmY);
@@ -162,6 +180,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const uint32_t sbase = smem_u32(base);
+  ACLK(threadIdx.x == 0, 1);
 
   if (warp == 8) {
     // ---------------- TMA producer (converged warp, one elected lane issues)
@@ -174,10 +193,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_arrive_expect_tx(&full1[s], C::STAGE1);
 #pragma unroll
         for (int c = 0; c < TN / 32; ++c) tma_load_3d(st + c * 4096, &tmY, &full1[s], t0 + 32 * c, kb * BK, g);
-        tma_load_4d(st + C::A1, &tmU, &full1[s], kb * BK, 0, 0, g);
+        tma_load_3d(st + C::A1, &tmU, &full1[s], 2 * kb * BK, 0, g);
       }
       __syncwarp();
     }
+    // the V ring reuses product-1 stage memory: wait for the last product-1 MMAs (last chunk committed)
+    mbar_wait(&tfull1[(nch1 - 1) & 1], ((nch1 - 1) >> 1) & 1);
     int idx = 0;
     for (int mt = 0; mt < nmt; ++mt)
       for (int kb2 = 0; kb2 < C::NKB2; ++kb2, ++idx) {
@@ -186,16 +207,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (idx >= S2) mbar_wait(&empty2[s], ph ^ 1);
         if (elect_one()) {
           mbar_arrive_expect_tx(&full2[s], C::A2);
-          tma_load_4d(r2 + s * C::A2, &tmV, &full2[s], kb2 * BK, mt * 128, 0, g);
+          tma_load_3d(r2 + s * C::A2, &tmV, &full2[s], 2 * kb2 * BK, mt * 128, g);
         }
         __syncwarp();
       }
   } else if (warp == 9) {
     // ---------------- MMA issuer (converged warp, one elected lane issues)
-    // product 1: A = Y tile split in place (1 KB groups of 8 hi rows + 8 lo rows: SBO 1024, lo at +512),
-    //            B = U twin (hi plane, lo plane at +KP*64: SBO 512); K-step 16 = +32 B
+    // every operand: K-major SWIZZLE_128B rows [hi 32 k | lo 32 k], 8-row groups 1024 B apart (SBO),
+    // K-step 16 = +32 B in the row, the lo half at +64 B
+    // product 1: A = Y tile (128 rows t, split in place), B = U twin tile (KP rows j)
     const uint32_t idesc1 = idesc_f16(KP);
-    const uint32_t a1_hiw = umma_desc_hi(1024, 4), p_hiw = umma_desc_hi(512, 4);
+    const uint32_t hiw = umma_desc_hi(1024, 2);
     for (int kb = 0; kb < nkb1; ++kb) {
       const int s = kb % S1;
       const uint32_t ph = (kb / S1) & 1;
@@ -209,13 +231,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc_fence_after();
       const bool last_in_chunk = (kb & 3) == 3 || kb == nkb1 - 1;
       if (elect_one()) {
+        ACLK(kb == 0, 2);
+        ACLK(kb == nkb1 - 1, 3);
         const uint32_t d = tmem + (uint32_t)(buf * KP);
         const uint32_t st0 = sbase + s * C::STAGE1;
         const uint32_t a0 = umma_desc_lo(st0, 16), b0 = umma_desc_lo(st0 + C::A1, 16);
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
-          const uint64_t dah = umma_desc2(a0 + kk * 2, a1_hiw), dal = umma_desc2(a0 + 32 + kk * 2, a1_hiw);
-          const uint64_t dbh = umma_desc2(b0 + kk * 2, p_hiw), dbl = umma_desc2(b0 + (KP * 64 >> 4) + kk * 2, p_hiw);
+          const uint64_t dah = umma_desc2(a0 + kk * 2, hiw), dal = umma_desc2(a0 + 4 + kk * 2, hiw);
+          const uint64_t dbh = umma_desc2(b0 + kk * 2, hiw), dbl = umma_desc2(b0 + 4 + kk * 2, hiw);
           mma_f16(d, dal, dbh, idesc1, (first && kk == 0) ? 0u : 1u);
           mma_f16(d, dah, dbl, idesc1, 1);
           mma_f16(d, dah, dbh, idesc1, 1);
@@ -225,10 +249,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       __syncwarp();
     }
-    // product 2: A = V twin tile (128 rows: hi plane, lo plane at +8 KB), B = Z k-block kb2 in the
-    // product-1 ring's memory (128 rows t: hi plane, lo plane at +8 KB), both SBO 512
+    // product 2: Z k-block kb2 (128 rows t) in the product-1 ring's memory and the V twin tile (128 rows m)
     mbar_wait(&zs_bar, 0);
     tc_fence_after();
+    ACLK(lane == 0, 5);
     const uint32_t idesc2 = idesc_f16(TN);
     int idx = 0;
     for (int mt = 0; mt < nmt; ++mt) {
@@ -244,12 +268,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t d = tmem + (uint32_t)(buf2 * 256 + (kb2 >> 2) * 128);
-          const uint32_t a0 = umma_desc_lo(sbase + C::R1 + s * C::A2, 16);
-          const uint32_t b0 = umma_desc_lo(sbase + kb2 * (TN * BK * 4), 16);
+          // F^T tile: lanes = RHS column t (A = Z^T k-block), TMEM columns = row m of the tile (B = V tile):
+          // a warp's 32 lanes then store 32 consecutive t of one F row, 128 contiguous bytes
+          const uint32_t b0 = umma_desc_lo(sbase + C::ZS + s * C::A2, 16);
+          const uint32_t a0 = umma_desc_lo(sbase + kb2 * (TN * BK * 4), 16);
 #pragma unroll
           for (int kk = 0; kk < 2; ++kk) {
-            const uint64_t dah = umma_desc2(a0 + kk * 2, p_hiw), dal = umma_desc2(a0 + (128 * 64 >> 4) + kk * 2, p_hiw);
-            const uint64_t dbh = umma_desc2(b0 + kk * 2, p_hiw), dbl = umma_desc2(b0 + (TN * 64 >> 4) + kk * 2, p_hiw);
+            const uint64_t dah = umma_desc2(a0 + kk * 2, hiw), dal = umma_desc2(a0 + 4 + kk * 2, hiw);
+            const uint64_t dbh = umma_desc2(b0 + kk * 2, hiw), dbl = umma_desc2(b0 + 4 + kk * 2, hiw);
             mma_f16(d, dal, dbh, idesc2, ((kb2 & 3) == 0 && kk == 0) ? 0u : 1u);
             mma_f16(d, dah, dbl, idesc2, 1);
             mma_f16(d, dah, dbh, idesc2, 1);
@@ -290,8 +316,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t ph = (kb / S1) & 1;
       mbar_wait(&full1[s], ph);
       // the tile landed as 4 chunks [32 rows kk][32 columns t] (128-byte rows, SWIZZLE_128B); thread
-      // units (t row r, 4 consecutive kk) are read transposed, then written as the K-major hi | lo
-      // groups (8 t rows per 1 KB: 8 hi rows of 64 B, then the 8 lo rows)
+      // units (t row r, 4 consecutive kk) are read transposed, then written as K-major rows t of
+      // [hi 32 kk | lo 32 kk] (128 bytes, SWIZZLE_128B: 16-byte unit u of row r at u ^ (r & 7))
       uint8_t* reg = base + s * C::STAGE1;
       float4 x[4];
 #pragma unroll
@@ -311,8 +337,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int u = t + i * NEPI, kq = u >> 7, r = u & 127;
-        uint8_t* gb = reg + (r >> 3) * 1024;
-        f16_split_store(gb, gb + 512, r & 7, kq, x[i]);
+        uint2 hv, lv;
+        split4(x[i], 1.0f, hv, lv);
+        uint8_t* row = reg + r * 128 + ((kq & 1) << 3);
+        *reinterpret_cast<uint2*>(row + (((kq >> 1) ^ (r & 7)) << 4)) = hv;
+        *reinterpret_cast<uint2*>(row + (((4 + (kq >> 1)) ^ (r & 7)) << 4)) = lv;
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -320,6 +349,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       while (drained < nch1 - 1 && kb >= (drained + 1) * 4 + 1) drain(drained++);
     }
     while (drained < nch1) drain(drained++);
+    ACLK(t == 0, 4);
 
     // Z^T[t][j] = acc * c / sigma_j * 2^-(e_y + e_u); CTA-local exponent e_z from max|Z|
     const float a1 = ldexpf(1.0f, -(ey + eu));
@@ -340,16 +370,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const float zsc = isfinite(zmax) && zmax > 0.f ? ldexpf(1.0f, ez) : 1.0f;
     {
       const int r = q * 32 + lane;
-      const int sw = (r >> 1) & 3;
+      const int sw = r & 7;
 #pragma unroll
       for (int kbl = 0; kbl < C::HALF / 32; ++kbl) {
-        uint8_t* zb = base + (h * (C::HALF / 32) + kbl) * (TN * BK * 4) + r * 64;
+        uint8_t* zb = base + (h * (C::HALF / 32) + kbl) * (TN * BK * 4) + r * 128;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           uint4 hv, lv;
           split8(&acc[kbl * 32 + u * 8], zsc, hv, lv);
           *reinterpret_cast<uint4*>(zb + ((u ^ sw) << 4)) = hv;
-          *reinterpret_cast<uint4*>(zb + TN * 64 + ((u ^ sw) << 4)) = lv;
+          *reinterpret_cast<uint4*>(zb + (((4 + u) ^ sw) << 4)) = lv;
         }
       }
     }
@@ -357,13 +387,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&zs_bar);
 
-    // F tiles: drain, rescale by 2^-(e_v + e_z), stage 32 x 16 per warp, store 64-byte row pieces
+    // F tiles: drain, rescale by 2^-(e_v + e_z), store (a warp instruction = 128 contiguous bytes of one F row)
     const float a2 = (isfinite(zmax) && zmax > 0.f) ? ldexpf(1.0f, -(ev + ez)) : ldexpf(1.0f, -ev);
-    float* st = reinterpret_cast<float*>(r3) + warp * 32 * 20;
     for (int mt = 0; mt < nmt; ++mt) {
       const int buf2 = mt & 1;
       mbar_wait(&tfull2[buf2], (mt >> 1) & 1);
       tc_fence_after();
+      ACLK(t == 0, 6 + 2 * mt);
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf2 * 256 + h * 64);
       float v[64];
 #pragma unroll
@@ -381,28 +411,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty2[buf2]);
-      const int mw0 = mt * 128 + q * 32;
+      ACLK(t == 0, 22 + mt);
+      // thread = RHS column tt, v[j] = F[row mt*128 + h*64 + j][tt]
+      const int tt = t0 + q * 32 + lane;
+      if (tt < aa.T) {
+        float* fcol = aa.F + ((int64_t)g * aa.b + mt * 128 + h * 64) * aa.T + tt;
+        const int mrows = min(64, aa.b - (mt * 128 + h * 64));
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 16) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          *reinterpret_cast<float4*>(st + lane * 20 + 4 * i) =
-              make_float4(v[c0 + 4 * i] * a2, v[c0 + 4 * i + 1] * a2, v[c0 + 4 * i + 2] * a2, v[c0 + 4 * i + 3] * a2);
-        __syncwarp();
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const int row = it * 8 + (lane >> 2), col = 4 * (lane & 3);
-          const int m = mw0 + row, tt = t0 + h * 64 + c0 + col;
-          if (m < aa.b && tt < aa.T)
-            *reinterpret_cast<float4*>(aa.F + ((int64_t)g * aa.b + m) * aa.T + tt) =
-                *reinterpret_cast<const float4*>(st + row * 20 + col);
-        }
-        __syncwarp();
+        for (int j = 0; j < 64; ++j)
+          if (j < mrows) fcol[(int64_t)j * aa.T] = v[j] * a2;
       }
+      ACLK(t == 0, 7 + 2 * mt);
     }
   }
   tc_fence_before();
   __syncthreads();
+  ACLK(threadIdx.x == 0, 31);
   if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
@@ -433,10 +457,9 @@ __global__ void k_fill_bits(uint32_t* out, int n, int ld, uint32_t v) {
   if (i < 2 * n) out[(i / n) * ld + i % n] = v;
 }
 
-// U twin: hi / lo planes of fp16(2^e x) in the layout of x ([nb][rows][b]), e from amax[g]
+// U twin (tw_off layout) of x [nb][rows][b]: fp16(2^e x), e from amax[g]
 __global__ void __launch_bounds__(256) k_split_rows(const float* __restrict__ x, int64_t per_block8,
-                                                    const uint32_t* __restrict__ amax, uint16_t* __restrict__ hi,
-                                                    uint16_t* __restrict__ lo) {
+                                                    const uint32_t* __restrict__ amax, uint16_t* __restrict__ out16) {
   const int g = blockIdx.y;
   const float sc = ldexpf(1.0f, f16_exp_of(__uint_as_float(amax[g]), 14));
   const int64_t base = (int64_t)g * per_block8;
@@ -446,16 +469,16 @@ __global__ void __launch_bounds__(256) k_split_rows(const float* __restrict__ x,
     const float v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
     uint4 hv, lv;
     split8(v, sc, hv, lv);
-    reinterpret_cast<uint4*>(hi)[base + i] = hv;
-    reinterpret_cast<uint4*>(lo)[base + i] = lv;
+    uint16_t* o = out16 + tw_off(8 * (base + i));
+    *reinterpret_cast<uint4*>(o) = hv;
+    *reinterpret_cast<uint4*>(o + TW_LO) = lv;
   }
 }
 
-// V twin, transposed: src Vt [nb][ldk][b] (row j = singular vector j) -> hi / lo planes [nb][b][k] of
-// fp16(2^e V[i][j]); grid (ceil(b/32), ceil(k/32), nb), 32 x 32 tiles through shared memory
+// V twin, transposed: src Vt [nb][ldk][b] (row j = singular vector j) -> the twin (tw_off layout) of
+// V [nb][b][k], fp16(2^e V[i][j]); grid (ceil(b/32), k/32, nb), 32 x 32 tiles through shared memory
 __global__ void __launch_bounds__(256) k_split_t(const float* __restrict__ Vt, int b, int k, int ldk,
-                                                 const uint32_t* __restrict__ amax, uint16_t* __restrict__ hi,
-                                                 uint16_t* __restrict__ lo) {
+                                                 const uint32_t* __restrict__ amax, uint16_t* __restrict__ out16) {
   __shared__ float tile[32][33];
   const int g = blockIdx.z, i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -471,9 +494,9 @@ __global__ void __launch_bounds__(256) k_split_t(const float* __restrict__ Vt, i
     const float x0 = tile[4 * jq][i], x1 = tile[4 * jq + 1][i], x2 = tile[4 * jq + 2][i], x3 = tile[4 * jq + 3][i];
     uint2 hv, lv;
     split4(make_float4(x0, x1, x2, x3), 1.0f, hv, lv);
-    const int64_t o = ((int64_t)g * b + i0 + i) * k + j0 + 4 * jq;
-    *reinterpret_cast<uint2*>(hi + o) = hv;
-    *reinterpret_cast<uint2*>(lo + o) = lv;
+    uint16_t* o = out16 + tw_off(((int64_t)g * b + i0 + i) * k + j0 + 4 * jq);
+    *reinterpret_cast<uint2*>(o) = hv;
+    *reinterpret_cast<uint2*>(o + TW_LO) = lv;
   }
 }
 
@@ -494,24 +517,30 @@ cudaError_t launch_fused(const CUtensorMap& tY, const CUtensorMap& tU, const CUt
 
 }  // namespace
 
+#ifdef HG_APPLY_CLK
+extern "C" int hg_debug_apply_clk(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_aclk, sizeof(unsigned long long) * (size_t)n);
+}
+#endif
+
 bool apply_fused_supported(int b, int k, int ldk, int T, const void* Ut, const void* Vt, const void* Y, const void* F) {
   static const bool off = [] {
     const char* v = getenv("HG_APPLY_FUSED");
     return v && v[0] == '0';
   }();
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  return !off && k >= 8 && k <= 256 && (k % 8) == 0 && (b % 8) == 0 && (T % 4) == 0 && T > 0 && ldk >= k &&
+  return !off && k >= 32 && k <= 256 && (k % 32) == 0 && (b % 32) == 0 && (T % 4) == 0 && T > 0 && ldk >= k &&
          al16(Ut) && al16(Vt) && al16(Y) && al16(F);
 }
 
 size_t apply_fused_amax_bytes(int nb) { return sizeof(uint32_t) * 3 * (size_t)nb; }
 
 // Apply prep: the exponent words and the operand twins of the fused kernel.
-// Ut, Vt [nb][ldk][b] fp32; twins u16 [nb][ldk][b] and v16 [nb][b][k] (hi planes, lo planes tw_lo fp16
-// elements further); amax: [3][amax_ld] words, this part's first block at [0].  uv_unit: |U|, |V| <= 1
+// Ut, Vt [nb][ldk][b] fp32; u16, v16: the twins (tw_off layout) of Ut [nb][ldk][b] and of V [nb][b][k];
+// amax: [3][amax_ld] words, this part's first block at [0].  uv_unit: |U|, |V| <= 1
 // (exponent 14, no max pass); otherwise the per-block maxima are measured.
 cudaError_t launch_apply_prep(const float* Ut, const float* Vt, int nb, int b, int k, int ldk, const float* Y, int T,
-                              uint16_t* u16, uint16_t* v16, int64_t tw_lo, uint32_t* amax, int amax_ld, bool uv_unit,
+                              uint16_t* u16, uint16_t* v16, uint32_t* amax, int amax_ld, bool uv_unit,
                               cudaStream_t s, int* launches) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(amax, 0, sizeof(uint32_t) * nb, s)) != cudaSuccess) return e;
@@ -531,21 +560,21 @@ cudaError_t launch_apply_prep(const float* Ut, const float* Vt, int nb, int b, i
     k_absmax<<<dim3(gu, nb), 256, 0, s>>>(Vt, u4, amax + 2 * amax_ld);
     *launches += 2;
   }
-  k_split_rows<<<dim3(gu, nb), 256, 0, s>>>(Ut, (int64_t)ldk * b / 8, amax + amax_ld, u16, u16 + tw_lo);
-  k_split_t<<<dim3((b + 31) / 32, (k + 31) / 32, nb), 256, 0, s>>>(Vt, b, k, ldk, amax + 2 * amax_ld, v16, v16 + tw_lo);
+  k_split_rows<<<dim3(gu, nb), 256, 0, s>>>(Ut, (int64_t)ldk * b / 8, amax + amax_ld, u16);
+  k_split_t<<<dim3((b + 31) / 32, (k + 31) / 32, nb), 256, 0, s>>>(Vt, b, k, ldk, amax + 2 * amax_ld, v16);
   *launches += 2;
   return cudaGetLastError();
 }
 
 // The fused kernel on the twins and exponent words of launch_apply_prep; sigma [nb][ldk], Y, F [nb*b][T].
 cudaError_t launch_apply_fused(const float* sigma, int nb, int b, int k, int ldk, const float* Y, int T, float scale,
-                               float* F, int32_t* status, const uint16_t* u16, const uint16_t* v16, int64_t tw_lo,
+                               float* F, int32_t* status, const uint16_t* u16, const uint16_t* v16,
                                const uint32_t* amax, int amax_ld, cudaStream_t s, int* launches) {
   CUtensorMap tY, tU, tV;
   const int KP = k <= 64 ? 64 : (k <= 128 ? 128 : 256);
   bool ok = hg_tma_map_f32(&tY, Y, T, b, nb, T, (int64_t)b * T, 32, true, true);
-  ok = ok && hg_tma_map_pair(&tU, u16, b, k, nb, b, (int64_t)ldk * b, tw_lo, KP);
-  ok = ok && hg_tma_map_pair(&tV, v16, k, b, nb, k, (int64_t)b * k, tw_lo, 128);
+  ok = ok && hg_tma_map_twin(&tU, u16, b, k, nb, b, (int64_t)ldk * b, KP);
+  ok = ok && hg_tma_map_twin(&tV, v16, k, b, nb, k, (int64_t)b * k, 128);
   if (!ok) return cudaErrorInvalidValue;
   ApplyArgs aa{T, b, k, ldk, sigma, scale, F, status, amax, amax_ld};
   ++*launches;

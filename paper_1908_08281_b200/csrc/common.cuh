@@ -81,6 +81,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Pure polling wait (mbarrier.test_wait, no suspend): for waits on a pipeline's critical chain, where
+// the wake-up of a suspended try_wait would add to every stage's latency.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "SPIN_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra SPIN_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -179,6 +192,14 @@ __device__ __forceinline__ bool elect_one() {
       : "=r"(pred));
   return pred != 0;
 }
+
+// 3xF16 twin layout of a dense [rows][K] fp32 array (K % 32 == 0): every 32 consecutive elements o..o+31
+// (o % 32 == 0) become 64 fp16 -- the 32 hi halves fp16_rn(2^e x), then the 32 lo halves
+// fp16_rn(2^e x - hi) -- so a TMA box of 64 fp16 x R rows with SWIZZLE_128B lands as 128-byte
+// shared-memory rows [hi 32 k | lo 32 k]: the K-major SWIZZLE_128B operand layout the tensor core reads
+// at full rate.  Element o's hi half sits at tw_off(o), its lo half TW_LO further.
+__host__ __device__ __forceinline__ int64_t tw_off(int64_t o) { return 2 * o - (o & 31); }
+constexpr int TW_LO = 32;
 
 // UMMA shared-memory descriptor (sm100 version bits); start, lbo, sbo in bytes
 // (encoded >> 4).  layout: 2 = SWIZZLE_128B (16-byte atoms, 8-row period; the

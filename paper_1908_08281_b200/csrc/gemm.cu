@@ -22,9 +22,10 @@
 //   * 3xF16 (GemmDesc::prec = 1): the same pipeline on kind::f16 (twice the tf32 MMA rate):
 //     hi = fp16_rn(2^e x), lo = fp16_rn(2^e x - hi) -- 22 significant bits like the tf32 pair,
 //     the power-of-two prescale 2^e (from the caller's bound on |x|) keeps the pair inside the
-//     fp16 exponent range.  The split is done in place (fp32 landing tile -> K-major SWIZZLE_64B
-//     hi | lo halves, both majors), or not at all for operands the producer stored pre-split
-//     (GemmDesc::A16 / B16: hi and lo fp16 planes, TMA-loaded straight into the same layout).
+//     fp16 exponent range.  Operands the producer stored as twins (GemmDesc::A16 / B16, the tw_off
+//     layout of common.cuh) are TMA-loaded straight into 128-byte SWIZZLE_128B rows [hi | lo] and feed
+//     the MMAs as they stand (PRE kernels: the epilogue warps only drain); fp32 operands are split in
+//     place (fp32 landing tile -> K-major SWIZZLE_64B hi | lo halves, both majors).
 //     TMEM chunks of K = 128 (24 MMAs per chunk, the same truncation bound as the tf32 path).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -60,12 +61,10 @@ struct EpiArgs {
   float beta;
   int b_upper;    // B(kk, n) = 0 for kk > n (GemmDesc::b_upper): per k-block, MMAs over n >= kk only
   // 3xF16 only
-  int a_pre, b_pre;   // operand TMA-loaded pre-split (hi | lo fp16 planes): no in-kernel split
   float a_sc, b_sc;   // 2^a_exp, 2^b_exp: prescale of the in-kernel split
   // optional pre-split copy of the (transposed) output for a later 3xF16 GEMM: hi / lo planes of
-  // fp16_rn(2^d_exp D) at D16[g*sd + n*ldd + m] and D16 + d_lo (both precisions)
+  // fp16_rn(2^d_exp D) in the twin layout (tw_off) of D[g*sd + n*ldd + m] (both precisions)
   uint16_t* D16;
-  int64_t d_lo;
   float d_sc;
 };
 
@@ -121,10 +120,18 @@ __device__ __forceinline__ float4 split_hi(float4& x) {
 // at K = 1024).  The MMAs of each K-chunk of 64 go to a fresh TMEM buffer (two
 // buffers, ping-pong); the epilogue warps drain finished chunks and sum them in
 // fp32 round-to-nearest registers, bounding the truncation to 24 MMAs.
-template <int BN, bool F16>
+// PRE (3xF16 with both operands pre-split): each 128-byte shared-memory row holds the hi fp16 of the
+// k-block's 32 K elements in bytes 0-63 and their lo in bytes 64-127 (SWIZZLE_128B K-major rows of 64
+// "elements"; the TMA box is (32 k, {hi, lo}, rows)).  The hi K-steps sit at +0 / +32 B of the row, the
+// lo ones at +64 / +96 B.  The tensor core fetches 64-byte-row (SWIZZLE_64B) operands at half rate
+// (two rows of every 8-row core matrix share their banks: ~250 instead of 128 cycles per 128 x 256 x 16
+// MMA, measured), so only the in-kernel-split 3xF16 paths -- whose 128-byte fp32 landing rows become a
+// 64-byte hi and a 64-byte lo row in place -- keep that layout.
+template <int BN, bool F16, bool PRE = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    EpiArgs ea) {
+  static_assert(!PRE || F16, "pre-split operands are 3xF16 only");
   using C = Cfg<BN, F16>;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[C::STAGES], conv_bar[C::STAGES], empty_bar[C::STAGES];
@@ -136,7 +143,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (ea.lower && n0 >= m0 + BM) return;   // tile above the diagonal (uniform: before any setup)
   const int num_kb = (ea.K + BK - 1) / BK;
   const int nchunks = (num_kb + C::CHUNK - 1) / C::CHUNK;
-  const bool pre_ab = F16 && ea.a_pre && ea.b_pre;   // no in-kernel split at all
+  constexpr bool pre_ab = PRE;   // twin operands: no in-kernel split at all
 
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   auto sA_hi = [&](int s) { return base + s * C::STAGE_BYTES; };
@@ -174,16 +181,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (elect_one()) {
         mbar_arrive_expect_tx(&full_bar[s], C::TX);
         const int k0 = kb * BK;
-        if (F16 && ea.a_pre) {
-          tma_load_4d(sA_hi(s), &tmA, &full_bar[s], k0, m0, 0, g);   // hi rows then lo rows
+        if (PRE) {
+          tma_load_3d(sA_hi(s), &tmA, &full_bar[s], 2 * k0, m0, g);   // rows of [hi 32 k | lo 32 k]
+          tma_load_3d(sB_hi(s), &tmB, &full_bar[s], 2 * k0, n0, g);
         } else if (!ea.a_mn) {
           tma_load_3d(sA_hi(s), &tmA, &full_bar[s], k0, m0, g);
         } else {
 #pragma unroll
           for (int c = 0; c < BM / 32; ++c) tma_load_3d(sA_hi(s) + c * 4096, &tmA, &full_bar[s], m0 + 32 * c, k0, g);
         }
-        if (F16 && ea.b_pre) {
-          tma_load_4d(sB_hi(s), &tmB, &full_bar[s], k0, n0, 0, g);
+        if (PRE) {
         } else if (!ea.b_mn) {
           tma_load_3d(sB_hi(s), &tmB, &full_bar[s], k0, n0, g);
         } else {
@@ -197,22 +204,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ---------------- MMA issuer: the warp stays converged, one elected lane issues (under
     // `if (lane == 0)` every UTCHMMA sat in a per-lane R2UR loop); descriptors from 32-bit words
     const uint32_t sbase = smem_u32(base);
-    // 3xF16: both operands K-major SWIZZLE_64B fp16 (64-byte rows, 8-row groups 512 B apart),
-    // hi plane then lo plane; K-step 16 = +32 B in the row.
-    // split in the kernel: 1 KB groups of 8 hi rows + 8 lo rows (SBO 1024, lo at +512);
-    // pre-split (TMA): the hi plane then the lo plane (SBO 512, lo at +R * 64)
+    // 3xF16 twins (PRE): K-major SWIZZLE_128B rows [hi 32 k | lo 32 k], 8-row groups 1024 B apart (SBO),
+    // K-step 16 = +32 B in the row, the lo half at +64 B.
+    // 3xF16 split in the kernel: K-major SWIZZLE_64B fp16, 1 KB groups of 8 hi rows (64 B each) + 8 lo
+    // rows (SBO 1024, lo at +512); K-step 16 = +32 B in the row.
     // 3xTF32, K-major (SWIZZLE_128B): 8-row groups 1024 B apart (SBO), K-step = +32 B in the row.
     // MN-major (SWIZZLE_128B_BASE32B): 32-element chunks BK*128 B apart (LBO),
     // 4-row groups 512 B apart (SBO), K-step = +1024 B (8 rows).
     const uint32_t idesc = F16 ? make_idesc_f16(BN) : make_idesc(BN, ea.a_mn, ea.b_mn);
     const uint32_t a_lbo = (!F16 && ea.a_mn) ? BK * 128 : 16, b_lbo = (!F16 && ea.b_mn) ? BK * 128 : 16;
-    const uint32_t a_hiw = F16 ? umma_desc_hi(ea.a_pre ? 512 : 1024, 4) : umma_desc_hi(ea.a_mn ? 512 : 1024, ea.a_mn ? 1 : 2);
-    const uint32_t b_hiw = F16 ? umma_desc_hi(ea.b_pre ? 512 : 1024, 4) : umma_desc_hi(ea.b_mn ? 512 : 1024, ea.b_mn ? 1 : 2);
+    const uint32_t a_hiw = PRE ? umma_desc_hi(1024, 2)
+                         : F16 ? umma_desc_hi(1024, 4) : umma_desc_hi(ea.a_mn ? 512 : 1024, ea.a_mn ? 1 : 2);
+    const uint32_t b_hiw = PRE ? umma_desc_hi(1024, 2)
+                         : F16 ? umma_desc_hi(1024, 4) : umma_desc_hi(ea.b_mn ? 512 : 1024, ea.b_mn ? 1 : 2);
     // offsets (in 16-byte units) of the lo operands from the hi ones and of a K-step; bytes per B row n
-    const uint32_t a_lo_off = (F16 ? (ea.a_pre ? BM * 64 : 512) : C::A_BYTES) >> 4;
-    const uint32_t b_lo_off = (F16 ? (ea.b_pre ? BN * 64 : 512) : C::B_BYTES) >> 4;
+    const uint32_t a_lo_off = (PRE ? 64 : F16 ? 512 : C::A_BYTES) >> 4;
+    const uint32_t b_lo_off = (PRE ? 64 : F16 ? 512 : C::B_BYTES) >> 4;
     const uint32_t a_kstep = (F16 ? 32 : (ea.a_mn ? 1024 : 32)) >> 4, b_kstep = (F16 ? 32 : (ea.b_mn ? 1024 : 32)) >> 4;
-    const uint32_t b_row = (F16 && ea.b_pre) ? 64 : 128;
+    const uint32_t b_row = 128;
     constexpr int KSTEPS = F16 ? BK / 16 : BK / 8;
     for (int kb = 0; kb < num_kb; ++kb) {
       const int s = kb % C::STAGES;
@@ -340,13 +349,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             f16_split_store(gb, gb + 512, r & 7, kq, x[i]);
           }
         };
-        if (!ea.a_pre) {
-          if (ea.a_mn) conv_mn(sA_hi(s), BM, ea.a_sc); else conv_k(sA_hi(s), BM, ea.a_sc);
-        }
-        if (!ea.b_pre) {
-          if (ea.b_mn) conv_mn(sB_hi(s), BN, ea.b_sc); else conv_k(sB_hi(s), BN, ea.b_sc);
-        }
-        if (!(ea.a_pre && ea.b_pre)) fence_proxy_async_smem();
+        if (ea.a_mn) conv_mn(sA_hi(s), BM, ea.a_sc); else conv_k(sA_hi(s), BM, ea.a_sc);
+        if (ea.b_mn) conv_mn(sB_hi(s), BN, ea.b_sc); else conv_k(sB_hi(s), BN, ea.b_sc);
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv_bar[s]);
         while (drained < nchunks - 1 && kb >= (drained + 1) * C::CHUNK + 1) drain(drained++);
@@ -425,9 +430,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (ea.D16) {
               uint2 hv, lv;
               split4(v, ea.d_sc, hv, lv);
-              uint16_t* d16 = ea.D16 + (int64_t)g * ea.sd + (int64_t)n * ea.ldd + mw0 + 4 * l4;
+              uint16_t* d16 = ea.D16 + tw_off((int64_t)g * ea.sd + (int64_t)n * ea.ldd + mw0 + 4 * l4);
               *reinterpret_cast<uint2*>(d16) = hv;
-              *reinterpret_cast<uint2*>(d16 + ea.d_lo) = lv;
+              *reinterpret_cast<uint2*>(d16 + TW_LO) = lv;
             }
           }
         }
@@ -443,9 +448,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               const float x = val * ea.d_sc;
               const __half hh = __float2half_rn(x);
               const __half ll = __float2half_rn(x - __half2float(hh));
-              uint16_t* d16 = ea.D16 + (int64_t)g * ea.sd + (int64_t)n * ea.ldd + m;
+              uint16_t* d16 = ea.D16 + tw_off((int64_t)g * ea.sd + (int64_t)n * ea.ldd + m);
               d16[0] = *reinterpret_cast<const uint16_t*>(&hh);
-              d16[ea.d_lo] = *reinterpret_cast<const uint16_t*>(&ll);
+              d16[TW_LO] = *reinterpret_cast<const uint16_t*>(&ll);
             }
           }
         }
@@ -552,11 +557,10 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
 }
 
 // ------------------------------------------------------------------ pre-split producer
-// hi[i] = fp16_rn(2^e x[i]), lo[i] = fp16_rn(2^e x[i] - hi[i]) over rows x cols (row pitch ld for x,
-// ldo for hi / lo); 8 elements per thread (16-byte fp16 stores).
+// The 3xF16 twin (common.cuh tw_off) of a dense rows x cols fp32 matrix (row pitch ld, cols % 32 == 0):
+// hi = fp16_rn(2^e x), lo = fp16_rn(2^e x - hi); 8 elements per thread (16-byte fp16 stores).
 __global__ void __launch_bounds__(256) k_f16_split(const float* __restrict__ x, int64_t rows, int cols, int64_t ld,
-                                                   float sc, uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
-                                                   int64_t ldo) {
+                                                   float sc, uint16_t* __restrict__ out16) {
   const int c8 = cols / 8;
   const int64_t n = rows * c8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -574,8 +578,9 @@ __global__ void __launch_bounds__(256) k_f16_split(const float* __restrict__ x, 
       h[j] = *reinterpret_cast<const uint32_t*>(&hh);
       l[j] = *reinterpret_cast<const uint32_t*>(&ll);
     }
-    *reinterpret_cast<uint4*>(hi + r * ldo + c) = make_uint4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<uint4*>(lo + r * ldo + c) = make_uint4(l[0], l[1], l[2], l[3]);
+    uint16_t* o = out16 + tw_off(r * cols + c);
+    *reinterpret_cast<uint4*>(o) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(o + TW_LO) = make_uint4(l[0], l[1], l[2], l[3]);
   }
 }
 
@@ -613,47 +618,48 @@ bool make_map(CUtensorMap* m, const float* ptr, int64_t inner, int64_t outer, in
   return r == CUDA_SUCCESS;
 }
 
-// Pre-split fp16 operand: 4D map (K, rows, {hi, lo}, batch) over hi[g*bs + row*ld + kk] and
-// lo = hi + lo_off; box (32, box_rows, 2, 1) lands as the hi plane then the lo plane, SWIZZLE_64B.
-bool make_map_pair(CUtensorMap* m, const uint16_t* hi, int64_t K, int64_t rows, int64_t batch, int64_t ld,
-                   int64_t bs, int64_t lo_off, int box_rows) {
+// 3xF16 twin operand (common.cuh tw_off): logical [batch][rows][K] (row pitch ld, batch pitch bs, in
+// logical elements, multiples of 32) is [batch][rows][2 ld] fp16; box (64, box_rows, 1) at inner
+// coordinate 2 k0 lands as 128-byte rows [hi 32 k | lo 32 k], SWIZZLE_128B.
+bool make_map_twin(CUtensorMap* m, const uint16_t* tw, int64_t K, int64_t rows, int64_t batch, int64_t ld,
+                   int64_t bs, int box_rows) {
   auto enc = get_encode();
   if (!enc) return false;
   if (batch <= 1) bs = ld * rows;
-  cuuint64_t dims[4] = {(cuuint64_t)K, (cuuint64_t)rows, 2, (cuuint64_t)(batch < 1 ? 1 : batch)};
-  cuuint64_t strides[3] = {(cuuint64_t)ld * 2, (cuuint64_t)lo_off * 2, (cuuint64_t)bs * 2};
-  cuuint32_t box[4] = {32, (cuuint32_t)box_rows, 2, 1};
-  cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<uint16_t*>(hi), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  cuuint64_t dims[3] = {(cuuint64_t)(2 * K), (cuuint64_t)rows, (cuuint64_t)(batch < 1 ? 1 : batch)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)bs * 4};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<uint16_t*>(tw), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool F16>
+template <int BN, bool F16, bool PRE = false>
 cudaError_t launch_tc(const GemmDesc& g, const EpiArgs& ea, cudaStream_t stream) {
   using C = Cfg<BN, F16>;
   static bool attr_set = false;  // per-instantiation; set once per process
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, F16, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   CUtensorMap ta, tb;
   bool ok;
-  if (F16 && g.A16)
-    ok = make_map_pair(&ta, g.A16, g.K, g.M, g.batch, g.lda, g.sa, g.a_lo, BM);
+  if (PRE)
+    ok = make_map_twin(&ta, g.A16, g.K, g.M, g.batch, g.lda, g.sa, BM);
   else
     ok = g.a_mn ? make_map(&ta, g.A, g.M, g.K, g.batch, g.lda, g.sa, 32, true, F16)
                 : make_map(&ta, g.A, g.K, g.M, g.batch, g.lda, g.sa, BM, false);
-  if (F16 && g.B16)
-    ok = ok && make_map_pair(&tb, g.B16, g.K, g.N, g.batch, g.ldb, g.sb, g.b_lo, BN);
+  if (PRE)
+    ok = ok && make_map_twin(&tb, g.B16, g.K, g.N, g.batch, g.ldb, g.sb, BN);
   else
     ok = ok && (g.b_mn ? make_map(&tb, g.B, g.N, g.K, g.batch, g.ldb, g.sb, 32, true, F16)
                        : make_map(&tb, g.B, g.K, g.N, g.batch, g.ldb, g.sb, BN, false));
   if (!ok) return cudaErrorInvalidValue;
   dim3 grid((g.M + BM - 1) / BM, (g.N + BN - 1) / BN, g.batch);
-  gemm_tc_kernel<BN, F16><<<grid, NTHREADS, C::SMEM, stream>>>(ta, tb, ea);
+  gemm_tc_kernel<BN, F16, PRE><<<grid, NTHREADS, C::SMEM, stream>>>(ta, tb, ea);
   return cudaGetLastError();
 }
 
@@ -663,9 +669,9 @@ bool hg_tma_map_f32(CUtensorMap* m, const float* ptr, int64_t inner, int64_t out
                     int64_t bs, int box_outer, bool mn_major, bool f16_split) {
   return make_map(m, ptr, inner, outer, batch, ld, bs, box_outer, mn_major, f16_split);
 }
-bool hg_tma_map_pair(CUtensorMap* m, const uint16_t* hi, int64_t K, int64_t rows, int64_t batch, int64_t ld,
-                     int64_t bs, int64_t lo_off, int box_rows) {
-  return make_map_pair(m, hi, K, rows, batch, ld, bs, lo_off, box_rows);
+bool hg_tma_map_twin(CUtensorMap* m, const uint16_t* tw, int64_t K, int64_t rows, int64_t batch, int64_t ld,
+                     int64_t bs, int box_rows) {
+  return make_map_twin(m, tw, K, rows, batch, ld, bs, box_rows);
 }
 
 static int prec_env() {   // HG_GEMM_PREC=f16 | tf32: the precision of GEMMs that leave GemmDesc::prec = -1
@@ -683,14 +689,13 @@ const char* gemm_check(const GemmDesc& g) {
   if (g.batch > 65535) return "gemm: batch > 65535";
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool pa = g.A16 != nullptr, pb = g.B16 != nullptr;
-  if ((pa || pb) && gemm_prec(g) != 1) return "gemm: pre-split fp16 operands need prec = 1";
-  if (pa ? (!al16(g.A16) || (g.lda & 7) || (g.a_lo & 7) || (g.batch > 1 && (g.sa & 7)) || g.lda < g.K)
-         : (!g.A || !al16(g.A)))
-    return pa ? "gemm: pre-split A needs 16-byte alignment, lda/a_lo/sa multiples of 8, lda >= K"
+  if ((pa || pb) && gemm_prec(g) != 1) return "gemm: 3xF16 twin operands need prec = 1";
+  if (pa != pb) return "gemm: 3xF16 twin operands come in pairs (A16 and B16)";
+  if (pa ? (!al16(g.A16) || (g.lda & 31) || (g.batch > 1 && (g.sa & 31)) || g.lda < g.K) : (!g.A || !al16(g.A)))
+    return pa ? "gemm: twin A needs 16-byte alignment, lda and sa multiples of 32, lda >= K"
               : "gemm: A must be non-null and 16-byte aligned";
-  if (pb ? (!al16(g.B16) || (g.ldb & 7) || (g.b_lo & 7) || (g.batch > 1 && (g.sb & 7)) || g.ldb < g.K)
-         : (!g.B || !al16(g.B)))
-    return pb ? "gemm: pre-split B needs 16-byte alignment, ldb/b_lo/sb multiples of 8, ldb >= K"
+  if (pb ? (!al16(g.B16) || (g.ldb & 31) || (g.batch > 1 && (g.sb & 31)) || g.ldb < g.K) : (!g.B || !al16(g.B)))
+    return pb ? "gemm: twin B needs 16-byte alignment, ldb and sb multiples of 32, ldb >= K"
               : "gemm: B must be non-null and 16-byte aligned";
   if ((!pa && (g.lda & 3)) || (!pb && (g.ldb & 3))) return "gemm: lda/ldb must be multiples of 4";
   if (g.batch > 1 && ((!pa && (g.sa & 3)) || (!pb && (g.sb & 3)))) return "gemm: batch strides must be multiples of 4";
@@ -699,8 +704,8 @@ const char* gemm_check(const GemmDesc& g) {
   if (g.C && (g.d_trans || g.ldc < g.N)) return "gemm: residual C needs row-major D and ldc >= N";
   if (g.a_exp < -40 || g.a_exp > 40 || g.b_exp < -40 || g.b_exp > 40 || g.d_exp < -40 || g.d_exp > 40)
     return "gemm: |a_exp|, |b_exp|, |d_exp| must be <= 40";
-  if (g.D16 && (!g.d_trans || !al16(g.D16) || (g.ldd & 3) || (g.d_lo & 3) || (g.batch > 1 && (g.sd & 3))))
-    return "gemm: the pre-split output D16 needs d_trans, 16-byte alignment, ldd/d_lo/sd multiples of 4";
+  if (g.D16 && (!g.d_trans || !al16(g.D16) || (g.ldd & 31) || (g.batch > 1 && (g.sd & 31))))
+    return "gemm: the twin output D16 needs d_trans, 16-byte alignment, ldd and sd multiples of 32";
   return nullptr;
 }
 
@@ -718,8 +723,7 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
   EpiArgs ea{g.M, g.N, g.K, g.D, g.ldd, g.sd, g.d_trans ? 1 : 0, alpha, g.rs, g.srs, g.cs, g.scs,
              g.a_mn ? 1 : 0, g.b_mn ? 1 : 0, trunc_hi, g.lower ? 1 : 0, g.C, g.ldc, g.sc, g.beta,
              (g.b_upper && (f16 || !g.b_mn)) ? 1 : 0,
-             g.A16 ? 1 : 0, g.B16 ? 1 : 0, ldexpf(1.0f, g.a_exp), ldexpf(1.0f, g.b_exp),
-             g.D16, g.d_lo, ldexpf(1.0f, g.d_exp)};
+             ldexpf(1.0f, g.a_exp), ldexpf(1.0f, g.b_exp), g.D16, ldexpf(1.0f, g.d_exp)};
   if (simt) {
     if (g.A16 || g.B16) return cudaErrorInvalidValue;
     dim3 grid((g.M + 63) / 64, (g.N + 63) / 64, g.batch);
@@ -727,6 +731,12 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
     return cudaGetLastError();
   }
   const int n = g.N < g.bn_max ? g.N : g.bn_max;
+  if (f16 && g.A16 && g.B16) {
+    if (n <= 32) return launch_tc<32, true, true>(g, ea, stream);
+    if (n <= 64) return launch_tc<64, true, true>(g, ea, stream);
+    if (n <= 128) return launch_tc<128, true, true>(g, ea, stream);
+    return launch_tc<256, true, true>(g, ea, stream);
+  }
   if (f16) {
     if (n <= 32) return launch_tc<32, true>(g, ea, stream);
     if (n <= 64) return launch_tc<64, true>(g, ea, stream);
@@ -739,12 +749,12 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
   return launch_tc<256, false>(g, ea, stream);
 }
 
-cudaError_t launch_f16_split(const float* x, int64_t rows, int cols, int64_t ld, int exp, uint16_t* hi, uint16_t* lo,
-                             int64_t ldo, cudaStream_t stream) {
+cudaError_t launch_f16_split(const float* x, int64_t rows, int cols, int64_t ld, int exp, uint16_t* out16,
+                             cudaStream_t stream) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
-  if ((cols & 7) || (ld & 3) || (ldo & 7)) return cudaErrorInvalidValue;
+  if ((cols & 31) || (ld & 3)) return cudaErrorInvalidValue;
   const int64_t n = rows * (cols / 8);
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  k_f16_split<<<grid, 256, 0, stream>>>(x, rows, cols, ld, ldexpf(1.0f, exp), hi, lo, ldo);
+  k_f16_split<<<grid, 256, 0, stream>>>(x, rows, cols, ld, ldexpf(1.0f, exp), out16);
   return cudaGetLastError();
 }

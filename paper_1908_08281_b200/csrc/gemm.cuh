@@ -39,18 +39,15 @@ struct GemmDesc {
   // 2^-(a_exp + b_exp) in the epilogue).
   int prec = -1;
   int a_exp = 0, b_exp = 0;
-  // Pre-split operands (prec 1 only, K-major): hi planes A16[g*sa + m*lda + kk], lo planes at
-  // A16 + a_lo (fp16 element offsets, multiples of 8), already scaled by 2^a_exp.  When set,
-  // A / a_mn are ignored (likewise B16 / b_lo for B).
+  // 3xF16 twin operands (prec 1 only, K-major, both or neither): A16 / B16 are the twins (common.cuh
+  // tw_off layout: per 32 K elements the 32 hi then the 32 lo fp16) of logical arrays
+  // A[g*sa + m*lda + kk] / B[g*sb + n*ldb + kk], already scaled by 2^a_exp / 2^b_exp; lda, ldb, sa, sb
+  // multiples of 32.  When set, A / a_mn / B / b_mn are ignored.
   const uint16_t* A16 = nullptr;
-  int64_t a_lo = 0;
   const uint16_t* B16 = nullptr;
-  int64_t b_lo = 0;
-  // Optional pre-split copy of a transposed output (d_trans only, either precision): hi / lo
-  // planes of fp16_rn(2^d_exp D) at D16[g*sd + n*ldd + m] and D16 + d_lo -- the B16 / A16 form
-  // of a later 3xF16 GEMM that reads D K-major.
+  // Optional twin of a transposed output (d_trans only, either precision): fp16_rn(2^d_exp D) in the twin
+  // layout of D[g*sd + n*ldd + m] -- the B16 / A16 form of a later 3xF16 GEMM that reads D K-major.
   uint16_t* D16 = nullptr;
-  int64_t d_lo = 0;
   int d_exp = 0;
 };
 
@@ -62,7 +59,7 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt);
 const char* gemm_check(const GemmDesc& g);
 // The precision launch_gemm will use for g (0 = 3xTF32, 1 = 3xF16).
 int gemm_prec(const GemmDesc& g);
-// Pre-split producer for 3xF16 operands: hi = fp16_rn(2^exp x), lo = fp16_rn(2^exp x - hi) over a
-// rows x cols fp32 matrix (row pitch ld) into hi / lo planes of row pitch ldo (cols % 8 == 0).
-cudaError_t launch_f16_split(const float* x, int64_t rows, int cols, int64_t ld, int exp, uint16_t* hi, uint16_t* lo,
-                             int64_t ldo, cudaStream_t stream);
+// Twin producer for 3xF16 operands: out16 = the twin (common.cuh tw_off) of the dense rows x cols fp32
+// matrix x (row pitch ld, cols % 32 == 0), scaled by 2^exp.
+cudaError_t launch_f16_split(const float* x, int64_t rows, int cols, int64_t ld, int exp, uint16_t* out16,
+                             cudaStream_t stream);

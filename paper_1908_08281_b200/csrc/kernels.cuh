@@ -53,10 +53,10 @@ cudaError_t launch_inv_sigma(int nb, int k, int ld, const float* sigma, float sc
 bool apply_fused_supported(int b, int k, int ldk, int T, const void* Ut, const void* Vt, const void* Y, const void* F);
 size_t apply_fused_amax_bytes(int nb);
 cudaError_t launch_apply_prep(const float* Ut, const float* Vt, int nb, int b, int k, int ldk, const float* Y, int T,
-                              uint16_t* u16, uint16_t* v16, int64_t tw_lo, uint32_t* amax, int amax_ld, bool uv_unit,
+                              uint16_t* u16, uint16_t* v16, uint32_t* amax, int amax_ld, bool uv_unit,
                               cudaStream_t s, int* launches);
 cudaError_t launch_apply_fused(const float* sigma, int nb, int b, int k, int ldk, const float* Y, int T, float scale,
-                               float* F, int32_t* status, const uint16_t* u16, const uint16_t* v16, int64_t tw_lo,
+                               float* F, int32_t* status, const uint16_t* u16, const uint16_t* v16,
                                const uint32_t* amax, int amax_ld, cudaStream_t s, int* launches);
 
 // reading R2: rs[i][j] = c sigma_ij / ((1+mu) - sigma_ij)  (Woodbury weights)

@@ -54,7 +54,7 @@ __global__ void k_gauss(uint64_t seed, int64_t total, float* __restrict__ out) {
 // Panels: block i (global blk0 + i) gets out[(i*k + c)*b + m] = Omega[(blk0+i)*b + m][c].
 // k % 4 == 0, so normals 4j..4j+3 share a row: a thread owns (m, c..c+3) and a warp
 // covers 32 consecutive m, i.e. every store instruction writes one 128-byte line.
-// out16 (3xF16 twin, instead of out): hi / lo fp16 planes of 2^exp Omega at out16[i] and out16[lo + i].
+// out16 (3xF16 twin, instead of out): 2^exp Omega in the tw_off layout (common.cuh) of out.
 __global__ void k_gauss_panel(uint64_t seed, int64_t blk0, int b, int k, float* __restrict__ out,
                               uint16_t* __restrict__ out16, int64_t lo, float sc) {
   const int local = blockIdx.x * blockDim.x + threadIdx.x;   // (c/4) * b + m
@@ -71,8 +71,9 @@ __global__ void k_gauss_panel(uint64_t seed, int64_t blk0, int b, int k, float* 
       const float x = z[t] * sc;
       const __half h = __float2half_rn(x);
       const __half l = __float2half_rn(x - __half2float(h));
-      out16[o + (int64_t)t * b] = __half_as_ushort(h);
-      out16[lo + o + (int64_t)t * b] = __half_as_ushort(l);
+      uint16_t* o16 = out16 + tw_off(o + (int64_t)t * b);
+      o16[0] = __half_as_ushort(h);
+      o16[TW_LO] = __half_as_ushort(l);
     }
     return;
   }

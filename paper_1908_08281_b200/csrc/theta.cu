@@ -882,7 +882,7 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, const
       o.w = ((uu == v + 3) ? 1.0f : 0.0f) - o.w * inv1pmu;
     }
     if (orow) *reinterpret_cast<float4*>(orow + v) = o;
-    if (x16) {   // the 3xF16 twin, exponent 14 (|X_ij|, |Theta_ij| <= 1): hi / lo fp16 planes
+    if (x16) {   // the 3xF16 twin (tw_off layout), exponent 14 (|X_ij|, |Theta_ij| <= 1)
       const __half2 h01 = __floats2half2_rn(o.x * 16384.f, o.y * 16384.f);
       const __half2 h23 = __floats2half2_rn(o.z * 16384.f, o.w * 16384.f);
       const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
@@ -891,8 +891,9 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, const
       uint2 hv, lv;
       hv.x = *reinterpret_cast<const uint32_t*>(&h01); hv.y = *reinterpret_cast<const uint32_t*>(&h23);
       lv.x = *reinterpret_cast<const uint32_t*>(&l01); lv.y = *reinterpret_cast<const uint32_t*>(&l23);
-      *reinterpret_cast<uint2*>(x16 + ooff + v) = hv;
-      *reinterpret_cast<uint2*>(x16 + x_lo + ooff + v) = lv;
+      uint16_t* o16 = x16 + tw_off(ooff + v);
+      *reinterpret_cast<uint2*>(o16) = hv;
+      *reinterpret_cast<uint2*>(o16 + TW_LO) = lv;
     }
   }
 }
@@ -1040,7 +1041,7 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
   // the other assembly paths write fp32 only: split the part's blocks into the twin afterwards
   const int64_t off = (int64_t)blk0 * b * b;
   ++*launches;
-  return launch_f16_split(blocks + off, (int64_t)nb * b, b, b, 14, x16 + off, x16 + x_lo + off, b, s);
+  return launch_f16_split(blocks + off, (int64_t)nb * b, b, b, 14, x16 + 2 * off, s);
 }
 
 cudaError_t launch_assemble_tiles(int blk0, int nb, int b, const int64_t* row_ptr, const int32_t* col_idx,

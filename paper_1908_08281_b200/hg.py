@@ -69,9 +69,9 @@ _solve_host = _sig("hg_solve_host", ctypes.c_int, _i32, _i32, _i64, _P, _P, _P, 
                    _i32, _P, _P, _u32, _P, _sz, _P)
 _gemm = _sig("hg_gemm", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i32, _i64, _i64, _P, _i32, _i64, _i64, _P, _i32,
              _i64, _i64, _f32, _P, _i64, _P, _i64, _u32, _P)
-_f16_split = _sig("hg_f16_split", ctypes.c_int, _P, _i64, _i32, _i64, _i32, _P, _P, _i64, _P)
-_gemm_f16pre = _sig("hg_gemm_f16pre", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i64, _i64, _i64, _i32, _P, _i64, _i64,
-                    _i64, _i32, _P, _i32, _i64, _i64, _f32, _P)
+_f16_split = _sig("hg_f16_split", ctypes.c_int, _P, _i64, _i32, _i64, _i32, _P, _P)
+_gemm_f16pre = _sig("hg_gemm_f16pre", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i64, _i64, _i32, _P, _i64, _i64,
+                    _i32, _P, _i32, _i64, _i64, _f32, _P)
 _gemm_ex = _sig("hg_gemm_ex", ctypes.c_int, _i32, _i32, _i32, _i32, _P, _i32, _i64, _i64, _P, _i32, _i64, _i64, _P,
                 _i32, _i64, _i64, _f32, _P, _i64, _P, _i64, _u32, _i32, _i32, _i32, _P)
 _cg_workspace_size = _sig("hg_cg_workspace_size", ctypes.c_int, _i32, _i32, _i64, _i32, _i32, ctypes.POINTER(_sz))
@@ -413,23 +413,23 @@ def gemm(A: torch.Tensor, B: torch.Tensor, *, M: int, N: int, K: int, batch: int
 
 
 def f16_split(x: torch.Tensor, exp: int, stream=None):
-    """Verification export: the 3xF16 pre-split of a 2D/3D fp32 tensor (last dim % 8 == 0) into
-    (hi, lo) int16 tensors holding fp16 bit patterns of 2^exp x and 2^exp x - hi."""
+    """Verification export: the 3xF16 twin of a 2D/3D fp32 tensor (last dim % 32 == 0): an int16 tensor of
+    twice the elements holding, per 32 consecutive elements, the 32 fp16 bit patterns of hi = fp16(2^exp x)
+    and then the 32 of lo = fp16(2^exp x - hi)."""
     _dev(x, torch.float32)
     cols = x.shape[-1]
     rows = x.numel() // cols
-    hi = torch.empty(x.shape, dtype=torch.int16, device=x.device)
-    lo = torch.empty_like(hi)
-    _check(_f16_split(_ptr(x), rows, cols, cols, exp, _ptr(hi), _ptr(lo), cols, _stream(stream)))
-    return hi, lo
+    out = torch.empty(x.shape[:-1] + (2 * cols,), dtype=torch.int16, device=x.device)
+    _check(_f16_split(_ptr(x), rows, cols, cols, exp, _ptr(out), _stream(stream)))
+    return out
 
 
-def gemm_f16pre(A16: torch.Tensor, a_lo: int, B16: torch.Tensor, b_lo: int, *, M: int, N: int, K: int, batch: int,
+def gemm_f16pre(A16: torch.Tensor, B16: torch.Tensor, *, M: int, N: int, K: int, batch: int,
                 lda: int, sa: int, a_exp: int, ldb: int, sb: int, b_exp: int, D: torch.Tensor, d_trans: bool = False,
                 ldd: int, sd: int = 0, alpha: float = 1.0, stream=None):
-    """Verification export: 3xF16 GEMM on pre-split K-major operands (hi planes at A16 / B16, lo planes
-    a_lo / b_lo fp16 elements further on)."""
-    _check(_gemm_f16pre(M, N, K, batch, _ptr(A16), a_lo, lda, sa, a_exp, _ptr(B16), b_lo, ldb, sb, b_exp, _ptr(D),
+    """Verification export: 3xF16 GEMM on twin K-major operands (f16_split outputs; lda, sa, ldb, sb in
+    elements of the fp32 arrays)."""
+    _check(_gemm_f16pre(M, N, K, batch, _ptr(A16), lda, sa, a_exp, _ptr(B16), ldb, sb, b_exp, _ptr(D),
                         int(d_trans), ldd, sd, alpha, _stream(stream)))
     return D
 

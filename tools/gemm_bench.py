@@ -29,10 +29,12 @@ def main():
     ap.add_argument("--shapes", nargs="*", default=list(SHAPES))
     ap.add_argument("--prec", type=int, default=0)
     ap.add_argument("--pre", action="store_true", help="3xF16 with both operands pre-split (K-major shapes only)")
+    ap.add_argument("--batch", type=int, default=0, help="override the batch (8 = one stream part of configs[3])")
     a = ap.parse_args()
     g = torch.Generator(device="cuda").manual_seed(0)
     for name in a.shapes:
         M, N, K, B, a_mn, b_mn, d_trans = SHAPES[name]
+        B = a.batch or B
         A = torch.randn(B, *((K, M) if a_mn else (M, K)), device="cuda", generator=g)
         Bm = torch.randn(B, *((K, N) if b_mn else (N, K)), device="cuda", generator=g)
         D = torch.empty(B, *((N, M) if d_trans else (M, N)), device="cuda")
@@ -40,13 +42,11 @@ def main():
         if a.pre:
             if a_mn or b_mn:
                 continue
-            ah, al = hg.f16_split(A, 11)
-            bh, bl = hg.f16_split(Bm, 11)
-            A16 = torch.cat([ah.flatten(), al.flatten()])
-            B16 = torch.cat([bh.flatten(), bl.flatten()])
+            A16 = hg.f16_split(A, 11)
+            B16 = hg.f16_split(Bm, 11)
 
             def run():
-                hg.gemm_f16pre(A16, ah.numel(), B16, bh.numel(), M=M, N=N, K=K, batch=B, lda=A.shape[2],
+                hg.gemm_f16pre(A16, B16, M=M, N=N, K=K, batch=B, lda=A.shape[2],
                                sa=A[0].numel(), a_exp=11, ldb=Bm.shape[2], sb=Bm[0].numel(), b_exp=11, D=D,
                                d_trans=d_trans, ldd=D.shape[2], sd=D[0].numel())
         else:
