@@ -373,6 +373,9 @@ struct Bufs {
   int32_t* perm;
   uint32_t* amax;   // fused apply: [3][amax_ld] exponent words, this part's first block at [0]
   int amax_ld;
+  // hg_solve with the fused apply: finalize writes U's twin (P16[0]) and the v_j scales (rs) instead of
+  // fp32 Ut / Vt; the apply prep forms V's twin (P16[1]) from the unsorted panel P[2] through perm
+  bool fuse_twins = false;
 };
 Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k, int T) {
   Bufs B;
@@ -552,7 +555,8 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
   }
   {
     ProfScope ps(ST_FINALIZE, s);
-    HG_CU(launch_finalize(nb, b, k, P[2], P[3], Ut, sigma, Vt, sig, Bf.perm, st, s, &g_launches, uv_bk),
+    HG_CU(launch_finalize(nb, b, k, P[2], P[3], Ut, sigma, Vt, sig, Bf.perm, st, s, &g_launches, uv_bk,
+                          Bf.fuse_twins ? Bf.P16[0] : nullptr, Bf.fuse_twins ? Bf.rs : nullptr),
           "finalize");
   }
   return HG_OK;
@@ -589,9 +593,14 @@ hg_status run_apply(const float* Ut, const float* sigma, const float* Vt, int nb
   if (!wb && !simt && !uv_bk && Bf.P16[0] && apply_fused_supported(b, k, ldk, T, Ut, Vt, Y, F)) {
     {
       ProfScope ps(ST_INV_SIGMA, s);   // apply prep: exponents and twins
-      HG_CU(launch_apply_prep(Ut, Vt, nb, b, k, ldk, Y, T, Bf.P16[0], Bf.P16[1], Bf.amax, Bf.amax_ld,
-                              uv_unit, s, &g_launches),
-            "apply prep");
+      if (Bf.fuse_twins)
+        HG_CU(launch_apply_prep(nullptr, Bf.P[2], nb, b, k, ldk, Y, T, Bf.P16[0], Bf.P16[1], Bf.amax, Bf.amax_ld, true,
+                                s, &g_launches, Bf.perm, Bf.rs),
+              "apply prep");
+      else
+        HG_CU(launch_apply_prep(Ut, Vt, nb, b, k, ldk, Y, T, Bf.P16[0], Bf.P16[1], Bf.amax, Bf.amax_ld,
+                                uv_unit, s, &g_launches),
+              "apply prep");
     }
     ProfScope ps(ST_GEMM_APPLY, s);
     HG_CU(launch_apply_fused(sigma, nb, b, k, ldk, Y, T, scale, F, st, Bf.P16[0], Bf.P16[1], Bf.amax,
@@ -1093,7 +1102,10 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     const int blk0 = rb0 + (int)((int64_t)rcnt * pt / nparts);
     const int nbp = rb0 + (int)((int64_t)rcnt * (pt + 1) / nparts) - blk0;
     const int64_t kb = (int64_t)blk0 * l * b;
-    const Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, l, T);
+    Bufs Bf = part_bufs(ws, Lo, nb, blk0, b, l, T);
+    // U, V are internal here: with the fused apply (same condition as run_apply's) they exist only as twins
+    Bf.fuse_twins = T > 0 && T % 4 == 0 && p == 0 && !woodbury && !simt && f16_on(b, simt) &&
+                    apply_fused_supported(b, k, l, T, Ut, Vt, Y, F);
     g_cur_part = pt;
     // with the 3xF16 products the assembly writes the blocks' twin (|X_ij|, |Theta_ij| <= 1: exponent 14)
     // instead of fp32 blocks -- nothing downstream reads those

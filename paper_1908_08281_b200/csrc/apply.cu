@@ -478,7 +478,8 @@ __global__ void __launch_bounds__(256) k_split_rows(const float* __restrict__ x,
 // V twin, transposed: src Vt [nb][ldk][b] (row j = singular vector j) -> the twin (tw_off layout) of
 // V [nb][b][k], fp16(2^e V[i][j]); grid (ceil(b/32), k/32, nb), 32 x 32 tiles through shared memory
 __global__ void __launch_bounds__(256) k_split_t(const float* __restrict__ Vt, int b, int k, int ldk,
-                                                 const uint32_t* __restrict__ amax, uint16_t* __restrict__ out16) {
+                                                 const uint32_t* __restrict__ amax, uint16_t* __restrict__ out16,
+                                                 const int32_t* __restrict__ perm, const float* __restrict__ vs) {
   __shared__ float tile[32][33];
   const int g = blockIdx.z, i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -486,7 +487,13 @@ __global__ void __launch_bounds__(256) k_split_t(const float* __restrict__ Vt, i
 #pragma unroll
   for (int jj = w; jj < 32; jj += 8) {
     const int j = j0 + jj, i = i0 + lane;
-    tile[jj][lane] = (j < k && i < b) ? Vt[((int64_t)g * ldk + j) * b + i] * sc : 0.f;
+    float x = 0.f;
+    if (j < k && i < b) {
+      // perm: row j of V^T is row perm[j] of the unsorted B^T U~ panel times sign_j / sigma_j (finalize.cu)
+      const int js = perm ? perm[(int64_t)g * ldk + j] : j;
+      x = Vt[((int64_t)g * ldk + js) * b + i] * (perm ? vs[(int64_t)g * ldk + j] * sc : sc);
+    }
+    tile[jj][lane] = x;
   }
   __syncthreads();
   const int i = threadIdx.x >> 3, jq = threadIdx.x & 7;   // row i of the tile, 4 consecutive j
@@ -541,7 +548,7 @@ size_t apply_fused_amax_bytes(int nb) { return sizeof(uint32_t) * 3 * (size_t)nb
 // (exponent 14, no max pass); otherwise the per-block maxima are measured.
 cudaError_t launch_apply_prep(const float* Ut, const float* Vt, int nb, int b, int k, int ldk, const float* Y, int T,
                               uint16_t* u16, uint16_t* v16, uint32_t* amax, int amax_ld, bool uv_unit,
-                              cudaStream_t s, int* launches) {
+                              cudaStream_t s, int* launches, const int32_t* perm, const float* vs) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(amax, 0, sizeof(uint32_t) * nb, s)) != cudaSuccess) return e;
   const int64_t y4 = (int64_t)b * T / 4;
@@ -560,9 +567,12 @@ cudaError_t launch_apply_prep(const float* Ut, const float* Vt, int nb, int b, i
     k_absmax<<<dim3(gu, nb), 256, 0, s>>>(Vt, u4, amax + 2 * amax_ld);
     *launches += 2;
   }
-  k_split_rows<<<dim3(gu, nb), 256, 0, s>>>(Ut, (int64_t)ldk * b / 8, amax + amax_ld, u16);
-  k_split_t<<<dim3((b + 31) / 32, (k + 31) / 32, nb), 256, 0, s>>>(Vt, b, k, ldk, amax + 2 * amax_ld, v16);
-  *launches += 2;
+  if (!perm) {
+    k_split_rows<<<dim3(gu, nb), 256, 0, s>>>(Ut, (int64_t)ldk * b / 8, amax + amax_ld, u16);
+    ++*launches;
+  }
+  k_split_t<<<dim3((b + 31) / 32, (k + 31) / 32, nb), 256, 0, s>>>(Vt, b, k, ldk, amax + 2 * amax_ld, v16, perm, vs);
+  ++*launches;
   return cudaGetLastError();
 }
 

@@ -54,7 +54,8 @@ __global__ void k_rank(int k, const double* __restrict__ sig, int32_t* __restric
 __global__ void __launch_bounds__(NT) k_rows(int b, int k, const float* __restrict__ Vw_t,
                                              const float* __restrict__ Uw_t, const int32_t* __restrict__ perm,
                                              const double* __restrict__ sig, float* __restrict__ Ut,
-                                             float* __restrict__ Vt, int uv_bk) {
+                                             float* __restrict__ Vt, int uv_bk, uint16_t* __restrict__ u16,
+                                             float* __restrict__ vs_out) {
   __shared__ float bv[NT / 32];
   __shared__ int bi[NT / 32];
   const int blk = blockIdx.x / k, jj = blockIdx.x % k;
@@ -85,6 +86,20 @@ __global__ void __launch_bounds__(NT) k_rows(int b, int k, const float* __restri
   // v_j = B^T u_j / sigma_j; a zero (or noise-level) sigma_j of a rank-deficient block has no
   // defined v_j: write 0 instead of inf/NaN (the R1 apply flags such a sigma, k_inv_sigma)
   const float vs = (sv > 1e-7 * smax && sv > 0.0) ? (float)((double)sgn / sv) : 0.f;
+  if (u16) {
+    // hg_solve with the fused apply: U and V only feed that kernel -- write U's 3xF16 twin (unit vectors:
+    // exponent 14, tw_off layout) and v_j's scale (the apply prep forms V's twin from Vw_t); no fp32 Ut / Vt
+    if (threadIdx.x == 0) vs_out[(int64_t)blk * k + jj] = vs;
+    for (int i = 4 * threadIdx.x; i < b; i += 4 * NT) {
+      const float4 x = *reinterpret_cast<const float4*>(u + i);
+      uint2 hv, lv;
+      split4(x, sgn * 16384.f, hv, lv);
+      uint16_t* o = u16 + tw_off(dst + i);
+      *reinterpret_cast<uint2*>(o) = hv;
+      *reinterpret_cast<uint2*>(o + TW_LO) = lv;
+    }
+    return;
+  }
   const float* v = Vw_t + src;
   if (uv_bk) {   // HG_UV_BK: U, V [nb][b][k] (column jj of U_i, V_i)
     const int64_t ob = (int64_t)blk * b * k + jj;
@@ -184,10 +199,10 @@ cudaError_t launch_unit_columns_t(int nb, int k, const float* Wf, float* Uk, cud
 
 cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float* Uw_t, float* Ut, float* sigma,
                             float* Vt, double* sig_raw, int32_t* perm, int32_t* status, cudaStream_t s,
-                            int* launches, bool uv_bk) {
+                            int* launches, bool uv_bk, uint16_t* u16, float* vs_out) {
   k_colnorm<<<nb * k, NT, 0, s>>>(b, Vw_t, sig_raw);
   k_rank<<<nb, 256, 0, s>>>(k, sig_raw, perm, sigma, status);
-  k_rows<<<nb * k, NT, 0, s>>>(b, k, Vw_t, Uw_t, perm, sig_raw, Ut, Vt, uv_bk ? 1 : 0);
+  k_rows<<<nb * k, NT, 0, s>>>(b, k, Vw_t, Uw_t, perm, sig_raw, Ut, Vt, uv_bk ? 1 : 0, u16, vs_out);
   *launches += 3;
   return cudaGetLastError();
 }

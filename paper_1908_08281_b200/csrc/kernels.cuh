@@ -43,7 +43,9 @@ cudaError_t launch_jacobi(int nb, int k, const float* L, float* Wf, int32_t* sta
 // finalize.cu -- sigma_j = ||V_w column j|| (fp64), sort, normalise, sign rule
 cudaError_t launch_finalize(int nb, int b, int k, const float* Vw_t, const float* Uw_t, float* Ut, float* sigma,
                             float* Vt, double* sig_raw, int32_t* perm, int32_t* status, cudaStream_t s,
-                            int* launches, bool uv_bk = false);
+                            int* launches, bool uv_bk = false, uint16_t* u16 = nullptr, float* vs_out = nullptr);
+// (u16: instead of Ut / Vt write U's 3xF16 twin (exponent 14, b % 32 == 0) and vs_out[i][j] = sign_j / sigma_j,
+//  the scale of v_j = vs B^T u~_j -- the fused apply's inputs, launch_apply_prep with perm / vs)
 // apply prep: rs[i][j] = scale / sigma[i][j]; flags singular sigma
 // (sigma, rs are [nb][ld]; the first k per block are used, the rest of rs is zeroed)
 cudaError_t launch_inv_sigma(int nb, int k, int ld, const float* sigma, float scale, float* rs, int32_t* status,
@@ -54,7 +56,9 @@ bool apply_fused_supported(int b, int k, int ldk, int T, const void* Ut, const v
 size_t apply_fused_amax_bytes(int nb);
 cudaError_t launch_apply_prep(const float* Ut, const float* Vt, int nb, int b, int k, int ldk, const float* Y, int T,
                               uint16_t* u16, uint16_t* v16, uint32_t* amax, int amax_ld, bool uv_unit,
-                              cudaStream_t s, int* launches);
+                              cudaStream_t s, int* launches, const int32_t* perm = nullptr, const float* vs = nullptr);
+// (perm / vs given: u16 is already written (launch_finalize), Ut is unused and Vt is the unsorted,
+//  unnormalised Vw_t [nb][k][b]: V's twin takes row perm[j] scaled by vs[j])
 cudaError_t launch_apply_fused(const float* sigma, int nb, int b, int k, int ldk, const float* Y, int T, float scale,
                                float* F, int32_t* status, const uint16_t* u16, const uint16_t* v16,
                                const uint32_t* amax, int amax_ld, cudaStream_t s, int* launches);
