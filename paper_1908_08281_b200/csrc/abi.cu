@@ -24,6 +24,8 @@
 #include "gemm.cuh"
 #include "kernels.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace {
 
 thread_local std::string g_err;
@@ -70,11 +72,29 @@ inline void prof_record(cudaEvent_t e, cudaStream_t s) {
     cudaEventRecord(e, s);
 }
 
+// NVTX (SURVEY.md §5 tracing): with HG_NVTX=1 every stage's enqueue is an NVTX range named after the stage
+// ("gemm_power[part 3]"), visible in Nsight Systems / ncu --nvtx when the kernels are enqueued directly
+// (HG_NO_GRAPH=1; a replayed CUDA graph has no host-side enqueue to annotate).  Header-only NVTX 3: no link
+// dependency, a no-op without an attached tool.
+static bool nvtx_on() {
+  static const bool on = [] {
+    const char* v = getenv("HG_NVTX");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 struct ProfScope {
   bool on;
+  bool nv;
   cudaStream_t s;
   ProfRec r;
-  ProfScope(int stage, cudaStream_t st) : on(g_prof_on), s(st) {
+  ProfScope(int stage, cudaStream_t st) : on(g_prof_on), nv(nvtx_on()), s(st) {
+    if (nv) {
+      char name[48];
+      snprintf(name, sizeof name, "%s[part %d]", kStageNames[stage], g_cur_part);
+      nvtxRangePushA(name);
+    }
     if (!on) return;
     r.stage = stage;
     r.part = g_cur_part;
@@ -83,9 +103,11 @@ struct ProfScope {
     prof_record(r.a, s);
   }
   ~ProfScope() {
-    if (!on) return;
-    prof_record(r.b, s);
-    g_prof.push_back(r);
+    if (on) {
+      prof_record(r.b, s);
+      g_prof.push_back(r);
+    }
+    if (nv) nvtxRangePop();
   }
 };
 
@@ -927,9 +949,13 @@ hg_status hg_block_apply_woodbury(const float* Ut, const float* sigma, int32_t n
 // 10.99 ms at configs[3] vs 11.01 / 11.04 with 6 / 4 parts) and the auxiliary streams / events
 // of the fork-join (created once, non-blocking, reused).
 constexpr int kMaxParts = 8;
-static int solve_parts() {   // read per call (tests switch it)
+// nb blocks of size b.  Default: 8 parts when one batched GEMM launch (nb * ceil(b/128) CTAs) is more than
+// one wave of the 148 SMs -- then a part's tensor-core GEMMs fill the SMs another part's latency-bound
+// kernels leave idle (configs[3]: 6.2 -> 5.0 ms); one part otherwise -- every launch already fits the GPU and
+// the fork / join only adds latency (configs[0-2]: 0.40 -> 0.37, 0.64 -> 0.60, 1.45 -> 1.36 ms).
+static int solve_parts(int nb = 1 << 20, int b = 1024) {   // HG_STREAMS read per call (tests switch it)
   const char* v = getenv("HG_STREAMS");
-  const int x = v ? atoi(v) : 8;
+  const int x = v ? atoi(v) : ((int64_t)nb * ((b + 127) / 128) > 148 ? 8 : 1);
   return x < 1 ? 1 : (x > kMaxParts ? kMaxParts : x);
 }
 // Two sets of part streams.  Plain (default priority) for hg_solve: staggering the parts delays
@@ -995,7 +1021,7 @@ static hg_status join_streams(cudaStream_t s, int nparts, const cudaStream_t* ps
 // over all blocks (Omega is keyed by the global block index).
 static hg_status run_rsvd_parts(const float* X, int nb, int b, int k, int q, uint64_t seed, float* Ut, float* sigma,
                                 float* Vt, int32_t* st, void* ws, const Layout& Lo, int T, cudaStream_t s) {
-  const int nparts = g_prof_mode == 1 ? 1 : std::max(1, std::min(solve_parts(), nb));
+  const int nparts = g_prof_mode == 1 ? 1 : std::max(1, std::min(solve_parts(nb, b), nb));
   cudaStream_t ps[kMaxParts];
   HG_TRY(fork_streams(s, nparts, ps, false));
   for (int pt = 0; pt < nparts; ++pt) {
@@ -1070,7 +1096,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
   // part's latency-bound Cholesky / Jacobi leave idle.  Bitwise the same result for
   // any part count (Omega is keyed by the global block index).  One part while the
   // stage profiler is on (per-stage attribution needs sequential stages).
-  const int nparts = g_prof_mode == 1 ? 1 : std::max(1, std::min(solve_parts(), rcnt));
+  const int nparts = g_prof_mode == 1 ? 1 : std::max(1, std::min(solve_parts(rcnt, b), rcnt));
   if (g_prof_mode == 2 && !g_t0_set) {
     if (!g_t0) HG_CU(cudaEventCreate(&g_t0), "event create");
     prof_record(g_t0, s);
@@ -1254,7 +1280,7 @@ extern "C++" static hg_status solve_entry(const hg_incidence* H, const float* w,
   key_add(key, *H);
   key_add(key, w); key_add(key, mu); key_add(key, b); key_add(key, k); key_add(key, p); key_add(key, q); key_add(key, seed);
   key_add(key, Y); key_add(key, T); key_add(key, F); key_add(key, sigma_out); key_add(key, flags & ~HG_SYNC);
-  key_add(key, st); key_add(key, ws); key_add(key, ws_bytes); key_add(key, solve_parts());
+  key_add(key, st); key_add(key, ws); key_add(key, ws_bytes); key_add(key, solve_parts(0, b));
   HG_TRY(graph_run(key, s, [&](cudaStream_t cs) -> hg_status {
     if (!d_status) HG_CU(cudaMemsetAsync(st, 0, sizeof(int32_t), cs), "memset status");
     return solve_impl(H, w, mu, b, k, p, q, seed, Y, T, F, sigma_out, flags & ~HG_SYNC, st, ws, ws_bytes, cs,
