@@ -434,14 +434,16 @@ def run_ours(args):
     tf32_peak_kind = "sustained (sw_power_cap seen in the timed region)" if power_capped else \
         "burst (no power cap in the timed region)"
     # the power products and Grams run 3xF16 on pre-split operands unless HG_GEMM_F16=0
-    f16_gemms = os.environ.get("HG_GEMM_F16", "1") != "0" and c.b % 8 == 0
+    f16_gemms = os.environ.get("HG_GEMM_F16", "1") != "0" and c.b % 32 == 0
+    apply_fused = "gemm_apply" in prof and round(prof["gemm_apply"][1] / args.steps) == 1
     # algorithmic work per launch
     nb, b, k, q, T = c.nb, c.b, c.k, c.q, c.T
     work = {
         "gemm_power": ("tensor", 2.0 * b * b * k * nb, 2 * q + 2),
         "gemm_gram": ("tensor", 2.0 * b * k * k * nb, 4 * q + 3),
         "gemm_qform": ("tensor", 2.0 * b * k * k * nb, 4 * q + 2),
-        "gemm_apply": ("tensor", 2.0 * b * k * T * nb, 2),
+        # the fused kernel (apply.cu: both products of Eq. 15 in one launch, 3xF16) or the two 3xTF32 GEMMs
+        "gemm_apply": ("tensor", (4.0 if apply_fused else 2.0) * b * k * T * nb, 1 if apply_fused else 2),
         "assemble": ("hbm", 4.0 * b * b * nb, 1),
     }
 
@@ -477,7 +479,7 @@ def run_ours(args):
         if bound == "tensor":
             useful = per_launch / avg_s / 1e12
             achieved = 3.0 * useful          # 3xTF32 / 3xF16: three tensor products per fp32 product
-            if stage in F16_STAGES and f16_gemms:
+            if (stage in F16_STAGES and f16_gemms) or (stage == "gemm_apply" and apply_fused):
                 # kind::f16 (3xF16 pre-split operands): the fp16 dense peak = the measured bf16 one
                 f16_burst, f16_sust = peaks["bf16_tflops"], peaks["bf16_tflops_sustained"]
                 f16_peak = f16_sust if power_capped else f16_burst
@@ -505,6 +507,15 @@ def run_ours(args):
     gemm_roof = roof("gemm_power")
     if gemm_roof and "gemm_power" in traffic:
         gemm_roof["traffic"] = traffic["gemm_power"]
+    # the fused Eq. 15 kernel: tensor work of both products, and its algorithmic HBM bytes (Y read + F written)
+    apply_roof = roof("gemm_apply")
+    if apply_roof:
+        apply_roof["fused"] = bool(apply_fused)
+        apply_roof["hbm_algorithmic_gbs"] = 2.0 * 4.0 * c.N * T / (apply_roof["avg_launch_ms"] / 1e3) / 1e9 * \
+            (1.0 if apply_fused else 0.5)
+        apply_roof["hbm_frac"] = apply_roof["hbm_algorithmic_gbs"] / peaks["hbm_gbs"]
+    if apply_roof and traffic.get("gemm_apply") and apply_fused:
+        apply_roof["traffic"] = traffic["gemm_apply"]
     dom_roof = roof(dominant) if dominant in work else None
     if dom_roof is None and dominant is not None:
         dom_roof = {"kernel": dominant, "bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None,
@@ -857,7 +868,7 @@ def run_ours(args):
         "solve_ms": ms, "blocks_per_s_per_gpu": c.nb / (ms / 1e3),
         "gemm_useful_tflops": gemm_useful_tflops,
         "gemm_tf32_pipe_frac": gemm_roof["frac"] if gemm_roof else None,
-        "roofline": dom_roof, "gemm_roofline": gemm_roof,
+        "roofline": dom_roof, "gemm_roofline": gemm_roof, "apply_roofline": apply_roof,
         "stages": stages, "profiled_ms_per_step": prof_ms_per_step,
         "jacobi_sweeps_avg": sweeps_avg, "jacobi_sweeps_max": dbg["jacobi_max_sweeps"],
         "e2e": {"value": (c.nb if shard else world * c.nb) / (e2e_ms / 1e3), "unit": "blocks/s",

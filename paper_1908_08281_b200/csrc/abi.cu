@@ -539,7 +539,8 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
     }
     Rsvd Rk{nb, k, k, simt, s, nullptr};
     float* J0t = nullptr;
-    HG_TRY(cholqr(Rk, Uk, Wf, G, Linv, work, st, 2, &J0t));   // work: Z is consumed (L2 tiles when k > 256)
+    static const int j0_passes = getenv("HG_J0_PASSES") ? atoi(getenv("HG_J0_PASSES")) : 2;
+    HG_TRY(cholqr(Rk, Uk, Wf, G, Linv, work, st, j0_passes < 2 ? 1 : 2, &J0t));   // work: Z is consumed (L2 tiles when k > 256)
     {
       GemmDesc g;   // W0 = L J0 (row-major, the layout the Jacobi reads L in)
       g.M = k; g.N = k; g.K = k; g.batch = nb;

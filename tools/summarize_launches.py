@@ -7,9 +7,10 @@ per-launch DRAM traffic of the bench's roofline kernels.
 
 Stage mapping for --traffic (launch order inside a step is fixed by run_rsvd):
   jacobi     -> k_jacobi_blk
-  cholinv    -> k_cholinv (mean over the step's launches)
-  assemble   -> k_seg_sort + k_assemble_rows (sum: one assembly)
-  gemm_power -> the step's first gemm_tf32x3 launch (Y0 = X Omega)
+  cholinv    -> k_cholinv* (mean over the step's launches)
+  assemble   -> the row-walk kernels (sum: one assembly)
+  gemm_power -> mean over the step's power-product launches (gemm_tc_kernel<256, 1, 1>)
+  gemm_apply -> k_apply_fused
 """
 import collections
 import csv
@@ -66,13 +67,15 @@ def main(argv):
         def per_launch(pred):
             xs = [x["dram"] for x in L if pred(x["name"])]
             return sum(xs) / len(xs) if xs else None
-        gemms = [x for x in L if x["name"].startswith("gemm_tf32x3")]
-        asm = [x["dram"] for x in L if x["name"] in ("k_seg_sort", "k_assemble_rows", "k_assemble")]
+        # power products: the 3xF16 twin kernel <256, 1, 1> (round 1: gemm_tf32x3); the first launch is Y0 = X Omega
+        gemms = [x for x in L if x["name"].startswith("gemm_tf32x3") or x["name"].startswith("gemm_tc_kernel<256, 1, 1>")]
+        asm = [x["dram"] for x in L if x["name"] in ("k_seg_sort", "k_assemble_rows", "k_assemble", "k_assemble_rows3")]
         traffic = {
             "jacobi": per_launch(lambda n: n.startswith("k_jacobi")),
-            "cholinv": per_launch(lambda n: n == "k_cholinv"),
+            "cholinv": per_launch(lambda n: n.startswith("k_cholinv")),
             "assemble": sum(asm) if asm else None,
-            "gemm_power": gemms[0]["dram"] if gemms else None,
+            "gemm_power": (sum(x["dram"] for x in gemms) / len(gemms)) if gemms else None,
+            "gemm_apply": per_launch(lambda n: n.startswith("k_apply_fused")),
             "source": path + " (ncu dram__bytes_read.sum + dram__bytes_write.sum, one step, bytes per launch)",
         }
         json.dump(traffic, open(traffic_out, "w"), indent=1)
