@@ -318,7 +318,8 @@ struct Rsvd {
     return gemm(g, s, simt, "Gram P^T P", ST_GEMM_GRAM);
   }
   // Q = P L^-T  ->  Q_t
-  hg_status qform(const float* P_t, const float* Linv, float* Q_t) const {
+  // need_f32 = false: only Q's twin is read afterwards (an intermediate basis feeds one power product)
+  hg_status qform(const float* P_t, const float* Linv, float* Q_t, bool need_f32 = true) const {
     GemmDesc g;
     g.M = b; g.N = k; g.K = k; g.batch = nb;
     g.A = P_t; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
@@ -332,6 +333,7 @@ struct Rsvd {
       tw->exp[o] = kNoTwin;
       if (!simt) {
         g.D16 = tw->h[o]; g.d_exp = f16_exp(2.f);
+        g.d16_only = !need_f32;
         tw->exp[o] = g.d_exp;
         tw->cb[o] = 2.f;
       }
@@ -367,8 +369,9 @@ static bool jacobi_precond_on(int k) {
 // CholeskyQR2 on a_t (result in a_t, scratch_t clobbered).  passes = 3 runs one more
 // pass (shifted CholeskyQR3): used for the first QR when 2k > b, where X Omega can be
 // ill-conditioned and k_cholinv's shifted retry leaves Q1 merely well-conditioned.
+// q_f32 = false: the result is only read through its 3xF16 twin (the last pass skips the fp32 store)
 hg_status cholqr(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* Linv, float* work, int32_t* st,
-                 int passes, float** q_out) {
+                 int passes, float** q_out, bool q_f32 = true) {
   float* src = a_t;
   float* dst = scratch_t;
   for (int p = 0; p < passes; ++p) {
@@ -377,7 +380,7 @@ hg_status cholqr(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* L
       ProfScope ps(ST_CHOLINV, R.s);
       HG_CU(launch_cholinv(R.nb, R.k, G, nullptr, Linv, work, st, R.s, &g_launches), "cholinv");
     }
-    HG_TRY(R.qform(src, Linv, dst));
+    HG_TRY(R.qform(src, Linv, dst, q_f32 || p + 1 < passes));
     float* tmp = src; src = dst; dst = tmp;
   }
   *q_out = src;   // a_t after an even pass count, scratch_t after an odd one
@@ -486,13 +489,16 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
     oth = (qn == cur) ? oth : cur;
     cur = qn;
   } else {
-    HG_TRY(cholqr(R, P[1], P[0], G, Linv, work, st, passes(true, q == 0), &cur));
+    // an intermediate basis is only the B operand of the next power product: with the twins on, its fp32
+    // copy is never read (the final S feeds U = S U~ in fp32)
+    const bool tw_on = R.tw != nullptr;
+    HG_TRY(cholqr(R, P[1], P[0], G, Linv, work, st, passes(true, q == 0), &cur, !tw_on || q == 0));
     oth = (cur == P[1]) ? P[0] : P[1];
     // loop i = 1..q: S~ = qr(X^T S), S = qr(X S~)
     for (int it = 0; it < 2 * q; ++it) {
       HG_TRY(R.power(cur, oth, it % 2 == 0));
       float* qn = nullptr;
-      HG_TRY(cholqr(R, oth, cur, G, Linv, work, st, passes(false, it == 2 * q - 1), &qn));
+      HG_TRY(cholqr(R, oth, cur, G, Linv, work, st, passes(false, it == 2 * q - 1), &qn, !tw_on || it == 2 * q - 1));
       oth = (qn == oth) ? cur : oth;
       cur = qn;
     }

@@ -66,6 +66,7 @@ struct EpiArgs {
   // fp16_rn(2^d_exp D) in the twin layout (tw_off) of D[g*sd + n*ldd + m] (both precisions)
   uint16_t* D16;
   float d_sc;
+  int d16_only;   // store only the twin
 };
 
 constexpr int NEPI = 256;            // converter / epilogue threads (8 warps)
@@ -426,7 +427,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (n < ea.N) {
             HG_DCHECK(mw0 + 4 * l4 + 3 < ea.ldd);
             const float4 v = *reinterpret_cast<const float4*>(st + j * TP + 4 * l4);
-            *reinterpret_cast<float4*>(dcol + (int64_t)n * ea.ldd) = v;
+            if (!ea.d16_only) *reinterpret_cast<float4*>(dcol + (int64_t)n * ea.ldd) = v;
             if (ea.D16) {
               uint2 hv, lv;
               split4(v, ea.d_sc, hv, lv);
@@ -443,7 +444,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (n < ea.N) {
             float val = acc[j] * rsv;
             if (ea.cs) val *= ea.cs[(int64_t)g * ea.scs + n];
-            Dg[(int64_t)n * ea.ldd + m] = val;
+            if (!ea.d16_only) Dg[(int64_t)n * ea.ldd + m] = val;
             if (ea.D16) {
               const float x = val * ea.d_sc;
               const __half hh = __float2half_rn(x);
@@ -723,7 +724,8 @@ cudaError_t launch_gemm(const GemmDesc& g, cudaStream_t stream, bool simt) {
   EpiArgs ea{g.M, g.N, g.K, g.D, g.ldd, g.sd, g.d_trans ? 1 : 0, alpha, g.rs, g.srs, g.cs, g.scs,
              g.a_mn ? 1 : 0, g.b_mn ? 1 : 0, trunc_hi, g.lower ? 1 : 0, g.C, g.ldc, g.sc, g.beta,
              (g.b_upper && (f16 || !g.b_mn)) ? 1 : 0,
-             ldexpf(1.0f, g.a_exp), ldexpf(1.0f, g.b_exp), g.D16, ldexpf(1.0f, g.d_exp)};
+             ldexpf(1.0f, g.a_exp), ldexpf(1.0f, g.b_exp), g.D16, ldexpf(1.0f, g.d_exp),
+             (g.D16 && g.d16_only) ? 1 : 0};
   if (simt) {
     if (g.A16 || g.B16) return cudaErrorInvalidValue;
     dim3 grid((g.M + 63) / 64, (g.N + 63) / 64, g.batch);

@@ -49,6 +49,7 @@ struct GemmDesc {
   // layout of D[g*sd + n*ldd + m] -- the B16 / A16 form of a later 3xF16 GEMM that reads D K-major.
   uint16_t* D16 = nullptr;
   int d_exp = 0;
+  bool d16_only = false;   // with D16: the fp32 D is not stored (nothing reads it), D may be null
 };
 
 // Enqueue the GEMM; returns cudaSuccess or the launch error.  `simt` selects the
