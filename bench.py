@@ -726,6 +726,54 @@ def run_ours(args):
 
         leg.append(leg_r2)
 
+    # Variant (opt-in, NOT the headline): HG_QR_SKIP_HALF=1 leaves the half-step basis S~ = qr(X^T S) of Alg. 1
+    # un-orthonormalised (Eq. 10 inside one iteration, Alg. 1's QR once per iteration) -- the
+    # same subspace, so the same F and sigma to rounding; reported next to the literal Alg. 1 of `value`
+    qrv = None
+    if not args.no_r2:
+        Fv = torch.empty((c.N, c.T), dtype=torch.float32, device=dev)
+        sv = torch.empty((c.nb, c.k), dtype=torch.float32, device=dev)
+        os.environ["HG_QR_SKIP_HALF"] = "1"
+
+        def qrv_step():
+            hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, sync=False, ws=ws, F=Fv, sigma=sv,
+                     status=status, stream=stream)
+
+        for _ in range(3):
+            qrv_step()
+        torch.cuda.synchronize(dev)
+        n_v = max(3, min(args.steps, 10))
+        v0_, v1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0_.record(stream)
+        for _ in range(n_v):
+            qrv_step()
+        v1_.record(stream)
+        torch.cuda.synchronize(dev)
+        os.environ.pop("HG_QR_SKIP_HALF")
+        qrv_ms = max_over_ranks(v0_.elapsed_time(v1_) / n_v, dev)
+        qrv = {"workload": "the bench workload with HG_QR_SKIP_HALF=1: one QR per power iteration (after X S~) "
+                           "instead of Alg. 1's two; opt-in, not the headline",
+               "solve_ms": qrv_ms, "blocks_per_s": world * c.nb / (qrv_ms / 1e3), "status": int(status.item()),
+               "F_vs_alg1_gpu_rel_fro": float(((Fv - F).norm() / F.norm()).item()) if not shard else None}
+
+        def leg_qrv():
+            import oracle
+            rov = oracle.solve(h.row_ptr, h.col_idx, h.w, h.Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed,
+                               blocks=[0, c.nb - 1])
+            Fgv, sgv = Fv.double().cpu().numpy(), sv.double().cpu().numpy()
+            fe, se = 0.0, 0.0
+            for s_, blk in enumerate(rov.blocks):
+                rows = slice(blk * c.b, (blk + 1) * c.b)
+                fo = rov.F[s_ * c.b:(s_ + 1) * c.b]
+                fe = max(fe, float(np.linalg.norm(Fgv[rows] - fo) / np.linalg.norm(fo)))
+                se = max(se, float(np.max(np.abs(sgv[blk] - rov.sigma[s_]) / rov.sigma[s_])))
+            qrv["parity"] = {"blocks": rov.blocks, "F_rel_fro": fe, "sigma_rel_max": se,
+                             "tol": {"F": 2e-5, "sigma": 1e-5}, "ok": fe <= 2e-5 and se <= 1e-5,
+                             "of": "against the oracle's literal Alg. 1"}
+
+        if not shard:
+            leg.append(leg_qrv)
+
     # one Eq. 12 Schur level over pairs of adjacent blocks (reading R2 inverses)
     sch = None
     if not args.no_schur and c.nb % 2 == 0:
@@ -878,7 +926,8 @@ def run_ours(args):
         "clocks": clk.summary(),
         "parity": parity,
         "cpu_baseline": cpu_base,
-        "next_rows": {"cg": cg, "r2_woodbury": r2, "schur": sch, "nested": nst, "weights": wts},
+        "next_rows": {"cg": cg, "r2_woodbury": r2, "schur": sch, "nested": nst, "weights": wts,
+                      "qr_once_per_iteration": qrv},
         "peaks": {"source": peak_src, "tf32_tflops_sustained": tf32_sust, "tf32_tflops_burst": tf32_burst,
                   "tf32_source": tf32_src, "tf32_denominator": tf32_peak_kind,
                   "tf32_measured": tf32_meas, "hbm_gbs": peaks["hbm_gbs"]},

@@ -495,8 +495,17 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
     HG_TRY(cholqr(R, P[1], P[0], G, Linv, work, st, passes(true, q == 0), &cur, !tw_on || q == 0));
     oth = (cur == P[1]) ? P[0] : P[1];
     // loop i = 1..q: S~ = qr(X^T S), S = qr(X S~)
+    // HG_QR_SKIP_HALF=1 (opt-in, measured in DESIGN.md §15; NOT Alg. 1 as printed): the half-step basis
+    // S~ = qr(X^T S) is left un-orthonormalised -- Y_i = X (X^T S_{i-1}) is Eq. 10 inside one iteration,
+    // with Alg. 1's QR once per iteration; same subspace, cond(Y_i) <= cond(X)^2 (4 at mu = 1)
+    const char* sh = getenv("HG_QR_SKIP_HALF");   // read per call (bench.py measures both)
+    const bool skip_half = sh && sh[0] == '1';
     for (int it = 0; it < 2 * q; ++it) {
       HG_TRY(R.power(cur, oth, it % 2 == 0));
+      if (skip_half && tw_on && it % 2 == 0) {
+        float* t = cur; cur = oth; oth = t;
+        continue;
+      }
       float* qn = nullptr;
       HG_TRY(cholqr(R, oth, cur, G, Linv, work, st, passes(false, it == 2 * q - 1), &qn, !tw_on || it == 2 * q - 1));
       oth = (qn == oth) ? cur : oth;
@@ -1199,7 +1208,7 @@ constexpr size_t kMaxGraphs = 8;
 std::string knob_env() {   // enqueue-time knobs that change the captured sequence
   std::string e;
   for (const char* n : {"HG_ASSEMBLE", "HG_STREAMS_SERIAL", "HG_BN_POWER", "HG_BN_GRAM", "HG_BN_QFORM", "HG_GRAM_FULL",
-                        "HG_QR_PASSES", "HG_STREAM_PRIO", "HG_GEMM_F16", "HG_JACOBI_PRE"}) {
+                        "HG_QR_PASSES", "HG_STREAM_PRIO", "HG_GEMM_F16", "HG_JACOBI_PRE", "HG_QR_SKIP_HALF"}) {
     const char* v = getenv(n);
     e += v ? v : "-";
     e += '|';

@@ -445,6 +445,28 @@ def test_qr_passes_knob_both_parity_green(inputs, cfg, monkeypatch):
     assert rel(F1.double().cpu().numpy(), F2.double().cpu().numpy()) <= 1e-5
 
 
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_qr_skip_half_variant_parity_green(inputs, cfg, monkeypatch):
+    """HG_QR_SKIP_HALF=1 (opt-in variant): the half-step basis S~ = qr(X^T S) of Alg. 1
+     stays un-orthonormalised -- Eq. 10 inside one iteration, one QR
+    per iteration.  range(S) is unchanged, so F and sigma still match the oracle's literal Alg. 1."""
+    hg = hgm()
+    h = inputs(cfg)
+    c = CONFIGS[cfg]
+    H, w, Y = dev_inputs(h)
+    F1, s1, st1 = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    monkeypatch.setenv("HG_QR_SKIP_HALF", "1")
+    F2, s2, st2 = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    n2 = hg.last_launch_count()
+    monkeypatch.delenv("HG_QR_SKIP_HALF")
+    F3, s3, st3 = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    n3 = hg.last_launch_count()
+    assert int(st2.item()) == 0 and n2 < n3          # fewer launches: the variant really ran
+    assert torch.equal(F1, F3) and torch.equal(s1, s3)   # and the default is back afterwards
+    check_against_oracle(h, c, F2, s2, list(range(c.nb)) if cfg < 3 else [0, c.nb - 1])
+    assert rel(F1.double().cpu().numpy(), F2.double().cpu().numpy()) <= 1e-5
+
+
 def test_solve_without_rhs_returns_sigma_only(inputs):
     """T = 0 (no right-hand sides): the factorisation runs, sigma matches the oracle, F is empty."""
     hg = hgm()
