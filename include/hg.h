@@ -159,7 +159,10 @@ hg_status hg_workspace_size_ex(int32_t N, int32_t E, int64_t nnz, int32_t b, int
  *   F_i = scale * V_i diag(1/sigma_i) U_i^T Y_i,   Y_i = rows [ib,(i+1)b) of Y.
  *   Y, F [nb*b][T];  scale = mu/(1+mu) for Eq. 3.
  *   T >= 0 arbitrary (T % 4 != 0: Y and F pass through 16-byte-pitched workspace copies).
- * Device errors: HG_ST_SINGULAR_SIGMA (sigma_j <= 1e-6 sigma_1; reading A14). */
+ * One fused kernel (c / sigma, both products, the k x T intermediate on chip; 3xF16 with the operand
+ * exponents taken from per-block maxima of Y, Ut, Vt) when k <= 256, k % 32 == 0 and b % 32 == 0;
+ * otherwise a scale kernel and two 3xTF32 GEMMs.  Either way F matches the FP64 definition to ~2e-6.
+ * Device errors: HG_ST_SINGULAR_SIGMA (sigma_j <= 1e-6 sigma_1; reading A14: that triplet is dropped). */
 hg_status hg_block_apply_inverse(const float* Ut, const float* sigma, const float* Vt, int32_t nb, int32_t b,
                                  int32_t k, const float* Y, int32_t T, float scale, float* F,
                                  int32_t* d_status, void* ws, size_t ws_bytes, hg_stream_t stream);

@@ -245,7 +245,6 @@ constexpr int kNoTwin = -99;
 struct Twins {
   const float* f[4] = {nullptr, nullptr, nullptr, nullptr};
   uint16_t* h[4] = {nullptr, nullptr, nullptr, nullptr};
-  int64_t lo = 0;
   int exp[4] = {kNoTwin, kNoTwin, kNoTwin, kNoTwin};
   float cb[4] = {0.f, 0.f, 0.f, 0.f};
   int find(const float* p) const {
@@ -268,7 +267,6 @@ struct Rsvd {
   const float* X;
   bool general = false;   // HG_GENERAL: X^T products use the literal transpose (else X^T = X, reading A12)
   const uint16_t* X16 = nullptr;   // pre-split X (exponent 14, |X_ij| <= 1): 3xF16 power products
-  int64_t x_lo = 0;
   Twins* tw = nullptr;
 
   // out_t = (X P)^T  with P given as P_t [k][b]; trans: (X^T P)^T, the literal X^T only when general
@@ -392,7 +390,6 @@ hg_status cholqr(const Rsvd& R, float* a_t, float* scratch_t, float* G, float* L
 struct Bufs {
   float* P[4];
   uint16_t* P16[4];   // 3xF16 twins of P (common.cuh tw_off layout: 2 fp16 per element)
-  int64_t p16_lo;
   float *G, *L, *Linv, *Wf, *Uk, *work, *eig, *rs, *Z, *Yp, *Fp;
   double* sig;
   int32_t* perm;
@@ -407,7 +404,6 @@ Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k,
   const int64_t kb = (int64_t)blk0 * k * b, kk = (int64_t)blk0 * k * k, k1 = (int64_t)blk0 * k;
   for (int i = 0; i < 4; ++i) B.P[i] = at<float>(ws, Lo.P[i]) + kb;
   for (int i = 0; i < 4; ++i) B.P16[i] = at<uint16_t>(ws, Lo.P16[i]) + 2 * kb;   // twin of the part's panels (tw_off)
-  B.p16_lo = (int64_t)nb_total * k * b;
   B.G = at<float>(ws, Lo.G) + kk;
   B.L = at<float>(ws, Lo.L) + kk;
   B.Linv = at<float>(ws, Lo.Linv) + kk;
@@ -433,7 +429,7 @@ Bufs part_bufs(void* ws, const Layout& Lo, int nb_total, int blk0, int b, int k,
 // and orthonormalised once (shifted CholeskyQR3).
 hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64_t seed, bool simt, float* Ut,
                    float* sigma, float* Vt, int32_t* st, const Bufs& Bf, cudaStream_t s, int scheme = 0,
-                   bool general = false, bool uv_bk = false, const uint16_t* X16 = nullptr, int64_t x_lo = 0) {
+                   bool general = false, bool uv_bk = false, const uint16_t* X16 = nullptr) {
   Rsvd R{nb, b, k, simt, s, X, general};
   Twins tw;
   if (X16 && !simt && !general) {
@@ -441,9 +437,7 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
       tw.f[i] = Bf.P[i];
       tw.h[i] = Bf.P16[i];
     }
-    tw.lo = Bf.p16_lo;
     R.X16 = X16;
-    R.x_lo = x_lo;
     R.tw = &tw;
   }
   float* P[4];
@@ -462,7 +456,7 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
     if (R.tw) {   // |Omega_ij| <= 8.7: only the twin, for the first 3xF16 power product
       tw.exp[0] = f16_exp(8.7f);
       tw.cb[0] = 8.7f * sqrtf((float)b);
-      HG_CU(launch_omega_panels(seed, blk0, nb, b, k, P[0], s, &g_launches, tw.h[0], tw.lo, tw.exp[0]), "omega");
+      HG_CU(launch_omega_panels(seed, blk0, nb, b, k, P[0], s, &g_launches, tw.h[0], tw.exp[0]), "omega");
     } else {
       HG_CU(launch_omega_panels(seed, blk0, nb, b, k, P[0], s, &g_launches), "omega");
     }
@@ -697,12 +691,11 @@ hg_status run_degrees(const hg_incidence* H, const float* w, int b, float* dvr, 
 
 // Eq. 1 blocks [blk0, blk0 + nb) of the N/b diagonal blocks (degrees already computed)
 hg_status run_assemble(const hg_incidence* H, float mu, int b, bool raw, int blk0, int nb, float* blocks,
-                       const float* dvr, void* ws, const Layout& Lo, cudaStream_t s, uint16_t* x16 = nullptr,
-                       int64_t x_lo = 0) {
+                       const float* dvr, void* ws, const Layout& Lo, cudaStream_t s, uint16_t* x16 = nullptr) {
   ProfScope ps(ST_ASSEMBLE, s);
   HG_CU(launch_assemble(blk0, nb, H->n_vertices / b, b, H->n_edges, H->nnz, H->row_ptr, H->col_idx,
                         at<float>(ws, Lo.eval), dvr, mu, raw, blocks, at<void>(ws, Lo.keys), s, &g_launches, x16,
-                        x_lo, x16 != nullptr),
+                        x16 != nullptr),
         "assemble");
   return HG_OK;
 }
@@ -884,21 +877,20 @@ hg_status hg_block_rsvd_ex(const float* blocks, int32_t nb, int32_t b, int32_t k
   const bool general = (flags & HG_GENERAL) != 0, uv_bk = (flags & HG_UV_BK) != 0;
   // HG_X_UNIT: the caller's bound |X_ij| <= 1, ||X||_2 <= 1 makes the 3xF16 twins safe (as in hg_solve)
   uint16_t* x16 = ((flags & HG_X_UNIT) && !general && f16_on(b, simt)) ? at<uint16_t>(ws, Lo.X16) : nullptr;
-  const int64_t x_lo = (int64_t)nb * b * b;
   if (x16) {
     HG_CU(launch_f16_split(blocks, (int64_t)nb * b, b, b, 14, x16, s), "blocks split");
     ++g_launches;
   }
   if (p == 0)
     return run_rsvd(blocks, nb, 0, b, k, q, seed, simt, Ut, sigma, Vt, d_status, part_bufs(ws, Lo, nb, 0, b, k, 0), s,
-                    scheme, general, uv_bk, x16, x_lo);
+                    scheme, general, uv_bk, x16);
   if (uv_bk) return fail(HG_ERR_INVALID, "HG_UV_BK is not supported with oversampling (p > 0)");
   // oversampled: factor at width l into the workspace, keep the top k triplets (rank-k truncation)
   float* Ul = at<float>(ws, Lo.Ut);
   float* Vl = at<float>(ws, Lo.Vt);
   float* sl = at<float>(ws, Lo.sigl);
   HG_TRY(run_rsvd(blocks, nb, 0, b, l, q, seed, simt, Ul, sl, Vl, d_status, part_bufs(ws, Lo, nb, 0, b, l, 0), s,
-                  scheme, general, false, x16, x_lo));
+                  scheme, general, false, x16));
   HG_CU(cudaMemcpy2DAsync(Ut, 4 * (size_t)k * b, Ul, 4 * (size_t)l * b, 4 * (size_t)k * b, nb, cudaMemcpyDeviceToDevice,
                           s), "truncate U");
   HG_CU(cudaMemcpy2DAsync(Vt, 4 * (size_t)k * b, Vl, 4 * (size_t)l * b, 4 * (size_t)k * b, nb, cudaMemcpyDeviceToDevice,
@@ -1152,8 +1144,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     // with the 3xF16 products the assembly writes the blocks' twin (|X_ij|, |Theta_ij| <= 1: exponent 14)
     // instead of fp32 blocks -- nothing downstream reads those
     uint16_t* x16 = f16_on(b, simt) ? at<uint16_t>(ws, Lo.X16) : nullptr;
-    const int64_t x_lo = (int64_t)nb * b * b;
-    HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[pt], x16, x_lo));
+    HG_TRY(run_assemble(H, mu, b, woodbury, blk0, nbp, blocks, dvr, ws, Lo, ps[pt], x16));
     if (x16) x16 += 2 * (int64_t)blk0 * b * b;
     // HG_JACOBI_WIDE = bitmask of parts whose Jacobi runs on 64-row cluster CTAs (twice the SMs
     // per block: a shorter per-block latency for that part).  Off by default in BOTH entries: the
@@ -1164,8 +1155,7 @@ static hg_status solve_impl(const hg_incidence* H, const float* w, float mu, int
     static const int wide_rows = getenv("HG_JACOBI_WIDE_ROWS") ? atoi(getenv("HG_JACOBI_WIDE_ROWS")) : 64;
     jacobi_rows_hint(((wide >> pt) & 1) ? wide_rows : 0);
     hg_status rs = run_rsvd(blocks + (int64_t)blk0 * b * b, nbp, blk0, b, l, q, seed, simt, Ut + kb,
-                            sigma + (int64_t)(blk0 - soff) * l, Vt + kb, st, Bf, ps[pt], scheme, false, false, x16,
-                            x_lo);
+                            sigma + (int64_t)(blk0 - soff) * l, Vt + kb, st, Bf, ps[pt], scheme, false, false, x16);
     jacobi_rows_hint(0);
     HG_TRY(rs);
     if (cps) HG_CU(cudaStreamWaitEvent(ps[pt], ev_y[pt], 0), "wait Y");

@@ -10,9 +10,9 @@ cudaError_t launch_degrees(int N, int E, int64_t nnz, const int64_t* row_ptr, co
 cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_t nnz, const int64_t* row_ptr,
                             const int32_t* col_idx, const float* edge_val, const float* dv_rsqrt, float mu,
                             bool raw_theta, float* blocks, void* keys_ws, cudaStream_t s, int* launches,
-                            uint16_t* x16 = nullptr, int64_t x_lo = 0, bool skip_f32 = false);
-// (x16: also write the 3xF16 twin of the blocks -- hi / lo fp16 planes of 2^14 X at x16[i] and
-//  x16[x_lo + i]; skip_f32: the fp32 blocks are not needed (written anyway on the fallback paths))
+                            uint16_t* x16 = nullptr, bool skip_f32 = false);
+// (x16: also write the 3xF16 twin of the blocks, 2^14 X in the tw_off layout of common.cuh;
+//  skip_f32: the fp32 blocks are not needed (written anyway on the fallback paths))
 size_t assemble_keys_bytes(int64_t nnz, int nb, int E);
 // grouped assembly (default when nb * E is small enough): degrees and the (block, edge) grouping of the
 // incidences of all nb_total blocks once per solve (instead of launch_degrees), before launch_assemble
@@ -25,8 +25,8 @@ cudaError_t launch_degrees_grouped(int nb_total, int b, int E, int64_t nnz, cons
 // panel: out[i][c][m] = Omega[i*b + m][c] (Omega is N x k, normal index r*k + c)
 cudaError_t launch_omega_panels(uint64_t seed, int blk0, int nb, int b, int k, float* out, cudaStream_t s,
                                 int* launches,
-                                uint16_t* out16 = nullptr, int64_t lo = 0, int exp = 0);
-// (out16: write only the 3xF16 twin -- hi / lo fp16 planes of 2^exp Omega -- not out)
+                                uint16_t* out16 = nullptr, int exp = 0);
+// (out16: write only the 3xF16 twin of 2^exp Omega (common.cuh tw_off layout) -- not out)
 // row-major rows x cols: out[r][c] = normal r*cols + c
 cudaError_t launch_gaussian_rowmajor(uint64_t seed, int rows, int cols, float* out, cudaStream_t s,
                                      int* launches);

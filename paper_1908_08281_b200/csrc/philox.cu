@@ -56,7 +56,7 @@ __global__ void k_gauss(uint64_t seed, int64_t total, float* __restrict__ out) {
 // covers 32 consecutive m, i.e. every store instruction writes one 128-byte line.
 // out16 (3xF16 twin, instead of out): 2^exp Omega in the tw_off layout (common.cuh) of out.
 __global__ void k_gauss_panel(uint64_t seed, int64_t blk0, int b, int k, float* __restrict__ out,
-                              uint16_t* __restrict__ out16, int64_t lo, float sc) {
+                              uint16_t* __restrict__ out16, float sc) {
   const int local = blockIdx.x * blockDim.x + threadIdx.x;   // (c/4) * b + m
   if (local >= b * (k / 4)) return;
   const int m = local % b, c = 4 * (local / b);
@@ -84,9 +84,9 @@ __global__ void k_gauss_panel(uint64_t seed, int64_t blk0, int b, int k, float* 
 }  // namespace
 
 cudaError_t launch_omega_panels(uint64_t seed, int blk0, int nb, int b, int k, float* out, cudaStream_t s,
-                                int* launches, uint16_t* out16, int64_t lo, int exp) {
+                                int* launches, uint16_t* out16, int exp) {
   const int per = b * (k / 4);
-  k_gauss_panel<<<dim3((per + 255) / 256, nb), 256, 0, s>>>(seed, blk0, b, k, out, out16, lo, ldexpf(1.f, exp));
+  k_gauss_panel<<<dim3((per + 255) / 256, nb), 256, 0, s>>>(seed, blk0, b, k, out, out16, ldexpf(1.f, exp));
   ++*launches;
   return cudaGetLastError();
 }

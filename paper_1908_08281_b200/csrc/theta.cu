@@ -763,8 +763,7 @@ __global__ void __launch_bounds__(R2_NT) k_assemble_rows3(int blk0, int b, const
                                                           const int2* __restrict__ rng,
                                                           const float* __restrict__ eval,
                                                           const float* __restrict__ dvr, float inv1pmu, int raw,
-                                                          float* __restrict__ blocks, uint16_t* __restrict__ x16,
-                                                          int64_t x_lo) {
+                                                          float* __restrict__ blocks, uint16_t* __restrict__ x16) {
   const int blk = blk0 + blockIdx.x;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   float* acc = reinterpret_cast<float*>(smem_raw);                                  // [R2_ROWS][b]
@@ -966,7 +965,7 @@ cudaError_t launch_degrees_grouped(int nb_total, int b, int E, int64_t nnz, cons
 cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_t nnz, const int64_t* row_ptr,
                             const int32_t* col_idx, const float* edge_val, const float* dv_rsqrt, float mu,
                             bool raw_theta, float* blocks, void* keys_ws, cudaStream_t s, int* launches,
-                            uint16_t* x16, int64_t x_lo, bool skip_f32) {
+                            uint16_t* x16, bool skip_f32) {
   uint32_t* keys = reinterpret_cast<uint32_t*>(keys_ws);
   int32_t* overflow = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(keys_ws) + al256((size_t)nnz * 4));
   int2* rng = reinterpret_cast<int2*>(reinterpret_cast<char*>(keys_ws) + al256((size_t)nnz * 4) +
@@ -984,7 +983,7 @@ cudaError_t launch_assemble(int blk0, int nb, int nb_total, int b, int E, int64_
     }
     k_assemble_rows3<<<dim3(nb, (b + R2_ROWS - 1) / R2_ROWS), R2_NT, smem, s>>>(
         blk0, b, row_ptr, col_idx, keys, rng, edge_val, dv_rsqrt, 1.0f / (1.0f + mu), raw_theta ? 1 : 0,
-        (x16 && skip_f32) ? nullptr : blocks, x16, x_lo);
+        (x16 && skip_f32) ? nullptr : blocks, x16);
     ++*launches;
     return cudaGetLastError();
   }
