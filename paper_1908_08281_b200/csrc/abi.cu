@@ -26,6 +26,12 @@
 
 #include <nvtx3/nvToolsExt.h>
 
+// A part's side stream (defined next to the part streams below): side_fork makes the side stream of the
+// current part wait for everything enqueued on `main` so far and returns it (or `main` itself when the
+// streams cannot be made); side_join makes `main` wait for the side stream.  Plain graph edges under capture.
+static cudaStream_t side_fork(cudaStream_t main_s);
+static void side_join(cudaStream_t main_s, cudaStream_t side);
+
 namespace {
 
 thread_local std::string g_err;
@@ -271,7 +277,8 @@ struct Rsvd {
 
   // out_t = (X P)^T  with P given as P_t [k][b]; trans: (X^T P)^T, the literal X^T only when general
   // (X symmetric: X^T P = X P, reading A12)
-  hg_status power(const float* P_t, float* out_t, bool trans = false) const {
+  // want_twin = false: the output is read as fp32 only (the lazy QR's W = X Y)
+  hg_status power(const float* P_t, float* out_t, bool trans = false, bool want_twin = true) const {
     GemmDesc g;
     g.M = b; g.N = k; g.K = b; g.batch = nb;
     g.A = X; g.a_mn = trans && general; g.lda = b; g.sa = (int64_t)b * b;
@@ -290,7 +297,7 @@ struct Rsvd {
     }
     if (o >= 0) {
       tw->exp[o] = kNoTwin;
-      if (f16) {   // |(X P)_ij| <= cb(P); the column norms do not grow either
+      if (f16 && want_twin) {   // |(X P)_ij| <= cb(P); the column norms do not grow either
         g.D16 = tw->h[o]; g.d_exp = f16_exp(tw->cb[i]);
         tw->exp[o] = g.d_exp;
         tw->cb[o] = tw->cb[i];
@@ -486,14 +493,53 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
     // an intermediate basis is only the B operand of the next power product: with the twins on, its fp32
     // copy is never read (the final S feeds U = S U~ in fp32)
     const bool tw_on = R.tw != nullptr;
-    HG_TRY(cholqr(R, P[1], P[0], G, Linv, work, st, passes(true, q == 0), &cur, !tw_on || q == 0));
-    oth = (cur == P[1]) ? P[0] : P[1];
-    // loop i = 1..q: S~ = qr(X^T S), S = qr(X S~)
     // HG_QR_SKIP_HALF=1 (opt-in, measured in DESIGN.md §15; NOT Alg. 1 as printed): the half-step basis
     // S~ = qr(X^T S) is left un-orthonormalised -- Y_i = X (X^T S_{i-1}) is Eq. 10 inside one iteration,
     // with Alg. 1's QR once per iteration; same subspace, cond(Y_i) <= cond(X)^2 (4 at mu = 1)
     const char* sh = getenv("HG_QR_SKIP_HALF");   // read per call (bench.py measures both)
     const bool skip_half = sh && sh[0] == '1';
+    const char* lz = getenv("HG_QR_LAZY");
+    const bool lazy = tw_on && !skip_half && !(lz && lz[0] == '0');
+    if (lazy) {
+      // Lazy application of an intermediate QR: the next panel of Alg. 1 is
+      //   Y_{j+1} = X S_j = X (Y_j R_j^-1) = (X Y_j) R_j^-1,
+      // so W = X Y_j runs on the part's side stream WHILE the main stream forms Y_j^T Y_j and its Cholesky
+      // factor R_j (the chain's longest kernel); one Q-formation GEMM then gives Y_{j+1} = W R_j^-1.  Every
+      // QR of Alg. 1 is still computed -- S_j is applied through associativity instead of being stored -- and
+      // the power product leaves the chain.  QRs that take more than one pass (the first one when 2k > b,
+      // HG_QR_PASSES=2) and the final S are formed explicitly as before.
+      float* Yc = P[1];   // Y_j (twin valid; fp32 valid when the explicit path needs it)
+      float* Wb = P[0];
+      auto pj = [&](int j) { return passes(j == 0, false); };
+      for (int j = 0; j < 2 * q; ++j) {
+        const bool next_lazy = j + 1 < 2 * q && pj(j + 1) == 1;
+        if (pj(j) == 1) {
+          cudaStream_t side = side_fork(s);
+          Rsvd Rs = R;
+          Rs.s = side;
+          HG_TRY(Rs.power(Yc, Wb, j % 2 == 0, false));
+          HG_TRY(R.gram(Yc, G));
+          {
+            ProfScope ps(ST_CHOLINV, s);
+            HG_CU(launch_cholinv(nb, k, G, nullptr, Linv, work, st, s, &g_launches), "cholinv");
+          }
+          side_join(s, side);
+          HG_TRY(R.qform(Wb, Linv, Yc, !next_lazy));
+        } else {
+          float* qn = nullptr;
+          HG_TRY(cholqr(R, Yc, Wb, G, Linv, work, st, pj(j), &qn, false));
+          float* other = (qn == Yc) ? Wb : Yc;
+          HG_TRY(R.power(qn, other, j % 2 == 0));
+          Yc = other;
+          Wb = qn;
+        }
+      }
+      HG_TRY(cholqr(R, Yc, Wb, G, Linv, work, st, passes(q == 0, true), &cur, true));
+      oth = (cur == Yc) ? Wb : Yc;
+    } else {
+    HG_TRY(cholqr(R, P[1], P[0], G, Linv, work, st, passes(true, q == 0), &cur, !tw_on || q == 0));
+    oth = (cur == P[1]) ? P[0] : P[1];
+    // loop i = 1..q: S~ = qr(X^T S), S = qr(X S~)
     for (int it = 0; it < 2 * q; ++it) {
       HG_TRY(R.power(cur, oth, it % 2 == 0));
       if (skip_half && tw_on && it % 2 == 0) {
@@ -504,6 +550,7 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
       HG_TRY(cholqr(R, oth, cur, G, Linv, work, st, passes(false, it == 2 * q - 1), &qn, !tw_on || it == 2 * q - 1));
       oth = (qn == oth) ? cur : oth;
       cur = qn;
+    }
     }
   }
   // step 4: B = S^T X, stored as B [k][b] = (X^T S)^T
@@ -974,6 +1021,8 @@ static int solve_parts(int nb = 1 << 20, int b = 1024) {   // HG_STREAMS read pe
 // priorities hold under replay.  HG_STREAM_PRIO=0/1 forces one set for both entries.
 // per host thread (concurrent hg_solve calls from different threads never share events)
 static thread_local cudaStream_t g_aux[2][kMaxParts] = {};
+static thread_local cudaStream_t g_side[kMaxParts] = {};   // per part: the lazy QR's concurrent power product
+static thread_local cudaEvent_t g_ev_side[2][kMaxParts] = {};
 static thread_local cudaEvent_t g_ev_fork = nullptr, g_ev_join[kMaxParts] = {};
 // library streams / events, created once and outside any stream capture
 static hg_status ensure_streams() {
@@ -986,11 +1035,30 @@ static hg_status ensure_streams() {
       if (pr > least) pr = least;
       HG_CU(cudaStreamCreateWithPriority(&g_aux[set][p], cudaStreamNonBlocking, pr), "stream create");
     }
-  for (int p = 0; p < kMaxParts; ++p)
+  for (int p = 0; p < kMaxParts; ++p) {
     HG_CU(cudaEventCreateWithFlags(&g_ev_join[p], cudaEventDisableTiming), "event create");
+    HG_CU(cudaStreamCreateWithFlags(&g_side[p], cudaStreamNonBlocking), "stream create");
+    for (int i = 0; i < 2; ++i) HG_CU(cudaEventCreateWithFlags(&g_ev_side[i][p], cudaEventDisableTiming), "event create");
+  }
   HG_CU(cudaEventCreateWithFlags(&g_ev_fork, cudaEventDisableTiming), "event create");
   return HG_OK;
 }
+extern "C++" {
+static cudaStream_t side_fork(cudaStream_t main_s) {
+  if (ensure_streams() != HG_OK) return main_s;
+  const int p = g_cur_part;
+  if (p < 0 || p >= kMaxParts) return main_s;
+  if (cudaEventRecord(g_ev_side[0][p], main_s) != cudaSuccess) return main_s;
+  if (cudaStreamWaitEvent(g_side[p], g_ev_side[0][p], 0) != cudaSuccess) return main_s;
+  return g_side[p];
+}
+static void side_join(cudaStream_t main_s, cudaStream_t side) {
+  if (side == main_s) return;
+  const int p = g_cur_part;
+  cudaEventRecord(g_ev_side[1][p], side);
+  cudaStreamWaitEvent(main_s, g_ev_side[1][p], 0);
+}
+}  // extern "C++"
 static bool use_prio_streams(bool host_entry) {
   const char* pv = getenv("HG_STREAM_PRIO");
   if (pv && (pv[0] == '0' || pv[0] == '1')) return pv[0] == '1';
@@ -1198,7 +1266,7 @@ constexpr size_t kMaxGraphs = 8;
 std::string knob_env() {   // enqueue-time knobs that change the captured sequence
   std::string e;
   for (const char* n : {"HG_ASSEMBLE", "HG_STREAMS_SERIAL", "HG_BN_POWER", "HG_BN_GRAM", "HG_BN_QFORM", "HG_GRAM_FULL",
-                        "HG_QR_PASSES", "HG_STREAM_PRIO", "HG_GEMM_F16", "HG_JACOBI_PRE", "HG_QR_SKIP_HALF"}) {
+                        "HG_QR_PASSES", "HG_STREAM_PRIO", "HG_GEMM_F16", "HG_JACOBI_PRE", "HG_QR_SKIP_HALF", "HG_QR_LAZY"}) {
     const char* v = getenv(n);
     e += v ? v : "-";
     e += '|';

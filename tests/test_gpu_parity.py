@@ -467,6 +467,26 @@ def test_qr_skip_half_variant_parity_green(inputs, cfg, monkeypatch):
     assert rel(F1.double().cpu().numpy(), F2.double().cpu().numpy()) <= 1e-5
 
 
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_lazy_qr_and_explicit_qr_both_parity_green(inputs, cfg, monkeypatch):
+    """Default: an intermediate S_j = Y_j R_j^-1 of Alg. 1 is applied lazily,
+    Y_{j+1} = (X Y_j) R_j^-1, with X Y_j concurrent to the Cholesky; HG_QR_LAZY=0 forms every
+    S_j explicitly.  The same matrices up to rounding: both meet the oracle tolerances and agree closely."""
+    hg = hgm()
+    h = inputs(cfg)
+    c = CONFIGS[cfg]
+    H, w, Y = dev_inputs(h)
+    F1, s1, st1 = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    monkeypatch.setenv("HG_QR_LAZY", "0")
+    F2, s2, st2 = hg.solve(H, w, Y, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=c.seed)
+    monkeypatch.delenv("HG_QR_LAZY")
+    assert int(st1.item()) == 0 and int(st2.item()) == 0
+    blocks = list(range(c.nb)) if cfg < 3 else [0, c.nb - 1]
+    check_against_oracle(h, c, F1, s1, blocks)
+    check_against_oracle(h, c, F2, s2, blocks)
+    assert rel(F1.double().cpu().numpy(), F2.double().cpu().numpy()) <= 1e-5
+
+
 def test_solve_without_rhs_returns_sigma_only(inputs):
     """T = 0 (no right-hand sides): the factorisation runs, sigma matches the oracle, F is empty."""
     hg = hgm()
