@@ -1045,6 +1045,7 @@ static hg_status ensure_streams() {
 }
 extern "C++" {
 static cudaStream_t side_fork(cudaStream_t main_s) {
+  if (g_prof_mode == 1) return main_s;   // per-stage totals: stages in sequence, each timed alone
   if (ensure_streams() != HG_OK) return main_s;
   const int p = g_cur_part;
   if (p < 0 || p >= kMaxParts) return main_s;
