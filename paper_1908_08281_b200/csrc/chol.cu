@@ -401,12 +401,11 @@ __global__ void __maxnreg__(128) k_cholinv(int k, const float* __restrict__ G, f
 // ================================================================== k_cholinv2 (k <= 256)
 // All 16 warps share every phase (no single-warp tile loops on the critical path):
 //   per panel p:  warp 0 factors the diagonal tile (row per lane, the pivot column broadcast
-//                 through a double-buffered shared column -- no shuffle chains) and inverts it,
-//                 D_p = L_pp^-1 (kept beside the tiles);
-//                 all warps: L_ip = A_ip D_p^T (TRSM as a product, i > p), then the trailing
+//                 through a double-buffered shared column -- no shuffle chains);
+//                 L_ip = A_ip L_pp^-T by forward substitution, a panel row per thread (i > p), then the trailing
 //                 update A_ij -= L_ip L_jp^T -- 16-row half-tile units, 4 x 4 outputs per lane,
 //                 float4 operand rows (8 LDS.128 per 64 FMA, conflict-free);
-//   triangular inverse: X_ii = D_i, then block columns j = nt-2 .. 0: T_i = sum_{m=j+1..i} X_im L_mj
+//   triangular inverse: D_i = L_ii^-1 (a warp per tile, in parallel), X_ii = D_i, then block columns j = nt-2 .. 0: T_i = sum_{m=j+1..i} X_im L_mj
 //                 into the (then free) D area, X_ij = -T_i D_j -- the LAPACK trtri order, in place.
 constexpr int NT2 = 512, NW2 = NT2 / 32;
 
@@ -480,10 +479,10 @@ __device__ __forceinline__ void half_store(float* out, const float (&acc)[4][4],
         make_float4(sign * acc[i][0], sign * acc[i][1], sign * acc[i][2], sign * acc[i][3]);
 }
 
-// warp: Cholesky of the 32 x 32 tile T in place (lower; zeros written above the diagonal) and its
-// inverse into Dt (lower, zeros above).  Row per lane; the scaled pivot column is published through
-// colbuf (two 32-float buffers, alternating) and read back as float4 broadcasts.
-__device__ void diag_factor(float* T, float* Dt, float* colbuf, int lane, bool& bad) {
+// warp: Cholesky of the 32 x 32 tile T in place (lower; zeros written above the diagonal); the reciprocal
+// diagonal 1 / L_cc goes to rdiag[c].  Row per lane; the scaled pivot column is published through colbuf
+// (two 32-float buffers, alternating) and read back as float4 broadcasts.
+__device__ void diag_potrf(float* T, float* rdiag, float* colbuf, int lane, bool& bad) {
   float a[TS];
 #pragma unroll
   for (int t = 0; t < TS; ++t) a[t] = T[lane * LDT + t];
@@ -496,7 +495,10 @@ __device__ void diag_factor(float* T, float* Dt, float* colbuf, int lane, bool& 
     }
     float inv = rsqrtf(d);
     inv = inv * fmaf(-0.5f * d * inv, inv, 1.5f);
-    if (lane == c) a[c] = d * inv;
+    if (lane == c) {
+      a[c] = d * inv;
+      rdiag[c] = inv;
+    }
     if (lane > c) a[c] *= inv;
     float* cb = colbuf + (c & 1) * TS;
     cb[lane] = a[c];
@@ -516,7 +518,11 @@ __device__ void diag_factor(float* T, float* Dt, float* colbuf, int lane, bool& 
 #pragma unroll
   for (int t = 0; t < TS; ++t) T[lane * LDT + t] = (t <= lane) ? a[t] : 0.f;
   __syncwarp();
-  // D = L^-1: lane r solves row r of I L^-T = column r of L^-1 (four independent FMA chains)
+}
+
+// warp: Dt = L^-1 of the factored 32 x 32 tile T (lower, zeros above): lane r solves row r of I L^-T =
+// column r of L^-1 (four independent FMA chains)
+__device__ void diag_inverse(const float* T, float* Dt, int lane) {
   float x[TS];
   const float rd = __frcp_rn(T[lane * LDT + lane]);
 #pragma unroll
@@ -531,11 +537,39 @@ __device__ void diag_factor(float* T, float* Dt, float* colbuf, int lane, bool& 
   __syncwarp();
 }
 
+// thread: row A (32 floats, in place) <- A L^-T for the factored lower tile L (forward substitution along the
+// row: x_c = (a_c - sum_{t<c} x_t L_ct) / L_cc; L rows are warp-wide broadcasts, four FMA chains per entry)
+__device__ __forceinline__ void row_trsm(float* A, const float* L, const float* rdiag) {
+  float x[TS];
+#pragma unroll
+  for (int q = 0; q < TS / 4; ++q) {
+    const float4 v = *reinterpret_cast<const float4*>(A + 4 * q);
+    x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+  }
+#pragma unroll
+  for (int c = 0; c < TS; ++c) {
+    float y[4] = {x[c], 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; 4 * q < c; ++q) {
+      const float4 l = *reinterpret_cast<const float4*>(L + c * LDT + 4 * q);
+      const float lv[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (4 * q + u < c) y[u] = fmaf(-x[4 * q + u], lv[u], y[u]);
+    }
+    x[c] = ((y[0] + y[1]) + (y[2] + y[3])) * rdiag[c];
+  }
+#pragma unroll
+  for (int q = 0; q < TS / 4; ++q)
+    *reinterpret_cast<float4*>(A + 4 * q) = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+}
+
 __global__ void __launch_bounds__(NT2, 1) k_cholinv2(int k, const float* __restrict__ G, float* __restrict__ Lout,
                                                      float* __restrict__ Linv, int32_t* status) {
   extern __shared__ __align__(16) float sm[];
   __shared__ float red[NW2];
   __shared__ __align__(16) float colbuf[2 * TS];
+  __shared__ float rdiag[TS];
   __shared__ int s_bad;
   __shared__ float s_shift;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -628,16 +662,15 @@ __global__ void __launch_bounds__(NT2, 1) k_cholinv2(int k, const float* __restr
     for (int p = 0; p < nt; ++p) {
       CHOL_CLK(2 + 3 * p);
       if (warp == 0) {
-        diag_factor(T(p, p), D(p), colbuf, lane, bad);
+        diag_potrf(T(p, p), rdiag, colbuf, lane, bad);
         if (bad && lane == 0) s_bad = 1;
       }
       __syncthreads();
       CHOL_CLK(3 + 3 * p);
       const int m = nt - 1 - p;
-      for (int u = warp; u < 2 * m; u += NW2) {   // L_ip = A_ip D_p^T
-        const int i = p + 1 + (u >> 1);
-        half_abt(T(i, p), T(i, p), D(p), lane, (u & 1) * 16, 0);
-      }
+      // L_ip = A_ip L_pp^-T by forward substitution, one panel row per thread (no diagonal inverse on the
+      // panel chain: the eight D_i the triangular inverse needs are formed in parallel after the loop)
+      if (t < m * TS) row_trsm(T(p + 1 + (t >> 5), p) + (t & 31) * LDT, T(p, p), rdiag);
       __syncthreads();
       CHOL_CLK(4 + 3 * p);
       const int nu = m * (m + 1);                  // half tiles of the trailing lower tiles
@@ -659,6 +692,9 @@ __global__ void __launch_bounds__(NT2, 1) k_cholinv2(int k, const float* __restr
 
   if (Lb) store_lower(Lb, tiles, k, nt, warp, lane);
   if (!Ib) return;
+  // ---- D_i = L_ii^-1, one warp per diagonal tile
+  for (int i = warp; i < nt; i += NW2) diag_inverse(T(i, i), D(i), lane);
+  __syncthreads();
   // ---- triangular inverse in place: X_ii = D_i; columns j = nt-2 .. 0
   for (int task = t; task < nt * TS * 8; task += NT2) {
     const int i = task >> 8, r = (task >> 3) & 31, c4 = task & 7;
