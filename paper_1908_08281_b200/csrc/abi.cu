@@ -622,15 +622,20 @@ hg_status run_rsvd(const float* X, int nb, int blk0, int b, int k, int q, uint64
     g.D = Uk; g.d_trans = true; g.ldd = k; g.sd = (int64_t)k * k;
     HG_TRY(gemm(g, s, simt, "U~ = L^-T W_f"));
   }
-  // V_w = B^T U~ -> P[2];  U_w = S U~ -> P[3]  (step 6)
-  for (int w = 0; w < 2; ++w) {
-    GemmDesc g;
-    g.M = b; g.N = k; g.K = k; g.batch = nb;
-    g.A = (w == 0) ? Bt : cur; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
-    g.B = Uk; g.b_mn = false; g.ldb = k; g.sb = (int64_t)k * k;
-    g.D = P[2 + w]; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
-    HG_TRY(gemm(g, s, simt, w == 0 ? "V = B^T U~" : "U = S U~"));
-    if (R.tw) tw.exp[2 + w] = kNoTwin;
+  // V_w = B^T U~ -> P[2];  U_w = S U~ -> P[3]  (step 6): independent products, the second on the part's
+  // side stream
+  {
+    cudaStream_t side = side_fork(s);
+    for (int w = 0; w < 2; ++w) {
+      GemmDesc g;
+      g.M = b; g.N = k; g.K = k; g.batch = nb;
+      g.A = (w == 0) ? Bt : cur; g.a_mn = true; g.lda = b; g.sa = (int64_t)k * b;
+      g.B = Uk; g.b_mn = false; g.ldb = k; g.sb = (int64_t)k * k;
+      g.D = P[2 + w]; g.d_trans = true; g.ldd = b; g.sd = (int64_t)k * b;
+      HG_TRY(gemm(g, w == 0 ? s : side, simt, w == 0 ? "V = B^T U~" : "U = S U~"));
+      if (R.tw) tw.exp[2 + w] = kNoTwin;
+    }
+    side_join(s, side);
   }
   {
     ProfScope ps(ST_FINALIZE, s);
