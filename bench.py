@@ -416,6 +416,55 @@ def run_ours(args):
     stages = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                   "share": v[0] / args.steps / prof_ms_per_step} for k, v in prof.items()}
 
+    # (the end-to-end timing comes BEFORE the TF32 peak measurement below: its 4 s sustained GEMM loop drives the
+    #  GPU into its power cap, and a host-entry timing taken right after it read 0.3-0.6 ms high)
+    # end to end through the host entry point (pinned buffers, copies inside the timed region).
+    # Sharded (N > 1): per rank, the pinned H2D of H, w and its Y rows into the device buffers, its
+    # block range (hg_solve_blocks), the all-gather of F and sigma, and the D2H of the full F and
+    # sigma on rank 0 (the user's result), all inside the timed region.
+    rp = torch.from_numpy(h.row_ptr).pin_memory()
+    ci = torch.from_numpy(h.col_idx).pin_memory()
+    wh = torch.from_numpy(h.w).pin_memory()
+    Yh = torch.from_numpy(h.Y).pin_memory()
+    Fh = torch.empty((c.N, c.T), dtype=torch.float32).pin_memory()
+    sh = torch.empty((c.nb, c.k), dtype=torch.float32).pin_memory()
+    yr0, yr1 = sb0 * c.b, (sb0 + scnt) * c.b
+
+    def e2e_step():
+        if not shard:
+            hg.solve_host(rp, ci, wh, Yh, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, F=Fh, sigma=sh, ws=ws,
+                          stream=stream)
+            return
+        H.row_ptr.copy_(rp, non_blocking=True)
+        H.col_idx.copy_(ci, non_blocking=True)
+        w.copy_(wh, non_blocking=True)
+        Y[yr0:yr1].copy_(Yh[yr0:yr1], non_blocking=True)
+        step()
+        if rank == 0:
+            Fh.copy_(F_all, non_blocking=True)
+            sh.copy_(sigma, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+
+    for _ in range(max(3, min(args.warmup, 5))):   # pinned buffers first-touched, graph uploaded, copy engines warm
+        e2e_step()
+    barrier()
+    n_e2e = max(5, min(args.steps, 20))
+    t0 = time.perf_counter()
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ee0.record(stream)
+    for _ in range(n_e2e):
+        e2e_step()
+    ee1.record(stream)
+    torch.cuda.synchronize(dev)
+    wall_e2e = (time.perf_counter() - t0) / n_e2e
+    e2e_ms = max_over_ranks(max(ee0.elapsed_time(ee1) / n_e2e, wall_e2e * 1e3), dev)
+    if shard:
+        h2d = (c.N + 1) * 8 + h.nnz * 4 + h.E * 4 + (yr1 - yr0) * c.T * 4
+        d2h = (c.N * c.T * 4 + c.nb * c.k * 4) if rank == 0 else 0
+    else:
+        h2d = (c.N + 1) * 8 + h.nnz * 4 + h.E * 4 + c.N * c.T * 4
+        d2h = c.N * c.T * 4 + c.nb * c.k * 4
+
     peaks, peak_src = load_peaks()
     # TF32 peak: measured here (cuBLAS tf32 8192^3, burst and sustained); the
     # bf16-derived figure (MEASURED_PEAKS bf16 x nominal 1.1/2.25) only with --no-tf32-peak
@@ -525,53 +574,6 @@ def run_ours(args):
     gemm_useful_tflops = None
     if "gemm_power" in prof:
         gemm_useful_tflops = (2 * q + 2) * 2.0 * b * b * k * nb / (prof["gemm_power"][0] / args.steps / 1e3) / 1e12
-
-    # end to end through the host entry point (pinned buffers, copies inside the timed region).
-    # Sharded (N > 1): per rank, the pinned H2D of H, w and its Y rows into the device buffers, its
-    # block range (hg_solve_blocks), the all-gather of F and sigma, and the D2H of the full F and
-    # sigma on rank 0 (the user's result), all inside the timed region.
-    rp = torch.from_numpy(h.row_ptr).pin_memory()
-    ci = torch.from_numpy(h.col_idx).pin_memory()
-    wh = torch.from_numpy(h.w).pin_memory()
-    Yh = torch.from_numpy(h.Y).pin_memory()
-    Fh = torch.empty((c.N, c.T), dtype=torch.float32).pin_memory()
-    sh = torch.empty((c.nb, c.k), dtype=torch.float32).pin_memory()
-    yr0, yr1 = sb0 * c.b, (sb0 + scnt) * c.b
-
-    def e2e_step():
-        if not shard:
-            hg.solve_host(rp, ci, wh, Yh, mu=c.mu, b=c.b, k=c.k, q=c.q, seed=seed, F=Fh, sigma=sh, ws=ws,
-                          stream=stream)
-            return
-        H.row_ptr.copy_(rp, non_blocking=True)
-        H.col_idx.copy_(ci, non_blocking=True)
-        w.copy_(wh, non_blocking=True)
-        Y[yr0:yr1].copy_(Yh[yr0:yr1], non_blocking=True)
-        step()
-        if rank == 0:
-            Fh.copy_(F_all, non_blocking=True)
-            sh.copy_(sigma, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
-
-    for _ in range(max(1, min(args.warmup, 2))):
-        e2e_step()
-    barrier()
-    n_e2e = max(3, min(args.steps, 10))
-    t0 = time.perf_counter()
-    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ee0.record(stream)
-    for _ in range(n_e2e):
-        e2e_step()
-    ee1.record(stream)
-    torch.cuda.synchronize(dev)
-    wall_e2e = (time.perf_counter() - t0) / n_e2e
-    e2e_ms = max_over_ranks(max(ee0.elapsed_time(ee1) / n_e2e, wall_e2e * 1e3), dev)
-    if shard:
-        h2d = (c.N + 1) * 8 + h.nnz * 4 + h.E * 4 + (yr1 - yr0) * c.T * 4
-        d2h = (c.N * c.T * 4 + c.nb * c.k * 4) if rank == 0 else 0
-    else:
-        h2d = (c.N + 1) * 8 + h.nnz * 4 + h.E * 4 + c.N * c.T * 4
-        d2h = c.N * c.T * 4 + c.nb * c.k * 4
 
     # Every use of the FP64 oracle below is deferred into the cpu_baseline leg (cpu_baseline_leg, run
     # once after all GPU timing on rank 0): the CPU baseline timing itself and the parity / accuracy
