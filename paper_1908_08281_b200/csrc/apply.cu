@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   using C = ACfg<KP>;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full1[S1], conv1[S1], empty1[S1], tfull1[2], tempty1[2];
-  __shared__ __align__(8) uint64_t zs_bar, full2[S2], empty2[S2], tfull2[2], tempty2[2];
+  __shared__ __align__(8) uint64_t zs_bar, p1_bar, full2[S2], empty2[S2], tfull2[2], tempty2[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ float rs_sh[KP];
   __shared__ float red_sh[NEPI / 32];
@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(&tempty2[i], NEPI / 32);
     }
     mbar_init(&zs_bar, NEPI / 32);
+    mbar_init(&p1_bar, 1);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc<512>(&tmem_base_sh);
@@ -197,8 +198,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       __syncwarp();
     }
-    // the V ring reuses product-1 stage memory: wait for the last product-1 MMAs (last chunk committed)
-    mbar_wait(&tfull1[(nch1 - 1) & 1], ((nch1 - 1) >> 1) & 1);
+    // the V ring reuses product-1 stage memory: wait until every product-1 MMA has read its operands
+    // (a barrier of its own: a parity wait on tfull1 is only exact for a waiter that follows every phase)
+    mbar_wait(&p1_bar, 0);
     int idx = 0;
     for (int mt = 0; mt < nmt; ++mt)
       for (int kb2 = 0; kb2 < C::NKB2; ++kb2, ++idx) {
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         mma_commit(&empty1[s]);
         if (last_in_chunk) mma_commit(&tfull1[buf]);
+        if (kb == nkb1 - 1) mma_commit(&p1_bar);
       }
       __syncwarp();
     }
